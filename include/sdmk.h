@@ -1,0 +1,162 @@
+/*
+ * sdmk.h -- C-ABI of the B200-native DMK hot path (libsdmk_b200.so).
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ * Every entry point returns an sdmk_status (0 = success) and never throws;
+ * sdmk_last_error() describes the last failure on the calling thread.  The
+ * C++ drop-in header include/stokesdmk_b200/dmk.hpp maps these codes back to
+ * the reference's exception types.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to the reference's proj/core):
+ *
+ *   sdmk_select_parameters   stokesdmk::select_parameters     include/stokesdmk/dmk.hpp:50-51, src/params.cpp:60-115
+ *   sdmk_outgoing_channels   stokesdmk::outgoing_channels     dmk.hpp:59, params.cpp:117-125
+ *   sdmk_evaluate_with_plan  stokesdmk::evaluate_with_plan    dmk.hpp:151-155, dmk.cpp:1036-1117
+ *   sdmk_evaluate            stokesdmk::evaluate              dmk.hpp:159-161, dmk.cpp:1119-1124
+ *   sdmk_evaluate_device     (device-resident variant of evaluate_with_plan; inputs/outputs in HBM)
+ *   sdmk_setup               stokesdmk::build_tree + validate_system/wrap_into_box
+ *                            (tree.hpp:90-92, oracle.hpp:54-58): builds the tree of one problem
+ *                            in the context so the pass-level entry points can run on it
+ *   sdmk_tree_info/boxes/perm/dump   Tree fields + dump_tree (tree.hpp:52-81, 104)
+ *   sdmk_upward_pass         stokesdmk::upward_pass           dmk.hpp:84-85, dmk.cpp:555-655
+ *   sdmk_incoming            make_incoming + root_far_field (+ downward_pass)  dmk.hpp:88-112
+ *   sdmk_target_far_fields   stokesdmk::target_far_fields     dmk.hpp:116-117, dmk.cpp:861-915
+ *   sdmk_residual_pass       stokesdmk::residual_pass         dmk.hpp:128-131, dmk.cpp:919-1032
+ *   sdmk_load_tables / sdmk_save_tables   import/export_split_kernel (split.hpp:153-154, SDMKSPLT v1)
+ *
+ * Enumerations use the reference's enumerator order:
+ *   kernel: 0 stokeslet, 1 stresslet, 2 rotlet  (KernelType, split.hpp:28)
+ *   window: 0 prolate, 1 gaussian               (WindowKind, windows.hpp:19)
+ *   mode:   0 free_space, 1 periodic            (EwaldMode, oracle.hpp:82)
+ */
+#ifndef SDMK_H
+#define SDMK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum sdmk_status {
+  SDMK_OK = 0,
+  SDMK_EINVAL = 1,   /* std::invalid_argument in the reference */
+  SDMK_EDOMAIN = 2,  /* std::domain_error (coincident points) */
+  SDMK_ERUNTIME = 3, /* std::runtime_error (I/O, fit non-convergence) */
+  SDMK_ECUDA = 4,    /* CUDA runtime / launch failure */
+  SDMK_EOOM = 5      /* device allocation failed */
+} sdmk_status;
+
+/* Field order and meaning of stokesdmk::DmkPlan (dmk.hpp:27-40). */
+typedef struct sdmk_plan {
+  int32_t kernel;
+  int32_t dim;
+  int32_t window;
+  double tol;
+  double c;
+  double sigma;
+  int32_t p;
+  int32_t N1;
+  int32_t N_per;
+  int32_t n_s;
+  double table_tol;
+} sdmk_plan;
+
+/* stokesdmk::DmkReport (dmk.hpp:134-145) plus device-side detail.  The
+   t_* fields are seconds of the same passes as the reference report, taken
+   with CUDA events on the context stream. */
+typedef struct sdmk_report {
+  int32_t num_boxes;
+  int32_t max_level;
+  int32_t num_sources;
+  int32_t num_targets;
+  double t_tree;
+  double t_upward;
+  double t_root;
+  double t_downward;
+  double t_residual;
+  /* extras */
+  double t_h2d;          /* host->device copies (host-pointer entry points) */
+  double t_d2h;          /* device->host copy of u */
+  double t_total;        /* whole call, CUDA events */
+  int64_t p2p_candidates; /* source-target pairs tested in the residual kernel */
+  int64_t p2p_in_support; /* pairs evaluated (r < nu * support) */
+  int32_t kernel_launches;
+  double t_residual_kernel; /* residual kernel alone */
+  double t_planewave;       /* forward/accumulate/inverse kernels of the downward pass */
+} sdmk_report;
+
+typedef struct sdmk_context sdmk_context;
+
+int sdmk_create(int device, sdmk_context** out);
+int sdmk_destroy(sdmk_context* ctx);
+const char* sdmk_last_error(void);
+/* 1 when the library was built for and is running on an sm_100 device */
+int sdmk_device_ok(int device);
+
+int sdmk_select_parameters(int kernel, double eps, int window, int dim, sdmk_plan* out);
+int sdmk_outgoing_channels(int kernel, int dim);
+int sdmk_strength_components(int kernel, int dim);
+
+/* Split tables: built from the plan on first use and cached in the context
+   (keyed by kernel/dim/window/c|sigma/table_tol).  load/save use the
+   reference's SDMKSPLT v1 format, so a table cache written by either library
+   can be read by the other. */
+int sdmk_load_tables(sdmk_context* ctx, const char* path);
+int sdmk_save_tables(sdmk_context* ctx, const sdmk_plan* plan, const char* path);
+
+/* Full evaluation from HOST buffers (caller point order, point-major AoS as in
+   ParticleSystem, oracle.hpp:29-46).  n_tgt == 0 (tgt may be NULL) means the
+   targets alias the sources.  u receives dim * max(n_tgt, n_src-if-alias)
+   doubles.  report may be NULL. */
+int sdmk_evaluate_with_plan(sdmk_context* ctx, const sdmk_plan* plan, int dim, int64_t n_src,
+                            const double* src, int64_t n_tgt, const double* tgt, const double* str,
+                            int mode, double* u, sdmk_report* report);
+
+int sdmk_evaluate(sdmk_context* ctx, int kernel, int dim, int64_t n_src, const double* src,
+                  int64_t n_tgt, const double* tgt, const double* str, double eps, int window,
+                  int mode, double* u, sdmk_report* report);
+
+/* Same as sdmk_evaluate_with_plan with every array already in device memory
+   (the device-resident "value" path of the benchmark). */
+int sdmk_evaluate_device(sdmk_context* ctx, const sdmk_plan* plan, int dim, int64_t n_src,
+                         const double* d_src, int64_t n_tgt, const double* d_tgt,
+                         const double* d_str, int mode, double* d_u, sdmk_report* report);
+
+/* ---- pass-level API on one problem held by the context ---- */
+int sdmk_setup(sdmk_context* ctx, const sdmk_plan* plan, int dim, int64_t n_src, const double* src,
+               int64_t n_tgt, const double* tgt, const double* str, int mode);
+/* info[7]: num_boxes, max_level, n_src, n_tgt, alias, depth_capped, channels */
+int sdmk_tree_info(sdmk_context* ctx, int32_t* info);
+/* 11 int32 per box: level parent first_child leaf a0 a1 a2 src_begin src_end tgt_begin tgt_end */
+int sdmk_tree_boxes(sdmk_context* ctx, int32_t* out);
+int sdmk_tree_perm(sdmk_context* ctx, int32_t* src_perm, int32_t* tgt_perm);
+/* returns the dump length; copies at most cap bytes into buf (may be NULL) */
+int64_t sdmk_tree_dump(sdmk_context* ctx, char* buf, int64_t cap);
+/* outgoing proxies: num_boxes * channels * p^dim doubles (ProxyData layout) */
+int sdmk_upward_pass(sdmk_context* ctx, double* outgoing);
+/* incoming proxies: num_boxes * dim * p^dim doubles; stage 0 = root far field
+   only, 1 = after the downward pass */
+int sdmk_incoming(sdmk_context* ctx, int stage, double* incoming);
+int sdmk_target_far_fields(sdmk_context* ctx, double* u);
+int sdmk_residual_pass(sdmk_context* ctx, double* u);
+
+/* ---- host-only helpers (no GPU needed; used by the CPU test suite) ----
+   Plan-level setup exactly as the GPU path uses it. */
+int sdmk_host_save_tables(const sdmk_plan* plan, const char* path);
+/* symbol table of one grid (dmk.cpp:259-318); kind 0 level_diff, 1 root_free,
+   2 root_periodic; out receives s2max + 1 doubles */
+int sdmk_host_symbol_table(const sdmk_plan* plan, double h, int s2max, int kind, double r_coarse,
+                           double r_fine, double* out);
+/* box topology from SORTED quantized coordinates (SoA int32, q[axis*n+i]);
+   n_tgt == 0 aliases; returns the dump_tree text length, copies <= cap bytes */
+int64_t sdmk_host_topology_dump(int dim, int periodic, int n_s, int p, int64_t n_src,
+                                const int32_t* q_src, int64_t n_tgt, const int32_t* q_tgt, char* buf,
+                                int64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SDMK_H */

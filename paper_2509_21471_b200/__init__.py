@@ -1,0 +1,377 @@
+"""B200-native DMK hot path (stokesdmk drop-in), Python mirror.
+
+The product is ``libsdmk_b200.so`` (CUDA kernels for sm_100a + C++ host
+engine) behind the C-ABI in ``include/sdmk.h``.  This module binds that ABI
+with ctypes and mirrors the reference's public API names and argument meaning
+(``/root/reference/proj/core/include/stokesdmk/dmk.hpp``):
+
+    select_parameters(kernel, eps, window, dim)          dmk.hpp:50-51
+    evaluate_with_plan(plan, sys, mode, report=None)      dmk.hpp:151-155
+    evaluate(kernel, sys, eps, window, mode, report=None) dmk.hpp:159-161
+    outgoing_channels(kernel, dim)                        dmk.hpp:59
+
+Errors map back to the reference's exception types: ``ValueError`` for
+std::invalid_argument, ``ArithmeticError`` (DomainError) for
+std::domain_error, ``RuntimeError`` otherwise.  There is no CPU fallback: if
+the library or a B200 is missing, every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsdmk_b200.so")
+
+STOKESLET, STRESSLET, ROTLET = 0, 1, 2
+PROLATE, GAUSSIAN = 0, 1
+FREE_SPACE, PERIODIC = 0, 1
+
+KERNELS = {"stokeslet": STOKESLET, "stresslet": STRESSLET, "rotlet": ROTLET}
+WINDOWS = {"prolate": PROLATE, "gaussian": GAUSSIAN}
+MODES = {"free_space": FREE_SPACE, "free": FREE_SPACE, "periodic": PERIODIC}
+
+
+class DomainError(ArithmeticError):
+    """std::domain_error (coincident points)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class sdmk_plan(C.Structure):
+    _fields_ = [("kernel", C.c_int32), ("dim", C.c_int32), ("window", C.c_int32), ("tol", C.c_double),
+                ("c", C.c_double), ("sigma", C.c_double), ("p", C.c_int32), ("N1", C.c_int32),
+                ("N_per", C.c_int32), ("n_s", C.c_int32), ("table_tol", C.c_double)]
+
+
+class sdmk_report(C.Structure):
+    _fields_ = [("num_boxes", C.c_int32), ("max_level", C.c_int32), ("num_sources", C.c_int32),
+                ("num_targets", C.c_int32), ("t_tree", C.c_double), ("t_upward", C.c_double),
+                ("t_root", C.c_double), ("t_downward", C.c_double), ("t_residual", C.c_double),
+                ("t_h2d", C.c_double), ("t_d2h", C.c_double), ("t_total", C.c_double),
+                ("p2p_candidates", C.c_int64), ("p2p_in_support", C.c_int64), ("kernel_launches", C.c_int32),
+                ("t_residual_kernel", C.c_double), ("t_planewave", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libsdmk_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run `make -C paper_2509_21471_b200/csrc` "
+                               "(or __graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        P = C.POINTER
+        dp, ip = P(C.c_double), P(C.c_int32)
+        sig = {
+            "sdmk_last_error": ([], C.c_char_p),
+            "sdmk_device_ok": ([C.c_int], C.c_int),
+            "sdmk_create": ([C.c_int, P(C.c_void_p)], C.c_int),
+            "sdmk_destroy": ([C.c_void_p], C.c_int),
+            "sdmk_select_parameters": ([C.c_int, C.c_double, C.c_int, C.c_int, P(sdmk_plan)], C.c_int),
+            "sdmk_outgoing_channels": ([C.c_int, C.c_int], C.c_int),
+            "sdmk_strength_components": ([C.c_int, C.c_int], C.c_int),
+            "sdmk_load_tables": ([C.c_void_p, C.c_char_p], C.c_int),
+            "sdmk_save_tables": ([C.c_void_p, P(sdmk_plan), C.c_char_p], C.c_int),
+            "sdmk_evaluate_with_plan": ([C.c_void_p, P(sdmk_plan), C.c_int, C.c_int64, dp, C.c_int64, dp, dp,
+                                         C.c_int, dp, P(sdmk_report)], C.c_int),
+            "sdmk_evaluate": ([C.c_void_p, C.c_int, C.c_int, C.c_int64, dp, C.c_int64, dp, dp, C.c_double,
+                               C.c_int, C.c_int, dp, P(sdmk_report)], C.c_int),
+            "sdmk_evaluate_device": ([C.c_void_p, P(sdmk_plan), C.c_int, C.c_int64, C.c_void_p, C.c_int64,
+                                      C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, P(sdmk_report)], C.c_int),
+            "sdmk_setup": ([C.c_void_p, P(sdmk_plan), C.c_int, C.c_int64, dp, C.c_int64, dp, dp, C.c_int], C.c_int),
+            "sdmk_tree_info": ([C.c_void_p, ip], C.c_int),
+            "sdmk_tree_boxes": ([C.c_void_p, ip], C.c_int),
+            "sdmk_tree_perm": ([C.c_void_p, ip, ip], C.c_int),
+            "sdmk_tree_dump": ([C.c_void_p, C.c_char_p, C.c_int64], C.c_int64),
+            "sdmk_upward_pass": ([C.c_void_p, dp], C.c_int),
+            "sdmk_incoming": ([C.c_void_p, C.c_int, dp], C.c_int),
+            "sdmk_target_far_fields": ([C.c_void_p, dp], C.c_int),
+            "sdmk_residual_pass": ([C.c_void_p, dp], C.c_int),
+            "sdmk_host_save_tables": ([P(sdmk_plan), C.c_char_p], C.c_int),
+            "sdmk_host_symbol_table": ([P(sdmk_plan), C.c_double, C.c_int, C.c_int, C.c_double, C.c_double, dp],
+                                       C.c_int),
+            "sdmk_host_topology_dump": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, ip, C.c_int64, ip,
+                                         C.c_char_p, C.c_int64], C.c_int64),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def _raise(code: int):
+    if code == 0:
+        return
+    msg = lib().sdmk_last_error().decode()
+    if code == 1:
+        raise ValueError(msg)
+    if code == 2:
+        raise DomainError(msg)
+    if code == 4:
+        raise CudaError(msg)
+    if code == 5:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def _dptr(a: Optional[np.ndarray]):
+    if a is None:
+        return C.cast(None, C.POINTER(C.c_double))
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _iptr(a: Optional[np.ndarray]):
+    if a is None:
+        return C.cast(None, C.POINTER(C.c_int32))
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def _enum(v, table):
+    return table[v] if isinstance(v, str) else int(v)
+
+
+@dataclass
+class DmkPlan:
+    """stokesdmk::DmkPlan (dmk.hpp:27-40)."""
+    kernel: int = STOKESLET
+    dim: int = 3
+    window: int = PROLATE
+    tol: float = 1e-6
+    c: float = 0.0
+    sigma: float = 0.0
+    p: int = 0
+    N1: int = 0
+    N_per: int = 0
+    n_s: int = 0
+    table_tol: float = 0.0
+
+    def to_c(self) -> sdmk_plan:
+        return sdmk_plan(self.kernel, self.dim, self.window, self.tol, self.c, self.sigma, self.p, self.N1,
+                         self.N_per, self.n_s, self.table_tol)
+
+    @staticmethod
+    def from_c(p: sdmk_plan) -> "DmkPlan":
+        return DmkPlan(p.kernel, p.dim, p.window, p.tol, p.c, p.sigma, p.p, p.N1, p.N_per, p.n_s, p.table_tol)
+
+
+@dataclass
+class ParticleSystem:
+    """stokesdmk::ParticleSystem (oracle.hpp:29-46): point-major arrays."""
+    dim: int = 3
+    sources: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    targets: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    strengths: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+    def num_sources(self) -> int:
+        return int(np.asarray(self.sources).size // self.dim)
+
+    def num_targets(self) -> int:
+        t = np.asarray(self.targets)
+        return self.num_sources() if t.size == 0 else int(t.size // self.dim)
+
+
+def select_parameters(kernel, eps: float, window=PROLATE, dim: int = 3) -> DmkPlan:
+    out = sdmk_plan()
+    _raise(lib().sdmk_select_parameters(_enum(kernel, KERNELS), float(eps), _enum(window, WINDOWS), int(dim),
+                                        C.byref(out)))
+    return DmkPlan.from_c(out)
+
+
+def outgoing_channels(kernel, dim: int) -> int:
+    r = lib().sdmk_outgoing_channels(_enum(kernel, KERNELS), int(dim))
+    if r < 0:
+        _raise(1)
+    return r
+
+
+def strength_components(kernel, dim: int) -> int:
+    return lib().sdmk_strength_components(_enum(kernel, KERNELS), int(dim))
+
+
+def _arr(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64).ravel())
+
+
+class Context:
+    """One GPU context (device, stream, buffers, table cache)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _raise(lib().sdmk_create(int(device), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().sdmk_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- full evaluation -------------------------------------------------
+    def evaluate_with_plan(self, plan: DmkPlan, sys: ParticleSystem, mode=FREE_SPACE,
+                           report: Optional[dict] = None) -> np.ndarray:
+        src, tgt, stw = _arr(sys.sources), _arr(sys.targets), _arr(sys.strengths)
+        d = int(sys.dim)
+        ns = src.size // d if d else 0
+        nt = tgt.size // d if d else 0
+        u = np.empty((nt if nt else ns) * d)
+        rep = sdmk_report()
+        cp = plan.to_c()
+        _raise(lib().sdmk_evaluate_with_plan(self._h, C.byref(cp), d, ns, _dptr(src), nt,
+                                             _dptr(tgt if nt else None), _dptr(stw), _enum(mode, MODES),
+                                             _dptr(u), C.byref(rep)))
+        if report is not None:
+            report.update(rep.as_dict())
+        return u
+
+    def evaluate(self, kernel, sys: ParticleSystem, eps: float, window=PROLATE, mode=FREE_SPACE,
+                 report: Optional[dict] = None) -> np.ndarray:
+        plan = select_parameters(kernel, eps, window, sys.dim)
+        return self.evaluate_with_plan(plan, sys, mode, report)
+
+    def evaluate_device(self, plan: DmkPlan, dim: int, ns: int, d_src: int, nt: int, d_tgt: int, d_str: int,
+                        mode, d_u: int, report: Optional[dict] = None):
+        """Device-resident variant: integer device addresses (e.g. torch tensor.data_ptr())."""
+        rep = sdmk_report()
+        cp = plan.to_c()
+        _raise(lib().sdmk_evaluate_device(self._h, C.byref(cp), int(dim), int(ns), C.c_void_p(d_src), int(nt),
+                                          C.c_void_p(d_tgt if nt else None), C.c_void_p(d_str),
+                                          _enum(mode, MODES), C.c_void_p(d_u), C.byref(rep)))
+        if report is not None:
+            report.update(rep.as_dict())
+
+    # ---- pass-level API (dmk.hpp:84-131, tree.hpp:90-104) -----------------
+    def setup(self, plan: DmkPlan, sys: ParticleSystem, mode=FREE_SPACE):
+        src, tgt, stw = _arr(sys.sources), _arr(sys.targets), _arr(sys.strengths)
+        d = int(sys.dim)
+        cp = plan.to_c()
+        _raise(lib().sdmk_setup(self._h, C.byref(cp), d, src.size // d, _dptr(src), tgt.size // d,
+                                _dptr(tgt if tgt.size else None), _dptr(stw), _enum(mode, MODES)))
+        self._plan = plan
+        self._dim = d
+
+    def tree_info(self) -> dict:
+        info = np.zeros(7, np.int32)
+        _raise(lib().sdmk_tree_info(self._h, _iptr(info)))
+        keys = ["num_boxes", "max_level", "n_src", "n_tgt", "alias", "depth_capped", "channels"]
+        return dict(zip(keys, info.tolist()))
+
+    def tree_boxes(self) -> np.ndarray:
+        nb = self.tree_info()["num_boxes"]
+        out = np.zeros(nb * 11, np.int32)
+        _raise(lib().sdmk_tree_boxes(self._h, _iptr(out)))
+        return out.reshape(nb, 11)
+
+    def tree_perm(self):
+        info = self.tree_info()
+        sp = np.zeros(info["n_src"], np.int32)
+        tp = np.zeros(info["n_tgt"], np.int32) if not info["alias"] else None
+        _raise(lib().sdmk_tree_perm(self._h, _iptr(sp), _iptr(tp)))
+        return sp, tp
+
+    def tree_dump(self) -> str:
+        n = lib().sdmk_tree_dump(self._h, None, 0)
+        if n < 0:
+            _raise(1)
+        buf = C.create_string_buffer(int(n))
+        lib().sdmk_tree_dump(self._h, buf, n)
+        return buf.raw[:n].decode()
+
+    def _nodes(self):
+        p, d = self._plan.p, self._dim
+        return p ** d
+
+    def upward_pass(self) -> np.ndarray:
+        info = self.tree_info()
+        out = np.empty(info["num_boxes"] * info["channels"] * self._nodes())
+        _raise(lib().sdmk_upward_pass(self._h, _dptr(out)))
+        return out
+
+    def incoming(self, stage: int = 1) -> np.ndarray:
+        info = self.tree_info()
+        out = np.empty(info["num_boxes"] * self._dim * self._nodes())
+        _raise(lib().sdmk_incoming(self._h, int(stage), _dptr(out)))
+        return out
+
+    def target_far_fields(self) -> np.ndarray:
+        out = np.empty(self.tree_info()["n_tgt"] * self._dim)
+        _raise(lib().sdmk_target_far_fields(self._h, _dptr(out)))
+        return out
+
+    def residual_pass(self) -> np.ndarray:
+        out = np.empty(self.tree_info()["n_tgt"] * self._dim)
+        _raise(lib().sdmk_residual_pass(self._h, _dptr(out)))
+        return out
+
+    def save_tables(self, plan: DmkPlan, path: str):
+        cp = plan.to_c()
+        _raise(lib().sdmk_save_tables(self._h, C.byref(cp), path.encode()))
+
+    def load_tables(self, path: str):
+        _raise(lib().sdmk_load_tables(self._h, path.encode()))
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def evaluate_with_plan(plan: DmkPlan, sys: ParticleSystem, mode=FREE_SPACE, report=None) -> np.ndarray:
+    return default_context().evaluate_with_plan(plan, sys, mode, report)
+
+
+def evaluate(kernel, sys: ParticleSystem, eps: float, window=PROLATE, mode=FREE_SPACE, report=None) -> np.ndarray:
+    return default_context().evaluate(kernel, sys, eps, window, mode, report)
+
+
+# ---- host-only helpers (CPU tests of the setup / topology code) ----------
+def host_save_tables(plan: DmkPlan, path: str):
+    cp = plan.to_c()
+    _raise(lib().sdmk_host_save_tables(C.byref(cp), path.encode()))
+
+
+def host_symbol_table(plan: DmkPlan, h: float, s2max: int, kind: int, r_coarse: float, r_fine: float):
+    out = np.empty(s2max + 1)
+    cp = plan.to_c()
+    _raise(lib().sdmk_host_symbol_table(C.byref(cp), h, s2max, kind, r_coarse, r_fine, _dptr(out)))
+    return out
+
+
+def host_topology_dump(dim, periodic, n_s, p, q_src_sorted, q_tgt_sorted=None) -> str:
+    qs = np.ascontiguousarray(np.asarray(q_src_sorted, np.int32).T.ravel())  # (n, d) -> SoA
+    ns = np.asarray(q_src_sorted).shape[0]
+    if q_tgt_sorted is not None and np.asarray(q_tgt_sorted).size:
+        qt = np.ascontiguousarray(np.asarray(q_tgt_sorted, np.int32).T.ravel())
+        nt = np.asarray(q_tgt_sorted).shape[0]
+    else:
+        qt, nt = None, 0
+    n = lib().sdmk_host_topology_dump(dim, int(periodic), n_s, p, ns, _iptr(qs), nt, _iptr(qt), None, 0)
+    if n < 0:
+        _raise(1)
+    buf = C.create_string_buffer(int(n))
+    lib().sdmk_host_topology_dump(dim, int(periodic), n_s, p, ns, _iptr(qs), nt, _iptr(qt), buf, n)
+    return buf.raw[:n].decode()

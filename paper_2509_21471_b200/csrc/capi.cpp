@@ -1,0 +1,278 @@
+// extern "C" boundary of libsdmk_b200.so (declared in include/sdmk.h).
+// Never throws: exceptions become sdmk_status codes plus sdmk_last_error().
+#include <cstring>
+#include <string>
+
+#include "../../include/sdmk.h"
+#include "engine.hpp"
+
+using namespace sdmkb;
+
+struct sdmk_context {
+  Context* ctx;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return SDMK_OK;
+  } catch (const InvalidArgument& e) {
+    g_err = e.what();
+    return SDMK_EINVAL;
+  } catch (const DomainError& e) {
+    g_err = e.what();
+    return SDMK_EDOMAIN;
+  } catch (const RuntimeError& e) {
+    g_err = e.what();
+    return SDMK_ERUNTIME;
+  } catch (const OomError& e) {
+    g_err = e.what();
+    return SDMK_EOOM;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return SDMK_ECUDA;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return SDMK_EOOM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SDMK_ERUNTIME;
+  }
+}
+
+Plan to_plan(const sdmk_plan* p) {
+  Plan P;
+  P.kernel = p->kernel;
+  P.dim = p->dim;
+  P.window = p->window;
+  P.tol = p->tol;
+  P.c = p->c;
+  P.sigma = p->sigma;
+  P.p = p->p;
+  P.N1 = p->N1;
+  P.N_per = p->N_per;
+  P.n_s = p->n_s;
+  P.table_tol = p->table_tol;
+  return P;
+}
+
+void from_plan(const Plan& P, sdmk_plan* p) {
+  p->kernel = P.kernel;
+  p->dim = P.dim;
+  p->window = P.window;
+  p->tol = P.tol;
+  p->c = P.c;
+  p->sigma = P.sigma;
+  p->p = P.p;
+  p->N1 = P.N1;
+  p->N_per = P.N_per;
+  p->n_s = P.n_s;
+  p->table_tol = P.table_tol;
+}
+
+Context* need_ctx(sdmk_context* c) {
+  if (!c || !c->ctx) throw InvalidArgument("null sdmk_context");
+  return c->ctx;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sdmk_last_error(void) { return g_err.c_str(); }
+
+int sdmk_device_ok(int device) {
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return prop.major == 10 && prop.minor == 0;
+}
+
+int sdmk_create(int device, sdmk_context** out) {
+  return guarded([&] {
+    if (!out) throw InvalidArgument("sdmk_create: null output pointer");
+    *out = nullptr;
+    int n = 0;
+    cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (device < 0 || device >= n) throw InvalidArgument("sdmk_create: no such CUDA device");
+    if (!sdmk_device_ok(device)) throw CudaError("sdmk_create: device is not an sm_100 (B200) GPU");
+    auto* c = new sdmk_context;
+    c->ctx = new Context(device);
+    *out = c;
+  });
+}
+
+int sdmk_destroy(sdmk_context* c) {
+  return guarded([&] {
+    if (!c) return;
+    delete c->ctx;
+    delete c;
+  });
+}
+
+int sdmk_select_parameters(int kernel, double eps, int window, int dim, sdmk_plan* out) {
+  return guarded([&] {
+    if (!out) throw InvalidArgument("sdmk_select_parameters: null output");
+    from_plan(select_plan(kernel, eps, window, dim), out);
+  });
+}
+
+int sdmk_outgoing_channels(int kernel, int dim) {
+  int r = -1;
+  if (guarded([&] { r = channels_out(kernel, dim); }) != SDMK_OK) return -1;
+  return r;
+}
+
+int sdmk_strength_components(int kernel, int dim) { return strength_width(kernel, dim); }
+
+int sdmk_load_tables(sdmk_context* c, const char* path) {
+  return guarded([&] { need_ctx(c)->load_tables(path ? path : ""); });
+}
+
+int sdmk_save_tables(sdmk_context* c, const sdmk_plan* plan, const char* path) {
+  return guarded([&] { save_tables(need_ctx(c)->tables_for(to_plan(plan)), path ? path : ""); });
+}
+
+int sdmk_evaluate_with_plan(sdmk_context* c, const sdmk_plan* plan, int dim, int64_t n_src, const double* src,
+                            int64_t n_tgt, const double* tgt, const double* str, int mode, double* u,
+                            sdmk_report* report) {
+  return guarded([&] {
+    if (!plan || !src || !str || !u || (n_tgt > 0 && !tgt)) throw InvalidArgument("evaluate: null array");
+    need_ctx(c)->evaluate(to_plan(plan), dim, n_src, src, n_tgt, tgt, str, mode, u, report, false);
+  });
+}
+
+int sdmk_evaluate(sdmk_context* c, int kernel, int dim, int64_t n_src, const double* src, int64_t n_tgt,
+                  const double* tgt, const double* str, double eps, int window, int mode, double* u,
+                  sdmk_report* report) {
+  return guarded([&] {
+    if (!src || !str || !u || (n_tgt > 0 && !tgt)) throw InvalidArgument("evaluate: null array");
+    Plan P = select_plan(kernel, eps, window, dim);
+    need_ctx(c)->evaluate(P, dim, n_src, src, n_tgt, tgt, str, mode, u, report, false);
+  });
+}
+
+int sdmk_evaluate_device(sdmk_context* c, const sdmk_plan* plan, int dim, int64_t n_src, const double* d_src,
+                         int64_t n_tgt, const double* d_tgt, const double* d_str, int mode, double* d_u,
+                         sdmk_report* report) {
+  return guarded([&] {
+    if (!plan || !d_src || !d_str || !d_u || (n_tgt > 0 && !d_tgt)) throw InvalidArgument("evaluate: null array");
+    need_ctx(c)->evaluate(to_plan(plan), dim, n_src, d_src, n_tgt, d_tgt, d_str, mode, d_u, report, true);
+  });
+}
+
+int sdmk_setup(sdmk_context* c, const sdmk_plan* plan, int dim, int64_t n_src, const double* src, int64_t n_tgt,
+               const double* tgt, const double* str, int mode) {
+  return guarded([&] {
+    if (!plan || !src || !str || (n_tgt > 0 && !tgt)) throw InvalidArgument("setup: null array");
+    need_ctx(c)->setup(to_plan(plan), dim, n_src, src, n_tgt, tgt, str, mode);
+  });
+}
+
+int sdmk_tree_info(sdmk_context* c, int32_t* info) {
+  return guarded([&] {
+    const Problem& p = need_ctx(c)->problem();
+    if (!p.ready) throw InvalidArgument("no problem set up");
+    info[0] = p.tree.num_boxes();
+    info[1] = p.tree.max_level;
+    info[2] = p.ns;
+    info[3] = p.nt;
+    info[4] = p.alias;
+    info[5] = p.tree.depth_capped;
+    info[6] = p.nch;
+  });
+}
+
+int sdmk_tree_boxes(sdmk_context* c, int32_t* out) {
+  return guarded([&] {
+    const Problem& p = need_ctx(c)->problem();
+    if (!p.ready) throw InvalidArgument("no problem set up");
+    for (int b = 0; b < p.tree.num_boxes(); ++b) {
+      const Box& x = p.tree.boxes[b];
+      int32_t* o = out + 11 * (size_t)b;
+      o[0] = x.level;
+      o[1] = x.parent;
+      o[2] = x.first_child;
+      o[3] = x.leaf;
+      o[4] = x.anchor[0];
+      o[5] = x.anchor[1];
+      o[6] = x.anchor[2];
+      o[7] = x.sb;
+      o[8] = x.se;
+      o[9] = x.tb;
+      o[10] = x.te;
+    }
+  });
+}
+
+int sdmk_tree_perm(sdmk_context* c, int32_t* src_perm, int32_t* tgt_perm) {
+  return guarded([&] {
+    const Problem& p = need_ctx(c)->problem();
+    if (!p.ready) throw InvalidArgument("no problem set up");
+    cuda_check(cudaMemcpy(src_perm, p.sperm, sizeof(int) * p.ns, cudaMemcpyDeviceToHost), "D2H perm");
+    if (tgt_perm && !p.alias)
+      cuda_check(cudaMemcpy(tgt_perm, p.tperm, sizeof(int) * p.nt, cudaMemcpyDeviceToHost), "D2H perm");
+  });
+}
+
+int64_t sdmk_tree_dump(sdmk_context* c, char* buf, int64_t cap) {
+  int64_t len = -1;
+  guarded([&] {
+    const Problem& p = need_ctx(c)->problem();
+    if (!p.ready) throw InvalidArgument("no problem set up");
+    std::string s = dump_topology(p.tree);
+    len = (int64_t)s.size();
+    if (buf && cap > 0) std::memcpy(buf, s.data(), (size_t)std::min<int64_t>(cap, len));
+  });
+  return len;
+}
+
+int sdmk_upward_pass(sdmk_context* c, double* out) {
+  return guarded([&] { need_ctx(c)->upward(out); });
+}
+
+int sdmk_incoming(sdmk_context* c, int stage, double* out) {
+  return guarded([&] { need_ctx(c)->incoming(stage, out); });
+}
+
+int sdmk_target_far_fields(sdmk_context* c, double* out) {
+  return guarded([&] { need_ctx(c)->target_far(out); });
+}
+
+int sdmk_residual_pass(sdmk_context* c, double* out) {
+  return guarded([&] { need_ctx(c)->residual(out); });
+}
+
+int sdmk_host_save_tables(const sdmk_plan* plan, const char* path) {
+  return guarded([&] { save_tables(tables_for_plan(to_plan(plan)), path ? path : ""); });
+}
+
+int sdmk_host_symbol_table(const sdmk_plan* plan, double h, int s2max, int kind, double rc, double rf, double* out) {
+  return guarded([&] {
+    Tables t = tables_for_plan(to_plan(plan));
+    std::vector<double> A = symbol_table(t, h, s2max, kind, rc, rf);
+    std::memcpy(out, A.data(), A.size() * sizeof(double));
+  });
+}
+
+int64_t sdmk_host_topology_dump(int dim, int periodic, int n_s, int p, int64_t ns, const int32_t* qs, int64_t nt,
+                                const int32_t* qt, char* buf, int64_t cap) {
+  int64_t len = -1;
+  guarded([&] {
+    HostTree t = build_topology(dim, periodic != 0, n_s, p, (int)ns, qs, (int)nt, qt);
+    std::string s = dump_topology(t);
+    len = (int64_t)s.size();
+    if (buf && cap > 0) std::memcpy(buf, s.data(), (size_t)std::min<int64_t>(cap, len));
+  });
+  return len;
+}
+
+}  // extern "C"

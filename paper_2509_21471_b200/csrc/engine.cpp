@@ -1,0 +1,883 @@
+// B200 DMK engine: host orchestration of the sm_100a passes.
+// Citations are to the reference passes each stage reproduces.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+
+namespace sdmkb {
+
+namespace {
+
+constexpr double PI = 3.14159265358979323846;
+
+// Chebyshev proxy machinery on the host (dmk.cpp:25-66): nodes, barycentric
+// weights, Lagrange basis with the exact-hit rule, child matrices.
+struct Cheb1 {
+  int p;
+  std::vector<double> x, w;
+  explicit Cheb1(int p_) : p(p_), x(p_), w(p_) {
+    for (int i = 0; i < p; ++i) {
+      double a = (2.0 * i + 1.0) * PI / (2.0 * p);
+      x[i] = std::cos(a);
+      w[i] = (i % 2 ? -1.0 : 1.0) * std::sin(a);
+    }
+  }
+  void basis(double t, double* out) const {
+    for (int i = 0; i < p; ++i)
+      if (t == x[i]) {
+        for (int j = 0; j < p; ++j) out[j] = j == i ? 1.0 : 0.0;
+        return;
+      }
+    double s = 0.0;
+    for (int i = 0; i < p; ++i) {
+      out[i] = w[i] / (t - x[i]);
+      s += out[i];
+    }
+    double inv = 1.0 / s;
+    for (int i = 0; i < p; ++i) out[i] *= inv;
+  }
+  // row i: parent basis at child node i of the lower (bit 0) / upper half
+  std::vector<double> child(int bit) const {
+    std::vector<double> M((size_t)p * p);
+    double off = bit ? 1.0 : -1.0;
+    for (int i = 0; i < p; ++i) basis((x[i] + off) * 0.5, M.data() + (size_t)i * p);
+    return M;
+  }
+};
+
+std::vector<double> transpose(const std::vector<double>& M, int p) {
+  std::vector<double> T((size_t)p * p);
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j) T[(size_t)j * p + i] = M[(size_t)i * p + j];
+  return T;
+}
+
+// band limit in mode-index units, squared (dmk.cpp:472-477)
+double band_r2(const Plan& P, int M, double spacing) {
+  if (P.window != kProlate) return 3.0 * double(M) * M + 1.0;
+  double b = P.c / spacing;
+  return b * b * (1.0 + 1e-12);
+}
+
+// Packs host vectors into one pinned blob for a single H2D copy.
+struct Packer {
+  struct Item {
+    size_t off, bytes;
+    const void* src;
+  };
+  std::vector<Item> items;
+  size_t total = 0;
+  template <class T>
+  size_t add(const std::vector<T>& v) {
+    total = (total + 127) & ~size_t(127);
+    size_t off = total;
+    items.push_back({off, v.size() * sizeof(T), v.data()});
+    total += v.size() * sizeof(T);
+    return off;
+  }
+};
+
+}  // namespace
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    throw OomError(std::string(what) + ": out of device memory");
+  }
+  throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+Arena::~Arena() {
+  for (auto& kv : bufs_) cudaFree(kv.second.first);
+}
+
+void* Arena::get(const std::string& name, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  auto it = bufs_.find(name);
+  if (it != bufs_.end() && it->second.second >= bytes) return it->second.first;
+  if (it != bufs_.end()) {
+    cudaFree(it->second.first);
+    bufs_.erase(it);
+  }
+  size_t alloc = bytes + bytes / 16 + 256;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, alloc);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw OomError("device allocation of " + std::to_string(alloc) + " bytes for '" + name + "' failed");
+  }
+  bufs_[name] = {p, alloc};
+  return p;
+}
+
+size_t Arena::bytes() const {
+  size_t s = 0;
+  for (auto& kv : bufs_) s += kv.second.second;
+  return s;
+}
+
+Pinned::~Pinned() {
+  for (auto& kv : bufs_) cudaFreeHost(kv.second.first);
+}
+
+void* Pinned::get(const std::string& name, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  auto it = bufs_.find(name);
+  if (it != bufs_.end() && it->second.second >= bytes) return it->second.first;
+  if (it != bufs_.end()) {
+    cudaFreeHost(it->second.first);
+    bufs_.erase(it);
+  }
+  size_t alloc = bytes + bytes / 8 + 256;
+  void* p = nullptr;
+  cuda_check(cudaMallocHost(&p, alloc), "cudaMallocHost");
+  bufs_[name] = {p, alloc};
+  return p;
+}
+
+Context::Context(int device) : device_(device) {
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "cudaStreamCreate");
+  for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+}
+
+Context::~Context() {
+  cudaSetDevice(device_);
+  if (st_) cudaStreamSynchronize(st_);
+  for (auto& e : ev_) cudaEventDestroy(e);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+void Context::sync() { cuda_check(cudaStreamSynchronize(st_), "stream synchronize"); }
+
+double Context::ev_ms(int a, int b) {
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, ev_[a], ev_[b]);
+  return ms;
+}
+
+void Context::load_tables(const std::string& path) {
+  Tables t = sdmkb::load_tables(path);
+  char key[256];
+  double wpar = t.win.kind == kProlate ? t.win.c : t.win.sigma;
+  std::snprintf(key, sizeof key, "%d/%d/%d/%.17g/%.17g", t.kernel, t.dim, t.win.kind, wpar, t.table_tol);
+  tables_[key] = t;
+}
+
+const Tables& Context::tables_for(const Plan& P) {
+  double tt = P.table_tol > 0.0 ? P.table_tol : std::max(0.03 * P.tol, P.dim == 2 ? 1e-12 : 1e-14);
+  double wpar = P.window == kProlate ? P.c : P.sigma;
+  char key[256];
+  std::snprintf(key, sizeof key, "%d/%d/%d/%.17g/%.17g", P.kernel, P.dim, P.window, wpar, tt);
+  auto it = tables_.find(key);
+  if (it == tables_.end()) it = tables_.emplace(key, tables_for_plan(P)).first;
+  return it->second;
+}
+
+void Context::check_inputs(const Plan& P, int dim, int64_t ns, int64_t nt, int mode) {
+  if (P.dim != dim) throw InvalidArgument("evaluate: plan and system dimensions differ");
+  if (P.kernel != kStokeslet && P.kernel != kStresslet && P.kernel != kRotlet)
+    throw InvalidArgument("particle sums support the Stokeslet, stresslet, and rotlet kernels");
+  if (dim != 2 && dim != 3) throw InvalidArgument("ParticleSystem: dim must be 2 or 3");
+  if (ns < 1) throw InvalidArgument("ParticleSystem: bad source array length");
+  if (nt < 0) throw InvalidArgument("ParticleSystem: bad target array length");
+  if (ns > (int64_t(1) << 31) - 1 || nt > (int64_t(1) << 31) - 1)
+    throw InvalidArgument("evaluate: more than 2^31-1 points");
+  if (mode != 0 && mode != 1) throw InvalidArgument("evaluate: bad EwaldMode");
+  if (mode == 1 && P.kernel == kStresslet && dim == 2)
+    throw InvalidArgument("evaluate: the periodic 2D stresslet sum is not absolutely convergent");
+  if (P.n_s < 1) throw InvalidArgument("build_tree: n_s must be >= 1");
+  if (P.p < 1) throw InvalidArgument("build_tree: proxy order must be >= 1");
+  if (P.p > (dim == 3 ? 48 : 64)) throw InvalidArgument("evaluate: proxy order above the GPU path limit (48 in 3D, 64 in 2D)");
+  if (P.N1 < 1 || P.N1 > 127 || P.N_per < 1 || P.N_per > 127)
+    throw InvalidArgument("evaluate: Fourier grid size outside [1, 127]");
+  if (P.window == kProlate && !(P.c > 0.0)) throw InvalidArgument("build_prolate: c must be positive");
+  if (P.window == kGaussian && !(P.sigma > 0.0)) throw InvalidArgument("build_gaussian: sigma must be positive");
+}
+
+GridDev& Context::grid(GridDev& gd, const std::string& name, int dim, int p, int N, double theta, double br2) {
+  if (gd.key_N == N && gd.key_p == p && gd.key_dim == dim && gd.key_theta == theta && gd.key_band == br2) return gd;
+  const int M = (N - 1) / 2, Nz = dim == 3 ? N : 1, Mz = dim == 3 ? M : 0, pz = dim == 3 ? p : 1;
+  Cheb1 cb(p);
+  // E[m+M][i] = exp(-i theta m s_i)  (dmk.cpp:137-147)
+  std::vector<double2> E((size_t)N * p), Ez((size_t)Nz * pz);
+  for (int m = -M; m <= M; ++m)
+    for (int i = 0; i < p; ++i) {
+      double a = -theta * m * cb.x[i];
+      E[(size_t)(m + M) * p + i] = make_double2(std::cos(a), std::sin(a));
+    }
+  if (dim == 3) Ez = E;
+  else Ez[0] = make_double2(1.0, 0.0);
+  // row limits (dmk.cpp:323-333)
+  auto lim = [&](int mz, int my) {
+    double rem = br2 - double(mz) * mz - double(my) * my;
+    return rem >= 0.0 ? std::min(M, (int)std::floor(std::sqrt(rem))) : -1;
+  };
+  struct Col {
+    int my, m0, lz;
+  };
+  std::vector<Col> cols;
+  for (int m0 = 0; m0 <= M; ++m0)
+    for (int my = -M; my <= M; ++my) {
+      int lz = -1;
+      for (int mz = -Mz; mz <= Mz; ++mz)
+        if (lim(mz, my) >= m0) lz = std::max(lz, std::abs(mz));
+      if (lz < 0) continue;
+      for (int mz = -lz; mz <= lz; ++mz)
+        if (lim(mz, my) < m0) throw RuntimeError("plane-wave band is not z-convex");
+      cols.push_back({my, m0, lz});
+    }
+  std::stable_sort(cols.begin(), cols.end(), [](const Col& a, const Col& b) {
+    if (a.lz != b.lz) return a.lz > b.lz;
+    int ra = a.my * a.my + a.m0 * a.m0, rb = b.my * b.my + b.m0 * b.m0;
+    if (ra != rb) return ra < rb;
+    if (a.m0 != b.m0) return a.m0 < b.m0;
+    return a.my < b.my;
+  });
+  const int ncol = (int)cols.size();
+  std::vector<int> col_my(ncol), col_m0(ncol), col_lz(ncol), slab_ncol(Nz), slab_off(Nz + 1, 0), m0_start(M + 2, 0),
+      m0_cols;
+  for (int c = 0; c < ncol; ++c) {
+    col_my[c] = cols[c].my;
+    col_m0[c] = cols[c].m0;
+    col_lz[c] = cols[c].lz;
+  }
+  for (int s = 0; s < Nz; ++s) {
+    int mz = s - Mz, cnt = 0;
+    for (int c = 0; c < ncol; ++c) cnt += col_lz[c] >= std::abs(mz);
+    slab_ncol[s] = cnt;
+    slab_off[s + 1] = slab_off[s] + cnt;
+  }
+  const int nhalf = slab_off[Nz];
+  std::vector<int> mode_code(nhalf);
+  for (int s = 0; s < Nz; ++s)
+    for (int c = 0; c < slab_ncol[s]; ++c) mode_code[slab_off[s] + c] = (s << 16) | c;
+  for (int m0 = 0; m0 <= M; ++m0) {
+    for (int c = 0; c < ncol; ++c)
+      if (col_m0[c] == m0) m0_cols.push_back(c);
+    m0_start[m0 + 1] = (int)m0_cols.size();
+  }
+  Packer pk;
+  size_t oE = pk.add(E), oEz = pk.add(Ez), omy = pk.add(col_my), om0 = pk.add(col_m0), olz = pk.add(col_lz),
+         oso = pk.add(slab_off), osn = pk.add(slab_ncol), oms = pk.add(m0_start), omc = pk.add(m0_cols),
+         omd = pk.add(mode_code);
+  char* h = (char*)pinned_.get(name, pk.total);
+  for (auto& it : pk.items) std::memcpy(h + it.off, it.src, it.bytes);
+  char* d = (char*)arena_.get(name, pk.total);
+  cuda_check(cudaMemcpyAsync(d, h, pk.total, cudaMemcpyHostToDevice, st_), "grid upload");
+  sync();
+  PWGrid& g = gd.g;
+  g.N = N;
+  g.M = M;
+  g.Nz = Nz;
+  g.Mz = Mz;
+  g.p = p;
+  g.pz = pz;
+  g.dim = dim;
+  g.ncol = ncol;
+  g.nhalf = nhalf;
+  g.E = (const double2*)(d + oE);
+  g.Ez = (const double2*)(d + oEz);
+  g.col_my = (const int*)(d + omy);
+  g.col_m0 = (const int*)(d + om0);
+  g.col_lz = (const int*)(d + olz);
+  g.slab_off = (const int*)(d + oso);
+  g.slab_ncol = (const int*)(d + osn);
+  g.m0_start = (const int*)(d + oms);
+  g.m0_cols = (const int*)(d + omc);
+  g.mode_code = (const int*)(d + omd);
+  gd.key_N = N;
+  gd.key_p = p;
+  gd.key_dim = dim;
+  gd.key_theta = theta;
+  gd.key_band = br2;
+  gd.col_lz_host = col_lz;
+  return gd;
+}
+
+// ------------------------------------------------------------ problem ----
+void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode) {
+  Problem& pr = prob_;
+  pr.ready = false;
+  pr.plan = P;
+  pr.dim = dim;
+  pr.periodic = mode == 1;
+  pr.nch = channels_out(P.kernel, dim);
+  pr.sc = strength_width(P.kernel, dim);
+  pr.ns = ns;
+  pr.alias = nt == 0;
+  pr.nt = pr.alias ? ns : nt;
+  const int d = dim;
+  double* src = arena_.as<double>("src_in", (size_t)ns * d);
+  double* tgt = pr.alias ? nullptr : arena_.as<double>("tgt_in", (size_t)nt * d);
+  double* str = arena_.as<double>("str_in", (size_t)ns * pr.sc);
+  int* flags = arena_.as<int>("flags", 8);
+  cuda_check(cudaMemsetAsync(flags, 0, 8 * sizeof(int), st_), "memset");
+  // validate_system (oracle.cpp:103-131) then wrap_into_box (oracle.cpp:133-141)
+  launch_validate(src, (int64_t)ns * d, pr.periodic, flags, 0, st_);
+  if (tgt) launch_validate(tgt, (int64_t)nt * d, pr.periodic, flags, 0, st_);
+  launch_validate(str, (int64_t)ns * pr.sc, 1, flags, 2, st_);
+  if (pr.periodic) {
+    launch_wrap(src, (int64_t)ns * d, st_);
+    if (tgt) launch_wrap(tgt, (int64_t)nt * d, st_);
+  }
+  launches_ += 3 + (pr.periodic ? 2 : 0);
+  // Morton sort (tree.cpp:258-281)
+  auto sort_set = [&](const double* pts, int n, const std::string& tag, int*& perm, double*& soa, int32_t*& q) {
+    uint64_t* klo = arena_.as<uint64_t>("klo", n);
+    uint64_t* khi = arena_.as<uint64_t>("khi", n);
+    uint64_t* klo2 = arena_.as<uint64_t>("klo2", n);
+    uint64_t* khi2 = arena_.as<uint64_t>("khi2", n);
+    int* idx = arena_.as<int>("idx", n);
+    int* idx2 = arena_.as<int>("idx2", n);
+    perm = arena_.as<int>(tag + "perm", n);
+    size_t tb = sort_temp_bytes(n);
+    void* tmp = arena_.get("sort_tmp", tb);
+    launch_morton(pts, n, d, klo, khi, idx, st_);
+    sort_morton(n, d, klo, khi, idx, klo2, khi2, idx2, perm, tmp, tb, st_);
+    soa = arena_.as<double>(tag + "pts", (size_t)n * d);
+    q = arena_.as<int32_t>(tag + "q", (size_t)n * d);
+    launch_gather_points(pts, perm, n, d, soa, q, st_);
+    launches_ += 3;
+  };
+  int32_t *sq = nullptr, *tq = nullptr;
+  sort_set(src, ns, "s", pr.sperm, pr.spts, sq);
+  pr.sstr = arena_.as<double>("sstr", (size_t)ns * pr.sc);
+  launch_gather_strengths(str, pr.sperm, ns, pr.sc, pr.sstr, st_);
+  ++launches_;
+  if (!pr.alias) {
+    sort_set(tgt, nt, "t", pr.tperm, pr.tpts, tq);
+    pr.tpts_caller = tgt;
+  } else {
+    pr.tperm = pr.sperm;
+    pr.tpts = pr.spts;
+    pr.tpts_caller = src;
+  }
+  // quantized coordinates -> host for the box topology
+  int32_t* hq = (int32_t*)pinned_.get("hq", sizeof(int32_t) * ((size_t)ns + (pr.alias ? 0 : nt)) * d + 64);
+  int* hflags = (int*)pinned_.get("hflags", 64);
+  cuda_check(cudaMemcpyAsync(hq, sq, sizeof(int32_t) * (size_t)ns * d, cudaMemcpyDeviceToHost, st_), "D2H q");
+  if (!pr.alias)
+    cuda_check(cudaMemcpyAsync(hq + (size_t)ns * d, tq, sizeof(int32_t) * (size_t)nt * d, cudaMemcpyDeviceToHost, st_),
+               "D2H q");
+  cuda_check(cudaMemcpyAsync(hflags, flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H flags");
+  sync();
+  if (hflags[2]) throw InvalidArgument("ParticleSystem: non-finite strength");
+  if (hflags[0]) throw InvalidArgument("ParticleSystem: non-finite coordinate");
+  if (hflags[1]) throw InvalidArgument("ParticleSystem: coordinate outside the unit box");
+  pr.tree = build_topology(d, pr.periodic, P.n_s, P.p, ns, hq, pr.alias ? 0 : nt,
+                           pr.alias ? nullptr : hq + (size_t)ns * d);
+  upload_tree_lists();
+  pr.ready = true;
+}
+
+void Context::upload_tree_lists() {
+  Problem& pr = prob_;
+  const HostTree& t = pr.tree;
+  const int nb = t.num_boxes(), d = pr.dim, nchild = 1 << d;
+  std::vector<dev::DBox> boxes(nb);
+  for (int b = 0; b < nb; ++b) {
+    const Box& x = t.boxes[b];
+    dev::DBox& o = boxes[b];
+    o.sb = x.sb;
+    o.se = x.se;
+    o.tb = x.tb;
+    o.te = x.te;
+    o.level = x.level;
+    o.parent = x.parent;
+    o.first_child = x.first_child;
+    o.leaf = x.leaf;
+    auto c = t.center(b);
+    o.c[0] = c[0];
+    o.c[1] = c[1];
+    o.c[2] = c[2];
+    o.side = t.side(b);
+    o.half = 0.5 * o.side;
+  }
+  std::vector<int> ant, itp, rs(1, 0), rbox, rinfo;
+  for (int b = 0; b < nb; ++b) {
+    if (t.boxes[b].leaf && t.nsrc(b) > 0) ant.push_back(b);
+    if (t.boxes[b].leaf && t.ntgt(b) > 0) itp.push_back(b);
+  }
+  // near ranges per target leaf (dmk.cpp:966-990)
+  auto scode = [](const int8_t* s) { return (s[0] + 1) + 3 * (s[1] + 1) + 9 * (s[2] + 1); };
+  int max_ranges = 0;
+  for (int b : itp) {
+    int before = (int)rbox.size();
+    auto add = [&](int sbx, const int8_t* sh, bool fine_scale, bool self) {
+      if (t.nsrc(sbx) == 0) return;
+      rbox.push_back(sbx);
+      rinfo.push_back(scode(sh) | (fine_scale ? 32 : 0) | (self ? 64 : 0));
+    };
+    const int8_t zero[3] = {0, 0, 0};
+    add(b, zero, false, true);
+    for (const Nbr& e : t.col[b]) {
+      if (e.box == b && !e.shift[0] && !e.shift[1] && !e.shift[2]) continue;
+      if (!t.boxes[e.box].leaf) continue;
+      add(e.box, e.shift, true, false);
+    }
+    for (const Nbr& e : t.crs[b]) add(e.box, e.shift, false, false);
+    for (const Nbr& e : t.fin[b]) add(e.box, e.shift, true, false);
+    rs.push_back((int)rbox.size());
+    max_ranges = std::max(max_ranges, (int)rbox.size() - before);
+  }
+  if (max_ranges > 160) throw RuntimeError("residual pass: more than 160 near ranges for one leaf");
+  // per-level lists
+  const int L = t.max_level + 1;
+  struct LV {
+    std::vector<int> m_out, m_in, m_ci, i_in, i_out, i_ci, sbx, tbx, es, eslot, etau;
+  };
+  std::vector<LV> lv(L);
+  std::vector<int> gslot(nb, -1);
+  for (int lev = 0; lev < L; ++lev) {
+    LV& V = lv[lev];
+    for (int b : t.level_boxes[lev]) {
+      const Box& x = t.boxes[b];
+      if (!x.leaf && t.nsrc(b) > 0) {  // upward merge (dmk.cpp:638-651)
+        V.m_out.push_back(b);
+        for (int ci = 0; ci < nchild; ++ci) {
+          int c = x.first_child + ci;
+          V.m_in.push_back(t.nsrc(c) > 0 ? c : -1);
+          V.m_ci.push_back(ci);
+        }
+      }
+      if (!x.leaf && t.ntgt(b) > 0)  // downward interpolation (dmk.cpp:840-853)
+        for (int ci = 0; ci < nchild; ++ci) {
+          int c = x.first_child + ci;
+          if (t.ntgt(c) == 0) continue;
+          V.i_in.push_back(b);
+          V.i_out.push_back(c);
+          V.i_ci.push_back(ci);
+        }
+      if (t.nsrc(b) > 0) {
+        gslot[b] = (int)V.sbx.size();
+        V.sbx.push_back(b);
+      }
+    }
+    // plane-wave targets and their colleague entries (dmk.cpp:760-797)
+    const int64_t side_int = int64_t(1) << (30 - lev);
+    V.es.push_back(0);
+    for (int b : t.level_boxes[lev]) {
+      if (t.ntgt(b) == 0) continue;
+      int cnt = 0;
+      for (const Nbr& ce : t.col[b]) {
+        if (t.boxes[b].leaf && ce.box == b && !ce.shift[0] && !ce.shift[1] && !ce.shift[2]) continue;
+        if (t.nsrc(ce.box) == 0) continue;
+        int tau[3] = {0, 0, 0};
+        for (int ax = 0; ax < d; ++ax) {
+          int64_t diff = int64_t(t.boxes[ce.box].anchor[ax]) + (int64_t(ce.shift[ax]) << 30) -
+                         int64_t(t.boxes[b].anchor[ax]);
+          tau[ax] = int(diff / side_int);
+          if (tau[ax] < -1 || tau[ax] > 1) throw RuntimeError("colleague offset outside {-1,0,1}");
+        }
+        V.eslot.push_back(gslot[ce.box]);
+        V.etau.push_back((tau[0] + 1) + 3 * (tau[1] + 1) + 9 * (tau[2] + 1));
+        ++cnt;
+      }
+      if (cnt == 0) continue;
+      if (cnt > 64) throw RuntimeError("plane-wave pass: more than 64 colleague entries");
+      V.tbx.push_back(b);
+      V.es.push_back((int)V.eslot.size());
+    }
+  }
+  // root lists: box 0 with one zero-offset entry
+  std::vector<int> root_ids = {0}, root_es = {0, 1}, root_slot = {0}, root_tau = {13};
+  Packer pk;
+  size_t o_boxes = pk.add(boxes), o_ant = pk.add(ant), o_itp = pk.add(itp), o_rs = pk.add(rs), o_rbox = pk.add(rbox),
+         o_rinfo = pk.add(rinfo), o_rid = pk.add(root_ids), o_res = pk.add(root_es), o_rsl = pk.add(root_slot),
+         o_rta = pk.add(root_tau);
+  struct Off {
+    size_t m_out, m_in, m_ci, i_in, i_out, i_ci, sbx, tbx, es, eslot, etau;
+  };
+  std::vector<Off> off(L);
+  for (int lev = 0; lev < L; ++lev) {
+    LV& V = lv[lev];
+    off[lev] = {pk.add(V.m_out), pk.add(V.m_in), pk.add(V.m_ci), pk.add(V.i_in), pk.add(V.i_out), pk.add(V.i_ci),
+                pk.add(V.sbx),   pk.add(V.tbx),  pk.add(V.es),   pk.add(V.eslot), pk.add(V.etau)};
+  }
+  char* h = (char*)pinned_.get("tree", pk.total + 64);
+  for (auto& it : pk.items)
+    if (it.bytes) std::memcpy(h + it.off, it.src, it.bytes);
+  char* dv = (char*)arena_.get("tree", pk.total + 64);
+  cuda_check(cudaMemcpyAsync(dv, h, pk.total, cudaMemcpyHostToDevice, st_), "tree upload");
+  pr.boxes = (dev::DBox*)(dv + o_boxes);
+  pr.ant_leaves = (int*)(dv + o_ant);
+  pr.int_leaves = (int*)(dv + o_itp);
+  pr.n_ant = (int)ant.size();
+  pr.n_int = (int)itp.size();
+  pr.rng_start = (int*)(dv + o_rs);
+  pr.rng_box = (int*)(dv + o_rbox);
+  pr.rng_info = (int*)(dv + o_rinfo);
+  pr.levels.assign(L, {});
+  for (int lev = 0; lev < L; ++lev) {
+    Problem::LevelLists& X = pr.levels[lev];
+    LV& V = lv[lev];
+    X.n_merge = (int)V.m_out.size();
+    X.n_interp = (int)V.i_out.size();
+    X.n_src = (int)V.sbx.size();
+    X.n_tgt = (int)V.tbx.size();
+    X.merge_out = (int*)(dv + off[lev].m_out);
+    X.merge_in = (int*)(dv + off[lev].m_in);
+    X.merge_ci = (int*)(dv + off[lev].m_ci);
+    X.interp_in = (int*)(dv + off[lev].i_in);
+    X.interp_out = (int*)(dv + off[lev].i_out);
+    X.interp_ci = (int*)(dv + off[lev].i_ci);
+    X.src_boxes = (int*)(dv + off[lev].sbx);
+    X.tgt_boxes = (int*)(dv + off[lev].tbx);
+    X.ent_start = (int*)(dv + off[lev].es);
+    X.ent_slot = (int*)(dv + off[lev].eslot);
+    X.ent_tau = (int*)(dv + off[lev].etau);
+  }
+  // root lists live after the per-level ones in the same blob
+  root_dev_ids_ = (int*)(dv + o_rid);
+  root_dev_es_ = (int*)(dv + o_res);
+  root_dev_slot_ = (int*)(dv + o_rsl);
+  root_dev_tau_ = (int*)(dv + o_rta);
+  // Chebyshev nodes/weights and the child matrices (dmk.cpp:25-66, 626-629)
+  const int p = pr.plan.p;
+  Cheb1 cb(p);
+  std::vector<double> m0 = cb.child(0), m1 = cb.child(1), t0 = transpose(m0, p), t1 = transpose(m1, p);
+  std::vector<double> blob;
+  blob.insert(blob.end(), cb.x.begin(), cb.x.end());
+  blob.insert(blob.end(), cb.w.begin(), cb.w.end());
+  blob.insert(blob.end(), t0.begin(), t0.end());  // upward: transposed child matrices
+  blob.insert(blob.end(), t1.begin(), t1.end());
+  blob.insert(blob.end(), m0.begin(), m0.end());  // downward: child matrices
+  blob.insert(blob.end(), m1.begin(), m1.end());
+  double* hb = (double*)pinned_.get("cheb", blob.size() * sizeof(double));
+  std::memcpy(hb, blob.data(), blob.size() * sizeof(double));
+  double* db = arena_.as<double>("cheb", blob.size());
+  cuda_check(cudaMemcpyAsync(db, hb, blob.size() * sizeof(double), cudaMemcpyHostToDevice, st_), "cheb upload");
+  cheb_nodes_ = db;
+  cheb_wts_ = db + p;
+  mats_up_ = db + 2 * p;
+  mats_down_ = db + 2 * p + 2 * p * p;
+  sync();  // pinned staging buffers are reused by the next call
+}
+
+// ---------------------------------------------------------------- passes --
+void Context::run_upward() {  // dmk.cpp:555-655
+  Problem& pr = prob_;
+  const int d = pr.dim, p = pr.plan.p, pz = d == 3 ? p : 1;
+  const size_t nodes = (size_t)pz * p * p;
+  const int nb = pr.tree.num_boxes();
+  double* og = arena_.as<double>("outgoing", (size_t)nb * pr.nch * nodes);
+  cuda_check(cudaMemsetAsync(og, 0, sizeof(double) * nb * pr.nch * nodes, st_), "memset outgoing");
+  ChebDev cb{p, pz, d, cheb_nodes_, cheb_wts_};
+  launch_anterp(pr.plan.kernel, cb, pr.boxes, pr.ant_leaves, pr.n_ant, pr.spts, pr.ns, pr.sstr, og, pr.nch, st_);
+  ++launches_;
+  for (int lev = pr.tree.max_level - 1; lev >= 0; --lev) {
+    const Problem::LevelLists& X = pr.levels[lev];
+    if (X.n_merge == 0) continue;
+    launch_tensor_apply(p, pz, d, mats_up_, X.merge_in, X.merge_out, X.merge_ci, X.n_merge, pr.nch, og, og, 2, st_);
+    ++launches_;
+  }
+}
+
+void Context::run_root() {  // dmk.cpp:657-701
+  Problem& pr = prob_;
+  const Plan& P = pr.plan;
+  const int d = pr.dim, p = P.p, pz = d == 3 ? p : 1;
+  const size_t nodes = (size_t)pz * p * p;
+  const int nb = pr.tree.num_boxes();
+  double* in = arena_.as<double>("incoming", (size_t)nb * d * nodes);
+  cuda_check(cudaMemsetAsync(in, 0, sizeof(double) * nb * d * nodes, st_), "memset incoming");
+  const int N = pr.periodic ? P.N_per : P.N1;
+  const double h = pr.periodic ? 2.0 * PI : PI / 3.0;
+  const int M = (N - 1) / 2;
+  GridDev& gd = grid(grid_root_, "grid_root", d, p, N, 0.5 * h, band_r2(P, M, h));
+  const PWGrid& g = gd.g;
+  std::vector<double> A = symbol_table(*tab_, h, 3 * M * M, pr.periodic ? kRootPeriodic : kRootFree, 1.0, 1.0);
+  double* hA = (double*)pinned_.get("symroot", A.size() * sizeof(double));
+  std::memcpy(hA, A.data(), A.size() * sizeof(double));
+  double* dA = arena_.as<double>("symroot", A.size());
+  cuda_check(cudaMemcpyAsync(dA, hA, A.size() * sizeof(double), cudaMemcpyHostToDevice, st_), "symbol upload");
+  const double pf = pr.periodic ? 1.0 : std::pow(1.0 / 6.0, d);
+  double2* B = arena_.as<double2>("pw_B_root", (size_t)pr.nch * g.pz * g.ncol);
+  double2* G = arena_.as<double2>("pw_G_root", (size_t)pr.nch * g.nhalf);
+  double2* F = arena_.as<double2>("pw_F_root", (size_t)d * g.nhalf);
+  double2* C = arena_.as<double2>("pw_C_root", (size_t)d * g.pz * g.ncol);
+  launch_forward(g, root_dev_ids_, 1, pr.nch, arena_.as<double>("outgoing", 1), B, G, st_);
+  launch_accumulate_symbol(g, P.kernel, 1, root_dev_es_, root_dev_slot_, root_dev_tau_, G, pr.nch, dA, h, F, st_);
+  launch_inverse(g, root_dev_ids_, 1, d, F, C, pf, in, st_);
+  launches_ += 5;
+  sync();  // hA is reused
+}
+
+void Context::run_downward() {  // dmk.cpp:705-857
+  Problem& pr = prob_;
+  const Plan& P = pr.plan;
+  const int d = pr.dim, p = P.p, pz = d == 3 ? p : 1;
+  const double* og = arena_.as<double>("outgoing", 1);
+  double* in = arena_.as<double>("incoming", 1);
+  const int M = (P.N1 - 1) / 2;
+  GridDev& gd = grid(grid_lev_, "grid_lev", d, p, P.N1, PI / 3.0, band_r2(P, M, PI / 3.0));
+  const PWGrid& g = gd.g;
+  const int L = pr.tree.max_level + 1;
+  const int S = 3 * M * M + 1;
+  // per-level symbol tables (dmk.cpp:741-746), one upload
+  std::vector<double> Aall((size_t)L * S);
+  for (int lev = 0; lev < L; ++lev) {
+    double r_c = std::ldexp(1.0, -lev), r_f = 0.5 * r_c, h = PI / (3.0 * r_f);
+    std::vector<double> A = symbol_table(*tab_, h, 3 * M * M, kLevelDiff, r_c, r_f);
+    std::copy(A.begin(), A.end(), Aall.begin() + (size_t)lev * S);
+  }
+  double* hA = (double*)pinned_.get("symlev", Aall.size() * sizeof(double));
+  std::memcpy(hA, Aall.data(), Aall.size() * sizeof(double));
+  double* dA = arena_.as<double>("symlev", Aall.size());
+  cuda_check(cudaMemcpyAsync(dA, hA, Aall.size() * sizeof(double), cudaMemcpyHostToDevice, st_), "symbol upload");
+  const size_t bytes_B = sizeof(double2) * pr.nch * g.pz * g.ncol;
+  const size_t bytes_FC = sizeof(double2) * d * ((size_t)g.nhalf + (size_t)g.pz * g.ncol);
+  const size_t budget = size_t(2) << 30;
+  const int chunk_src = (int)std::max<size_t>(1, budget / bytes_B);
+  const int chunk_tgt = (int)std::max<size_t>(1, budget / bytes_FC);
+  cudaEvent_t e0 = ev_[14], e1 = ev_[15];
+  float pw_ms = 0.0f;
+  for (int lev = 0; lev < L; ++lev) {
+    const Problem::LevelLists& X = pr.levels[lev];
+    if (X.n_src > 0 && X.n_tgt > 0) {
+      double r_c = std::ldexp(1.0, -lev), r_f = 0.5 * r_c, h = PI / (3.0 * r_f);
+      double pf = std::pow(1.0 / (6.0 * r_f), d);
+      double2* G = arena_.as<double2>("pw_G", (size_t)X.n_src * pr.nch * g.nhalf);
+      cudaEventRecord(e0, st_);
+      for (int s0 = 0; s0 < X.n_src; s0 += chunk_src) {
+        int n = std::min(chunk_src, X.n_src - s0);
+        double2* B = arena_.as<double2>("pw_B", (size_t)n * pr.nch * g.pz * g.ncol);
+        launch_forward(g, X.src_boxes + s0, n, pr.nch, og, B, G + (size_t)s0 * pr.nch * g.nhalf, st_);
+        launches_ += 2;
+      }
+      for (int t0 = 0; t0 < X.n_tgt; t0 += chunk_tgt) {
+        int n = std::min(chunk_tgt, X.n_tgt - t0);
+        double2* F = arena_.as<double2>("pw_F", (size_t)n * d * g.nhalf);
+        double2* C = arena_.as<double2>("pw_C", (size_t)n * d * g.pz * g.ncol);
+        launch_accumulate_symbol(g, P.kernel, n, X.ent_start + t0, X.ent_slot, X.ent_tau, G, pr.nch,
+                                 dA + (size_t)lev * S, h, F, st_);
+        launch_inverse(g, X.tgt_boxes + t0, n, d, F, C, pf, in, st_);
+        launches_ += 3;
+      }
+      cudaEventRecord(e1, st_);
+      cudaEventSynchronize(e1);
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      pw_ms += ms;
+    }
+    if (X.n_interp > 0) {
+      launch_tensor_apply(p, pz, d, mats_down_, X.interp_in, X.interp_out, X.interp_ci, X.n_interp, d, in, in, 1,
+                          st_);
+      ++launches_;
+    }
+  }
+  t_pw_ms_ = pw_ms;
+  sync();
+}
+
+void Context::run_target_far(double* ufar) {  // dmk.cpp:861-915
+  Problem& pr = prob_;
+  const int p = pr.plan.p, pz = pr.dim == 3 ? p : 1;
+  ChebDev cb{p, pz, pr.dim, cheb_nodes_, cheb_wts_};
+  launch_interp_targets(cb, pr.boxes, pr.int_leaves, pr.n_int, pr.tpts, pr.nt, pr.tperm,
+                        arena_.as<double>("incoming", 1), ufar, st_);
+  ++launches_;
+}
+
+void Context::run_residual(double* ures, bool stats) {  // dmk.cpp:919-1032
+  Problem& pr = prob_;
+  const Tables& T = *tab_;
+  const Cheb* cd = nullptr;
+  const Cheb* co = nullptr;
+  if (pr.plan.kernel == kStokeslet) {
+    cd = &T.s_diag;
+    co = &T.s_offd;
+  } else if (pr.plan.kernel == kStresslet) {
+    cd = &T.t_diag;
+    co = &T.t_offd;
+  } else {
+    co = &T.w_offd;
+  }
+  if ((cd && cd->a.size() > 128) || co->a.size() > 128) throw RuntimeError("residual table longer than 128 coefficients");
+  if (cd && (cd->lo != co->lo || cd->hi != co->hi)) throw RuntimeError("residual tables on different intervals");
+  ResidTables rt{cd ? (int)cd->a.size() : 0, (int)co->a.size(), co->lo, co->hi, T.support, pr.plan.kernel, pr.dim};
+  double* hc = (double*)pinned_.get("rtab", 256 * sizeof(double));
+  std::fill(hc, hc + 256, 0.0);
+  if (cd) std::copy(cd->a.begin(), cd->a.end(), hc);
+  std::copy(co->a.begin(), co->a.end(), hc + 128);
+  set_residual_tables(hc, rt.nd, hc + 128, rt.no, st_);
+  int* flags = arena_.as<int>("flags", 8);
+  unsigned long long* st = arena_.as<unsigned long long>("stats", 4);
+  if (stats) cuda_check(cudaMemsetAsync(st, 0, 4 * sizeof(unsigned long long), st_), "memset");
+  cudaEventRecord(ev_[13], st_);
+  launch_residual(rt, pr.boxes, pr.int_leaves, pr.n_int, pr.rng_start, pr.rng_box, pr.rng_info, pr.spts, pr.ns,
+                  pr.sstr, pr.tpts, pr.nt, pr.tperm, pr.alias ? 1 : 0, 0.0, T.self_const, ures, flags + 3,
+                  stats ? st : nullptr, st_);
+  cudaEventRecord(ev_[12], st_);
+  ++launches_;
+}
+
+// ------------------------------------------------------------- entries --
+void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, int64_t nt, const double* tgt,
+                       const double* str, int mode, double* u, sdmk_report* rep, bool device_ptrs) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  check_inputs(P, dim, ns, nt, mode);
+  tab_ = &tables_for(P);
+  if (tab_->kernel != P.kernel || tab_->dim != P.dim || tab_->win.kind != P.window)
+    throw InvalidArgument("evaluate: supplied split tables do not match the plan");
+  launches_ = 0;
+  const int sc = strength_width(P.kernel, dim);
+  const bool alias = nt == 0;
+  const int ntt = alias ? (int)ns : (int)nt;
+  cudaMemcpyKind kind = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  cudaEventRecord(ev_[0], st_);
+  cuda_check(cudaMemcpyAsync(arena_.as<double>("src_in", (size_t)ns * dim), src, sizeof(double) * ns * dim, kind, st_),
+             "copy sources");
+  if (!alias)
+    cuda_check(
+        cudaMemcpyAsync(arena_.as<double>("tgt_in", (size_t)nt * dim), tgt, sizeof(double) * nt * dim, kind, st_),
+        "copy targets");
+  cuda_check(cudaMemcpyAsync(arena_.as<double>("str_in", (size_t)ns * sc), str, sizeof(double) * ns * sc, kind, st_),
+             "copy strengths");
+  cudaEventRecord(ev_[1], st_);
+  build_problem(P, dim, (int)ns, (int)nt, mode);
+  cudaEventRecord(ev_[2], st_);
+  run_upward();
+  cudaEventRecord(ev_[3], st_);
+  run_root();
+  cudaEventRecord(ev_[4], st_);
+  double* ufar = arena_.as<double>("ufar", (size_t)ntt * dim);
+  double* ures = arena_.as<double>("ures", (size_t)ntt * dim);
+  run_downward();
+  run_target_far(ufar);
+  cudaEventRecord(ev_[5], st_);
+  run_residual(ures, rep != nullptr);
+  // global terms (dmk.cpp:1086-1102)
+  Problem& pr = prob_;
+  double* sums = arena_.as<double>("sums", 16);
+  double* scratch = arena_.as<double>("sum_scratch", 256 * 8);
+  double corr_scale = 0.0;
+  const double* corr = nullptr;
+  const double* zm = nullptr;
+  if (P.kernel == kStokeslet && !pr.periodic && tab_->corr_const != 0.0) {
+    launch_column_sums(pr.sstr, pr.ns, dim, sums, scratch, st_);
+    corr = sums;
+    corr_scale = tab_->corr_const;
+    launches_ += 2;
+  }
+  if (P.kernel == kStresslet && pr.periodic) {
+    launch_zero_mode_moments(pr.spts, pr.sstr, pr.ns, dim, sums + 8, scratch, st_);
+    zm = sums + 8;
+    launches_ += 2;
+  }
+  double* du = device_ptrs ? u : arena_.as<double>("u", (size_t)ntt * dim);
+  launch_combine(ntt, dim, ufar, ures, corr, corr_scale, zm, pr.tpts_caller, du, st_);
+  ++launches_;
+  cudaEventRecord(ev_[6], st_);
+  if (!device_ptrs)
+    cuda_check(cudaMemcpyAsync(u, du, sizeof(double) * ntt * dim, cudaMemcpyDeviceToHost, st_), "copy u");
+  cudaEventRecord(ev_[7], st_);
+  int* hflags = (int*)pinned_.get("hflags", 64);
+  cuda_check(cudaMemcpyAsync(hflags, arena_.as<int>("flags", 8), 8 * sizeof(int), cudaMemcpyDeviceToHost, st_),
+             "D2H flags");
+  unsigned long long* hst = (unsigned long long*)pinned_.get("hstats", 64);
+  if (rep)
+    cuda_check(cudaMemcpyAsync(hst, arena_.as<unsigned long long>("stats", 4), 4 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, st_),
+               "D2H stats");
+  sync();
+  cuda_check(cudaGetLastError(), "kernel launch");
+  if (hflags[3]) throw DomainError("residual_pass: coincident points");
+  if (rep) {
+    rep->num_boxes = pr.tree.num_boxes();
+    rep->max_level = pr.tree.max_level;
+    rep->num_sources = (int)ns;
+    rep->num_targets = ntt;
+    rep->t_h2d = ev_ms(0, 1) * 1e-3;
+    rep->t_tree = ev_ms(1, 2) * 1e-3;
+    rep->t_upward = ev_ms(2, 3) * 1e-3;
+    rep->t_root = ev_ms(3, 4) * 1e-3;
+    rep->t_downward = ev_ms(4, 5) * 1e-3;
+    rep->t_residual = ev_ms(5, 6) * 1e-3;
+    rep->t_d2h = ev_ms(6, 7) * 1e-3;
+    rep->t_total = ev_ms(0, 7) * 1e-3;
+    rep->t_residual_kernel = ev_ms(13, 12) * 1e-3;
+    rep->t_planewave = t_pw_ms_ * 1e-3;
+    rep->p2p_candidates = (int64_t)hst[0];
+    rep->p2p_in_support = (int64_t)hst[1];
+    rep->kernel_launches = launches_;
+  }
+}
+
+void Context::setup(const Plan& P, int dim, int64_t ns, const double* src, int64_t nt, const double* tgt,
+                    const double* str, int mode) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  prob_.ready = false;
+  check_inputs(P, dim, ns, nt, mode);
+  tab_ = &tables_for(P);
+  const int sc = strength_width(P.kernel, dim);
+  cuda_check(cudaMemcpyAsync(arena_.as<double>("src_in", (size_t)ns * dim), src, sizeof(double) * ns * dim,
+                             cudaMemcpyHostToDevice, st_),
+             "copy sources");
+  if (nt > 0)
+    cuda_check(cudaMemcpyAsync(arena_.as<double>("tgt_in", (size_t)nt * dim), tgt, sizeof(double) * nt * dim,
+                               cudaMemcpyHostToDevice, st_),
+               "copy targets");
+  cuda_check(cudaMemcpyAsync(arena_.as<double>("str_in", (size_t)ns * sc), str, sizeof(double) * ns * sc,
+                             cudaMemcpyHostToDevice, st_),
+             "copy strengths");
+  build_problem(P, dim, (int)ns, (int)nt, mode);
+}
+
+static void need(const Problem& p) {
+  if (!p.ready) throw InvalidArgument("no problem set up in this context (call sdmk_setup first)");
+}
+
+void Context::upward(double* out) {
+  need(prob_);
+  run_upward();
+  const int p = prob_.plan.p, pz = prob_.dim == 3 ? p : 1;
+  size_t n = (size_t)prob_.tree.num_boxes() * prob_.nch * pz * p * p;
+  cuda_check(cudaMemcpyAsync(out, arena_.as<double>("outgoing", 1), n * sizeof(double), cudaMemcpyDeviceToHost, st_),
+             "D2H outgoing");
+  sync();
+}
+
+void Context::incoming(int stage, double* out) {
+  need(prob_);
+  run_upward();
+  run_root();
+  if (stage >= 1) run_downward();
+  const int p = prob_.plan.p, pz = prob_.dim == 3 ? p : 1;
+  size_t n = (size_t)prob_.tree.num_boxes() * prob_.dim * pz * p * p;
+  cuda_check(cudaMemcpyAsync(out, arena_.as<double>("incoming", 1), n * sizeof(double), cudaMemcpyDeviceToHost, st_),
+             "D2H incoming");
+  sync();
+}
+
+void Context::target_far(double* out) {
+  need(prob_);
+  run_upward();
+  run_root();
+  run_downward();
+  double* uf = arena_.as<double>("ufar", (size_t)prob_.nt * prob_.dim);
+  run_target_far(uf);
+  cuda_check(cudaMemcpyAsync(out, uf, sizeof(double) * prob_.nt * prob_.dim, cudaMemcpyDeviceToHost, st_), "D2H u");
+  sync();
+}
+
+void Context::residual(double* out) {
+  need(prob_);
+  int* flags = arena_.as<int>("flags", 8);
+  cuda_check(cudaMemsetAsync(flags, 0, 8 * sizeof(int), st_), "memset");
+  double* ur = arena_.as<double>("ures", (size_t)prob_.nt * prob_.dim);
+  run_residual(ur, false);
+  int* hflags = (int*)pinned_.get("hflags", 64);
+  cuda_check(cudaMemcpyAsync(out, ur, sizeof(double) * prob_.nt * prob_.dim, cudaMemcpyDeviceToHost, st_), "D2H u");
+  cuda_check(cudaMemcpyAsync(hflags, flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H flags");
+  sync();
+  cuda_check(cudaGetLastError(), "kernel launch");
+  if (hflags[3]) throw DomainError("residual_pass: coincident points");
+}
+
+}  // namespace sdmkb

@@ -1,0 +1,141 @@
+// The B200 DMK engine: owns the device, stream, buffers and the current
+// problem; implements evaluate_with_plan (dmk.cpp:1036-1117) and the
+// pass-level entry points of dmk.hpp on the GPU.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/sdmk.h"
+#include "host/setup.hpp"
+#include "host/tree.hpp"
+#include "kernels/launch.hpp"
+
+namespace sdmkb {
+
+struct CudaError : std::exception {
+  std::string msg;
+  explicit CudaError(std::string m) : msg(std::move(m)) {}
+  const char* what() const noexcept override { return msg.c_str(); }
+};
+struct OomError : std::exception {
+  std::string msg;
+  explicit OomError(std::string m) : msg(std::move(m)) {}
+  const char* what() const noexcept override { return msg.c_str(); }
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+// Grow-only named device buffers (cudaMalloc is far too slow per call).
+class Arena {
+ public:
+  ~Arena();
+  void* get(const std::string& name, size_t bytes);
+  template <class T>
+  T* as(const std::string& name, size_t count) { return static_cast<T*>(get(name, count * sizeof(T))); }
+  size_t bytes() const;
+
+ private:
+  std::map<std::string, std::pair<void*, size_t>> bufs_;
+};
+
+class Pinned {
+ public:
+  ~Pinned();
+  void* get(const std::string& name, size_t bytes);
+
+ private:
+  std::map<std::string, std::pair<void*, size_t>> bufs_;
+};
+
+// Device copy of one plane-wave grid (PWGrid + its arrays in one blob).
+struct GridDev {
+  PWGrid g{};
+  int key_N = -1, key_p = -1, key_dim = -1;
+  double key_theta = 0.0, key_band = -1.0;
+  std::vector<int> col_lz_host;
+};
+
+struct Problem {
+  bool ready = false;
+  Plan plan;
+  bool periodic = false;
+  int dim = 3, nch = 3, sc = 3;
+  int ns = 0, nt = 0;  // nt == ns when aliased
+  bool alias = true;
+  HostTree tree;
+  // device views (arena-owned)
+  double *spts = nullptr, *sstr = nullptr, *tpts = nullptr, *tpts_caller = nullptr;
+  int *sperm = nullptr, *tperm = nullptr;
+  // tree lists on device
+  dev::DBox* boxes = nullptr;
+  int *ant_leaves = nullptr, *int_leaves = nullptr;
+  int n_ant = 0, n_int = 0;
+  int *rng_start = nullptr, *rng_box = nullptr, *rng_info = nullptr;
+  struct LevelLists {
+    int n_merge = 0, n_interp = 0, n_src = 0, n_tgt = 0;
+    int *merge_out = nullptr, *merge_in = nullptr, *merge_ci = nullptr;
+    int *interp_in = nullptr, *interp_out = nullptr, *interp_ci = nullptr;
+    int *src_boxes = nullptr, *tgt_boxes = nullptr;
+    int *ent_start = nullptr, *ent_slot = nullptr, *ent_tau = nullptr;
+    int max_entries = 0;
+  };
+  std::vector<LevelLists> levels;
+};
+
+class Context {
+ public:
+  explicit Context(int device);
+  ~Context();
+
+  void load_tables(const std::string& path);
+  const Tables& tables_for(const Plan& plan);
+
+  // Host-pointer evaluation; u may be host memory.  report may be null.
+  void evaluate(const Plan& plan, int dim, int64_t ns, const double* src, int64_t nt, const double* tgt,
+                const double* str, int mode, double* u, sdmk_report* rep, bool device_ptrs);
+
+  // pass-level API
+  void setup(const Plan& plan, int dim, int64_t ns, const double* src, int64_t nt, const double* tgt,
+             const double* str, int mode);
+  const Problem& problem() const { return prob_; }
+  void upward(double* host_out);
+  void incoming(int stage, double* host_out);
+  void target_far(double* host_out);
+  void residual(double* host_out);
+
+ private:
+  void check_inputs(const Plan& plan, int dim, int64_t ns, int64_t nt, int mode);
+  // inputs already in the arena ("src_in", "tgt_in", "str_in"): validate, wrap, sort, topology, upload
+  void build_problem(const Plan& plan, int dim, int ns, int nt, int mode);
+  void upload_tree_lists();
+  void run_upward();
+  void run_root();
+  void run_downward();
+  void run_target_far(double* ufar);
+  void run_residual(double* ures, bool stats);
+  GridDev& grid(GridDev& cache, const std::string& name, int dim, int p, int N, double theta, double band_r2);
+  void sync();
+  double ev_ms(int a, int b);
+
+  int device_;
+  cudaStream_t st_ = nullptr;
+  cudaEvent_t ev_[16];
+  Arena arena_;
+  Pinned pinned_;
+  std::map<std::string, Tables> tables_;
+  const Tables* tab_ = nullptr;
+  Problem prob_;
+  GridDev grid_lev_, grid_root_;
+  int launches_ = 0;
+  int *root_dev_ids_ = nullptr, *root_dev_es_ = nullptr, *root_dev_slot_ = nullptr, *root_dev_tau_ = nullptr;
+  const double *cheb_nodes_ = nullptr, *cheb_wts_ = nullptr, *mats_up_ = nullptr, *mats_down_ = nullptr;
+  double t_pw_ms_ = 0.0;
+  unsigned long long stats_[3] = {0, 0, 0};
+};
+
+}  // namespace sdmkb

@@ -1,0 +1,56 @@
+// Host-side box topology of the adaptive level-restricted 2^d tree.
+//
+// The points are quantized, Morton-keyed and radix-sorted on the GPU
+// (kernels/tree_kernels.cu); this module consumes the sorted quantized
+// coordinates and reproduces the reference's box ids, ranges and neighbour
+// lists bit-exactly (tree.cpp:62-212): ids follow the DFS subdivision order
+// of refine_to_capacity, then the append order of the 2:1 repair sweeps.
+// Boxes are few (<= ~1e5) compared with points, so this is a host pass;
+// child point ranges come from binary searches over the sorted keys instead
+// of the reference's linear scans (same result: within a box the child index
+// is non-decreasing in Morton order).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace sdmkb {
+
+constexpr int kMaxLevel = 30;
+
+struct Box {
+  int level = 0, parent = -1, first_child = -1;
+  bool leaf = true;
+  int32_t anchor[3] = {0, 0, 0};
+  int sb = 0, se = 0, tb = 0, te = 0;  // permuted source / target ranges
+};
+
+struct Nbr {
+  int box;
+  int8_t shift[3];
+};
+
+struct HostTree {
+  int dim = 3, n_s = 0, p = 0, max_level = 0;
+  bool periodic = false, alias = true, depth_capped = false;
+  std::vector<Box> boxes;
+  std::vector<std::vector<int>> level_boxes;
+  std::vector<std::vector<Nbr>> col, crs, fin;  // colleagues / coarse / fine
+  int num_boxes() const { return (int)boxes.size(); }
+  int nsrc(int b) const { return boxes[b].se - boxes[b].sb; }
+  int ntgt(int b) const { return boxes[b].te - boxes[b].tb; }
+  double side(int b) const;
+  std::array<double, 3> center(int b) const;
+};
+
+// qs / qt: sorted quantized coordinates, SoA (q[axis * n + i]).  nt == 0
+// means the targets alias the sources.
+HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, const int32_t* qs, int nt,
+                        const int32_t* qt);
+
+// The reference's canonical text dump (tree.cpp:325-354).
+std::string dump_topology(const HostTree& t);
+
+}  // namespace sdmkb

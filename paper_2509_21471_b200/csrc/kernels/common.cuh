@@ -1,0 +1,55 @@
+// Shared device-side definitions for the sm_100a DMK kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "launch.hpp"
+
+namespace sdmkb {
+namespace dev {
+
+constexpr double kPI = 3.141592653589793238462643383279502884;
+
+// Barycentric Lagrange basis on first-kind Chebyshev nodes with the exact-hit
+// rule (dmk.cpp:39-53); nodes/weights come from the host (dmk.cpp:30-36).
+__device__ __forceinline__ void cheb_basis(int p, const double* __restrict__ nodes,
+                                           const double* __restrict__ wts, double x,
+                                           double* __restrict__ out, int stride) {
+  int hit = -1;
+  for (int i = 0; i < p; ++i)
+    if (x == nodes[i]) { hit = i; break; }
+  if (hit >= 0) {
+    for (int j = 0; j < p; ++j) out[j * stride] = (j == hit) ? 1.0 : 0.0;
+    return;
+  }
+  double s = 0.0;
+  for (int i = 0; i < p; ++i) {
+    double v = __ddiv_rn(wts[i], __dsub_rn(x, nodes[i]));
+    out[i * stride] = v;
+    s = __dadd_rn(s, v);
+  }
+  double inv = __ddiv_rn(1.0, s);
+  for (int i = 0; i < p; ++i) out[i * stride] = __dmul_rn(out[i * stride], inv);
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a += b * c
+__device__ __forceinline__ void cfma(double2& a, double2 b, double2 c) {
+  a.x = fma(b.x, c.x, a.x);
+  a.x = fma(-b.y, c.y, a.x);
+  a.y = fma(b.x, c.y, a.y);
+  a.y = fma(b.y, c.x, a.y);
+}
+// a += conj(b) * c
+__device__ __forceinline__ void cfma_conj(double2& a, double2 b, double2 c) {
+  a.x = fma(b.x, c.x, a.x);
+  a.x = fma(b.y, c.y, a.x);
+  a.y = fma(b.x, c.y, a.y);
+  a.y = fma(-b.y, c.x, a.y);
+}
+
+}  // namespace dev
+}  // namespace sdmkb

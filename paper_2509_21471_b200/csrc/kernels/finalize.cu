@@ -1,0 +1,96 @@
+// K13: global scalars and the final combine (dmk.cpp:1086-1102,
+// oracle.cpp:250-274).  Sums use compensated per-thread accumulation and a
+// fixed-shape reduction tree, so results are deterministic run to run.
+#include "common.cuh"
+#include "launch.hpp"
+
+namespace sdmkb {
+
+namespace {
+
+constexpr int kSumBlocks = 256;
+constexpr int kSumThreads = 256;
+constexpr int kMaxComp = 4;
+
+struct KSum {
+  double s = 0.0, c = 0.0;
+  __device__ void add(double v) {  // Neumaier
+    double t = s + v;
+    if (fabs(s) >= fabs(v)) c += (s - t) + v;
+    else c += (v - t) + s;
+    s = t;
+  }
+  __device__ double value() const { return s + c; }
+};
+
+// mode 0: columns of soa (ncomp <= 4); mode 1: zero-mode moments (W, sum x (f.n))
+__global__ void __launch_bounds__(kSumThreads) k_partial(int mode, const double* __restrict__ a,
+                                                         const double* __restrict__ b, int n, int ncomp,
+                                                         int dim, double* part) {
+  __shared__ double sh[kMaxComp][kSumThreads];
+  KSum acc[kMaxComp];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (mode == 0) {
+      for (int j = 0; j < ncomp; ++j) acc[j].add(a[(size_t)j * n + i]);
+    } else {
+      double fn = 0.0;
+      for (int k = 0; k < dim; ++k) fn += b[(size_t)k * n + i] * b[(size_t)(dim + k) * n + i];
+      acc[0].add(fn);
+      for (int k = 0; k < dim; ++k) acc[1 + k].add(a[(size_t)k * n + i] * fn);
+    }
+  }
+  for (int j = 0; j < ncomp; ++j) sh[j][threadIdx.x] = acc[j].value();
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s)
+      for (int j = 0; j < ncomp; ++j) sh[j][threadIdx.x] += sh[j][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int j = 0; j < ncomp; ++j) part[(size_t)j * gridDim.x + blockIdx.x] = sh[j][0];
+}
+
+__global__ void k_final(const double* part, int nblk, int ncomp, double* out) {
+  if (threadIdx.x != 0) return;
+  for (int j = 0; j < ncomp; ++j) {
+    KSum s;
+    for (int b = 0; b < nblk; ++b) s.add(part[(size_t)j * nblk + b]);
+    out[j] = s.value();
+  }
+}
+
+__global__ void k_combine(int nt, int dim, const double* __restrict__ ufar, const double* __restrict__ ures,
+                          const double* __restrict__ corr, double cs, const double* __restrict__ zm,
+                          const double* __restrict__ tp, double* __restrict__ u) {
+  int64_t n = (int64_t)nt * dim;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int j = (int)(i % dim);
+    double v = ufar[i] + ures[i];
+    if (corr) v += cs * corr[j];
+    if (zm) v += zm[1 + j] - zm[0] * tp[i];
+    u[i] = v;
+  }
+}
+
+}  // namespace
+
+void launch_column_sums(const double* soa, int n, int ncomp, double* sums, double* scratch, cudaStream_t st) {
+  k_partial<<<kSumBlocks, kSumThreads, 0, st>>>(0, soa, nullptr, n, ncomp, 0, scratch);
+  k_final<<<1, 32, 0, st>>>(scratch, kSumBlocks, ncomp, sums);
+}
+
+void launch_zero_mode_moments(const double* spts, const double* sstr, int n, int dim, double* out, double* scratch,
+                              cudaStream_t st) {
+  k_partial<<<kSumBlocks, kSumThreads, 0, st>>>(1, spts, sstr, n, 1 + dim, dim, scratch);
+  k_final<<<1, 32, 0, st>>>(scratch, kSumBlocks, 1 + dim, out);
+}
+
+void launch_combine(int nt, int dim, const double* ufar, const double* ures, const double* corr, double cs,
+                    const double* zm, const double* tpts_caller, double* u, cudaStream_t st) {
+  int64_t n = (int64_t)nt * dim;
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  k_combine<<<(int)(g < 1 ? 1 : g), 256, 0, st>>>(nt, dim, ufar, ures, corr, cs, zm, tpts_caller, u);
+}
+
+}  // namespace sdmkb

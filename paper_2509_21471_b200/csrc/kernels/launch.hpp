@@ -1,0 +1,128 @@
+// Host-callable launchers for the sm_100a kernels (one .cu per stage).
+// All pointers are device pointers; every launcher enqueues on `st`.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstddef>
+
+namespace sdmkb {
+namespace dev {
+// Per-box record in HBM (64 B, one line per box).  Centers/half sides are
+// computed on the host with the reference's formula (tree.cpp:217-228) so the
+// leaf-local coordinates (x - c) / half agree bit for bit (dmk.cpp:600-603).
+struct DBox {
+  int sb, se, tb, te;
+  int level, parent, first_child, leaf;
+  double c[3];
+  double half;
+  double side;
+};
+
+}  // namespace dev
+
+// ---- tree_kernels.cu -------------------------------------------------------
+// flags[0]: non-finite coordinate, flags[1]: coordinate outside [-1/2, 1/2]
+// (ignored when periodic), flags[2]: non-finite strength.
+void launch_validate(const double* pts, int64_t nvals, int periodic, int* flags, int flag_base,
+                     cudaStream_t st);
+void launch_wrap(double* pts, int64_t nvals, cudaStream_t st);
+// 90/60-bit Morton keys of quantized points (tree.cpp:19-35) split in two
+// 64-bit words, with the identity permutation in idx.
+void launch_morton(const double* pts, int n, int dim, uint64_t* klo, uint64_t* khi, int* idx,
+                   cudaStream_t st);
+// Stable LSD radix sort of (key, index): exactly std::sort over (key, idx)
+// pairs (tree.cpp:262-267).  perm receives the sorted original indices.
+size_t sort_temp_bytes(int n);
+void sort_morton(int n, int dim, uint64_t* klo, uint64_t* khi, int* idx, uint64_t* klo2,
+                 uint64_t* khi2, int* idx2, int* perm, void* temp, size_t temp_bytes, cudaStream_t st);
+// AoS caller-order points -> SoA sorted points + SoA quantized coordinates.
+void launch_gather_points(const double* pts, const int* perm, int n, int dim, double* soa,
+                          int32_t* q, cudaStream_t st);
+// AoS caller-order strengths -> SoA sorted strengths (sc components).
+void launch_gather_strengths(const double* str, const int* perm, int n, int sc, double* soa,
+                             cudaStream_t st);
+
+// ---- anterp.cu (K3 leaf anterpolation, K11 target interpolation) -----------
+struct ChebDev {
+  int p, pz, dim;
+  const double* nodes;  // p
+  const double* wts;    // p
+};
+// outgoing[b][ch][node] for leaves `leaves[0..nleaf)` (outgoing zeroed first)
+void launch_anterp(int kernel, const ChebDev& cb, const dev::DBox* boxes, const int* leaves,
+                   int nleaf, const double* pts, int n, const double* str, double* outgoing,
+                   int nch, cudaStream_t st);
+// u_far[perm[t]*d + j] for targets of leaves `leaves`
+void launch_interp_targets(const ChebDev& cb, const dev::DBox* boxes, const int* leaves, int nleaf,
+                           const double* tpts, int nt, const int* tperm, const double* incoming,
+                           double* ufar, cudaStream_t st);
+
+// ---- tensor.cu (K4 child->parent merge, K9 parent->child interpolation) ----
+// For each pair i: dst[out_box[i]] (+)= (Mz (x) My (x) Mx) src[in_box[i]] on
+// `nch` channels, matrices chosen by the child index bits of ci[i]
+// (dmk.cpp:82-121, 481-490).  mats: [2][p][p] (bit 0 / bit 1).
+// accumulate: 1 -> dst += (one input per pair, downward interpolation);
+//             2 -> merge mode: 2^d inputs per pair (-1 = skip), dst = sum.
+void launch_tensor_apply(int p, int pz, int dim, const double* mats, const int* in_box,
+                         const int* out_box, const int* ci, int npairs, int nch,
+                         const double* src, double* dst, int accumulate, cudaStream_t st);
+
+// ---- planewave.cu (K5-K8/K10: forward DFT, phased accumulation + symbol,
+// inverse DFT) -----------------------------------------------------------------
+struct PWGrid {
+  int N, M, Nz, Mz, p, pz, dim;
+  int ncol, nhalf;
+  const double2* E;      // [N][p]  exp(-i theta m s_i)
+  const double2* Ez;     // [Nz][pz] (identity in 2D)
+  const int* col_my;     // [ncol]
+  const int* col_m0;
+  const int* col_lz;     // in-band |mz| <= lz
+  const int* slab_off;   // [Nz + 1]
+  const int* slab_ncol;  // [Nz]
+  const int* m0_start;   // [M + 2] CSR of columns grouped by m0
+  const int* m0_cols;    // column ids
+  const int* mode_code;  // [nhalf]: (mz + Mz) << 16 | column
+};
+// G[slot][ch][mode] from outgoing[box(slot)][ch]; B is scratch
+// [nbox][nch][pz][ncol] double2.
+void launch_forward(const PWGrid& g, const int* boxes, int nbox, int nch, const double* outgoing,
+                    double2* B, double2* G, cudaStream_t st);
+// F[t][j][mode] = symbol(sum_e phase(m, tau_e) G[slot_e]) for target boxes t
+void launch_accumulate_symbol(const PWGrid& g, int kernel, int ntb, const int* ent_start,
+                              const int* ent_slot, const int* ent_tau, const double2* G, int nch,
+                              const double* A, double h, double2* F, cudaStream_t st);
+// incoming[box(t)][j] += pf * Re(inverse(F[t][j])); C is scratch
+void launch_inverse(const PWGrid& g, const int* tboxes, int ntb, int d, const double2* F,
+                    double2* C, double pf, double* incoming, cudaStream_t st);
+
+// ---- residual.cu (K12) -------------------------------------------------------
+struct ResidTables {
+  int nd, no;          // coefficient counts of the diag / offd tables
+  double lo, hi;       // table domain (shared by both tables)
+  double support;
+  int kernel, dim;
+};
+void set_residual_tables(const double* diag, int nd, const double* offd, int no, cudaStream_t st);
+// u_res[perm[t]*d+j] for all targets of leaves `leaves`; flags[0] <- coincident
+// points; stats[0..1] <- candidates / in-support pairs (if stats != nullptr)
+void launch_residual(const ResidTables& rt, const dev::DBox* boxes, const int* leaves, int nleaf,
+                     const int* rng_start, const int* rng_box, const int* rng_info,
+                     const double* spts, int ns, const double* sstr, const double* tpts, int nt,
+                     const int* tperm, int alias, double self_coef_scale, double self_const,
+                     double* ures, int* flags, unsigned long long* stats, cudaStream_t st);
+
+// ---- finalize.cu --------------------------------------------------------------
+// sums[j] = sum_a col_j(a) for j < ncomp (deterministic block tree)
+void launch_column_sums(const double* soa, int n, int ncomp, double* sums, double* scratch,
+                        cudaStream_t st);
+// periodic stresslet zero mode moments: out[0] = W = sum f.n, out[1..d] = sum x_a (f.n)
+void launch_zero_mode_moments(const double* spts, const double* sstr, int n, int dim,
+                              double* out, double* scratch, cudaStream_t st);
+// u = ((ufar + ures) + corr_scale * sums[j]) (+ (mom[j] - W x_t[j])) in caller order
+void launch_combine(int nt, int dim, const double* ufar, const double* ures, const double* sums,
+                    double corr_scale, const double* zm, const double* tpts_caller, double* u,
+                    cudaStream_t st);
+
+}  // namespace sdmkb
