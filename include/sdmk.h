@@ -142,6 +142,12 @@ int sdmk_incoming(sdmk_context* ctx, int stage, double* incoming);
 int sdmk_target_far_fields(sdmk_context* ctx, double* u);
 int sdmk_residual_pass(sdmk_context* ctx, double* u);
 
+/* ---- instrumentation ----
+   the context's CUDA stream (cudaStream_t) so callers can time on it */
+int sdmk_get_stream(sdmk_context* ctx, void** stream);
+/* measured FP64 FMA throughput of the device (TFLOP/s, best of 5) */
+int sdmk_fp64_peak(sdmk_context* ctx, double* tflops);
+
 /* ---- host-only helpers (no GPU needed; used by the CPU test suite) ----
    Plan-level setup exactly as the GPU path uses it. */
 int sdmk_host_save_tables(const sdmk_plan* plan, const char* path);

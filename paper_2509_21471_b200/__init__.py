@@ -100,6 +100,8 @@ def lib():
             "sdmk_incoming": ([C.c_void_p, C.c_int, dp], C.c_int),
             "sdmk_target_far_fields": ([C.c_void_p, dp], C.c_int),
             "sdmk_residual_pass": ([C.c_void_p, dp], C.c_int),
+            "sdmk_get_stream": ([C.c_void_p, P(C.c_void_p)], C.c_int),
+            "sdmk_fp64_peak": ([C.c_void_p, P(C.c_double)], C.c_int),
             "sdmk_host_save_tables": ([P(sdmk_plan), C.c_char_p], C.c_int),
             "sdmk_host_symbol_table": ([P(sdmk_plan), C.c_double, C.c_int, C.c_int, C.c_double, C.c_double, dp],
                                        C.c_int),
@@ -321,6 +323,17 @@ class Context:
         out = np.empty(self.tree_info()["n_tgt"] * self._dim)
         _raise(lib().sdmk_residual_pass(self._h, _dptr(out)))
         return out
+
+    def stream_handle(self) -> int:
+        """cudaStream_t of this context (for CUDA-event timing by the caller)."""
+        s = C.c_void_p()
+        _raise(lib().sdmk_get_stream(self._h, C.byref(s)))
+        return int(s.value or 0)
+
+    def fp64_peak_tflops(self) -> float:
+        v = C.c_double()
+        _raise(lib().sdmk_fp64_peak(self._h, C.byref(v)))
+        return float(v.value)
 
     def save_tables(self, plan: DmkPlan, path: str):
         cp = plan.to_c()

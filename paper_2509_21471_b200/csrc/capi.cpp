@@ -251,6 +251,18 @@ int sdmk_residual_pass(sdmk_context* c, double* out) {
   return guarded([&] { need_ctx(c)->residual(out); });
 }
 
+int sdmk_get_stream(sdmk_context* c, void** stream) {
+  return guarded([&] { *stream = (void*)need_ctx(c)->stream(); });
+}
+
+int sdmk_fp64_peak(sdmk_context* c, double* tflops) {
+  return guarded([&] {
+    Context* x = need_ctx(c);
+    *tflops = measure_fp64_peak_tflops(x->stream());
+    cuda_check(cudaGetLastError(), "fp64 peak kernel");
+  });
+}
+
 int sdmk_host_save_tables(const sdmk_plan* plan, const char* path) {
   return guarded([&] { save_tables(tables_for_plan(to_plan(plan)), path ? path : ""); });
 }

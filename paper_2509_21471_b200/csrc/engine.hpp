@@ -103,6 +103,7 @@ class Context {
   void setup(const Plan& plan, int dim, int64_t ns, const double* src, int64_t nt, const double* tgt,
              const double* str, int mode);
   const Problem& problem() const { return prob_; }
+  cudaStream_t stream() const { return st_; }
   void upward(double* host_out);
   void incoming(int stage, double* host_out);
   void target_far(double* host_out);

@@ -125,4 +125,7 @@ void launch_combine(int nt, int dim, const double* ufar, const double* ures, con
                     double corr_scale, const double* zm, const double* tpts_caller, double* u,
                     cudaStream_t st);
 
+// ---- peak.cu ----------------------------------------------------------------
+double measure_fp64_peak_tflops(cudaStream_t st);
+
 }  // namespace sdmkb

@@ -1,0 +1,236 @@
+"""GPU parity of the sm_100a path against the reference (C-ABI calls).
+
+Checker: the golden vectors (tests/golden, made by the compiled reference),
+the compiled reference itself (oracle/_ref, which travels with the repo) at
+sizes it finishes in seconds, and size-independent properties at the
+BASELINE sizes.  Bar: trees/permutations bit-exact; every output component
+within 1e-10 * max(|u_ref|, 1e-3 ||u_ref||_inf).
+"""
+import numpy as np
+import pytest
+
+from conftest import golden_case, golden_index, parity_ok
+
+import paper_2509_21471_b200 as g
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-10
+
+
+def _sys(meta, d):
+    return g.ParticleSystem(meta["dim"], d["sources"], d["targets"] if meta["ntgt"] else np.zeros(0), d["strengths"])
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in golden_index()])
+def test_golden_evaluate(gpu_ctx, name):
+    meta, d, _ = golden_case(name)
+    u = gpu_ctx.evaluate_with_plan(g.DmkPlan(**meta["plan"]), _sys(meta, d), int(meta["periodic"]))
+    ok, err = parity_ok(u, d["u"], RTOL)
+    assert ok, err
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in golden_index()])
+def test_golden_tree_and_passes(gpu_ctx, name):
+    meta, d, dump = golden_case(name)
+    gpu_ctx.setup(g.DmkPlan(**meta["plan"]), _sys(meta, d), int(meta["periodic"]))
+    assert gpu_ctx.tree_dump() == dump
+    sp, tp = gpu_ctx.tree_perm()
+    assert np.array_equal(sp, d["sperm"])
+    if meta["ntgt"]:
+        assert np.array_equal(tp, d["tperm"])
+    ok, err = parity_ok(gpu_ctx.residual_pass(), d["residual"], RTOL)
+    assert ok, ("residual", err)
+    ok, err = parity_ok(gpu_ctx.target_far_fields(), d["far"], RTOL)
+    assert ok, ("far", err)
+
+
+def _ref():
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not present")
+    return ref
+
+
+def _make(kernel, dim, n, seed, dist="uniform", ntgt=0):
+    rng = np.random.default_rng(seed)
+    if dist == "uniform":
+        x = rng.uniform(-0.5, 0.5, (n, dim))
+    elif dist == "spheres":  # 64-sphere surfaces (cfg3 shape, scaled down)
+        c = rng.uniform(-0.4, 0.4, (64, dim))
+        r = rng.uniform(0.01, 0.05, 64)
+        k = rng.integers(0, 64, n)
+        v = rng.standard_normal((n, dim))
+        v /= np.linalg.norm(v, axis=1, keepdims=True)
+        x = c[k] + r[k, None] * v
+    else:  # gaussian mixture (cfg4/cfg5 shape)
+        c = rng.uniform(-0.45, 0.45, (16, dim))
+        sg = rng.uniform(1e-3, 1e-2, 16)
+        k = rng.integers(0, 16, n)
+        x = np.clip(c[k] + sg[k, None] * rng.standard_normal((n, dim)), -0.5, 0.5)
+    sc = g.strength_components(kernel, dim)
+    s = rng.standard_normal((n, sc))
+    if kernel == 1:
+        nn = rng.standard_normal((n, dim))
+        s[:, dim:] = nn / np.linalg.norm(nn, axis=1, keepdims=True)
+    t = rng.uniform(-0.5, 0.5, (ntgt, dim)) if ntgt else None
+    return x, s, t
+
+
+CASES = [
+    # kernel, dim, n, eps, periodic, dist, ntgt
+    (0, 3, 20000, 1e-6, False, "uniform", 0),
+    (0, 3, 30000, 1e-6, False, "mixture", 0),
+    (1, 3, 20000, 1e-6, False, "spheres", 0),
+    (2, 3, 10000, 1e-9, False, "uniform", 0),
+    (0, 2, 40000, 1e-9, False, "mixture", 0),
+    (1, 2, 20000, 1e-6, False, "mixture", 0),
+    (0, 3, 20000, 1e-8, True, "uniform", 0),
+    (1, 3, 10000, 1e-6, True, "uniform", 0),
+    (2, 3, 10000, 1e-6, True, "uniform", 0),
+    (0, 3, 15000, 1e-6, False, "mixture", 9000),
+    (0, 3, 8000, 1e-3, False, "uniform", 0),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_against_live_reference(gpu_ctx, case):
+    ref = _ref()
+    kernel, dim, n, eps, per, dist, ntgt = case
+    x, s, t = _make(kernel, dim, n, 11 + n, dist, ntgt)
+    plan = ref.select_parameters(kernel, eps, 0, dim)
+    P = ref.RefProblem(plan, dim, x, s, t, per)
+    sys_ = g.ParticleSystem(dim, x, t if t is not None else np.zeros(0), s)
+    gpu_ctx.setup(g.DmkPlan(**plan), sys_, int(per))
+    assert gpu_ctx.tree_dump() == P.tree_dump()
+    ok, err = parity_ok(gpu_ctx.upward_pass(), P.upward(), 1e-12)
+    assert ok, ("upward", err)
+    ok, err = parity_ok(gpu_ctx.incoming(1), P.incoming(1), 1e-11)
+    assert ok, ("incoming", err)
+    ur, _ = P.evaluate()
+    u = gpu_ctx.evaluate_with_plan(g.DmkPlan(**plan), sys_, int(per))
+    ok, err = parity_ok(u, ur, RTOL)
+    assert ok, ("evaluate", err)
+
+
+def test_accuracy_against_direct_sum(gpu_ctx):
+    """acceptance.cpp:451-474 style: DMK within eps of the exact sum, all kernels."""
+    ref = _ref()
+    for kernel in (0, 1, 2):
+        for eps in (1e-3, 1e-6, 1e-9):
+            x, s, _ = _make(kernel, 3, 5000, 5, "uniform")
+            plan = ref.select_parameters(kernel, eps, 0, 3)
+            P = ref.RefProblem(plan, 3, x, s)
+            ex = P.direct_sum()
+            u = gpu_ctx.evaluate(kernel, g.ParticleSystem(3, x, np.zeros(0), s), eps)
+            assert np.linalg.norm(u - ex) / np.linalg.norm(ex) <= eps
+
+
+# ------------------------------------------------------------------ edges --
+def test_single_point_and_distant_singletons(gpu_ctx):
+    plan = g.select_parameters(0, 1e-6, 0, 3)
+    u = gpu_ctx.evaluate_with_plan(plan, g.ParticleSystem(3, np.array([[0.1, -0.2, 0.3]]), np.zeros(0),
+                                                         np.array([[1.0, 2.0, 3.0]])))
+    assert u.shape == (3,) and np.all(np.isfinite(u))
+    # distant singleton leaves: residual is exactly the self term (test_dmk.cpp:374-390)
+    plan.n_s = 1
+    sys_ = g.ParticleSystem(3, np.array([[-0.45] * 3, [0.45] * 3]), np.zeros(0),
+                            np.array([[1.0, 2.0, 3.0], [-1.0, 0.5, 0.25]]))
+    gpu_ctx.setup(plan, sys_)
+    res = gpu_ctx.residual_pass().reshape(2, 3)
+    assert np.all(res != 0.0)
+    assert np.allclose(res[0] / np.array([1.0, 2.0, 3.0]), res[0, 0], rtol=1e-15, atol=0)
+    assert np.allclose(res[1] / np.array([-1.0, 0.5, 0.25]), res[0, 0], rtol=1e-15, atol=0)
+
+
+def test_zero_strengths_give_exact_zero(gpu_ctx):
+    x, s, _ = _make(1, 3, 5000, 3)
+    u = gpu_ctx.evaluate(1, g.ParticleSystem(3, x, np.zeros(0), np.zeros_like(s)), 1e-6)
+    assert np.all(u == 0.0)
+
+
+def test_errors_map_to_reference_exceptions(gpu_ctx):
+    plan = g.select_parameters(0, 1e-6, 0, 3)
+    with pytest.raises(ValueError):  # out of the unit box in free space
+        gpu_ctx.evaluate_with_plan(plan, g.ParticleSystem(3, np.array([[0.6, 0, 0], [0, 0, 0]]), np.zeros(0),
+                                                         np.ones((2, 3))))
+    with pytest.raises(ValueError):  # non-finite strength
+        gpu_ctx.evaluate_with_plan(plan, g.ParticleSystem(3, np.array([[0.1, 0, 0], [0, 0, 0]]), np.zeros(0),
+                                                         np.array([[np.nan, 0, 0], [1, 1, 1]])))
+    with pytest.raises(ValueError):  # periodic 2D stresslet (dmk.cpp:1049-1051)
+        gpu_ctx.evaluate(1, g.ParticleSystem(2, np.zeros((2, 2)) + [[0.1, 0.1], [0.2, 0.2]], np.zeros(0),
+                                             np.ones((2, 4))), 1e-6, 0, 1)
+    with pytest.raises(g.DomainError):  # coincident distinct points
+        gpu_ctx.evaluate_with_plan(plan, g.ParticleSystem(3, np.array([[0.1, 0.2, 0.3]] * 2 + [[0, 0, 0]]),
+                                                         np.zeros(0), np.ones((3, 3))))
+    # periodic inputs outside the box are legal and wrap
+    u = gpu_ctx.evaluate(0, g.ParticleSystem(3, np.array([[1.1, 0, 0], [0.2, -0.7, 0.3]]), np.zeros(0),
+                                             np.ones((2, 3))), 1e-6, 0, 1)
+    assert np.all(np.isfinite(u))
+
+
+def test_determinism_linearity_permutation(gpu_ctx):
+    x, s, _ = _make(0, 3, 200000, 21, "mixture")
+    plan = g.select_parameters(0, 1e-6, 0, 3)
+    u1 = gpu_ctx.evaluate_with_plan(plan, g.ParticleSystem(3, x, np.zeros(0), s))
+    u2 = gpu_ctx.evaluate_with_plan(plan, g.ParticleSystem(3, x, np.zeros(0), s))
+    assert np.array_equal(u1, u2)  # bitwise run-to-run (test_dmk.cpp:637-642)
+    s2 = np.random.default_rng(2).standard_normal(s.shape)
+    ua = gpu_ctx.evaluate_with_plan(plan, g.ParticleSystem(3, x, np.zeros(0), 2.0 * s - 3.0 * s2))
+    ub = gpu_ctx.evaluate_with_plan(plan, g.ParticleSystem(3, x, np.zeros(0), s2))
+    lin = 2.0 * u1 - 3.0 * ub
+    assert np.max(np.abs(ua - lin)) <= 1e-11 * np.max(np.abs(lin))
+    perm = np.random.default_rng(3).permutation(len(x))
+    up = gpu_ctx.evaluate_with_plan(plan, g.ParticleSystem(3, x[perm], np.zeros(0), s[perm]))
+    assert np.max(np.abs(up.reshape(-1, 3) - u1.reshape(-1, 3)[perm])) <= 1e-13 * np.max(np.abs(u1))
+
+
+def test_periodic_lattice_shift(gpu_ctx):
+    """Shifting every point by a lattice vector changes nothing (test_dmk.cpp:512-548)."""
+    x, s, _ = _make(0, 3, 20000, 4)
+    s -= s.mean(0)
+    plan = g.select_parameters(0, 1e-8, 0, 3)
+    u0 = gpu_ctx.evaluate_with_plan(plan, g.ParticleSystem(3, x, np.zeros(0), s), 1)
+    u1 = gpu_ctx.evaluate_with_plan(plan, g.ParticleSystem(3, x + np.array([1.0, -2.0, 3.0]), np.zeros(0), s), 1)
+    assert np.max(np.abs(u1 - u0)) <= 1e-10 * np.max(np.abs(u0))
+
+
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_metric_size_properties(gpu_ctx, kernel):
+    """BASELINE metric size (N=1e7 uniform, eps=1e-6): bitwise determinism, linearity
+    and the device-pointer entry point agreeing with the host-pointer one."""
+    import torch
+    n = 10_000_000
+    x, s, _ = _make(kernel, 3, n, 0)
+    plan = g.select_parameters(kernel, 1e-6, 0, 3)
+    sys_ = g.ParticleSystem(3, x, np.zeros(0), s)
+    u1 = gpu_ctx.evaluate_with_plan(plan, sys_)
+    dx, ds = torch.from_numpy(x).cuda(), torch.from_numpy(2.0 * s).cuda()
+    du = torch.empty(3 * n, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    gpu_ctx.evaluate_device(plan, 3, n, dx.data_ptr(), 0, 0, ds.data_ptr(), 0, du.data_ptr())
+    u2 = du.cpu().numpy()
+    assert np.all(np.isfinite(u1))
+    assert np.max(np.abs(u2 - 2.0 * u1)) <= 1e-12 * np.max(np.abs(u1))
+    # accuracy spot check at full size: exact sum (fp64, on the GPU via torch) for 64 targets
+    idx = np.random.default_rng(1).choice(n, 64, replace=False)
+    xt = torch.from_numpy(x[idx]).cuda()
+    sv = torch.from_numpy(s).cuda()
+    ex = torch.zeros((64, 3), dtype=torch.float64, device="cuda")
+    for a0 in range(0, n, 1_000_000):
+        xs = dx[a0:a0 + 1_000_000]
+        r = xt[:, None, :] - xs[None, :, :]
+        r2 = (r * r).sum(-1)
+        r2 = torch.where(r2 == 0, torch.full_like(r2, float("inf")), r2)
+        rn = torch.sqrt(r2)
+        if kernel == 0:
+            f = sv[a0:a0 + 1_000_000]
+            xf = (r * f[None]).sum(-1)
+            ex += (f[None] / (8 * np.pi * rn)[..., None] + (xf / (8 * np.pi * r2 * rn))[..., None] * r).sum(1)
+        else:
+            f, nn = sv[a0:a0 + 1_000_000, :3], sv[a0:a0 + 1_000_000, 3:]
+            xf, xn = (r * f[None]).sum(-1), (r * nn[None]).sum(-1)
+            ex += ((-3.0 / (4 * np.pi)) * xf * xn / (r2 * r2 * rn))[..., None].mul(r).sum(1)
+    ex = ex.cpu().numpy()
+    got = u1.reshape(-1, 3)[idx]
+    assert np.linalg.norm(got - ex) / np.linalg.norm(ex) <= 5e-6
