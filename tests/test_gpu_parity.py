@@ -122,8 +122,14 @@ def test_accuracy_against_direct_sum(gpu_ctx):
             plan = ref.select_parameters(kernel, eps, 0, 3)
             P = ref.RefProblem(plan, 3, x, s)
             ex = P.direct_sum()
+            ur, _ = P.evaluate()
             u = gpu_ctx.evaluate(kernel, g.ParticleSystem(3, x, np.zeros(0), s), eps)
-            assert np.linalg.norm(u - ex) / np.linalg.norm(ex) <= eps
+            err = np.linalg.norm(u - ex) / np.linalg.norm(ex)
+            err_ref = np.linalg.norm(ur - ex) / np.linalg.norm(ex)
+            # same accuracy as the reference DMK (which itself lands at up to ~1.5x eps for the
+            # stresslet at 1e-3, a documented parameter-table limit, proj/README.md:123-139)
+            assert abs(err - err_ref) <= 1e-9 * err_ref + 1e-15
+            assert err <= 2.0 * eps
 
 
 # ------------------------------------------------------------------ edges --
@@ -205,7 +211,9 @@ def test_metric_size_properties(gpu_ctx, kernel):
     plan = g.select_parameters(kernel, 1e-6, 0, 3)
     sys_ = g.ParticleSystem(3, x, np.zeros(0), s)
     u1 = gpu_ctx.evaluate_with_plan(plan, sys_)
-    dx, ds = torch.from_numpy(x).cuda(), torch.from_numpy(2.0 * s).cuda()
+    s2 = s.copy()
+    s2[:, :3] *= 2.0  # the field is linear in the force (the stresslet is bilinear in f, n)
+    dx, ds = torch.from_numpy(x).cuda(), torch.from_numpy(s2).cuda()
     du = torch.empty(3 * n, dtype=torch.float64, device="cuda")
     torch.cuda.synchronize()
     gpu_ctx.evaluate_device(plan, 3, n, dx.data_ptr(), 0, 0, ds.data_ptr(), 0, du.data_ptr())
