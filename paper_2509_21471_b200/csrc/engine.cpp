@@ -568,8 +568,15 @@ void Context::run_upward() {  // dmk.cpp:555-655
   double* og = arena_.as<double>("outgoing", (size_t)nb * pr.nch * nodes);
   cuda_check(cudaMemsetAsync(og, 0, sizeof(double) * nb * pr.nch * nodes, st_), "memset outgoing");
   ChebDev cb{p, pz, d, cheb_nodes_, cheb_wts_};
-  launch_anterp(pr.plan.kernel, cb, pr.boxes, pr.ant_leaves, pr.n_ant, pr.spts, pr.ns, pr.sstr, og, pr.nch, st_);
-  ++launches_;
+  if (mma_anterp_supported(p)) {
+    double* basis = arena_.as<double>("basis_s", (size_t)3 * pr.ns * p);
+    launch_basis(cb, pr.boxes, pr.ant_leaves, pr.n_ant, pr.spts, pr.ns, 0, basis, st_);
+    launch_anterp_mma(pr.plan.kernel, cb, pr.boxes, pr.ant_leaves, pr.n_ant, basis, pr.sstr, pr.ns, og, pr.nch, st_);
+    launches_ += 2;
+  } else {
+    launch_anterp(pr.plan.kernel, cb, pr.boxes, pr.ant_leaves, pr.n_ant, pr.spts, pr.ns, pr.sstr, og, pr.nch, st_);
+    ++launches_;
+  }
   for (int lev = pr.tree.max_level - 1; lev >= 0; --lev) {
     const Problem::LevelLists& X = pr.levels[lev];
     if (X.n_merge == 0) continue;
@@ -679,8 +686,22 @@ void Context::run_target_far(double* ufar) {  // dmk.cpp:861-915
   Problem& pr = prob_;
   const int p = pr.plan.p, pz = pr.dim == 3 ? p : 1;
   ChebDev cb{p, pz, pr.dim, cheb_nodes_, cheb_wts_};
-  launch_interp_targets(cb, pr.boxes, pr.int_leaves, pr.n_int, pr.tpts, pr.nt, pr.tperm,
-                        arena_.as<double>("incoming", 1), ufar, st_);
+  const double* incoming = arena_.as<double>("incoming", 1);
+  if (mma_anterp_supported(p)) {
+    // alias targets reuse the source bases computed by the upward pass
+    const double* tb = nullptr;
+    if (pr.alias) {
+      tb = arena_.as<double>("basis_s", (size_t)3 * pr.ns * p);
+    } else {
+      double* b = arena_.as<double>("basis_t", (size_t)3 * pr.nt * p);
+      launch_basis(cb, pr.boxes, pr.int_leaves, pr.n_int, pr.tpts, pr.nt, 1, b, st_);
+      ++launches_;
+      tb = b;
+    }
+    launch_interp_mma(cb, pr.boxes, pr.int_leaves, pr.n_int, tb, pr.nt, pr.tperm, incoming, ufar, st_);
+  } else {
+    launch_interp_targets(cb, pr.boxes, pr.int_leaves, pr.n_int, pr.tpts, pr.nt, pr.tperm, incoming, ufar, st_);
+  }
   ++launches_;
 }
 

@@ -1,0 +1,334 @@
+// K3 (leaf anterpolation, dmk.cpp:587-622) and K11 (target interpolation,
+// dmk.cpp:877-913) on the FP64 tensor cores (mma.sync m8n8k4 f64, "DMMA").
+//
+// k_basis   : barycentric Lagrange bases of every point of every leaf, three
+//             axes, written once to HBM ([axis][point][p]); K3 and K11 (alias
+//             targets) share them.
+// K3        : per leaf, C[(ch,iz,iy), ix] = sum_a A[(ch,iz,iy), a] * bx[a, ix]
+//             with A = (s_ch(a) bz(a,iz)) by(a,iy) formed while building the A
+//             fragment.  Warps own up to 8 m-tiles x all n-tiles; the points
+//             stream through shared memory 32 at a time.
+// K11       : per leaf, C[a, (j,iz,iy)] = sum_ix bx[a, ix] W[(j,iz,iy), ix]
+//             (W = the leaf's incoming proxy grid streamed through shared
+//             memory in 256-row chunks), reduced on the fly with the weights
+//             bz(a,iz) by(a,iy) into u[a][j]; one 8-target m-tile per warp.
+// Shared-memory row strides are chosen = 8 (mod 16) doubles (resp. KP + 4)
+// so every fragment load is bank-conflict free.
+#include "common.cuh"
+#include "launch.hpp"
+
+namespace sdmkb {
+
+namespace {
+
+using dev::DBox;
+
+__host__ __device__ __forceinline__ int stride816(int x) {  // smallest y >= x with y % 16 == 8
+  int y = (x + 7) / 8 * 8;
+  return (y % 16 == 8) ? y : y + 8;
+}
+
+// ---------------------------------------------------------------- bases --
+__global__ void __launch_bounds__(256) k_basis(ChebDev cb, const DBox* __restrict__ boxes,
+                                               const int* __restrict__ leaves, const double* __restrict__ pts, int n,
+                                               int use_targets, double* __restrict__ basis) {
+  __shared__ double nodes[64], wts[64];
+  const int p = cb.p, dim = cb.dim;
+  for (int i = threadIdx.x; i < p; i += blockDim.x) {
+    nodes[i] = cb.nodes[i];
+    wts[i] = cb.wts[i];
+  }
+  __syncthreads();
+  const DBox box = boxes[leaves[blockIdx.x]];
+  const int b0 = use_targets ? box.tb : box.sb, b1 = use_targets ? box.te : box.se;
+  const double hinv = 1.0 / box.half;
+  const int cnt = b1 - b0;
+  for (int task = threadIdx.x; task < cnt * dim; task += blockDim.x) {
+    const int ax = task / cnt, i = b0 + task % cnt;
+    const double x = __dmul_rn(__dsub_rn(pts[(size_t)ax * n + i], box.c[ax]), hinv);
+    dev::cheb_basis(p, nodes, wts, x, basis + ((size_t)ax * n + i) * p, 1);
+  }
+}
+
+// build_source_channels (dmk.cpp:492-525) from SoA strengths
+__device__ __forceinline__ void channels(int kernel, int dim, const double* __restrict__ str, int n, int a, double* ch) {
+  if (kernel == 1) {
+    double f[3] = {0, 0, 0}, nn[3] = {0, 0, 0}, w = 0.0;
+    for (int j = 0; j < dim; ++j) {
+      f[j] = str[(size_t)j * n + a];
+      nn[j] = str[(size_t)(dim + j) * n + a];
+      w += f[j] * nn[j];
+    }
+    if (dim == 3) {
+      ch[0] = 2.0 * f[0] * nn[0] + w;
+      ch[1] = 2.0 * f[1] * nn[1] + w;
+      ch[2] = 2.0 * f[2] * nn[2] + w;
+      ch[3] = f[0] * nn[1] + f[1] * nn[0];
+      ch[4] = f[0] * nn[2] + f[2] * nn[0];
+      ch[5] = f[1] * nn[2] + f[2] * nn[1];
+    } else {
+      ch[0] = 2.0 * f[0] * nn[0] + w;
+      ch[1] = 2.0 * f[1] * nn[1] + w;
+      ch[2] = f[0] * nn[1] + f[1] * nn[0];
+    }
+    return;
+  }
+  const int nc = kernel == 0 ? dim : (dim == 3 ? 3 : 1);
+  for (int j = 0; j < nc; ++j) ch[j] = str[(size_t)j * n + a];
+}
+
+// -------------------------------------------------------------------- K3 --
+constexpr int kKC = 32;     // points per shared chunk
+constexpr int kAWarps = 8;
+
+template <int NT, int kMTW>
+__global__ void __launch_bounds__(kAWarps * 32, 2) k_anterp_mma(int kernel, ChebDev cb, const DBox* __restrict__ boxes,
+                                                               const int* __restrict__ leaves,
+                                                               const double* __restrict__ basis,
+                                                               const double* __restrict__ str, int n,
+                                                               double* __restrict__ out, int nch, int mt_per_cta) {
+  extern __shared__ double sm[];
+  const int p = cb.p, pz = cb.pz, dim = cb.dim;
+  const int RS = stride816(nch * pz), BS = stride816(p), XS = stride816(NT * 8);
+  double* sbz = sm;                 // [kKC][RS]  s_ch * bz(iz)
+  double* bys = sbz + kKC * RS;     // [kKC][BS]
+  double* bxs = bys + kKC * BS;     // [kKC][XS]  zero-padded to NT*8 columns
+  double* svs = bxs + kKC * XS;     // [kKC][6]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int b = leaves[blockIdx.x];
+  const DBox box = boxes[b];
+  const int M = nch * pz * p, total_mt = (M + 7) / 8;
+  const int mt0 = blockIdx.y * mt_per_cta, mt1 = min(total_mt, mt0 + mt_per_cta);
+  int chiz[kMTW], iyv[kMTW];
+  bool val[kMTW];
+#pragma unroll
+  for (int i = 0; i < kMTW; ++i) {
+    const int mt = mt0 + warp + kAWarps * i;
+    const int m = mt * 8 + g;
+    val[i] = mt < mt1;
+    const bool ok = val[i] && m < M;
+    chiz[i] = ok ? m / p : 0;
+    iyv[i] = ok ? m % p : 0;
+  }
+  double acc[kMTW][NT][2];
+#pragma unroll
+  for (int i = 0; i < kMTW; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const double* bxg = basis;
+  const double* byg = basis + (size_t)n * p;
+  const double* bzg = basis + (size_t)2 * n * p;
+  for (int a0 = box.sb; a0 < box.se; a0 += kKC) {
+    const int kc = min(kKC, box.se - a0);
+    __syncthreads();
+    for (int pt = tid; pt < kKC; pt += blockDim.x) {
+      if (pt < kc) channels(kernel, dim, str, n, a0 + pt, svs + pt * 6);
+      else for (int j = 0; j < 6; ++j) svs[pt * 6 + j] = 0.0;
+    }
+    for (int e = tid; e < kKC * XS; e += blockDim.x) {
+      const int pt = e / XS, i = e % XS;
+      bxs[e] = (pt < kc && i < p) ? bxg[(size_t)(a0 + pt) * p + i] : 0.0;
+    }
+    for (int e = tid; e < kKC * p; e += blockDim.x) {
+      const int pt = e / p, i = e % p;
+      bys[pt * BS + i] = pt < kc ? byg[(size_t)(a0 + pt) * p + i] : 0.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < kKC * nch * pz; e += blockDim.x) {
+      const int pt = e / (nch * pz), r = e % (nch * pz), ch = r / pz, iz = r % pz;
+      const double bz = dim == 3 ? (pt < kc ? bzg[(size_t)(a0 + pt) * p + iz] : 0.0) : 1.0;
+      sbz[pt * RS + r] = svs[pt * 6 + ch] * bz;
+    }
+    __syncthreads();
+    const int ksteps = (kc + 3) / 4;
+    for (int ks = 0; ks < ksteps; ++ks) {
+      const int k = ks * 4 + t;
+      double bv[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) bv[j] = bxs[k * XS + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < kMTW; ++i) {
+        if (val[i]) {
+          const double av = sbz[k * RS + chiz[i]] * bys[k * BS + iyv[i]];
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dev::dmma(acc[i][j][0], acc[i][j][1], av, bv[j]);
+        }
+      }
+    }
+  }
+  double* ob = out + (size_t)b * M * p;
+#pragma unroll
+  for (int i = 0; i < kMTW; ++i) {
+    if (!val[i]) continue;
+    const int m = (mt0 + warp + kAWarps * i) * 8 + g;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int c = j * 8 + 2 * t;
+      if (c < p) ob[(size_t)m * p + c] = acc[i][j][0];
+      if (c + 1 < p) ob[(size_t)m * p + c + 1] = acc[i][j][1];
+    }
+  }
+}
+
+// ------------------------------------------------------------------- K11 --
+constexpr int kTB = 64;      // targets per block (one m-tile per warp)
+constexpr int kNC = 256;     // W rows per shared chunk
+
+template <int KS>
+__global__ void __launch_bounds__(256, 2) k_interp_mma(ChebDev cb, const DBox* __restrict__ boxes,
+                                                      const int* __restrict__ leaves,
+                                                      const double* __restrict__ tbasis, int nt,
+                                                      const int* __restrict__ tperm,
+                                                      const double* __restrict__ incoming,
+                                                      double* __restrict__ ufar) {
+  extern __shared__ double sm[];
+  constexpr int KP = KS * 4, WS = KP + 4;
+  const int p = cb.p, pz = cb.pz, dim = cb.dim;
+  const int N = dim * pz * p, BS = p + 1;
+  double* Ws = sm;                    // [kNC][WS]
+  double* bxs = Ws + kNC * WS;        // [kTB][WS]
+  double* bys = bxs + kTB * WS;       // [kTB][BS]
+  double* bzs = bys + kTB * BS;       // [kTB][BS]
+  int* ntab = reinterpret_cast<int*>(bzs + kTB * BS);  // [N]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int b = leaves[blockIdx.x];
+  const DBox box = boxes[b];
+  for (int e = tid; e < N; e += blockDim.x) {
+    const int j = e / (pz * p), r = e % (pz * p);
+    ntab[e] = (j << 16) | ((r / p) << 8) | (r % p);
+  }
+  const double* W = incoming + (size_t)b * N * p;
+  const double* bxg = tbasis;
+  const double* byg = tbasis + (size_t)nt * p;
+  const double* bzg = tbasis + (size_t)2 * nt * p;
+  for (int t0 = box.tb; t0 < box.te; t0 += kTB) {
+    const int tc = min(kTB, box.te - t0);
+    __syncthreads();
+    for (int e = tid; e < kTB * KP; e += blockDim.x) {
+      const int a = e / KP, k = e % KP;
+      bxs[a * WS + k] = (a < tc && k < p) ? bxg[(size_t)(t0 + a) * p + k] : 0.0;
+    }
+    for (int e = tid; e < kTB * p; e += blockDim.x) {
+      const int a = e / p, k = e % p;
+      bys[a * BS + k] = a < tc ? byg[(size_t)(t0 + a) * p + k] : 0.0;
+      bzs[a * BS + k] = a < tc ? (dim == 3 ? bzg[(size_t)(t0 + a) * p + k] : (k == 0 ? 1.0 : 0.0)) : 0.0;
+    }
+    __syncthreads();
+    const int arow = warp * 8 + g;  // this lane's target (A row / C row)
+    double av[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) av[ks] = bxs[arow * WS + ks * 4 + t];
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    for (int n0 = 0; n0 < N; n0 += kNC) {
+      const int nc = min(kNC, N - n0);
+      __syncthreads();
+      for (int e = tid; e < kNC * KP; e += blockDim.x) {
+        const int r = e / KP, k = e % KP;
+        Ws[r * WS + k] = (r < nc && k < p) ? W[(size_t)(n0 + r) * p + k] : 0.0;
+      }
+      __syncthreads();
+      if (warp * 8 < tc) {
+        const int ntiles = (nc + 7) / 8;
+        for (int nt_ = 0; nt_ < ntiles; ++nt_) {
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) dev::dmma(c0, c1, av[ks], Ws[(nt_ * 8 + g) * WS + ks * 4 + t]);
+          const int na = n0 + nt_ * 8 + 2 * t;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int nn = na + e;
+            if (nn < N) {
+              const int code = ntab[nn];
+              const int j = code >> 16, iz = (code >> 8) & 255, iy = code & 255;
+              const double w = bzs[arow * BS + iz] * bys[arow * BS + iy] * (e ? c1 : c0);
+              if (j == 0) v0 += w;
+              else if (j == 1) v1 += w;
+              else v2 += w;
+            }
+          }
+        }
+      }
+    }
+    // combine the 4 lanes of each row (fixed order -> deterministic)
+    v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+    v2 += __shfl_xor_sync(0xffffffffu, v2, 1);
+    v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
+    v2 += __shfl_xor_sync(0xffffffffu, v2, 2);
+    if (t == 0 && arow < tc) {
+      double* ut = ufar + (size_t)tperm[t0 + arow] * dim;
+      ut[0] = v0;
+      ut[1] = v1;
+      if (dim == 3) ut[2] = v2;
+    }
+  }
+}
+
+void smem_attr(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+}  // namespace
+
+bool mma_anterp_supported(int p) { return p <= 48; }
+
+void launch_basis(const ChebDev& cb, const DBox* boxes, const int* leaves, int nleaf, const double* pts, int n,
+                  int use_targets, double* basis, cudaStream_t st) {
+  if (nleaf <= 0) return;
+  k_basis<<<nleaf, 256, 0, st>>>(cb, boxes, leaves, pts, n, use_targets, basis);
+}
+
+void launch_anterp_mma(int kernel, const ChebDev& cb, const DBox* boxes, const int* leaves, int nleaf,
+                       const double* basis, const double* str, int n, double* out, int nch, cudaStream_t st) {
+  if (nleaf <= 0) return;
+  const int p = cb.p, pz = cb.pz;
+  const int M = nch * pz * p, total_mt = (M + 7) / 8;
+  const int NTv = (p + 7) / 8;
+  const int mtw = NTv <= 2 ? 8 : (NTv == 3 ? 6 : (NTv == 4 ? 4 : 3));
+  const int per_cta_max = kAWarps * mtw;
+  const int nct = (total_mt + per_cta_max - 1) / per_cta_max;
+  const int mt_per = (total_mt + nct - 1) / nct;
+  const size_t smem =
+      sizeof(double) * (size_t)kKC * (stride816(nch * pz) + stride816(p) + stride816(NTv * 8) + 6);
+  dim3 grid(nleaf, nct);
+#define AM(NTT, MW)                                                                                             \
+  do {                                                                                                          \
+    smem_attr((const void*)k_anterp_mma<NTT, MW>, smem);                                                        \
+    k_anterp_mma<NTT, MW><<<grid, kAWarps * 32, smem, st>>>(kernel, cb, boxes, leaves, basis, str, n, out, nch, \
+                                                             mt_per);                                           \
+  } while (0)
+  if (NTv <= 1) AM(1, 8);
+  else if (NTv == 2) AM(2, 8);
+  else if (NTv == 3) AM(3, 6);
+  else if (NTv == 4) AM(4, 4);
+  else if (NTv == 5) AM(5, 3);
+  else AM(6, 3);
+#undef AM
+}
+
+void launch_interp_mma(const ChebDev& cb, const DBox* boxes, const int* leaves, int nleaf, const double* tbasis,
+                       int nt, const int* tperm, const double* incoming, double* ufar, cudaStream_t st) {
+  if (nleaf <= 0) return;
+  const int p = cb.p, N = cb.dim * cb.pz * p;
+  const int KSv = (p + 3) / 4;
+  auto smem_for = [&](int KS) {
+    const int WS = KS * 4 + 4;
+    return sizeof(double) * ((size_t)kNC * WS + (size_t)kTB * WS + 2 * (size_t)kTB * (p + 1)) + sizeof(int) * N;
+  };
+#define IM(KSS)                                                                                          \
+  do {                                                                                                   \
+    size_t sm = smem_for(KSS);                                                                           \
+    smem_attr((const void*)k_interp_mma<KSS>, sm);                                                       \
+    k_interp_mma<KSS><<<nleaf, 256, sm, st>>>(cb, boxes, leaves, tbasis, nt, tperm, incoming, ufar);     \
+  } while (0)
+  if (KSv <= 2) IM(2);
+  else if (KSv <= 4) IM(4);
+  else if (KSv <= 6) IM(6);
+  else if (KSv <= 8) IM(8);
+  else IM(12);
+#undef IM
+}
+
+}  // namespace sdmkb

@@ -59,6 +59,17 @@ void launch_interp_targets(const ChebDev& cb, const dev::DBox* boxes, const int*
                            const double* tpts, int nt, const int* tperm, const double* incoming,
                            double* ufar, cudaStream_t st);
 
+// ---- anterp_mma.cu (DMMA versions of K3 / K11) ------------------------------
+bool mma_anterp_supported(int p);
+// basis[axis][i][p] for the source (use_targets = 0) or target points of `leaves`
+void launch_basis(const ChebDev& cb, const dev::DBox* boxes, const int* leaves, int nleaf, const double* pts,
+                  int n, int use_targets, double* basis, cudaStream_t st);
+void launch_anterp_mma(int kernel, const ChebDev& cb, const dev::DBox* boxes, const int* leaves, int nleaf,
+                       const double* basis, const double* str, int n, double* out, int nch, cudaStream_t st);
+void launch_interp_mma(const ChebDev& cb, const dev::DBox* boxes, const int* leaves, int nleaf,
+                       const double* tbasis, int nt, const int* tperm, const double* incoming, double* ufar,
+                       cudaStream_t st);
+
 // ---- tensor.cu (K4 child->parent merge, K9 parent->child interpolation) ----
 // For each pair i: dst[out_box[i]] (+)= (Mz (x) My (x) Mx) src[in_box[i]] on
 // `nch` channels, matrices chosen by the child index bits of ci[i]
