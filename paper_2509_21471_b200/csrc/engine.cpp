@@ -580,7 +580,10 @@ void Context::run_upward() {  // dmk.cpp:555-655
   for (int lev = pr.tree.max_level - 1; lev >= 0; --lev) {
     const Problem::LevelLists& X = pr.levels[lev];
     if (X.n_merge == 0) continue;
-    launch_tensor_apply(p, pz, d, mats_up_, X.merge_in, X.merge_out, X.merge_ci, X.n_merge, pr.nch, og, og, 2, st_);
+    if (tensor_mma_supported(p, d))
+      launch_tensor_mma(p, mats_up_, X.merge_in, X.merge_out, X.merge_ci, X.n_merge, pr.nch, og, og, 2, d, st_);
+    else
+      launch_tensor_apply(p, pz, d, mats_up_, X.merge_in, X.merge_out, X.merge_ci, X.n_merge, pr.nch, og, og, 2, st_);
     ++launches_;
   }
 }
@@ -624,6 +627,7 @@ void Context::run_downward() {  // dmk.cpp:705-857
   const int M = (P.N1 - 1) / 2;
   GridDev& gd = grid(grid_lev_, "grid_lev", d, p, P.N1, PI / 3.0, band_r2(P, M, PI / 3.0));
   const PWGrid& g = gd.g;
+  const bool use_mma = pw_mma_supported(g) && !getenv("SDMK_NO_PW_MMA");
   const int L = pr.tree.max_level + 1;
   const int S = 3 * M * M + 1;
   // per-level symbol tables (dmk.cpp:741-746), one upload
@@ -654,7 +658,10 @@ void Context::run_downward() {  // dmk.cpp:705-857
       for (int s0 = 0; s0 < X.n_src; s0 += chunk_src) {
         int n = std::min(chunk_src, X.n_src - s0);
         double2* B = arena_.as<double2>("pw_B", (size_t)n * pr.nch * g.pz * g.ncol);
-        launch_forward(g, X.src_boxes + s0, n, pr.nch, og, B, G + (size_t)s0 * pr.nch * g.nhalf, st_);
+        if (use_mma)
+          launch_forward_mma(g, X.src_boxes + s0, n, pr.nch, og, B, G + (size_t)s0 * pr.nch * g.nhalf, st_);
+        else
+          launch_forward(g, X.src_boxes + s0, n, pr.nch, og, B, G + (size_t)s0 * pr.nch * g.nhalf, st_);
         launches_ += 2;
       }
       for (int t0 = 0; t0 < X.n_tgt; t0 += chunk_tgt) {
@@ -663,7 +670,10 @@ void Context::run_downward() {  // dmk.cpp:705-857
         double2* C = arena_.as<double2>("pw_C", (size_t)n * d * g.pz * g.ncol);
         launch_accumulate_symbol(g, P.kernel, n, X.ent_start + t0, X.ent_slot, X.ent_tau, G, pr.nch,
                                  dA + (size_t)lev * S, h, F, st_);
-        launch_inverse(g, X.tgt_boxes + t0, n, d, F, C, pf, in, st_);
+        if (use_mma)
+          launch_inverse_mma(g, X.tgt_boxes + t0, n, d, F, C, pf, in, st_);
+        else
+          launch_inverse(g, X.tgt_boxes + t0, n, d, F, C, pf, in, st_);
         launches_ += 3;
       }
       cudaEventRecord(e1, st_);
@@ -673,8 +683,11 @@ void Context::run_downward() {  // dmk.cpp:705-857
       pw_ms += ms;
     }
     if (X.n_interp > 0) {
-      launch_tensor_apply(p, pz, d, mats_down_, X.interp_in, X.interp_out, X.interp_ci, X.n_interp, d, in, in, 1,
-                          st_);
+      if (tensor_mma_supported(p, d))
+        launch_tensor_mma(p, mats_down_, X.interp_in, X.interp_out, X.interp_ci, X.n_interp, d, in, in, 1, d, st_);
+      else
+        launch_tensor_apply(p, pz, d, mats_down_, X.interp_in, X.interp_out, X.interp_ci, X.n_interp, d, in, in, 1,
+                            st_);
       ++launches_;
     }
   }

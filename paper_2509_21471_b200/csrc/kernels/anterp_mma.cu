@@ -23,9 +23,12 @@ namespace {
 
 using dev::DBox;
 
-__host__ __device__ __forceinline__ int stride816(int x) {  // smallest y >= x with y % 16 == 8
-  int y = (x + 7) / 8 * 8;
-  return (y % 16 == 8) ? y : y + 8;
+// Shared-memory row stride (in doubles) for fragment loads: a warp-wide 8-byte
+// load is served per half-warp, whose 16 lanes touch 4 rows x 4 consecutive
+// columns; a stride == 4 (mod 8) puts the 4 rows on disjoint bank quads.
+__host__ __device__ __forceinline__ int cstride(int x) {  // smallest y >= x with y % 8 == 4
+  int y = (x + 3) / 4 * 4;
+  return (y % 8 == 4) ? y : y + 4;
 }
 
 // ---------------------------------------------------------------- bases --
@@ -81,6 +84,10 @@ __device__ __forceinline__ void channels(int kernel, int dim, const double* __re
 constexpr int kKC = 32;     // points per shared chunk
 constexpr int kAWarps = 8;
 
+// Raw per-chunk data arrives by cp.async (double buffered): bx rows (the B
+// operand, zero padded to NT*8), by rows, bz rows and the raw strengths.  The
+// product s_ch * bz is formed once per chunk in shared memory; the A fragment
+// is (s_ch bz) * by.
 template <int NT, int kMTW>
 __global__ void __launch_bounds__(kAWarps * 32, 2) k_anterp_mma(int kernel, ChebDev cb, const DBox* __restrict__ boxes,
                                                                const int* __restrict__ leaves,
@@ -89,11 +96,11 @@ __global__ void __launch_bounds__(kAWarps * 32, 2) k_anterp_mma(int kernel, Cheb
                                                                double* __restrict__ out, int nch, int mt_per_cta) {
   extern __shared__ double sm[];
   const int p = cb.p, pz = cb.pz, dim = cb.dim;
-  const int RS = stride816(nch * pz), BS = stride816(p), XS = stride816(NT * 8);
-  double* sbz = sm;                 // [kKC][RS]  s_ch * bz(iz)
-  double* bys = sbz + kKC * RS;     // [kKC][BS]
-  double* bxs = bys + kKC * BS;     // [kKC][XS]  zero-padded to NT*8 columns
-  double* svs = bxs + kKC * XS;     // [kKC][6]
+  const int sc = kernel == 0 ? dim : (kernel == 1 ? 2 * dim : (dim == 3 ? 3 : 1));
+  const int RS = cstride(nch * pz), BS = cstride(p), XS = cstride(NT * 8);
+  const int RAW = kKC * (XS + 2 * BS + 8);   // one raw buffer
+  double* sbz = sm;                          // [kKC][RS]  s_ch * bz(iz)
+  double* raw = sbz + kKC * RS;              // 2 x { bx[kKC][XS], by[kKC][BS], bz[kKC][BS], str[kKC][8] }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int b = leaves[blockIdx.x];
   const DBox box = boxes[b];
@@ -118,38 +125,87 @@ __global__ void __launch_bounds__(kAWarps * 32, 2) k_anterp_mma(int kernel, Cheb
   const double* bxg = basis;
   const double* byg = basis + (size_t)n * p;
   const double* bzg = basis + (size_t)2 * n * p;
-  for (int a0 = box.sb; a0 < box.se; a0 += kKC) {
-    const int kc = min(kKC, box.se - a0);
-    __syncthreads();
-    for (int pt = tid; pt < kKC; pt += blockDim.x) {
-      if (pt < kc) channels(kernel, dim, str, n, a0 + pt, svs + pt * 6);
-      else for (int j = 0; j < 6; ++j) svs[pt * 6 + j] = 0.0;
-    }
+  const int nchunks = (box.se - box.sb + kKC - 1) / kKC;
+  auto issue = [&](int c, int buf) {
+    const int a0 = box.sb + c * kKC, kc = min(kKC, box.se - a0);
+    double* rb = raw + buf * RAW;
+    double* bx = rb;
+    double* by = bx + kKC * XS;
+    double* bz = by + kKC * BS;
+    double* ss = bz + kKC * BS;
     for (int e = tid; e < kKC * XS; e += blockDim.x) {
       const int pt = e / XS, i = e % XS;
-      bxs[e] = (pt < kc && i < p) ? bxg[(size_t)(a0 + pt) * p + i] : 0.0;
+      const bool v = pt < kc && i < p;
+      dev::cp_async8(bx + e, v ? bxg + (size_t)(a0 + pt) * p + i : bxg, v);
     }
     for (int e = tid; e < kKC * p; e += blockDim.x) {
       const int pt = e / p, i = e % p;
-      bys[pt * BS + i] = pt < kc ? byg[(size_t)(a0 + pt) * p + i] : 0.0;
+      const bool v = pt < kc;
+      dev::cp_async8(by + pt * BS + i, v ? byg + (size_t)(a0 + pt) * p + i : byg, v);
+      if (dim == 3) dev::cp_async8(bz + pt * BS + i, v ? bzg + (size_t)(a0 + pt) * p + i : bzg, v);
+    }
+    for (int e = tid; e < kKC * sc; e += blockDim.x) {
+      const int pt = e / sc, j = e % sc;
+      const bool v = pt < kc;
+      dev::cp_async8(ss + pt * 8 + j, v ? str + (size_t)j * n + a0 + pt : str, v);
+    }
+    dev::cp_commit();
+  };
+  if (nchunks > 0) issue(0, 0);
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c & 1;
+    __syncthreads();  // everyone is done with the buffer the next issue overwrites
+    if (c + 1 < nchunks) {
+      issue(c + 1, buf ^ 1);
+      dev::cp_wait1();
+    } else {
+      dev::cp_wait0();
     }
     __syncthreads();
-    for (int e = tid; e < kKC * nch * pz; e += blockDim.x) {
-      const int pt = e / (nch * pz), r = e % (nch * pz), ch = r / pz, iz = r % pz;
-      const double bz = dim == 3 ? (pt < kc ? bzg[(size_t)(a0 + pt) * p + iz] : 0.0) : 1.0;
-      sbz[pt * RS + r] = svs[pt * 6 + ch] * bz;
+    const double* bx = raw + buf * RAW;
+    const double* by = bx + kKC * XS;
+    const double* bz = by + kKC * BS;
+    const double* ss = bz + kKC * BS;
+    for (int e = tid; e < kKC * nch; e += blockDim.x) {  // s_ch * bz (dmk.cpp:492-525 channels)
+      const int pt = e / nch, ch = e % nch;
+      double chv[6];
+      if (kernel == 1) {
+        const double* s = ss + pt * 8;
+        double w = 0.0;
+        for (int j = 0; j < dim; ++j) w += s[j] * s[dim + j];
+        if (dim == 3) {
+          chv[0] = 2.0 * s[0] * s[3] + w;
+          chv[1] = 2.0 * s[1] * s[4] + w;
+          chv[2] = 2.0 * s[2] * s[5] + w;
+          chv[3] = s[0] * s[4] + s[1] * s[3];
+          chv[4] = s[0] * s[5] + s[2] * s[3];
+          chv[5] = s[1] * s[5] + s[2] * s[4];
+        } else {
+          chv[0] = 2.0 * s[0] * s[2] + w;
+          chv[1] = 2.0 * s[1] * s[3] + w;
+          chv[2] = s[0] * s[3] + s[1] * s[2];
+        }
+      } else {
+        for (int j = 0; j < 6; ++j) chv[j] = j < sc ? ss[pt * 8 + j] : 0.0;
+      }
+      double sv = 0.0;
+#pragma unroll
+      for (int j = 0; j < 6; ++j)
+        if (j == ch) sv = chv[j];
+      for (int iz = 0; iz < pz; ++iz) sbz[pt * RS + ch * pz + iz] = sv * (dim == 3 ? bz[pt * BS + iz] : 1.0);
     }
     __syncthreads();
+    const int kc = min(kKC, box.se - (box.sb + c * kKC));
     const int ksteps = (kc + 3) / 4;
     for (int ks = 0; ks < ksteps; ++ks) {
       const int k = ks * 4 + t;
       double bv[NT];
 #pragma unroll
-      for (int j = 0; j < NT; ++j) bv[j] = bxs[k * XS + j * 8 + g];
+      for (int j = 0; j < NT; ++j) bv[j] = bx[k * XS + j * 8 + g];
 #pragma unroll
       for (int i = 0; i < kMTW; ++i) {
         if (val[i]) {
-          const double av = sbz[k * RS + chiz[i]] * bys[k * BS + iyv[i]];
+          const double av = sbz[k * RS + chiz[i]] * by[k * BS + iyv[i]];
 #pragma unroll
           for (int j = 0; j < NT; ++j) dev::dmma(acc[i][j][0], acc[i][j][1], av, bv[j]);
         }
@@ -164,19 +220,21 @@ __global__ void __launch_bounds__(kAWarps * 32, 2) k_anterp_mma(int kernel, Cheb
     if (m >= M) continue;
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
-      const int c = j * 8 + 2 * t;
-      if (c < p) ob[(size_t)m * p + c] = acc[i][j][0];
-      if (c + 1 < p) ob[(size_t)m * p + c + 1] = acc[i][j][1];
+      const int cc = j * 8 + 2 * t;
+      if (cc < p) ob[(size_t)m * p + cc] = acc[i][j][0];
+      if (cc + 1 < p) ob[(size_t)m * p + cc + 1] = acc[i][j][1];
     }
   }
 }
 
 // ------------------------------------------------------------------- K11 --
-constexpr int kTB = 64;      // targets per block (one m-tile per warp)
-constexpr int kNC = 256;     // W rows per shared chunk
+constexpr int kTB = 128;     // targets per block (two m-tiles per warp)
 
-template <int KS>
-__global__ void __launch_bounds__(256, 2) k_interp_mma(ChebDev cb, const DBox* __restrict__ boxes,
+// W chunks arrive by cp.async, double buffered; each warp keeps the A
+// fragments of its two 8-target m-tiles in registers and runs their DMMA
+// chains interleaved.
+template <int KS, int kNC>  // kNC: W rows per shared chunk
+__global__ void __launch_bounds__(256, 1) k_interp_mma(ChebDev cb, const DBox* __restrict__ boxes,
                                                       const int* __restrict__ leaves,
                                                       const double* __restrict__ tbasis, int nt,
                                                       const int* __restrict__ tperm,
@@ -186,8 +244,8 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(ChebDev cb, const DBox* _
   constexpr int KP = KS * 4, WS = KP + 4;
   const int p = cb.p, pz = cb.pz, dim = cb.dim;
   const int N = dim * pz * p, BS = p + 1;
-  double* Ws = sm;                    // [kNC][WS]
-  double* bxs = Ws + kNC * WS;        // [kTB][WS]
+  double* Ws = sm;                    // [2][kNC][WS]
+  double* bxs = Ws + 2 * kNC * WS;    // [kTB][WS]
   double* bys = bxs + kTB * WS;       // [kTB][BS]
   double* bzs = bys + kTB * BS;       // [kTB][BS]
   int* ntab = reinterpret_cast<int*>(bzs + kTB * BS);  // [N]
@@ -198,13 +256,26 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(ChebDev cb, const DBox* _
     const int j = e / (pz * p), r = e % (pz * p);
     ntab[e] = (j << 16) | ((r / p) << 8) | (r % p);
   }
+  for (int e = tid; e < 2 * kNC * WS; e += blockDim.x) Ws[e] = 0.0;  // k padding stays zero
   const double* W = incoming + (size_t)b * N * p;
   const double* bxg = tbasis;
   const double* byg = tbasis + (size_t)nt * p;
   const double* bzg = tbasis + (size_t)2 * nt * p;
+  const int nchunk = (N + kNC - 1) / kNC;
+  auto issue = [&](int c, int buf) {
+    const int n0 = c * kNC, nc = min(kNC, N - n0);
+    double* dstb = Ws + buf * kNC * WS;
+    for (int e = tid; e < kNC * p; e += blockDim.x) {
+      const int r = e / p, k = e % p;
+      const bool v = r < nc;
+      dev::cp_async8(dstb + r * WS + k, v ? W + (size_t)(n0 + r) * p + k : W, v);
+    }
+    dev::cp_commit();
+  };
   for (int t0 = box.tb; t0 < box.te; t0 += kTB) {
     const int tc = min(kTB, box.te - t0);
     __syncthreads();
+    issue(0, 0);
     for (int e = tid; e < kTB * KP; e += blockDim.x) {
       const int a = e / KP, k = e % KP;
       bxs[a * WS + k] = (a < tc && k < p) ? bxg[(size_t)(t0 + a) * p + k] : 0.0;
@@ -215,25 +286,36 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(ChebDev cb, const DBox* _
       bzs[a * BS + k] = a < tc ? (dim == 3 ? bzg[(size_t)(t0 + a) * p + k] : (k == 0 ? 1.0 : 0.0)) : 0.0;
     }
     __syncthreads();
-    const int arow = warp * 8 + g;  // this lane's target (A row / C row)
-    double av[KS];
+    const int r0 = warp * 16 + g, r1 = r0 + 8;  // this lane's two targets (A / C rows)
+    double a0[KS], a1[KS];
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) av[ks] = bxs[arow * WS + ks * 4 + t];
-    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-    for (int n0 = 0; n0 < N; n0 += kNC) {
-      const int nc = min(kNC, N - n0);
-      __syncthreads();
-      for (int e = tid; e < kNC * KP; e += blockDim.x) {
-        const int r = e / KP, k = e % KP;
-        Ws[r * WS + k] = (r < nc && k < p) ? W[(size_t)(n0 + r) * p + k] : 0.0;
+    for (int ks = 0; ks < KS; ++ks) {
+      a0[ks] = bxs[r0 * WS + ks * 4 + t];
+      a1[ks] = bxs[r1 * WS + ks * 4 + t];
+    }
+    double v[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+    const bool active = warp * 16 < tc;
+    for (int c = 0; c < nchunk; ++c) {
+      const int buf = c & 1;
+      if (c + 1 < nchunk) {
+        issue(c + 1, buf ^ 1);
+        dev::cp_wait1();
+      } else {
+        dev::cp_wait0();
       }
       __syncthreads();
-      if (warp * 8 < tc) {
+      const double* Wc = Ws + buf * kNC * WS;
+      const int n0 = c * kNC, nc = min(kNC, N - n0);
+      if (active) {
         const int ntiles = (nc + 7) / 8;
         for (int nt_ = 0; nt_ < ntiles; ++nt_) {
-          double c0 = 0.0, c1 = 0.0;
+          double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) dev::dmma(c0, c1, av[ks], Ws[(nt_ * 8 + g) * WS + ks * 4 + t]);
+          for (int ks = 0; ks < KS; ++ks) {
+            const double bv = Wc[(nt_ * 8 + g) * WS + ks * 4 + t];
+            dev::dmma(c00, c01, a0[ks], bv);
+            dev::dmma(c10, c11, a1[ks], bv);
+          }
           const int na = n0 + nt_ * 8 + 2 * t;
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
@@ -241,27 +323,34 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(ChebDev cb, const DBox* _
             if (nn < N) {
               const int code = ntab[nn];
               const int j = code >> 16, iz = (code >> 8) & 255, iy = code & 255;
-              const double w = bzs[arow * BS + iz] * bys[arow * BS + iy] * (e ? c1 : c0);
-              if (j == 0) v0 += w;
-              else if (j == 1) v1 += w;
-              else v2 += w;
+              const double w0 = bzs[r0 * BS + iz] * bys[r0 * BS + iy] * (e ? c01 : c00);
+              const double w1 = bzs[r1 * BS + iz] * bys[r1 * BS + iy] * (e ? c11 : c10);
+              v[0][j] += w0;
+              v[1][j] += w1;
             }
           }
         }
       }
+      __syncthreads();  // the next issue overwrites this buffer
     }
-    // combine the 4 lanes of each row (fixed order -> deterministic)
-    v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
-    v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
-    v2 += __shfl_xor_sync(0xffffffffu, v2, 1);
-    v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
-    v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
-    v2 += __shfl_xor_sync(0xffffffffu, v2, 2);
-    if (t == 0 && arow < tc) {
-      double* ut = ufar + (size_t)tperm[t0 + arow] * dim;
-      ut[0] = v0;
-      ut[1] = v1;
-      if (dim == 3) ut[2] = v2;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        v[h][j] += __shfl_xor_sync(0xffffffffu, v[h][j], 1);
+        v[h][j] += __shfl_xor_sync(0xffffffffu, v[h][j], 2);
+      }
+    if (t == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = h ? r1 : r0;
+        if (r < tc) {
+          double* ut = ufar + (size_t)tperm[t0 + r] * dim;
+          ut[0] = v[h][0];
+          ut[1] = v[h][1];
+          if (dim == 3) ut[2] = v[h][2];
+        }
+      }
     }
   }
 }
@@ -291,7 +380,7 @@ void launch_anterp_mma(int kernel, const ChebDev& cb, const DBox* boxes, const i
   const int nct = (total_mt + per_cta_max - 1) / per_cta_max;
   const int mt_per = (total_mt + nct - 1) / nct;
   const size_t smem =
-      sizeof(double) * (size_t)kKC * (stride816(nch * pz) + stride816(p) + stride816(NTv * 8) + 6);
+      sizeof(double) * (size_t)kKC * (cstride(nch * pz) + 2 * (cstride(NTv * 8) + 2 * cstride(p) + 8));
   dim3 grid(nleaf, nct);
 #define AM(NTT, MW)                                                                                             \
   do {                                                                                                          \
@@ -313,21 +402,21 @@ void launch_interp_mma(const ChebDev& cb, const DBox* boxes, const int* leaves, 
   if (nleaf <= 0) return;
   const int p = cb.p, N = cb.dim * cb.pz * p;
   const int KSv = (p + 3) / 4;
-  auto smem_for = [&](int KS) {
+  auto smem_for = [&](int KS, int NC) {
     const int WS = KS * 4 + 4;
-    return sizeof(double) * ((size_t)kNC * WS + (size_t)kTB * WS + 2 * (size_t)kTB * (p + 1)) + sizeof(int) * N;
+    return sizeof(double) * (2 * (size_t)NC * WS + (size_t)kTB * WS + 2 * (size_t)kTB * (p + 1)) + sizeof(int) * N;
   };
-#define IM(KSS)                                                                                          \
-  do {                                                                                                   \
-    size_t sm = smem_for(KSS);                                                                           \
-    smem_attr((const void*)k_interp_mma<KSS>, sm);                                                       \
-    k_interp_mma<KSS><<<nleaf, 256, sm, st>>>(cb, boxes, leaves, tbasis, nt, tperm, incoming, ufar);     \
+#define IM(KSS, NCC)                                                                                      \
+  do {                                                                                                    \
+    size_t sm = smem_for(KSS, NCC);                                                                       \
+    smem_attr((const void*)k_interp_mma<KSS, NCC>, sm);                                                   \
+    k_interp_mma<KSS, NCC><<<nleaf, 256, sm, st>>>(cb, boxes, leaves, tbasis, nt, tperm, incoming, ufar); \
   } while (0)
-  if (KSv <= 2) IM(2);
-  else if (KSv <= 4) IM(4);
-  else if (KSv <= 6) IM(6);
-  else if (KSv <= 8) IM(8);
-  else IM(12);
+  if (KSv <= 2) IM(2, 256);
+  else if (KSv <= 4) IM(4, 256);
+  else if (KSv <= 6) IM(6, 256);
+  else if (KSv <= 8) IM(8, 128);
+  else IM(12, 64);
 #undef IM
 }
 

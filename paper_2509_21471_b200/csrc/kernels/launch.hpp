@@ -80,6 +80,12 @@ void launch_tensor_apply(int p, int pz, int dim, const double* mats, const int* 
                          const int* out_box, const int* ci, int npairs, int nch,
                          const double* src, double* dst, int accumulate, cudaStream_t st);
 
+// ---- tensor_mma.cu: DMMA version of the above (3D, p <= 32) ----
+bool tensor_mma_supported(int p, int dim);
+void launch_tensor_mma(int p, const double* mats, const int* in_list, const int* out_box, const int* ci,
+                       int npairs, int nch, const double* src, double* dst, int accumulate, int dim,
+                       cudaStream_t st);
+
 // ---- planewave.cu (K5-K8/K10: forward DFT, phased accumulation + symbol,
 // inverse DFT) -----------------------------------------------------------------
 struct PWGrid {
@@ -107,6 +113,13 @@ void launch_accumulate_symbol(const PWGrid& g, int kernel, int ntb, const int* e
 // incoming[box(t)][j] += pf * Re(inverse(F[t][j])); C is scratch
 void launch_inverse(const PWGrid& g, const int* tboxes, int ntb, int d, const double2* F,
                     double2* C, double pf, double* incoming, cudaStream_t st);
+
+// ---- planewave_mma.cu: DMMA versions of the transforms (3D, p <= 32, N <= 48) ----
+bool pw_mma_supported(const PWGrid& g);
+void launch_forward_mma(const PWGrid& g, const int* boxes, int nbox, int nch, const double* outgoing,
+                        double2* B, double2* G, cudaStream_t st);
+void launch_inverse_mma(const PWGrid& g, const int* tboxes, int ntb, int d, const double2* F,
+                        double2* C, double pf, double* incoming, cudaStream_t st);
 
 // ---- residual.cu (K12) -------------------------------------------------------
 struct ResidTables {

@@ -1,0 +1,426 @@
+// Plane-wave transforms (K5 forward, K8 inverse; dmk.cpp:166-243) on the FP64
+// tensor cores, 3D.  Same half-spectrum / band-compressed layout as
+// planewave.cu; the four stages become dense DMMA GEMMs (complex products as
+// real GEMMs with the K dimension doubled over (index, re/im)):
+//
+//  fwd_xy : per (box, ch), four z-slabs at a time (cp.async double buffered)
+//           X  a[(s,iy), (m0,re|im)] = w[(s,iy), ix] * EX[ix, (m0,re|im)]
+//           Y  b[s][my, m0]          = E[my, iy] a[s][iy, m0]   (complex)
+//           -> B[box][ch][iz][col] for the in-band columns (my, m0)
+//  fwd_z  : per (box, ch, 64-column block)
+//           G[mz, col] = E[mz, iz] B[iz, col]                    (complex)
+//  inv_z  : per (box, j, 64-column block)
+//           C1[iz, col] = conj(E)[mz, iz]^T F[mz, col]           (complex)
+//  inv_xy : per (box, j), four slabs at a time
+//           Y  d[(s,iy), m0] = conj(E)[my, iy]^T C1[s][(my, m0)] (complex)
+//           X  out[(s,iy), ix] += pf * sum_m0 wt(m0) Re(conj(E)[m0, ix] d)
+//
+// Fragment-load strides follow the bank rule in anterp_mma.cu (== 4 mod 8 for
+// row-indexed operands; the interleaved (index, re|im) B operands use rows of
+// stride == 8 mod 16).
+#include "common.cuh"
+#include "launch.hpp"
+
+namespace sdmkb {
+
+namespace {
+
+using dev::cp_async8;
+using dev::cp_commit;
+using dev::cp_wait0;
+using dev::cp_wait1;
+using dev::dmma;
+
+constexpr int kW = 8;  // warps per CTA
+
+__host__ __device__ constexpr int r4(int x) { return (x + 3) / 4 * 4 % 8 == 4 ? (x + 3) / 4 * 4 : (x + 3) / 4 * 4 + 4; }
+__host__ __device__ constexpr int r8(int x) { return (x + 7) / 8 * 8 % 16 == 8 ? (x + 7) / 8 * 8 : (x + 7) / 8 * 8 + 8; }
+
+// ------------------------------------------------------------------ fwd_xy --
+// smem layout (doubles): EX[NX8][SE]  (rows (m0,part) -> B^T of the X stage)
+//                        EYr/EYi[NY8][SY] (A' of the Y stage, k' = 2 iy + part)
+//                        win[2][4*P8][SE] (A of the X stage), a[4*P8][SAa]
+template <int PT>
+__global__ void __launch_bounds__(kW * 32, 1) k_fwd_xy_mma(PWGrid g, const int* __restrict__ boxes, int nch,
+                                                          const double* __restrict__ outgoing,
+                                                          double2* __restrict__ B) {
+  constexpr int P8 = PT * 8;
+  constexpr int SE = P8 + 4;  // == 4 mod 8 for P8 = 24, 32
+  const int p = g.p, M = g.M, N = g.N, ncol = g.ncol, pp = p * p;
+  const int M1 = M + 1, NX = 2 * M1, NX8 = (NX + 7) / 8 * 8, NY8 = (N + 7) / 8 * 8, M18 = (M1 + 7) / 8 * 8;
+  const int SY = r4(2 * P8), SAa = r8(NX8 > 2 * M18 ? NX8 : 2 * M18);
+  extern __shared__ double sm[];
+  double* EX = sm;                        // [NX8][SE]
+  double* EYr = EX + NX8 * SE;            // [NY8][SY]
+  double* EYi = EYr + NY8 * SY;           // [NY8][SY]
+  double* win = EYi + NY8 * SY;           // [2][4*P8][SE]
+  double* a = win + 2 * 4 * P8 * SE;      // [4*P8][SAa]
+  int* colidx = reinterpret_cast<int*>(a + 4 * P8 * SAa);  // [N][M1]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
+  for (int e = tid; e < NX8 * SE; e += blockDim.x) {  // EX[(m0,part)][ix] = E[m0][ix].re|im
+    const int r = e / SE, ix = e % SE, m0 = r >> 1, part = r & 1;
+    double v = 0.0;
+    if (m0 < M1 && ix < p) {
+      const double2 ev = g.E[(size_t)(m0 + M) * p + ix];
+      v = part ? ev.y : ev.x;
+    }
+    EX[e] = v;
+  }
+  for (int e = tid; e < NY8 * SY; e += blockDim.x) {  // EY'[my][(iy,part)]: re' = [Er | -Ei], im' = [Ei | Er]
+    const int my = e / SY, k = e % SY, iy = k >> 1, part = k & 1;
+    double vr = 0.0, vi = 0.0;
+    if (my < N && iy < p && k < 2 * P8) {
+      const double2 ev = g.E[(size_t)my * p + iy];
+      vr = part ? -ev.y : ev.x;
+      vi = part ? ev.x : ev.y;
+    }
+    EYr[e] = vr;
+    EYi[e] = vi;
+  }
+  for (int e = tid; e < N * M1; e += blockDim.x) colidx[e] = -1;
+  for (int e = tid; e < 2 * 4 * P8 * SE; e += blockDim.x) win[e] = 0.0;
+  for (int e = tid; e < 4 * P8 * SAa; e += blockDim.x) a[e] = 0.0;
+  __syncthreads();
+  for (int c = tid; c < ncol; c += blockDim.x) colidx[(g.col_my[c] + M) * M1 + g.col_m0[c]] = c;
+  const int slot = blockIdx.x, ch = blockIdx.y;
+  const double* w = outgoing + ((size_t)boxes[slot] * nch + ch) * (size_t)(p * pp);
+  double2* Bo = B + ((size_t)slot * nch + ch) * (size_t)g.pz * ncol;
+  const int ngroups = (p + 3) / 4;
+  auto issue = [&](int grp, int buf) {
+    double* dst = win + buf * 4 * P8 * SE;
+    const int jz0 = grp * 4;
+    for (int e = tid; e < 4 * pp; e += blockDim.x) {
+      const int s = e / pp, r = (e / p) % p, cc = e % p;
+      const bool v = jz0 + s < p;
+      cp_async8(dst + (s * P8 + r) * SE + cc, v ? w + (size_t)(jz0 + s) * pp + r * p + cc : w, v);
+    }
+    cp_commit();
+  };
+  issue(0, 0);
+  const int xtiles = 4 * PT * (NX8 / 8);
+  const int ytiles = 4 * (NY8 / 8) * (M18 / 8);  // (s, my-tile, m0-tile); re and im computed together
+  for (int grp = 0; grp < ngroups; ++grp) {
+    const int buf = grp & 1;
+    __syncthreads();
+    if (grp + 1 < ngroups) {
+      issue(grp + 1, buf ^ 1);
+      cp_wait1();
+    } else {
+      cp_wait0();
+    }
+    __syncthreads();
+    const double* A = win + buf * 4 * P8 * SE;
+    // X stage
+    for (int tile0 = warp; tile0 < xtiles; tile0 += 2 * kW) {
+      const int tile1 = tile0 + kW;
+      const bool two = tile1 < xtiles;
+      const int nnt = NX8 / 8;
+      const int mA = tile0 / nnt, nA = tile0 % nnt, mB = two ? tile1 / nnt : mA, nB = two ? tile1 % nnt : nA;
+      double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < PT * 2; ++ks) {
+        dmma(c0, c1, A[(mA * 8 + gq) * SE + ks * 4 + t], EX[(nA * 8 + gq) * SE + ks * 4 + t]);
+        if (two) dmma(d0, d1, A[(mB * 8 + gq) * SE + ks * 4 + t], EX[(nB * 8 + gq) * SE + ks * 4 + t]);
+      }
+      a[(mA * 8 + gq) * SAa + nA * 8 + 2 * t] = c0;
+      a[(mA * 8 + gq) * SAa + nA * 8 + 2 * t + 1] = c1;
+      if (two) {
+        a[(mB * 8 + gq) * SAa + nB * 8 + 2 * t] = d0;
+        a[(mB * 8 + gq) * SAa + nB * 8 + 2 * t + 1] = d1;
+      }
+    }
+    __syncthreads();
+    // Y stage: b[s][my][m0] (complex); B'[(iy,part)][m0] = a[s][iy][2 m0 + part]
+    const int nmy = NY8 / 8, nm0 = M18 / 8;
+    for (int tile = warp; tile < ytiles; tile += kW) {
+      const int s = tile / (nmy * nm0), mt = (tile / nm0) % nmy, nt = tile % nm0;
+      double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < PT * 4; ++ks) {
+        const int k = ks * 4 + t, iy = k >> 1, part = k & 1;
+        const double bv = a[(s * P8 + iy) * SAa + 2 * (nt * 8 + gq) + part];
+        dmma(cr0, cr1, EYr[(mt * 8 + gq) * SY + k], bv);
+        dmma(ci0, ci1, EYi[(mt * 8 + gq) * SY + k], bv);
+      }
+      const int my = mt * 8 + gq, iz = grp * 4 + s;
+      if (my < N && iz < p) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int m0 = nt * 8 + 2 * t + e;
+          if (m0 < M1) {
+            const int cidx = colidx[my * M1 + m0];
+            if (cidx >= 0) Bo[(size_t)iz * ncol + cidx] = make_double2(e ? cr1 : cr0, e ? ci1 : ci0);
+          }
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ z stages ----
+// Complex GEMM over 64-column blocks: OUT[rr, col] = sum_k A'[rr, (k,part)] IN[(k,part), col]
+// with IN loaded zero-filled from the compressed source.
+//  forward : rr = mz (G, compressed out), k = iz (B, dense in), A'_re = [Er | -Ei], A'_im = [Ei | Er]
+//  inverse : rr = iz (C1, dense out), k = mz (F, compressed in), conj(E)^T:
+//            A'_re = [Er | Ei], A'_im = [-Ei | Er]
+constexpr int kCB = 64;
+
+template <int KT, int RT, bool INV>  // KT: k-tiles of 8 (K8 = KT*8); RT: row tiles of 8
+__global__ void __launch_bounds__(kW * 32, 2) k_z_mma(PWGrid g, int nc, const double2* __restrict__ IN,
+                                                      double2* __restrict__ OUT) {
+  constexpr int K8 = KT * 8, SK = 2 * K8 + 4;       // A' row stride (k' = 2k + part), == 4 mod 8
+  constexpr int SI = (2 * kCB) % 16 == 8 ? 2 * kCB : 2 * kCB + 8;  // IN rows (k) of interleaved (col, part)
+  extern __shared__ double sm[];
+  double* Ar = sm;                  // [RT*8][SK]
+  double* Ai = Ar + RT * 8 * SK;    // [RT*8][SK]
+  double* In = Ai + RT * 8 * SK;    // [K8][SI]
+  const int pz = g.pz, Mz = g.Mz, ncol = g.ncol;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
+  const int rows = INV ? pz : g.Nz, kdim = INV ? g.Nz : pz;
+  for (int e = tid; e < RT * 8 * SK; e += blockDim.x) {
+    const int rr = e / SK, kk = e % SK, k = kk >> 1, part = kk & 1;
+    double vr = 0.0, vi = 0.0;
+    if (rr < rows && k < kdim && kk < 2 * K8) {
+      // forward: E[mz=rr][iz=k]; inverse: E[mz=k][iz=rr]
+      const double2 ev = INV ? g.Ez[(size_t)k * pz + rr] : g.Ez[(size_t)rr * pz + k];
+      if (!INV) {
+        vr = part ? -ev.y : ev.x;
+        vi = part ? ev.x : ev.y;
+      } else {
+        vr = part ? ev.y : ev.x;
+        vi = part ? ev.x : -ev.y;
+      }
+    }
+    Ar[e] = vr;
+    Ai[e] = vi;
+  }
+  const int box = blockIdx.x, comp = blockIdx.y, c0 = blockIdx.z * kCB;
+  const int ncb = min(kCB, ncol - c0);
+  const size_t in_stride = INV ? (size_t)g.nhalf : (size_t)pz * ncol;
+  const size_t out_stride = INV ? (size_t)pz * ncol : (size_t)g.nhalf;
+  const double2* src = IN + ((size_t)box * nc + comp) * in_stride;
+  double2* dst = OUT + ((size_t)box * nc + comp) * out_stride;
+  for (int e = tid; e < K8 * kCB; e += blockDim.x) {
+    const int k = e / kCB, cc = e % kCB, col = c0 + cc;
+    double2 v = make_double2(0.0, 0.0);
+    if (k < kdim && cc < ncb) {
+      if (INV) {
+        if (col < g.slab_ncol[k]) v = src[g.slab_off[k] + col];
+      } else {
+        v = src[(size_t)k * ncol + col];
+      }
+    }
+    In[k * SI + 2 * cc] = v.x;
+    In[k * SI + 2 * cc + 1] = v.y;
+  }
+  __syncthreads();
+  // C tiles: (row tile, column tile of 8) with re and im; warp owns tiles warp + kW*i
+  const int ntc = kCB / 8, ntile = RT * ntc;
+  for (int tile = warp; tile < ntile; tile += kW) {
+    const int rt = tile / ntc, ct = tile % ntc;
+    double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KT * 4; ++ks) {
+      const int kk = ks * 4 + t, k = kk >> 1, part = kk & 1;
+      const double bv = In[k * SI + 2 * (ct * 8 + gq) + part];
+      dmma(cr0, cr1, Ar[(rt * 8 + gq) * SK + kk], bv);
+      dmma(ci0, ci1, Ai[(rt * 8 + gq) * SK + kk], bv);
+    }
+    const int rr = rt * 8 + gq;
+    if (rr >= rows) continue;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int col = c0 + ct * 8 + 2 * t + e;
+      if (col >= c0 + ncb) continue;
+      const double2 v = make_double2(e ? cr1 : cr0, e ? ci1 : ci0);
+      if (INV) {
+        dst[(size_t)rr * ncol + col] = v;
+      } else if (col < g.slab_ncol[rr]) {
+        dst[g.slab_off[rr] + col] = v;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ inv_xy --
+template <int PT>
+__global__ void __launch_bounds__(kW * 32, 1) k_inv_xy_mma(PWGrid g, const int* __restrict__ tboxes, int d,
+                                                          const double2* __restrict__ C, double pf,
+                                                          double* __restrict__ incoming) {
+  constexpr int P8 = PT * 8;
+  const int p = g.p, M = g.M, N = g.N, ncol = g.ncol, pp = p * p;
+  const int M1 = M + 1, NY8 = (N + 7) / 8 * 8, M18 = (M1 + 7) / 8 * 8, NX = 2 * M1, NX8 = (NX + 7) / 8 * 8;
+  const int SD = r8(2 * M18);      // D rows (s,my) of interleaved (m0, part)
+  const int SA = r4(2 * NY8);      // A' rows iy, k' = 2 my + part
+  const int SX = r4(NX8 > 2 * M18 ? NX8 : 2 * M18);  // X-stage A rows (s,iy), k = (m0, part); B^T rows ix
+  extern __shared__ double sm[];
+  double* Ar = sm;                          // [P8][SA]  conj(E)^T re'
+  double* Ai = Ar + P8 * SA;                // [P8][SA]  im'
+  double* EXw = Ai + P8 * SA;               // [P8 (ix)][SX]  wt * E.re|im
+  double* D = EXw + P8 * SX;                // [4][NY8][SD]
+  double* dd = D + 4 * NY8 * SD;            // [4*P8][SX]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
+  for (int e = tid; e < P8 * SA; e += blockDim.x) {  // conj(E)^T: re' = [Er | Ei], im' = [-Ei | Er]
+    const int iy = e / SA, kk = e % SA, my = kk >> 1, part = kk & 1;
+    double vr = 0.0, vi = 0.0;
+    if (iy < p && my < N && kk < 2 * NY8) {
+      const double2 ev = g.E[(size_t)my * p + iy];
+      vr = part ? ev.y : ev.x;
+      vi = part ? ev.x : -ev.y;
+    }
+    Ar[e] = vr;
+    Ai[e] = vi;
+  }
+  for (int e = tid; e < P8 * SX; e += blockDim.x) {  // Re(conj(E) d) = Er d.re + Ei d.im, weight 1 | 2
+    const int ix = e / SX, k = e % SX, m0 = k >> 1, part = k & 1;
+    double v = 0.0;
+    if (ix < p && m0 < M1) {
+      const double2 ev = g.E[(size_t)(m0 + M) * p + ix];
+      v = (m0 ? 2.0 : 1.0) * (part ? ev.y : ev.x);
+    }
+    EXw[e] = v;
+  }
+  for (int e = tid; e < 4 * NY8 * SD; e += blockDim.x) D[e] = 0.0;
+  const int tb = blockIdx.x, j = blockIdx.y;
+  const double2* Ci = C + ((size_t)tb * d + j) * (size_t)g.pz * ncol;
+  double* out = incoming + ((size_t)tboxes[tb] * d + j) * (size_t)(p * pp);
+  const int ngroups = (p + 3) / 4;
+  for (int grp = 0; grp < ngroups; ++grp) {
+    __syncthreads();
+    for (int e = tid; e < 4 * ncol; e += blockDim.x) {  // scatter the in-band columns into dense D
+      const int s = e / ncol, c = e % ncol, iz = grp * 4 + s;
+      const double2 v = iz < p ? Ci[(size_t)iz * ncol + c] : make_double2(0.0, 0.0);
+      double* row = D + (s * NY8 + g.col_my[c] + M) * SD + 2 * g.col_m0[c];
+      row[0] = v.x;
+      row[1] = v.y;
+    }
+    __syncthreads();
+    // Y stage: d[(s,iy), m0] = sum_{(my,part)} A'[iy][(my,part)] D[s][my][(m0,part)]
+    const int nit = PT, nm0 = M18 / 8;
+    for (int tile = warp; tile < 4 * nit * nm0; tile += kW) {
+      const int s = tile / (nit * nm0), it = (tile / nm0) % nit, nt = tile % nm0;
+      double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
+      const int ksteps = NY8 / 2;  // K' = 2*NY8, 4 per step
+      for (int ks = 0; ks < ksteps; ++ks) {
+        const int kk = ks * 4 + t, my = kk >> 1, part = kk & 1;
+        const double bv = D[(s * NY8 + my) * SD + 2 * (nt * 8 + gq) + part];
+        dmma(cr0, cr1, Ar[(it * 8 + gq) * SA + kk], bv);
+        dmma(ci0, ci1, Ai[(it * 8 + gq) * SA + kk], bv);
+      }
+      const int r = s * P8 + it * 8 + gq;
+      const int cbase = 2 * (nt * 8 + 2 * t);
+      dd[r * SX + cbase] = cr0;
+      dd[r * SX + cbase + 1] = ci0;
+      dd[r * SX + cbase + 2] = cr1;
+      dd[r * SX + cbase + 3] = ci1;
+    }
+    __syncthreads();
+    // X stage: out[(s,iy), ix] += pf * sum_{(m0,part)} dd[(s,iy)][(m0,part)] EXw[ix][(m0,part)]
+    const int xt = 4 * PT * PT;
+    for (int tile = warp; tile < xt; tile += kW) {
+      const int mt = tile / PT, nt = tile % PT;
+      double c0 = 0.0, c1 = 0.0;
+      for (int ks = 0; ks < NX8 / 4; ++ks)
+        dmma(c0, c1, dd[(mt * 8 + gq) * SX + ks * 4 + t], EXw[(nt * 8 + gq) * SX + ks * 4 + t]);
+      const int s = mt / PT, iy = (mt % PT) * 8 + gq, iz = grp * 4 + s, ix = nt * 8 + 2 * t;
+      if (iz < p && iy < p) {
+        double* o = out + (size_t)iz * pp + iy * p;
+        if (ix < p) o[ix] += pf * c0;
+        if (ix + 1 < p) o[ix + 1] += pf * c1;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < 4 * ncol; e += blockDim.x) {  // clear the scattered entries for the next group
+      const int s = e / ncol, c = e % ncol;
+      double* row = D + (s * NY8 + g.col_my[c] + M) * SD + 2 * g.col_m0[c];
+      row[0] = 0.0;
+      row[1] = 0.0;
+    }
+  }
+}
+
+void attr(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+}  // namespace
+
+bool pw_mma_supported(const PWGrid& g) {
+  return g.dim == 3 && g.p <= 32 && g.N <= 48 && g.pz == g.p;
+}
+
+void launch_forward_mma(const PWGrid& g, const int* boxes, int nbox, int nch, const double* outgoing, double2* B,
+                        double2* G, cudaStream_t st) {
+  if (nbox <= 0) return;
+  const int PT = (g.p + 7) / 8 <= 3 ? 3 : 4;  // the instantiated template sizes
+  const int M1 = g.M + 1, NX8 = (2 * M1 + 7) / 8 * 8, NY8 = (g.N + 7) / 8 * 8;
+  {
+    const int M18 = (M1 + 7) / 8 * 8;
+    const int P8 = PT * 8, SE = P8 + 4, SY = r4(2 * P8), SAa = r8(NX8 > 2 * M18 ? NX8 : 2 * M18);
+    size_t smem = sizeof(double) * ((size_t)NX8 * SE + 2 * (size_t)NY8 * SY + 2 * 4 * (size_t)P8 * SE +
+                                    4 * (size_t)P8 * SAa) + sizeof(int) * (size_t)g.N * M1;
+    dim3 grid(nbox, nch);
+    if (PT <= 3) {
+      attr((const void*)k_fwd_xy_mma<3>, smem);
+      k_fwd_xy_mma<3><<<grid, kW * 32, smem, st>>>(g, boxes, nch, outgoing, B);
+    } else {
+      attr((const void*)k_fwd_xy_mma<4>, smem);
+      k_fwd_xy_mma<4><<<grid, kW * 32, smem, st>>>(g, boxes, nch, outgoing, B);
+    }
+  }
+  {
+    const int KT = PT, RT = (g.Nz + 7) / 8 <= 5 ? 5 : 6;
+    const int K8 = KT * 8, SK = 2 * K8 + 4, SI = (2 * kCB) % 16 == 8 ? 2 * kCB : 2 * kCB + 8;
+    size_t smem = sizeof(double) * (2 * (size_t)RT * 8 * SK + (size_t)K8 * SI);
+    dim3 grid(nbox, nch, (g.ncol + kCB - 1) / kCB);
+#define ZF(KT_, RT_)                                                                  \
+  do {                                                                                \
+    attr((const void*)k_z_mma<KT_, RT_, false>, smem);                                \
+    k_z_mma<KT_, RT_, false><<<grid, kW * 32, smem, st>>>(g, nch, B, G);              \
+  } while (0)
+    if (KT <= 3) {
+      if (RT <= 5) ZF(3, 5); else ZF(3, 6);
+    } else {
+      if (RT <= 5) ZF(4, 5); else ZF(4, 6);
+    }
+#undef ZF
+  }
+}
+
+void launch_inverse_mma(const PWGrid& g, const int* tboxes, int ntb, int d, const double2* F, double2* C, double pf,
+                        double* incoming, cudaStream_t st) {
+  if (ntb <= 0) return;
+  const int PT = (g.p + 7) / 8 <= 3 ? 3 : 4;  // the instantiated template sizes
+  {
+    const int KT = (g.Nz + 7) / 8 <= 5 ? 5 : 6, RT = PT;
+    const int K8 = KT * 8, SK = 2 * K8 + 4, SI = (2 * kCB) % 16 == 8 ? 2 * kCB : 2 * kCB + 8;
+    size_t smem = sizeof(double) * (2 * (size_t)RT * 8 * SK + (size_t)K8 * SI);
+    dim3 grid(ntb, d, (g.ncol + kCB - 1) / kCB);
+#define ZI(KT_, RT_)                                                                  \
+  do {                                                                                \
+    attr((const void*)k_z_mma<KT_, RT_, true>, smem);                                 \
+    k_z_mma<KT_, RT_, true><<<grid, kW * 32, smem, st>>>(g, d, F, C);                 \
+  } while (0)
+    if (RT <= 3) {
+      if (KT <= 5) ZI(5, 3); else ZI(6, 3);
+    } else {
+      if (KT <= 5) ZI(5, 4); else ZI(6, 4);
+    }
+#undef ZI
+  }
+  {
+    const int P8 = PT * 8, M1 = g.M + 1, NY8 = (g.N + 7) / 8 * 8, M18 = (M1 + 7) / 8 * 8;
+    const int NX8 = (2 * M1 + 7) / 8 * 8, SD = r8(2 * M18), SA = r4(2 * NY8), SX = r4(NX8 > 2 * M18 ? NX8 : 2 * M18);
+    size_t smem = sizeof(double) * (2 * (size_t)P8 * SA + (size_t)P8 * SX + 4 * (size_t)NY8 * SD + 4 * (size_t)P8 * SX);
+    dim3 grid(ntb, d);
+    if (PT <= 3) {
+      attr((const void*)k_inv_xy_mma<3>, smem);
+      k_inv_xy_mma<3><<<grid, kW * 32, smem, st>>>(g, tboxes, d, C, pf, incoming);
+    } else {
+      attr((const void*)k_inv_xy_mma<4>, smem);
+      k_inv_xy_mma<4><<<grid, kW * 32, smem, st>>>(g, tboxes, d, C, pf, incoming);
+    }
+  }
+}
+
+}  // namespace sdmkb
