@@ -3,7 +3,10 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 
@@ -53,6 +56,11 @@ std::vector<double> transpose(const std::vector<double>& M, int p) {
   for (int i = 0; i < p; ++i)
     for (int j = 0; j < p; ++j) T[(size_t)j * p + i] = M[(size_t)i * p + j];
   return T;
+}
+
+bool timing_on() {
+  static const bool on = std::getenv("SDMK_TIMING") != nullptr;
+  return on;
 }
 
 // band limit in mode-index units, squared (dmk.cpp:472-477)
@@ -365,13 +373,22 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode) {
     cuda_check(cudaMemcpyAsync(hq + (size_t)ns * d, tq, sizeof(int32_t) * (size_t)nt * d, cudaMemcpyDeviceToHost, st_),
                "D2H q");
   cuda_check(cudaMemcpyAsync(hflags, flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H flags");
+  const auto w0 = std::chrono::steady_clock::now();
   sync();
+  const auto w1 = std::chrono::steady_clock::now();
   if (hflags[2]) throw InvalidArgument("ParticleSystem: non-finite strength");
   if (hflags[0]) throw InvalidArgument("ParticleSystem: non-finite coordinate");
   if (hflags[1]) throw InvalidArgument("ParticleSystem: coordinate outside the unit box");
   pr.tree = build_topology(d, pr.periodic, P.n_s, P.p, ns, hq, pr.alias ? 0 : nt,
                            pr.alias ? nullptr : hq + (size_t)ns * d);
+  const auto w2 = std::chrono::steady_clock::now();
   upload_tree_lists();
+  const auto w3 = std::chrono::steady_clock::now();
+  if (timing_on()) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[sdmk timing] sort+D2H wait %.2f ms, host topology %.2f ms, lists+upload %.2f ms (%d boxes)\n",
+                 ms(w0, w1), ms(w1, w2), ms(w2, w3), pr.tree.num_boxes());
+  }
   pr.ready = true;
 }
 
@@ -380,6 +397,7 @@ void Context::upload_tree_lists() {
   const HostTree& t = pr.tree;
   const int nb = t.num_boxes(), d = pr.dim, nchild = 1 << d;
   std::vector<dev::DBox> boxes(nb);
+#pragma omp parallel for schedule(static)
   for (int b = 0; b < nb; ++b) {
     const Box& x = t.boxes[b];
     dev::DBox& o = boxes[b];
@@ -398,20 +416,22 @@ void Context::upload_tree_lists() {
     o.side = t.side(b);
     o.half = 0.5 * o.side;
   }
-  std::vector<int> ant, itp, rs(1, 0), rbox, rinfo;
+  std::vector<int> ant, itp;
   for (int b = 0; b < nb; ++b) {
     if (t.boxes[b].leaf && t.nsrc(b) > 0) ant.push_back(b);
     if (t.boxes[b].leaf && t.ntgt(b) > 0) itp.push_back(b);
   }
-  // near ranges per target leaf (dmk.cpp:966-990)
+  // near ranges per target leaf (dmk.cpp:966-990); two-pass CSR, parallel over leaves
   auto scode = [](const int8_t* s) { return (s[0] + 1) + 3 * (s[1] + 1) + 9 * (s[2] + 1); };
-  int max_ranges = 0;
-  for (int b : itp) {
-    int before = (int)rbox.size();
+  auto ranges = [&](int b, int* obox, int* oinfo) {
+    int n = 0;
     auto add = [&](int sbx, const int8_t* sh, bool fine_scale, bool self) {
       if (t.nsrc(sbx) == 0) return;
-      rbox.push_back(sbx);
-      rinfo.push_back(scode(sh) | (fine_scale ? 32 : 0) | (self ? 64 : 0));
+      if (obox) {
+        obox[n] = sbx;
+        oinfo[n] = scode(sh) | (fine_scale ? 32 : 0) | (self ? 64 : 0);
+      }
+      ++n;
     };
     const int8_t zero[3] = {0, 0, 0};
     add(b, zero, false, true);
@@ -422,10 +442,21 @@ void Context::upload_tree_lists() {
     }
     for (const Nbr& e : t.crs[b]) add(e.box, e.shift, false, false);
     for (const Nbr& e : t.fin[b]) add(e.box, e.shift, true, false);
-    rs.push_back((int)rbox.size());
-    max_ranges = std::max(max_ranges, (int)rbox.size() - before);
+    return n;
+  };
+  const int nitp = (int)itp.size();
+  std::vector<int> rs(nitp + 1, 0);
+  int max_ranges = 0;
+#pragma omp parallel for schedule(static) reduction(max : max_ranges)
+  for (int i = 0; i < nitp; ++i) {
+    rs[i + 1] = ranges(itp[i], nullptr, nullptr);
+    max_ranges = std::max(max_ranges, rs[i + 1]);
   }
   if (max_ranges > 160) throw RuntimeError("residual pass: more than 160 near ranges for one leaf");
+  for (int i = 0; i < nitp; ++i) rs[i + 1] += rs[i];
+  std::vector<int> rbox(rs[nitp]), rinfo(rs[nitp]);
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < nitp; ++i) ranges(itp[i], rbox.data() + rs[i], rinfo.data() + rs[i]);
   // per-level lists
   const int L = t.max_level + 1;
   struct LV {
@@ -433,6 +464,7 @@ void Context::upload_tree_lists() {
   };
   std::vector<LV> lv(L);
   std::vector<int> gslot(nb, -1);
+  bool bad_tau = false;
   for (int lev = 0; lev < L; ++lev) {
     LV& V = lv[lev];
     for (int b : t.level_boxes[lev]) {
@@ -458,32 +490,55 @@ void Context::upload_tree_lists() {
         V.sbx.push_back(b);
       }
     }
-    // plane-wave targets and their colleague entries (dmk.cpp:760-797)
+    // plane-wave targets and their colleague entries (dmk.cpp:760-797); two-pass, parallel
     const int64_t side_int = int64_t(1) << (30 - lev);
-    V.es.push_back(0);
-    for (int b : t.level_boxes[lev]) {
-      if (t.ntgt(b) == 0) continue;
+    const std::vector<int>& ids = t.level_boxes[lev];
+    const int nl = (int)ids.size();
+    auto entries = [&](int b, int* oslot, int* otau) {
+      if (t.ntgt(b) == 0) return 0;
       int cnt = 0;
       for (const Nbr& ce : t.col[b]) {
         if (t.boxes[b].leaf && ce.box == b && !ce.shift[0] && !ce.shift[1] && !ce.shift[2]) continue;
         if (t.nsrc(ce.box) == 0) continue;
-        int tau[3] = {0, 0, 0};
-        for (int ax = 0; ax < d; ++ax) {
-          int64_t diff = int64_t(t.boxes[ce.box].anchor[ax]) + (int64_t(ce.shift[ax]) << 30) -
-                         int64_t(t.boxes[b].anchor[ax]);
-          tau[ax] = int(diff / side_int);
-          if (tau[ax] < -1 || tau[ax] > 1) throw RuntimeError("colleague offset outside {-1,0,1}");
+        if (oslot) {
+          int tau[3] = {0, 0, 0};
+          for (int ax = 0; ax < d; ++ax) {
+            int64_t diff = int64_t(t.boxes[ce.box].anchor[ax]) + (int64_t(ce.shift[ax]) << 30) -
+                           int64_t(t.boxes[b].anchor[ax]);
+            tau[ax] = int(diff / side_int);
+            if (tau[ax] < -1 || tau[ax] > 1) bad_tau = true;
+          }
+          oslot[cnt] = gslot[ce.box];
+          otau[cnt] = (tau[0] + 1) + 3 * (tau[1] + 1) + 9 * (tau[2] + 1);
         }
-        V.eslot.push_back(gslot[ce.box]);
-        V.etau.push_back((tau[0] + 1) + 3 * (tau[1] + 1) + 9 * (tau[2] + 1));
         ++cnt;
       }
-      if (cnt == 0) continue;
-      if (cnt > 64) throw RuntimeError("plane-wave pass: more than 64 colleague entries");
-      V.tbx.push_back(b);
-      V.es.push_back((int)V.eslot.size());
+      return cnt;
+    };
+    std::vector<int> cnt(nl);
+    int max_e = 0;
+#pragma omp parallel for schedule(static) reduction(max : max_e)
+    for (int i = 0; i < nl; ++i) {
+      cnt[i] = entries(ids[i], nullptr, nullptr);
+      max_e = std::max(max_e, cnt[i]);
     }
+    if (max_e > 64) throw RuntimeError("plane-wave pass: more than 64 colleague entries");
+    std::vector<int> eoff(nl + 1, 0);
+    V.es.push_back(0);
+    for (int i = 0; i < nl; ++i) {
+      eoff[i + 1] = eoff[i] + cnt[i];
+      if (cnt[i] > 0) {
+        V.tbx.push_back(ids[i]);
+        V.es.push_back(eoff[i + 1]);
+      }
+    }
+    V.eslot.resize(eoff[nl]);
+    V.etau.resize(eoff[nl]);
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < nl; ++i)
+      if (cnt[i] > 0) entries(ids[i], V.eslot.data() + eoff[i], V.etau.data() + eoff[i]);
   }
+  if (bad_tau) throw RuntimeError("colleague offset outside {-1,0,1}");
   // root lists: box 0 with one zero-offset entry
   std::vector<int> root_ids = {0}, root_es = {0, 1}, root_slot = {0}, root_tau = {13};
   Packer pk;
@@ -732,14 +787,26 @@ void Context::run_residual(double* ures, bool stats) {  // dmk.cpp:919-1032
   } else {
     co = &T.w_offd;
   }
-  if ((cd && cd->a.size() > 128) || co->a.size() > 128) throw RuntimeError("residual table longer than 128 coefficients");
   if (cd && (cd->lo != co->lo || cd->hi != co->hi)) throw RuntimeError("residual tables on different intervals");
-  ResidTables rt{cd ? (int)cd->a.size() : 0, (int)co->a.size(), co->lo, co->hi, T.support, pr.plan.kernel, pr.dim};
-  double* hc = (double*)pinned_.get("rtab", 256 * sizeof(double));
-  std::fill(hc, hc + 256, 0.0);
-  if (cd) std::copy(cd->a.begin(), cd->a.end(), hc);
-  std::copy(co->a.begin(), co->a.end(), hc + 128);
-  set_residual_tables(hc, rt.nd, hc + 128, rt.no, st_);
+  // piecewise re-expansion of the radial tables (same values to ~1e-15; see setup.hpp)
+  PiecewisePoly po = piecewise_from_cheb(*co), pd;
+  if (cd) {
+    pd = piecewise_from_cheb(*cd);
+    if (pd.deg != po.deg) {
+      const int deg = std::max(pd.deg, po.deg);
+      pd = piecewise_from_cheb(*cd, 32, deg);
+      po = piecewise_from_cheb(*co, 32, deg);
+    }
+  }
+  const int npw = po.ni * (po.deg + 1);
+  if (npw > residual_max_pw()) throw RuntimeError("residual table re-expansion too large");
+  double* hc = (double*)pinned_.get("rtab", 2 * npw * sizeof(double));
+  std::copy(po.c.begin(), po.c.end(), hc + npw);
+  if (cd) std::copy(pd.c.begin(), pd.c.end(), hc);
+  else std::fill(hc, hc + npw, 0.0);
+  double* dc = arena_.as<double>("rtab", 2 * npw);
+  cuda_check(cudaMemcpyAsync(dc, hc, 2 * npw * sizeof(double), cudaMemcpyHostToDevice, st_), "table upload");
+  ResidTables rt{po.ni, po.deg, co->lo, co->hi, T.support, pr.plan.kernel, pr.dim, dc, dc + npw};
   int* flags = arena_.as<int>("flags", 8);
   unsigned long long* st = arena_.as<unsigned long long>("stats", 4);
   if (stats) cuda_check(cudaMemsetAsync(st, 0, 4 * sizeof(unsigned long long), st_), "memset");

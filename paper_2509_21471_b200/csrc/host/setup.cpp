@@ -691,6 +691,66 @@ double Cheb::eval(double x) const {  // Clenshaw (chebyshev.cpp:9-19)
   return t * b1 - b2 + a[0];
 }
 
+PiecewisePoly piecewise_from_cheb(const Cheb& t, int ni, int min_deg) {
+  PiecewisePoly P;
+  P.ni = ni;
+  P.lo = t.lo;
+  P.hi = t.hi;
+  if (t.a.empty()) {
+    P.deg = min_deg;
+    P.c.assign((size_t)ni * (min_deg + 1), 0.0);
+    return P;
+  }
+  double fmax = 0.0;
+  for (int j = 0; j <= 4096; ++j) fmax = std::max(fmax, std::fabs(t.eval(t.lo + (t.hi - t.lo) * j / 4096.0)));
+  const double tol = 4e-15 * std::max(1.0, fmax);
+  for (int deg : {8, 10, 12, 14, 16, 20, 24}) {
+    if (deg < min_deg) continue;
+    const int n = deg + 1;
+    std::vector<double> c((size_t)ni * n, 0.0);
+    double worst = 0.0;
+    for (int i = 0; i < ni; ++i) {
+      const double a = t.lo + (t.hi - t.lo) * i / ni, b = t.lo + (t.hi - t.lo) * (i + 1) / ni;
+      // Chebyshev interpolation coefficients on [a, b]
+      std::vector<double> fv(n), ch(n, 0.0);
+      for (int j = 0; j < n; ++j) fv[j] = t.eval(0.5 * (a + b) + 0.5 * (b - a) * std::cos(M_PI * (2 * j + 1) / (2.0 * n)));
+      for (int k = 0; k < n; ++k) {
+        double s = 0.0;
+        for (int j = 0; j < n; ++j) s += fv[j] * std::cos(k * M_PI * (2 * j + 1) / (2.0 * n));
+        ch[k] = s * (k == 0 ? 1.0 : 2.0) / n;
+      }
+      // Chebyshev -> monomial: T_{k+1} = 2u T_k - T_{k-1}
+      std::vector<double> Tk0(n, 0.0), Tk1(n, 0.0), Tk2(n, 0.0);
+      double* mono = c.data() + (size_t)i * n;
+      Tk0[0] = 1.0;
+      for (int j = 0; j < n; ++j) mono[j] += ch[0] * Tk0[j];
+      if (n > 1) {
+        Tk1[1] = 1.0;
+        for (int j = 0; j < n; ++j) mono[j] += ch[1] * Tk1[j];
+      }
+      for (int k = 2; k < n; ++k) {
+        for (int j = 0; j < n; ++j) Tk2[j] = (j ? 2.0 * Tk1[j - 1] : 0.0) - Tk0[j];
+        for (int j = 0; j < n; ++j) mono[j] += ch[k] * Tk2[j];
+        Tk0 = Tk1;
+        Tk1 = Tk2;
+      }
+      for (int j = 0; j <= 64; ++j) {  // check with the same Horner the kernel uses
+        const double u = -1.0 + 2.0 * j / 64.0, x = 0.5 * (a + b) + 0.5 * (b - a) * u;
+        double v = mono[deg];
+        for (int k = deg - 1; k >= 0; --k) v = std::fma(v, u, mono[k]);
+        worst = std::max(worst, std::fabs(v - t.eval(x)));
+      }
+    }
+    if (worst <= tol || deg == 24) {
+      P.deg = deg;
+      P.c = c;
+      P.max_err = worst;
+      return P;
+    }
+  }
+  return P;
+}
+
 // Residual tables: closed forms in phi / Phi in 3D (split.cpp:319-381), the
 // Fourier quadrature pipeline in 2D (split.cpp:383-395, split2d.cpp:263-326).
 Tables build_tables(int kernel, int dim, const WindowFn& win, double tol) {

@@ -86,6 +86,19 @@ struct Tables {
   Cheb s_diag, s_offd, t_diag, t_offd, w_offd, b_res, phi;
 };
 
+// Piecewise monomial re-expansion of a Chebyshev table for the GPU residual
+// kernel: ni equal sub-intervals of [lo, hi], degree deg in the local
+// variable u in [-1, 1]; c[i * (deg + 1) + k] multiplies u^k.  Built by
+// interpolating the table at Chebyshev points of each sub-interval and
+// accepted only if it reproduces the table's Clenshaw value to
+// 4e-15 * max(1, |f|) on a dense check grid (else the degree grows).
+struct PiecewisePoly {
+  int ni = 0, deg = 0;
+  double lo = 0.0, hi = 1.0, max_err = 0.0;
+  std::vector<double> c;
+};
+PiecewisePoly piecewise_from_cheb(const Cheb& t, int ni = 32, int min_deg = 8);
+
 Tables build_tables(int kernel, int dim, const WindowFn& win, double tol);
 // tables exactly as evaluate_with_plan builds them when none are supplied
 Tables tables_for_plan(const Plan& plan);

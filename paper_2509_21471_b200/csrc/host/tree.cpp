@@ -1,8 +1,14 @@
 #include "tree.hpp"
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <sstream>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 namespace sdmkb {
 
@@ -39,20 +45,14 @@ struct Builder {
     bnd[nchild] = hi;
   }
 
-  void subdivide(int b) {  // tree.cpp:62-99
-    int lev = t.boxes[b].level;
-    int32_t half = int32_t(1) << (kMaxLevel - 1 - lev);
-    int fc = t.num_boxes();
+  // children of box `par` (ranges from the bnd arrays), appended at ids fc..fc+2^d-1
+  void make_children(int b, const int* sb, const int* tb) {  // tree.cpp:62-99
+    const int lev = t.boxes[b].level;
+    const int32_t half = int32_t(1) << (kMaxLevel - 1 - lev);
     t.boxes[b].leaf = false;
-    t.boxes[b].first_child = fc;
+    t.boxes[b].first_child = t.num_boxes();
     if (lev + 1 > t.max_level) t.max_level = lev + 1;
-    int sb[9], tb[9];
-    split_range(S, t.boxes[b].sb, t.boxes[b].se, lev, sb);
-    if (t.alias)
-      for (int i = 0; i <= nchild; ++i) tb[i] = sb[i];
-    else
-      split_range(T, t.boxes[b].tb, t.boxes[b].te, lev, tb);
-    Box par = t.boxes[b];
+    const Box par = t.boxes[b];
     for (int ci = 0; ci < nchild; ++ci) {
       Box c;
       c.level = lev + 1;
@@ -66,6 +66,16 @@ struct Builder {
     }
   }
 
+  void subdivide(int b) {
+    int sb[9], tb[9];
+    split_range(S, t.boxes[b].sb, t.boxes[b].se, t.boxes[b].level, sb);
+    if (t.alias)
+      for (int i = 0; i <= nchild; ++i) tb[i] = sb[i];
+    else
+      split_range(T, t.boxes[b].tb, t.boxes[b].te, t.boxes[b].level, tb);
+    make_children(b, sb, tb);
+  }
+
   int descend(const int32_t* probe) const {  // tree.cpp:102-107
     int b = 0;
     while (!t.boxes[b].leaf) {
@@ -76,38 +86,138 @@ struct Builder {
     return b;
   }
 
-  void refine() {  // tree.cpp:109-123 (DFS pre-order allocation)
+  // refine_to_capacity (tree.cpp:109-123).  The set of subdivided boxes
+  // depends only on counts; build it breadth first with parallel searches,
+  // then allocate ids in the reference's DFS pre-order.
+  void refine() {
+    struct Node {
+      Box box;
+      int kids = -1;  // index of first child in `nodes` (BFS order)
+      int sb[9], tb[9];
+    };
+    std::vector<Node> nodes(1);
+    nodes[0].box = t.boxes[0];
+    std::vector<int> cur(1, 0);
+    bool capped = false;
+    while (!cur.empty()) {
+      const int nc = (int)cur.size();
+      std::vector<char> split(nc, 0);
+#pragma omp parallel for schedule(dynamic, 16) reduction(|| : capped)
+      for (int i = 0; i < nc; ++i) {
+        Node& nd = nodes[cur[i]];
+        if (nd.box.se - nd.box.sb <= t.n_s) continue;
+        if (nd.box.level >= kMaxLevel) {
+          capped = true;
+          continue;
+        }
+        split[i] = 1;
+        split_range(S, nd.box.sb, nd.box.se, nd.box.level, nd.sb);
+        if (t.alias)
+          for (int k = 0; k <= nchild; ++k) nd.tb[k] = nd.sb[k];
+        else
+          split_range(T, nd.box.tb, nd.box.te, nd.box.level, nd.tb);
+      }
+      std::vector<int> next;
+      for (int i = 0; i < nc; ++i) {
+        if (!split[i]) continue;
+        const int id = cur[i];
+        const int first = (int)nodes.size();
+        nodes[id].kids = first;
+        const Box par = nodes[id].box;
+        const int32_t half = int32_t(1) << (kMaxLevel - 1 - par.level);
+        for (int ci = 0; ci < nchild; ++ci) {
+          Node c;
+          c.box.level = par.level + 1;
+          for (int a = 0; a < t.dim; ++a) c.box.anchor[a] = par.anchor[a] + ((ci >> a) & 1) * half;
+          c.box.sb = nodes[id].sb[ci];
+          c.box.se = nodes[id].sb[ci + 1];
+          c.box.tb = nodes[id].tb[ci];
+          c.box.te = nodes[id].tb[ci + 1];
+          nodes.push_back(c);
+          next.push_back(first + ci);
+        }
+      }
+      cur.swap(next);
+    }
+    t.depth_capped = capped;
+    // DFS pre-order id allocation (stack pop order as in tree.cpp:110-122)
+    std::vector<int> final_id(nodes.size(), -1);
+    t.boxes.assign(1, nodes[0].box);
+    final_id[0] = 0;
     std::vector<int> stack(1, 0);
     while (!stack.empty()) {
-      int b = stack.back();
+      const int n = stack.back();
       stack.pop_back();
-      if (t.nsrc(b) <= t.n_s) continue;
-      if (t.boxes[b].level >= kMaxLevel) {
-        t.depth_capped = true;
-        continue;
+      if (nodes[n].kids < 0) continue;
+      const int b = final_id[n];
+      const int fc = t.num_boxes();
+      t.boxes[b].leaf = false;
+      t.boxes[b].first_child = fc;
+      t.max_level = std::max(t.max_level, t.boxes[b].level + 1);
+      for (int ci = 0; ci < nchild; ++ci) {
+        Box c = nodes[nodes[n].kids + ci].box;
+        c.parent = b;
+        t.boxes.push_back(c);
+        final_id[nodes[n].kids + ci] = fc + ci;
       }
-      subdivide(b);
-      for (int ci = nchild - 1; ci >= 0; --ci) stack.push_back(t.boxes[b].first_child + ci);
+      for (int ci = nchild - 1; ci >= 0; --ci) stack.push_back(nodes[n].kids + ci);
     }
   }
 
-  void repair() {  // tree.cpp:125-165 (sweeps until no leaf is 2 levels coarser than a neighbour)
+  // does any of the 3^d - 1 probes of leaf b land in a leaf >= 2 levels coarser?
+  bool probe_triggers(int b, int* first_off) const {
+    const int lev = t.boxes[b].level;
+    if (lev < 2) return false;
+    const int64_t side = kCells >> lev;
+    const int zr = t.dim == 3 ? 1 : 0;
+    int k = 0;
+    for (int o2 = -zr; o2 <= zr; ++o2)
+      for (int o1 = -1; o1 <= 1; ++o1)
+        for (int o0 = -1; o0 <= 1; ++o0, ++k) {
+          if (!o0 && !o1 && !o2) continue;
+          const int off[3] = {o0, o1, o2};
+          int32_t probe[3] = {0, 0, 0};
+          bool inside = true;
+          for (int a = 0; a < t.dim && inside; ++a) {
+            int64_t v = t.boxes[b].anchor[a] + off[a] * side + side / 2;
+            if (t.periodic)
+              v = ((v % kCells) + kCells) % kCells;
+            else if (v < 0 || v >= kCells)
+              inside = false;
+            probe[a] = int32_t(v);
+          }
+          if (!inside) continue;
+          const int a = descend(probe);
+          if (t.boxes[a].leaf && t.boxes[a].level <= lev - 2) {
+            if (first_off) *first_off = k;
+            return true;
+          }
+        }
+    return false;
+  }
+
+  void repair() {  // tree.cpp:125-165
     for (bool again = true; again;) {
       again = false;
       std::vector<int> leaves;
       for (int b = 0; b < t.num_boxes(); ++b)
         if (t.boxes[b].leaf) leaves.push_back(b);
-      for (int b : leaves) {
+      const int nl = (int)leaves.size();
+      std::vector<char> cand(nl, 0);
+#pragma omp parallel for schedule(dynamic, 64)
+      for (int i = 0; i < nl; ++i) cand[i] = probe_triggers(leaves[i], nullptr);
+      for (int i = 0; i < nl; ++i) {
+        if (!cand[i]) continue;  // cannot trigger: later subdivisions only refine
+        const int b = leaves[i];
         if (!t.boxes[b].leaf) continue;
-        int lev = t.boxes[b].level;
-        if (lev < 2) continue;
-        int64_t side = kCells >> lev;
-        int zr = t.dim == 3 ? 1 : 0;
+        const int lev = t.boxes[b].level;
+        const int64_t side = kCells >> lev;
+        const int zr = t.dim == 3 ? 1 : 0;
         for (int o2 = -zr; o2 <= zr; ++o2)
           for (int o1 = -1; o1 <= 1; ++o1)
             for (int o0 = -1; o0 <= 1; ++o0) {
               if (!o0 && !o1 && !o2) continue;
-              int off[3] = {o0, o1, o2};
+              const int off[3] = {o0, o1, o2};
               int32_t probe[3] = {0, 0, 0};
               bool inside = true;
               for (int a = 0; a < t.dim && inside; ++a) {
@@ -119,7 +229,7 @@ struct Builder {
                 probe[a] = int32_t(v);
               }
               if (!inside) continue;
-              int a = descend(probe);
+              const int a = descend(probe);
               if (t.boxes[a].leaf && t.boxes[a].level <= lev - 2) {
                 subdivide(a);
                 again = true;
@@ -138,44 +248,104 @@ struct Builder {
     return true;
   }
 
+  // two-pass CSR fill over `ids`: count(b) then emit(b, out)
+  template <class Count, class Emit>
+  void csr_pass(Csr& L, const std::vector<int>& ids, Count count, Emit emit) {
+    const int n = (int)ids.size();
+    std::vector<int> cnt(n);
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int i = 0; i < n; ++i) cnt[i] = count(ids[i]);
+    int64_t base = (int64_t)L.v.size();
+    std::vector<int64_t> off(n);
+    for (int i = 0; i < n; ++i) {
+      off[i] = base;
+      base += cnt[i];
+    }
+    L.v.resize(base);
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int i = 0; i < n; ++i) {
+      L.off[ids[i]] = off[i];
+      L.len[ids[i]] = cnt[i];
+      emit(ids[i], L.v.data() + off[i]);
+    }
+  }
+
   void neighbours() {  // tree.cpp:167-212
-    int nb = t.num_boxes();
-    t.col.assign(nb, {});
-    t.crs.assign(nb, {});
-    t.fin.assign(nb, {});
+    const int nb = t.num_boxes();
+    for (Csr* L : {&t.col, &t.crs, &t.fin}) {
+      L->off.assign(nb, 0);
+      L->len.assign(nb, 0);
+      L->v.clear();
+    }
     t.level_boxes.assign(t.max_level + 1, {});
     for (int b = 0; b < nb; ++b) t.level_boxes[t.boxes[b].level].push_back(b);
+    std::vector<Nbr> root;
     if (t.periodic) {
-      int zr = t.dim == 3 ? 1 : 0;
+      const int zr = t.dim == 3 ? 1 : 0;
       for (int s2 = -zr; s2 <= zr; ++s2)
         for (int s1 = -1; s1 <= 1; ++s1)
-          for (int s0 = -1; s0 <= 1; ++s0) t.col[0].push_back({0, {int8_t(s0), int8_t(s1), int8_t(s2)}});
+          for (int s0 = -1; s0 <= 1; ++s0) root.push_back({0, {int8_t(s0), int8_t(s1), int8_t(s2)}});
     } else {
-      t.col[0].push_back({0, {0, 0, 0}});
+      root.push_back({0, {0, 0, 0}});
     }
-    for (int lev = 1; lev <= t.max_level; ++lev)
-      for (int b : t.level_boxes[lev]) {
-        int par = t.boxes[b].parent;
-        for (const Nbr& pc : t.col[par]) {
-          if (t.boxes[pc.box].leaf) {
-            if (touch(b, pc.box, pc.shift)) t.crs[b].push_back(pc);
-            continue;
-          }
-          for (int ci = 0; ci < nchild; ++ci) {
-            int d = t.boxes[pc.box].first_child + ci;
-            if (touch(b, d, pc.shift)) t.col[b].push_back({d, {pc.shift[0], pc.shift[1], pc.shift[2]}});
-          }
-        }
-      }
-    for (int b = 0; b < nb; ++b)
+    t.col.off[0] = 0;
+    t.col.len[0] = (int)root.size();
+    t.col.v = root;
+    for (int lev = 1; lev <= t.max_level; ++lev) {
+      const std::vector<int>& ids = t.level_boxes[lev];
+      // colleagues: children of the parent's non-leaf colleagues that touch b
+      csr_pass(
+          t.col, ids,
+          [&](int b) {
+            int c = 0;
+            for (const Nbr& pc : t.col[t.boxes[b].parent]) {
+              if (t.boxes[pc.box].leaf) continue;
+              for (int ci = 0; ci < nchild; ++ci) c += touch(b, t.boxes[pc.box].first_child + ci, pc.shift);
+            }
+            return c;
+          },
+          [&](int b, Nbr* out) {
+            for (const Nbr& pc : t.col[t.boxes[b].parent]) {
+              if (t.boxes[pc.box].leaf) continue;
+              for (int ci = 0; ci < nchild; ++ci) {
+                const int d = t.boxes[pc.box].first_child + ci;
+                if (touch(b, d, pc.shift)) *out++ = {d, {pc.shift[0], pc.shift[1], pc.shift[2]}};
+              }
+            }
+          });
+      // coarse: the parent's leaf colleagues that touch b
+      csr_pass(
+          t.crs, ids,
+          [&](int b) {
+            int c = 0;
+            for (const Nbr& pc : t.col[t.boxes[b].parent])
+              if (t.boxes[pc.box].leaf) c += touch(b, pc.box, pc.shift);
+            return c;
+          },
+          [&](int b, Nbr* out) {
+            for (const Nbr& pc : t.col[t.boxes[b].parent])
+              if (t.boxes[pc.box].leaf && touch(b, pc.box, pc.shift)) *out++ = pc;
+          });
+    }
+    // fine: leaf children of non-leaf colleagues (other than self) that touch b
+    std::vector<int> all(nb);
+    for (int b = 0; b < nb; ++b) all[b] = b;
+    auto fine_scan = [&](int b, Nbr* out) {
+      int c = 0;
       for (const Nbr& ce : t.col[b]) {
         if (ce.box == b && !ce.shift[0] && !ce.shift[1] && !ce.shift[2]) continue;
         if (t.boxes[ce.box].leaf) continue;
         for (int ci = 0; ci < nchild; ++ci) {
-          int d = t.boxes[ce.box].first_child + ci;
-          if (t.boxes[d].leaf && touch(b, d, ce.shift)) t.fin[b].push_back({d, {ce.shift[0], ce.shift[1], ce.shift[2]}});
+          const int d = t.boxes[ce.box].first_child + ci;
+          if (t.boxes[d].leaf && touch(b, d, ce.shift)) {
+            if (out) out[c] = {d, {ce.shift[0], ce.shift[1], ce.shift[2]}};
+            ++c;
+          }
         }
       }
+      return c;
+    };
+    csr_pass(t.fin, all, [&](int b) { return fine_scan(b, nullptr); }, [&](int b, Nbr* out) { fine_scan(b, out); });
   }
 };
 
@@ -207,9 +377,18 @@ HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, const in
   root.se = ns;
   root.te = B.t.alias ? ns : nt;
   B.t.boxes.push_back(root);
+  const auto c0 = std::chrono::steady_clock::now();
   B.refine();
+  const auto c1 = std::chrono::steady_clock::now();
   B.repair();
+  const auto c2 = std::chrono::steady_clock::now();
   B.neighbours();
+  const auto c3 = std::chrono::steady_clock::now();
+  if (std::getenv("SDMK_TIMING")) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[sdmk timing] topology: refine %.2f ms, repair %.2f ms, neighbours %.2f ms\n", ms(c0, c1),
+                 ms(c1, c2), ms(c2, c3));
+  }
   if (B.t.depth_capped)
     std::fprintf(stderr, "build_tree: depth cap %d reached with leaves above capacity (duplicate points?)\n",
                  kMaxLevel);
@@ -218,13 +397,13 @@ HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, const in
 
 std::string dump_topology(const HostTree& t) {  // tree.cpp:325-354
   std::ostringstream os;
-  auto lst = [&](const char* tag, const std::vector<Nbr>& v) {
+  auto lst = [&](const char* tag, NbrSpan v) {
     os << ' ' << tag << "={";
-    for (size_t i = 0; i < v.size(); ++i) {
+    for (int i = 0; i < v.n; ++i) {
       if (i) os << ' ';
-      os << v[i].box;
-      if (v[i].shift[0] || v[i].shift[1] || v[i].shift[2])
-        os << '@' << int(v[i].shift[0]) << ',' << int(v[i].shift[1]) << ',' << int(v[i].shift[2]);
+      os << v.p[i].box;
+      if (v.p[i].shift[0] || v.p[i].shift[1] || v.p[i].shift[2])
+        os << '@' << int(v.p[i].shift[0]) << ',' << int(v.p[i].shift[1]) << ',' << int(v.p[i].shift[2]);
     }
     os << '}';
   };

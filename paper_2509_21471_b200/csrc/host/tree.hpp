@@ -5,10 +5,16 @@
 // coordinates and reproduces the reference's box ids, ranges and neighbour
 // lists bit-exactly (tree.cpp:62-212): ids follow the DFS subdivision order
 // of refine_to_capacity, then the append order of the 2:1 repair sweeps.
-// Boxes are few (<= ~1e5) compared with points, so this is a host pass;
-// child point ranges come from binary searches over the sorted keys instead
-// of the reference's linear scans (same result: within a box the child index
-// is non-decreasing in Morton order).
+// Boxes are few (<= ~1e5) compared with points, so this is a host pass; it
+// is restructured for speed without changing the result:
+//  * refine: the subdivision set depends only on counts, so it is built
+//    level by level with parallel binary searches (within a box the child
+//    index is non-decreasing in Morton order), then renumbered in the DFS
+//    pre-order the reference allocates ids in;
+//  * repair: a parallel read-only pre-scan finds every leaf that could
+//    trigger a subdivision (a subdivision only makes boxes finer, so it can
+//    only remove triggers); only those are replayed sequentially, in order;
+//  * neighbours: CSR lists, built level by level in parallel.
 #pragma once
 
 #include <array>
@@ -32,12 +38,27 @@ struct Nbr {
   int8_t shift[3];
 };
 
+struct NbrSpan {
+  const Nbr* p = nullptr;
+  int n = 0;
+  const Nbr* begin() const { return p; }
+  const Nbr* end() const { return p + n; }
+  int size() const { return n; }
+};
+
+struct Csr {
+  std::vector<int64_t> off;  // per box: start
+  std::vector<int> len;      // per box: count
+  std::vector<Nbr> v;
+  NbrSpan operator[](int b) const { return {v.data() + off[b], len[b]}; }
+};
+
 struct HostTree {
   int dim = 3, n_s = 0, p = 0, max_level = 0;
   bool periodic = false, alias = true, depth_capped = false;
   std::vector<Box> boxes;
   std::vector<std::vector<int>> level_boxes;
-  std::vector<std::vector<Nbr>> col, crs, fin;  // colleagues / coarse / fine
+  Csr col, crs, fin;  // colleagues / coarse / fine
   int num_boxes() const { return (int)boxes.size(); }
   int nsrc(int b) const { return boxes[b].se - boxes[b].sb; }
   int ntgt(int b) const { return boxes[b].te - boxes[b].tb; }

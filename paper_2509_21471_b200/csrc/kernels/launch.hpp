@@ -122,13 +122,17 @@ void launch_inverse_mma(const PWGrid& g, const int* tboxes, int ntb, int d, cons
                         double2* C, double pf, double* incoming, cudaStream_t st);
 
 // ---- residual.cu (K12) -------------------------------------------------------
+// Radial residual tables as piecewise monomials (host/setup.hpp PiecewisePoly):
+// ni sub-intervals of [lo, hi], degree deg; device arrays of ni*(deg+1).
 struct ResidTables {
-  int nd, no;          // coefficient counts of the diag / offd tables
+  int ni, deg;
   double lo, hi;       // table domain (shared by both tables)
   double support;
   int kernel, dim;
+  const double* pw_d;  // diag table (unused for the rotlet)
+  const double* pw_o;  // offd table
 };
-void set_residual_tables(const double* diag, int nd, const double* offd, int no, cudaStream_t st);
+int residual_max_pw();
 // u_res[perm[t]*d+j] for all targets of leaves `leaves`; flags[0] <- coincident
 // points; stats[0..1] <- candidates / in-support pairs (if stats != nullptr)
 void launch_residual(const ResidTables& rt, const dev::DBox* boxes, const int* leaves, int nleaf,

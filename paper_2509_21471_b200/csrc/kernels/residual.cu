@@ -28,64 +28,61 @@ constexpr int kRBlock = 256;
 constexpr int kWarps = kRBlock / 32;
 constexpr int kCap = 128;
 constexpr int kMaxRanges = 160;
-constexpr int kMaxCoef = 128;
-
-__constant__ double c_diag[kMaxCoef];
-__constant__ double c_offd[kMaxCoef];
+constexpr int kMaxPW = 32 * 25;  // ni * (deg + 1) <= 800 doubles per table
 
 struct RangeS {
   double sh[3];
   double lo[3], hi[3];
-  double nu, sup2, cull2;
+  double nu, inu, sup2, cull2;
   int sb, se, self;
 };
 
-__device__ __forceinline__ double clenshaw(const double* __restrict__ c, int n, double t) {
-  double b1 = 0.0, b2 = 0.0;
-  for (int k = n - 1; k >= 1; --k) {
-    double b0 = 2.0 * t * b1 - b2 + c[k];
-    b2 = b1;
-    b1 = b0;
+// Radial table values at s (unit scale) from the piecewise monomial form held
+// in shared memory: interval i = floor((s - lo) ni / (hi - lo)), local
+// u = 2 (frac) - 1, Horner.  Zero at/after the support (split.cpp:147-179).
+template <int KERNEL>
+__device__ __forceinline__ void radial_tables(const ResidTables& rt, const double* __restrict__ pd,
+                                              const double* __restrict__ po, double s, double& fd, double& fo) {
+  const bool in = s < rt.support;
+  const double y = (s - rt.lo) * (rt.ni / (rt.hi - rt.lo));
+  int iv = (int)y;
+  iv = iv < 0 ? 0 : (iv >= rt.ni ? rt.ni - 1 : iv);
+  const double u = 2.0 * (y - iv) - 1.0;
+  const int n1 = rt.deg + 1;
+  const double* cd = pd + iv * n1;
+  const double* co = po + iv * n1;
+  double vd = KERNEL != 2 ? cd[rt.deg] : 0.0, vo = co[rt.deg];
+  for (int k = rt.deg - 1; k >= 0; --k) {
+    if (KERNEL != 2) vd = fma(vd, u, cd[k]);
+    vo = fma(vo, u, co[k]);
   }
-  return t * b1 - b2 + c[0];
+  fd = (KERNEL != 2 && in) ? vd : 0.0;
+  fo = in ? vo : 0.0;
 }
 
+// residual_apply assembly (split.cpp:258-317) given the radial table values;
+// rinv = 1/r from rsqrt, so 1/r, 1/r^2, 1/r^3, 1/r^5 are products.
 template <int KERNEL, int DIM>
-__device__ __forceinline__ void apply_pair(const ResidTables& rt, const double* x, double r2, double nu,
-                                           const double* __restrict__ sstr, int ns, int a, double* u) {
-  const double r = sqrt(r2), s = r / nu;
-  const double tscale = 1.0 / (rt.hi - rt.lo);
-  const double t = (2.0 * s - rt.lo - rt.hi) * tscale;
-  const bool in = s < rt.support;  // table lookups return 0 at/after the support (split.cpp:147-179)
+__device__ __forceinline__ void assemble(double fd, double fo, const double* x, double rinv, double s,
+                                         double support, double nu, const double* __restrict__ sstr, int ns, int a,
+                                         double* u) {
+  constexpr double k8pi = 1.0 / (8.0 * dev::kPI), k4pi = 1.0 / (4.0 * dev::kPI);
+  const double rinv2 = rinv * rinv;
   if (KERNEL == 0) {  // Stokeslet
+    if (DIM == 2) fd = s < support ? (s > 0.0 ? -2.0 * s * log(s) : 0.0) - fd : 0.0;  // split.cpp:147-155
     const double amp = DIM == 2 ? nu : 1.0;
-    double fd = 0.0, fo = 0.0;
-    if (in) {
-      fd = clenshaw(c_diag, rt.nd, t);
-      if (DIM == 2) fd = (s > 0.0 ? -2.0 * s * log(s) : 0.0) - fd;
-      fo = clenshaw(c_offd, rt.no, t);
-    }
-    fd *= amp;
-    fo *= amp;
-    const double c0 = 1.0 / (8.0 * dev::kPI * r);
+    const double c0 = k8pi * rinv;
     double f[DIM], xf = 0.0;
 #pragma unroll
     for (int i = 0; i < DIM; ++i) {
       f[i] = sstr[(size_t)i * ns + a];
       xf += x[i] * f[i];
     }
-    const double cf = fo * c0 * xf / r2;
+    const double cd = amp * fd * c0, cf = amp * fo * c0 * xf * rinv2;
 #pragma unroll
-    for (int j = 0; j < DIM; ++j) u[j] += fd * c0 * f[j] + cf * x[j];
+    for (int j = 0; j < DIM; ++j) u[j] += cd * f[j] + cf * x[j];
   } else if (KERNEL == 1) {  // stresslet
     const double amp = DIM == 2 ? nu : 1.0;
-    double fd = 0.0, fo = 0.0;
-    if (in) {
-      fd = clenshaw(c_diag, rt.nd, t);
-      fo = clenshaw(c_offd, rt.no, t);
-    }
-    fd *= amp;
-    fo *= amp;
     double f[DIM], nn[DIM], xf = 0.0, xn = 0.0, fn = 0.0;
 #pragma unroll
     for (int i = 0; i < DIM; ++i) {
@@ -95,18 +92,18 @@ __device__ __forceinline__ void apply_pair(const ResidTables& rt, const double* 
       xn += x[i] * nn[i];
       fn += f[i] * nn[i];
     }
-    const double cd = fd / (8.0 * dev::kPI * r2 * r);
-    const double co = -3.0 * fo * xf * xn / (4.0 * dev::kPI * r2 * r2 * r);
+    const double rinv3 = rinv2 * rinv;
+    const double cd = amp * fd * k8pi * rinv3;
+    const double co = -3.0 * k4pi * amp * fo * xf * xn * rinv3 * rinv2;
 #pragma unroll
     for (int j = 0; j < DIM; ++j) u[j] += cd * (f[j] * xn + x[j] * fn + nn[j] * xf) + co * x[j];
   } else {  // rotlet
-    const double fo = in ? clenshaw(c_offd, rt.no, t) : 0.0;
     if (DIM == 2) {
-      const double c0 = fo * sstr[a] / (4.0 * dev::kPI * r2);
+      const double c0 = fo * sstr[a] * k4pi * rinv2;
       u[0] += c0 * x[1];
       u[1] -= c0 * x[0];
     } else {
-      const double c0 = fo / (8.0 * dev::kPI * r2 * r);
+      const double c0 = fo * k8pi * rinv2 * rinv;
       const double g0 = sstr[a], g1 = sstr[(size_t)ns + a], g2 = sstr[(size_t)2 * ns + a];
       u[0] += c0 * (g1 * x[2] - g2 * x[1]);
       u[1] += c0 * (g2 * x[0] - g0 * x[2]);
@@ -130,11 +127,19 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
   __shared__ RangeS rs[kMaxRanges];
   __shared__ int lsrc[kWarps][kCap];
   __shared__ unsigned char lrng[kWarps][kCap];
+  __shared__ double s_pd[kMaxPW], s_po[kMaxPW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int leaf = leaves[blockIdx.x];
   const DBox box = boxes[leaf];
   const double r_l = box.side, r_f = 0.5 * r_l;
   const int r0 = rng_start[blockIdx.x], nr = rng_start[blockIdx.x + 1] - r0;
+  {
+    const int npw = rt.ni * (rt.deg + 1);
+    for (int k = tid; k < npw; k += blockDim.x) {
+      s_pd[k] = KERNEL != 2 ? rt.pw_d[k] : 0.0;
+      s_po[k] = rt.pw_o[k];
+    }
+  }
   for (int k = tid; k < nr; k += blockDim.x) {
     const int sbx = rng_box[r0 + k], info = rng_info[r0 + k];
     const DBox sb = boxes[sbx];
@@ -142,6 +147,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     const int code = info & 31;
     const int sh[3] = {code % 3 - 1, (code / 3) % 3 - 1, code / 9 - 1};
     R.nu = (info >> 5) & 1 ? r_f : r_l;
+    R.inu = 1.0 / R.nu;
     R.self = (info >> 6) & 1;
     const double sup = R.nu * rt.support;
     R.sup2 = sup * sup;
@@ -173,13 +179,17 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       for (int k = lane; k < cnt; k += 32) {
         const int a = ls[k];
         const RangeS& R = rs[lr[k]];
-        double x[3], r2 = 0.0;
+        double x[3] = {0.0, 0.0, 0.0}, r2 = 0.0;
 #pragma unroll
         for (int ax = 0; ax < DIM; ++ax) {
           x[ax] = xt[ax] - (spts[(size_t)ax * ns + a] + R.sh[ax]);
           r2 += x[ax] * x[ax];
         }
-        apply_pair<KERNEL, DIM>(rt, x, r2, R.nu, sstr, ns, a, u);
+        const double rinv = rsqrt(r2);
+        const double s = (r2 * rinv) * R.inu;  // nu is a power of two: r * (1/nu) == r / nu
+        double fd, fo;
+        radial_tables<KERNEL>(rt, s_pd, s_po, s, fd, fo);
+        assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, R.nu, sstr, ns, a, u);
       }
       cnt = 0;
       __syncwarp();
@@ -249,11 +259,6 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
 
 }  // namespace
 
-void set_residual_tables(const double* diag, int nd, const double* offd, int no, cudaStream_t st) {
-  if (nd > 0) cudaMemcpyToSymbolAsync(c_diag, diag, sizeof(double) * nd, 0, cudaMemcpyHostToDevice, st);
-  if (no > 0) cudaMemcpyToSymbolAsync(c_offd, offd, sizeof(double) * no, 0, cudaMemcpyHostToDevice, st);
-}
-
 void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves, int nleaf, const int* rng_start,
                      const int* rng_box, const int* rng_info, const double* spts, int ns, const double* sstr,
                      const double* tpts, int nt, const int* tperm, int alias, double /*unused*/, double self_const,
@@ -275,6 +280,6 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
 }
 
 int residual_max_ranges() { return kMaxRanges; }
-int residual_max_coef() { return kMaxCoef; }
+int residual_max_pw() { return kMaxPW; }
 
 }  // namespace sdmkb
