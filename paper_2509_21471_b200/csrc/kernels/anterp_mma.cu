@@ -88,15 +88,19 @@ constexpr int kAWarps = 8;
 // operand, zero padded to NT*8), by rows, bz rows and the raw strengths.  The
 // product s_ch * bz is formed once per chunk in shared memory; the A fragment
 // is (s_ch bz) * by.
-template <int NT, int kMTW>
-__global__ void __launch_bounds__(kAWarps * 32, 2) k_anterp_mma(int kernel, ChebDev cb, const DBox* __restrict__ boxes,
+// PC / KC / DC > 0 (resp. >= 0 for KC) fix p, the kernel and the dimension at
+// compile time so the staging index arithmetic folds (BASELINE cases).
+template <int NT, int kMTW, int PC, int KC, int DC>
+__global__ void __launch_bounds__(kAWarps * 32, 2) k_anterp_mma(int kernel_rt, ChebDev cb, const DBox* __restrict__ boxes,
                                                                const int* __restrict__ leaves,
                                                                const double* __restrict__ basis,
                                                                const double* __restrict__ str, int n,
                                                                double* __restrict__ out, int nch, int mt_per_cta) {
   extern __shared__ double sm[];
-  const int p = cb.p, pz = cb.pz, dim = cb.dim;
+  const int p = PC > 0 ? PC : cb.p, dim = DC > 0 ? DC : cb.dim, pz = dim == 3 ? p : 1;
+  const int kernel = KC >= 0 ? KC : kernel_rt;
   const int sc = kernel == 0 ? dim : (kernel == 1 ? 2 * dim : (dim == 3 ? 3 : 1));
+  nch = kernel == 0 ? dim : (kernel == 1 ? dim * (dim + 1) / 2 : (dim == 3 ? 3 : 1));
   const int RS = cstride(nch * pz), BS = cstride(p), XS = cstride(NT * 8);
   const int RAW = kKC * (XS + 2 * BS + 8);   // one raw buffer
   double* sbz = sm;                          // [kKC][RS]  s_ch * bz(iz)
@@ -233,7 +237,7 @@ constexpr int kTB = 128;     // targets per block (two m-tiles per warp)
 // W chunks arrive by cp.async, double buffered; each warp keeps the A
 // fragments of its two 8-target m-tiles in registers and runs their DMMA
 // chains interleaved.
-template <int KS, int kNC>  // kNC: W rows per shared chunk
+template <int KS, int kNC, int PC, int DC>  // kNC: W rows per shared chunk; PC/DC: compile-time p, dim
 __global__ void __launch_bounds__(256, 1) k_interp_mma(ChebDev cb, const DBox* __restrict__ boxes,
                                                       const int* __restrict__ leaves,
                                                       const double* __restrict__ tbasis, int nt,
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(256, 1) k_interp_mma(ChebDev cb, const DBox* _
                                                       double* __restrict__ ufar) {
   extern __shared__ double sm[];
   constexpr int KP = KS * 4, WS = KP + 4;
-  const int p = cb.p, pz = cb.pz, dim = cb.dim;
+  const int p = PC > 0 ? PC : cb.p, dim = DC > 0 ? DC : cb.dim, pz = dim == 3 ? p : 1;
   const int N = dim * pz * p, BS = p + 1;
   double* Ws = sm;                    // [2][kNC][WS]
   double* bxs = Ws + 2 * kNC * WS;    // [kTB][WS]
@@ -382,19 +386,24 @@ void launch_anterp_mma(int kernel, const ChebDev& cb, const DBox* boxes, const i
   const size_t smem =
       sizeof(double) * (size_t)kKC * (cstride(nch * pz) + 2 * (cstride(NTv * 8) + 2 * cstride(p) + 8));
   dim3 grid(nleaf, nct);
-#define AM(NTT, MW)                                                                                             \
-  do {                                                                                                          \
-    smem_attr((const void*)k_anterp_mma<NTT, MW>, smem);                                                        \
-    k_anterp_mma<NTT, MW><<<grid, kAWarps * 32, smem, st>>>(kernel, cb, boxes, leaves, basis, str, n, out, nch, \
-                                                             mt_per);                                           \
+#define AMS(NTT, MW, PC_, KC_, DC_)                                                                    \
+  do {                                                                                                 \
+    smem_attr((const void*)k_anterp_mma<NTT, MW, PC_, KC_, DC_>, smem);                                \
+    k_anterp_mma<NTT, MW, PC_, KC_, DC_><<<grid, kAWarps * 32, smem, st>>>(kernel, cb, boxes, leaves, basis, \
+                                                                           str, n, out, nch, mt_per);   \
   } while (0)
-  if (NTv <= 1) AM(1, 8);
+#define AM(NTT, MW) AMS(NTT, MW, 0, -1, 0)
+  if (cb.dim == 3 && p == 23 && kernel == 0) AMS(3, 6, 23, 0, 3);
+  else if (cb.dim == 3 && p == 22 && kernel == 1) AMS(3, 6, 22, 1, 3);
+  else if (cb.dim == 3 && p == 30 && kernel == 0) AMS(4, 4, 30, 0, 3);
+  else if (NTv <= 1) AM(1, 8);
   else if (NTv == 2) AM(2, 8);
   else if (NTv == 3) AM(3, 6);
   else if (NTv == 4) AM(4, 4);
   else if (NTv == 5) AM(5, 3);
   else AM(6, 3);
 #undef AM
+#undef AMS
 }
 
 void launch_interp_mma(const ChebDev& cb, const DBox* boxes, const int* leaves, int nleaf, const double* tbasis,
@@ -406,18 +415,24 @@ void launch_interp_mma(const ChebDev& cb, const DBox* boxes, const int* leaves, 
     const int WS = KS * 4 + 4;
     return sizeof(double) * (2 * (size_t)NC * WS + (size_t)kTB * WS + 2 * (size_t)kTB * (p + 1)) + sizeof(int) * N;
   };
-#define IM(KSS, NCC)                                                                                      \
+#define IMS(KSS, NCC, PC_, DC_)                                                                           \
   do {                                                                                                    \
     size_t sm = smem_for(KSS, NCC);                                                                       \
-    smem_attr((const void*)k_interp_mma<KSS, NCC>, sm);                                                   \
-    k_interp_mma<KSS, NCC><<<nleaf, 256, sm, st>>>(cb, boxes, leaves, tbasis, nt, tperm, incoming, ufar); \
+    smem_attr((const void*)k_interp_mma<KSS, NCC, PC_, DC_>, sm);                                         \
+    k_interp_mma<KSS, NCC, PC_, DC_><<<nleaf, 256, sm, st>>>(cb, boxes, leaves, tbasis, nt, tperm, incoming, \
+                                                              ufar);                                      \
   } while (0)
-  if (KSv <= 2) IM(2, 256);
+#define IM(KSS, NCC) IMS(KSS, NCC, 0, 0)
+  if (cb.dim == 3 && p == 23) IMS(6, 256, 23, 3);
+  else if (cb.dim == 3 && p == 22) IMS(6, 256, 22, 3);
+  else if (cb.dim == 3 && p == 30) IMS(8, 128, 30, 3);
+  else if (KSv <= 2) IM(2, 256);
   else if (KSv <= 4) IM(4, 256);
   else if (KSv <= 6) IM(6, 256);
   else if (KSv <= 8) IM(8, 128);
   else IM(12, 64);
 #undef IM
+#undef IMS
 }
 
 }  // namespace sdmkb

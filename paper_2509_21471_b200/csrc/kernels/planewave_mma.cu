@@ -40,13 +40,15 @@ __host__ __device__ constexpr int r8(int x) { return (x + 7) / 8 * 8 % 16 == 8 ?
 // smem layout (doubles): EX[NX8][SE]  (rows (m0,part) -> B^T of the X stage)
 //                        EYr/EYi[NY8][SY] (A' of the Y stage, k' = 2 iy + part)
 //                        win[2][4*P8][SE] (A of the X stage), a[4*P8][SAa]
-template <int PT>
+// PC / NC > 0: p and N fixed at compile time (the BASELINE grids), so the
+// index arithmetic folds to constants.
+template <int PT, int PC, int NC>
 __global__ void __launch_bounds__(kW * 32, 1) k_fwd_xy_mma(PWGrid g, const int* __restrict__ boxes, int nch,
                                                           const double* __restrict__ outgoing,
                                                           double2* __restrict__ B) {
   constexpr int P8 = PT * 8;
   constexpr int SE = P8 + 4;  // == 4 mod 8 for P8 = 24, 32
-  const int p = g.p, M = g.M, N = g.N, ncol = g.ncol, pp = p * p;
+  const int p = PC > 0 ? PC : g.p, N = NC > 0 ? NC : g.N, M = (N - 1) / 2, ncol = g.ncol, pp = p * p;
   const int M1 = M + 1, NX = 2 * M1, NX8 = (NX + 7) / 8 * 8, NY8 = (N + 7) / 8 * 8, M18 = (M1 + 7) / 8 * 8;
   const int SY = r4(2 * P8), SAa = r8(NX8 > 2 * M18 ? NX8 : 2 * M18);
   extern __shared__ double sm[];
@@ -89,10 +91,11 @@ __global__ void __launch_bounds__(kW * 32, 1) k_fwd_xy_mma(PWGrid g, const int* 
   auto issue = [&](int grp, int buf) {
     double* dst = win + buf * 4 * P8 * SE;
     const int jz0 = grp * 4;
-    for (int e = tid; e < 4 * pp; e += blockDim.x) {
-      const int s = e / pp, r = (e / p) % p, cc = e % p;
+    for (int row = warp; row < 4 * p; row += kW) {  // rows (s, r), lanes along the row
+      const int s = row / p, r = row % p;
       const bool v = jz0 + s < p;
-      cp_async8(dst + (s * P8 + r) * SE + cc, v ? w + (size_t)(jz0 + s) * pp + r * p + cc : w, v);
+      const double* srow = w + (size_t)(v ? jz0 + s : 0) * pp + r * p;
+      for (int cc = lane; cc < p; cc += 32) cp_async8(dst + (s * P8 + r) * SE + cc, srow + cc, v);
     }
     cp_commit();
   };
@@ -243,12 +246,12 @@ __global__ void __launch_bounds__(kW * 32, 2) k_z_mma(PWGrid g, int nc, const do
 }
 
 // ------------------------------------------------------------------ inv_xy --
-template <int PT>
+template <int PT, int PC, int NC>
 __global__ void __launch_bounds__(kW * 32, 1) k_inv_xy_mma(PWGrid g, const int* __restrict__ tboxes, int d,
                                                           const double2* __restrict__ C, double pf,
                                                           double* __restrict__ incoming) {
   constexpr int P8 = PT * 8;
-  const int p = g.p, M = g.M, N = g.N, ncol = g.ncol, pp = p * p;
+  const int p = PC > 0 ? PC : g.p, N = NC > 0 ? NC : g.N, M = (N - 1) / 2, ncol = g.ncol, pp = p * p;
   const int M1 = M + 1, NY8 = (N + 7) / 8 * 8, M18 = (M1 + 7) / 8 * 8, NX = 2 * M1, NX8 = (NX + 7) / 8 * 8;
   const int SD = r8(2 * M18);      // D rows (s,my) of interleaved (m0, part)
   const int SA = r4(2 * NY8);      // A' rows iy, k' = 2 my + part
@@ -287,12 +290,15 @@ __global__ void __launch_bounds__(kW * 32, 1) k_inv_xy_mma(PWGrid g, const int* 
   const int ngroups = (p + 3) / 4;
   for (int grp = 0; grp < ngroups; ++grp) {
     __syncthreads();
-    for (int e = tid; e < 4 * ncol; e += blockDim.x) {  // scatter the in-band columns into dense D
-      const int s = e / ncol, c = e % ncol, iz = grp * 4 + s;
-      const double2 v = iz < p ? Ci[(size_t)iz * ncol + c] : make_double2(0.0, 0.0);
-      double* row = D + (s * NY8 + g.col_my[c] + M) * SD + 2 * g.col_m0[c];
-      row[0] = v.x;
-      row[1] = v.y;
+    for (int s = 0; s < 4; ++s) {  // scatter the in-band columns into dense D
+      const int iz = grp * 4 + s;
+      if (iz >= p) break;
+      for (int c = tid; c < ncol; c += blockDim.x) {
+        const double2 v = Ci[(size_t)iz * ncol + c];
+        double* row = D + (s * NY8 + g.col_my[c] + M) * SD + 2 * g.col_m0[c];
+        row[0] = v.x;
+        row[1] = v.y;
+      }
     }
     __syncthreads();
     // Y stage: d[(s,iy), m0] = sum_{(my,part)} A'[iy][(my,part)] D[s][my][(m0,part)]
@@ -330,12 +336,12 @@ __global__ void __launch_bounds__(kW * 32, 1) k_inv_xy_mma(PWGrid g, const int* 
       }
     }
     __syncthreads();
-    for (int e = tid; e < 4 * ncol; e += blockDim.x) {  // clear the scattered entries for the next group
-      const int s = e / ncol, c = e % ncol;
-      double* row = D + (s * NY8 + g.col_my[c] + M) * SD + 2 * g.col_m0[c];
-      row[0] = 0.0;
-      row[1] = 0.0;
-    }
+    for (int s = 0; s < 4; ++s)  // clear the scattered entries for the next group
+      for (int c = tid; c < ncol; c += blockDim.x) {
+        double* row = D + (s * NY8 + g.col_my[c] + M) * SD + 2 * g.col_m0[c];
+        row[0] = 0.0;
+        row[1] = 0.0;
+      }
   }
 }
 
@@ -360,13 +366,17 @@ void launch_forward_mma(const PWGrid& g, const int* boxes, int nbox, int nch, co
     size_t smem = sizeof(double) * ((size_t)NX8 * SE + 2 * (size_t)NY8 * SY + 2 * 4 * (size_t)P8 * SE +
                                     4 * (size_t)P8 * SAa) + sizeof(int) * (size_t)g.N * M1;
     dim3 grid(nbox, nch);
-    if (PT <= 3) {
-      attr((const void*)k_fwd_xy_mma<3>, smem);
-      k_fwd_xy_mma<3><<<grid, kW * 32, smem, st>>>(g, boxes, nch, outgoing, B);
-    } else {
-      attr((const void*)k_fwd_xy_mma<4>, smem);
-      k_fwd_xy_mma<4><<<grid, kW * 32, smem, st>>>(g, boxes, nch, outgoing, B);
-    }
+#define FX(PT_, PC_, NC_)                                                             \
+  do {                                                                                \
+    attr((const void*)k_fwd_xy_mma<PT_, PC_, NC_>, smem);                             \
+    k_fwd_xy_mma<PT_, PC_, NC_><<<grid, kW * 32, smem, st>>>(g, boxes, nch, outgoing, B); \
+  } while (0)
+    if (g.p == 23 && g.N == 33) FX(3, 23, 33);
+    else if (g.p == 22 && g.N == 33) FX(3, 22, 33);
+    else if (g.p == 30 && g.N == 45) FX(4, 30, 45);
+    else if (PT <= 3) FX(3, 0, 0);
+    else FX(4, 0, 0);
+#undef FX
   }
   {
     const int KT = PT, RT = (g.Nz + 7) / 8 <= 5 ? 5 : 6;
@@ -413,13 +423,17 @@ void launch_inverse_mma(const PWGrid& g, const int* tboxes, int ntb, int d, cons
     const int NX8 = (2 * M1 + 7) / 8 * 8, SD = r8(2 * M18), SA = r4(2 * NY8), SX = r4(NX8 > 2 * M18 ? NX8 : 2 * M18);
     size_t smem = sizeof(double) * (2 * (size_t)P8 * SA + (size_t)P8 * SX + 4 * (size_t)NY8 * SD + 4 * (size_t)P8 * SX);
     dim3 grid(ntb, d);
-    if (PT <= 3) {
-      attr((const void*)k_inv_xy_mma<3>, smem);
-      k_inv_xy_mma<3><<<grid, kW * 32, smem, st>>>(g, tboxes, d, C, pf, incoming);
-    } else {
-      attr((const void*)k_inv_xy_mma<4>, smem);
-      k_inv_xy_mma<4><<<grid, kW * 32, smem, st>>>(g, tboxes, d, C, pf, incoming);
-    }
+#define IX(PT_, PC_, NC_)                                                                   \
+  do {                                                                                      \
+    attr((const void*)k_inv_xy_mma<PT_, PC_, NC_>, smem);                                   \
+    k_inv_xy_mma<PT_, PC_, NC_><<<grid, kW * 32, smem, st>>>(g, tboxes, d, C, pf, incoming); \
+  } while (0)
+    if (g.p == 23 && g.N == 33) IX(3, 23, 33);
+    else if (g.p == 22 && g.N == 33) IX(3, 22, 33);
+    else if (g.p == 30 && g.N == 45) IX(4, 30, 45);
+    else if (PT <= 3) IX(3, 0, 0);
+    else IX(4, 0, 0);
+#undef IX
   }
 }
 

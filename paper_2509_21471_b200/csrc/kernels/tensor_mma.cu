@@ -12,8 +12,11 @@
 // The z-stage accumulators stay in registers for the whole box (and, for the
 // merge, across the 2^d children), so the p^3 intermediate never touches HBM.
 // Every dimension is padded to PT*8 with zeros; fragment loads use
-// bank-conflict-free strides (== 4 mod 16 for row-indexed A / B^T, == 8 mod 16
-// for k-indexed B).
+// bank-conflict-free strides (== 4 mod 8 doubles).
+//
+// PC > 0 compiles the kernel for a fixed p (the BASELINE orders 22, 23, 30):
+// all index arithmetic then folds to constants -- with a runtime p the
+// integer division sequences outnumbered the DMMAs ~8:1 (ncu source page).
 #include "common.cuh"
 #include "launch.hpp"
 
@@ -26,8 +29,8 @@ using dev::cp_commit;
 using dev::cp_wait0;
 using dev::cp_wait1;
 
-template <int PT, int NW, int ZT>  // PT: 8-tiles per axis; NW warps; ZT max z-stage tiles per warp
-__global__ void __launch_bounds__(NW * 32, 1) k_tensor_mma(int p, const double* __restrict__ mats,
+template <int PC, int PT, int NW, int ZT>
+__global__ void __launch_bounds__(NW * 32, 1) k_tensor_mma(int p_rt, const double* __restrict__ mats,
                                                            const int* __restrict__ in_list,
                                                            const int* __restrict__ out_box,
                                                            const int* __restrict__ ci_list, int nin, int nch,
@@ -36,43 +39,52 @@ __global__ void __launch_bounds__(NW * 32, 1) k_tensor_mma(int p, const double* 
   constexpr int P8 = PT * 8;
   constexpr int SA = P8 + 4;
   constexpr int S1 = P8 % 8 == 4 ? P8 : P8 + 4;
+  const int p = PC > 0 ? PC : p_rt;
   extern __shared__ double sm[];
   const int pp = p * p, nodes = p * pp;
   const int NP = (pp + 7) / 8 * 8;
   const int SS = NP % 8 == 4 ? NP : NP + 4;
+  __shared__ int s_in[8], s_ci[8], s_nq;
   double* Mm = sm;                    // [2][P8][SA]
   double* inS = Mm + 2 * P8 * SA;     // [2 buffers][4*P8][SA]
   double* T1 = inS + 2 * 4 * P8 * SA; // [4*P8][S1]
   double* T2 = T1 + 4 * P8 * S1;      // [4][SS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-  for (int e = tid; e < 2 * P8 * SA; e += blockDim.x) {
-    const int bsel = e / (P8 * SA), r = (e / SA) % P8, c = e % SA;
-    Mm[e] = (r < p && c < p) ? mats[(size_t)bsel * pp + r * p + c] : 0.0;
+  for (int r = warp; r < 2 * P8; r += NW) {  // zero-padded bit-0 / bit-1 matrices
+    const int bsel = r / P8, rr = r % P8;
+    for (int c = lane; c < SA; c += 32) Mm[r * SA + c] = (rr < p && c < p) ? mats[(size_t)bsel * pp + rr * p + c] : 0.0;
   }
   for (int e = tid; e < 4 * SS; e += blockDim.x) T2[e] = 0.0;
   for (int e = tid; e < 2 * 4 * P8 * SA; e += blockDim.x) inS[e] = 0.0;  // padding stays zero
   const int pair = blockIdx.x, ch = blockIdx.y;
+  if (tid == 0) {
+    int nq = 0;
+    for (int q = 0; q < nin; ++q) {
+      const int ib = in_list[pair * nin + q];
+      if (ib >= 0) {
+        s_in[nq] = ib;
+        s_ci[nq] = ci_list[pair * nin + q];
+        ++nq;
+      }
+    }
+    s_nq = nq;
+  }
+  __syncthreads();
   const int ngroups = (p + 3) / 4;
-  // work items: (input q, z-group)
-  int qs[8];
-  int nq = 0;
-  for (int q = 0; q < nin; ++q)
-    if (in_list[pair * nin + q] >= 0) qs[nq++] = q;
-  const int nitems = nq * ngroups;
+  const int nitems = s_nq * ngroups;
   const int ntn = NP / 8, ntiles = PT * ntn;
   double acc[ZT][2];
 #pragma unroll
   for (int i = 0; i < ZT; ++i) acc[i][0] = acc[i][1] = 0.0;
-  __syncthreads();
   auto issue = [&](int item, int buf) {
-    const int q = qs[item / ngroups], jz0 = (item % ngroups) * 4;
-    const double* in = src + ((size_t)in_list[pair * nin + q] * nch + ch) * nodes;
+    const int q = item / ngroups, jz0 = (item % ngroups) * 4;
+    const double* in = src + ((size_t)s_in[q] * nch + ch) * nodes;
     double* dstb = inS + buf * 4 * P8 * SA;
-    const int cnt = 4 * pp;
-    for (int e = tid; e < cnt; e += blockDim.x) {
-      const int s = e / pp, r = (e / p) % p, c = e % p, jz = jz0 + s;
+    for (int row = warp; row < 4 * p; row += NW) {  // rows (s, r) of the group, lanes along c
+      const int s = row / p, r = row % p, jz = jz0 + s;
       const bool v = jz < p;
-      cp_async8(dstb + (s * P8 + r) * SA + c, v ? in + (size_t)jz * pp + r * p + c : in, v);
+      const double* srow = in + (size_t)(v ? jz : 0) * pp + r * p;
+      for (int c = lane; c < p; c += 32) cp_async8(dstb + (s * P8 + r) * SA + c, srow + c, v);
     }
     cp_commit();
   };
@@ -86,8 +98,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_tensor_mma(int p, const double* 
       cp_wait0();
     }
     __syncthreads();
-    const int q = qs[item / ngroups], jz0 = (item % ngroups) * 4;
-    const int cb = ci_list[pair * nin + q];
+    const int q = item / ngroups, jz0 = (item % ngroups) * 4;
+    const int cb = s_ci[q];
     const double* Mx = Mm + (cb & 1) * P8 * SA;
     const double* My = Mm + ((cb >> 1) & 1) * P8 * SA;
     const double* Mz = Mm + ((cb >> 2) & 1) * P8 * SA;
@@ -179,7 +191,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_tensor_mma(int p, const double* 
   }
 }
 
-template <int PT, int NW, int ZT>
+template <int PC, int PT, int NW, int ZT>
 void tensor_mma_t(int p, const double* mats, const int* in_list, const int* out_box, const int* ci, int npairs,
                   int nin, int nch, const double* src, double* dst, int accumulate, cudaStream_t st) {
   constexpr int P8 = PT * 8, SA = P8 + 4, S1 = P8 % 8 == 4 ? P8 : P8 + 4;
@@ -187,12 +199,12 @@ void tensor_mma_t(int p, const double* mats, const int* in_list, const int* out_
   size_t smem = sizeof(double) * (2 * P8 * SA + 2 * 4 * P8 * SA + 4 * P8 * S1 + 4 * SS);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_tensor_mma<PT, NW, ZT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tensor_mma<PC, PT, NW, ZT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   dim3 grid(npairs, nch);
-  k_tensor_mma<PT, NW, ZT><<<grid, NW * 32, smem, st>>>(p, mats, in_list, out_box, ci, nin, nch, src, dst,
-                                                         accumulate);
+  k_tensor_mma<PC, PT, NW, ZT><<<grid, NW * 32, smem, st>>>(p, mats, in_list, out_box, ci, nin, nch, src, dst,
+                                                             accumulate);
 }
 
 }  // namespace
@@ -205,10 +217,16 @@ void launch_tensor_mma(int p, const double* mats, const int* in_list, const int*
   const int nin = accumulate >= 2 ? (1 << dim) : 1;
   const int acc = accumulate == 1 ? 1 : 0;
   const int PT = (p + 7) / 8;
-  if (PT <= 1) tensor_mma_t<1, 4, 8>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
-  else if (PT == 2) tensor_mma_t<2, 8, 12>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
-  else if (PT == 3) tensor_mma_t<3, 16, 13>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
-  else tensor_mma_t<4, 16, 32>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
+#define TM(PC_, PT_, NW_, ZT_) \
+  tensor_mma_t<PC_, PT_, NW_, ZT_>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st)
+  if (p == 22) TM(22, 3, 16, 13);
+  else if (p == 23) TM(23, 3, 16, 13);
+  else if (p == 30) TM(30, 4, 16, 32);
+  else if (PT <= 1) TM(0, 1, 4, 8);
+  else if (PT == 2) TM(0, 2, 8, 12);
+  else if (PT == 3) TM(0, 3, 16, 13);
+  else TM(0, 4, 16, 32);
+#undef TM
 }
 
 }  // namespace sdmkb
