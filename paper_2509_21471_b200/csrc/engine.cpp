@@ -382,7 +382,7 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode) {
   pr.tree = build_topology(d, pr.periodic, P.n_s, P.p, ns, hq, pr.alias ? 0 : nt,
                            pr.alias ? nullptr : hq + (size_t)ns * d);
   const auto w2 = std::chrono::steady_clock::now();
-  upload_tree_lists();
+  upload_tree_lists(hq);
   const auto w3 = std::chrono::steady_clock::now();
   if (timing_on()) {
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
@@ -392,7 +392,7 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode) {
   pr.ready = true;
 }
 
-void Context::upload_tree_lists() {
+void Context::upload_tree_lists(const int32_t* qs) {
   Problem& pr = prob_;
   const HostTree& t = pr.tree;
   const int nb = t.num_boxes(), d = pr.dim, nchild = 1 << d;
@@ -542,6 +542,9 @@ void Context::upload_tree_lists() {
   // root lists: box 0 with one zero-offset entry
   std::vector<int> root_ids = {0}, root_es = {0, 1}, root_slot = {0}, root_tau = {13};
   Packer pk;
+  std::vector<int> subr;
+  leaf_subranges(t, pr.ns, qs, subr);  // source sub-cells for the residual cull
+  size_t o_sub = pk.add(subr);
   size_t o_boxes = pk.add(boxes), o_ant = pk.add(ant), o_itp = pk.add(itp), o_rs = pk.add(rs), o_rbox = pk.add(rbox),
          o_rinfo = pk.add(rinfo), o_rid = pk.add(root_ids), o_res = pk.add(root_es), o_rsl = pk.add(root_slot),
          o_rta = pk.add(root_tau);
@@ -567,6 +570,7 @@ void Context::upload_tree_lists() {
   pr.rng_start = (int*)(dv + o_rs);
   pr.rng_box = (int*)(dv + o_rbox);
   pr.rng_info = (int*)(dv + o_rinfo);
+  pr.subrange = (int*)(dv + o_sub);
   pr.levels.assign(L, {});
   for (int lev = 0; lev < L; ++lev) {
     Problem::LevelLists& X = pr.levels[lev];
@@ -811,7 +815,7 @@ void Context::run_residual(double* ures, bool stats) {  // dmk.cpp:919-1032
   unsigned long long* st = arena_.as<unsigned long long>("stats", 4);
   if (stats) cuda_check(cudaMemsetAsync(st, 0, 4 * sizeof(unsigned long long), st_), "memset");
   cudaEventRecord(ev_[13], st_);
-  launch_residual(rt, pr.boxes, pr.int_leaves, pr.n_int, pr.rng_start, pr.rng_box, pr.rng_info, pr.spts, pr.ns,
+  launch_residual(rt, pr.boxes, pr.int_leaves, pr.n_int, pr.rng_start, pr.rng_box, pr.rng_info, pr.subrange, pr.spts, pr.ns,
                   pr.sstr, pr.tpts, pr.nt, pr.tperm, pr.alias ? 1 : 0, 0.0, T.self_const, ures, flags + 3,
                   stats ? st : nullptr, st_);
   cudaEventRecord(ev_[12], st_);

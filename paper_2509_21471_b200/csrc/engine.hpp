@@ -75,7 +75,7 @@ struct Problem {
   dev::DBox* boxes = nullptr;
   int *ant_leaves = nullptr, *int_leaves = nullptr;
   int n_ant = 0, n_int = 0;
-  int *rng_start = nullptr, *rng_box = nullptr, *rng_info = nullptr;
+  int *rng_start = nullptr, *rng_box = nullptr, *rng_info = nullptr, *subrange = nullptr;
   struct LevelLists {
     int n_merge = 0, n_interp = 0, n_src = 0, n_tgt = 0;
     int *merge_out = nullptr, *merge_in = nullptr, *merge_ci = nullptr;
@@ -113,7 +113,7 @@ class Context {
   void check_inputs(const Plan& plan, int dim, int64_t ns, int64_t nt, int mode);
   // inputs already in the arena ("src_in", "tgt_in", "str_in"): validate, wrap, sort, topology, upload
   void build_problem(const Plan& plan, int dim, int ns, int nt, int mode);
-  void upload_tree_lists();
+  void upload_tree_lists(const int32_t* qs);
   void run_upward();
   void run_root();
   void run_downward();

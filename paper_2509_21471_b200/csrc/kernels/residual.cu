@@ -1,20 +1,23 @@
 // K12: near-field residual pass (dmk.cpp:919-1032) with the fused residual
-// apply (split.cpp:258-317) and Clenshaw table lookups (chebyshev.cpp:9-19).
+// apply (split.cpp:258-317).
 //
-// One CTA per target leaf, one warp per target at a time.
+// One CTA per target leaf; each warp owns 32 Morton-consecutive targets of the
+// leaf, one per lane (so each target's pairs are summed by one lane, in the
+// reference's order: ranges in order, sources in order).
 //  1. The leaf's near ranges (own box nu = r_l, colleague leaves and fine
 //     neighbours nu = r_l/2, coarse neighbours nu = r_l; dmk.cpp:980-990) are
 //     staged in shared memory with their (shifted) bounding boxes.
-//  2. A range whose box lies entirely outside the target's support sphere is
-//     skipped warp-uniformly (conservative margin, so no pair with
+//  2. A range is skipped warp-uniformly when its box lies outside the support
+//     sphere of every target of the warp (distance to the warp's target
+//     bounding box; conservative 1e-12 margin, so no pair with
 //     r^2 < (nu*support)^2 is ever dropped).
-//  3. Lanes test 32 sources at a time (coalesced SoA loads); in-support pairs
-//     are compacted with a ballot into a per-warp list in shared memory.
-//  4. When the list fills, all 32 lanes evaluate list entries (two Clenshaw
-//     tables + tensor assembly), so the expensive path runs at full SIMT
-//     width even though only a few percent of candidates are in support.
-//  5. Lane partial sums are combined by a fixed xor-shuffle tree
-//     (deterministic run to run), then the alias self term is added.
+//  3. Sources stream as warp-uniform broadcast loads; every lane tests its own
+//     target (same arithmetic as the reference: x = xt - (xs + shift)) and
+//     appends in-support pairs to a lane-private list in shared memory.
+//  4. When any list fills, all lanes evaluate their lists in lockstep: the
+//     radial tables come from a piecewise re-expansion held in shared memory
+//     (host/setup.hpp PiecewisePoly), and 1/r from rsqrt.
+// No atomics and a fixed per-target order: bitwise reproducible.
 #include "common.cuh"
 #include "launch.hpp"
 
@@ -26,15 +29,16 @@ using dev::DBox;
 
 constexpr int kRBlock = 256;
 constexpr int kWarps = kRBlock / 32;
-constexpr int kCap = 128;
+constexpr int kList = 24;        // per-lane list capacity (entries)
 constexpr int kMaxRanges = 160;
 constexpr int kMaxPW = 32 * 25;  // ni * (deg + 1) <= 800 doubles per table
 
 struct RangeS {
   double sh[3];
   double lo[3], hi[3];
-  double nu, inu, sup2, cull2;
-  int sb, se, self;
+  double nu, inu, sup2, cull, half;
+  int sb, se, self, zero_shift;
+  int sub[9];  // Morton child sub-ranges of the source leaf (contiguous, in order)
 };
 
 // Radial table values at s (unit scale) from the piecewise monomial form held
@@ -118,6 +122,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
                                                       const int* __restrict__ rng_start,
                                                       const int* __restrict__ rng_box,
                                                       const int* __restrict__ rng_info,
+                                                      const int* __restrict__ subrange,
                                                       const double* __restrict__ spts, int ns,
                                                       const double* __restrict__ sstr,
                                                       const double* __restrict__ tpts, int nt,
@@ -125,9 +130,10 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
                                                       double* __restrict__ ures, int* flags,
                                                       unsigned long long* stats) {
   __shared__ RangeS rs[kMaxRanges];
-  __shared__ int lsrc[kWarps][kCap];
-  __shared__ unsigned char lrng[kWarps][kCap];
   __shared__ double s_pd[kMaxPW], s_po[kMaxPW];
+  extern __shared__ int dyn[];  // lane-interleaved lists: [kWarps][kList][32] ints then bytes
+  int (*lsrc)[kList][32] = reinterpret_cast<int (*)[kList][32]>(dyn);
+  unsigned char (*lrng)[kList][32] = reinterpret_cast<unsigned char (*)[kList][32]>(dyn + kWarps * kList * 32);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int leaf = leaves[blockIdx.x];
   const DBox box = boxes[leaf];
@@ -151,95 +157,145 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     R.self = (info >> 6) & 1;
     const double sup = R.nu * rt.support;
     R.sup2 = sup * sup;
-    const double cs = sup * (1.0 + 1e-12) + 1e-15;
-    R.cull2 = cs * cs;
+    R.cull = sup * (1.0 + 1e-12) + 1e-15;
+    R.zero_shift = 1;
     for (int ax = 0; ax < 3; ++ax) {
       R.sh[ax] = ax < DIM ? (double)sh[ax] : 0.0;
+      if (R.sh[ax] != 0.0) R.zero_shift = 0;
       R.lo[ax] = sb.c[ax] - sb.half + R.sh[ax];
       R.hi[ax] = sb.c[ax] + sb.half + R.sh[ax];
     }
     R.sb = sb.sb;
     R.se = sb.se;
+    R.half = sb.half;
+    for (int c = 0; c < 9; ++c) R.sub[c] = subrange[(size_t)sbx * 9 + c];
     rs[k] = R;
   }
   __syncthreads();
+  const double* __restrict__ spx = spts;
+  const double* __restrict__ spy = spts + ns;
+  const double* __restrict__ spz = spts + (size_t)(DIM == 3 ? 2 : 1) * ns;
   double selfc = 0.0;
   if (alias && KERNEL == 0) selfc = DIM == 3 ? self_const / r_l : self_const + log(r_l) / (4.0 * dev::kPI);
   unsigned long long n_ref = 0, n_test = 0, n_in = 0;
   int singular = 0;
-  int* ls = lsrc[warp];
-  unsigned char* lr = lrng[warp];
-  for (int t = box.tb + warp; t < box.te; t += kWarps) {
+  for (int t0 = box.tb + warp * 32; t0 < box.te; t0 += kRBlock) {
+    const int t = t0 + lane;
+    const bool valid = t < box.te;
+    const int tt = valid ? t : t0;
     double xt[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-    for (int ax = 0; ax < DIM; ++ax) xt[ax] = tpts[(size_t)ax * nt + t];
+    for (int ax = 0; ax < DIM; ++ax) xt[ax] = tpts[(size_t)ax * nt + tt];
+    double bl[3], bh[3];  // the warp's target bounding box
+#pragma unroll
+    for (int ax = 0; ax < DIM; ++ax) {
+      double lo = xt[ax], hi = xt[ax];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      bl[ax] = lo;
+      bh[ax] = hi;
+    }
     double u[3] = {0.0, 0.0, 0.0};
     int cnt = 0;
     auto flush = [&]() {
-      for (int k = lane; k < cnt; k += 32) {
-        const int a = ls[k];
-        const RangeS& R = rs[lr[k]];
-        double x[3] = {0.0, 0.0, 0.0}, r2 = 0.0;
+      int mx = cnt;
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) {
-          x[ax] = xt[ax] - (spts[(size_t)ax * ns + a] + R.sh[ax]);
-          r2 += x[ax] * x[ax];
+      for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      for (int i = 0; i < mx; ++i) {
+        if (i < cnt) {
+          const int a = lsrc[warp][i][lane];
+          const RangeS& R = rs[lrng[warp][i][lane]];
+          double x[3] = {0.0, 0.0, 0.0}, r2 = 0.0;
+          x[0] = xt[0] - (spx[a] + R.sh[0]);
+          x[1] = xt[1] - (spy[a] + R.sh[1]);
+          if (DIM == 3) x[2] = xt[2] - (spz[a] + R.sh[2]);
+#pragma unroll
+          for (int ax = 0; ax < DIM; ++ax) r2 += x[ax] * x[ax];
+          const double rinv = rsqrt(r2);
+          const double s = (r2 * rinv) * R.inu;  // nu is a power of two: r * (1/nu) == r / nu
+          double fd, fo;
+          radial_tables<KERNEL>(rt, s_pd, s_po, s, fd, fo);
+          assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, R.nu, sstr, ns, a, u);
         }
-        const double rinv = rsqrt(r2);
-        const double s = (r2 * rinv) * R.inu;  // nu is a power of two: r * (1/nu) == r / nu
-        double fd, fo;
-        radial_tables<KERNEL>(rt, s_pd, s_po, s, fd, fo);
-        assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, R.nu, sstr, ns, a, u);
       }
       cnt = 0;
-      __syncwarp();
     };
     for (int k = 0; k < nr; ++k) {
       const RangeS& R = rs[k];
       const int len = R.se - R.sb;
-      n_ref += len - ((alias && R.self) ? 1 : 0);
-      double d2 = 0.0;
+      n_ref += valid ? len - ((alias && R.self) ? 1 : 0) : 0;
+      double d2 = 0.0;  // distance from the warp's target box to the source box
 #pragma unroll
       for (int ax = 0; ax < DIM; ++ax) {
-        double dd = fmax(0.0, fmax(R.lo[ax] - xt[ax], xt[ax] - R.hi[ax]));
+        const double dd = fmax(0.0, fmax(R.lo[ax] - bh[ax], bl[ax] - R.hi[ax]));
         d2 += dd * dd;
       }
-      if (d2 > R.cull2) continue;  // whole range outside the support sphere
-      n_test += len;
-      for (int a0 = R.sb; a0 < R.se; a0 += 32) {
-        const int a = a0 + lane;
-        bool in = false;
-        if (a < R.se && !(alias && R.self && a == t)) {
-          double r2 = 0.0;
+      if (d2 > R.cull * R.cull) continue;
+      const double sup2 = R.sup2, cull2 = R.cull * R.cull;
+      const bool zs = R.zero_shift;
+      const bool skip_self = alias && R.self;
+      constexpr int NC = 1 << DIM;
+      for (int ci = 0; ci < NC; ++ci) {  // Morton child sub-cells of the source leaf
+        const int a0 = R.sub[ci], a1 = R.sub[ci + 1];
+        if (a0 == a1) continue;
+        double e2 = 0.0;
 #pragma unroll
-          for (int ax = 0; ax < DIM; ++ax) {
-            double xv = xt[ax] - (spts[(size_t)ax * ns + a] + R.sh[ax]);
-            r2 += xv * xv;
+        for (int ax = 0; ax < DIM; ++ax) {
+          const double lo = R.lo[ax] + ((ci >> ax) & 1) * R.half, hi = lo + R.half;
+          const double dd = fmax(0.0, fmax(lo - bh[ax], bl[ax] - hi));
+          e2 += dd * dd;
+        }
+        if (e2 > cull2) continue;
+        n_test += valid ? a1 - a0 : 0;
+        auto test = [&](int a, double sx, double sy, double sz) {
+          double x0, x1, x2 = 0.0;
+          if (zs) {  // xs + 0 == xs exactly
+            x0 = xt[0] - sx;
+            x1 = xt[1] - sy;
+            if (DIM == 3) x2 = xt[2] - sz;
+          } else {
+            x0 = xt[0] - (sx + R.sh[0]);
+            x1 = xt[1] - (sy + R.sh[1]);
+            if (DIM == 3) x2 = xt[2] - (sz + R.sh[2]);
           }
-          in = r2 < R.sup2;
+          double r2 = x0 * x0 + x1 * x1;
+          if (DIM == 3) r2 += x2 * x2;
+          bool in = valid && r2 < sup2 && !(skip_self && a == t);
           if (in && r2 == 0.0) {
             singular = 1;
             in = false;
           }
+          if (in) {
+            lsrc[warp][cnt][lane] = a;
+            lrng[warp][cnt][lane] = (unsigned char)k;
+            ++cnt;
+            ++n_in;
+          }
+        };
+        int a = a0;
+        for (; a + 4 <= a1; a += 4) {  // 4 broadcast loads in flight before the tests
+          if (__any_sync(0xffffffffu, cnt > kList - 4)) flush();
+          double sx[4], sy[4], sz[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            sx[q] = spx[a + q];
+            sy[q] = spy[a + q];
+            if (DIM == 3) sz[q] = spz[a + q];
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) test(a + q, sx[q], sy[q], sz[q]);
         }
-        const unsigned mask = __ballot_sync(0xffffffffu, in);
-        if (in) {
-          const int pos = cnt + __popc(mask & ((1u << lane) - 1u));
-          ls[pos] = a;
-          lr[pos] = (unsigned char)k;
+        for (; a < a1; ++a) {
+          if (__any_sync(0xffffffffu, cnt == kList)) flush();
+          test(a, spx[a], spy[a], DIM == 3 ? spz[a] : 0.0);
         }
-        cnt += __popc(mask);
-        n_in += __popc(mask);
-        __syncwarp();
-        if (cnt > kCap - 32) flush();
       }
     }
     flush();
-#pragma unroll
-    for (int j = 0; j < DIM; ++j)
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) u[j] += __shfl_xor_sync(0xffffffffu, u[j], o);
-    if (lane == 0) {
+    if (valid) {
       double* ut = ures + (size_t)tperm[t] * DIM;
 #pragma unroll
       for (int j = 0; j < DIM; ++j) {
@@ -250,23 +306,35 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     }
   }
   if (singular) atomicOr(flags, 1);
-  if (stats && lane == 0) {
-    atomicAdd(stats + 0, n_test);
-    atomicAdd(stats + 1, n_in);
-    atomicAdd(stats + 2, n_ref);
+  if (stats) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      n_test += __shfl_xor_sync(0xffffffffu, n_test, o);
+      n_ref += __shfl_xor_sync(0xffffffffu, n_ref, o);
+      n_in += __shfl_xor_sync(0xffffffffu, n_in, o);
+    }
+    if (lane == 0) {
+      atomicAdd(stats + 0, n_test);
+      atomicAdd(stats + 1, n_in);
+      atomicAdd(stats + 2, n_ref);
+    }
   }
 }
 
 }  // namespace
 
 void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves, int nleaf, const int* rng_start,
-                     const int* rng_box, const int* rng_info, const double* spts, int ns, const double* sstr,
+                     const int* rng_box, const int* rng_info, const int* subrange, const double* spts, int ns, const double* sstr,
                      const double* tpts, int nt, const int* tperm, int alias, double /*unused*/, double self_const,
                      double* ures, int* flags, unsigned long long* stats, cudaStream_t st) {
   if (nleaf <= 0) return;
-#define RES(K, D)                                                                                              \
-  k_residual<K, D><<<nleaf, kRBlock, 0, st>>>(rt, boxes, leaves, rng_start, rng_box, rng_info, spts, ns, sstr, \
-                                              tpts, nt, tperm, alias, self_const, ures, flags, stats)
+  const size_t dsm = (size_t)kWarps * kList * 32 * (sizeof(int) + 1);
+#define RES(K, D)                                                                                                \
+  do {                                                                                                           \
+    cudaFuncSetAttribute(k_residual<K, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);               \
+    k_residual<K, D><<<nleaf, kRBlock, dsm, st>>>(rt, boxes, leaves, rng_start, rng_box, rng_info, subrange, spts, ns, \
+                                                  sstr, tpts, nt, tperm, alias, self_const, ures, flags, stats); \
+  } while (0)
   if (rt.dim == 3) {
     if (rt.kernel == 0) RES(0, 3);
     else if (rt.kernel == 1) RES(1, 3);
