@@ -246,22 +246,31 @@ __global__ void __launch_bounds__(kW * 32, 2) k_z_mma(PWGrid g, int nc, const do
 }
 
 // ------------------------------------------------------------------ inv_xy --
+// 16 warps; the compressed C1 rows of the next four slabs arrive by cp.async
+// (double buffered) and feed the Y-stage B fragments directly through the
+// (my, m0) -> column table (zero outside the band); each warp's X-stage
+// outputs are loaded from HBM at the start of the group so the read of the
+// incoming proxies overlaps the Y stage.
+constexpr int kWI = 16;
+
 template <int PT, int PC, int NC>
-__global__ void __launch_bounds__(kW * 32, 1) k_inv_xy_mma(PWGrid g, const int* __restrict__ tboxes, int d,
-                                                          const double2* __restrict__ C, double pf,
-                                                          double* __restrict__ incoming) {
+__global__ void __launch_bounds__(kWI * 32, 1) k_inv_xy_mma(PWGrid g, const int* __restrict__ tboxes, int d,
+                                                           const double2* __restrict__ C, double pf,
+                                                           double* __restrict__ incoming) {
   constexpr int P8 = PT * 8;
+  constexpr int XTW = (4 * PT * PT + kWI - 1) / kWI;  // X tiles per warp
   const int p = PC > 0 ? PC : g.p, N = NC > 0 ? NC : g.N, M = (N - 1) / 2, ncol = g.ncol, pp = p * p;
   const int M1 = M + 1, NY8 = (N + 7) / 8 * 8, M18 = (M1 + 7) / 8 * 8, NX = 2 * M1, NX8 = (NX + 7) / 8 * 8;
-  const int SD = r8(2 * M18);      // D rows (s,my) of interleaved (m0, part)
   const int SA = r4(2 * NY8);      // A' rows iy, k' = 2 my + part
-  const int SX = r4(NX8 > 2 * M18 ? NX8 : 2 * M18);  // X-stage A rows (s,iy), k = (m0, part); B^T rows ix
+  const int SX = r4(NX8 > 2 * M18 ? NX8 : 2 * M18);
+  const int SC = 2 * ncol;         // staged C1 row (interleaved re, im)
   extern __shared__ double sm[];
   double* Ar = sm;                          // [P8][SA]  conj(E)^T re'
   double* Ai = Ar + P8 * SA;                // [P8][SA]  im'
   double* EXw = Ai + P8 * SA;               // [P8 (ix)][SX]  wt * E.re|im
-  double* D = EXw + P8 * SX;                // [4][NY8][SD]
-  double* dd = D + 4 * NY8 * SD;            // [4*P8][SX]
+  double* dd = EXw + P8 * SX;               // [4*P8][SX]
+  double* stg = dd + 4 * P8 * SX;           // [2][4][SC]
+  int* colidx = reinterpret_cast<int*>(stg + 2 * 4 * SC);  // [NY8][M18]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
   for (int e = tid; e < P8 * SA; e += blockDim.x) {  // conj(E)^T: re' = [Er | Ei], im' = [-Ei | Er]
     const int iy = e / SA, kk = e % SA, my = kk >> 1, part = kk & 1;
@@ -283,33 +292,62 @@ __global__ void __launch_bounds__(kW * 32, 1) k_inv_xy_mma(PWGrid g, const int* 
     }
     EXw[e] = v;
   }
-  for (int e = tid; e < 4 * NY8 * SD; e += blockDim.x) D[e] = 0.0;
+  for (int e = tid; e < NY8 * M18; e += blockDim.x) colidx[e] = -1;
+  __syncthreads();
+  for (int c = tid; c < ncol; c += blockDim.x) colidx[(g.col_my[c] + M) * M18 + g.col_m0[c]] = c;
   const int tb = blockIdx.x, j = blockIdx.y;
   const double2* Ci = C + ((size_t)tb * d + j) * (size_t)g.pz * ncol;
   double* out = incoming + ((size_t)tboxes[tb] * d + j) * (size_t)(p * pp);
   const int ngroups = (p + 3) / 4;
-  for (int grp = 0; grp < ngroups; ++grp) {
-    __syncthreads();
-    for (int s = 0; s < 4; ++s) {  // scatter the in-band columns into dense D
+  auto issue = [&](int grp, int buf) {
+    double* dst = stg + buf * 4 * SC;
+    for (int s = 0; s < 4; ++s) {
       const int iz = grp * 4 + s;
       if (iz >= p) break;
-      for (int c = tid; c < ncol; c += blockDim.x) {
-        const double2 v = Ci[(size_t)iz * ncol + c];
-        double* row = D + (s * NY8 + g.col_my[c] + M) * SD + 2 * g.col_m0[c];
-        row[0] = v.x;
-        row[1] = v.y;
-      }
+      const double* src = reinterpret_cast<const double*>(Ci + (size_t)iz * ncol);
+      for (int e = tid; e < SC; e += blockDim.x) cp_async8(dst + s * SC + e, src + e, true);
+    }
+    cp_commit();
+  };
+  issue(0, 0);
+  const int nit = PT, nm0 = M18 / 8;
+  for (int grp = 0; grp < ngroups; ++grp) {
+    const int buf = grp & 1;
+    __syncthreads();  // the buffer the next issue overwrites is free
+    if (grp + 1 < ngroups) {
+      issue(grp + 1, buf ^ 1);
+      cp_wait1();
+    } else {
+      cp_wait0();
     }
     __syncthreads();
-    // Y stage: d[(s,iy), m0] = sum_{(my,part)} A'[iy][(my,part)] D[s][my][(m0,part)]
-    const int nit = PT, nm0 = M18 / 8;
-    for (int tile = warp; tile < 4 * nit * nm0; tile += kW) {
+    // this warp's X-stage outputs: start their HBM reads now
+    double o0[XTW], o1[XTW];
+#pragma unroll
+    for (int i = 0; i < XTW; ++i) {
+      o0[i] = o1[i] = 0.0;
+      const int tile = warp + kWI * i;
+      if (tile < 4 * PT * PT) {
+        const int mt = tile / PT, nt = tile % PT;
+        const int s = mt / PT, iy = (mt % PT) * 8 + gq, iz = grp * 4 + s, ix = nt * 8 + 2 * t;
+        if (iz < p && iy < p) {
+          const double* o = out + (size_t)iz * pp + iy * p;
+          if (ix < p) o0[i] = o[ix];
+          if (ix + 1 < p) o1[i] = o[ix + 1];
+        }
+      }
+    }
+    const double* S = stg + buf * 4 * SC;
+    // Y stage: d[(s,iy), m0] = sum_{(my,part)} A'[iy][(my,part)] C1[s][col(my, m0)].part
+    for (int tile = warp; tile < 4 * nit * nm0; tile += kWI) {
       const int s = tile / (nit * nm0), it = (tile / nm0) % nit, nt = tile % nm0;
       double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
       const int ksteps = NY8 / 2;  // K' = 2*NY8, 4 per step
+      const int m0 = nt * 8 + gq;
       for (int ks = 0; ks < ksteps; ++ks) {
         const int kk = ks * 4 + t, my = kk >> 1, part = kk & 1;
-        const double bv = D[(s * NY8 + my) * SD + 2 * (nt * 8 + gq) + part];
+        const int cidx = colidx[my * M18 + m0];
+        const double bv = cidx >= 0 ? S[s * SC + 2 * cidx + part] : 0.0;
         dmma(cr0, cr1, Ar[(it * 8 + gq) * SA + kk], bv);
         dmma(ci0, ci1, Ai[(it * 8 + gq) * SA + kk], bv);
       }
@@ -322,8 +360,10 @@ __global__ void __launch_bounds__(kW * 32, 1) k_inv_xy_mma(PWGrid g, const int* 
     }
     __syncthreads();
     // X stage: out[(s,iy), ix] += pf * sum_{(m0,part)} dd[(s,iy)][(m0,part)] EXw[ix][(m0,part)]
-    const int xt = 4 * PT * PT;
-    for (int tile = warp; tile < xt; tile += kW) {
+#pragma unroll
+    for (int i = 0; i < XTW; ++i) {
+      const int tile = warp + kWI * i;
+      if (tile >= 4 * PT * PT) continue;
       const int mt = tile / PT, nt = tile % PT;
       double c0 = 0.0, c1 = 0.0;
       for (int ks = 0; ks < NX8 / 4; ++ks)
@@ -331,17 +371,10 @@ __global__ void __launch_bounds__(kW * 32, 1) k_inv_xy_mma(PWGrid g, const int* 
       const int s = mt / PT, iy = (mt % PT) * 8 + gq, iz = grp * 4 + s, ix = nt * 8 + 2 * t;
       if (iz < p && iy < p) {
         double* o = out + (size_t)iz * pp + iy * p;
-        if (ix < p) o[ix] += pf * c0;
-        if (ix + 1 < p) o[ix + 1] += pf * c1;
+        if (ix < p) o[ix] = o0[i] + pf * c0;
+        if (ix + 1 < p) o[ix + 1] = o1[i] + pf * c1;
       }
     }
-    __syncthreads();
-    for (int s = 0; s < 4; ++s)  // clear the scattered entries for the next group
-      for (int c = tid; c < ncol; c += blockDim.x) {
-        double* row = D + (s * NY8 + g.col_my[c] + M) * SD + 2 * g.col_m0[c];
-        row[0] = 0.0;
-        row[1] = 0.0;
-      }
   }
 }
 
@@ -420,13 +453,14 @@ void launch_inverse_mma(const PWGrid& g, const int* tboxes, int ntb, int d, cons
   }
   {
     const int P8 = PT * 8, M1 = g.M + 1, NY8 = (g.N + 7) / 8 * 8, M18 = (M1 + 7) / 8 * 8;
-    const int NX8 = (2 * M1 + 7) / 8 * 8, SD = r8(2 * M18), SA = r4(2 * NY8), SX = r4(NX8 > 2 * M18 ? NX8 : 2 * M18);
-    size_t smem = sizeof(double) * (2 * (size_t)P8 * SA + (size_t)P8 * SX + 4 * (size_t)NY8 * SD + 4 * (size_t)P8 * SX);
+    const int NX8 = (2 * M1 + 7) / 8 * 8, SA = r4(2 * NY8), SX = r4(NX8 > 2 * M18 ? NX8 : 2 * M18);
+    size_t smem = sizeof(double) * (2 * (size_t)P8 * SA + (size_t)P8 * SX + 4 * (size_t)P8 * SX +
+                                    2 * 4 * 2 * (size_t)g.ncol) + sizeof(int) * (size_t)NY8 * M18;
     dim3 grid(ntb, d);
-#define IX(PT_, PC_, NC_)                                                                   \
-  do {                                                                                      \
-    attr((const void*)k_inv_xy_mma<PT_, PC_, NC_>, smem);                                   \
-    k_inv_xy_mma<PT_, PC_, NC_><<<grid, kW * 32, smem, st>>>(g, tboxes, d, C, pf, incoming); \
+#define IX(PT_, PC_, NC_)                                                                    \
+  do {                                                                                       \
+    attr((const void*)k_inv_xy_mma<PT_, PC_, NC_>, smem);                                    \
+    k_inv_xy_mma<PT_, PC_, NC_><<<grid, kWI * 32, smem, st>>>(g, tboxes, d, C, pf, incoming); \
   } while (0)
     if (g.p == 23 && g.N == 33) IX(3, 23, 33);
     else if (g.p == 22 && g.N == 33) IX(3, 22, 33);
