@@ -392,6 +392,84 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode) {
   pr.ready = true;
 }
 
+// Sibling groups for k_acc_group: consecutive plane-wave targets with one
+// parent.  Each colleague entry (slot, tau) of child c sits at the
+// parent-relative position c + tau in {-1..2}^d; the group kernel sums every
+// position inside child c's 3^d window, so the level is grouped only when
+// those windows reproduce each target's entry list exactly (one slot per
+// position, no repeats, the leaf's own position the only one skipped).
+// Otherwise the lists are left empty and the level stays per-target.
+static void build_groups(const HostTree& t, int lev, const std::vector<int>& tbx, const std::vector<int>& es,
+                         const std::vector<int>& eslot, const std::vector<int>& etau, std::vector<int>& gstart,
+                         std::vector<int>& gslot, std::vector<int>& tmeta) {
+  const int d = t.dim, ntg = (int)tbx.size();
+  if (ntg == 0) return;
+  const int64_t side_int = int64_t(1) << (30 - lev);
+  for (int i = 0; i < ntg; ++i)
+    if (i == 0 || t.boxes[tbx[i]].parent != t.boxes[tbx[i - 1]].parent) gstart.push_back(i);
+  gstart.push_back(ntg);
+  const int ng = (int)gstart.size() - 1;
+  gslot.assign((size_t)ng * 64, -1);
+  tmeta.assign(ntg, 0);
+  auto pcode = [&](int x, int y, int z) { return (x + 1) + 4 * (y + 1) + 16 * (d == 3 ? z + 1 : 1); };
+  uint64_t window[8];
+  for (int c = 0; c < (1 << d); ++c) {
+    const int cx = c & 1, cy = (c >> 1) & 1, cz = d == 3 ? (c >> 2) & 1 : 0;
+    uint64_t m = 0;
+    for (int z = (d == 3 ? -1 : 0); z <= (d == 3 ? 1 : 0); ++z)
+      for (int y = -1; y <= 1; ++y)
+        for (int x = -1; x <= 1; ++x) m |= uint64_t(1) << pcode(cx + x, cy + y, cz + z);
+    window[c] = m;
+  }
+  int ok = 1;
+#pragma omp parallel for schedule(static) reduction(min : ok)
+  for (int gi = 0; gi < ng; ++gi) {
+    const int i0 = gstart[gi], i1 = gstart[gi + 1];
+    const Box& P = t.boxes[t.boxes[tbx[i0]].parent];
+    int* slot = gslot.data() + (size_t)gi * 64;
+    uint64_t emask[8], umask = 0;
+    int cc[8];
+    bool good = i1 - i0 <= (1 << d);
+    for (int i = i0; i < i1 && good; ++i) {
+      const Box& B = t.boxes[tbx[i]];
+      int c = 0;
+      for (int ax = 0; ax < d; ++ax) {
+        const int64_t diff = int64_t(B.anchor[ax]) - int64_t(P.anchor[ax]);
+        if (diff != 0 && diff != side_int) good = false;
+        c |= (diff == side_int) << ax;
+      }
+      const int k = i - i0;
+      cc[k] = c;
+      emask[k] = 0;
+      for (int e = es[i]; e < es[i + 1]; ++e) {
+        const int code = etau[e];
+        const int pc = pcode((c & 1) + code % 3 - 1, ((c >> 1) & 1) + (code / 3) % 3 - 1,
+                             ((c >> 2) & 1) + code / 9 - 1);
+        if ((emask[k] >> pc) & 1) good = false;
+        emask[k] |= uint64_t(1) << pc;
+        if (slot[pc] == -1) slot[pc] = eslot[e];
+        else if (slot[pc] != eslot[e]) good = false;
+      }
+      umask |= emask[k];
+    }
+    for (int i = i0; i < i1 && good; ++i) {
+      const int k = i - i0, c = cc[k];
+      const uint64_t self = uint64_t(1) << pcode(c & 1, (c >> 1) & 1, (c >> 2) & 1);
+      uint64_t expect = window[c] & umask;
+      const bool sub = t.boxes[tbx[i]].leaf && (umask & self);
+      if (sub) expect &= ~self;
+      if (expect != emask[k]) good = false;
+      tmeta[i] = c | (sub ? 8 : 0);
+    }
+    if (!good) ok = 0;
+  }
+  if (!ok) {
+    gstart.clear();
+    gslot.clear();
+    tmeta.clear();
+  }
+}
+
 void Context::upload_tree_lists(const int32_t* qs) {
   Problem& pr = prob_;
   const HostTree& t = pr.tree;
@@ -460,9 +538,10 @@ void Context::upload_tree_lists(const int32_t* qs) {
   // per-level lists
   const int L = t.max_level + 1;
   struct LV {
-    std::vector<int> m_out, m_in, m_ci, i_in, i_out, i_ci, sbx, tbx, es, eslot, etau;
+    std::vector<int> m_out, m_in, m_ci, i_in, i_out, i_ci, sbx, tbx, es, eslot, etau, gstart, gslot, tmeta;
   };
   std::vector<LV> lv(L);
+  const bool use_groups = !std::getenv("SDMK_NO_GROUP");
   std::vector<int> gslot(nb, -1);
   bool bad_tau = false;
   for (int lev = 0; lev < L; ++lev) {
@@ -537,6 +616,7 @@ void Context::upload_tree_lists(const int32_t* qs) {
 #pragma omp parallel for schedule(static)
     for (int i = 0; i < nl; ++i)
       if (cnt[i] > 0) entries(ids[i], V.eslot.data() + eoff[i], V.etau.data() + eoff[i]);
+    if (lev > 0 && use_groups) build_groups(t, lev, V.tbx, V.es, V.eslot, V.etau, V.gstart, V.gslot, V.tmeta);
   }
   if (bad_tau) throw RuntimeError("colleague offset outside {-1,0,1}");
   // root lists: box 0 with one zero-offset entry
@@ -549,13 +629,14 @@ void Context::upload_tree_lists(const int32_t* qs) {
          o_rinfo = pk.add(rinfo), o_rid = pk.add(root_ids), o_res = pk.add(root_es), o_rsl = pk.add(root_slot),
          o_rta = pk.add(root_tau);
   struct Off {
-    size_t m_out, m_in, m_ci, i_in, i_out, i_ci, sbx, tbx, es, eslot, etau;
+    size_t m_out, m_in, m_ci, i_in, i_out, i_ci, sbx, tbx, es, eslot, etau, gstart, gslot, tmeta;
   };
   std::vector<Off> off(L);
   for (int lev = 0; lev < L; ++lev) {
     LV& V = lv[lev];
-    off[lev] = {pk.add(V.m_out), pk.add(V.m_in), pk.add(V.m_ci), pk.add(V.i_in), pk.add(V.i_out), pk.add(V.i_ci),
-                pk.add(V.sbx),   pk.add(V.tbx),  pk.add(V.es),   pk.add(V.eslot), pk.add(V.etau)};
+    off[lev] = {pk.add(V.m_out), pk.add(V.m_in),  pk.add(V.m_ci),   pk.add(V.i_in),   pk.add(V.i_out),
+                pk.add(V.i_ci),  pk.add(V.sbx),   pk.add(V.tbx),    pk.add(V.es),     pk.add(V.eslot),
+                pk.add(V.etau),  pk.add(V.gstart), pk.add(V.gslot), pk.add(V.tmeta)};
   }
   char* h = (char*)pinned_.get("tree", pk.total + 64);
   for (auto& it : pk.items)
@@ -590,6 +671,10 @@ void Context::upload_tree_lists(const int32_t* qs) {
     X.ent_start = (int*)(dv + off[lev].es);
     X.ent_slot = (int*)(dv + off[lev].eslot);
     X.ent_tau = (int*)(dv + off[lev].etau);
+    X.grp_start_h = V.gstart;
+    X.grp_tstart = (int*)(dv + off[lev].gstart);
+    X.grp_slot = (int*)(dv + off[lev].gslot);
+    X.t_meta = (int*)(dv + off[lev].tmeta);
   }
   // root lists live after the per-level ones in the same blob
   root_dev_ids_ = (int*)(dv + o_rid);
@@ -723,17 +808,30 @@ void Context::run_downward() {  // dmk.cpp:705-857
           launch_forward(g, X.src_boxes + s0, n, pr.nch, og, B, G + (size_t)s0 * pr.nch * g.nhalf, st_);
         launches_ += 2;
       }
-      for (int t0 = 0; t0 < X.n_tgt; t0 += chunk_tgt) {
-        int n = std::min(chunk_tgt, X.n_tgt - t0);
+      const std::vector<int>& gs = X.grp_start_h;
+      const int ng = gs.empty() ? 0 : (int)gs.size() - 1;
+      for (int t0 = 0, g0 = 0; t0 < X.n_tgt;) {
+        int n = std::min(chunk_tgt, X.n_tgt - t0), g1 = g0;
+        if (ng > 0) {  // chunk boundaries on group boundaries
+          while (g1 < ng && gs[g1 + 1] - t0 <= chunk_tgt) ++g1;
+          if (g1 == g0) g1 = g0 + 1;
+          n = gs[g1] - t0;
+        }
         double2* F = arena_.as<double2>("pw_F", (size_t)n * d * g.nhalf);
         double2* C = arena_.as<double2>("pw_C", (size_t)n * d * g.pz * g.ncol);
-        launch_accumulate_symbol(g, P.kernel, n, X.ent_start + t0, X.ent_slot, X.ent_tau, G, pr.nch,
-                                 dA + (size_t)lev * S, h, F, st_);
+        if (ng > 0)
+          launch_accumulate_group(g, P.kernel, g1 - g0, X.grp_tstart + g0, X.grp_slot + (size_t)g0 * 64, X.t_meta,
+                                  t0, G, dA + (size_t)lev * S, h, F, st_);
+        else
+          launch_accumulate_symbol(g, P.kernel, n, X.ent_start + t0, X.ent_slot, X.ent_tau, G, pr.nch,
+                                   dA + (size_t)lev * S, h, F, st_);
         if (use_mma)
           launch_inverse_mma(g, X.tgt_boxes + t0, n, d, F, C, pf, in, st_);
         else
           launch_inverse(g, X.tgt_boxes + t0, n, d, F, C, pf, in, st_);
         launches_ += 3;
+        t0 += n;
+        g0 = g1;
       }
       cudaEventRecord(e1, st_);
       cudaEventSynchronize(e1);

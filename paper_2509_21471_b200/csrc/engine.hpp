@@ -83,6 +83,9 @@ struct Problem {
     int *src_boxes = nullptr, *tgt_boxes = nullptr;
     int *ent_start = nullptr, *ent_slot = nullptr, *ent_tau = nullptr;
     int max_entries = 0;
+    // sibling groups for the plane-wave accumulation (empty: per-target kernel)
+    std::vector<int> grp_start_h;  // host copy of grp_tstart, for chunking
+    int *grp_tstart = nullptr, *grp_slot = nullptr, *t_meta = nullptr;
   };
   std::vector<LevelLists> levels;
 };

@@ -110,6 +110,14 @@ void launch_forward(const PWGrid& g, const int* boxes, int nbox, int nch, const 
 void launch_accumulate_symbol(const PWGrid& g, int kernel, int ntb, const int* ent_start,
                               const int* ent_slot, const int* ent_tau, const double2* G, int nch,
                               const double* A, double h, double2* F, cudaStream_t st);
+// Same sums by sibling group: grp_tstart[ngroups + 1] indexes the level's
+// target list; grp_slot[group][64] is the G slot at each parent-relative
+// position (x + 4 y + 16 z over {-1..2}^d shifted by 1; 2D uses z = 0) or -1;
+// t_meta[target] = child code | 8 if the target's own G must be removed.
+// F rows are target index - t_base.
+void launch_accumulate_group(const PWGrid& g, int kernel, int ngroups, const int* grp_tstart, const int* grp_slot,
+                             const int* t_meta, int t_base, const double2* G, const double* A, double h,
+                             double2* F, cudaStream_t st);
 // incoming[box(t)][j] += pf * Re(inverse(F[t][j])); C is scratch
 void launch_inverse(const PWGrid& g, const int* tboxes, int ntb, int d, const double2* F,
                     double2* C, double pf, double* incoming, cudaStream_t st);

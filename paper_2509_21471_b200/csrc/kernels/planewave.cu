@@ -22,6 +22,9 @@
 #include "common.cuh"
 #include "launch.hpp"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace sdmkb {
 
 namespace {
@@ -104,6 +107,75 @@ __global__ void __launch_bounds__(kPWBlock) k_fwd_z(PWGrid g, int nch, const dou
 }
 
 // ------------------------------------------------- accumulate + symbol --
+// Kernel symbol applied to the phased colleague sum Ph (dmk.cpp:387-469):
+// out[j] = F_j(k) for k = h m; A[|m|^2] is the level's radial symbol table.
+template <int KERNEL, int DIM, int NCH>
+__device__ __forceinline__ void apply_symbol(const double2 (&Ph)[NCH], int m0, int my, int mz,
+                                             const double* __restrict__ A, double h, double2 (&out)[DIM]) {
+#pragma unroll
+  for (int j = 0; j < DIM; ++j) out[j] = make_double2(0.0, 0.0);
+  const int s2 = m0 * m0 + my * my + mz * mz;
+  const double av = A[s2];
+  const double k0 = h * m0, k1 = h * my, k2 = DIM == 3 ? h * mz : 0.0;
+  const double kk = k0 * k0 + k1 * k1 + k2 * k2;
+  if (av != 0.0) {
+    if (KERNEL == 0) {  // Stokeslet: A (k^2 f - k (k.f))
+      double2 kf;
+      kf.x = k0 * Ph[0].x + k1 * Ph[1].x + (DIM == 3 ? k2 * Ph[DIM - 1].x : 0.0);
+      kf.y = k0 * Ph[0].y + k1 * Ph[1].y + (DIM == 3 ? k2 * Ph[DIM - 1].y : 0.0);
+      const double kv[3] = {k0, k1, k2};
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) {
+        out[j].x = av * (kk * Ph[j].x - kv[j] * kf.x);
+        out[j].y = av * (kk * Ph[j].y - kv[j] * kf.y);
+      }
+    } else if (KERNEL == 1) {  // stresslet: i A (k^2 Sk - k (kSk) + k tr(S) k^2 / (d+2))
+      const double kv[3] = {k0, k1, k2};
+      double2 Sk[3], kSk, wtr;
+      if (DIM == 3) {
+        const double2 S00 = Ph[0], S11 = Ph[1], S22 = Ph[2], S01 = Ph[3], S02 = Ph[4], S12 = Ph[5];
+        Sk[0] = make_double2(S00.x * k0 + S01.x * k1 + S02.x * k2, S00.y * k0 + S01.y * k1 + S02.y * k2);
+        Sk[1] = make_double2(S01.x * k0 + S11.x * k1 + S12.x * k2, S01.y * k0 + S11.y * k1 + S12.y * k2);
+        Sk[2] = make_double2(S02.x * k0 + S12.x * k1 + S22.x * k2, S02.y * k0 + S12.y * k1 + S22.y * k2);
+        kSk = make_double2(k0 * Sk[0].x + k1 * Sk[1].x + k2 * Sk[2].x, k0 * Sk[0].y + k1 * Sk[1].y + k2 * Sk[2].y);
+        const double q = kk / 5.0;
+        wtr = make_double2((S00.x + S11.x + S22.x) * q, (S00.y + S11.y + S22.y) * q);
+      } else {
+        const double2 S00 = Ph[0], S11 = Ph[1], S01 = Ph[2];
+        Sk[0] = make_double2(S00.x * k0 + S01.x * k1, S00.y * k0 + S01.y * k1);
+        Sk[1] = make_double2(S01.x * k0 + S11.x * k1, S01.y * k0 + S11.y * k1);
+        Sk[2] = make_double2(0.0, 0.0);
+        kSk = make_double2(k0 * Sk[0].x + k1 * Sk[1].x, k0 * Sk[0].y + k1 * Sk[1].y);
+        const double q = kk / 4.0;
+        wtr = make_double2((S00.x + S11.x) * q, (S00.y + S11.y) * q);
+      }
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) {
+        double2 v = make_double2(av * (kk * Sk[j].x - kv[j] * kSk.x + kv[j] * wtr.x),
+                                 av * (kk * Sk[j].y - kv[j] * kSk.y + kv[j] * wtr.y));
+        out[j] = make_double2(-v.y, v.x);  // times i
+      }
+    } else {  // rotlet: -(i/2) A (g x k)
+      const double ha = -0.5 * av;
+      if (DIM == 3) {
+        const double2 g0 = Ph[0], g1 = Ph[1], g2 = Ph[2];
+        double2 c0 = make_double2(g1.x * k2 - g2.x * k1, g1.y * k2 - g2.y * k1);
+        double2 c1 = make_double2(g2.x * k0 - g0.x * k2, g2.y * k0 - g0.y * k2);
+        double2 c2 = make_double2(g0.x * k1 - g1.x * k0, g0.y * k1 - g1.y * k0);
+        out[0] = make_double2(-ha * c0.y, ha * c0.x);
+        out[1] = make_double2(-ha * c1.y, ha * c1.x);
+        out[DIM - 1] = make_double2(-ha * c2.y, ha * c2.x);
+      } else {
+        const double2 g0 = Ph[0];
+        double2 a = make_double2(k1 * g0.x, k1 * g0.y);
+        double2 b = make_double2(k0 * g0.x, k0 * g0.y);
+        out[0] = make_double2(-ha * a.y, ha * a.x);
+        out[1] = make_double2(ha * b.y, -ha * b.x);
+      }
+    }
+  }
+}
+
 template <int KERNEL, int DIM>
 __global__ void __launch_bounds__(kPWBlock) k_acc_sym(PWGrid g, const int* __restrict__ ent_start,
                                                       const int* __restrict__ ent_slot,
@@ -153,71 +225,221 @@ __global__ void __launch_bounds__(kPWBlock) k_acc_sym(PWGrid g, const int* __res
       Ph[k].x = S0[k].x + w1r * (S1[k].x + S2[k].x) - w1i * (S1[k].y - S2[k].y);
       Ph[k].y = S0[k].y + w1r * (S1[k].y + S2[k].y) + w1i * (S1[k].x - S2[k].x);
     }
-    const int s2 = m0 * m0 + my * my + mz * mz;
-    const double av = A[s2];
-    const double k0 = h * m0, k1 = h * my, k2 = DIM == 3 ? h * mz : 0.0;
-    const double kk = k0 * k0 + k1 * k1 + k2 * k2;
     double2 out[DIM];
+    apply_symbol<KERNEL, DIM, NCH>(Ph, m0, my, mz, A, h, out);
 #pragma unroll
-    for (int j = 0; j < DIM; ++j) out[j] = make_double2(0.0, 0.0);
-    if (av != 0.0) {
-      if (KERNEL == 0) {  // Stokeslet: A (k^2 f - k (k.f))
-        double2 kf;
-        kf.x = k0 * Ph[0].x + k1 * Ph[1].x + (DIM == 3 ? k2 * Ph[DIM - 1].x : 0.0);
-        kf.y = k0 * Ph[0].y + k1 * Ph[1].y + (DIM == 3 ? k2 * Ph[DIM - 1].y : 0.0);
-        const double kv[3] = {k0, k1, k2};
+    for (int j = 0; j < DIM; ++j) Fo[(size_t)j * nhalf + idx] = out[j];
+  }
+}
+
+// Sibling-group accumulation: the same sums as k_acc_sym, grouped so that
+// each colleague transform is read once per parent instead of once per
+// target.  The 2^d children of one parent only see colleagues inside the
+// parent's 4^d neighbourhood, positions pos in {-1..2}^d relative to the
+// parent's anchor; child c sees the boxes at pos in c + {-1,0,1}^d, with
+// phase w^{m.(pos - c)} = w^{-m.c} w^{m.pos}.  So every colleague is phased
+// once per group, H(pos) = w^{m.pos} G(pos); the 3^d window sums of H are
+// formed separably (two windows per axis sharing one pair sum); child c
+// takes w^{-m.c} window_c, without its own H when it is a leaf (the
+// reference skips a leaf's self entry, dmk.cpp:775).  The host verifies
+// that the windows reproduce each target's reference entry list
+// (dmk.cpp:760-797) and keeps levels where they would not (the periodic top
+// levels) on k_acc_sym.
+//
+// Data movement: one CTA streams a group through mode chunks of kGM modes;
+// each neighbourhood row (yi, zi) of a chunk is 4 positions x NCH channels
+// of contiguous kGM-mode segments, fetched by the TMA engine (1D bulk
+// copies, mbarrier byte count) into a kGS-stage shared ring, so the loads of
+// the next rows are in flight while this row is summed (thread per mode).
+constexpr int kGroupPos = 64;
+constexpr int kGM = 128;  // modes per chunk = threads per CTA
+
+__device__ __forceinline__ double2 phase3(int r, double2 v) {  // w^r v, w = exp(-2 pi i / 3)
+  const double ci = r == 0 ? 0.0 : (r == 1 ? -0.8660254037844386467637232 : 0.8660254037844386467637232);
+  const double cr = r == 0 ? 1.0 : -0.5;
+  return make_double2(cr * v.x - ci * v.y, cr * v.y + ci * v.x);
+}
+
+// Shape per (kernel, dim, passes): ring stages and resident CTAs per SM,
+// sized so registers (one pass keeps 8 or 4 windows x channels live) and
+// the shared ring both fit; the stage count divides the rows per chunk so
+// every row's stage is a compile-time constant.
+template <int KERNEL, int DIM, int ZH>
+struct GroupCfg {
+  static constexpr int kNch = KERNEL == 0 ? DIM : (KERNEL == 1 ? (DIM == 3 ? 6 : 3) : (DIM == 3 ? 3 : 1));
+  static constexpr int kRowBytes = 4 * kNch * kGM * 16;
+  static constexpr int kRows = ZH * 4 * (DIM == 3 ? (ZH == 1 ? 4 : 3) : 1);  // rows per chunk
+  static constexpr int kMinBlocks = (DIM == 3 && ZH == 1) || kNch > 3 ? 2 : 3;
+  static constexpr int kZeroBytes = kNch * kGM * 16;  // stands in for absent positions
+  static constexpr int kMaxStages = (227 * 1024 / kMinBlocks - 4096 - kZeroBytes) / kRowBytes;
+  static constexpr int stages(int n) { return n <= 1 ? 1 : (kRows % n == 0 ? n : stages(n - 1)); }
+  static constexpr int kStages = stages(kMaxStages);
+  static constexpr int kBytes = kStages * kRowBytes;
+};
+constexpr int kGroupThreads = kGM + 32;  // 4 consumer warps + 1 TMA producer warp
+
+template <int KERNEL, int DIM, int ZH>
+__global__ void __launch_bounds__(kGroupThreads, GroupCfg<KERNEL, DIM, ZH>::kMinBlocks)
+    k_acc_group(PWGrid g, const int* __restrict__ grp_tstart, const int* __restrict__ grp_slot,
+                const int* __restrict__ t_meta, int t_base, const double2* __restrict__ G,
+                const double* __restrict__ A, double h, double2* __restrict__ F) {
+  using Cfg = GroupCfg<KERNEL, DIM, ZH>;
+  constexpr int NCH = Cfg::kNch;
+  constexpr int NCZ = DIM == 3 ? 2 : 1;  // z windows (children along z)
+  constexpr int CZP = NCZ / ZH;          // z windows per pass
+  constexpr int NW = 4 * CZP;            // windows per pass
+  constexpr int NL = DIM == 3 ? (ZH == 1 ? 4 : 3) : 1;  // z layers per pass
+  constexpr int RP = 4 * NL;                             // rows per pass
+  constexpr int RC = Cfg::kRows;                         // rows per chunk
+  constexpr int NS = Cfg::kStages;
+  static_assert(NS >= 2 && RC % NS == 0, "ring shape");
+  constexpr double kS3 = 0.8660254037844386467637232;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double2* ring = reinterpret_cast<double2*>(smraw);  // [NS][4][NCH][kGM]
+  __shared__ uint64_t full[NS], empty[NS];
+  __shared__ int s_slot[kGroupPos];
+  __shared__ int s_tgt[8];  // child code -> target index in the group | leaf << 8, or -1
+  __shared__ __align__(16) double2 zero[NCH * kGM];
+  const int grp = blockIdx.x, tid = threadIdx.x;
+  const int ta = grp_tstart[grp], nt = grp_tstart[grp + 1] - ta;
+  if (tid < kGroupPos) s_slot[tid] = grp_slot[(size_t)grp * kGroupPos + tid];
+  if (tid < 8) s_tgt[tid] = -1;
+  for (int e = tid; e < NCH * kGM; e += kGroupThreads) zero[e] = make_double2(0.0, 0.0);
+  if (tid < NS) {
+    dev::mbar_init(&full[tid], 1);
+    dev::mbar_init(&empty[tid], kGM / 32);
+  }
+  if (tid == 0) dev::mbar_fence_init();
+  __syncthreads();
+  if (tid < nt) {
+    const int meta = t_meta[ta + tid];
+    s_tgt[meta & 7] = tid | ((meta & 8) << 5);
+  }
+  __syncthreads();
+  const int nhalf = g.nhalf;
+  const size_t bstride = (size_t)NCH * nhalf;
+  const int nchunk = (nhalf + kGM - 1) / kGM;
+  const int my_chunks = (nchunk - (int)blockIdx.y + (int)gridDim.y - 1) / (int)gridDim.y;
+  if (tid >= kGM) {  // producer warp: refill each stage once the 4 consumer warps released it
+    if (tid == kGM) {
+      const int nrows = my_chunks * RC;
+      for (int i = 0; i < nrows; ++i) {
+        if (i >= NS) dev::mbar_wait(&empty[i % NS], (uint32_t)((i / NS - 1) & 1));
+        const int ck = (int)blockIdx.y + (i / RC) * (int)gridDim.y, r = i % RC;
+        const int zh = r / RP, rr = r % RP;
+        const int yi = rr & 3, zi = DIM == 3 ? zh + (rr >> 2) : 1;
+        const int m_begin = ck * kGM, nm = min(kGM, nhalf - m_begin);
+        const uint32_t seg = (uint32_t)nm * 16u;
+        const int* srow = s_slot + 4 * yi + 16 * zi;
+        uint32_t tx = 0;
 #pragma unroll
-        for (int j = 0; j < DIM; ++j) {
-          out[j].x = av * (kk * Ph[j].x - kv[j] * kf.x);
-          out[j].y = av * (kk * Ph[j].y - kv[j] * kf.y);
-        }
-      } else if (KERNEL == 1) {  // stresslet: i A (k^2 Sk - k (kSk) + k tr(S) k^2 / (d+2))
-        const double kv[3] = {k0, k1, k2};
-        double2 Sk[3], kSk, wtr;
-        if (DIM == 3) {
-          const double2 S00 = Ph[0], S11 = Ph[1], S22 = Ph[2], S01 = Ph[3], S02 = Ph[4], S12 = Ph[5];
-          Sk[0] = make_double2(S00.x * k0 + S01.x * k1 + S02.x * k2, S00.y * k0 + S01.y * k1 + S02.y * k2);
-          Sk[1] = make_double2(S01.x * k0 + S11.x * k1 + S12.x * k2, S01.y * k0 + S11.y * k1 + S12.y * k2);
-          Sk[2] = make_double2(S02.x * k0 + S12.x * k1 + S22.x * k2, S02.y * k0 + S12.y * k1 + S22.y * k2);
-          kSk = make_double2(k0 * Sk[0].x + k1 * Sk[1].x + k2 * Sk[2].x, k0 * Sk[0].y + k1 * Sk[1].y + k2 * Sk[2].y);
-          const double q = kk / 5.0;
-          wtr = make_double2((S00.x + S11.x + S22.x) * q, (S00.y + S11.y + S22.y) * q);
-        } else {
-          const double2 S00 = Ph[0], S11 = Ph[1], S01 = Ph[2];
-          Sk[0] = make_double2(S00.x * k0 + S01.x * k1, S00.y * k0 + S01.y * k1);
-          Sk[1] = make_double2(S01.x * k0 + S11.x * k1, S01.y * k0 + S11.y * k1);
-          Sk[2] = make_double2(0.0, 0.0);
-          kSk = make_double2(k0 * Sk[0].x + k1 * Sk[1].x, k0 * Sk[0].y + k1 * Sk[1].y);
-          const double q = kk / 4.0;
-          wtr = make_double2((S00.x + S11.x) * q, (S00.y + S11.y) * q);
-        }
+        for (int xi = 0; xi < 4; ++xi) tx += srow[xi] >= 0 ? NCH * seg : 0u;
+        uint64_t* bar = &full[i % NS];
+        dev::mbar_expect_tx(bar, tx);
+        double2* st = ring + (size_t)(i % NS) * 4 * NCH * kGM;
 #pragma unroll
-        for (int j = 0; j < DIM; ++j) {
-          double2 v = make_double2(av * (kk * Sk[j].x - kv[j] * kSk.x + kv[j] * wtr.x),
-                                   av * (kk * Sk[j].y - kv[j] * kSk.y + kv[j] * wtr.y));
-          out[j] = make_double2(-v.y, v.x);  // times i
-        }
-      } else {  // rotlet: -(i/2) A (g x k)
-        const double ha = -0.5 * av;
-        if (DIM == 3) {
-          const double2 g0 = Ph[0], g1 = Ph[1], g2 = Ph[2];
-          double2 c0 = make_double2(g1.x * k2 - g2.x * k1, g1.y * k2 - g2.y * k1);
-          double2 c1 = make_double2(g2.x * k0 - g0.x * k2, g2.y * k0 - g0.y * k2);
-          double2 c2 = make_double2(g0.x * k1 - g1.x * k0, g0.y * k1 - g1.y * k0);
-          out[0] = make_double2(-ha * c0.y, ha * c0.x);
-          out[1] = make_double2(-ha * c1.y, ha * c1.x);
-          out[DIM - 1] = make_double2(-ha * c2.y, ha * c2.x);
-        } else {
-          const double2 g0 = Ph[0];
-          double2 a = make_double2(k1 * g0.x, k1 * g0.y);
-          double2 b = make_double2(k0 * g0.x, k0 * g0.y);
-          out[0] = make_double2(-ha * a.y, ha * a.x);
-          out[1] = make_double2(ha * b.y, -ha * b.x);
+        for (int xi = 0; xi < 4; ++xi) {
+          const int sl = srow[xi];
+          if (sl < 0) continue;
+#pragma unroll
+          for (int k = 0; k < NCH; ++k)
+            dev::bulk_g2s(st + (xi * NCH + k) * kGM, G + (size_t)sl * bstride + (size_t)k * nhalf + m_begin, seg,
+                          bar);
         }
       }
     }
+    return;
+  }
+  for (int it = 0; it < my_chunks; ++it) {
+    const int ck = (int)blockIdx.y + it * (int)gridDim.y;
+    const int idx = ck * kGM + tid;
+    const bool act = idx < nhalf;
+    int m0 = 0, my = 0, mz = 0;
+    if (act) {
+      const int code = g.mode_code[idx];
+      const int c = code & 0xffff;
+      mz = (code >> 16) - g.Mz;
+      m0 = g.col_m0[c];
+      my = g.col_my[c];
+    }
+    const int a0 = ((m0 % 3) + 3) % 3, a1 = ((my % 3) + 3) % 3, a2 = ((mz % 3) + 3) % 3;
+    // x phases w^{m0 (xi - 1)} as coefficients (xi = 1 is 1); y/z phases per row
+    const double pxr = a0 == 0 ? 1.0 : -0.5;
+    const double pxi = a0 == 0 ? 0.0 : (a0 == 1 ? -kS3 : kS3);  // w^{a0}
+    const double2 px2 = make_double2(pxr, pxi), px0 = make_double2(pxr, -pxi);  // w^{m0}, w^{-m0}
+    const double2 px3 = make_double2(pxr * pxr - pxi * pxi, 2.0 * pxr * pxi);   // w^{2 m0}
+    const int ry[4] = {(3 - a1) % 3, 0, a1, (2 * a1) % 3};
+    const int rz[4] = {(3 - a2) % 3, 0, a2, (2 * a2) % 3};
 #pragma unroll
-    for (int j = 0; j < DIM; ++j) Fo[(size_t)j * nhalf + idx] = out[j];
+    for (int zh = 0; zh < ZH; ++zh) {
+      double2 W[NW][NCH];
+#pragma unroll
+      for (int w = 0; w < NW; ++w)
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) W[w][k] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int rr = 0; rr < RP; ++rr) {
+        const int r = zh * RP + rr;
+        const int yi = rr & 3, zi = DIM == 3 ? zh + (rr >> 2) : 1;
+        const int stage = r % NS;
+        dev::mbar_wait(&full[stage], (uint32_t)((it * (RC / NS) + r / NS) & 1));
+        const double2* st = ring + (size_t)stage * 4 * NCH * kGM + tid;
+        const double2* q[4];
+#pragma unroll
+        for (int xi = 0; xi < 4; ++xi) q[xi] = s_slot[xi + 4 * yi + 16 * zi] >= 0 ? st + xi * NCH * kGM : zero + tid;
+        int ryz = ry[yi] + (DIM == 3 ? rz[zi] : 0);
+        ryz = ryz >= 3 ? ryz - 3 : ryz;
+        const double rr_ = ryz == 0 ? 1.0 : -0.5;
+        const double ri_ = ryz == 0 ? 0.0 : (ryz == 1 ? -kS3 : kS3);
+        const double2 prow = make_double2(rr_, ri_);
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+          const double2 v0 = dev::cmul(px0, q[0][k * kGM]);
+          const double2 v1 = q[1][k * kGM];
+          const double2 v2 = dev::cmul(px2, q[2][k * kGM]);
+          const double2 v3 = dev::cmul(px3, q[3][k * kGM]);
+          const double2 mid = make_double2(v1.x + v2.x, v1.y + v2.y);
+          const double2 X[2] = {dev::cmul(prow, make_double2(v0.x + mid.x, v0.y + mid.y)),
+                                dev::cmul(prow, make_double2(mid.x + v3.x, mid.y + v3.y))};
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            const int cx = w & 1, cy = (w >> 1) & 1, czg = DIM == 3 ? zh + (w >> 2) : 0;
+            const bool in = yi >= cy && yi <= cy + 2 && (DIM == 2 || (zi >= czg && zi <= czg + 2));
+            if (!in) continue;
+            W[w][k].x += X[cx].x;
+            W[w][k].y += X[cx].y;
+            if (yi == cy + 1 && (DIM == 2 || zi == czg + 1)) {  // the window's own position
+              const int tg = s_tgt[cx + 2 * cy + 4 * czg];
+              if (tg >= 0 && (tg >> 8)) {  // a leaf child leaves its own H out
+                const double2 sv = dev::cmul(prow, cx ? v2 : v1);
+                W[w][k].x -= sv.x;
+                W[w][k].y -= sv.y;
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) dev::mbar_arrive(&empty[stage]);  // stage consumed by this warp
+      }
+      if (act) {  // pass complete: phase, symbol, store
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const int cx = w & 1, cy = (w >> 1) & 1, cz = DIM == 3 ? zh + (w >> 2) : 0;
+          const int tg = s_tgt[cx + 2 * cy + 4 * cz];
+          if (tg < 0) continue;
+          int rv = (a0 * cx + a1 * cy + a2 * cz) % 3;  // w^{-m.c}
+          rv = rv == 0 ? 0 : 3 - rv;
+          double2 Ph[NCH];
+#pragma unroll
+          for (int k = 0; k < NCH; ++k) Ph[k] = phase3(rv, W[w][k]);
+          double2 out[DIM];
+          apply_symbol<KERNEL, DIM, NCH>(Ph, m0, my, mz, A, h, out);
+          double2* Fo = F + (size_t)(ta + (tg & 0xff) - t_base) * DIM * nhalf + idx;
+#pragma unroll
+          for (int j = 0; j < DIM; ++j) Fo[(size_t)j * nhalf] = out[j];
+        }
+      }
+    }
   }
 }
 
@@ -340,6 +562,42 @@ void launch_accumulate_symbol(const PWGrid& g, int kernel, int ntb, const int* e
     if (kernel == 0) ACC(0, 2);
     else if (kernel == 1) ACC(1, 2);
     else ACC(2, 2);
+  }
+#undef ACC
+}
+
+void launch_accumulate_group(const PWGrid& g, int kernel, int ngroups, const int* grp_tstart, const int* grp_slot,
+                             const int* t_meta, int t_base, const double2* G, const double* A, double h,
+                             double2* F, cudaStream_t st) {
+  if (ngroups <= 0) return;
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // enough CTAs for ~4 waves at 2 per SM; big levels stream whole groups
+  const int nchunk = (g.nhalf + kGM - 1) / kGM;
+  const int want = 8 * num_sms;
+  const int gy = std::max(1, std::min(nchunk, (want + ngroups - 1) / ngroups));
+  dim3 grid(ngroups, gy);
+  static const int zh = std::getenv("SDMK_ACC_ZH") ? std::atoi(std::getenv("SDMK_ACC_ZH")) : 1;
+#define ACC(K, D, Z)                                                                                         \
+  do {                                                                                                       \
+    const int sm_ = GroupCfg<K, D, Z>::kBytes;                                                               \
+    cudaFuncSetAttribute(k_acc_group<K, D, Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_);            \
+    k_acc_group<K, D, Z><<<grid, kGroupThreads, sm_, st>>>(g, grp_tstart, grp_slot, t_meta, t_base, G, A, h, F); \
+  } while (0)
+  if (g.dim == 3) {
+    if (kernel == 0 && zh == 1) ACC(0, 3, 1);
+    else if (kernel == 0) ACC(0, 3, 2);
+    else if (kernel == 1) ACC(1, 3, 2);
+    else if (zh == 1) ACC(2, 3, 1);
+    else ACC(2, 3, 2);
+  } else {
+    if (kernel == 0) ACC(0, 2, 1);
+    else if (kernel == 1) ACC(1, 2, 1);
+    else ACC(2, 2, 1);
   }
 #undef ACC
 }
