@@ -232,73 +232,84 @@ __global__ void __launch_bounds__(kAWarps * 32, 2) k_anterp_mma(int kernel_rt, C
 }
 
 // ------------------------------------------------------------------- K11 --
-constexpr int kTB = 128;     // targets per block (two m-tiles per warp)
+constexpr int kTB = 128;  // targets per pass: 16 m-tiles, warp w owns tiles w and w + 8
 
-// W chunks arrive by cp.async, double buffered; each warp keeps the A
-// fragments of its two 8-target m-tiles in registers and runs their DMMA
-// chains interleaved.
-template <int KS, int kNC, int PC, int DC>  // kNC: W rows per shared chunk; PC/DC: compile-time p, dim
-__global__ void __launch_bounds__(256, 1) k_interp_mma(ChebDev cb, const DBox* __restrict__ boxes,
+// u_j(t) = sum_{iz,iy,ix} W[j,iz,iy,ix] bz[t,iz] by[t,iy] bx[t,ix]  (dmk.cpp:861-915)
+//  * x contraction on the FP64 tensor cores: C[t, (j,iz,iy)] = bx[t,:] . W[(j,iz,iy),:]
+//    with the (j,iz) rows padded to PY = 8 TY in iy, so every 8-column tile
+//    has one (j, iz) and a fixed iy block;
+//  * y contraction in the epilogue: a lane's C columns are always
+//    iy = 8q + 2t + {0,1}, so its 2 TY by values per target live in registers;
+//  * z contraction once per (j, iz) row with bz from shared memory.
+// W streams through shared memory by cp.async in chunks of RG (j, iz) rows,
+// double buffered; each warp runs TY x 2 independent DMMA chains per k-step.
+template <int TY, int PC, int DC>
+__global__ void __launch_bounds__(256, 2) k_interp_mma(ChebDev cb, const DBox* __restrict__ boxes,
                                                       const int* __restrict__ leaves,
                                                       const double* __restrict__ tbasis, int nt,
                                                       const int* __restrict__ tperm,
                                                       const double* __restrict__ incoming,
                                                       double* __restrict__ ufar) {
+  constexpr int PY = 8 * TY, KS = 2 * TY, WS = PY + 4;
+  constexpr int RG = PY >= 128 ? 1 : 128 / PY;  // (j, iz) rows per chunk
+  constexpr int NR = RG * PY;                   // W rows per chunk
   extern __shared__ double sm[];
-  constexpr int KP = KS * 4, WS = KP + 4;
   const int p = PC > 0 ? PC : cb.p, dim = DC > 0 ? DC : cb.dim, pz = dim == 3 ? p : 1;
-  const int N = dim * pz * p, BS = p + 1;
-  double* Ws = sm;                    // [2][kNC][WS]
-  double* bxs = Ws + 2 * kNC * WS;    // [kTB][WS]
-  double* bys = bxs + kTB * WS;       // [kTB][BS]
-  double* bzs = bys + kTB * BS;       // [kTB][BS]
-  int* ntab = reinterpret_cast<int*>(bzs + kTB * BS);  // [N]
+  const int NG = dim * pz;          // (j, iz) rows
+  const int BZ = p | 1;             // odd row stride: the 8 target rows of a fragment hit distinct banks
+  double* Ws = sm;                  // [2][NR][WS]
+  double* bxs = Ws + 2 * NR * WS;   // [kTB][WS]
+  double* bzs = bxs + kTB * WS;     // [kTB][BZ]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int b = leaves[blockIdx.x];
   const DBox box = boxes[b];
-  for (int e = tid; e < N; e += blockDim.x) {
-    const int j = e / (pz * p), r = e % (pz * p);
-    ntab[e] = (j << 16) | ((r / p) << 8) | (r % p);
-  }
-  for (int e = tid; e < 2 * kNC * WS; e += blockDim.x) Ws[e] = 0.0;  // k padding stays zero
-  const double* W = incoming + (size_t)b * N * p;
+  for (int e = tid; e < 2 * NR * WS; e += blockDim.x) Ws[e] = 0.0;  // k padding stays zero
+  const double* W = incoming + (size_t)b * NG * p * p;
   const double* bxg = tbasis;
   const double* byg = tbasis + (size_t)nt * p;
   const double* bzg = tbasis + (size_t)2 * nt * p;
-  const int nchunk = (N + kNC - 1) / kNC;
+  const int nchunk = (NG + RG - 1) / RG;
   auto issue = [&](int c, int buf) {
-    const int n0 = c * kNC, nc = min(kNC, N - n0);
-    double* dstb = Ws + buf * kNC * WS;
-    for (int e = tid; e < kNC * p; e += blockDim.x) {
-      const int r = e / p, k = e % p;
-      const bool v = r < nc;
-      dev::cp_async8(dstb + r * WS + k, v ? W + (size_t)(n0 + r) * p + k : W, v);
+    double* dstb = Ws + buf * NR * WS;
+    for (int e = tid; e < NR * p; e += blockDim.x) {
+      const int r = e / p, k = e - r * p;
+      const int gi = c * RG + r / PY, iy = r % PY;
+      const bool v = gi < NG && iy < p;
+      dev::cp_async8(dstb + r * WS + k, v ? W + ((size_t)gi * p + iy) * p + k : W, v);
     }
     dev::cp_commit();
   };
   for (int t0 = box.tb; t0 < box.te; t0 += kTB) {
     const int tc = min(kTB, box.te - t0);
+    const int ntm = (tc + 7) / 8;
     __syncthreads();
     issue(0, 0);
-    for (int e = tid; e < kTB * KP; e += blockDim.x) {
-      const int a = e / KP, k = e % KP;
+    for (int e = tid; e < kTB * PY; e += blockDim.x) {
+      const int a = e / PY, k = e % PY;
       bxs[a * WS + k] = (a < tc && k < p) ? bxg[(size_t)(t0 + a) * p + k] : 0.0;
     }
     for (int e = tid; e < kTB * p; e += blockDim.x) {
       const int a = e / p, k = e % p;
-      bys[a * BS + k] = a < tc ? byg[(size_t)(t0 + a) * p + k] : 0.0;
-      bzs[a * BS + k] = a < tc ? (dim == 3 ? bzg[(size_t)(t0 + a) * p + k] : (k == 0 ? 1.0 : 0.0)) : 0.0;
+      bzs[a * BZ + k] = a < tc ? (dim == 3 ? bzg[(size_t)(t0 + a) * p + k] : (k == 0 ? 1.0 : 0.0)) : 0.0;
     }
     __syncthreads();
-    const int r0 = warp * 16 + g, r1 = r0 + 8;  // this lane's two targets (A / C rows)
-    double a0[KS], a1[KS];
+    const bool act0 = warp < ntm, act1 = warp + 8 < ntm;
+    const int r0 = warp * 8 + g, r1 = r0 + 64;  // this lane's two targets (A / C rows)
+    double a0[KS], a1[KS], by0[TY][2], by1[TY][2];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       a0[ks] = bxs[r0 * WS + ks * 4 + t];
       a1[ks] = bxs[r1 * WS + ks * 4 + t];
     }
+#pragma unroll
+    for (int q = 0; q < TY; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int iy = 8 * q + 2 * t + e;
+        by0[q][e] = (r0 < tc && iy < p) ? byg[(size_t)(t0 + r0) * p + iy] : 0.0;
+        by1[q][e] = (r1 < tc && iy < p) ? byg[(size_t)(t0 + r1) * p + iy] : 0.0;
+      }
     double v[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
-    const bool active = warp * 16 < tc;
     for (int c = 0; c < nchunk; ++c) {
       const int buf = c & 1;
       if (c + 1 < nchunk) {
@@ -308,31 +319,37 @@ __global__ void __launch_bounds__(256, 1) k_interp_mma(ChebDev cb, const DBox* _
         dev::cp_wait0();
       }
       __syncthreads();
-      const double* Wc = Ws + buf * kNC * WS;
-      const int n0 = c * kNC, nc = min(kNC, N - n0);
-      if (active) {
-        const int ntiles = (nc + 7) / 8;
-        for (int nt_ = 0; nt_ < ntiles; ++nt_) {
-          double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+      const double* Wc = Ws + buf * NR * WS;
+      if (act0) {
+        const int ng = min(RG, NG - c * RG);
+        for (int gl = 0; gl < ng; ++gl) {
+          const int gi = c * RG + gl, j = gi / pz, iz = gi - j * pz;
+          double cc[2][TY][2];
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) {
-            const double bv = Wc[(nt_ * 8 + g) * WS + ks * 4 + t];
-            dev::dmma(c00, c01, a0[ks], bv);
-            dev::dmma(c10, c11, a1[ks], bv);
-          }
-          const int na = n0 + nt_ * 8 + 2 * t;
+          for (int q = 0; q < TY; ++q) cc[0][q][0] = cc[0][q][1] = cc[1][q][0] = cc[1][q][1] = 0.0;
+          const double* Wg = Wc + (gl * PY + g) * WS + t;
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int nn = na + e;
-            if (nn < N) {
-              const int code = ntab[nn];
-              const int j = code >> 16, iz = (code >> 8) & 255, iy = code & 255;
-              const double w0 = bzs[r0 * BS + iz] * bys[r0 * BS + iy] * (e ? c01 : c00);
-              const double w1 = bzs[r1 * BS + iz] * bys[r1 * BS + iy] * (e ? c11 : c10);
-              v[0][j] += w0;
-              v[1][j] += w1;
+          for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+            for (int q = 0; q < TY; ++q) {
+              const double bv = Wg[q * 8 * WS + ks * 4];
+              dev::dmma(cc[0][q][0], cc[0][q][1], a0[ks], bv);
+              if (act1) dev::dmma(cc[1][q][0], cc[1][q][1], a1[ks], bv);
             }
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int q = 0; q < TY; ++q) {
+            s0 = fma(by0[q][0], cc[0][q][0], fma(by0[q][1], cc[0][q][1], s0));
+            s1 = fma(by1[q][0], cc[1][q][0], fma(by1[q][1], cc[1][q][1], s1));
           }
+          s0 *= bzs[r0 * BZ + iz];
+          s1 *= bzs[r1 * BZ + iz];
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj)
+            if (jj == j) {
+              v[0][jj] += s0;
+              v[1][jj] += s1;
+            }
         }
       }
       __syncthreads();  // the next issue overwrites this buffer
@@ -409,29 +426,27 @@ void launch_anterp_mma(int kernel, const ChebDev& cb, const DBox* boxes, const i
 void launch_interp_mma(const ChebDev& cb, const DBox* boxes, const int* leaves, int nleaf, const double* tbasis,
                        int nt, const int* tperm, const double* incoming, double* ufar, cudaStream_t st) {
   if (nleaf <= 0) return;
-  const int p = cb.p, N = cb.dim * cb.pz * p;
-  const int KSv = (p + 3) / 4;
-  auto smem_for = [&](int KS, int NC) {
-    const int WS = KS * 4 + 4;
-    return sizeof(double) * (2 * (size_t)NC * WS + (size_t)kTB * WS + 2 * (size_t)kTB * (p + 1)) + sizeof(int) * N;
+  const int p = cb.p;
+  const int TYv = (p + 7) / 8;
+  auto smem_for = [&](int TY) {
+    const int PY = 8 * TY, WS = PY + 4, RG = PY >= 128 ? 1 : 128 / PY;
+    return sizeof(double) * (2 * (size_t)RG * PY * WS + (size_t)kTB * WS + (size_t)kTB * (p | 1));
   };
-#define IMS(KSS, NCC, PC_, DC_)                                                                           \
+#define IMS(TY_, PC_, DC_)                                                                                \
   do {                                                                                                    \
-    size_t sm = smem_for(KSS, NCC);                                                                       \
-    smem_attr((const void*)k_interp_mma<KSS, NCC, PC_, DC_>, sm);                                         \
-    k_interp_mma<KSS, NCC, PC_, DC_><<<nleaf, 256, sm, st>>>(cb, boxes, leaves, tbasis, nt, tperm, incoming, \
-                                                              ufar);                                      \
+    size_t sm = smem_for(TY_);                                                                            \
+    smem_attr((const void*)k_interp_mma<TY_, PC_, DC_>, sm);                                              \
+    k_interp_mma<TY_, PC_, DC_><<<nleaf, 256, sm, st>>>(cb, boxes, leaves, tbasis, nt, tperm, incoming, ufar); \
   } while (0)
-#define IM(KSS, NCC) IMS(KSS, NCC, 0, 0)
-  if (cb.dim == 3 && p == 23) IMS(6, 256, 23, 3);
-  else if (cb.dim == 3 && p == 22) IMS(6, 256, 22, 3);
-  else if (cb.dim == 3 && p == 30) IMS(8, 128, 30, 3);
-  else if (KSv <= 2) IM(2, 256);
-  else if (KSv <= 4) IM(4, 256);
-  else if (KSv <= 6) IM(6, 256);
-  else if (KSv <= 8) IM(8, 128);
-  else IM(12, 64);
-#undef IM
+  if (cb.dim == 3 && p == 23) IMS(3, 23, 3);
+  else if (cb.dim == 3 && p == 22) IMS(3, 22, 3);
+  else if (cb.dim == 3 && p == 30) IMS(4, 30, 3);
+  else if (TYv <= 1) IMS(1, 0, 0);
+  else if (TYv == 2) IMS(2, 0, 0);
+  else if (TYv == 3) IMS(3, 0, 0);
+  else if (TYv == 4) IMS(4, 0, 0);
+  else if (TYv == 5) IMS(5, 0, 0);
+  else IMS(6, 0, 0);
 #undef IMS
 }
 
