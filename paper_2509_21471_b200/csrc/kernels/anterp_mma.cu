@@ -232,7 +232,9 @@ __global__ void __launch_bounds__(kAWarps * 32, 2) k_anterp_mma(int kernel_rt, C
 }
 
 // ------------------------------------------------------------------- K11 --
-constexpr int kTB = 128;  // targets per pass: 16 m-tiles, warp w owns tiles w and w + 8
+constexpr int kIW = 12;                // warps per CTA
+constexpr int kITW = 4;                // m-tiles per warp
+constexpr int kTB = kIW * kITW * 8;    // targets per pass (one pass per leaf up to 384)
 
 // u_j(t) = sum_{iz,iy,ix} W[j,iz,iy,ix] bz[t,iz] by[t,iy] bx[t,ix]  (dmk.cpp:861-915)
 //  * x contraction on the FP64 tensor cores: C[t, (j,iz,iy)] = bx[t,:] . W[(j,iz,iy),:]
@@ -241,15 +243,17 @@ constexpr int kTB = 128;  // targets per pass: 16 m-tiles, warp w owns tiles w a
 //  * y contraction in the epilogue: a lane's C columns are always
 //    iy = 8q + 2t + {0,1}, so its 2 TY by values per target live in registers;
 //  * z contraction once per (j, iz) row with bz from shared memory.
-// W streams through shared memory by cp.async in chunks of RG (j, iz) rows,
-// double buffered; each warp runs TY x 2 independent DMMA chains per k-step.
+// The leaf's W streams once through shared memory (cp.async, RG (j, iz) rows
+// per chunk, double buffered) while every target of the leaf is resident:
+// warp w owns m-tiles w, w + kIW, ..., and each B fragment feeds its
+// kITW tiles (TY x kITW independent DMMA chains per k-step).
 template <int TY, int PC, int DC>
-__global__ void __launch_bounds__(256, 2) k_interp_mma(ChebDev cb, const DBox* __restrict__ boxes,
-                                                      const int* __restrict__ leaves,
-                                                      const double* __restrict__ tbasis, int nt,
-                                                      const int* __restrict__ tperm,
-                                                      const double* __restrict__ incoming,
-                                                      double* __restrict__ ufar) {
+__global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DBox* __restrict__ boxes,
+                                                           const int* __restrict__ leaves,
+                                                           const double* __restrict__ tbasis, int nt,
+                                                           const int* __restrict__ tperm,
+                                                           const double* __restrict__ incoming,
+                                                           double* __restrict__ ufar) {
   constexpr int PY = 8 * TY, KS = 2 * TY, WS = PY + 4;
   constexpr int RG = PY >= 128 ? 1 : 128 / PY;  // (j, iz) rows per chunk
   constexpr int NR = RG * PY;                   // W rows per chunk
@@ -258,8 +262,7 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(ChebDev cb, const DBox* _
   const int NG = dim * pz;          // (j, iz) rows
   const int BZ = p | 1;             // odd row stride: the 8 target rows of a fragment hit distinct banks
   double* Ws = sm;                  // [2][NR][WS]
-  double* bxs = Ws + 2 * NR * WS;   // [kTB][WS]
-  double* bzs = bxs + kTB * WS;     // [kTB][BZ]
+  double* bzs = Ws + 2 * NR * WS;   // [kTB][BZ]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int b = leaves[blockIdx.x];
   const DBox box = boxes[b];
@@ -269,13 +272,13 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(ChebDev cb, const DBox* _
   const double* byg = tbasis + (size_t)nt * p;
   const double* bzg = tbasis + (size_t)2 * nt * p;
   const int nchunk = (NG + RG - 1) / RG;
-  auto issue = [&](int c, int buf) {
+  auto issue = [&](int c, int buf) {  // a warp per W row, a lane per column
     double* dstb = Ws + buf * NR * WS;
-    for (int e = tid; e < NR * p; e += blockDim.x) {
-      const int r = e / p, k = e - r * p;
+    for (int r = warp; r < NR; r += kIW) {
       const int gi = c * RG + r / PY, iy = r % PY;
       const bool v = gi < NG && iy < p;
-      dev::cp_async8(dstb + r * WS + k, v ? W + ((size_t)gi * p + iy) * p + k : W, v);
+      const double* src = W + ((size_t)(v ? gi : 0) * p + (v ? iy : 0)) * p;
+      for (int k = lane; k < p; k += 32) dev::cp_async8(dstb + r * WS + k, src + k, v);
     }
     dev::cp_commit();
   };
@@ -284,32 +287,26 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(ChebDev cb, const DBox* _
     const int ntm = (tc + 7) / 8;
     __syncthreads();
     issue(0, 0);
-    for (int e = tid; e < kTB * PY; e += blockDim.x) {
-      const int a = e / PY, k = e % PY;
-      bxs[a * WS + k] = (a < tc && k < p) ? bxg[(size_t)(t0 + a) * p + k] : 0.0;
-    }
     for (int e = tid; e < kTB * p; e += blockDim.x) {
       const int a = e / p, k = e % p;
       bzs[a * BZ + k] = a < tc ? (dim == 3 ? bzg[(size_t)(t0 + a) * p + k] : (k == 0 ? 1.0 : 0.0)) : 0.0;
     }
-    __syncthreads();
-    const bool act0 = warp < ntm, act1 = warp + 8 < ntm;
-    const int r0 = warp * 8 + g, r1 = r0 + 64;  // this lane's two targets (A / C rows)
-    double a0[KS], a1[KS], by0[TY][2], by1[TY][2];
+    double af[kITW][KS], byv[kITW][TY][2], v[kITW][3];
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      a0[ks] = bxs[r0 * WS + ks * 4 + t];
-      a1[ks] = bxs[r1 * WS + ks * 4 + t];
+    for (int i = 0; i < kITW; ++i) {
+      const int r = (warp + kIW * i) * 8 + g;
+      const bool ok = r < tc;
+      const double* bxr = bxg + (size_t)(t0 + (ok ? r : 0)) * p;
+      const double* byr = byg + (size_t)(t0 + (ok ? r : 0)) * p;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) af[i][ks] = (ok && ks * 4 + t < p) ? bxr[ks * 4 + t] : 0.0;
+#pragma unroll
+      for (int q = 0; q < TY; ++q)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) byv[i][q][e] = (ok && 8 * q + 2 * t + e < p) ? byr[8 * q + 2 * t + e] : 0.0;
+      v[i][0] = v[i][1] = v[i][2] = 0.0;
     }
-#pragma unroll
-    for (int q = 0; q < TY; ++q)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int iy = 8 * q + 2 * t + e;
-        by0[q][e] = (r0 < tc && iy < p) ? byg[(size_t)(t0 + r0) * p + iy] : 0.0;
-        by1[q][e] = (r1 < tc && iy < p) ? byg[(size_t)(t0 + r1) * p + iy] : 0.0;
-      }
-    double v[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+    const int nmine = warp < ntm ? (ntm - warp + kIW - 1) / kIW : 0;  // m-tiles this warp owns
     for (int c = 0; c < nchunk; ++c) {
       const int buf = c & 1;
       if (c + 1 < nchunk) {
@@ -320,57 +317,53 @@ __global__ void __launch_bounds__(256, 2) k_interp_mma(ChebDev cb, const DBox* _
       }
       __syncthreads();
       const double* Wc = Ws + buf * NR * WS;
-      if (act0) {
+      if (nmine > 0) {
         const int ng = min(RG, NG - c * RG);
         for (int gl = 0; gl < ng; ++gl) {
           const int gi = c * RG + gl, j = gi / pz, iz = gi - j * pz;
-          double cc[2][TY][2];
+          double cc[kITW][TY][2];
 #pragma unroll
-          for (int q = 0; q < TY; ++q) cc[0][q][0] = cc[0][q][1] = cc[1][q][0] = cc[1][q][1] = 0.0;
+          for (int i = 0; i < kITW; ++i)
+#pragma unroll
+            for (int q = 0; q < TY; ++q) cc[i][q][0] = cc[i][q][1] = 0.0;
           const double* Wg = Wc + (gl * PY + g) * WS + t;
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
             for (int q = 0; q < TY; ++q) {
               const double bv = Wg[q * 8 * WS + ks * 4];
-              dev::dmma(cc[0][q][0], cc[0][q][1], a0[ks], bv);
-              if (act1) dev::dmma(cc[1][q][0], cc[1][q][1], a1[ks], bv);
-            }
-          double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-          for (int q = 0; q < TY; ++q) {
-            s0 = fma(by0[q][0], cc[0][q][0], fma(by0[q][1], cc[0][q][1], s0));
-            s1 = fma(by1[q][0], cc[1][q][0], fma(by1[q][1], cc[1][q][1], s1));
+              for (int i = 0; i < kITW; ++i)
+                if (i < nmine) dev::dmma(cc[i][q][0], cc[i][q][1], af[i][ks], bv);
+            }
+#pragma unroll
+          for (int i = 0; i < kITW; ++i) {
+            if (i >= nmine) continue;
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < TY; ++q) s = fma(byv[i][q][0], cc[i][q][0], fma(byv[i][q][1], cc[i][q][1], s));
+            s *= bzs[((warp + kIW * i) * 8 + g) * BZ + iz];
+#pragma unroll
+            for (int jj = 0; jj < 3; ++jj)
+              if (jj == j) v[i][jj] += s;
           }
-          s0 *= bzs[r0 * BZ + iz];
-          s1 *= bzs[r1 * BZ + iz];
-#pragma unroll
-          for (int jj = 0; jj < 3; ++jj)
-            if (jj == j) {
-              v[0][jj] += s0;
-              v[1][jj] += s1;
-            }
         }
       }
       __syncthreads();  // the next issue overwrites this buffer
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int i = 0; i < kITW; ++i) {
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-        v[h][j] += __shfl_xor_sync(0xffffffffu, v[h][j], 1);
-        v[h][j] += __shfl_xor_sync(0xffffffffu, v[h][j], 2);
+        v[i][j] += __shfl_xor_sync(0xffffffffu, v[i][j], 1);
+        v[i][j] += __shfl_xor_sync(0xffffffffu, v[i][j], 2);
       }
-    if (t == 0) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = h ? r1 : r0;
-        if (r < tc) {
-          double* ut = ufar + (size_t)tperm[t0 + r] * dim;
-          ut[0] = v[h][0];
-          ut[1] = v[h][1];
-          if (dim == 3) ut[2] = v[h][2];
-        }
+      const int r = (warp + kIW * i) * 8 + g;
+      if (t == 0 && r < tc) {
+        double* ut = ufar + (size_t)tperm[t0 + r] * dim;
+        ut[0] = v[i][0];
+        ut[1] = v[i][1];
+        if (dim == 3) ut[2] = v[i][2];
       }
     }
   }
@@ -430,13 +423,13 @@ void launch_interp_mma(const ChebDev& cb, const DBox* boxes, const int* leaves, 
   const int TYv = (p + 7) / 8;
   auto smem_for = [&](int TY) {
     const int PY = 8 * TY, WS = PY + 4, RG = PY >= 128 ? 1 : 128 / PY;
-    return sizeof(double) * (2 * (size_t)RG * PY * WS + (size_t)kTB * WS + (size_t)kTB * (p | 1));
+    return sizeof(double) * (2 * (size_t)RG * PY * WS + (size_t)kTB * (p | 1));
   };
 #define IMS(TY_, PC_, DC_)                                                                                \
   do {                                                                                                    \
     size_t sm = smem_for(TY_);                                                                            \
     smem_attr((const void*)k_interp_mma<TY_, PC_, DC_>, sm);                                              \
-    k_interp_mma<TY_, PC_, DC_><<<nleaf, 256, sm, st>>>(cb, boxes, leaves, tbasis, nt, tperm, incoming, ufar); \
+    k_interp_mma<TY_, PC_, DC_><<<nleaf, kIW * 32, sm, st>>>(cb, boxes, leaves, tbasis, nt, tperm, incoming, ufar); \
   } while (0)
   if (cb.dim == 3 && p == 23) IMS(3, 23, 3);
   else if (cb.dim == 3 && p == 22) IMS(3, 22, 3);

@@ -20,6 +20,8 @@
 #include "common.cuh"
 #include "launch.hpp"
 
+#include <cstdlib>
+
 namespace sdmkb {
 
 namespace {
@@ -191,6 +193,198 @@ __global__ void __launch_bounds__(NW * 32, 1) k_tensor_mma(int p_rt, const doubl
   }
 }
 
+// PT = 3 (p = 17..24) variant: 12 warps, 8 z-slabs per group, every stage
+// register-blocked so each shared fragment feeds several DMMAs:
+//   x: warp owns 2 of the 24 row tiles (s, jy) x all 3 ix tiles; its A
+//      fragments come straight from global memory (L2), prefetched into
+//      registers one group ahead, so the input never round-trips through
+//      shared memory;
+//   y: warp owns 2 of the 24 (slab, iy-tile) units x all 3 ix tiles;
+//   z: warp owns n-tiles w, w + 12, ... of the (iy, ix) plane x all 3 iz tiles,
+//      accumulated in registers over every group of every input box.
+// 2 barriers per group; the per-warp tile counts divide evenly (72 x/y
+// tiles, 67 z column tiles over 12 warps).
+constexpr int kT3W = 12;
+constexpr int kT3SG = 8;
+template <int PC>
+__global__ void __launch_bounds__(kT3W * 32, 1)
+    k_tensor3(int p_rt, const double* __restrict__ mats, const int* __restrict__ in_list,
+              const int* __restrict__ out_box, const int* __restrict__ ci_list, int nin, int nch,
+              const double* __restrict__ src, double* __restrict__ dst, int accumulate) {
+  constexpr int PT = 3, P8 = 24, SA = 28, S1 = 28, SG = kT3SG, NWp = kT3W;
+  const int p = PC > 0 ? PC : p_rt;
+  const int pp = p * p, nodes = p * pp;
+  const int NN = (pp + 7) / 8;               // z-stage column tiles
+  const int SS = NN * 8 + 4;                 // T2 row stride (== 4 mod 8)
+  constexpr int ZN = (9 * 8 + NWp - 1) / NWp; // max column tiles per warp (p <= 24: NN <= 72)
+  extern __shared__ double sm[];
+  __shared__ int s_in[8], s_ci[8], s_nq;
+  double* Mm = sm;                       // [2][P8][SA]
+  double* T1 = Mm + 2 * P8 * SA;         // [SG * P8][S1]
+  double* T2 = T1 + SG * P8 * S1;        // [SG][SS]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  for (int r = warp; r < 2 * P8; r += NWp) {
+    const int bsel = r / P8, rr = r % P8;
+    for (int c = lane; c < SA; c += 32) Mm[r * SA + c] = (rr < p && c < p) ? mats[(size_t)bsel * pp + rr * p + c] : 0.0;
+  }
+  for (int e = tid; e < SG * SS; e += blockDim.x) T2[e] = 0.0;
+  const int pair = blockIdx.x, ch = blockIdx.y;
+  if (tid == 0) {
+    int nq = 0;
+    for (int q = 0; q < nin; ++q) {
+      const int ib = in_list[pair * nin + q];
+      if (ib >= 0) {
+        s_in[nq] = ib;
+        s_ci[nq] = ci_list[pair * nin + q];
+        ++nq;
+      }
+    }
+    s_nq = nq;
+  }
+  __syncthreads();
+  const int ngroups = (p + SG - 1) / SG;
+  const int nitems = s_nq * ngroups;
+  double acc[ZN][PT][2];
+#pragma unroll
+  for (int i = 0; i < ZN; ++i)
+#pragma unroll
+    for (int m = 0; m < PT; ++m) acc[i][m][0] = acc[i][m][1] = 0.0;
+  // this lane's x-stage A fragments: rows (s, jy) of tiles warp, warp + 12; columns 4 ks + t
+  int roff[2];
+  bool rok[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int row = (warp + NWp * h) * 8 + g, sl = row / P8, jy = row % P8;
+    roff[h] = sl * pp + jy * p;
+    rok[h] = jy < p;
+  }
+  double af[2][2 * PT];
+  auto load_a = [&](int item) {
+    const int q = item / ngroups, jz0 = (item % ngroups) * SG;
+    const double* in = src + ((size_t)s_in[q] * nch + ch) * nodes + (size_t)jz0 * pp;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int sl = ((warp + NWp * h) * 8 + g) / P8;
+      const bool ok = rok[h] && jz0 + sl < p;
+#pragma unroll
+      for (int ks = 0; ks < 2 * PT; ++ks) {
+        const int jx = ks * 4 + t;
+        af[h][ks] = (ok && jx < p) ? __ldg(in + roff[h] + jx) : 0.0;
+      }
+    }
+  };
+  if (nitems > 0) load_a(0);
+  for (int item = 0; item < nitems; ++item) {
+    const int q = item / ngroups, jz0 = (item % ngroups) * SG;
+    const int cb = s_ci[q];
+    const double* Mx = Mm + (cb & 1) * P8 * SA;
+    const double* My = Mm + ((cb >> 1) & 1) * P8 * SA;
+    const double* Mz = Mm + ((cb >> 2) & 1) * P8 * SA;
+    double ax[2][2 * PT];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int ks = 0; ks < 2 * PT; ++ks) ax[h][ks] = af[h][ks];
+    if (item + 1 < nitems) load_a(item + 1);  // in flight during this group
+    {  // x stage: T1[(s,jy), ix] = sum_jx in[(s,jy), jx] Mx[ix, jx]
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int mt = warp + NWp * h;  // of SG * PT = 24 row tiles
+        double c[PT][2];
+#pragma unroll
+        for (int n = 0; n < PT; ++n) c[n][0] = c[n][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 2 * PT; ++ks)
+#pragma unroll
+          for (int n = 0; n < PT; ++n) dev::dmma(c[n][0], c[n][1], ax[h][ks], Mx[(n * 8 + g) * SA + ks * 4 + t]);
+#pragma unroll
+        for (int n = 0; n < PT; ++n) {
+          double* o = T1 + (mt * 8 + g) * S1 + n * 8 + 2 * t;
+          o[0] = c[n][0];
+          o[1] = c[n][1];
+        }
+      }
+    }
+    __syncthreads();
+    {  // y stage: T2[s][iy, ix] = sum_jy My[iy, jy] T1[(s,jy), ix]
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = warp + NWp * h, sl = u / PT, mt = u % PT;  // of SG * PT = 24 units
+        double c[PT][2];
+#pragma unroll
+        for (int n = 0; n < PT; ++n) c[n][0] = c[n][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 2 * PT; ++ks) {
+          const double av = My[(mt * 8 + g) * SA + ks * 4 + t];
+#pragma unroll
+          for (int n = 0; n < PT; ++n)
+            dev::dmma(c[n][0], c[n][1], av, T1[(sl * P8 + ks * 4 + t) * S1 + n * 8 + g]);
+        }
+        const int iy = mt * 8 + g;
+        if (iy < p) {
+#pragma unroll
+          for (int n = 0; n < PT; ++n) {
+            const int ix = n * 8 + 2 * t;
+            if (ix < p) T2[sl * SS + iy * p + ix] = c[n][0];
+            if (ix + 1 < p) T2[sl * SS + iy * p + ix + 1] = c[n][1];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // z stage: C[iz, n] += sum_{jz in group} Mz[iz, jz] T2[jz][n]
+#pragma unroll
+    for (int ks = 0; ks < SG / 4; ++ks) {
+      double av[PT];
+#pragma unroll
+      for (int m = 0; m < PT; ++m) av[m] = Mz[(m * 8 + g) * SA + jz0 + ks * 4 + t];
+#pragma unroll
+      for (int i = 0; i < ZN; ++i) {
+        const int nt = warp + NWp * i;
+        if (nt < NN) {
+          const double bv = T2[(ks * 4 + t) * SS + nt * 8 + g];
+#pragma unroll
+          for (int m = 0; m < PT; ++m) dev::dmma(acc[i][m][0], acc[i][m][1], av[m], bv);
+        }
+      }
+    }
+    // the next group's x stage rewrites T1 only (read by this y stage, fenced
+    // by the barrier above); its y stage rewrites T2 after the next barrier
+  }
+  double* out = dst + ((size_t)out_box[pair] * nch + ch) * nodes;
+#pragma unroll
+  for (int i = 0; i < ZN; ++i) {
+    const int nt = warp + NWp * i;
+    if (nt >= NN) continue;
+#pragma unroll
+    for (int m = 0; m < PT; ++m) {
+      const int iz = m * 8 + g, n = nt * 8 + 2 * t;
+      if (iz >= p) continue;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (n + e < pp) {
+          double* o = out + (size_t)iz * pp + n + e;
+          *o = accumulate ? *o + acc[i][m][e] : acc[i][m][e];
+        }
+      }
+    }
+  }
+}
+
+template <int PC>
+void tensor3_t(int p, const double* mats, const int* in_list, const int* out_box, const int* ci, int npairs, int nin,
+               int nch, const double* src, double* dst, int accumulate, cudaStream_t st) {
+  const int NN = (p * p + 7) / 8;
+  const size_t smem = sizeof(double) * (2 * 24 * 28 + kT3SG * 24 * 28 + kT3SG * (NN * 8 + 4));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tensor3<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  dim3 grid(npairs, nch);
+  k_tensor3<PC><<<grid, kT3W * 32, smem, st>>>(p, mats, in_list, out_box, ci, nin, nch, src, dst, accumulate);
+}
+
 template <int PC, int PT, int NW, int ZT>
 void tensor_mma_t(int p, const double* mats, const int* in_list, const int* out_box, const int* ci, int npairs,
                   int nin, int nch, const double* src, double* dst, int accumulate, cudaStream_t st) {
@@ -219,7 +413,11 @@ void launch_tensor_mma(int p, const double* mats, const int* in_list, const int*
   const int PT = (p + 7) / 8;
 #define TM(PC_, PT_, NW_, ZT_) \
   tensor_mma_t<PC_, PT_, NW_, ZT_>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st)
-  if (p == 22) TM(22, 3, 16, 13);
+  static const bool old3 = std::getenv("SDMK_TENSOR_OLD") != nullptr;
+  if (p == 22 && !old3) tensor3_t<22>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
+  else if (p == 23 && !old3) tensor3_t<23>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
+  else if (PT == 3 && !old3) tensor3_t<0>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
+  else if (p == 22) TM(22, 3, 16, 13);
   else if (p == 23) TM(23, 3, 16, 13);
   else if (p == 30) TM(30, 4, 16, 32);
   else if (PT <= 1) TM(0, 1, 4, 8);
