@@ -891,15 +891,26 @@ void Context::run_residual(double* ures, bool stats) {  // dmk.cpp:919-1032
   }
   if (cd && (cd->lo != co->lo || cd->hi != co->hi)) throw RuntimeError("residual tables on different intervals");
   // piecewise re-expansion of the radial tables (same values to ~1e-15; see setup.hpp)
-  PiecewisePoly po = piecewise_from_cheb(*co), pd;
-  if (cd) {
-    pd = piecewise_from_cheb(*cd);
-    if (pd.deg != po.deg) {
-      const int deg = std::max(pd.deg, po.deg);
-      pd = piecewise_from_cheb(*cd, 32, deg);
-      po = piecewise_from_cheb(*co, 32, deg);
+  // 32 intervals (degree ~8); fewer when a table needs a higher degree, so
+  // the 8 bank-group copies of the table fit the kernel's shared budget
+  PiecewisePoly po, pd;
+  for (int ni = 32; ni >= 8; ni /= 2) {
+    po = piecewise_from_cheb(*co, ni, 4);
+    if (cd) {
+      pd = piecewise_from_cheb(*cd, ni, 4);
+      if (pd.deg != po.deg) {
+        const int deg = std::max(pd.deg, po.deg);
+        pd = piecewise_from_cheb(*cd, ni, deg);
+        po = piecewise_from_cheb(*co, ni, deg);
+      }
     }
+    // the kernel is compiled for degrees 6, 8, 10, 12
+    const int want = std::max(6, std::max(po.deg, cd ? pd.deg : 0) + (std::max(po.deg, cd ? pd.deg : 0) & 1));
+    if (po.deg != want) po = piecewise_from_cheb(*co, ni, want);
+    if (cd && pd.deg != want) pd = piecewise_from_cheb(*cd, ni, want);
+    if (po.ni * (po.deg + 1) <= residual_max_pw() && po.deg <= 12) break;
   }
+  if (po.deg > 12) throw RuntimeError("residual table re-expansion needs degree > 12");
   const int npw = po.ni * (po.deg + 1);
   if (npw > residual_max_pw()) throw RuntimeError("residual table re-expansion too large");
   double* hc = (double*)pinned_.get("rtab", 2 * npw * sizeof(double));

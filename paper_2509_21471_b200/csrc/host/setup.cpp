@@ -704,7 +704,7 @@ PiecewisePoly piecewise_from_cheb(const Cheb& t, int ni, int min_deg) {
   double fmax = 0.0;
   for (int j = 0; j <= 4096; ++j) fmax = std::max(fmax, std::fabs(t.eval(t.lo + (t.hi - t.lo) * j / 4096.0)));
   const double tol = 4e-15 * std::max(1.0, fmax);
-  for (int deg : {8, 10, 12, 14, 16, 20, 24}) {
+  for (int deg : {4, 5, 6, 7, 8, 10, 12, 14, 16, 20, 24}) {
     if (deg < min_deg) continue;
     const int n = deg + 1;
     std::vector<double> c((size_t)ni * n, 0.0);

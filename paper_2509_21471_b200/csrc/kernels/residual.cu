@@ -31,37 +31,45 @@ constexpr int kRBlock = 256;
 constexpr int kWarps = kRBlock / 32;
 constexpr int kList = 24;        // per-lane list capacity (entries)
 constexpr int kMaxRanges = 160;
-constexpr int kMaxPW = 32 * 25;  // ni * (deg + 1) <= 800 doubles per table
+constexpr int kMaxPW = 384;      // ni * (deg + 1) <= 384 (d, o) coefficient pairs
+constexpr int kCopies = 8;       // table copies, one per 16-byte bank group
 
 struct RangeS {
   double sh[3];
   double lo[3], hi[3];
   double nu, inu, sup2, cull, half;
   int sb, se, self, zero_shift;
+  int code;    // image shift code (x + 3 y + 9 z over {-1,0,1}) | fine-scale flag << 5
   int sub[9];  // Morton child sub-ranges of the source leaf (contiguous, in order)
 };
 
 // Radial table values at s (unit scale) from the piecewise monomial form held
-// in shared memory: interval i = floor((s - lo) ni / (hi - lo)), local
-// u = 2 (frac) - 1, Horner.  Zero at/after the support (split.cpp:147-179).
-template <int KERNEL>
-__device__ __forceinline__ void radial_tables(const ResidTables& rt, const double* __restrict__ pd,
-                                              const double* __restrict__ po, double s, double& fd, double& fo) {
+// in shared memory as (diag, offdiag) pairs, one 16-byte load per degree:
+// interval i = floor((s - lo) ni / (hi - lo)), local u = 2 (frac) - 1,
+// Horner at a compile-time degree (the host pads the table with leading
+// zero coefficients, which leave Horner's value unchanged).  Zero at/after
+// the support (split.cpp:147-179).  The table is stored kCopies times
+// interleaved, copy c in 16-byte bank group c: lane L reads copy L % 8, so
+// the 8 lanes of a 128-bit load phase always hit 8 distinct bank groups
+// whatever intervals they need (no conflicts).
+template <int KERNEL, int DEG>
+__device__ __forceinline__ void radial_tables(const ResidTables& rt, const double2* __restrict__ pw, double yscale,
+                                              double s, double& fd, double& fo) {
   const bool in = s < rt.support;
-  const double y = (s - rt.lo) * (rt.ni / (rt.hi - rt.lo));
+  const double y = (s - rt.lo) * yscale;
   int iv = (int)y;
   iv = iv < 0 ? 0 : (iv >= rt.ni ? rt.ni - 1 : iv);
   const double u = 2.0 * (y - iv) - 1.0;
-  const int n1 = rt.deg + 1;
-  const double* cd = pd + iv * n1;
-  const double* co = po + iv * n1;
-  double vd = KERNEL != 2 ? cd[rt.deg] : 0.0, vo = co[rt.deg];
-  for (int k = rt.deg - 1; k >= 0; --k) {
-    if (KERNEL != 2) vd = fma(vd, u, cd[k]);
-    vo = fma(vo, u, co[k]);
+  const double2* c = pw + iv * (DEG + 1) * kCopies;  // pw already offset by this lane's copy
+  double2 v = c[DEG * kCopies];
+#pragma unroll
+  for (int k = DEG - 1; k >= 0; --k) {
+    const double2 ck = c[k * kCopies];
+    if (KERNEL != 2) v.x = fma(v.x, u, ck.x);
+    v.y = fma(v.y, u, ck.y);
   }
-  fd = (KERNEL != 2 && in) ? vd : 0.0;
-  fo = in ? vo : 0.0;
+  fd = (KERNEL != 2 && in) ? v.x : 0.0;
+  fo = in ? v.y : 0.0;
 }
 
 // residual_apply assembly (split.cpp:258-317) given the radial table values;
@@ -69,7 +77,7 @@ __device__ __forceinline__ void radial_tables(const ResidTables& rt, const doubl
 template <int KERNEL, int DIM>
 __device__ __forceinline__ void assemble(double fd, double fo, const double* x, double rinv, double s,
                                          double support, double nu, const double* __restrict__ sstr, int ns, int a,
-                                         double* u) {
+                                         double* u) {  // u: this pair's contribution (assigned)
   constexpr double k8pi = 1.0 / (8.0 * dev::kPI), k4pi = 1.0 / (4.0 * dev::kPI);
   const double rinv2 = rinv * rinv;
   if (KERNEL == 0) {  // Stokeslet
@@ -84,7 +92,7 @@ __device__ __forceinline__ void assemble(double fd, double fo, const double* x, 
     }
     const double cd = amp * fd * c0, cf = amp * fo * c0 * xf * rinv2;
 #pragma unroll
-    for (int j = 0; j < DIM; ++j) u[j] += cd * f[j] + cf * x[j];
+    for (int j = 0; j < DIM; ++j) u[j] = cd * f[j] + cf * x[j];
   } else if (KERNEL == 1) {  // stresslet
     const double amp = DIM == 2 ? nu : 1.0;
     double f[DIM], nn[DIM], xf = 0.0, xn = 0.0, fn = 0.0;
@@ -100,23 +108,23 @@ __device__ __forceinline__ void assemble(double fd, double fo, const double* x, 
     const double cd = amp * fd * k8pi * rinv3;
     const double co = -3.0 * k4pi * amp * fo * xf * xn * rinv3 * rinv2;
 #pragma unroll
-    for (int j = 0; j < DIM; ++j) u[j] += cd * (f[j] * xn + x[j] * fn + nn[j] * xf) + co * x[j];
+    for (int j = 0; j < DIM; ++j) u[j] = cd * (f[j] * xn + x[j] * fn + nn[j] * xf) + co * x[j];
   } else {  // rotlet
     if (DIM == 2) {
       const double c0 = fo * sstr[a] * k4pi * rinv2;
-      u[0] += c0 * x[1];
-      u[1] -= c0 * x[0];
+      u[0] = c0 * x[1];
+      u[1] = -(c0 * x[0]);
     } else {
       const double c0 = fo * k8pi * rinv2 * rinv;
       const double g0 = sstr[a], g1 = sstr[(size_t)ns + a], g2 = sstr[(size_t)2 * ns + a];
-      u[0] += c0 * (g1 * x[2] - g2 * x[1]);
-      u[1] += c0 * (g2 * x[0] - g0 * x[2]);
-      u[DIM - 1] += c0 * (g0 * x[1] - g1 * x[0]);
+      u[0] = c0 * (g1 * x[2] - g2 * x[1]);
+      u[1] = c0 * (g2 * x[0] - g0 * x[2]);
+      u[DIM - 1] = c0 * (g0 * x[1] - g1 * x[0]);
     }
   }
 }
 
-template <int KERNEL, int DIM>
+template <int KERNEL, int DIM, int DEG>
 __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox* __restrict__ boxes,
                                                       const int* __restrict__ leaves,
                                                       const int* __restrict__ rng_start,
@@ -130,20 +138,23 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
                                                       double* __restrict__ ures, int* flags,
                                                       unsigned long long* stats) {
   __shared__ RangeS rs[kMaxRanges];
-  __shared__ double s_pd[kMaxPW], s_po[kMaxPW];
-  extern __shared__ int dyn[];  // lane-interleaved lists: [kWarps][kList][32] ints then bytes
+  extern __shared__ __align__(16) double2 dyn2[];  // [npw][kCopies] table, then the lists
+  double2* s_pw = dyn2;
+  const int npw = rt.ni * (rt.deg + 1);
+  int* dyn = reinterpret_cast<int*>(dyn2 + npw * kCopies);  // lane-interleaved lists: [kWarps][kList][32] ints then bytes
   int (*lsrc)[kList][32] = reinterpret_cast<int (*)[kList][32]>(dyn);
   unsigned char (*lrng)[kList][32] = reinterpret_cast<unsigned char (*)[kList][32]>(dyn + kWarps * kList * 32);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int leaf = leaves[blockIdx.x];
   const DBox box = boxes[leaf];
   const double r_l = box.side, r_f = 0.5 * r_l;
+  const double inv_rl = 1.0 / r_l, inv_rf = 1.0 / r_f;
+  const double yscale = rt.ni / (rt.hi - rt.lo);
   const int r0 = rng_start[blockIdx.x], nr = rng_start[blockIdx.x + 1] - r0;
   {
-    const int npw = rt.ni * (rt.deg + 1);
-    for (int k = tid; k < npw; k += blockDim.x) {
-      s_pd[k] = KERNEL != 2 ? rt.pw_d[k] : 0.0;
-      s_po[k] = rt.pw_o[k];
+    for (int e = tid; e < npw * kCopies; e += blockDim.x) {
+      const int k = e / kCopies;
+      s_pw[e] = make_double2(KERNEL != 2 ? rt.pw_d[k] : 0.0, rt.pw_o[k]);
     }
   }
   for (int k = tid; k < nr; k += blockDim.x) {
@@ -153,6 +164,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     const int code = info & 31;
     const int sh[3] = {code % 3 - 1, (code / 3) % 3 - 1, code / 9 - 1};
     R.nu = (info >> 5) & 1 ? r_f : r_l;
+    R.code = (sh[0] + 1) | ((sh[1] + 1) << 2) | ((DIM == 3 ? sh[2] + 1 : 1) << 4) | ((info & 32) << 1);
     R.inu = 1.0 / R.nu;
     R.self = (info >> 6) & 1;
     const double sup = R.nu * rt.support;
@@ -204,21 +216,36 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       int mx = cnt;
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      for (int i = 0; i < mx; ++i) {
-        if (i < cnt) {
-          const int a = lsrc[warp][i][lane];
-          const RangeS& R = rs[lrng[warp][i][lane]];
-          double x[3] = {0.0, 0.0, 0.0}, r2 = 0.0;
-          x[0] = xt[0] - (spx[a] + R.sh[0]);
-          x[1] = xt[1] - (spy[a] + R.sh[1]);
-          if (DIM == 3) x[2] = xt[2] - (spz[a] + R.sh[2]);
+      // two list entries per step: independent dependency chains interleave,
+      // and their contributions are added in list order
+      auto eval = [&](int i, double* c) {
+        const int a = lsrc[warp][i][lane];
+        const int code = lrng[warp][i][lane];  // image shift (x+1 | y+1 << 2 | z+1 << 4) | fine << 6
+        const double nu = (code & 64) ? r_f : r_l, inu = (code & 64) ? inv_rf : inv_rl;
+        double x[3] = {0.0, 0.0, 0.0}, r2 = 0.0;
+        x[0] = xt[0] - (spx[a] + (double)((code & 3) - 1));
+        x[1] = xt[1] - (spy[a] + (double)(((code >> 2) & 3) - 1));
+        if (DIM == 3) x[2] = xt[2] - (spz[a] + (double)(((code >> 4) & 3) - 1));
 #pragma unroll
-          for (int ax = 0; ax < DIM; ++ax) r2 += x[ax] * x[ax];
-          const double rinv = rsqrt(r2);
-          const double s = (r2 * rinv) * R.inu;  // nu is a power of two: r * (1/nu) == r / nu
-          double fd, fo;
-          radial_tables<KERNEL>(rt, s_pd, s_po, s, fd, fo);
-          assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, R.nu, sstr, ns, a, u);
+        for (int ax = 0; ax < DIM; ++ax) r2 += x[ax] * x[ax];
+        const double rinv = rsqrt(r2);
+        const double s = (r2 * rinv) * inu;  // nu is a power of two: r * (1/nu) == r / nu
+        double fd, fo;
+        radial_tables<KERNEL, DEG>(rt, s_pw + (lane & (kCopies - 1)), yscale, s, fd, fo);
+        assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, nu, sstr, ns, a, c);
+      };
+      for (int i = 0; i < mx; i += 2) {  // both evaluations unconditional (clamped), straight-line
+        const int i0 = min(i, cnt - 1), i1 = min(i + 1, cnt - 1);
+        double c0[3] = {0.0, 0.0, 0.0}, c1[3] = {0.0, 0.0, 0.0};
+        if (cnt > 0) {
+          eval(i0, c0);
+          eval(i1, c1);
+        }
+        const bool h0 = i < cnt, h1 = i + 1 < cnt;
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) {
+          if (h0) u[j] += c0[j];
+          if (h1) u[j] += c1[j];
         }
       }
       cnt = 0;
@@ -270,7 +297,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           }
           if (in) {
             lsrc[warp][cnt][lane] = a;
-            lrng[warp][cnt][lane] = (unsigned char)k;
+            lrng[warp][cnt][lane] = (unsigned char)R.code;
             ++cnt;
             ++n_in;
           }
@@ -328,12 +355,21 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
                      const double* tpts, int nt, const int* tperm, int alias, double /*unused*/, double self_const,
                      double* ures, int* flags, unsigned long long* stats, cudaStream_t st) {
   if (nleaf <= 0) return;
-  const size_t dsm = (size_t)kWarps * kList * 32 * (sizeof(int) + 1);
+  const size_t dsm = (size_t)kWarps * kList * 32 * (sizeof(int) + 1) +
+                     sizeof(double) * 2 * kCopies * (size_t)rt.ni * (rt.deg + 1);
 #define RES(K, D)                                                                                                \
   do {                                                                                                           \
-    cudaFuncSetAttribute(k_residual<K, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);               \
-    k_residual<K, D><<<nleaf, kRBlock, dsm, st>>>(rt, boxes, leaves, rng_start, rng_box, rng_info, subrange, spts, ns, \
-                                                  sstr, tpts, nt, tperm, alias, self_const, ures, flags, stats); \
+    if (rt.deg == 6) RES1(K, D, 6);                                                                              \
+    else if (rt.deg == 8) RES1(K, D, 8);                                                                         \
+    else if (rt.deg == 10) RES1(K, D, 10);                                                                       \
+    else RES1(K, D, 12);                                                                                         \
+  } while (0)
+#define RES1(K, D, G)                                                                                            \
+  do {                                                                                                           \
+    cudaFuncSetAttribute(k_residual<K, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);            \
+    k_residual<K, D, G><<<nleaf, kRBlock, dsm, st>>>(rt, boxes, leaves, rng_start, rng_box, rng_info, subrange,  \
+                                                     spts, ns, sstr, tpts, nt, tperm, alias, self_const, ures,   \
+                                                     flags, stats);                                              \
   } while (0)
   if (rt.dim == 3) {
     if (rt.kernel == 0) RES(0, 3);
@@ -345,6 +381,7 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
     else RES(2, 2);
   }
 #undef RES
+#undef RES1
 }
 
 int residual_max_ranges() { return kMaxRanges; }
