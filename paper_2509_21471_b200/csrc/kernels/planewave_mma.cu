@@ -21,6 +21,8 @@
 #include "common.cuh"
 #include "launch.hpp"
 
+#include <cstdlib>
+
 namespace sdmkb {
 
 namespace {
@@ -155,6 +157,174 @@ __global__ void __launch_bounds__(kW * 32, 1) k_fwd_xy_mma(PWGrid g, const int* 
             if (cidx >= 0) Bo[(size_t)iz * ncol + cidx] = make_double2(e ? cr1 : cr0, e ? ci1 : ci0);
           }
         }
+      }
+    }
+  }
+}
+
+// fwd_xy with the Hermitian split of the Y stage.  E[-m] = conj E[m] and
+// E[0] = 1, so for m0 >= 1 (complex a = ar + i ai) and my >= 1
+//   P = Er ar, Q = Ei ai, R = Er ai, S = Ei ar      (Er, Ei: rows my = 1..M)
+//   b[+my] = (P - Q) + i (R + S),   b[-my] = (P + Q) + i (R - S),
+// four real GEMMs over M rows instead of one complex GEMM over 2M + 1 rows
+// with interleaved K (~3.7x fewer DMMAs).  The my = 0 row (column sums of a)
+// and the m0 = 0 column (a real: b[+-my] = P0 +- i S0) are CUDA-core dot
+// products.  X stage columns: n = 2 (m0 - 1) + part for m0 = 1..M, n = 2M for
+// m0 = 0 (E = 1).
+template <int PT, int PC, int NC>
+__global__ void __launch_bounds__(kW * 32, 1) k_fwd_xy2(PWGrid g, const int* __restrict__ boxes, int nch,
+                                                       const double* __restrict__ outgoing,
+                                                       double2* __restrict__ B) {
+  constexpr int P8 = PT * 8;
+  constexpr int SE = P8 + 4;  // == 4 mod 8 for P8 = 24, 32
+  constexpr int SY = P8 + 4;
+  const int p = PC > 0 ? PC : g.p, N = NC > 0 ? NC : g.N, M = (N - 1) / 2, ncol = g.ncol, pp = p * p;
+  const int M1 = M + 1, MT = (M + 7) / 8, M8 = MT * 8, NX8 = (2 * M + 1 + 7) / 8 * 8;
+  const int SAa = r8(NX8 > 2 * M8 ? NX8 : 2 * M8);  // Y reads columns up to 2 M8 - 1
+  extern __shared__ double sm[];
+  double* EXT = sm;                        // [NX8][SE]
+  double* EYr = EXT + NX8 * SE;            // [M8][SY]  rows my - 1
+  double* EYi = EYr + M8 * SY;             // [M8][SY]
+  double* win = EYi + M8 * SY;             // [2][4*P8][SE]
+  double* a = win + 2 * 4 * P8 * SE;       // [4*P8][SAa]
+  int* colidx = reinterpret_cast<int*>(a + 4 * P8 * SAa);  // [N][M1]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
+  for (int e = tid; e < NX8 * SE; e += blockDim.x) {
+    const int n = e / SE, ix = e % SE;
+    double v = 0.0;
+    if (ix < p) {
+      if (n < 2 * M) {
+        const double2 ev = g.E[(size_t)(n / 2 + 1 + M) * p + ix];
+        v = (n & 1) ? ev.y : ev.x;
+      } else if (n == 2 * M) {
+        v = 1.0;
+      }
+    }
+    EXT[e] = v;
+  }
+  for (int e = tid; e < M8 * SY; e += blockDim.x) {
+    const int r = e / SY, iy = e % SY;
+    double vr = 0.0, vi = 0.0;
+    if (r < M && iy < p) {
+      const double2 ev = g.E[(size_t)(r + 1 + M) * p + iy];
+      vr = ev.x;
+      vi = ev.y;
+    }
+    EYr[e] = vr;
+    EYi[e] = vi;
+  }
+  for (int e = tid; e < N * M1; e += blockDim.x) colidx[e] = -1;
+  for (int e = tid; e < 2 * 4 * P8 * SE; e += blockDim.x) win[e] = 0.0;
+  for (int e = tid; e < 4 * P8 * SAa; e += blockDim.x) a[e] = 0.0;
+  __syncthreads();
+  for (int c = tid; c < ncol; c += blockDim.x) colidx[(g.col_my[c] + M) * M1 + g.col_m0[c]] = c;
+  const int slot = blockIdx.x, ch = blockIdx.y;
+  const double* w = outgoing + ((size_t)boxes[slot] * nch + ch) * (size_t)(p * pp);
+  double2* Bo = B + ((size_t)slot * nch + ch) * (size_t)g.pz * ncol;
+  const int ngroups = (p + 3) / 4;
+  auto issue = [&](int grp, int buf) {
+    double* dst = win + buf * 4 * P8 * SE;
+    const int jz0 = grp * 4;
+    for (int row = warp; row < 4 * p; row += kW) {
+      const int s = row / p, r = row % p;
+      const bool v = jz0 + s < p;
+      const double* srow = w + (size_t)(v ? jz0 + s : 0) * pp + r * p;
+      for (int cc = lane; cc < p; cc += 32) cp_async8(dst + (s * P8 + r) * SE + cc, srow + cc, v);
+    }
+    cp_commit();
+  };
+  auto put = [&](int iz, int my, int m0, double re, double im) {
+    const int c = colidx[(my + M) * M1 + m0];
+    if (c >= 0) Bo[(size_t)iz * ncol + c] = make_double2(re, im);
+  };
+  issue(0, 0);
+  const int nnt = NX8 / 8;
+  const int xtiles = 4 * PT * nnt;
+  const int yunits = 4 * MT * MT;
+  for (int grp = 0; grp < ngroups; ++grp) {
+    const int buf = grp & 1;
+    __syncthreads();
+    if (grp + 1 < ngroups) {
+      issue(grp + 1, buf ^ 1);
+      cp_wait1();
+    } else {
+      cp_wait0();
+    }
+    __syncthreads();
+    const double* A = win + buf * 4 * P8 * SE;
+    // X stage (two tiles per warp iteration: independent chains)
+    for (int tile0 = warp; tile0 < xtiles; tile0 += 2 * kW) {
+      const int tile1 = tile0 + kW;
+      const bool two = tile1 < xtiles;
+      const int mA = tile0 / nnt, nA = tile0 % nnt, mB = two ? tile1 / nnt : mA, nB = two ? tile1 % nnt : nA;
+      double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < PT * 2; ++ks) {
+        dmma(c0, c1, A[(mA * 8 + gq) * SE + ks * 4 + t], EXT[(nA * 8 + gq) * SE + ks * 4 + t]);
+        if (two) dmma(d0, d1, A[(mB * 8 + gq) * SE + ks * 4 + t], EXT[(nB * 8 + gq) * SE + ks * 4 + t]);
+      }
+      a[(mA * 8 + gq) * SAa + nA * 8 + 2 * t] = c0;
+      a[(mA * 8 + gq) * SAa + nA * 8 + 2 * t + 1] = c1;
+      if (two) {
+        a[(mB * 8 + gq) * SAa + nB * 8 + 2 * t] = d0;
+        a[(mB * 8 + gq) * SAa + nB * 8 + 2 * t + 1] = d1;
+      }
+    }
+    __syncthreads();
+    // Y stage: units (s, my tile, m0 tile), four accumulators each
+    for (int u = warp; u < yunits; u += kW) {
+      const int s = u / (MT * MT), mt = (u / MT) % MT, nt = u % MT;
+      double P0 = 0, P1 = 0, Q0 = 0, Q1 = 0, R0 = 0, R1 = 0, S0 = 0, S1 = 0;
+#pragma unroll
+      for (int ks = 0; ks < PT * 2; ++ks) {
+        const int k = ks * 4 + t;
+        const double* ar = a + (s * P8 + k) * SAa + 2 * (nt * 8 + gq);
+        const double br = ar[0], bi = ar[1];
+        const double er = EYr[(mt * 8 + gq) * SY + k], ei = EYi[(mt * 8 + gq) * SY + k];
+        dmma(P0, P1, er, br);
+        dmma(Q0, Q1, ei, bi);
+        dmma(R0, R1, er, bi);
+        dmma(S0, S1, ei, br);
+      }
+      const int my = mt * 8 + gq + 1, iz = grp * 4 + s;
+      if (my <= M && iz < p) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int m0 = nt * 8 + 2 * t + e + 1;
+          if (m0 <= M) {
+            const double P = e ? P1 : P0, Q = e ? Q1 : Q0, R = e ? R1 : R0, S = e ? S1 : S0;
+            put(iz, my, m0, P - Q, R + S);
+            put(iz, -my, m0, P + Q, R - S);
+          }
+        }
+      }
+    }
+    // remainders on the CUDA cores: the m0 = 0 column (my >= 1) and the my = 0 row
+    for (int it = tid; it < 4 * (2 * M + 1); it += blockDim.x) {
+      const int s = it / (2 * M + 1), r = it % (2 * M + 1), iz = grp * 4 + s;
+      if (iz >= p) continue;
+      const double* as = a + s * P8 * SAa;
+      if (r < M) {  // my = r + 1, m0 = 0: a real
+        double P = 0.0, S = 0.0;
+        for (int iy = 0; iy < p; ++iy) {
+          const double a0 = as[iy * SAa + 2 * M];
+          P = fma(EYr[r * SY + iy], a0, P);
+          S = fma(EYi[r * SY + iy], a0, S);
+        }
+        put(iz, r + 1, 0, P, S);
+        put(iz, -(r + 1), 0, P, -S);
+      } else {  // my = 0, m0 = r - M
+        const int m0 = r - M;
+        double re = 0.0, im = 0.0;
+        if (m0 == 0) {
+          for (int iy = 0; iy < p; ++iy) re += as[iy * SAa + 2 * M];
+        } else {
+          for (int iy = 0; iy < p; ++iy) {
+            re += as[iy * SAa + 2 * (m0 - 1)];
+            im += as[iy * SAa + 2 * (m0 - 1) + 1];
+          }
+        }
+        put(iz, 0, m0, re, im);
       }
     }
   }
@@ -404,11 +574,30 @@ void launch_forward_mma(const PWGrid& g, const int* boxes, int nbox, int nch, co
     attr((const void*)k_fwd_xy_mma<PT_, PC_, NC_>, smem);                             \
     k_fwd_xy_mma<PT_, PC_, NC_><<<grid, kW * 32, smem, st>>>(g, boxes, nch, outgoing, B); \
   } while (0)
-    if (g.p == 23 && g.N == 33) FX(3, 23, 33);
-    else if (g.p == 22 && g.N == 33) FX(3, 22, 33);
-    else if (g.p == 30 && g.N == 45) FX(4, 30, 45);
-    else if (PT <= 3) FX(3, 0, 0);
-    else FX(4, 0, 0);
+    static const bool old_xy = std::getenv("SDMK_PW_OLD") != nullptr;
+    if (old_xy) {
+      if (g.p == 23 && g.N == 33) FX(3, 23, 33);
+      else if (g.p == 22 && g.N == 33) FX(3, 22, 33);
+      else if (g.p == 30 && g.N == 45) FX(4, 30, 45);
+      else if (PT <= 3) FX(3, 0, 0);
+      else FX(4, 0, 0);
+    } else {
+      const int M = g.M, MT = (M + 7) / 8, NX8b = (2 * M + 1 + 7) / 8 * 8, P8 = PT * 8;
+      const size_t sm2 = sizeof(double) * ((size_t)NX8b * (P8 + 4) + 2 * (size_t)MT * 8 * (P8 + 4) +
+                                           2 * 4 * (size_t)P8 * (P8 + 4) + 4 * (size_t)P8 * r8(NX8b > 16 * MT ? NX8b : 16 * MT)) +
+                         sizeof(int) * (size_t)g.N * M1;
+#define FX2(PT_, PC_, NC_)                                                            \
+  do {                                                                                \
+    attr((const void*)k_fwd_xy2<PT_, PC_, NC_>, sm2);                                 \
+    k_fwd_xy2<PT_, PC_, NC_><<<grid, kW * 32, sm2, st>>>(g, boxes, nch, outgoing, B); \
+  } while (0)
+      if (g.p == 23 && g.N == 33) FX2(3, 23, 33);
+      else if (g.p == 22 && g.N == 33) FX2(3, 22, 33);
+      else if (g.p == 30 && g.N == 45) FX2(4, 30, 45);
+      else if (PT <= 3) FX2(3, 0, 0);
+      else FX2(4, 0, 0);
+#undef FX2
+    }
 #undef FX
   }
   {
