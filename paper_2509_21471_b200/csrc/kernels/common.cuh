@@ -49,6 +49,11 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
   const int sz = valid ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(sz));
 }
+// 16-byte cp.async (both addresses 16-byte aligned), L2 only
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 
 // mbarrier + 1D bulk copy (TMA engine, no tensor map): global -> shared,

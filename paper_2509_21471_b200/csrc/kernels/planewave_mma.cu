@@ -415,6 +415,157 @@ __global__ void __launch_bounds__(kW * 32, 2) k_z_mma(PWGrid g, int nc, const do
   }
 }
 
+// z stages with the Hermitian split (E[-m] = conj E[m], E[0] = 1):
+//  forward  G[+-mz] = (P -+ Q) + i (R +- S), P = Er Br, Q = Ei Bi, R = Er Bi,
+//           S = Ei Br over mz = 1..M; G[0] = sum_iz B (CUDA cores);
+//  inverse  C1.re = F[0].re + [Er | Ei] [Ur ; Vi],  C1.im = F[0].im + [Er | -Ei] [Ui ; Vr]
+//           with U = F[+mz] + F[-mz], V = F[+mz] - F[-mz] (zero outside the band).
+// ~2.5x fewer DMMAs than the complex GEMMs over all 2M + 1 rows.
+template <int PT>
+__global__ void __launch_bounds__(kW * 32, 2) k_zf2(PWGrid g, int nc, const double2* __restrict__ IN,
+                                                   double2* __restrict__ OUT) {
+  constexpr int P8 = PT * 8, SK = P8 + 4;
+  constexpr int SI = (2 * kCB) % 16 == 8 ? 2 * kCB : 2 * kCB + 8;
+  extern __shared__ double sm[];
+  const int M = g.Mz, MT = (M + 7) / 8, M8 = MT * 8, pz = g.pz, ncol = g.ncol;
+  double* Ar = sm;               // [M8][SK]  Er[mz = r + 1][iz]
+  double* Ai = Ar + M8 * SK;     // [M8][SK]
+  double* In = Ai + M8 * SK;     // [P8][SI]  (col, re|im) interleaved
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
+  for (int e = tid; e < M8 * SK; e += blockDim.x) {
+    const int r = e / SK, k = e % SK;
+    double vr = 0.0, vi = 0.0;
+    if (r < M && k < pz) {
+      const double2 ev = g.Ez[(size_t)(r + 1 + M) * pz + k];
+      vr = ev.x;
+      vi = ev.y;
+    }
+    Ar[e] = vr;
+    Ai[e] = vi;
+  }
+  const int box = blockIdx.x, comp = blockIdx.y, c0 = blockIdx.z * kCB;
+  const int ncb = min(kCB, ncol - c0);
+  const double2* src = IN + ((size_t)box * nc + comp) * (size_t)pz * ncol;
+  double2* dst = OUT + ((size_t)box * nc + comp) * (size_t)g.nhalf;
+  for (int e = tid; e < P8 * kCB; e += blockDim.x) {
+    const int k = e / kCB, cc = e % kCB;
+    double2 v = make_double2(0.0, 0.0);
+    if (k < pz && cc < ncb) v = src[(size_t)k * ncol + c0 + cc];
+    In[k * SI + 2 * cc] = v.x;
+    In[k * SI + 2 * cc + 1] = v.y;
+  }
+  __syncthreads();
+  const int ntc = kCB / 8, ntile = MT * ntc;
+  for (int tile = warp; tile < ntile; tile += kW) {
+    const int rt = tile / ntc, ct = tile % ntc;
+    double P0 = 0, P1 = 0, Q0 = 0, Q1 = 0, R0 = 0, R1 = 0, S0 = 0, S1 = 0;
+#pragma unroll
+    for (int ks = 0; ks < 2 * PT; ++ks) {
+      const int k = ks * 4 + t;
+      const double br = In[k * SI + 2 * (ct * 8 + gq)], bi = In[k * SI + 2 * (ct * 8 + gq) + 1];
+      const double er = Ar[(rt * 8 + gq) * SK + k], ei = Ai[(rt * 8 + gq) * SK + k];
+      dmma(P0, P1, er, br);
+      dmma(Q0, Q1, ei, bi);
+      dmma(R0, R1, er, bi);
+      dmma(S0, S1, ei, br);
+    }
+    const int mz = rt * 8 + gq + 1;
+    if (mz > M) continue;
+    const int np = g.slab_ncol[mz + M], nm = g.slab_ncol[M - mz];
+    const int op = g.slab_off[mz + M], om = g.slab_off[M - mz];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int cc = ct * 8 + 2 * t + e, col = c0 + cc;
+      if (cc >= ncb) continue;
+      const double P = e ? P1 : P0, Q = e ? Q1 : Q0, R = e ? R1 : R0, S = e ? S1 : S0;
+      if (col < np) dst[op + col] = make_double2(P - Q, R + S);
+      if (col < nm) dst[om + col] = make_double2(P + Q, R - S);
+    }
+  }
+  // mz = 0: column sums over iz
+  for (int cc = tid; cc < ncb; cc += blockDim.x) {
+    const int col = c0 + cc;
+    if (col >= g.slab_ncol[M]) continue;
+    double re = 0.0, im = 0.0;
+    for (int k = 0; k < pz; ++k) {
+      re += In[k * SI + 2 * cc];
+      im += In[k * SI + 2 * cc + 1];
+    }
+    dst[g.slab_off[M] + col] = make_double2(re, im);
+  }
+}
+
+template <int PT>
+__global__ void __launch_bounds__(kW * 32, 2) k_zi2(PWGrid g, int nc, const double2* __restrict__ IN,
+                                                   double2* __restrict__ OUT) {
+  constexpr int P8 = PT * 8;
+  constexpr int SBc = (kCB % 16 == 8) ? kCB : kCB + 8;  // B' rows (== 8 mod 16)
+  extern __shared__ double sm[];
+  const int M = g.Mz, MT = (M + 7) / 8, M8 = MT * 8, K2 = 2 * M8, SA = r4(K2), pz = g.pz, ncol = g.ncol;
+  double* Are = sm;                  // [P8][SA]  [Er | Ei]
+  double* Aim = Are + P8 * SA;       // [P8][SA]  [Er | -Ei]
+  double* Bre = Aim + P8 * SA;       // [K2][SBc] [Ur ; Vi]
+  double* Bim = Bre + K2 * SBc;      // [K2][SBc] [Ui ; Vr]
+  double2* F0 = reinterpret_cast<double2*>(Bim + K2 * SBc);  // [kCB]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
+  for (int e = tid; e < P8 * SA; e += blockDim.x) {
+    const int iz = e / SA, k = e % SA;
+    double vr = 0.0, vi = 0.0;
+    if (iz < pz && k < K2) {
+      const int r = k < M8 ? k : k - M8;
+      if (r < M) {
+        const double2 ev = g.Ez[(size_t)(r + 1 + M) * pz + iz];
+        vr = k < M8 ? ev.x : ev.y;
+        vi = k < M8 ? ev.x : -ev.y;
+      }
+    }
+    Are[e] = vr;
+    Aim[e] = vi;
+  }
+  const int box = blockIdx.x, comp = blockIdx.y, c0 = blockIdx.z * kCB;
+  const int ncb = min(kCB, ncol - c0);
+  const double2* src = IN + ((size_t)box * nc + comp) * (size_t)g.nhalf;
+  double2* dst = OUT + ((size_t)box * nc + comp) * (size_t)pz * ncol;
+  for (int e = tid; e < M8 * kCB; e += blockDim.x) {
+    const int r = e / kCB, cc = e % kCB, col = c0 + cc;
+    double2 fp = make_double2(0.0, 0.0), fm = fp;
+    if (r < M && cc < ncb) {
+      const int mz = r + 1;
+      if (col < g.slab_ncol[M + mz]) fp = src[g.slab_off[M + mz] + col];
+      if (col < g.slab_ncol[M - mz]) fm = src[g.slab_off[M - mz] + col];
+    }
+    Bre[r * SBc + cc] = fp.x + fm.x;
+    Bre[(M8 + r) * SBc + cc] = fp.y - fm.y;
+    Bim[r * SBc + cc] = fp.y + fm.y;
+    Bim[(M8 + r) * SBc + cc] = fp.x - fm.x;
+  }
+  for (int cc = tid; cc < kCB; cc += blockDim.x) {
+    const int col = c0 + cc;
+    F0[cc] = (cc < ncb && col < g.slab_ncol[M]) ? src[g.slab_off[M] + col] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const int ntc = kCB / 8, ntile = PT * ntc;
+  for (int tile = warp; tile < ntile; tile += kW) {
+    const int rt = tile / ntc, ct = tile % ntc;
+    double r0 = 0.0, r1 = 0.0, i0 = 0.0, i1 = 0.0;
+#pragma unroll 4
+    for (int ks = 0; ks < K2 / 4; ++ks) {
+      const int k = ks * 4 + t;
+      dmma(r0, r1, Are[(rt * 8 + gq) * SA + k], Bre[k * SBc + ct * 8 + gq]);
+      dmma(i0, i1, Aim[(rt * 8 + gq) * SA + k], Bim[k * SBc + ct * 8 + gq]);
+    }
+    const int iz = rt * 8 + gq;
+    if (iz >= pz) continue;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int cc = ct * 8 + 2 * t + e;
+      if (cc >= ncb) continue;
+      const double2 f0 = F0[cc];
+      dst[(size_t)iz * ncol + c0 + cc] = make_double2((e ? r1 : r0) + f0.x, (e ? i1 : i0) + f0.y);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ inv_xy --
 // 16 warps; the compressed C1 rows of the next four slabs arrive by cp.async
 // (double buffered) and feed the Y-stage B fragments directly through the
@@ -548,6 +699,178 @@ __global__ void __launch_bounds__(kWI * 32, 1) k_inv_xy_mma(PWGrid g, const int*
   }
 }
 
+// inv_xy with the Hermitian split of the Y stage.  conj E[+-my] = Er -+ i Ei,
+// so with U = C[+my] + C[-my], V = C[+my] - C[-my] (my >= 1)
+//   d.re = C[0].re + sum_my Er Ur + Ei Vi,   d.im = C[0].im + sum_my Er Ui - Ei Vr
+// -- two real GEMMs with K = 2M (A' = [Er | +-Ei], B' = [U ; V] parts)
+// instead of a complex GEMM with K = 2 (2M + 1).  The compressed C1 rows of
+// four slabs are scattered by cp.async into dense (my, m0) slabs (zero
+// outside the band); a pre-pass forms B'; the m0 = 0 column is a CUDA-core
+// dot product.  X stage as before over K = (m0, re|im), m0 = 0..M.
+template <int PT, int PC, int NC>
+__global__ void __launch_bounds__(kWI * 32, 1) k_inv_xy2(PWGrid g, const int* __restrict__ tboxes, int d,
+                                                        const double2* __restrict__ C, double pf,
+                                                        double* __restrict__ incoming) {
+  constexpr int P8 = PT * 8;
+  constexpr int XTW = (4 * PT * PT + kWI - 1) / kWI;  // X tiles per warp
+  const int p = PC > 0 ? PC : g.p, N = NC > 0 ? NC : g.N, M = (N - 1) / 2, ncol = g.ncol, pp = p * p;
+  const int M1 = M + 1, MT = (M + 7) / 8, M8 = MT * 8, K2 = 2 * M8;
+  const int SA2 = r4(K2);                    // A' rows iy
+  const int SB = (M8 % 16 == 8) ? M8 : M8 + 8;  // B' rows k' (== 8 mod 16)
+  const int NXK = (2 * M1 + 3) / 4 * 4;      // X-stage K
+  const int SX = r4(NXK);
+  const int ND = N * M1;                     // dense slab entries (my + M, m0)
+  extern __shared__ double sm[];
+  double* Are = sm;                          // [P8][SA2]
+  double* Aim = Are + P8 * SA2;              // [P8][SA2]
+  double* EXw = Aim + P8 * SA2;              // [P8 (ix)][SX]
+  double* dd = EXw + P8 * SX;                // [4*P8][SX]
+  double* Bre = dd + 4 * P8 * SX;            // [4][K2][SB]
+  double* Bim = Bre + 4 * K2 * SB;           // [4][K2][SB]
+  double2* den = reinterpret_cast<double2*>(Bim + 4 * K2 * SB);  // [2][4][ND]
+  int* dix = reinterpret_cast<int*>(den + 2 * 4 * ND);            // [ncol]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
+  for (int e = tid; e < P8 * SA2; e += blockDim.x) {
+    const int iy = e / SA2, k = e % SA2;
+    double vr = 0.0, vi = 0.0;
+    if (iy < p && k < K2) {
+      const int myp = k < M8 ? k : k - M8;
+      if (myp < M) {
+        const double2 ev = g.E[(size_t)(myp + 1 + M) * p + iy];
+        vr = k < M8 ? ev.x : ev.y;
+        vi = k < M8 ? ev.x : -ev.y;
+      }
+    }
+    Are[e] = vr;
+    Aim[e] = vi;
+  }
+  for (int e = tid; e < P8 * SX; e += blockDim.x) {  // Re(conj(E) d) = Er d.re + Ei d.im, weight 1 | 2
+    const int ix = e / SX, k = e % SX, m0 = k >> 1, part = k & 1;
+    double v = 0.0;
+    if (ix < p && m0 < M1) {
+      const double2 ev = g.E[(size_t)(m0 + M) * p + ix];
+      v = (m0 ? 2.0 : 1.0) * (part ? ev.y : ev.x);
+    }
+    EXw[e] = v;
+  }
+  for (int e = tid; e < 4 * P8 * SX; e += blockDim.x) dd[e] = 0.0;
+  for (int e = tid; e < 2 * 4 * ND; e += blockDim.x) den[e] = make_double2(0.0, 0.0);
+  for (int e = tid; e < 2 * 4 * K2 * SB; e += blockDim.x) Bre[e] = 0.0;  // Bre and Bim
+  for (int c = tid; c < ncol; c += blockDim.x) dix[c] = (g.col_my[c] + M) * M1 + g.col_m0[c];
+  __syncthreads();
+  const int tb = blockIdx.x, j = blockIdx.y;
+  const double2* Ci = C + ((size_t)tb * d + j) * (size_t)g.pz * ncol;
+  double* out = incoming + ((size_t)tboxes[tb] * d + j) * (size_t)(p * pp);
+  const int ngroups = (p + 3) / 4;
+  auto issue = [&](int grp, int buf) {
+    double2* dst = den + buf * 4 * ND;
+    for (int s = 0; s < 4; ++s) {
+      const int iz = grp * 4 + s;
+      if (iz >= p) break;
+      const double2* src = Ci + (size_t)iz * ncol;
+      for (int c = tid; c < ncol; c += blockDim.x) dev::cp_async16(dst + s * ND + dix[c], src + c);
+    }
+    cp_commit();
+  };
+  issue(0, 0);
+  const int nyu = 4 * PT * MT;  // Y units (s, iy tile, m0 tile)
+  for (int grp = 0; grp < ngroups; ++grp) {
+    const int buf = grp & 1;
+    __syncthreads();  // the buffer the next issue overwrites is free
+    if (grp + 1 < ngroups) {
+      issue(grp + 1, buf ^ 1);
+      cp_wait1();
+    } else {
+      cp_wait0();
+    }
+    __syncthreads();
+    // this warp's X-stage outputs: start their HBM reads now
+    double o0[XTW], o1[XTW];
+#pragma unroll
+    for (int i = 0; i < XTW; ++i) {
+      o0[i] = o1[i] = 0.0;
+      const int tile = warp + kWI * i;
+      if (tile < 4 * PT * PT) {
+        const int mt = tile / PT, nt = tile % PT;
+        const int s = mt / PT, iy = (mt % PT) * 8 + gq, iz = grp * 4 + s, ix = nt * 8 + 2 * t;
+        if (iz < p && iy < p) {
+          const double* o = out + (size_t)iz * pp + iy * p;
+          if (ix < p) o0[i] = o[ix];
+          if (ix + 1 < p) o1[i] = o[ix + 1];
+        }
+      }
+    }
+    const double2* D = den + buf * 4 * ND;
+    // B' = [U ; V] parts for my, m0 = 1..M
+    for (int e = tid; e < 4 * M * M; e += blockDim.x) {
+      const int s = e / (M * M), r = e % (M * M), myp = r / M, m0p = r % M;
+      const double2 cp = D[s * ND + (myp + 1 + M) * M1 + m0p + 1];
+      const double2 cm = D[s * ND + (M - myp - 1) * M1 + m0p + 1];
+      double* br = Bre + s * K2 * SB;
+      double* bi = Bim + s * K2 * SB;
+      br[myp * SB + m0p] = cp.x + cm.x;         // Ur
+      br[(M8 + myp) * SB + m0p] = cp.y - cm.y;  // Vi
+      bi[myp * SB + m0p] = cp.y + cm.y;         // Ui
+      bi[(M8 + myp) * SB + m0p] = cp.x - cm.x;  // Vr
+    }
+    // m0 = 0 column on the CUDA cores
+    for (int e = tid; e < 4 * p; e += blockDim.x) {
+      const int s = e / p, iy = e % p;
+      const double2* Ds = D + s * ND;
+      double re = Ds[M * M1].x, im = Ds[M * M1].y;
+      for (int myp = 0; myp < M; ++myp) {
+        const double2 cp = Ds[(myp + 1 + M) * M1], cm = Ds[(M - myp - 1) * M1];
+        const double er = Are[iy * SA2 + myp], ei = Are[iy * SA2 + M8 + myp];
+        re = fma(er, cp.x + cm.x, fma(ei, cp.y - cm.y, re));
+        im = fma(er, cp.y + cm.y, fma(-ei, cp.x - cm.x, im));
+      }
+      dd[(s * P8 + iy) * SX] = re;
+      dd[(s * P8 + iy) * SX + 1] = im;
+    }
+    __syncthreads();
+    // Y stage: d[(s,iy), m0] for m0 = 1..M, plus the my = 0 term
+    for (int u = warp; u < nyu; u += kWI) {
+      const int s = u / (PT * MT), it = (u / MT) % PT, nt = u % MT;
+      double r0 = 0.0, r1 = 0.0, i0 = 0.0, i1 = 0.0;
+      const double* br = Bre + s * K2 * SB;
+      const double* bi = Bim + s * K2 * SB;
+#pragma unroll 4
+      for (int ks = 0; ks < K2 / 4; ++ks) {
+        const int k = ks * 4 + t;
+        dmma(r0, r1, Are[(it * 8 + gq) * SA2 + k], br[k * SB + nt * 8 + gq]);
+        dmma(i0, i1, Aim[(it * 8 + gq) * SA2 + k], bi[k * SB + nt * 8 + gq]);
+      }
+      const int row = s * P8 + it * 8 + gq;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int m0 = nt * 8 + 2 * t + e + 1;
+        if (m0 <= M) {
+          const double2 c0 = D[s * ND + M * M1 + m0];
+          dd[row * SX + 2 * m0] = (e ? r1 : r0) + c0.x;
+          dd[row * SX + 2 * m0 + 1] = (e ? i1 : i0) + c0.y;
+        }
+      }
+    }
+    __syncthreads();
+    // X stage: out[(s,iy), ix] += pf * sum_{(m0,part)} dd[(s,iy)][(m0,part)] EXw[ix][(m0,part)]
+#pragma unroll
+    for (int i = 0; i < XTW; ++i) {
+      const int tile = warp + kWI * i;
+      if (tile >= 4 * PT * PT) continue;
+      const int mt = tile / PT, nt = tile % PT;
+      double c0 = 0.0, c1 = 0.0;
+      for (int ks = 0; ks < NXK / 4; ++ks)
+        dmma(c0, c1, dd[(mt * 8 + gq) * SX + ks * 4 + t], EXw[(nt * 8 + gq) * SX + ks * 4 + t]);
+      const int s = mt / PT, iy = (mt % PT) * 8 + gq, iz = grp * 4 + s, ix = nt * 8 + 2 * t;
+      if (iz < p && iy < p) {
+        double* o = out + (size_t)iz * pp + iy * p;
+        if (ix < p) o[ix] = o0[i] + pf * c0;
+        if (ix + 1 < p) o[ix + 1] = o1[i] + pf * c1;
+      }
+    }
+  }
+}
+
 void attr(const void* fn, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
@@ -610,10 +933,23 @@ void launch_forward_mma(const PWGrid& g, const int* boxes, int nbox, int nch, co
     attr((const void*)k_z_mma<KT_, RT_, false>, smem);                                \
     k_z_mma<KT_, RT_, false><<<grid, kW * 32, smem, st>>>(g, nch, B, G);              \
   } while (0)
-    if (KT <= 3) {
-      if (RT <= 5) ZF(3, 5); else ZF(3, 6);
+    static const bool old_z = std::getenv("SDMK_PW_OLD") != nullptr;
+    if (old_z) {
+      if (KT <= 3) {
+        if (RT <= 5) ZF(3, 5); else ZF(3, 6);
+      } else {
+        if (RT <= 5) ZF(4, 5); else ZF(4, 6);
+      }
     } else {
-      if (RT <= 5) ZF(4, 5); else ZF(4, 6);
+      const int M8 = (g.Mz + 7) / 8 * 8, P8 = PT * 8;
+      const size_t sz = sizeof(double) * (2 * (size_t)M8 * (P8 + 4) + (size_t)P8 * SI);
+      if (PT <= 3) {
+        attr((const void*)k_zf2<3>, sz);
+        k_zf2<3><<<grid, kW * 32, sz, st>>>(g, nch, B, G);
+      } else {
+        attr((const void*)k_zf2<4>, sz);
+        k_zf2<4><<<grid, kW * 32, sz, st>>>(g, nch, B, G);
+      }
     }
 #undef ZF
   }
@@ -633,10 +969,24 @@ void launch_inverse_mma(const PWGrid& g, const int* tboxes, int ntb, int d, cons
     attr((const void*)k_z_mma<KT_, RT_, true>, smem);                                 \
     k_z_mma<KT_, RT_, true><<<grid, kW * 32, smem, st>>>(g, d, F, C);                 \
   } while (0)
-    if (RT <= 3) {
-      if (KT <= 5) ZI(5, 3); else ZI(6, 3);
+    static const bool old_z = std::getenv("SDMK_PW_OLD") != nullptr;
+    if (old_z) {
+      if (RT <= 3) {
+        if (KT <= 5) ZI(5, 3); else ZI(6, 3);
+      } else {
+        if (KT <= 5) ZI(5, 4); else ZI(6, 4);
+      }
     } else {
-      if (KT <= 5) ZI(5, 4); else ZI(6, 4);
+      const int M8 = (g.Mz + 7) / 8 * 8, P8 = PT * 8, SBc = (kCB % 16 == 8) ? kCB : kCB + 8;
+      const size_t sz = sizeof(double) * (2 * (size_t)P8 * r4(2 * M8) + 2 * 2 * (size_t)M8 * SBc) +
+                        sizeof(double2) * kCB;
+      if (PT <= 3) {
+        attr((const void*)k_zi2<3>, sz);
+        k_zi2<3><<<grid, kW * 32, sz, st>>>(g, d, F, C);
+      } else {
+        attr((const void*)k_zi2<4>, sz);
+        k_zi2<4><<<grid, kW * 32, sz, st>>>(g, d, F, C);
+      }
     }
 #undef ZI
   }
@@ -651,11 +1001,35 @@ void launch_inverse_mma(const PWGrid& g, const int* tboxes, int ntb, int d, cons
     attr((const void*)k_inv_xy_mma<PT_, PC_, NC_>, smem);                                    \
     k_inv_xy_mma<PT_, PC_, NC_><<<grid, kWI * 32, smem, st>>>(g, tboxes, d, C, pf, incoming); \
   } while (0)
-    if (g.p == 23 && g.N == 33) IX(3, 23, 33);
-    else if (g.p == 22 && g.N == 33) IX(3, 22, 33);
-    else if (g.p == 30 && g.N == 45) IX(4, 30, 45);
-    else if (PT <= 3) IX(3, 0, 0);
-    else IX(4, 0, 0);
+    static const bool old_xy = std::getenv("SDMK_PW_OLD") != nullptr;
+    const int M_ = g.M, M8_ = (M_ + 7) / 8 * 8, SB_ = (M8_ % 16 == 8) ? M8_ : M8_ + 8, NXK_ = (2 * M1 + 3) / 4 * 4;
+    const size_t sm2_ = sizeof(double) * (2 * (size_t)P8 * r4(2 * M8_) + 5 * (size_t)P8 * r4(NXK_) +
+                                          2 * 4 * (size_t)2 * M8_ * SB_) +
+                        sizeof(double2) * 2 * 4 * (size_t)g.N * M1 + sizeof(int) * (size_t)g.ncol;
+    if (old_xy || sm2_ > 227 * 1024) {  // the split kernel stages dense slabs: too big for the largest grids
+      if (g.p == 23 && g.N == 33) IX(3, 23, 33);
+      else if (g.p == 22 && g.N == 33) IX(3, 22, 33);
+      else if (g.p == 30 && g.N == 45) IX(4, 30, 45);
+      else if (PT <= 3) IX(3, 0, 0);
+      else IX(4, 0, 0);
+    } else {
+      const int M = g.M, MT = (M + 7) / 8, M8 = MT * 8, K2 = 2 * M8;
+      const int SA2 = r4(K2), SB = (M8 % 16 == 8) ? M8 : M8 + 8, NXK = (2 * M1 + 3) / 4 * 4, SX2 = r4(NXK);
+      const size_t sm2 = sizeof(double) * (2 * (size_t)P8 * SA2 + (size_t)P8 * SX2 + 4 * (size_t)P8 * SX2 +
+                                           2 * 4 * (size_t)K2 * SB) +
+                         sizeof(double2) * 2 * 4 * (size_t)g.N * M1 + sizeof(int) * (size_t)g.ncol;
+#define IX2(PT_, PC_, NC_)                                                                  \
+  do {                                                                                      \
+    attr((const void*)k_inv_xy2<PT_, PC_, NC_>, sm2);                                       \
+    k_inv_xy2<PT_, PC_, NC_><<<grid, kWI * 32, sm2, st>>>(g, tboxes, d, C, pf, incoming);   \
+  } while (0)
+      if (g.p == 23 && g.N == 33) IX2(3, 23, 33);
+      else if (g.p == 22 && g.N == 33) IX2(3, 22, 33);
+      else if (g.p == 30 && g.N == 45) IX2(4, 30, 45);
+      else if (PT <= 3) IX2(3, 0, 0);
+      else IX2(4, 0, 0);
+#undef IX2
+    }
 #undef IX
   }
 }
