@@ -730,6 +730,7 @@ void Context::run_upward() {  // dmk.cpp:555-655
       launch_tensor_apply(p, pz, d, mats_up_, X.merge_in, X.merge_out, X.merge_ci, X.n_merge, pr.nch, og, og, 2, st_);
     ++launches_;
   }
+  cuda_check(cudaPeekAtLastError(), "kernel launch");
 }
 
 void Context::run_root() {  // dmk.cpp:657-701
@@ -850,6 +851,7 @@ void Context::run_downward() {  // dmk.cpp:705-857
   }
   t_pw_ms_ = pw_ms;
   sync();
+  cuda_check(cudaPeekAtLastError(), "kernel launch");
 }
 
 void Context::run_target_far(double* ufar) {  // dmk.cpp:861-915

@@ -32,24 +32,63 @@ __host__ __device__ __forceinline__ int cstride(int x) {  // smallest y >= x wit
 }
 
 // ---------------------------------------------------------------- bases --
-__global__ void __launch_bounds__(256) k_basis(ChebDev cb, const DBox* __restrict__ boxes,
-                                               const int* __restrict__ leaves, const double* __restrict__ pts, int n,
-                                               int use_targets, double* __restrict__ basis) {
+// Barycentric Lagrange basis (dmk.cpp:39-53) without p divisions per point:
+// with d_j = x - x_j, w_i / d_i = w_i q_i / P where q_i = prod_{j != i} d_j and
+// P = prod_j d_j, and P cancels in the normalisation, so
+//   l_i(x) = w_i q_i / sum_j w_j q_j
+// (q from prefix / suffix products; one division per point and axis).  The
+// exact-hit rule is kept.  A warp owns 32 consecutive points of one axis; the
+// rows are assembled in shared memory and stored coalesced.
+constexpr int kBasisW = 8;
+__global__ void __launch_bounds__(kBasisW * 32) k_basis(ChebDev cb, const DBox* __restrict__ boxes,
+                                                       const int* __restrict__ leaves, const double* __restrict__ pts,
+                                                       int n, int use_targets, double* __restrict__ basis) {
   __shared__ double nodes[64], wts[64];
-  const int p = cb.p, dim = cb.dim;
+  extern __shared__ double rowbuf[];  // [kBasisW][32][p | 1]: odd row stride, conflict-free lanes
+  const int p = cb.p, dim = cb.dim, P1 = p | 1;
   for (int i = threadIdx.x; i < p; i += blockDim.x) {
     nodes[i] = cb.nodes[i];
     wts[i] = cb.wts[i];
   }
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* rb = rowbuf + warp * 32 * P1;
   const DBox box = boxes[leaves[blockIdx.x]];
   const int b0 = use_targets ? box.tb : box.sb, b1 = use_targets ? box.te : box.se;
   const double hinv = 1.0 / box.half;
-  const int cnt = b1 - b0;
-  for (int task = threadIdx.x; task < cnt * dim; task += blockDim.x) {
-    const int ax = task / cnt, i = b0 + task % cnt;
-    const double x = __dmul_rn(__dsub_rn(pts[(size_t)ax * n + i], box.c[ax]), hinv);
-    dev::cheb_basis(p, nodes, wts, x, basis + ((size_t)ax * n + i) * p, 1);
+  const int cnt = b1 - b0, nchunk = (cnt + 31) / 32;
+  for (int task = warp; task < nchunk * dim; task += kBasisW) {
+    const int ax = task / nchunk, i0 = b0 + (task % nchunk) * 32, i = i0 + lane;
+    const int nv = min(32, b1 - i0);
+    double* r = rb + lane * P1;
+    if (lane < nv) {
+      const double x = __dmul_rn(__dsub_rn(pts[(size_t)ax * n + i], box.c[ax]), hinv);
+      int hit = -1;
+      for (int k = 0; k < p; ++k)
+        if (x == nodes[k]) hit = hit < 0 ? k : hit;
+      if (hit >= 0) {
+        for (int k = 0; k < p; ++k) r[k] = k == hit ? 1.0 : 0.0;
+      } else {
+        double pre = 1.0;
+        for (int k = 0; k < p; ++k) {  // r[k] = prod_{j < k} d_j
+          r[k] = pre;
+          pre *= x - nodes[k];
+        }
+        double suf = 1.0, sum = 0.0;
+        for (int k = p - 1; k >= 0; --k) {  // r[k] = w_k prod_{j != k} d_j
+          const double v = wts[k] * (r[k] * suf);
+          r[k] = v;
+          sum += v;
+          suf *= x - nodes[k];
+        }
+        const double inv = 1.0 / sum;
+        for (int k = 0; k < p; ++k) r[k] *= inv;
+      }
+    }
+    __syncwarp();
+    double* dst = basis + ((size_t)ax * n + i0) * p;
+    for (int e = lane; e < nv * p; e += 32) dst[e] = rb[(e / p) * P1 + e % p];
+    __syncwarp();
   }
 }
 
@@ -380,7 +419,9 @@ bool mma_anterp_supported(int p) { return p <= 48; }
 void launch_basis(const ChebDev& cb, const DBox* boxes, const int* leaves, int nleaf, const double* pts, int n,
                   int use_targets, double* basis, cudaStream_t st) {
   if (nleaf <= 0) return;
-  k_basis<<<nleaf, 256, 0, st>>>(cb, boxes, leaves, pts, n, use_targets, basis);
+  const size_t sm = sizeof(double) * kBasisW * 32 * (cb.p | 1);
+  cudaFuncSetAttribute((const void*)k_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_basis<<<nleaf, kBasisW * 32, sm, st>>>(cb, boxes, leaves, pts, n, use_targets, basis);
 }
 
 void launch_anterp_mma(int kernel, const ChebDev& cb, const DBox* boxes, const int* leaves, int nleaf,
