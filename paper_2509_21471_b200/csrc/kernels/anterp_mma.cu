@@ -17,6 +17,8 @@
 #include "common.cuh"
 #include "launch.hpp"
 
+#include <cstdlib>
+
 namespace sdmkb {
 
 namespace {
@@ -270,6 +272,140 @@ __global__ void __launch_bounds__(kAWarps * 32, 2) k_anterp_mma(int kernel_rt, C
   }
 }
 
+// K3, second form: C[(ch,iz), (iy,ix)] = sum_a S[a, (ch,iz)] (by[a,iy] bx[a,ix])
+// with S = s_ch bz formed once per chunk in shared memory (the A operand,
+// fragment loads only) and the B values by * bx formed per fragment, each
+// feeding all MT m-tiles of the (ch, iz) rows: 1 multiply per MT DMMAs
+// instead of one per n-tile.  A warp owns NTW column tiles of the (iy, ix)
+// plane; a CTA covers 8 NTW of them, so a leaf takes ceil(p^2 / 64 NTW) CTAs.
+constexpr int kA2W = 12;  // warps per CTA
+template <int MT, int NTW, int PC, int KC, int DC>
+__global__ void __launch_bounds__(kA2W * 32, 1) k_anterp2(ChebDev cb, const DBox* __restrict__ boxes,
+                                                            const int* __restrict__ leaves,
+                                                            const double* __restrict__ basis,
+                                                            const double* __restrict__ str, int n,
+                                                            double* __restrict__ out) {
+  extern __shared__ double sm[];
+  constexpr int p = PC, dim = DC, pz = dim == 3 ? p : 1, kernel = KC;
+  constexpr int sc = kernel == 0 ? dim : (kernel == 1 ? 2 * dim : (dim == 3 ? 3 : 1));
+  constexpr int nch = kernel == 0 ? dim : (kernel == 1 ? dim * (dim + 1) / 2 : (dim == 3 ? 3 : 1));
+  constexpr int MR = nch * pz, NN = p * p;
+  constexpr int RS = (MT * 8) % 8 == 4 ? MT * 8 : MT * 8 + 4;  // point rows: == 4 mod 8 (fragment loads)
+  constexpr int XS = (p + 3) / 4 * 4 % 8 == 4 ? (p + 3) / 4 * 4 : (p + 3) / 4 * 4 + 4;  // == 4 mod 8
+  constexpr int RAW = kKC * (3 * XS + 8);
+  double* sbz = sm;                 // [kKC][RS]
+  double* raw = sbz + kKC * RS;     // 2 x { bx[kKC][XS], by[kKC][XS], bz[kKC][XS], str[kKC][8] }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int b = leaves[blockIdx.x];
+  const DBox box = boxes[b];
+  const int nt0 = blockIdx.y * kA2W * NTW;
+  __shared__ int rcode[MT * 8];  // (ch, iz) of each S row
+  for (int r = tid; r < MT * 8; r += blockDim.x) rcode[r] = r < MR ? ((r / pz) | ((r % pz) << 8)) : -1;
+  int iyv[NTW], ixv[NTW];
+#pragma unroll
+  for (int j = 0; j < NTW; ++j) {
+    const int col = (nt0 + warp + kA2W * j) * 8 + g;
+    iyv[j] = col < NN ? col / p : 0;
+    ixv[j] = col < NN ? col % p : 0;
+  }
+  double acc[MT][NTW][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int e = tid; e < kKC * RS; e += blockDim.x) sbz[e] = 0.0;  // row padding stays zero
+  const double* bxg = basis;
+  const double* byg = basis + (size_t)n * p;
+  const double* bzg = basis + (size_t)2 * n * p;
+  const int nchunks = (box.se - box.sb + kKC - 1) / kKC;
+  auto issue = [&](int c, int buf) {
+    const int a0 = box.sb + c * kKC, kc = min(kKC, box.se - a0);
+    double* rb = raw + buf * RAW;
+    for (int e = tid; e < kKC * p; e += blockDim.x) {
+      const int pt = e / p, i = e % p;
+      const bool v = pt < kc;
+      const size_t o = (size_t)(a0 + (v ? pt : 0)) * p + i;
+      dev::cp_async8(rb + pt * XS + i, bxg + o, v);
+      dev::cp_async8(rb + kKC * XS + pt * XS + i, byg + o, v);
+      if (dim == 3) dev::cp_async8(rb + 2 * kKC * XS + pt * XS + i, bzg + o, v);
+    }
+    for (int e = tid; e < kKC * sc; e += blockDim.x) {
+      const int pt = e / sc, j = e % sc;
+      const bool v = pt < kc;
+      dev::cp_async8(rb + 3 * kKC * XS + pt * 8 + j, v ? str + (size_t)j * n + a0 + pt : str, v);
+    }
+    dev::cp_commit();
+  };
+  if (nchunks > 0) issue(0, 0);
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c & 1;
+    __syncthreads();  // everyone is done with the buffer the next issue overwrites (and with sbz)
+    if (c + 1 < nchunks) {
+      issue(c + 1, buf ^ 1);
+      dev::cp_wait1();
+    } else {
+      dev::cp_wait0();
+    }
+    __syncthreads();
+    const double* bx = raw + buf * RAW;
+    const double* by = bx + kKC * XS;
+    const double* bz = by + kKC * XS;
+    const double* ss = bz + kKC * XS;
+    for (int r = tid % (MT * 8), pt = tid / (MT * 8); pt < kKC; pt += blockDim.x / (MT * 8)) {  // S = s_ch * bz
+      if (tid >= (blockDim.x / (MT * 8)) * (MT * 8)) break;
+      const int code = rcode[r];
+      if (code < 0) continue;
+      const int ch = code & 255, iz = code >> 8;
+      const double* s = ss + pt * 8;
+      double sv;
+      if (kernel == 1) {
+        double w = 0.0;
+#pragma unroll
+        for (int j = 0; j < dim; ++j) w += s[j] * s[dim + j];
+        if (dim == 3) {
+          sv = ch == 0 ? 2.0 * s[0] * s[3] + w
+             : ch == 1 ? 2.0 * s[1] * s[4] + w
+             : ch == 2 ? 2.0 * s[2] * s[5] + w
+             : ch == 3 ? s[0] * s[4] + s[1] * s[3]
+             : ch == 4 ? s[0] * s[5] + s[2] * s[3]
+                       : s[1] * s[5] + s[2] * s[4];
+        } else {
+          sv = ch == 0 ? 2.0 * s[0] * s[2] + w : ch == 1 ? 2.0 * s[1] * s[3] + w : s[0] * s[3] + s[1] * s[2];
+        }
+      } else {
+        sv = s[ch];
+      }
+      sbz[pt * RS + r] = sv * (dim == 3 ? bz[pt * XS + iz] : 1.0);
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int ks = 0; ks < kKC / 4; ++ks) {
+      const int k = ks * 4 + t;
+      double bv[NTW];
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) bv[j] = by[k * XS + iyv[j]] * bx[k * XS + ixv[j]];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const double av = sbz[k * RS + i * 8 + g];
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) dev::dmma(acc[i][j][0], acc[i][j][1], av, bv[j]);
+      }
+    }
+  }
+  double* ob = out + (size_t)b * MR * NN;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int m = i * 8 + g;
+    if (m >= MR) continue;
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) {
+      const int cc = (nt0 + warp + kA2W * j) * 8 + 2 * t;
+      if (cc < NN) ob[(size_t)m * NN + cc] = acc[i][j][0];
+      if (cc + 1 < NN) ob[(size_t)m * NN + cc + 1] = acc[i][j][1];
+    }
+  }
+}
+
 // ------------------------------------------------------------------- K11 --
 constexpr int kIW = 12;                // warps per CTA
 constexpr int kITW = 4;                // m-tiles per warp
@@ -444,7 +580,21 @@ void launch_anterp_mma(int kernel, const ChebDev& cb, const DBox* boxes, const i
                                                                            str, n, out, nch, mt_per);   \
   } while (0)
 #define AM(NTT, MW) AMS(NTT, MW, 0, -1, 0)
-  if (cb.dim == 3 && p == 23 && kernel == 0) AMS(3, 6, 23, 0, 3);
+#define A2(MT_, NTW_, PC_, KC_)                                                                          \
+  do {                                                                                                  \
+    constexpr int RS_ = MT_ * 8 + 4;                                                                    \
+    constexpr int XS_ = (PC_ + 3) / 4 * 4 % 8 == 4 ? (PC_ + 3) / 4 * 4 : (PC_ + 3) / 4 * 4 + 4;         \
+    const size_t sm2 = sizeof(double) * (size_t)kKC * (RS_ + 2 * (3 * XS_ + 8));                       \
+    const int ntt = (PC_ * PC_ + 7) / 8, per = kA2W * NTW_;                                             \
+    smem_attr((const void*)k_anterp2<MT_, NTW_, PC_, KC_, 3>, sm2);                                     \
+    k_anterp2<MT_, NTW_, PC_, KC_, 3><<<dim3(nleaf, (ntt + per - 1) / per), kA2W * 32, sm2, st>>>(      \
+        cb, boxes, leaves, basis, str, n, out);                                                         \
+  } while (0)
+  static const bool old_a = std::getenv("SDMK_ANTERP_OLD") != nullptr;
+  if (!old_a && cb.dim == 3 && p == 23 && kernel == 0) A2(9, 2, 23, 0);
+  else if (!old_a && cb.dim == 3 && p == 22 && kernel == 1) A2(17, 2, 22, 1);
+  else if (!old_a && cb.dim == 3 && p == 30 && kernel == 0) A2(12, 2, 30, 0);
+  else if (cb.dim == 3 && p == 23 && kernel == 0) AMS(3, 6, 23, 0, 3);
   else if (cb.dim == 3 && p == 22 && kernel == 1) AMS(3, 6, 22, 1, 3);
   else if (cb.dim == 3 && p == 30 && kernel == 0) AMS(4, 4, 30, 0, 3);
   else if (NTv <= 1) AM(1, 8);
@@ -455,6 +605,7 @@ void launch_anterp_mma(int kernel, const ChebDev& cb, const DBox* boxes, const i
   else AM(6, 3);
 #undef AM
 #undef AMS
+#undef A2
 }
 
 void launch_interp_mma(const ChebDev& cb, const DBox* boxes, const int* leaves, int nleaf, const double* tbasis,
