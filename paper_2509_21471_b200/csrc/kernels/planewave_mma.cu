@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "launch.hpp"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace sdmkb {
@@ -421,8 +422,11 @@ __global__ void __launch_bounds__(kW * 32, 2) k_z_mma(PWGrid g, int nc, const do
 //  inverse  C1.re = F[0].re + [Er | Ei] [Ur ; Vi],  C1.im = F[0].im + [Er | -Ei] [Ui ; Vr]
 //           with U = F[+mz] + F[-mz], V = F[+mz] - F[-mz] (zero outside the band).
 // ~2.5x fewer DMMAs than the complex GEMMs over all 2M + 1 rows.
+// Persistent forms: a CTA keeps its E matrices and walks work items
+// (box, component, 64-column block) with stride gridDim.x, the next item's
+// input arriving by cp.async while the current one is multiplied.
 template <int PT>
-__global__ void __launch_bounds__(kW * 32, 2) k_zf2(PWGrid g, int nc, const double2* __restrict__ IN,
+__global__ void __launch_bounds__(kW * 32, 3) k_zf2(PWGrid g, int nc, int nbox, const double2* __restrict__ IN,
                                                    double2* __restrict__ OUT) {
   constexpr int P8 = PT * 8, SK = P8 + 4;
   constexpr int SI = (2 * kCB) % 16 == 8 ? 2 * kCB : 2 * kCB + 8;
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(kW * 32, 2) k_zf2(PWGrid g, int nc, const doub
   const int M = g.Mz, MT = (M + 7) / 8, M8 = MT * 8, pz = g.pz, ncol = g.ncol;
   double* Ar = sm;               // [M8][SK]  Er[mz = r + 1][iz]
   double* Ai = Ar + M8 * SK;     // [M8][SK]
-  double* In = Ai + M8 * SK;     // [P8][SI]  (col, re|im) interleaved
+  double* In = Ai + M8 * SK;     // [2][P8][SI]  (col, re|im) interleaved
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
   for (int e = tid; e < M8 * SK; e += blockDim.x) {
     const int r = e / SK, k = e % SK;
@@ -443,70 +447,85 @@ __global__ void __launch_bounds__(kW * 32, 2) k_zf2(PWGrid g, int nc, const doub
     Ar[e] = vr;
     Ai[e] = vi;
   }
-  const int box = blockIdx.x, comp = blockIdx.y, c0 = blockIdx.z * kCB;
-  const int ncb = min(kCB, ncol - c0);
-  const double2* src = IN + ((size_t)box * nc + comp) * (size_t)pz * ncol;
-  double2* dst = OUT + ((size_t)box * nc + comp) * (size_t)g.nhalf;
-  for (int e = tid; e < P8 * kCB; e += blockDim.x) {
-    const int k = e / kCB, cc = e % kCB;
-    double2 v = make_double2(0.0, 0.0);
-    if (k < pz && cc < ncb) v = src[(size_t)k * ncol + c0 + cc];
-    In[k * SI + 2 * cc] = v.x;
-    In[k * SI + 2 * cc + 1] = v.y;
-  }
-  __syncthreads();
-  const int ntc = kCB / 8, ntile = MT * ntc;
-  for (int tile = warp; tile < ntile; tile += kW) {
-    const int rt = tile / ntc, ct = tile % ntc;
-    double P0 = 0, P1 = 0, Q0 = 0, Q1 = 0, R0 = 0, R1 = 0, S0 = 0, S1 = 0;
+  const int ncbk = (ncol + kCB - 1) / kCB, nitems = nbox * nc * ncbk;
+  auto issue = [&](int w, int buf) {
+    const int bc = w / ncbk, c0 = (w % ncbk) * kCB, ncb = min(kCB, ncol - c0);
+    const double2* src = IN + (size_t)bc * pz * ncol + c0;
+    double* dst = In + buf * P8 * SI;
+    for (int e = tid; e < P8 * kCB; e += blockDim.x) {
+      const int k = e / kCB, cc = e % kCB;
+      const bool v = k < pz && cc < ncb;
+      dev::cp_async16z(dst + k * SI + 2 * cc, v ? src + (size_t)k * ncol + cc : src, v);
+    }
+    cp_commit();
+  };
+  int w = blockIdx.x;
+  if (w < nitems) issue(w, 0);
+  for (int it = 0; w < nitems; ++it, w += gridDim.x) {
+    const int buf = it & 1;
+    if (w + (int)gridDim.x < nitems) {
+      issue(w + gridDim.x, buf ^ 1);
+      cp_wait1();
+    } else {
+      cp_wait0();
+    }
+    __syncthreads();
+    const double* Ib = In + buf * P8 * SI;
+    const int bc = w / ncbk, c0 = (w % ncbk) * kCB, ncb = min(kCB, ncol - c0);
+    double2* dst = OUT + (size_t)bc * g.nhalf;
+    const int ntc = kCB / 8, ntile = MT * ntc;
+    for (int tile = warp; tile < ntile; tile += kW) {
+      const int rt = tile / ntc, ct = tile % ntc;
+      double P0 = 0, P1 = 0, Q0 = 0, Q1 = 0, R0 = 0, R1 = 0, S0 = 0, S1 = 0;
 #pragma unroll
-    for (int ks = 0; ks < 2 * PT; ++ks) {
-      const int k = ks * 4 + t;
-      const double br = In[k * SI + 2 * (ct * 8 + gq)], bi = In[k * SI + 2 * (ct * 8 + gq) + 1];
-      const double er = Ar[(rt * 8 + gq) * SK + k], ei = Ai[(rt * 8 + gq) * SK + k];
-      dmma(P0, P1, er, br);
-      dmma(Q0, Q1, ei, bi);
-      dmma(R0, R1, er, bi);
-      dmma(S0, S1, ei, br);
-    }
-    const int mz = rt * 8 + gq + 1;
-    if (mz > M) continue;
-    const int np = g.slab_ncol[mz + M], nm = g.slab_ncol[M - mz];
-    const int op = g.slab_off[mz + M], om = g.slab_off[M - mz];
+      for (int ks = 0; ks < 2 * PT; ++ks) {
+        const int k = ks * 4 + t;
+        const double br = Ib[k * SI + 2 * (ct * 8 + gq)], bi = Ib[k * SI + 2 * (ct * 8 + gq) + 1];
+        const double er = Ar[(rt * 8 + gq) * SK + k], ei = Ai[(rt * 8 + gq) * SK + k];
+        dmma(P0, P1, er, br);
+        dmma(Q0, Q1, ei, bi);
+        dmma(R0, R1, er, bi);
+        dmma(S0, S1, ei, br);
+      }
+      const int mz = rt * 8 + gq + 1;
+      if (mz > M) continue;
+      const int np = g.slab_ncol[mz + M], nm = g.slab_ncol[M - mz];
+      const int op = g.slab_off[mz + M], om = g.slab_off[M - mz];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int cc = ct * 8 + 2 * t + e, col = c0 + cc;
-      if (cc >= ncb) continue;
-      const double P = e ? P1 : P0, Q = e ? Q1 : Q0, R = e ? R1 : R0, S = e ? S1 : S0;
-      if (col < np) dst[op + col] = make_double2(P - Q, R + S);
-      if (col < nm) dst[om + col] = make_double2(P + Q, R - S);
+      for (int e = 0; e < 2; ++e) {
+        const int cc = ct * 8 + 2 * t + e, col = c0 + cc;
+        if (cc >= ncb) continue;
+        const double P = e ? P1 : P0, Q = e ? Q1 : Q0, R = e ? R1 : R0, S = e ? S1 : S0;
+        if (col < np) dst[op + col] = make_double2(P - Q, R + S);
+        if (col < nm) dst[om + col] = make_double2(P + Q, R - S);
+      }
     }
-  }
-  // mz = 0: column sums over iz
-  for (int cc = tid; cc < ncb; cc += blockDim.x) {
-    const int col = c0 + cc;
-    if (col >= g.slab_ncol[M]) continue;
-    double re = 0.0, im = 0.0;
-    for (int k = 0; k < pz; ++k) {
-      re += In[k * SI + 2 * cc];
-      im += In[k * SI + 2 * cc + 1];
+    // mz = 0: column sums over iz
+    for (int cc = tid; cc < ncb; cc += blockDim.x) {
+      const int col = c0 + cc;
+      if (col >= g.slab_ncol[M]) continue;
+      double re = 0.0, im = 0.0;
+      for (int k = 0; k < pz; ++k) {
+        re += Ib[k * SI + 2 * cc];
+        im += Ib[k * SI + 2 * cc + 1];
+      }
+      dst[g.slab_off[M] + col] = make_double2(re, im);
     }
-    dst[g.slab_off[M] + col] = make_double2(re, im);
+    __syncthreads();  // this buffer is refilled by the issue two items ahead
   }
 }
 
 template <int PT>
-__global__ void __launch_bounds__(kW * 32, 2) k_zi2(PWGrid g, int nc, const double2* __restrict__ IN,
+__global__ void __launch_bounds__(kW * 32, 2) k_zi2(PWGrid g, int nc, int nbox, const double2* __restrict__ IN,
                                                    double2* __restrict__ OUT) {
   constexpr int P8 = PT * 8;
-  constexpr int SBc = (kCB % 16 == 8) ? kCB : kCB + 8;  // B' rows (== 8 mod 16)
   extern __shared__ double sm[];
   const int M = g.Mz, MT = (M + 7) / 8, M8 = MT * 8, K2 = 2 * M8, SA = r4(K2), pz = g.pz, ncol = g.ncol;
+  const int NZ = 2 * M + 1;
   double* Are = sm;                  // [P8][SA]  [Er | Ei]
   double* Aim = Are + P8 * SA;       // [P8][SA]  [Er | -Ei]
-  double* Bre = Aim + P8 * SA;       // [K2][SBc] [Ur ; Vi]
-  double* Bim = Bre + K2 * SBc;      // [K2][SBc] [Ui ; Vr]
-  double2* F0 = reinterpret_cast<double2*>(Bim + K2 * SBc);  // [kCB]
+  constexpr int FR = kCB + 2;        // F row stride (double2): 16-byte fragment loads conflict-free
+  double2* Fs = reinterpret_cast<double2*>(Aim + P8 * SA);  // [2][NZ][FR]  raw F rows (mz + M)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
   for (int e = tid; e < P8 * SA; e += blockDim.x) {
     const int iz = e / SA, k = e % SA;
@@ -522,47 +541,72 @@ __global__ void __launch_bounds__(kW * 32, 2) k_zi2(PWGrid g, int nc, const doub
     Are[e] = vr;
     Aim[e] = vi;
   }
-  const int box = blockIdx.x, comp = blockIdx.y, c0 = blockIdx.z * kCB;
-  const int ncb = min(kCB, ncol - c0);
-  const double2* src = IN + ((size_t)box * nc + comp) * (size_t)g.nhalf;
-  double2* dst = OUT + ((size_t)box * nc + comp) * (size_t)pz * ncol;
-  for (int e = tid; e < M8 * kCB; e += blockDim.x) {
-    const int r = e / kCB, cc = e % kCB, col = c0 + cc;
-    double2 fp = make_double2(0.0, 0.0), fm = fp;
-    if (r < M && cc < ncb) {
-      const int mz = r + 1;
-      if (col < g.slab_ncol[M + mz]) fp = src[g.slab_off[M + mz] + col];
-      if (col < g.slab_ncol[M - mz]) fm = src[g.slab_off[M - mz] + col];
+  const int ncbk = (ncol + kCB - 1) / kCB, nitems = nbox * nc * ncbk;
+  auto issue = [&](int w, int buf) {
+    const int bc = w / ncbk, c0 = (w % ncbk) * kCB;
+    const double2* src = IN + (size_t)bc * g.nhalf;
+    double2* dst = Fs + buf * NZ * FR;
+    for (int e = tid; e < NZ * kCB; e += blockDim.x) {
+      const int s = e / kCB, cc = e % kCB, col = c0 + cc;
+      const bool v = col < g.slab_ncol[s];
+      dev::cp_async16z(dst + s * FR + cc, v ? src + g.slab_off[s] + col : src, v);
     }
-    Bre[r * SBc + cc] = fp.x + fm.x;
-    Bre[(M8 + r) * SBc + cc] = fp.y - fm.y;
-    Bim[r * SBc + cc] = fp.y + fm.y;
-    Bim[(M8 + r) * SBc + cc] = fp.x - fm.x;
-  }
-  for (int cc = tid; cc < kCB; cc += blockDim.x) {
-    const int col = c0 + cc;
-    F0[cc] = (cc < ncb && col < g.slab_ncol[M]) ? src[g.slab_off[M] + col] : make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-  const int ntc = kCB / 8, ntile = PT * ntc;
-  for (int tile = warp; tile < ntile; tile += kW) {
-    const int rt = tile / ntc, ct = tile % ntc;
-    double r0 = 0.0, r1 = 0.0, i0 = 0.0, i1 = 0.0;
-#pragma unroll 4
+    cp_commit();
+  };
+  int w = blockIdx.x;
+  if (w < nitems) issue(w, 0);
+  for (int it = 0; w < nitems; ++it, w += gridDim.x) {
+    const int buf = it & 1;
+    if (w + (int)gridDim.x < nitems) {
+      issue(w + gridDim.x, buf ^ 1);
+      cp_wait1();
+    } else {
+      cp_wait0();
+    }
+    __syncthreads();
+    const double2* Fb = Fs + buf * NZ * FR;
+    const int bc = w / ncbk, c0 = (w % ncbk) * kCB, ncb = min(kCB, ncol - c0);
+    double2* dst = OUT + (size_t)bc * pz * ncol;
+    // warp w: column tile w, all row (iz) tiles; B' = [U ; V] formed at fragment load
+    const int ct = warp;
+    double r0[PT], r1[PT], i0[PT], i1[PT];
+#pragma unroll
+    for (int m = 0; m < PT; ++m) r0[m] = r1[m] = i0[m] = i1[m] = 0.0;
+    const int cc_b = ct * 8 + gq;
+#pragma unroll 2
     for (int ks = 0; ks < K2 / 4; ++ks) {
       const int k = ks * 4 + t;
-      dmma(r0, r1, Are[(rt * 8 + gq) * SA + k], Bre[k * SBc + ct * 8 + gq]);
-      dmma(i0, i1, Aim[(rt * 8 + gq) * SA + k], Bim[k * SBc + ct * 8 + gq]);
-    }
-    const int iz = rt * 8 + gq;
-    if (iz >= pz) continue;
+      const int r = k < M8 ? k : k - M8;  // mz - 1
+      double br = 0.0, bi = 0.0;
+      if (r < M) {
+        const double2 fp = Fb[(M + 1 + r) * FR + cc_b], fm = Fb[(M - 1 - r) * FR + cc_b];
+        if (k < M8) {
+          br = fp.x + fm.x;  // Ur
+          bi = fp.y + fm.y;  // Ui
+        } else {
+          br = fp.y - fm.y;  // Vi
+          bi = fp.x - fm.x;  // Vr
+        }
+      }
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int cc = ct * 8 + 2 * t + e;
-      if (cc >= ncb) continue;
-      const double2 f0 = F0[cc];
-      dst[(size_t)iz * ncol + c0 + cc] = make_double2((e ? r1 : r0) + f0.x, (e ? i1 : i0) + f0.y);
+      for (int m = 0; m < PT; ++m) {
+        dmma(r0[m], r1[m], Are[(m * 8 + gq) * SA + k], br);
+        dmma(i0[m], i1[m], Aim[(m * 8 + gq) * SA + k], bi);
+      }
     }
+#pragma unroll
+    for (int m = 0; m < PT; ++m) {
+      const int iz = m * 8 + gq;
+      if (iz >= pz) continue;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cc = ct * 8 + 2 * t + e;
+        if (cc >= ncb) continue;
+        const double2 f0 = Fb[M * FR + cc];
+        dst[(size_t)iz * ncol + c0 + cc] = make_double2((e ? r1[m] : r0[m]) + f0.x, (e ? i1[m] : i0[m]) + f0.y);
+      }
+    }
+    __syncthreads();  // this buffer is refilled by the issue two items ahead
   }
 }
 
@@ -871,6 +915,16 @@ __global__ void __launch_bounds__(kWI * 32, 1) k_inv_xy2(PWGrid g, const int* __
   }
 }
 
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
 void attr(const void* fn, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
@@ -942,13 +996,15 @@ void launch_forward_mma(const PWGrid& g, const int* boxes, int nbox, int nch, co
       }
     } else {
       const int M8 = (g.Mz + 7) / 8 * 8, P8 = PT * 8;
-      const size_t sz = sizeof(double) * (2 * (size_t)M8 * (P8 + 4) + (size_t)P8 * SI);
+      const size_t sz = sizeof(double) * (2 * (size_t)M8 * (P8 + 4) + 2 * (size_t)P8 * SI);
+      const int items = nbox * nch * ((g.ncol + kCB - 1) / kCB);
+      const int ctas = std::min(items, 3 * num_sms());
       if (PT <= 3) {
         attr((const void*)k_zf2<3>, sz);
-        k_zf2<3><<<grid, kW * 32, sz, st>>>(g, nch, B, G);
+        k_zf2<3><<<ctas, kW * 32, sz, st>>>(g, nch, nbox, B, G);
       } else {
         attr((const void*)k_zf2<4>, sz);
-        k_zf2<4><<<grid, kW * 32, sz, st>>>(g, nch, B, G);
+        k_zf2<4><<<ctas, kW * 32, sz, st>>>(g, nch, nbox, B, G);
       }
     }
 #undef ZF
@@ -977,15 +1033,16 @@ void launch_inverse_mma(const PWGrid& g, const int* tboxes, int ntb, int d, cons
         if (KT <= 5) ZI(5, 4); else ZI(6, 4);
       }
     } else {
-      const int M8 = (g.Mz + 7) / 8 * 8, P8 = PT * 8, SBc = (kCB % 16 == 8) ? kCB : kCB + 8;
-      const size_t sz = sizeof(double) * (2 * (size_t)P8 * r4(2 * M8) + 2 * 2 * (size_t)M8 * SBc) +
-                        sizeof(double2) * kCB;
+      const int M8 = (g.Mz + 7) / 8 * 8, P8 = PT * 8;
+      const size_t sz = sizeof(double) * 2 * (size_t)P8 * r4(2 * M8) + sizeof(double2) * 2 * (size_t)g.Nz * (kCB + 2);
+      const int items = ntb * d * ((g.ncol + kCB - 1) / kCB);
+      const int ctas = std::min(items, 2 * num_sms());
       if (PT <= 3) {
         attr((const void*)k_zi2<3>, sz);
-        k_zi2<3><<<grid, kW * 32, sz, st>>>(g, d, F, C);
+        k_zi2<3><<<ctas, kW * 32, sz, st>>>(g, d, ntb, F, C);
       } else {
         attr((const void*)k_zi2<4>, sz);
-        k_zi2<4><<<grid, kW * 32, sz, st>>>(g, d, F, C);
+        k_zi2<4><<<ctas, kW * 32, sz, st>>>(g, d, ntb, F, C);
       }
     }
 #undef ZI
