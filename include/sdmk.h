@@ -142,6 +142,16 @@ int sdmk_incoming(sdmk_context* ctx, int stage, double* incoming);
 int sdmk_target_far_fields(sdmk_context* ctx, double* u);
 int sdmk_residual_pass(sdmk_context* ctx, double* u);
 
+/* ---- multi-GPU (one process per GPU) ----
+   Shard the following evaluations by target leaves:
+   rank owns a contiguous Morton run of target leaves (balanced by target
+   count); the upward pass stays replicated, the downward, far-field and
+   residual passes run only for the owned leaves and their ancestors, and u
+   is written as zeros for other ranks' targets, so an element-wise sum over
+   ranks (an all-reduce) is the full result, bitwise equal to nranks = 1.
+   No reference counterpart (the reference is a single-process library). */
+int sdmk_set_shard(sdmk_context* ctx, int rank, int nranks);
+
 /* ---- instrumentation ----
    the context's CUDA stream (cudaStream_t) so callers can time on it */
 int sdmk_get_stream(sdmk_context* ctx, void** stream);
@@ -160,6 +170,12 @@ int sdmk_host_symbol_table(const sdmk_plan* plan, double h, int s2max, int kind,
 int64_t sdmk_host_topology_dump(int dim, int periodic, int n_s, int p, int64_t n_src,
                                 const int32_t* q_src, int64_t n_tgt, const int32_t* q_tgt, char* buf,
                                 int64_t cap);
+
+/* the shard plan sdmk_set_shard applies, from the same host topology:
+   out[0..4] = owned Morton target range [t0, t1), owned target leaves,
+   boxes whose incoming expansions the rank forms, target leaves in total */
+int sdmk_host_shard_plan(int dim, int periodic, int n_s, int p, int64_t n_src, const int32_t* q_src,
+                         int64_t n_tgt, const int32_t* q_tgt, int rank, int nranks, int64_t* out);
 
 #ifdef __cplusplus
 }

@@ -107,6 +107,9 @@ def lib():
                                        C.c_int),
             "sdmk_host_topology_dump": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, ip, C.c_int64, ip,
                                          C.c_char_p, C.c_int64], C.c_int64),
+            "sdmk_set_shard": ([C.c_void_p, C.c_int, C.c_int], C.c_int),
+            "sdmk_host_shard_plan": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, ip, C.c_int64, ip, C.c_int,
+                                      C.c_int, P(C.c_int64)], C.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -324,6 +327,10 @@ class Context:
         _raise(lib().sdmk_residual_pass(self._h, _dptr(out)))
         return out
 
+    def set_shard(self, rank: int, nranks: int):
+        """Own a contiguous Morton run of target leaves (see include/sdmk.h)."""
+        _raise(lib().sdmk_set_shard(self._h, int(rank), int(nranks)))
+
     def stream_handle(self) -> int:
         """cudaStream_t of this context (for CUDA-event timing by the caller)."""
         s = C.c_void_p()
@@ -388,3 +395,18 @@ def host_topology_dump(dim, periodic, n_s, p, q_src_sorted, q_tgt_sorted=None) -
     buf = C.create_string_buffer(int(n))
     lib().sdmk_host_topology_dump(dim, int(periodic), n_s, p, ns, _iptr(qs), nt, _iptr(qt), buf, n)
     return buf.raw[:n].decode()
+
+
+def host_shard_plan(dim, periodic, n_s, p, q_src_sorted, rank, nranks, q_tgt_sorted=None) -> dict:
+    """The shard plan sdmk_set_shard applies (host topology, no GPU)."""
+    qs = np.ascontiguousarray(np.asarray(q_src_sorted, np.int32).T.ravel())
+    ns = np.asarray(q_src_sorted).shape[0]
+    if q_tgt_sorted is not None and np.asarray(q_tgt_sorted).size:
+        qt = np.ascontiguousarray(np.asarray(q_tgt_sorted, np.int32).T.ravel())
+        nt = np.asarray(q_tgt_sorted).shape[0]
+    else:
+        qt, nt = None, 0
+    out = (C.c_int64 * 5)()
+    _raise(lib().sdmk_host_shard_plan(dim, int(periodic), n_s, p, ns, _iptr(qs), nt, _iptr(qt), int(rank),
+                                      int(nranks), out))
+    return {"t0": out[0], "t1": out[1], "owned_leaves": out[2], "needed_boxes": out[3], "target_leaves": out[4]}

@@ -251,6 +251,10 @@ int sdmk_residual_pass(sdmk_context* c, double* out) {
   return guarded([&] { need_ctx(c)->residual(out); });
 }
 
+int sdmk_set_shard(sdmk_context* c, int rank, int nranks) {
+  return guarded([&] { need_ctx(c)->set_shard(rank, nranks); });
+}
+
 int sdmk_get_stream(sdmk_context* c, void** stream) {
   return guarded([&] { *stream = (void*)need_ctx(c)->stream(); });
 }
@@ -285,6 +289,23 @@ int64_t sdmk_host_topology_dump(int dim, int periodic, int n_s, int p, int64_t n
     if (buf && cap > 0) std::memcpy(buf, s.data(), (size_t)std::min<int64_t>(cap, len));
   });
   return len;
+}
+
+int sdmk_host_shard_plan(int dim, int periodic, int n_s, int p, int64_t ns, const int32_t* qs, int64_t nt,
+                         const int32_t* qt, int rank, int nranks, int64_t* out) {
+  return guarded([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("shard plan: need 0 <= rank < nranks");
+    HostTree t = build_topology(dim, periodic != 0, n_s, p, (int)ns, qs, (int)nt, qt);
+    ShardPlan sp = shard_plan(t, rank, nranks);
+    int64_t need = 0, tl = 0;
+    for (char x : sp.need) need += x;
+    for (int b = 0; b < t.num_boxes(); ++b) tl += t.boxes[b].leaf && t.ntgt(b) > 0;
+    out[0] = sp.t0;
+    out[1] = sp.t1;
+    out[2] = (int64_t)sp.leaves.size();
+    out[3] = need;
+    out[4] = tl;
+  });
 }
 
 }  // extern "C"

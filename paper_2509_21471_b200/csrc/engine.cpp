@@ -162,6 +162,13 @@ Context::~Context() {
 
 void Context::sync() { cuda_check(cudaStreamSynchronize(st_), "stream synchronize"); }
 
+void Context::set_shard(int rank, int nranks) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("set_shard: need 0 <= rank < nranks");
+  rank_ = rank;
+  nranks_ = nranks;
+  prob_.ready = false;  // lists depend on the shard
+}
+
 double Context::ev_ms(int a, int b) {
   float ms = 0.0f;
   cudaEventElapsedTime(&ms, ev_[a], ev_[b]);
@@ -494,11 +501,17 @@ void Context::upload_tree_lists(const int32_t* qs) {
     o.side = t.side(b);
     o.half = 0.5 * o.side;
   }
-  std::vector<int> ant, itp;
-  for (int b = 0; b < nb; ++b) {
+  std::vector<int> ant;
+  for (int b = 0; b < nb; ++b)
     if (t.boxes[b].leaf && t.nsrc(b) > 0) ant.push_back(b);
-    if (t.boxes[b].leaf && t.ntgt(b) > 0) itp.push_back(b);
-  }
+  // target ownership (one rank owns everything unless set_shard was called):
+  // the upward pass stays replicated, the downward, far-field and residual
+  // work is restricted to the owned target leaves and their ancestors
+  ShardPlan sp = shard_plan(t, rank_, nranks_);
+  const std::vector<int>& itp = sp.leaves;
+  const std::vector<char>& need = sp.need;
+  pr.t_own0 = sp.t0;
+  pr.t_own1 = sp.t1;
   // near ranges per target leaf (dmk.cpp:966-990); two-pass CSR, parallel over leaves
   auto scode = [](const int8_t* s) { return (s[0] + 1) + 3 * (s[1] + 1) + 9 * (s[2] + 1); };
   auto ranges = [&](int b, int* obox, int* oinfo) {
@@ -559,7 +572,7 @@ void Context::upload_tree_lists(const int32_t* qs) {
       if (!x.leaf && t.ntgt(b) > 0)  // downward interpolation (dmk.cpp:840-853)
         for (int ci = 0; ci < nchild; ++ci) {
           int c = x.first_child + ci;
-          if (t.ntgt(c) == 0) continue;
+          if (t.ntgt(c) == 0 || !need[c]) continue;
           V.i_in.push_back(b);
           V.i_out.push_back(c);
           V.i_ci.push_back(ci);
@@ -574,7 +587,7 @@ void Context::upload_tree_lists(const int32_t* qs) {
     const std::vector<int>& ids = t.level_boxes[lev];
     const int nl = (int)ids.size();
     auto entries = [&](int b, int* oslot, int* otau) {
-      if (t.ntgt(b) == 0) return 0;
+      if (t.ntgt(b) == 0 || !need[b]) return 0;
       int cnt = 0;
       for (const Nbr& ce : t.col[b]) {
         if (t.boxes[b].leaf && ce.box == b && !ce.shift[0] && !ce.shift[1] && !ce.shift[2]) continue;
@@ -964,6 +977,14 @@ void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, in
   cudaEventRecord(ev_[4], st_);
   double* ufar = arena_.as<double>("ufar", (size_t)ntt * dim);
   double* ures = arena_.as<double>("ures", (size_t)ntt * dim);
+  unsigned char* own = nullptr;
+  if (nranks_ > 1) {  // only the owned targets are written by the passes below
+    cuda_check(cudaMemsetAsync(ufar, 0, sizeof(double) * ntt * dim, st_), "memset ufar");
+    cuda_check(cudaMemsetAsync(ures, 0, sizeof(double) * ntt * dim, st_), "memset ures");
+    own = arena_.as<unsigned char>("own", (size_t)ntt);
+    launch_own_mask(ntt, prob_.tperm, prob_.t_own0, prob_.t_own1, own, st_);
+    ++launches_;
+  }
   run_downward();
   run_target_far(ufar);
   cudaEventRecord(ev_[5], st_);
@@ -987,7 +1008,7 @@ void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, in
     launches_ += 2;
   }
   double* du = device_ptrs ? u : arena_.as<double>("u", (size_t)ntt * dim);
-  launch_combine(ntt, dim, ufar, ures, corr, corr_scale, zm, pr.tpts_caller, du, st_);
+  launch_combine(ntt, dim, ufar, ures, corr, corr_scale, zm, pr.tpts_caller, own, du, st_);
   ++launches_;
   cudaEventRecord(ev_[6], st_);
   if (!device_ptrs)

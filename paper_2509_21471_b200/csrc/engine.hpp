@@ -76,6 +76,7 @@ struct Problem {
   int *ant_leaves = nullptr, *int_leaves = nullptr;
   int n_ant = 0, n_int = 0;
   int *rng_start = nullptr, *rng_box = nullptr, *rng_info = nullptr, *subrange = nullptr;
+  int64_t t_own0 = 0, t_own1 = 0;  // owned range of Morton-sorted targets (set_shard)
   struct LevelLists {
     int n_merge = 0, n_interp = 0, n_src = 0, n_tgt = 0;
     int *merge_out = nullptr, *merge_in = nullptr, *merge_ci = nullptr;
@@ -97,6 +98,10 @@ class Context {
 
   void load_tables(const std::string& path);
   const Tables& tables_for(const Plan& plan);
+  // Target sharding for multi-GPU runs (one process per GPU): rank owns a
+  // contiguous Morton run of target leaves; outputs of other ranks' targets
+  // are written as zeros, so a sum over ranks assembles the full result.
+  void set_shard(int rank, int nranks);
 
   // Host-pointer evaluation; u may be host memory.  report may be null.
   void evaluate(const Plan& plan, int dim, int64_t ns, const double* src, int64_t nt, const double* tgt,
@@ -139,6 +144,7 @@ class Context {
   int *root_dev_ids_ = nullptr, *root_dev_es_ = nullptr, *root_dev_slot_ = nullptr, *root_dev_tau_ = nullptr;
   const double *cheb_nodes_ = nullptr, *cheb_wts_ = nullptr, *mats_up_ = nullptr, *mats_down_ = nullptr;
   double t_pw_ms_ = 0.0;
+  int rank_ = 0, nranks_ = 1;
   unsigned long long stats_[3] = {0, 0, 0};
 };
 

@@ -1,5 +1,6 @@
 #include "tree.hpp"
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -448,6 +449,36 @@ std::string dump_topology(const HostTree& t) {  // tree.cpp:325-354
     os << '\n';
   }
   return os.str();
+}
+
+ShardPlan shard_plan(const HostTree& t, int rank, int nranks) {
+  ShardPlan sp;
+  const int nb = t.num_boxes();
+  std::vector<int> tl;
+  for (int b = 0; b < nb; ++b)
+    if (t.boxes[b].leaf && t.ntgt(b) > 0) tl.push_back(b);
+  std::sort(tl.begin(), tl.end(), [&](int a, int b) { return t.boxes[a].tb < t.boxes[b].tb; });
+  int64_t total = 0;
+  for (int b : tl) total += t.ntgt(b);
+  sp.need.assign(nb, 0);
+  if (nranks < 1) nranks = 1;
+  int64_t start = 0;
+  sp.t0 = -1;
+  for (int b : tl) {
+    const int64_t n = t.ntgt(b);
+    const int owner = nranks == 1 ? 0 : (int)std::min<int64_t>(nranks - 1, ((2 * start + n) * nranks) / (2 * total));
+    if (owner == rank) {
+      if (sp.t0 < 0) sp.t0 = t.boxes[b].tb;
+      sp.t1 = t.boxes[b].te;
+      sp.leaves.push_back(b);
+    }
+    start += n;
+  }
+  if (sp.t0 < 0) sp.t0 = sp.t1 = 0;
+  std::sort(sp.leaves.begin(), sp.leaves.end());
+  for (int b : sp.leaves)
+    for (int x = b; x >= 0 && !sp.need[x]; x = t.boxes[x].parent) sp.need[x] = 1;
+  return sp;
 }
 
 }  // namespace sdmkb

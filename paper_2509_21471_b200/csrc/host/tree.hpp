@@ -80,4 +80,18 @@ std::string dump_topology(const HostTree& t);
 // range).  Used by the residual kernel for sub-cell culling.
 void leaf_subranges(const HostTree& t, int ns, const int32_t* qs, std::vector<int>& out);
 
+// Target-leaf ownership of rank `rank` of `nranks`: the
+// target leaves in Morton order (by the start of their target range) are cut
+// into contiguous runs of about total / nranks targets (a leaf goes to the
+// rank whose share contains its midpoint).  `need` marks the owned leaves
+// and their ancestors -- the boxes whose incoming expansions the rank forms;
+// [t0, t1) is the owned range of Morton-sorted targets.  nranks == 1 owns
+// everything.
+struct ShardPlan {
+  int64_t t0 = 0, t1 = 0;
+  std::vector<int> leaves;  // owned target leaves, by id
+  std::vector<char> need;   // per box
+};
+ShardPlan shard_plan(const HostTree& t, int rank, int nranks);
+
 }  // namespace sdmkb

@@ -61,15 +61,23 @@ __global__ void k_final(const double* part, int nblk, int ncomp, double* out) {
 
 __global__ void k_combine(int nt, int dim, const double* __restrict__ ufar, const double* __restrict__ ures,
                           const double* __restrict__ corr, double cs, const double* __restrict__ zm,
-                          const double* __restrict__ tp, double* __restrict__ u) {
+                          const double* __restrict__ tp, const unsigned char* __restrict__ own,
+                          double* __restrict__ u) {
   int64_t n = (int64_t)nt * dim;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int j = (int)(i % dim);
     double v = ufar[i] + ures[i];
     if (corr) v += cs * corr[j];
     if (zm) v += zm[1 + j] - zm[0] * tp[i];
+    if (own && !own[i / dim]) v = 0.0;  // another rank's target
     u[i] = v;
   }
+}
+
+__global__ void k_own_mask(int nt, const int* __restrict__ tperm, int64_t t0, int64_t t1,
+                           unsigned char* __restrict__ own) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nt; s += (int64_t)gridDim.x * blockDim.x)
+    own[tperm[s]] = (s >= t0 && s < t1) ? 1 : 0;
 }
 
 }  // namespace
@@ -86,11 +94,18 @@ void launch_zero_mode_moments(const double* spts, const double* sstr, int n, int
 }
 
 void launch_combine(int nt, int dim, const double* ufar, const double* ures, const double* corr, double cs,
-                    const double* zm, const double* tpts_caller, double* u, cudaStream_t st) {
+                    const double* zm, const double* tpts_caller, const unsigned char* own, double* u,
+                    cudaStream_t st) {
   int64_t n = (int64_t)nt * dim;
   int64_t g = (n + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
-  k_combine<<<(int)(g < 1 ? 1 : g), 256, 0, st>>>(nt, dim, ufar, ures, corr, cs, zm, tpts_caller, u);
+  k_combine<<<(int)(g < 1 ? 1 : g), 256, 0, st>>>(nt, dim, ufar, ures, corr, cs, zm, tpts_caller, own, u);
+}
+
+void launch_own_mask(int nt, const int* tperm, int64_t t0, int64_t t1, unsigned char* own, cudaStream_t st) {
+  int64_t g = ((int64_t)nt + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  k_own_mask<<<(int)(g < 1 ? 1 : g), 256, 0, st>>>(nt, tperm, t0, t1, own);
 }
 
 }  // namespace sdmkb

@@ -157,9 +157,11 @@ void launch_column_sums(const double* soa, int n, int ncomp, double* sums, doubl
 void launch_zero_mode_moments(const double* spts, const double* sstr, int n, int dim,
                               double* out, double* scratch, cudaStream_t st);
 // u = ((ufar + ures) + corr_scale * sums[j]) (+ (mom[j] - W x_t[j])) in caller order
-void launch_combine(int nt, int dim, const double* ufar, const double* ures, const double* sums,
-                    double corr_scale, const double* zm, const double* tpts_caller, double* u,
+void launch_combine(int nt, int dim, const double* ufar, const double* ures, const double* sums, double corr_scale,
+                    const double* zm, const double* tpts_caller, const unsigned char* own, double* u,
                     cudaStream_t st);
+// own[tperm[s]] = (t0 <= s < t1): the caller-order mask of a shard's targets
+void launch_own_mask(int nt, const int* tperm, int64_t t0, int64_t t1, unsigned char* own, cudaStream_t st);
 
 // ---- peak.cu ----------------------------------------------------------------
 double measure_fp64_peak_tflops(cudaStream_t st);

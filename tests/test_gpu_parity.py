@@ -242,3 +242,36 @@ def test_metric_size_properties(gpu_ctx, kernel):
     ex = ex.cpu().numpy()
     got = u1.reshape(-1, 3)[idx]
     assert np.linalg.norm(got - ex) / np.linalg.norm(ex) <= 5e-6
+
+
+SHARD_CASES = [
+    # kernel, dim, n, eps, periodic, dist, ntgt, nranks
+    (0, 3, 60000, 1e-6, False, "mixture", 0, 2),
+    (0, 3, 40000, 1e-6, False, "uniform", 25000, 3),
+    (1, 3, 30000, 1e-6, True, "uniform", 0, 2),
+    (0, 2, 40000, 1e-9, False, "mixture", 0, 4),
+]
+
+
+@pytest.mark.parametrize("case", SHARD_CASES)
+def test_shards_sum_to_single(case):
+    """Target-leaf sharding (include/sdmk.h sdmk_set_shard): each rank writes its
+    own targets and zeros elsewhere, so the element-wise sum over ranks (what
+    distributed.evaluate_sharded's all-reduce forms) equals the single-GPU
+    result bitwise."""
+    kernel, dim, n, eps, per, dist, ntgt, nranks = case
+    x, s, t = _make(kernel, dim, n, 31, dist, ntgt)
+    plan = g.select_parameters(kernel, eps, 0, dim)
+    sysm = g.ParticleSystem(dim, x, t if ntgt else np.zeros(0), s)
+    ctx = g.Context(0)
+    full = ctx.evaluate_with_plan(plan, sysm, int(per))
+    acc = np.zeros_like(full)
+    owned = np.zeros(full.size // dim, dtype=int)
+    for r in range(nranks):
+        ctx.set_shard(r, nranks)
+        u = ctx.evaluate_with_plan(plan, sysm, int(per))
+        nz = np.any(u.reshape(-1, dim) != 0.0, axis=1)
+        owned += nz
+        acc += u
+    assert np.array_equal(acc, full)
+    assert owned.max() <= 1  # no target written by two ranks
