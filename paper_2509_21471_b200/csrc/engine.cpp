@@ -586,8 +586,11 @@ void Context::upload_tree_lists(const int32_t* qs) {
     const int64_t side_int = int64_t(1) << (30 - lev);
     const std::vector<int>& ids = t.level_boxes[lev];
     const int nl = (int)ids.size();
+    // a plane-wave target is kept with all its siblings (need of the parent), so
+    // the sibling groups -- and every target's sums -- match the unsharded run
     auto entries = [&](int b, int* oslot, int* otau) {
-      if (t.ntgt(b) == 0 || !need[b]) return 0;
+      const int par = t.boxes[b].parent;
+      if (t.ntgt(b) == 0 || !need[par >= 0 ? par : b]) return 0;
       int cnt = 0;
       for (const Nbr& ce : t.col[b]) {
         if (t.boxes[b].leaf && ce.box == b && !ce.shift[0] && !ce.shift[1] && !ce.shift[2]) continue;
