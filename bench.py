@@ -18,9 +18,14 @@ unit vector) reported beside it.  Seeded synthetic data (no dataset exists).
 --impl reference times the reference's own CPU implementation (oracle/_ref)
 on a bounded sample per step (rank 0 only).
 
-Multi-GPU (torchrun): every rank evaluates its own independent N-point system
-(weak scaling); the timed region is bracketed by barriers and the max over
-ranks is reported.
+Multi-GPU (torchrun): the SAME N-point system is sharded by target leaves
+(include/sdmk.h sdmk_set_shard, paper_2509_21471_b200/distributed.py): every
+rank builds the tree and the upward pass, forms the downward pass, far fields
+and residual for its own Morton run of target leaves, and one NCCL
+all_reduce assembles u (strong scaling; the sum is bitwise the 1-GPU
+result).  The timed region (CUDA events on the torch stream, the library
+call blocking in between) includes the all-reduce; barriers on both sides and
+the max over ranks.
 """
 from __future__ import annotations
 
@@ -143,7 +148,9 @@ def run_ours(args, rank, world, local_rank):
         if kname not in args.kernels:
             continue
         plan = g.select_parameters(kernel, args.eps, g.PROLATE, 3)
-        x, s = make_system(kernel, n, args.seed + 1000 * rank + kernel)
+        x, s = make_system(kernel, n, args.seed + kernel)  # the same system on every rank
+        if world > 1:
+            ctx.set_shard(rank, world)
         d_x = torch.from_numpy(x).cuda()
         d_s = torch.from_numpy(s).cuda()
         d_u = torch.empty(n * 3, dtype=torch.float64, device="cuda")
@@ -151,6 +158,10 @@ def run_ours(args, rank, world, local_rank):
 
         def step_dev():
             ctx.evaluate_device(plan, 3, n, d_x.data_ptr(), 0, 0, d_s.data_ptr(), g.FREE_SPACE, d_u.data_ptr(), rep)
+            if dist is not None:  # assemble the shards (evaluate_device returns after its stream drained)
+                dist.all_reduce(d_u, op=dist.ReduceOp.SUM)
+
+        tstream = stream if dist is None else torch.cuda.current_stream()
 
         for _ in range(args.warmup):
             step_dev()
@@ -159,12 +170,12 @@ def run_ours(args, rank, world, local_rank):
         e1 = torch.cuda.Event(enable_timing=True)
         sampler = ClockSampler(local_rank)
         with sampler:
-            e0.record(stream)
+            e0.record(tstream)
             reps = []
             for _ in range(args.steps):
                 step_dev()
                 reps.append(dict(rep))
-            e1.record(stream)
+            e1.record(tstream)
             e1.synchronize()
         barrier()
         ms = e0.elapsed_time(e1) / args.steps
@@ -181,6 +192,13 @@ def run_ours(args, rank, world, local_rank):
         lib = g.lib()
 
         def step_host():
+            if dist is not None:  # host in, H2D, sharded evaluate, all-reduce, D2H
+                d_x.copy_(h_x, non_blocking=True)
+                d_s.copy_(h_s, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                step_dev()
+                h_u.copy_(d_u)
+                return None
             r = g.sdmk_report()
             code = lib.sdmk_evaluate_with_plan(ctx._h, C.byref(cplan), 3, n, g._dptr(sys_.sources), 0, g._dptr(None),
                                                g._dptr(sys_.strengths), 0, g._dptr(h_u.numpy()), C.byref(r))
@@ -190,10 +208,10 @@ def run_ours(args, rank, world, local_rank):
         for _ in range(max(1, args.warmup // 2)):
             step_host()
         barrier()
-        e0.record(stream)
+        e0.record(tstream)
         for _ in range(args.steps):
             step_host()
-        e1.record(stream)
+        e1.record(tstream)
         e1.synchronize()
         barrier()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
@@ -206,6 +224,8 @@ def run_ours(args, rank, world, local_rank):
         log(f"[bench] {kname}: {ms:.2f} ms/step device, {e2e_ms:.2f} ms/step e2e; report {r0}")
         del d_x, d_s, d_u
         torch.cuda.empty_cache()
+        if world > 1:
+            ctx.set_shard(0, 1)
 
     # roofline of the dominant kernel (FP64): measured DFMA peak on this GPU
     peak = ctx.fp64_peak_tflops()
@@ -256,7 +276,8 @@ def main():
     config = {"workload": f"metric: 3D free-space DMK, N={args.n:.0e} iid uniform in [-1/2,1/2]^3, eps={args.eps:g}, "
                           "prolate window, targets = sources",
               "kernels": args.kernels, "n_points": args.n, "eps": args.eps, "seed": args.seed,
-              "parallelism": f"replica x{world}" if world > 1 else "single GPU",
+              "parallelism": (f"target-leaf shards x{world} (replicated tree + upward pass, NCCL all-reduce of u)"
+                              if world > 1 else "single GPU"),
               "l2": "inputs (>=480 MB) and proxy grids (>10 GB) exceed the 126 MB L2; no flush needed"}
 
     if args.impl == "reference":
@@ -275,7 +296,7 @@ def main():
         ms = float(np.mean([t for _, t in vals])) * 1e3
         line = {"metric": "points/sec (3D Stokeslet DMK, eps=1e-6)", "value": v, "unit": "points/s",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded uniform points, N(0,1) forces)", "config": config, "impl": "reference",
                 "cpu_baseline": {"value": v, "unit": "points/s", "cores": threads, "kind": "reference",
                                  "sample": f"evaluate_with_plan on N={args.cpu_sample} points of the same "
@@ -289,8 +310,8 @@ def main():
         return
     R = results.get("stokeslet") or next(iter(results.values()))
     n = args.n
-    value = n * world / (R["ms"] * 1e-3)
-    e2e = n * world / (R["e2e_ms"] * 1e-3)
+    value = n / (R["ms"] * 1e-3)  # one N-point system per step, all ranks together
+    e2e = n / (R["e2e_ms"] * 1e-3)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
@@ -303,15 +324,15 @@ def main():
                    "sample": f"unavailable: {e}"}
     extra = {}
     for k, r in results.items():
-        extra[k] = {"points_per_s": n * world / (r["ms"] * 1e-3), "ms_per_step": r["ms"],
-                    "e2e_points_per_s": n * world / (r["e2e_ms"] * 1e-3), "e2e_ms": r["e2e_ms"],
+        extra[k] = {"points_per_s": n / (r["ms"] * 1e-3), "ms_per_step": r["ms"],
+                    "e2e_points_per_s": n / (r["e2e_ms"] * 1e-3), "e2e_ms": r["e2e_ms"],
                     "p": r["plan"]["p"], "N1": r["plan"]["N1"], "num_boxes": r["rep"]["num_boxes"],
                     "max_level": r["rep"]["max_level"],
                     "pass_s": {k2: r["rep"][k2] for k2 in ("t_tree", "t_upward", "t_root", "t_downward",
                                                            "t_residual", "t_residual_kernel", "t_planewave")}}
     line = {"metric": "points/sec (3D Stokeslet DMK, N=1e7, eps=1e-6)", "value": value, "unit": "points/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": R["ms"],
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded uniform points, N(0,1) forces; stresslet normals random unit)",
             "config": config, "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "points/s", "h2d_bytes_per_step": n * 6 * 8, "d2h_bytes_per_step": n * 3 * 8},
