@@ -637,10 +637,20 @@ void Context::upload_tree_lists(const int32_t* qs) {
   if (bad_tau) throw RuntimeError("colleague offset outside {-1,0,1}");
   // root lists: box 0 with one zero-offset entry
   std::vector<int> root_ids = {0}, root_es = {0, 1}, root_slot = {0}, root_tau = {13};
+  // residual work items: 32-target chunks of each target leaf, in leaf order
+  std::vector<int> chunks;
+  for (int i = 0; i < nitp; ++i) {
+    const Box& x = t.boxes[itp[i]];
+    for (int t0 = x.tb; t0 < x.te; t0 += 32) {
+      chunks.push_back(i);
+      chunks.push_back(t0);
+    }
+  }
   Packer pk;
   std::vector<int> subr;
   leaf_subranges(t, pr.ns, qs, subr);  // source sub-cells for the residual cull
   size_t o_sub = pk.add(subr);
+  size_t o_chunks = pk.add(chunks);
   size_t o_boxes = pk.add(boxes), o_ant = pk.add(ant), o_itp = pk.add(itp), o_rs = pk.add(rs), o_rbox = pk.add(rbox),
          o_rinfo = pk.add(rinfo), o_rid = pk.add(root_ids), o_res = pk.add(root_es), o_rsl = pk.add(root_slot),
          o_rta = pk.add(root_tau);
@@ -668,6 +678,8 @@ void Context::upload_tree_lists(const int32_t* qs) {
   pr.rng_box = (int*)(dv + o_rbox);
   pr.rng_info = (int*)(dv + o_rinfo);
   pr.subrange = (int*)(dv + o_sub);
+  pr.res_chunks = (int*)(dv + o_chunks);
+  pr.n_chunks = (int)(chunks.size() / 2);
   pr.levels.assign(L, {});
   for (int lev = 0; lev < L; ++lev) {
     Problem::LevelLists& X = pr.levels[lev];
@@ -942,7 +954,7 @@ void Context::run_residual(double* ures, bool stats) {  // dmk.cpp:919-1032
   unsigned long long* st = arena_.as<unsigned long long>("stats", 4);
   if (stats) cuda_check(cudaMemsetAsync(st, 0, 4 * sizeof(unsigned long long), st_), "memset");
   cudaEventRecord(ev_[13], st_);
-  launch_residual(rt, pr.boxes, pr.int_leaves, pr.n_int, pr.rng_start, pr.rng_box, pr.rng_info, pr.subrange, pr.spts, pr.ns,
+  launch_residual(rt, pr.boxes, pr.int_leaves, pr.n_int, pr.res_chunks, pr.n_chunks, pr.rng_start, pr.rng_box, pr.rng_info, pr.subrange, pr.spts, pr.ns,
                   pr.sstr, pr.tpts, pr.nt, pr.tperm, pr.alias ? 1 : 0, 0.0, T.self_const, ures, flags + 3,
                   stats ? st : nullptr, st_);
   cudaEventRecord(ev_[12], st_);

@@ -77,6 +77,8 @@ struct Problem {
   int n_ant = 0, n_int = 0;
   int *rng_start = nullptr, *rng_box = nullptr, *rng_info = nullptr, *subrange = nullptr;
   int64_t t_own0 = 0, t_own1 = 0;  // owned range of Morton-sorted targets (set_shard)
+  int* res_chunks = nullptr;       // (leaf index, first target) per 32-target residual chunk
+  int n_chunks = 0;
   struct LevelLists {
     int n_merge = 0, n_interp = 0, n_src = 0, n_tgt = 0;
     int *merge_out = nullptr, *merge_in = nullptr, *merge_ci = nullptr;

@@ -29,18 +29,34 @@ using dev::DBox;
 
 constexpr int kRBlock = 256;
 constexpr int kWarps = kRBlock / 32;
-constexpr int kList = 24;        // per-lane list capacity (entries)
+constexpr int kList = 48;        // per-lane list capacity (entries): longer lists, less lockstep padding
 constexpr int kMaxRanges = 160;
 constexpr int kMaxPW = 384;      // ni * (deg + 1) <= 384 (d, o) coefficient pairs
 constexpr int kCopies = 8;       // table copies, one per 16-byte bank group
+
+template <bool B>
+struct BoolC {
+  static constexpr bool value = B;
+};
+
+// 1/sqrt(x) from the single-precision estimate and two Newton steps (~1 ulp;
+// the CUDA double rsqrt spends ~20 instructions on range handling).  x here
+// is a squared distance in (0, 3); tiny x falls back to rsqrt.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  if (x < 1e-30) return rsqrt(x);
+  double y = (double)rsqrtf(__double2float_rn(x));
+  double r = fma(-x * y, y, 1.0);
+  y = fma(0.5 * y, r, y);
+  r = fma(-x * y, y, 1.0);
+  return fma(0.5 * y, r, y);
+}
 
 struct RangeS {
   double sh[3];
   double lo[3], hi[3];
   double nu, inu, sup2, cull, half;
   int sb, se, self, zero_shift;
-  int code;    // image shift code (x + 3 y + 9 z over {-1,0,1}) | fine-scale flag << 5
-  int sub[9];  // Morton child sub-ranges of the source leaf (contiguous, in order)
+  int code;  // packed image shift (x+1 | y+1 << 2 | z+1 << 4) | fine-scale flag << 6
 };
 
 // Radial table values at s (unit scale) from the piecewise monomial form held
@@ -126,7 +142,7 @@ __device__ __forceinline__ void assemble(double fd, double fo, const double* x, 
 
 template <int KERNEL, int DIM, int DEG>
 __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox* __restrict__ boxes,
-                                                      const int* __restrict__ leaves,
+                                                      const int* __restrict__ leaves, const int2* __restrict__ chunks, int nchunks,
                                                       const int* __restrict__ rng_start,
                                                       const int* __restrict__ rng_box,
                                                       const int* __restrict__ rng_info,
@@ -137,7 +153,6 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
                                                       const int* __restrict__ tperm, int alias, double self_const,
                                                       double* __restrict__ ures, int* flags,
                                                       unsigned long long* stats) {
-  __shared__ RangeS rs[kMaxRanges];
   extern __shared__ __align__(16) double2 dyn2[];  // [npw][kCopies] table, then the lists
   double2* s_pw = dyn2;
   const int npw = rt.ni * (rt.deg + 1);
@@ -145,45 +160,22 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
   int (*lsrc)[kList][32] = reinterpret_cast<int (*)[kList][32]>(dyn);
   unsigned char (*lrng)[kList][32] = reinterpret_cast<unsigned char (*)[kList][32]>(dyn + kWarps * kList * 32);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int leaf = leaves[blockIdx.x];
+  for (int e = tid; e < npw * kCopies; e += blockDim.x) {
+    const int k = e / kCopies;
+    s_pw[e] = make_double2(KERNEL != 2 ? rt.pw_d[k] : 0.0, rt.pw_o[k]);
+  }
+  __syncthreads();
+  // one 32-target chunk of one leaf per warp (chunks never straddle leaves)
+  const int cid = blockIdx.x * kWarps + warp;
+  if (cid >= nchunks) return;
+  const int2 chunk = chunks[cid];
+  const int li = chunk.x;
+  const int leaf = leaves[li];
   const DBox box = boxes[leaf];
   const double r_l = box.side, r_f = 0.5 * r_l;
   const double inv_rl = 1.0 / r_l, inv_rf = 1.0 / r_f;
   const double yscale = rt.ni / (rt.hi - rt.lo);
-  const int r0 = rng_start[blockIdx.x], nr = rng_start[blockIdx.x + 1] - r0;
-  {
-    for (int e = tid; e < npw * kCopies; e += blockDim.x) {
-      const int k = e / kCopies;
-      s_pw[e] = make_double2(KERNEL != 2 ? rt.pw_d[k] : 0.0, rt.pw_o[k]);
-    }
-  }
-  for (int k = tid; k < nr; k += blockDim.x) {
-    const int sbx = rng_box[r0 + k], info = rng_info[r0 + k];
-    const DBox sb = boxes[sbx];
-    RangeS R;
-    const int code = info & 31;
-    const int sh[3] = {code % 3 - 1, (code / 3) % 3 - 1, code / 9 - 1};
-    R.nu = (info >> 5) & 1 ? r_f : r_l;
-    R.code = (sh[0] + 1) | ((sh[1] + 1) << 2) | ((DIM == 3 ? sh[2] + 1 : 1) << 4) | ((info & 32) << 1);
-    R.inu = 1.0 / R.nu;
-    R.self = (info >> 6) & 1;
-    const double sup = R.nu * rt.support;
-    R.sup2 = sup * sup;
-    R.cull = sup * (1.0 + 1e-12) + 1e-15;
-    R.zero_shift = 1;
-    for (int ax = 0; ax < 3; ++ax) {
-      R.sh[ax] = ax < DIM ? (double)sh[ax] : 0.0;
-      if (R.sh[ax] != 0.0) R.zero_shift = 0;
-      R.lo[ax] = sb.c[ax] - sb.half + R.sh[ax];
-      R.hi[ax] = sb.c[ax] + sb.half + R.sh[ax];
-    }
-    R.sb = sb.sb;
-    R.se = sb.se;
-    R.half = sb.half;
-    for (int c = 0; c < 9; ++c) R.sub[c] = subrange[(size_t)sbx * 9 + c];
-    rs[k] = R;
-  }
-  __syncthreads();
+  const int r0 = rng_start[li], nr = rng_start[li + 1] - r0;
   const double* __restrict__ spx = spts;
   const double* __restrict__ spy = spts + ns;
   const double* __restrict__ spz = spts + (size_t)(DIM == 3 ? 2 : 1) * ns;
@@ -191,7 +183,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
   if (alias && KERNEL == 0) selfc = DIM == 3 ? self_const / r_l : self_const + log(r_l) / (4.0 * dev::kPI);
   unsigned long long n_ref = 0, n_test = 0, n_in = 0;
   int singular = 0;
-  for (int t0 = box.tb + warp * 32; t0 < box.te; t0 += kRBlock) {
+  {
+    const int t0 = chunk.y;
     const int t = t0 + lane;
     const bool valid = t < box.te;
     const int tt = valid ? t : t0;
@@ -228,7 +221,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         if (DIM == 3) x[2] = xt[2] - (spz[a] + (double)(((code >> 4) & 3) - 1));
 #pragma unroll
         for (int ax = 0; ax < DIM; ++ax) r2 += x[ax] * x[ax];
-        const double rinv = rsqrt(r2);
+        const double rinv = rsqrt_nr(r2);
         const double s = (r2 * rinv) * inu;  // nu is a power of two: r * (1/nu) == r / nu
         double fd, fo;
         radial_tables<KERNEL, DEG>(rt, s_pw + (lane & (kCopies - 1)), yscale, s, fd, fo);
@@ -251,7 +244,31 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       cnt = 0;
     };
     for (int k = 0; k < nr; ++k) {
-      const RangeS& R = rs[k];
+      // the range's source leaf, image shift and scale (dmk.cpp:966-990), warp-uniform
+      const int sbx = rng_box[r0 + k], info = rng_info[r0 + k];
+      const DBox sbox = boxes[sbx];
+      RangeS R;
+      {
+        const int code = info & 31;
+        const int sh[3] = {code % 3 - 1, (code / 3) % 3 - 1, code / 9 - 1};
+        R.nu = (info >> 5) & 1 ? r_f : r_l;
+        R.code = (sh[0] + 1) | ((sh[1] + 1) << 2) | ((DIM == 3 ? sh[2] + 1 : 1) << 4) | ((info & 32) << 1);
+        R.self = (info >> 6) & 1;
+        const double sup = R.nu * rt.support;
+        R.sup2 = sup * sup;
+        R.cull = sup * (1.0 + 1e-12) + 1e-15;
+        R.zero_shift = code == 13;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+          R.sh[ax] = ax < DIM ? (double)sh[ax] : 0.0;
+          R.lo[ax] = sbox.c[ax] - sbox.half + R.sh[ax];
+          R.hi[ax] = sbox.c[ax] + sbox.half + R.sh[ax];
+        }
+        R.sb = sbox.sb;
+        R.se = sbox.se;
+        R.half = sbox.half;
+      }
+      const int* sub = subrange + (size_t)sbx * 9;
       const int len = R.se - R.sb;
       n_ref += valid ? len - ((alias && R.self) ? 1 : 0) : 0;
       double d2 = 0.0;  // distance from the warp's target box to the source box
@@ -266,7 +283,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       const bool skip_self = alias && R.self;
       constexpr int NC = 1 << DIM;
       for (int ci = 0; ci < NC; ++ci) {  // Morton child sub-cells of the source leaf
-        const int a0 = R.sub[ci], a1 = R.sub[ci + 1];
+        const int a0 = sub[ci], a1 = sub[ci + 1];
         if (a0 == a1) continue;
         double e2 = 0.0;
 #pragma unroll
@@ -277,48 +294,55 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         }
         if (e2 > cull2) continue;
         n_test += valid ? a1 - a0 : 0;
-        auto test = [&](int a, double sx, double sy, double sz) {
-          double x0, x1, x2 = 0.0;
-          if (zs) {  // xs + 0 == xs exactly
-            x0 = xt[0] - sx;
-            x1 = xt[1] - sy;
-            if (DIM == 3) x2 = xt[2] - sz;
-          } else {
-            x0 = xt[0] - (sx + R.sh[0]);
-            x1 = xt[1] - (sy + R.sh[1]);
-            if (DIM == 3) x2 = xt[2] - (sz + R.sh[2]);
+        // the zero-shift test (xs + 0 == xs) and the shifted one are separate
+        // loops, so the warp-uniform choice is made once per sub-cell
+        auto scan = [&](auto zsc) {
+          constexpr bool ZS = decltype(zsc)::value;
+          auto test = [&](int a, double sx, double sy, double sz) {
+            double x0, x1, x2 = 0.0;
+            if (ZS) {
+              x0 = xt[0] - sx;
+              x1 = xt[1] - sy;
+              if (DIM == 3) x2 = xt[2] - sz;
+            } else {
+              x0 = xt[0] - (sx + R.sh[0]);
+              x1 = xt[1] - (sy + R.sh[1]);
+              if (DIM == 3) x2 = xt[2] - (sz + R.sh[2]);
+            }
+            double r2 = x0 * x0 + x1 * x1;
+            if (DIM == 3) r2 += x2 * x2;
+            bool in = valid && r2 < sup2 && !(skip_self && a == t);
+            if (in && r2 == 0.0) {
+              singular = 1;
+              in = false;
+            }
+            if (in) {
+              lsrc[warp][cnt][lane] = a;
+              lrng[warp][cnt][lane] = (unsigned char)R.code;
+              ++cnt;
+              ++n_in;
+            }
+          };
+          int a = a0;
+          for (; a + 4 <= a1; a += 4) {  // 4 broadcast loads in flight before the tests
+            if (__any_sync(0xffffffffu, cnt > kList - 4)) flush();
+            double sx[4], sy[4], sz[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              sx[q] = spx[a + q];
+              sy[q] = spy[a + q];
+              if (DIM == 3) sz[q] = spz[a + q];
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) test(a + q, sx[q], sy[q], sz[q]);
           }
-          double r2 = x0 * x0 + x1 * x1;
-          if (DIM == 3) r2 += x2 * x2;
-          bool in = valid && r2 < sup2 && !(skip_self && a == t);
-          if (in && r2 == 0.0) {
-            singular = 1;
-            in = false;
-          }
-          if (in) {
-            lsrc[warp][cnt][lane] = a;
-            lrng[warp][cnt][lane] = (unsigned char)R.code;
-            ++cnt;
-            ++n_in;
+          for (; a < a1; ++a) {
+            if (__any_sync(0xffffffffu, cnt == kList)) flush();
+            test(a, spx[a], spy[a], DIM == 3 ? spz[a] : 0.0);
           }
         };
-        int a = a0;
-        for (; a + 4 <= a1; a += 4) {  // 4 broadcast loads in flight before the tests
-          if (__any_sync(0xffffffffu, cnt > kList - 4)) flush();
-          double sx[4], sy[4], sz[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            sx[q] = spx[a + q];
-            sy[q] = spy[a + q];
-            if (DIM == 3) sz[q] = spz[a + q];
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) test(a + q, sx[q], sy[q], sz[q]);
-        }
-        for (; a < a1; ++a) {
-          if (__any_sync(0xffffffffu, cnt == kList)) flush();
-          test(a, spx[a], spy[a], DIM == 3 ? spz[a] : 0.0);
-        }
+        if (zs) scan(BoolC<true>{});
+        else scan(BoolC<false>{});
       }
     }
     flush();
@@ -350,11 +374,14 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
 
 }  // namespace
 
-void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves, int nleaf, const int* rng_start,
+void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves, int nleaf, const int* chunks,
+                     int nchunks, const int* rng_start,
                      const int* rng_box, const int* rng_info, const int* subrange, const double* spts, int ns, const double* sstr,
                      const double* tpts, int nt, const int* tperm, int alias, double /*unused*/, double self_const,
                      double* ures, int* flags, unsigned long long* stats, cudaStream_t st) {
-  if (nleaf <= 0) return;
+  if (nleaf <= 0 || nchunks <= 0) return;
+  const int nblk = (nchunks + kWarps - 1) / kWarps;
+  const int2* ch2 = reinterpret_cast<const int2*>(chunks);
   const size_t dsm = (size_t)kWarps * kList * 32 * (sizeof(int) + 1) +
                      sizeof(double) * 2 * kCopies * (size_t)rt.ni * (rt.deg + 1);
 #define RES(K, D)                                                                                                \
@@ -367,7 +394,8 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
 #define RES1(K, D, G)                                                                                            \
   do {                                                                                                           \
     cudaFuncSetAttribute(k_residual<K, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);            \
-    k_residual<K, D, G><<<nleaf, kRBlock, dsm, st>>>(rt, boxes, leaves, rng_start, rng_box, rng_info, subrange,  \
+    k_residual<K, D, G><<<nblk, kRBlock, dsm, st>>>(rt, boxes, leaves, ch2, nchunks, rng_start, rng_box,         \
+                                                    rng_info, subrange,                                          \
                                                      spts, ns, sstr, tpts, nt, tperm, alias, self_const, ures,   \
                                                      flags, stats);                                              \
   } while (0)
