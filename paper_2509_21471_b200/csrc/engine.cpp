@@ -3,6 +3,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -157,6 +158,7 @@ Context::~Context() {
   cudaSetDevice(device_);
   if (st_) cudaStreamSynchronize(st_);
   for (auto& e : ev_) cudaEventDestroy(e);
+  for (auto& e : pw_ev_) cudaEventDestroy(e);
   if (st_) cudaStreamDestroy(st_);
 }
 
@@ -315,7 +317,7 @@ GridDev& Context::grid(GridDev& gd, const std::string& name, int dim, int p, int
 }
 
 // ------------------------------------------------------------ problem ----
-void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode) {
+void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bool defer_lists) {
   Problem& pr = prob_;
   pr.ready = false;
   pr.plan = P;
@@ -389,7 +391,10 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode) {
   pr.tree = build_topology(d, pr.periodic, P.n_s, P.p, ns, hq, pr.alias ? 0 : nt,
                            pr.alias ? nullptr : hq + (size_t)ns * d);
   const auto w2 = std::chrono::steady_clock::now();
-  upload_tree_lists(hq);
+  hq_ = hq;
+  pr.lists_b = false;
+  upload_tree_lists_a();
+  if (!defer_lists) upload_tree_lists_b(hq);
   const auto w3 = std::chrono::steady_clock::now();
   if (timing_on()) {
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
@@ -477,7 +482,11 @@ static void build_groups(const HostTree& t, int lev, const std::vector<int>& tbx
   }
 }
 
-void Context::upload_tree_lists(const int32_t* qs) {
+// Phase A: what the upward pass needs (box records, anterpolation leaves,
+// merge lists, Chebyshev matrices).  Phase B: everything the downward,
+// far-field and residual passes need; evaluate() builds it on the host while
+// the GPU runs the upward pass.
+void Context::upload_tree_lists_a() {
   Problem& pr = prob_;
   const HostTree& t = pr.tree;
   const int nb = t.num_boxes(), d = pr.dim, nchild = 1 << d;
@@ -504,6 +513,62 @@ void Context::upload_tree_lists(const int32_t* qs) {
   std::vector<int> ant;
   for (int b = 0; b < nb; ++b)
     if (t.boxes[b].leaf && t.nsrc(b) > 0) ant.push_back(b);
+  const int L = t.max_level + 1;
+  std::vector<std::vector<int>> m_out(L), m_in(L), m_ci(L);
+  for (int lev = 0; lev < L; ++lev)
+    for (int b : t.level_boxes[lev]) {
+      const Box& x = t.boxes[b];
+      if (!x.leaf && t.nsrc(b) > 0) {  // upward merge (dmk.cpp:638-651)
+        m_out[lev].push_back(b);
+        for (int ci = 0; ci < nchild; ++ci) {
+          int c = x.first_child + ci;
+          m_in[lev].push_back(t.nsrc(c) > 0 ? c : -1);
+          m_ci[lev].push_back(ci);
+        }
+      }
+    }
+  // Chebyshev nodes/weights and the child matrices (dmk.cpp:25-66, 626-629)
+  const int p = pr.plan.p;
+  Cheb1 cb(p);
+  std::vector<double> m0 = cb.child(0), m1 = cb.child(1), t0 = transpose(m0, p), t1 = transpose(m1, p);
+  std::vector<double> blob;
+  blob.insert(blob.end(), cb.x.begin(), cb.x.end());
+  blob.insert(blob.end(), cb.w.begin(), cb.w.end());
+  blob.insert(blob.end(), t0.begin(), t0.end());  // upward: transposed child matrices
+  blob.insert(blob.end(), t1.begin(), t1.end());
+  blob.insert(blob.end(), m0.begin(), m0.end());  // downward: child matrices
+  blob.insert(blob.end(), m1.begin(), m1.end());
+  Packer pk;
+  const size_t o_blob = pk.add(blob), o_boxes = pk.add(boxes), o_ant = pk.add(ant);
+  std::vector<std::array<size_t, 3>> off(L);
+  for (int lev = 0; lev < L; ++lev) off[lev] = {pk.add(m_out[lev]), pk.add(m_in[lev]), pk.add(m_ci[lev])};
+  char* h = (char*)pinned_.get("treeA", pk.total + 64);
+  for (auto& it : pk.items)
+    if (it.bytes) std::memcpy(h + it.off, it.src, it.bytes);
+  char* dv = (char*)arena_.get("treeA", pk.total + 64);
+  cuda_check(cudaMemcpyAsync(dv, h, pk.total, cudaMemcpyHostToDevice, st_), "tree upload");
+  const double* db = (const double*)(dv + o_blob);
+  cheb_nodes_ = db;
+  cheb_wts_ = db + p;
+  mats_up_ = db + 2 * p;
+  mats_down_ = db + 2 * p + 2 * p * p;
+  pr.boxes = (dev::DBox*)(dv + o_boxes);
+  pr.ant_leaves = (int*)(dv + o_ant);
+  pr.n_ant = (int)ant.size();
+  pr.levels.assign(L, {});
+  for (int lev = 0; lev < L; ++lev) {
+    Problem::LevelLists& X = pr.levels[lev];
+    X.n_merge = (int)m_out[lev].size();
+    X.merge_out = (int*)(dv + off[lev][0]);
+    X.merge_in = (int*)(dv + off[lev][1]);
+    X.merge_ci = (int*)(dv + off[lev][2]);
+  }
+}
+
+void Context::upload_tree_lists_b(const int32_t* qs) {
+  Problem& pr = prob_;
+  const HostTree& t = pr.tree;
+  const int nb = t.num_boxes(), d = pr.dim, nchild = 1 << d;
   // target ownership (one rank owns everything unless set_shard was called):
   // the upward pass stays replicated, the downward, far-field and residual
   // work is restricted to the owned target leaves and their ancestors
@@ -551,7 +616,7 @@ void Context::upload_tree_lists(const int32_t* qs) {
   // per-level lists
   const int L = t.max_level + 1;
   struct LV {
-    std::vector<int> m_out, m_in, m_ci, i_in, i_out, i_ci, sbx, tbx, es, eslot, etau, gstart, gslot, tmeta;
+    std::vector<int> i_in, i_out, i_ci, sbx, tbx, es, eslot, etau, gstart, gslot, tmeta;
   };
   std::vector<LV> lv(L);
   const bool use_groups = !std::getenv("SDMK_NO_GROUP");
@@ -561,14 +626,6 @@ void Context::upload_tree_lists(const int32_t* qs) {
     LV& V = lv[lev];
     for (int b : t.level_boxes[lev]) {
       const Box& x = t.boxes[b];
-      if (!x.leaf && t.nsrc(b) > 0) {  // upward merge (dmk.cpp:638-651)
-        V.m_out.push_back(b);
-        for (int ci = 0; ci < nchild; ++ci) {
-          int c = x.first_child + ci;
-          V.m_in.push_back(t.nsrc(c) > 0 ? c : -1);
-          V.m_ci.push_back(ci);
-        }
-      }
       if (!x.leaf && t.ntgt(b) > 0)  // downward interpolation (dmk.cpp:840-853)
         for (int ci = 0; ci < nchild; ++ci) {
           int c = x.first_child + ci;
@@ -651,28 +708,23 @@ void Context::upload_tree_lists(const int32_t* qs) {
   leaf_subranges(t, pr.ns, qs, subr);  // source sub-cells for the residual cull
   size_t o_sub = pk.add(subr);
   size_t o_chunks = pk.add(chunks);
-  size_t o_boxes = pk.add(boxes), o_ant = pk.add(ant), o_itp = pk.add(itp), o_rs = pk.add(rs), o_rbox = pk.add(rbox),
-         o_rinfo = pk.add(rinfo), o_rid = pk.add(root_ids), o_res = pk.add(root_es), o_rsl = pk.add(root_slot),
-         o_rta = pk.add(root_tau);
+  size_t o_itp = pk.add(itp), o_rs = pk.add(rs), o_rbox = pk.add(rbox), o_rinfo = pk.add(rinfo),
+         o_rid = pk.add(root_ids), o_res = pk.add(root_es), o_rsl = pk.add(root_slot), o_rta = pk.add(root_tau);
   struct Off {
-    size_t m_out, m_in, m_ci, i_in, i_out, i_ci, sbx, tbx, es, eslot, etau, gstart, gslot, tmeta;
+    size_t i_in, i_out, i_ci, sbx, tbx, es, eslot, etau, gstart, gslot, tmeta;
   };
   std::vector<Off> off(L);
   for (int lev = 0; lev < L; ++lev) {
     LV& V = lv[lev];
-    off[lev] = {pk.add(V.m_out), pk.add(V.m_in),  pk.add(V.m_ci),   pk.add(V.i_in),   pk.add(V.i_out),
-                pk.add(V.i_ci),  pk.add(V.sbx),   pk.add(V.tbx),    pk.add(V.es),     pk.add(V.eslot),
-                pk.add(V.etau),  pk.add(V.gstart), pk.add(V.gslot), pk.add(V.tmeta)};
+    off[lev] = {pk.add(V.i_in), pk.add(V.i_out), pk.add(V.i_ci),   pk.add(V.sbx),   pk.add(V.tbx),  pk.add(V.es),
+                pk.add(V.eslot), pk.add(V.etau), pk.add(V.gstart), pk.add(V.gslot), pk.add(V.tmeta)};
   }
-  char* h = (char*)pinned_.get("tree", pk.total + 64);
+  char* h = (char*)pinned_.get("treeB", pk.total + 64);
   for (auto& it : pk.items)
     if (it.bytes) std::memcpy(h + it.off, it.src, it.bytes);
-  char* dv = (char*)arena_.get("tree", pk.total + 64);
+  char* dv = (char*)arena_.get("treeB", pk.total + 64);
   cuda_check(cudaMemcpyAsync(dv, h, pk.total, cudaMemcpyHostToDevice, st_), "tree upload");
-  pr.boxes = (dev::DBox*)(dv + o_boxes);
-  pr.ant_leaves = (int*)(dv + o_ant);
   pr.int_leaves = (int*)(dv + o_itp);
-  pr.n_ant = (int)ant.size();
   pr.n_int = (int)itp.size();
   pr.rng_start = (int*)(dv + o_rs);
   pr.rng_box = (int*)(dv + o_rbox);
@@ -680,17 +732,12 @@ void Context::upload_tree_lists(const int32_t* qs) {
   pr.subrange = (int*)(dv + o_sub);
   pr.res_chunks = (int*)(dv + o_chunks);
   pr.n_chunks = (int)(chunks.size() / 2);
-  pr.levels.assign(L, {});
   for (int lev = 0; lev < L; ++lev) {
     Problem::LevelLists& X = pr.levels[lev];
     LV& V = lv[lev];
-    X.n_merge = (int)V.m_out.size();
     X.n_interp = (int)V.i_out.size();
     X.n_src = (int)V.sbx.size();
     X.n_tgt = (int)V.tbx.size();
-    X.merge_out = (int*)(dv + off[lev].m_out);
-    X.merge_in = (int*)(dv + off[lev].m_in);
-    X.merge_ci = (int*)(dv + off[lev].m_ci);
     X.interp_in = (int*)(dv + off[lev].i_in);
     X.interp_out = (int*)(dv + off[lev].i_out);
     X.interp_ci = (int*)(dv + off[lev].i_ci);
@@ -704,31 +751,11 @@ void Context::upload_tree_lists(const int32_t* qs) {
     X.grp_slot = (int*)(dv + off[lev].gslot);
     X.t_meta = (int*)(dv + off[lev].tmeta);
   }
-  // root lists live after the per-level ones in the same blob
   root_dev_ids_ = (int*)(dv + o_rid);
   root_dev_es_ = (int*)(dv + o_res);
   root_dev_slot_ = (int*)(dv + o_rsl);
   root_dev_tau_ = (int*)(dv + o_rta);
-  // Chebyshev nodes/weights and the child matrices (dmk.cpp:25-66, 626-629)
-  const int p = pr.plan.p;
-  Cheb1 cb(p);
-  std::vector<double> m0 = cb.child(0), m1 = cb.child(1), t0 = transpose(m0, p), t1 = transpose(m1, p);
-  std::vector<double> blob;
-  blob.insert(blob.end(), cb.x.begin(), cb.x.end());
-  blob.insert(blob.end(), cb.w.begin(), cb.w.end());
-  blob.insert(blob.end(), t0.begin(), t0.end());  // upward: transposed child matrices
-  blob.insert(blob.end(), t1.begin(), t1.end());
-  blob.insert(blob.end(), m0.begin(), m0.end());  // downward: child matrices
-  blob.insert(blob.end(), m1.begin(), m1.end());
-  double* hb = (double*)pinned_.get("cheb", blob.size() * sizeof(double));
-  std::memcpy(hb, blob.data(), blob.size() * sizeof(double));
-  double* db = arena_.as<double>("cheb", blob.size());
-  cuda_check(cudaMemcpyAsync(db, hb, blob.size() * sizeof(double), cudaMemcpyHostToDevice, st_), "cheb upload");
-  cheb_nodes_ = db;
-  cheb_wts_ = db + p;
-  mats_up_ = db + 2 * p;
-  mats_down_ = db + 2 * p + 2 * p * p;
-  sync();  // pinned staging buffers are reused by the next call
+  pr.lists_b = true;
 }
 
 // ---------------------------------------------------------------- passes --
@@ -788,7 +815,6 @@ void Context::run_root() {  // dmk.cpp:657-701
   launch_accumulate_symbol(g, P.kernel, 1, root_dev_es_, root_dev_slot_, root_dev_tau_, G, pr.nch, dA, h, F, st_);
   launch_inverse(g, root_dev_ids_, 1, d, F, C, pf, in, st_);
   launches_ += 5;
-  sync();  // hA is reused
 }
 
 void Context::run_downward() {  // dmk.cpp:705-857
@@ -819,14 +845,22 @@ void Context::run_downward() {  // dmk.cpp:705-857
   const size_t budget = size_t(2) << 30;
   const int chunk_src = (int)std::max<size_t>(1, budget / bytes_B);
   const int chunk_tgt = (int)std::max<size_t>(1, budget / bytes_FC);
-  cudaEvent_t e0 = ev_[14], e1 = ev_[15];
-  float pw_ms = 0.0f;
+  // plane-wave timing: one event pair per level, read after the evaluation's
+  // final synchronisation (no host round trip between levels)
+  while ((int)pw_ev_.size() < 2 * L) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    pw_ev_.push_back(e);
+  }
+  pw_used_ = 0;
   for (int lev = 0; lev < L; ++lev) {
     const Problem::LevelLists& X = pr.levels[lev];
     if (X.n_src > 0 && X.n_tgt > 0) {
       double r_c = std::ldexp(1.0, -lev), r_f = 0.5 * r_c, h = PI / (3.0 * r_f);
       double pf = std::pow(1.0 / (6.0 * r_f), d);
       double2* G = arena_.as<double2>("pw_G", (size_t)X.n_src * pr.nch * g.nhalf);
+      cudaEvent_t e0 = pw_ev_[2 * pw_used_], e1 = pw_ev_[2 * pw_used_ + 1];
+      ++pw_used_;
       cudaEventRecord(e0, st_);
       for (int s0 = 0; s0 < X.n_src; s0 += chunk_src) {
         int n = std::min(chunk_src, X.n_src - s0);
@@ -863,10 +897,6 @@ void Context::run_downward() {  // dmk.cpp:705-857
         g0 = g1;
       }
       cudaEventRecord(e1, st_);
-      cudaEventSynchronize(e1);
-      float ms = 0.0f;
-      cudaEventElapsedTime(&ms, e0, e1);
-      pw_ms += ms;
     }
     if (X.n_interp > 0) {
       if (tensor_mma_supported(p, d))
@@ -877,9 +907,17 @@ void Context::run_downward() {  // dmk.cpp:705-857
       ++launches_;
     }
   }
-  t_pw_ms_ = pw_ms;
-  sync();
   cuda_check(cudaPeekAtLastError(), "kernel launch");
+}
+
+double Context::planewave_ms() {  // after a synchronisation
+  double t = 0.0;
+  for (int i = 0; i < pw_used_; ++i) {
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, pw_ev_[2 * i], pw_ev_[2 * i + 1]);
+    t += ms;
+  }
+  return t;
 }
 
 void Context::run_target_far(double* ufar) {  // dmk.cpp:861-915
@@ -984,10 +1022,11 @@ void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, in
   cuda_check(cudaMemcpyAsync(arena_.as<double>("str_in", (size_t)ns * sc), str, sizeof(double) * ns * sc, kind, st_),
              "copy strengths");
   cudaEventRecord(ev_[1], st_);
-  build_problem(P, dim, (int)ns, (int)nt, mode);
+  build_problem(P, dim, (int)ns, (int)nt, mode, true);
   cudaEventRecord(ev_[2], st_);
   run_upward();
   cudaEventRecord(ev_[3], st_);
+  upload_tree_lists_b(hq_);  // host work overlaps the upward pass on the GPU
   run_root();
   cudaEventRecord(ev_[4], st_);
   double* ufar = arena_.as<double>("ufar", (size_t)ntt * dim);
@@ -1054,7 +1093,7 @@ void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, in
     rep->t_d2h = ev_ms(6, 7) * 1e-3;
     rep->t_total = ev_ms(0, 7) * 1e-3;
     rep->t_residual_kernel = ev_ms(13, 12) * 1e-3;
-    rep->t_planewave = t_pw_ms_ * 1e-3;
+    rep->t_planewave = planewave_ms() * 1e-3;
     rep->p2p_candidates = (int64_t)hst[0];
     rep->p2p_in_support = (int64_t)hst[1];
     rep->kernel_launches = launches_;

@@ -77,6 +77,7 @@ struct Problem {
   int n_ant = 0, n_int = 0;
   int *rng_start = nullptr, *rng_box = nullptr, *rng_info = nullptr, *subrange = nullptr;
   int64_t t_own0 = 0, t_own1 = 0;  // owned range of Morton-sorted targets (set_shard)
+  bool lists_b = false;            // downward / residual lists uploaded
   int* res_chunks = nullptr;       // (leaf index, first target) per 32-target residual chunk
   int n_chunks = 0;
   struct LevelLists {
@@ -122,8 +123,9 @@ class Context {
  private:
   void check_inputs(const Plan& plan, int dim, int64_t ns, int64_t nt, int mode);
   // inputs already in the arena ("src_in", "tgt_in", "str_in"): validate, wrap, sort, topology, upload
-  void build_problem(const Plan& plan, int dim, int ns, int nt, int mode);
-  void upload_tree_lists(const int32_t* qs);
+  void build_problem(const Plan& plan, int dim, int ns, int nt, int mode, bool defer_lists = false);
+  void upload_tree_lists_a();
+  void upload_tree_lists_b(const int32_t* qs);
   void run_upward();
   void run_root();
   void run_downward();
@@ -145,8 +147,11 @@ class Context {
   int launches_ = 0;
   int *root_dev_ids_ = nullptr, *root_dev_es_ = nullptr, *root_dev_slot_ = nullptr, *root_dev_tau_ = nullptr;
   const double *cheb_nodes_ = nullptr, *cheb_wts_ = nullptr, *mats_up_ = nullptr, *mats_down_ = nullptr;
-  double t_pw_ms_ = 0.0;
+  std::vector<cudaEvent_t> pw_ev_;
+  int pw_used_ = 0;
+  double planewave_ms();
   int rank_ = 0, nranks_ = 1;
+  const int32_t* hq_ = nullptr;  // pinned sorted quantized coordinates of the current problem
   unsigned long long stats_[3] = {0, 0, 0};
 };
 
