@@ -752,7 +752,7 @@ __global__ void __launch_bounds__(kWI * 32, 1) k_inv_xy_mma(PWGrid g, const int*
 // outside the band); a pre-pass forms B'; the m0 = 0 column is a CUDA-core
 // dot product.  X stage as before over K = (m0, re|im), m0 = 0..M.
 template <int PT, int PC, int NC>
-__global__ void __launch_bounds__(kWI * 32, 1) k_inv_xy2(PWGrid g, const int* __restrict__ tboxes, int d,
+__global__ void __launch_bounds__(kWI * 32, 1) k_inv_xy2(PWGrid g, const int* __restrict__ tboxes, int ntb, int d,
                                                         const double2* __restrict__ C, double pf,
                                                         double* __restrict__ incoming) {
   constexpr int P8 = PT * 8;
@@ -802,11 +802,13 @@ __global__ void __launch_bounds__(kWI * 32, 1) k_inv_xy2(PWGrid g, const int* __
   for (int e = tid; e < 2 * 4 * K2 * SB; e += blockDim.x) Bre[e] = 0.0;  // Bre and Bim
   for (int c = tid; c < ncol; c += blockDim.x) dix[c] = (g.col_my[c] + M) * M1 + g.col_m0[c];
   __syncthreads();
-  const int tb = blockIdx.x, j = blockIdx.y;
-  const double2* Ci = C + ((size_t)tb * d + j) * (size_t)g.pz * ncol;
-  double* out = incoming + ((size_t)tboxes[tb] * d + j) * (size_t)(p * pp);
-  const int ngroups = (p + 3) / 4;
-  auto issue = [&](int grp, int buf) {
+  // persistent: the CTA walks items (box, component) with stride gridDim.x;
+  // the flattened (item, slab group) sequence keeps one group in flight
+  const int ngroups = (p + 3) / 4, nitems = ntb * d;
+  const int nsteps = ((nitems - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * ngroups;
+  auto issue = [&](int step, int buf) {
+    const int w = blockIdx.x + (step / ngroups) * gridDim.x, grp = step % ngroups;
+    const double2* Ci = C + (size_t)w * g.pz * ncol;
     double2* dst = den + buf * 4 * ND;
     for (int s = 0; s < 4; ++s) {
       const int iz = grp * 4 + s;
@@ -816,13 +818,16 @@ __global__ void __launch_bounds__(kWI * 32, 1) k_inv_xy2(PWGrid g, const int* __
     }
     cp_commit();
   };
-  issue(0, 0);
+  if (nsteps > 0) issue(0, 0);
   const int nyu = 4 * PT * MT;  // Y units (s, iy tile, m0 tile)
-  for (int grp = 0; grp < ngroups; ++grp) {
-    const int buf = grp & 1;
+  for (int step = 0; step < nsteps; ++step) {
+    const int buf = step & 1;
+    const int w = blockIdx.x + (step / ngroups) * gridDim.x, grp = step % ngroups;
+    const int tb = w / d, j = w % d;
+    double* out = incoming + ((size_t)tboxes[tb] * d + j) * (size_t)(p * pp);
     __syncthreads();  // the buffer the next issue overwrites is free
-    if (grp + 1 < ngroups) {
-      issue(grp + 1, buf ^ 1);
+    if (step + 1 < nsteps) {
+      issue(step + 1, buf ^ 1);
       cp_wait1();
     } else {
       cp_wait0();
@@ -1078,7 +1083,8 @@ void launch_inverse_mma(const PWGrid& g, const int* tboxes, int ntb, int d, cons
 #define IX2(PT_, PC_, NC_)                                                                  \
   do {                                                                                      \
     attr((const void*)k_inv_xy2<PT_, PC_, NC_>, sm2);                                       \
-    k_inv_xy2<PT_, PC_, NC_><<<grid, kWI * 32, sm2, st>>>(g, tboxes, d, C, pf, incoming);   \
+    k_inv_xy2<PT_, PC_, NC_><<<std::min(ntb * d, num_sms()), kWI * 32, sm2, st>>>(g, tboxes, ntb, d, C, pf,      \
+                                                                                    incoming);                 \
   } while (0)
       if (g.p == 23 && g.N == 33) IX2(3, 23, 33);
       else if (g.p == 22 && g.N == 33) IX2(3, 22, 33);
