@@ -144,10 +144,13 @@ int residual_max_pw();
 // u_res[perm[t]*d+j] for all targets of leaves `leaves`; flags[0] <- coincident
 // points; stats[0..1] <- candidates / in-support pairs (if stats != nullptr)
 // chunks: (leaf index into `leaves`, first target) pairs, 32 targets each,
-// one per warp (a leaf's targets split into ceil(n / 32) chunks)
+// one per warp (a leaf's targets split into ceil(n / 32) chunks).  srec is
+// scratch for the packed source records (ns * (d + sc rounded up to even)
+// doubles).
 void launch_residual(const ResidTables& rt, const dev::DBox* boxes, const int* leaves, int nleaf,
                      const int* chunks, int nchunks, const int* rng_start, const int* rng_box, const int* rng_info, const int* subrange,
-                     const double* spts, int ns, const double* sstr, const double* tpts, int nt,
+                     const double* spts, int ns, const double* sstr, double* srec, int periodic,
+                     const double* tpts, int nt,
                      const int* tperm, int alias, double self_coef_scale, double self_const,
                      double* ures, int* flags, unsigned long long* stats, cudaStream_t st);
 

@@ -34,6 +34,25 @@ constexpr int kMaxRanges = 160;
 constexpr int kMaxPW = 384;      // ni * (deg + 1) <= 384 (d, o) coefficient pairs
 constexpr int kCopies = 8;       // table copies, one per 16-byte bank group
 
+// Packed source record (coordinates, then strengths), padded to an even
+// number of doubles: the pair evaluation gathers one record with 16-byte loads
+// instead of d + sc scattered 8-byte loads.
+template <int KERNEL, int DIM>
+struct Rec {
+  static constexpr int kSc = KERNEL == 0 ? DIM : (KERNEL == 1 ? 2 * DIM : (DIM == 3 ? 3 : 1));
+  static constexpr int kW = (DIM + kSc + 1) / 2 * 2;
+};
+
+__global__ void k_pack_sources(const double* __restrict__ spts, const double* __restrict__ sstr, int n, int dim,
+                               int sc, int rw, double* __restrict__ rec) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double* r = rec + (size_t)i * rw;
+    for (int k = 0; k < dim; ++k) r[k] = spts[(size_t)k * n + i];
+    for (int k = 0; k < sc; ++k) r[dim + k] = sstr[(size_t)k * n + i];
+    for (int k = dim + sc; k < rw; ++k) r[k] = 0.0;
+  }
+}
+
 template <bool B>
 struct BoolC {
   static constexpr bool value = B;
@@ -92,8 +111,7 @@ __device__ __forceinline__ void radial_tables(const ResidTables& rt, const doubl
 // rinv = 1/r from rsqrt, so 1/r, 1/r^2, 1/r^3, 1/r^5 are products.
 template <int KERNEL, int DIM>
 __device__ __forceinline__ void assemble(double fd, double fo, const double* x, double rinv, double s,
-                                         double support, double nu, const double* __restrict__ sstr, int ns, int a,
-                                         double* u) {  // u: this pair's contribution (assigned)
+                                         double support, double nu, const double* sv, double* u) {  // u: this pair's contribution (assigned)
   constexpr double k8pi = 1.0 / (8.0 * dev::kPI), k4pi = 1.0 / (4.0 * dev::kPI);
   const double rinv2 = rinv * rinv;
   if (KERNEL == 0) {  // Stokeslet
@@ -103,7 +121,7 @@ __device__ __forceinline__ void assemble(double fd, double fo, const double* x, 
     double f[DIM], xf = 0.0;
 #pragma unroll
     for (int i = 0; i < DIM; ++i) {
-      f[i] = sstr[(size_t)i * ns + a];
+      f[i] = sv[i];
       xf += x[i] * f[i];
     }
     const double cd = amp * fd * c0, cf = amp * fo * c0 * xf * rinv2;
@@ -114,8 +132,8 @@ __device__ __forceinline__ void assemble(double fd, double fo, const double* x, 
     double f[DIM], nn[DIM], xf = 0.0, xn = 0.0, fn = 0.0;
 #pragma unroll
     for (int i = 0; i < DIM; ++i) {
-      f[i] = sstr[(size_t)i * ns + a];
-      nn[i] = sstr[(size_t)(DIM + i) * ns + a];
+      f[i] = sv[i];
+      nn[i] = sv[DIM + i];
       xf += x[i] * f[i];
       xn += x[i] * nn[i];
       fn += f[i] * nn[i];
@@ -127,12 +145,12 @@ __device__ __forceinline__ void assemble(double fd, double fo, const double* x, 
     for (int j = 0; j < DIM; ++j) u[j] = cd * (f[j] * xn + x[j] * fn + nn[j] * xf) + co * x[j];
   } else {  // rotlet
     if (DIM == 2) {
-      const double c0 = fo * sstr[a] * k4pi * rinv2;
+      const double c0 = fo * sv[0] * k4pi * rinv2;
       u[0] = c0 * x[1];
       u[1] = -(c0 * x[0]);
     } else {
       const double c0 = fo * k8pi * rinv2 * rinv;
-      const double g0 = sstr[a], g1 = sstr[(size_t)ns + a], g2 = sstr[(size_t)2 * ns + a];
+      const double g0 = sv[0], g1 = sv[1], g2 = sv[2];
       u[0] = c0 * (g1 * x[2] - g2 * x[1]);
       u[1] = c0 * (g2 * x[0] - g0 * x[2]);
       u[DIM - 1] = c0 * (g0 * x[1] - g1 * x[0]);
@@ -149,6 +167,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
                                                       const int* __restrict__ subrange,
                                                       const double* __restrict__ spts, int ns,
                                                       const double* __restrict__ sstr,
+                                                      const double2* __restrict__ srec, int periodic,
                                                       const double* __restrict__ tpts, int nt,
                                                       const int* __restrict__ tperm, int alias, double self_const,
                                                       double* __restrict__ ures, int* flags,
@@ -215,17 +234,32 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         const int a = lsrc[warp][i][lane];
         const int code = lrng[warp][i][lane];  // image shift (x+1 | y+1 << 2 | z+1 << 4) | fine << 6
         const double nu = (code & 64) ? r_f : r_l, inu = (code & 64) ? inv_rf : inv_rl;
+        constexpr int RW = Rec<KERNEL, DIM>::kW;
+        double rv[RW];
+        const double2* rp = srec + (size_t)a * (RW / 2);
+#pragma unroll
+        for (int k = 0; k < RW / 2; ++k) {
+          const double2 v = rp[k];
+          rv[2 * k] = v.x;
+          rv[2 * k + 1] = v.y;
+        }
         double x[3] = {0.0, 0.0, 0.0}, r2 = 0.0;
-        x[0] = xt[0] - (spx[a] + (double)((code & 3) - 1));
-        x[1] = xt[1] - (spy[a] + (double)(((code >> 2) & 3) - 1));
-        if (DIM == 3) x[2] = xt[2] - (spz[a] + (double)(((code >> 4) & 3) - 1));
+        if (periodic) {  // image shifts (zero shifts add exactly 0)
+          x[0] = xt[0] - (rv[0] + (double)((code & 3) - 1));
+          x[1] = xt[1] - (rv[1] + (double)(((code >> 2) & 3) - 1));
+          if (DIM == 3) x[2] = xt[2] - (rv[2] + (double)(((code >> 4) & 3) - 1));
+        } else {
+          x[0] = xt[0] - rv[0];
+          x[1] = xt[1] - rv[1];
+          if (DIM == 3) x[2] = xt[2] - rv[2];
+        }
 #pragma unroll
         for (int ax = 0; ax < DIM; ++ax) r2 += x[ax] * x[ax];
         const double rinv = rsqrt_nr(r2);
         const double s = (r2 * rinv) * inu;  // nu is a power of two: r * (1/nu) == r / nu
         double fd, fo;
         radial_tables<KERNEL, DEG>(rt, s_pw + (lane & (kCopies - 1)), yscale, s, fd, fo);
-        assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, nu, sstr, ns, a, c);
+        assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, nu, rv + DIM, c);
       };
       for (int i = 0; i < mx; i += 2) {  // both evaluations unconditional (clamped), straight-line
         const int i0 = min(i, cnt - 1), i1 = min(i + 1, cnt - 1);
@@ -377,9 +411,15 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
 void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves, int nleaf, const int* chunks,
                      int nchunks, const int* rng_start,
                      const int* rng_box, const int* rng_info, const int* subrange, const double* spts, int ns, const double* sstr,
+                     double* srec, int periodic,
                      const double* tpts, int nt, const int* tperm, int alias, double /*unused*/, double self_const,
                      double* ures, int* flags, unsigned long long* stats, cudaStream_t st) {
   if (nleaf <= 0 || nchunks <= 0) return;
+  {
+    const int sc = rt.kernel == 0 ? rt.dim : (rt.kernel == 1 ? 2 * rt.dim : (rt.dim == 3 ? 3 : 1));
+    const int rw = (rt.dim + sc + 1) / 2 * 2;
+    k_pack_sources<<<148 * 8, 256, 0, st>>>(spts, sstr, ns, rt.dim, sc, rw, srec);
+  }
   const int nblk = (nchunks + kWarps - 1) / kWarps;
   const int2* ch2 = reinterpret_cast<const int2*>(chunks);
   const size_t dsm = (size_t)kWarps * kList * 32 * (sizeof(int) + 1) +
@@ -396,7 +436,8 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
     cudaFuncSetAttribute(k_residual<K, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);            \
     k_residual<K, D, G><<<nblk, kRBlock, dsm, st>>>(rt, boxes, leaves, ch2, nchunks, rng_start, rng_box,         \
                                                     rng_info, subrange,                                          \
-                                                     spts, ns, sstr, tpts, nt, tperm, alias, self_const, ures,   \
+                                                     spts, ns, sstr, reinterpret_cast<const double2*>(srec),     \
+                                                     periodic, tpts, nt, tperm, alias, self_const, ures,         \
                                                      flags, stats);                                              \
   } while (0)
   if (rt.dim == 3) {
