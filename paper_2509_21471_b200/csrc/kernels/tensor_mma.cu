@@ -371,6 +371,185 @@ __global__ void __launch_bounds__(kT3W * 32, 1)
   }
 }
 
+// PT = 4 (p = 25..32): the same schedule with the output's ix columns split
+// over two CTAs (blockIdx.z).  The x stage only needs the CTA's ix half of
+// Mx, the y stage contracts jy and keeps ix, the z stage contracts jz and
+// keeps (iy, ix) -- so the split duplicates no work and halves the z
+// accumulators (which would not fit in registers for p^3 = 27 000 outputs).
+constexpr int kT4W = 12;
+template <int PC>
+__global__ void __launch_bounds__(kT4W * 32, 1)
+    k_tensor4(int p_rt, const double* __restrict__ mats, const int* __restrict__ in_list,
+              const int* __restrict__ out_box, const int* __restrict__ ci_list, int nin, int nch,
+              const double* __restrict__ src, double* __restrict__ dst, int accumulate) {
+  constexpr int PT = 4, P8 = 32, SA = 36, NXH = 2, XW = 16, S1 = 20, SG = 8, NWp = kT4W;
+  const int p = PC > 0 ? PC : p_rt;
+  const int pp = p * p, nodes = p * pp;
+  const int ix0 = blockIdx.z * XW;
+  const int NC = p * XW;                      // z-stage columns (iy, ix local)
+  const int NN = NC / 8;
+  const int SS = NC + 4;                      // T2 row stride (== 4 mod 8)
+  constexpr int ZN = (32 * XW / 8 + NWp - 1) / NWp;  // max column tiles per warp
+  constexpr int XR = (SG * PT + NWp - 1) / NWp;      // x-stage row tiles per warp
+  extern __shared__ double sm[];
+  __shared__ int s_in[8], s_ci[8], s_nq;
+  double* Mm = sm;                       // [2][P8][SA]
+  double* T1 = Mm + 2 * P8 * SA;         // [SG * P8][S1]
+  double* T2 = T1 + SG * P8 * S1;        // [SG][SS]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  for (int r = warp; r < 2 * P8; r += NWp) {
+    const int bsel = r / P8, rr = r % P8;
+    for (int c = lane; c < SA; c += 32) Mm[r * SA + c] = (rr < p && c < p) ? mats[(size_t)bsel * pp + rr * p + c] : 0.0;
+  }
+  for (int e = tid; e < SG * SS; e += blockDim.x) T2[e] = 0.0;
+  const int pair = blockIdx.x, ch = blockIdx.y;
+  if (tid == 0) {
+    int nq = 0;
+    for (int q = 0; q < nin; ++q) {
+      const int ib = in_list[pair * nin + q];
+      if (ib >= 0) {
+        s_in[nq] = ib;
+        s_ci[nq] = ci_list[pair * nin + q];
+        ++nq;
+      }
+    }
+    s_nq = nq;
+  }
+  __syncthreads();
+  const int ngroups = (p + SG - 1) / SG;
+  const int nitems = s_nq * ngroups;
+  double acc[ZN][PT][2];
+#pragma unroll
+  for (int i = 0; i < ZN; ++i)
+#pragma unroll
+    for (int m = 0; m < PT; ++m) acc[i][m][0] = acc[i][m][1] = 0.0;
+  int roff[XR];
+  bool rok[XR];
+#pragma unroll
+  for (int h = 0; h < XR; ++h) {
+    const int mt = warp + NWp * h;
+    const int row = mt * 8 + g, sl = row / P8, jy = row % P8;
+    roff[h] = sl * pp + jy * p;
+    rok[h] = mt < SG * PT && jy < p;
+  }
+  double af[XR][2 * PT];
+  auto load_a = [&](int item) {
+    const int q = item / ngroups, jz0 = (item % ngroups) * SG;
+    const double* in = src + ((size_t)s_in[q] * nch + ch) * nodes + (size_t)jz0 * pp;
+#pragma unroll
+    for (int h = 0; h < XR; ++h) {
+      const int sl = ((warp + NWp * h) * 8 + g) / P8;
+      const bool ok = rok[h] && jz0 + sl < p;
+#pragma unroll
+      for (int ks = 0; ks < 2 * PT; ++ks) {
+        const int jx = ks * 4 + t;
+        af[h][ks] = (ok && jx < p) ? __ldg(in + roff[h] + jx) : 0.0;
+      }
+    }
+  };
+  if (nitems > 0) load_a(0);
+  for (int item = 0; item < nitems; ++item) {
+    const int q = item / ngroups, jz0 = (item % ngroups) * SG;
+    const int cb = s_ci[q];
+    const double* Mx = Mm + (cb & 1) * P8 * SA;
+    const double* My = Mm + ((cb >> 1) & 1) * P8 * SA;
+    const double* Mz = Mm + ((cb >> 2) & 1) * P8 * SA;
+    // x stage: T1[(s,jy), ixl] = sum_jx in[(s,jy), jx] Mx[ix0 + ixl, jx]
+#pragma unroll
+    for (int h = 0; h < XR; ++h) {
+      const int mt = warp + NWp * h;
+      if (mt >= SG * PT) continue;
+      double c[NXH][2];
+#pragma unroll
+      for (int n = 0; n < NXH; ++n) c[n][0] = c[n][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 2 * PT; ++ks)
+#pragma unroll
+        for (int n = 0; n < NXH; ++n)
+          dev::dmma(c[n][0], c[n][1], af[h][ks], Mx[(ix0 + n * 8 + g) * SA + ks * 4 + t]);
+#pragma unroll
+      for (int n = 0; n < NXH; ++n) {
+        double* o = T1 + (mt * 8 + g) * S1 + n * 8 + 2 * t;
+        o[0] = c[n][0];
+        o[1] = c[n][1];
+      }
+    }
+    if (item + 1 < nitems) load_a(item + 1);  // in flight during the y and z stages
+    __syncthreads();
+    // y stage: T2[s][iy, ixl] = sum_jy My[iy, jy] T1[(s,jy), ixl]
+    for (int u = warp; u < SG * PT; u += NWp) {
+      const int sl = u / PT, mt = u % PT;
+      double c[NXH][2];
+#pragma unroll
+      for (int n = 0; n < NXH; ++n) c[n][0] = c[n][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 2 * PT; ++ks) {
+        const double av = My[(mt * 8 + g) * SA + ks * 4 + t];
+#pragma unroll
+        for (int n = 0; n < NXH; ++n)
+          dev::dmma(c[n][0], c[n][1], av, T1[(sl * P8 + ks * 4 + t) * S1 + n * 8 + g]);
+      }
+      const int iy = mt * 8 + g;
+      if (iy < p) {
+#pragma unroll
+        for (int n = 0; n < NXH; ++n) {
+          T2[sl * SS + iy * XW + n * 8 + 2 * t] = c[n][0];
+          T2[sl * SS + iy * XW + n * 8 + 2 * t + 1] = c[n][1];
+        }
+      }
+    }
+    __syncthreads();
+    // z stage: C[iz, (iy, ixl)] += sum_{jz in group} Mz[iz, jz] T2[jz][(iy, ixl)]
+#pragma unroll
+    for (int ks = 0; ks < SG / 4; ++ks) {
+      double av[PT];
+#pragma unroll
+      for (int m = 0; m < PT; ++m) av[m] = Mz[(m * 8 + g) * SA + jz0 + ks * 4 + t];
+#pragma unroll
+      for (int i = 0; i < ZN; ++i) {
+        const int nt = warp + NWp * i;
+        if (nt < NN) {
+          const double bv = T2[(ks * 4 + t) * SS + nt * 8 + g];
+#pragma unroll
+          for (int m = 0; m < PT; ++m) dev::dmma(acc[i][m][0], acc[i][m][1], av[m], bv);
+        }
+      }
+    }
+  }
+  double* out = dst + ((size_t)out_box[pair] * nch + ch) * nodes;
+#pragma unroll
+  for (int i = 0; i < ZN; ++i) {
+    const int nt = warp + NWp * i;
+    if (nt >= NN) continue;
+#pragma unroll
+    for (int m = 0; m < PT; ++m) {
+      const int iz = m * 8 + g;
+      if (iz >= p) continue;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = nt * 8 + 2 * t + e, iy = col / XW, ix = ix0 + col % XW;
+        if (ix < p) {
+          double* o = out + (size_t)iz * pp + iy * p + ix;
+          *o = accumulate ? *o + acc[i][m][e] : acc[i][m][e];
+        }
+      }
+    }
+  }
+}
+
+template <int PC>
+void tensor4_t(int p, const double* mats, const int* in_list, const int* out_box, const int* ci, int npairs, int nin,
+               int nch, const double* src, double* dst, int accumulate, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (2 * 32 * 36 + 8 * 32 * 20 + 8 * ((size_t)p * 16 + 4));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tensor4<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  dim3 grid(npairs, nch, 2);
+  k_tensor4<PC><<<grid, kT4W * 32, smem, st>>>(p, mats, in_list, out_box, ci, nin, nch, src, dst, accumulate);
+}
+
 template <int PC>
 void tensor3_t(int p, const double* mats, const int* in_list, const int* out_box, const int* ci, int npairs, int nin,
                int nch, const double* src, double* dst, int accumulate, cudaStream_t st) {
@@ -419,6 +598,8 @@ void launch_tensor_mma(int p, const double* mats, const int* in_list, const int*
   else if (PT == 3 && !old3) tensor3_t<0>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
   else if (p == 22) TM(22, 3, 16, 13);
   else if (p == 23) TM(23, 3, 16, 13);
+  else if (p == 30 && !old3) tensor4_t<30>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
+  else if (PT == 4 && !old3) tensor4_t<0>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
   else if (p == 30) TM(30, 4, 16, 32);
   else if (PT <= 1) TM(0, 1, 4, 8);
   else if (PT == 2) TM(0, 2, 8, 12);
