@@ -197,9 +197,17 @@ struct Builder {
     return false;
   }
 
-  void repair() {  // tree.cpp:125-165
-    for (bool again = true; again;) {
-      again = false;
+  // repair (tree.cpp:125-165): sweeps over the leaves in id order, each leaf
+  // subdividing every leaf >= 2 levels coarser that one of its 3^d - 1 probes
+  // lands in, until a sweep changes nothing.  Subdivisions only refine, so a
+  // leaf that cannot trigger at the start of a sweep never triggers later;
+  // the next sweep therefore only has to look at the leaves this sweep created
+  // and the leaves that triggered in it (a coarse neighbour 3+ levels up may
+  // still be 2+ levels up after one split).  The first sweep probes every
+  // leaf in parallel; every replay runs in the reference's order.
+  void repair() {
+    std::vector<int> cand_ids;
+    {
       std::vector<int> leaves;
       for (int b = 0; b < t.num_boxes(); ++b)
         if (t.boxes[b].leaf) leaves.push_back(b);
@@ -207,13 +215,17 @@ struct Builder {
       std::vector<char> cand(nl, 0);
 #pragma omp parallel for schedule(dynamic, 64)
       for (int i = 0; i < nl; ++i) cand[i] = probe_triggers(leaves[i], nullptr);
-      for (int i = 0; i < nl; ++i) {
-        if (!cand[i]) continue;  // cannot trigger: later subdivisions only refine
-        const int b = leaves[i];
+      for (int i = 0; i < nl; ++i)
+        if (cand[i]) cand_ids.push_back(leaves[i]);
+    }
+    while (!cand_ids.empty()) {
+      std::vector<int> next;
+      for (const int b : cand_ids) {
         if (!t.boxes[b].leaf) continue;
         const int lev = t.boxes[b].level;
         const int64_t side = kCells >> lev;
         const int zr = t.dim == 3 ? 1 : 0;
+        bool fired = false;
         for (int o2 = -zr; o2 <= zr; ++o2)
           for (int o1 = -1; o1 <= 1; ++o1)
             for (int o0 = -1; o0 <= 1; ++o0) {
@@ -233,10 +245,21 @@ struct Builder {
               const int a = descend(probe);
               if (t.boxes[a].leaf && t.boxes[a].level <= lev - 2) {
                 subdivide(a);
-                again = true;
+                for (int ci = 0; ci < nchild; ++ci) next.push_back(t.boxes[a].first_child + ci);
+                fired = true;
               }
             }
+        if (fired) next.push_back(b);
       }
+      // the next sweep's candidates, in id order (the order the sweep visits leaves)
+      std::sort(next.begin(), next.end());
+      next.erase(std::unique(next.begin(), next.end()), next.end());
+      std::vector<char> trig(next.size(), 0);
+#pragma omp parallel for schedule(dynamic, 64)
+      for (int i = 0; i < (int)next.size(); ++i) trig[i] = t.boxes[next[i]].leaf && probe_triggers(next[i], nullptr);
+      cand_ids.clear();
+      for (size_t i = 0; i < next.size(); ++i)
+        if (trig[i]) cand_ids.push_back(next[i]);
     }
   }
 
@@ -272,6 +295,7 @@ struct Builder {
   }
 
   void neighbours() {  // tree.cpp:167-212
+    const auto tn0 = std::chrono::steady_clock::now();
     const int nb = t.num_boxes();
     for (Csr* L : {&t.col, &t.crs, &t.fin}) {
       L->off.assign(nb, 0);
@@ -292,28 +316,41 @@ struct Builder {
     t.col.off[0] = 0;
     t.col.len[0] = (int)root.size();
     t.col.v = root;
+    // relative position of box c (with periodic shift sh) to box b, in units of
+    // b's side, per axis: exact integer (anchors are multiples of the side)
+    auto rel = [&](int b, int c, const int8_t* sh, int64_t unit, int* o) {
+      for (int a = 0; a < t.dim; ++a)
+        o[a] = int((int64_t(t.boxes[c].anchor[a]) + int64_t(sh[a]) * kCells - int64_t(t.boxes[b].anchor[a])) / unit);
+    };
     for (int lev = 1; lev <= t.max_level; ++lev) {
       const std::vector<int>& ids = t.level_boxes[lev];
-      // colleagues: children of the parent's non-leaf colleagues that touch b
-      csr_pass(
-          t.col, ids,
-          [&](int b) {
-            int c = 0;
-            for (const Nbr& pc : t.col[t.boxes[b].parent]) {
-              if (t.boxes[pc.box].leaf) continue;
-              for (int ci = 0; ci < nchild; ++ci) c += touch(b, t.boxes[pc.box].first_child + ci, pc.shift);
+      const int64_t ps = kCells >> (lev - 1), hs = ps / 2;  // parent side, child side
+      // colleagues: children of the parent's non-leaf colleagues that touch b.
+      // A child at offset 2 o + cc (child units) from b's parent touches b at
+      // cb iff |2 o + cc - cb| <= 1 on every axis -- no child box is loaded.
+      auto col_scan = [&](int b, Nbr* out) {
+        const int par = t.boxes[b].parent;
+        int cb[3] = {0, 0, 0};
+        for (int a = 0; a < t.dim; ++a) cb[a] = int((t.boxes[b].anchor[a] - t.boxes[par].anchor[a]) / hs);
+        int n = 0;
+        for (const Nbr& pc : t.col[par]) {
+          if (t.boxes[pc.box].leaf) continue;
+          int o[3] = {0, 0, 0};
+          rel(par, pc.box, pc.shift, ps, o);
+          for (int ci = 0; ci < nchild; ++ci) {
+            bool ok = true;
+            for (int a = 0; a < t.dim; ++a) {
+              const int dlt = 2 * o[a] + ((ci >> a) & 1) - cb[a];
+              ok = ok && dlt >= -1 && dlt <= 1;
             }
-            return c;
-          },
-          [&](int b, Nbr* out) {
-            for (const Nbr& pc : t.col[t.boxes[b].parent]) {
-              if (t.boxes[pc.box].leaf) continue;
-              for (int ci = 0; ci < nchild; ++ci) {
-                const int d = t.boxes[pc.box].first_child + ci;
-                if (touch(b, d, pc.shift)) *out++ = {d, {pc.shift[0], pc.shift[1], pc.shift[2]}};
-              }
-            }
-          });
+            if (!ok) continue;
+            if (out) out[n] = {t.boxes[pc.box].first_child + ci, {pc.shift[0], pc.shift[1], pc.shift[2]}};
+            ++n;
+          }
+        }
+        return n;
+      };
+      csr_pass(t.col, ids, [&](int b) { return col_scan(b, nullptr); }, [&](int b, Nbr* out) { col_scan(b, out); });
       // coarse: the parent's leaf colleagues that touch b
       csr_pass(
           t.crs, ids,
@@ -328,17 +365,29 @@ struct Builder {
               if (t.boxes[pc.box].leaf && touch(b, pc.box, pc.shift)) *out++ = pc;
           });
     }
-    // fine: leaf children of non-leaf colleagues (other than self) that touch b
+    // fine: leaf children of non-leaf colleagues (other than self) that touch b.
+    // A colleague at offset o (b's units) has children at 2 o + cc (half
+    // units), touching b's [0, 2) iff 2 o + cc lies in [-1, 2].
+    const auto tn1 = std::chrono::steady_clock::now();
     std::vector<int> all(nb);
     for (int b = 0; b < nb; ++b) all[b] = b;
     auto fine_scan = [&](int b, Nbr* out) {
       int c = 0;
+      const int64_t side = kCells >> t.boxes[b].level;
       for (const Nbr& ce : t.col[b]) {
         if (ce.box == b && !ce.shift[0] && !ce.shift[1] && !ce.shift[2]) continue;
         if (t.boxes[ce.box].leaf) continue;
+        int o[3] = {0, 0, 0};
+        rel(b, ce.box, ce.shift, side, o);
         for (int ci = 0; ci < nchild; ++ci) {
+          bool ok = true;
+          for (int a = 0; a < t.dim; ++a) {
+            const int pos = 2 * o[a] + ((ci >> a) & 1);
+            ok = ok && pos >= -1 && pos <= 2;
+          }
+          if (!ok) continue;
           const int d = t.boxes[ce.box].first_child + ci;
-          if (t.boxes[d].leaf && touch(b, d, ce.shift)) {
+          if (t.boxes[d].leaf) {
             if (out) out[c] = {d, {ce.shift[0], ce.shift[1], ce.shift[2]}};
             ++c;
           }
@@ -347,6 +396,11 @@ struct Builder {
       return c;
     };
     csr_pass(t.fin, all, [&](int b) { return fine_scan(b, nullptr); }, [&](int b, Nbr* out) { fine_scan(b, out); });
+    if (std::getenv("SDMK_TIMING")) {
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      std::fprintf(stderr, "[sdmk timing] neighbours: levels %.2f ms, fine %.2f ms (%d boxes, %d levels)\n",
+                   ms(tn0, tn1), ms(tn1, std::chrono::steady_clock::now()), nb, t.max_level);
+    }
   }
 };
 
