@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(kA2W * 32, 1) k_anterp2(ChebDev cb, const DBox
   const DBox box = boxes[b];
   const int nt0 = blockIdx.y * kA2W * NTW;
   __shared__ int rcode[MT * 8];  // (ch, iz) of each S row
+  __shared__ double s_chv[kKC][8];
   for (int r = tid; r < MT * 8; r += blockDim.x) rcode[r] = r < MR ? ((r / pz) | ((r % pz) << 8)) : -1;
   int iyv[NTW], ixv[NTW];
 #pragma unroll
@@ -351,11 +352,9 @@ __global__ void __launch_bounds__(kA2W * 32, 1) k_anterp2(ChebDev cb, const DBox
     const double* by = bx + kKC * XS;
     const double* bz = by + kKC * XS;
     const double* ss = bz + kKC * XS;
-    for (int r = tid % (MT * 8), pt = tid / (MT * 8); pt < kKC; pt += blockDim.x / (MT * 8)) {  // S = s_ch * bz
-      if (tid >= (blockDim.x / (MT * 8)) * (MT * 8)) break;
-      const int code = rcode[r];
-      if (code < 0) continue;
-      const int ch = code & 255, iz = code >> 8;
+    // channel values once per point (build_source_channels, dmk.cpp:492-525) ...
+    for (int e = tid; e < kKC * nch; e += blockDim.x) {
+      const int pt = e / nch, ch = e % nch;
       const double* s = ss + pt * 8;
       double sv;
       if (kernel == 1) {
@@ -375,7 +374,13 @@ __global__ void __launch_bounds__(kA2W * 32, 1) k_anterp2(ChebDev cb, const DBox
       } else {
         sv = s[ch];
       }
-      sbz[pt * RS + r] = sv * (dim == 3 ? bz[pt * XS + iz] : 1.0);
+      s_chv[pt][ch] = sv;
+    }
+    __syncthreads();
+    // ... then S[pt][(ch, iz)] = s_ch * bz over all threads
+    for (int e = tid; e < kKC * MR; e += blockDim.x) {
+      const int pt = e / MR, r = e - pt * MR, code = rcode[r];
+      sbz[pt * RS + r] = s_chv[pt][code & 255] * (dim == 3 ? bz[pt * XS + (code >> 8)] : 1.0);
     }
     __syncthreads();
 #pragma unroll 2
