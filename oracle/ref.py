@@ -70,6 +70,8 @@ def lib():
         L.ref_incoming.argtypes = [C.c_int, dp]
         L.ref_evaluate.argtypes = [dp, C.POINTER(ref_report)]
         L.ref_direct_residual_sum.argtypes = [C.c_double, dp]
+        L.ref_ewald_reference.argtypes = [C.c_int, dp]
+        L.ref_self_scaled.argtypes = [C.c_double, dp]
         L.ref_export_tables.argtypes = [C.c_char_p]
         L.ref_window.argtypes = [dp, dp, C.c_int]
         for n in ["ref_window_fourier", "ref_mollifier_fourier", "ref_window_eval", "ref_phi_tail"]:
@@ -185,6 +187,16 @@ class RefProblem:
         out = np.empty(self.nt * self.dim)
         _chk(lib().ref_direct_residual_sum(cutoff, _dp(out)))
         return out
+
+    def ewald_reference(self, periodic=True):
+        out = np.empty(self.nt * self.dim)
+        _chk(lib().ref_ewald_reference(1 if periodic else 0, _dp(out)))
+        return out
+
+    def self_scaled(self, nu):
+        v = C.c_double()
+        _chk(lib().ref_self_scaled(nu, C.byref(v)))
+        return v.value
 
     def export_tables(self, path):
         _chk(lib().ref_export_tables(path.encode()))

@@ -289,6 +289,19 @@ int ref_direct_residual_sum(double cutoff, double* out) {
   });
 }
 
+/* the slow single-level split reference (oracle.cpp ewald_reference):
+   periodic = 1 for the Fourier series over 2 pi kappa, 0 for free space */
+int ref_ewald_reference(int periodic, double* out) {
+  return guard([&] {
+    copy_out(ewald_reference(g_sk, g_sys, periodic ? EwaldMode::periodic : EwaldMode::free_space), out);
+  });
+}
+
+/* split.cpp self_interaction_scaled: the self coefficient at scale nu */
+int ref_self_scaled(double nu, double* out) {
+  return guard([&] { *out = self_interaction_scaled(g_sk, nu); });
+}
+
 int ref_periodic_zero_mode(double* out) {
   return guard([&] { copy_out(periodic_zero_mode(g_plan.kernel, g_sys), out); });
 }
