@@ -148,3 +148,106 @@ def test_periodic_matches_slow_fourier_reference(dim, kernel, bound, n_s, ns, nt
     # reference DMK's own error is the yardstick where it is larger
     ref_err = _rel_l2(R.evaluate()[0], want)
     assert _rel_l2(u, want) <= max(bound, 1.001 * ref_err)
+
+
+def _direct(kernel, dim, x, s, t=None):
+    ref = _ref()
+    plan = ref.select_parameters(kernel, 1e-6, 0, dim)
+    return ref.RefProblem(plan, dim, x, s, targets=t).direct_sum()
+
+
+def _yardstick(plan, dim, x, s, t, bound, exact):
+    """max(bound, the reference DMK's own error on this system): the
+    reference's bounds were set on its own fixture (mixed_system)."""
+    ref = _ref()
+    ur, _ = ref.RefProblem(plan.__dict__, dim, x, s, targets=t).evaluate()
+    return max(bound, 1.001 * _rel_l2(ur, exact))
+
+
+@pytest.mark.parametrize("sep", [0.4, 0.26, 0.13, 0.06, 0.031, 0.015, 0.008, 0.004, 0.0019, 0.0009])
+def test_deep_trees_all_separation_classes(sep):  # test_dmk.cpp:393-413
+    ctx = g.Context(0)
+    plan = g.select_parameters(0, 1e-6, g.PROLATE, 3)
+    plan.n_s = 1
+    x = np.array([[-0.271, 0.113, -0.041], [-0.271 + sep, 0.113 + 0.3 * sep, -0.041 - 0.2 * sep]])
+    s = np.array([[0.8, -0.45, 0.3], [-0.6, 0.95, 0.21]])
+    u = ctx.evaluate_with_plan(plan, g.ParticleSystem(3, x, np.zeros(0), s))
+    assert _rel_l2(u, _direct(0, 3, x, s)) <= 5e-6
+
+
+@pytest.mark.parametrize("kernel,eps,bound", [(0, 1e-3, 1e-3), (0, 1e-6, 1e-6), (1, 1e-3, 1e-3), (1, 1e-6, 1e-6),
+                                              (2, 1e-3, 2e-3), (2, 1e-6, 2e-6)])
+def test_adaptive_accuracy_3d(kernel, eps, bound):  # test_dmk.cpp:415-458
+    ctx = g.Context(0)
+    plan = g.select_parameters(kernel, eps, g.PROLATE, 3)
+    plan.n_s = 75
+    x, s, t = _system(kernel, 3, 600, 150, 101 + kernel)
+    rep = {}
+    u = ctx.evaluate_with_plan(plan, g.ParticleSystem(3, x, t, s), g.FREE_SPACE, rep)
+    exact = _direct(kernel, 3, x, s, t)
+    assert rep["max_level"] >= 2
+    assert _rel_l2(u, exact) <= _yardstick(plan, 3, x, s, t, bound, exact)
+
+
+@pytest.mark.parametrize("eps", [1e-9, 1e-12])
+def test_tight_tolerances_shallow_tree(eps):
+    ctx = g.Context(0)
+    plan = g.select_parameters(0, eps, g.PROLATE, 3)
+    plan.n_s = 150
+    x, s, _ = _system(0, 3, 400, 0, 7)
+    u = ctx.evaluate_with_plan(plan, g.ParticleSystem(3, x, np.zeros(0), s))
+    exact = _direct(0, 3, x, s)
+    bound = 5e-12 if eps == 1e-12 else eps
+    assert _rel_l2(u, exact) <= _yardstick(plan, 3, x, s, np.zeros(0), bound, exact)
+
+
+@pytest.mark.parametrize("kernel,factor", [(0, 1.0), (1, 3.0), (2, 4.0)])
+@pytest.mark.parametrize("eps", [1e-3, 1e-6])
+def test_adaptive_accuracy_2d(kernel, factor, eps):  # test_dmk.cpp:460-492
+    ctx = g.Context(0)
+    plan = g.select_parameters(kernel, eps, g.PROLATE, 2)
+    plan.n_s = 48
+    x, s, t = _system(kernel, 2, 500, 120, 211 + kernel)
+    u = ctx.evaluate_with_plan(plan, g.ParticleSystem(2, x, t, s))
+    exact = _direct(kernel, 2, x, s, t)
+    assert _rel_l2(u, exact) <= _yardstick(plan, 2, x, s, t, factor * eps, exact)
+
+
+def test_gaussian_window_agrees_with_direct_and_prolate():  # test_dmk.cpp:494-510
+    ctx = g.Context(0)
+    gp = g.select_parameters(0, 1e-6, g.GAUSSIAN, 3)
+    gp.n_s = 75
+    x, s, t = _system(0, 3, 500, 100, 307)
+    sysm = g.ParticleSystem(3, x, t, s)
+    ug = ctx.evaluate_with_plan(gp, sysm)
+    exact = _direct(0, 3, x, s, t)
+    assert _rel_l2(ug, exact) <= _yardstick(gp, 3, x, s, t, 2e-6, exact)
+    pp = g.select_parameters(0, 1e-6, g.PROLATE, 3)
+    pp.n_s = 75
+    up = ctx.evaluate_with_plan(pp, sysm)
+    assert _rel_l2(up, ug) <= 3e-6
+
+
+def test_leaf_capacity_does_not_change_the_answer():  # test_dmk.cpp:625-634
+    ctx = g.Context(0)
+    plan = g.select_parameters(0, 1e-6, g.PROLATE, 3)
+    x, s, _ = _system(0, 3, 300, 0, 601)
+    exact = _direct(0, 3, x, s)
+    for n_s in (60, 200):
+        plan.n_s = n_s
+        u = ctx.evaluate_with_plan(plan, g.ParticleSystem(3, x, np.zeros(0), s))
+        assert _rel_l2(u, exact) <= 1e-6
+
+
+def test_report_and_convenience_wrapper():  # test_dmk.cpp:645-666
+    ctx = g.Context(0)
+    x, s, t = _system(2, 3, 250, 80, 701)
+    rep = {}
+    u = ctx.evaluate(g.ROTLET, g.ParticleSystem(3, x, t, s), 1e-3, g.PROLATE, g.FREE_SPACE, rep)
+    assert u.size == 80 * 3
+    assert rep["num_sources"] == 250 and rep["num_targets"] == 80 and rep["num_boxes"] >= 1
+    assert g.select_parameters(g.ROTLET, 1e-3, g.PROLATE, 3).p == 8
+    assert rep["t_tree"] >= 0.0 and rep["t_residual"] >= 0.0
+    assert _rel_l2(u, _direct(2, 3, x, s, t)) <= 1e-3
+    uz = ctx.evaluate(g.ROTLET, g.ParticleSystem(3, x, t, np.zeros_like(s)), 1e-3, g.PROLATE, g.FREE_SPACE)
+    assert np.all(uz == 0.0)
