@@ -159,10 +159,91 @@ Context::~Context() {
   if (st_) cudaStreamSynchronize(st_);
   for (auto& e : ev_) cudaEventDestroy(e);
   for (auto& e : pw_ev_) cudaEventDestroy(e);
+  for (auto& e : stage_ev_) cudaEventDestroy(e);
   if (st_) cudaStreamDestroy(st_);
 }
 
 void Context::sync() { cuda_check(cudaStreamSynchronize(st_), "stream synchronize"); }
+
+// Host <-> device copies of the caller's arrays.  Pinned (or device) memory
+// goes straight to the copy engine; pageable memory is staged through a ring
+// of pinned chunks, the chunk copies on the host threads overlapping the DMA
+// of the previous chunk (a pageable cudaMemcpy runs at a fraction of the
+// link rate).
+namespace {
+bool is_pageable(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const size_t blk = size_t(1) << 20;
+  const int64_t nblk = (int64_t)((bytes + blk - 1) / blk);
+#pragma omp parallel for schedule(static) if (nblk > 1)
+  for (int64_t i = 0; i < nblk; ++i) {
+    const size_t o = (size_t)i * blk, n = std::min(blk, bytes - o);
+    std::memcpy((char*)dst + o, (const char*)src + o, n);
+  }
+}
+constexpr size_t kStageBytes = size_t(32) << 20;
+constexpr int kStages = 4;
+}  // namespace
+
+void Context::stage_events() {
+  if (!stage_ev_.empty()) return;
+  for (int i = 0; i < kStages; ++i) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    stage_ev_.push_back(e);
+  }
+}
+
+void Context::copy_in(void* dst, const void* src, size_t bytes, bool device_ptrs) {
+  if (bytes == 0) return;
+  if (device_ptrs || !is_pageable(src) || bytes <= kStageBytes) {
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st_),
+               "copy in");
+    return;
+  }
+  stage_events();
+  char* ring = (char*)pinned_.get("stage", kStages * kStageBytes);
+  int k = 0;
+  for (size_t o = 0; o < bytes; o += kStageBytes, k = (k + 1) % kStages) {
+    const size_t n = std::min(kStageBytes, bytes - o);
+    cuda_check(cudaEventSynchronize(stage_ev_[k]), "stage wait");  // the chunk's previous DMA is done
+    par_memcpy(ring + k * kStageBytes, (const char*)src + o, n);
+    cuda_check(cudaMemcpyAsync((char*)dst + o, ring + k * kStageBytes, n, cudaMemcpyHostToDevice, st_), "copy in");
+    cudaEventRecord(stage_ev_[k], st_);
+  }
+}
+
+void Context::copy_out(void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return;
+  if (!is_pageable(dst) || bytes <= kStageBytes) {
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st_), "copy out");
+    return;
+  }
+  stage_events();
+  char* ring = (char*)pinned_.get("stage", kStages * kStageBytes);
+  const size_t nch = (bytes + kStageBytes - 1) / kStageBytes;
+  auto issue = [&](size_t c) {
+    const size_t o = c * kStageBytes, n = std::min(kStageBytes, bytes - o);
+    cuda_check(cudaMemcpyAsync(ring + (c % kStages) * kStageBytes, (const char*)src + o, n, cudaMemcpyDeviceToHost, st_),
+               "copy out");
+    cudaEventRecord(stage_ev_[c % kStages], st_);
+  };
+  for (size_t c = 0; c < std::min<size_t>(nch, kStages - 1); ++c) issue(c);
+  for (size_t c = 0; c < nch; ++c) {
+    if (c + kStages - 1 < nch) issue(c + kStages - 1);  // keep the copy engine busy
+    cuda_check(cudaEventSynchronize(stage_ev_[c % kStages]), "stage wait");
+    const size_t o = c * kStageBytes, n = std::min(kStageBytes, bytes - o);
+    par_memcpy((char*)dst + o, ring + (c % kStages) * kStageBytes, n);
+  }
+}
 
 void Context::set_shard(int rank, int nranks) {
   if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("set_shard: need 0 <= rank < nranks");
@@ -1013,16 +1094,10 @@ void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, in
   const int sc = strength_width(P.kernel, dim);
   const bool alias = nt == 0;
   const int ntt = alias ? (int)ns : (int)nt;
-  cudaMemcpyKind kind = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   cudaEventRecord(ev_[0], st_);
-  cuda_check(cudaMemcpyAsync(arena_.as<double>("src_in", (size_t)ns * dim), src, sizeof(double) * ns * dim, kind, st_),
-             "copy sources");
-  if (!alias)
-    cuda_check(
-        cudaMemcpyAsync(arena_.as<double>("tgt_in", (size_t)nt * dim), tgt, sizeof(double) * nt * dim, kind, st_),
-        "copy targets");
-  cuda_check(cudaMemcpyAsync(arena_.as<double>("str_in", (size_t)ns * sc), str, sizeof(double) * ns * sc, kind, st_),
-             "copy strengths");
+  copy_in(arena_.as<double>("src_in", (size_t)ns * dim), src, sizeof(double) * ns * dim, device_ptrs);
+  if (!alias) copy_in(arena_.as<double>("tgt_in", (size_t)nt * dim), tgt, sizeof(double) * nt * dim, device_ptrs);
+  copy_in(arena_.as<double>("str_in", (size_t)ns * sc), str, sizeof(double) * ns * sc, device_ptrs);
   cudaEventRecord(ev_[1], st_);
   build_problem(P, dim, (int)ns, (int)nt, mode, true);
   cudaEventRecord(ev_[2], st_);
@@ -1067,8 +1142,7 @@ void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, in
   launch_combine(ntt, dim, ufar, ures, corr, corr_scale, zm, pr.tpts_caller, own, du, st_);
   ++launches_;
   cudaEventRecord(ev_[6], st_);
-  if (!device_ptrs)
-    cuda_check(cudaMemcpyAsync(u, du, sizeof(double) * ntt * dim, cudaMemcpyDeviceToHost, st_), "copy u");
+  if (!device_ptrs) copy_out(u, du, sizeof(double) * ntt * dim);
   cudaEventRecord(ev_[7], st_);
   int* hflags = (int*)pinned_.get("hflags", 64);
   cuda_check(cudaMemcpyAsync(hflags, arena_.as<int>("flags", 8), 8 * sizeof(int), cudaMemcpyDeviceToHost, st_),

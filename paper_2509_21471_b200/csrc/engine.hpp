@@ -134,6 +134,10 @@ class Context {
   GridDev& grid(GridDev& cache, const std::string& name, int dim, int p, int N, double theta, double band_r2);
   void sync();
   double ev_ms(int a, int b);
+  void copy_in(void* dst, const void* src, size_t bytes, bool device_ptrs);
+  void copy_out(void* dst, const void* src, size_t bytes);
+  void stage_events();
+  std::vector<cudaEvent_t> stage_ev_;
 
   int device_;
   cudaStream_t st_ = nullptr;
