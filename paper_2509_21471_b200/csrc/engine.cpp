@@ -697,7 +697,7 @@ void Context::upload_tree_lists_b(const int32_t* qs) {
   // per-level lists
   const int L = t.max_level + 1;
   struct LV {
-    std::vector<int> i_in, i_out, i_ci, sbx, tbx, es, eslot, etau, gstart, gslot, tmeta;
+    std::vector<int> i_in, i_out, i_ci, i_seg, sbx, tbx, es, eslot, etau, gstart, gslot, tmeta;
   };
   std::vector<LV> lv(L);
   const bool use_groups = !std::getenv("SDMK_NO_GROUP");
@@ -707,7 +707,8 @@ void Context::upload_tree_lists_b(const int32_t* qs) {
     LV& V = lv[lev];
     for (int b : t.level_boxes[lev]) {
       const Box& x = t.boxes[b];
-      if (!x.leaf && t.ntgt(b) > 0)  // downward interpolation (dmk.cpp:840-853)
+      if (!x.leaf && t.ntgt(b) > 0) {  // downward interpolation (dmk.cpp:840-853)
+        const int first = (int)V.i_in.size();
         for (int ci = 0; ci < nchild; ++ci) {
           int c = x.first_child + ci;
           if (t.ntgt(c) == 0 || !need[c]) continue;
@@ -715,6 +716,8 @@ void Context::upload_tree_lists_b(const int32_t* qs) {
           V.i_out.push_back(c);
           V.i_ci.push_back(ci);
         }
+        if ((int)V.i_in.size() > first) V.i_seg.push_back(first);  // this parent's pairs
+      }
       if (t.nsrc(b) > 0) {
         gslot[b] = (int)V.sbx.size();
         V.sbx.push_back(b);
@@ -792,13 +795,15 @@ void Context::upload_tree_lists_b(const int32_t* qs) {
   size_t o_itp = pk.add(itp), o_rs = pk.add(rs), o_rbox = pk.add(rbox), o_rinfo = pk.add(rinfo),
          o_rid = pk.add(root_ids), o_res = pk.add(root_es), o_rsl = pk.add(root_slot), o_rta = pk.add(root_tau);
   struct Off {
-    size_t i_in, i_out, i_ci, sbx, tbx, es, eslot, etau, gstart, gslot, tmeta;
+    size_t i_in, i_out, i_ci, i_seg, sbx, tbx, es, eslot, etau, gstart, gslot, tmeta;
   };
   std::vector<Off> off(L);
   for (int lev = 0; lev < L; ++lev) {
     LV& V = lv[lev];
-    off[lev] = {pk.add(V.i_in), pk.add(V.i_out), pk.add(V.i_ci),   pk.add(V.sbx),   pk.add(V.tbx),  pk.add(V.es),
-                pk.add(V.eslot), pk.add(V.etau), pk.add(V.gstart), pk.add(V.gslot), pk.add(V.tmeta)};
+    V.i_seg.push_back((int)V.i_in.size());
+    off[lev] = {pk.add(V.i_in),  pk.add(V.i_out),  pk.add(V.i_ci),   pk.add(V.i_seg),
+                pk.add(V.sbx),   pk.add(V.tbx),    pk.add(V.es),     pk.add(V.eslot),
+                pk.add(V.etau),  pk.add(V.gstart), pk.add(V.gslot),  pk.add(V.tmeta)};
   }
   char* h = (char*)pinned_.get("treeB", pk.total + 64);
   for (auto& it : pk.items)
@@ -822,6 +827,8 @@ void Context::upload_tree_lists_b(const int32_t* qs) {
     X.interp_in = (int*)(dv + off[lev].i_in);
     X.interp_out = (int*)(dv + off[lev].i_out);
     X.interp_ci = (int*)(dv + off[lev].i_ci);
+    X.interp_seg = (int*)(dv + off[lev].i_seg);
+    X.n_interp_seg = (int)V.i_seg.size() - 1;
     X.src_boxes = (int*)(dv + off[lev].sbx);
     X.tgt_boxes = (int*)(dv + off[lev].tbx);
     X.ent_start = (int*)(dv + off[lev].es);
@@ -981,7 +988,11 @@ void Context::run_downward() {  // dmk.cpp:705-857
     }
     if (X.n_interp > 0) {
       if (tensor_mma_supported(p, d))
-        launch_tensor_mma(p, mats_down_, X.interp_in, X.interp_out, X.interp_ci, X.n_interp, d, in, in, 1, d, st_);
+        if (tensor_seg_supported(p, d))
+          launch_tensor_mma_seg(p, mats_down_, X.interp_in, X.interp_out, X.interp_ci, X.interp_seg, X.n_interp_seg,
+                                d, in, in, st_);
+        else
+          launch_tensor_mma(p, mats_down_, X.interp_in, X.interp_out, X.interp_ci, X.n_interp, d, in, in, 3, d, st_);
       else
         launch_tensor_apply(p, pz, d, mats_down_, X.interp_in, X.interp_out, X.interp_ci, X.n_interp, d, in, in, 1,
                             st_);

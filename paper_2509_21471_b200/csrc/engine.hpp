@@ -83,7 +83,8 @@ struct Problem {
   struct LevelLists {
     int n_merge = 0, n_interp = 0, n_src = 0, n_tgt = 0;
     int *merge_out = nullptr, *merge_in = nullptr, *merge_ci = nullptr;
-    int *interp_in = nullptr, *interp_out = nullptr, *interp_ci = nullptr;
+    int *interp_in = nullptr, *interp_out = nullptr, *interp_ci = nullptr, *interp_seg = nullptr;
+    int n_interp_seg = 0;
     int *src_boxes = nullptr, *tgt_boxes = nullptr;
     int *ent_start = nullptr, *ent_slot = nullptr, *ent_tau = nullptr;
     int max_entries = 0;

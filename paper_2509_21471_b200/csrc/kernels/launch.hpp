@@ -82,6 +82,13 @@ void launch_tensor_apply(int p, int pz, int dim, const double* mats, const int* 
 
 // ---- tensor_mma.cu: DMMA version of the above (3D, p <= 32) ----
 bool tensor_mma_supported(int p, int dim);
+// Downward interpolation by parent segment: pairs seg[k]..seg[k+1]-1 share one
+// parent (in_list), each adds into its own child (out_box) -- one CTA per
+// (segment, channel), so the per-CTA setup and the input prefetch pipeline
+// are shared by the parent's children.  3D, p = 17..24.
+bool tensor_seg_supported(int p, int dim);
+void launch_tensor_mma_seg(int p, const double* mats, const int* in_list, const int* out_box, const int* ci,
+                           const int* seg, int nseg, int nch, const double* src, double* dst, cudaStream_t st);
 void launch_tensor_mma(int p, const double* mats, const int* in_list, const int* out_box, const int* ci,
                        int npairs, int nch, const double* src, double* dst, int accumulate, int dim,
                        cudaStream_t st);

@@ -210,7 +210,8 @@ template <int PC>
 __global__ void __launch_bounds__(kT3W * 32, 1)
     k_tensor3(int p_rt, const double* __restrict__ mats, const int* __restrict__ in_list,
               const int* __restrict__ out_box, const int* __restrict__ ci_list, int nin, int nch,
-              const double* __restrict__ src, double* __restrict__ dst, int accumulate) {
+              const double* __restrict__ src, double* __restrict__ dst, int accumulate,
+              const int* __restrict__ seg) {
   constexpr int PT = 3, P8 = 24, SA = 28, S1 = 28, SG = kT3SG, NWp = kT3W;
   const int p = PC > 0 ? PC : p_rt;
   const int pp = p * p, nodes = p * pp;
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(kT3W * 32, 1)
   const int SS = NN * 8 + 4;                 // T2 row stride (== 4 mod 8)
   constexpr int ZN = (9 * 8 + NWp - 1) / NWp; // max column tiles per warp (p <= 24: NN <= 72)
   extern __shared__ double sm[];
-  __shared__ int s_in[8], s_ci[8], s_nq;
+  __shared__ int s_in[8], s_ci[8], s_out[8], s_nq;
   double* Mm = sm;                       // [2][P8][SA]
   double* T1 = Mm + 2 * P8 * SA;         // [SG * P8][S1]
   double* T2 = T1 + SG * P8 * S1;        // [SG][SS]
@@ -231,12 +232,21 @@ __global__ void __launch_bounds__(kT3W * 32, 1)
   const int pair = blockIdx.x, ch = blockIdx.y;
   if (tid == 0) {
     int nq = 0;
-    for (int q = 0; q < nin; ++q) {
-      const int ib = in_list[pair * nin + q];
-      if (ib >= 0) {
-        s_in[nq] = ib;
-        s_ci[nq] = ci_list[pair * nin + q];
+    if (seg) {  // downward: one parent, its children (one output each) in this segment
+      for (int q = seg[pair]; q < seg[pair + 1]; ++q) {
+        s_in[nq] = in_list[q];
+        s_ci[nq] = ci_list[q];
+        s_out[nq] = out_box[q];
         ++nq;
+      }
+    } else {
+      for (int q = 0; q < nin; ++q) {
+        const int ib = in_list[pair * nin + q];
+        if (ib >= 0) {
+          s_in[nq] = ib;
+          s_ci[nq] = ci_list[pair * nin + q];
+          ++nq;
+        }
       }
     }
     s_nq = nq;
@@ -350,25 +360,30 @@ __global__ void __launch_bounds__(kT3W * 32, 1)
     }
     // the next group's x stage rewrites T1 only (read by this y stage, fenced
     // by the barrier above); its y stage rewrites T2 after the next barrier
-  }
-  double* out = dst + ((size_t)out_box[pair] * nch + ch) * nodes;
+    const bool last = seg ? (item % ngroups == ngroups - 1) : (item == nitems - 1);
+    if (last) {
+      double* out = dst + ((size_t)(seg ? s_out[q] : out_box[pair]) * nch + ch) * nodes;
 #pragma unroll
-  for (int i = 0; i < ZN; ++i) {
-    const int nt = warp + NWp * i;
-    if (nt >= NN) continue;
+      for (int i = 0; i < ZN; ++i) {
+        const int nt = warp + NWp * i;
+        if (nt >= NN) continue;
 #pragma unroll
-    for (int m = 0; m < PT; ++m) {
-      const int iz = m * 8 + g, n = nt * 8 + 2 * t;
-      if (iz >= p) continue;
+        for (int m = 0; m < PT; ++m) {
+          const int iz = m * 8 + g, n = nt * 8 + 2 * t;
+          if (iz >= p) continue;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        if (n + e < pp) {
-          double* o = out + (size_t)iz * pp + n + e;
-          *o = accumulate ? *o + acc[i][m][e] : acc[i][m][e];
+          for (int e = 0; e < 2; ++e) {
+            if (n + e < pp) {
+              double* o = out + (size_t)iz * pp + n + e;
+              *o = accumulate ? *o + acc[i][m][e] : acc[i][m][e];
+            }
+            acc[i][m][e] = 0.0;  // the next child (downward) starts from zero
+          }
         }
       }
     }
   }
+
 }
 
 // PT = 4 (p = 25..32): the same schedule with the output's ix columns split
@@ -561,7 +576,8 @@ void tensor3_t(int p, const double* mats, const int* in_list, const int* out_box
     attr = true;
   }
   dim3 grid(npairs, nch);
-  k_tensor3<PC><<<grid, kT3W * 32, smem, st>>>(p, mats, in_list, out_box, ci, nin, nch, src, dst, accumulate);
+  k_tensor3<PC><<<grid, kT3W * 32, smem, st>>>(p, mats, in_list, out_box, ci, nin, nch, src, dst, accumulate,
+                                                nullptr);
 }
 
 template <int PC, int PT, int NW, int ZT>
@@ -580,14 +596,40 @@ void tensor_mma_t(int p, const double* mats, const int* in_list, const int* out_
                                                              accumulate);
 }
 
+template <int PC>
+void tensor3_seg_t(int p, const double* mats, const int* in_list, const int* out_box, const int* ci, const int* seg,
+                   int nseg, int nch, const double* src, double* dst, cudaStream_t st) {
+  const int NN = (p * p + 7) / 8;
+  const size_t smem = sizeof(double) * (2 * 24 * 28 + kT3SG * 24 * 28 + kT3SG * (NN * 8 + 4));
+  cudaFuncSetAttribute(k_tensor3<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  dim3 grid(nseg, nch);
+  // write, not add: a child's incoming receives nothing before its parent's
+  // interpolation (its own plane waves come at the next level), so the RMW
+  // of the reference's "+=" (dmk.cpp:850) is an add to exact zeros
+  k_tensor3<PC><<<grid, kT3W * 32, smem, st>>>(p, mats, in_list, out_box, ci, 1, nch, src, dst, 0, seg);
+}
+
 }  // namespace
+
+bool tensor_seg_supported(int p, int dim) { return dim == 3 && p >= 17 && p <= 24 && !std::getenv("SDMK_TENSOR_OLD"); }
+
+void launch_tensor_mma_seg(int p, const double* mats, const int* in_list, const int* out_box, const int* ci,
+                           const int* seg, int nseg, int nch, const double* src, double* dst, cudaStream_t st) {
+  if (nseg <= 0) return;
+  if (p == 23) tensor3_seg_t<23>(p, mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
+  else if (p == 22) tensor3_seg_t<22>(p, mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
+  else tensor3_seg_t<0>(p, mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
+}
+
 
 bool tensor_mma_supported(int p, int dim) { return dim == 3 && p >= 4 && p <= 32; }
 
 void launch_tensor_mma(int p, const double* mats, const int* in_list, const int* out_box, const int* ci, int npairs,
                        int nch, const double* src, double* dst, int accumulate, int dim, cudaStream_t st) {
   if (npairs <= 0) return;
-  const int nin = accumulate >= 2 ? (1 << dim) : 1;
+  // accumulate: 1 dst += (one input per pair), 2 merge (2^d inputs, dst =),
+  // 3 one input per pair, dst = (downward interpolation into zeroed children)
+  const int nin = accumulate == 2 ? (1 << dim) : 1;
   const int acc = accumulate == 1 ? 1 : 0;
   const int PT = (p + 7) / 8;
 #define TM(PC_, PT_, NW_, ZT_) \
