@@ -853,7 +853,10 @@ void Context::run_upward() {  // dmk.cpp:555-655
   const size_t nodes = (size_t)pz * p * p;
   const int nb = pr.tree.num_boxes();
   double* og = arena_.as<double>("outgoing", (size_t)nb * pr.nch * nodes);
-  cuda_check(cudaMemsetAsync(og, 0, sizeof(double) * nb * pr.nch * nodes, st_), "memset outgoing");
+  // outgoing of a box without sources is never read (forward transforms and
+  // merges skip them), so evaluate() skips the 10 GB-scale memset; the
+  // pass-level API returns whole arrays and keeps the reference's zeros
+  if (zero_all_) cuda_check(cudaMemsetAsync(og, 0, sizeof(double) * nb * pr.nch * nodes, st_), "memset outgoing");
   ChebDev cb{p, pz, d, cheb_nodes_, cheb_wts_};
   if (mma_anterp_supported(p)) {
     double* basis = arena_.as<double>("basis_s", (size_t)3 * pr.ns * p);
@@ -883,7 +886,13 @@ void Context::run_root() {  // dmk.cpp:657-701
   const size_t nodes = (size_t)pz * p * p;
   const int nb = pr.tree.num_boxes();
   double* in = arena_.as<double>("incoming", (size_t)nb * d * nodes);
-  cuda_check(cudaMemsetAsync(in, 0, sizeof(double) * nb * d * nodes, st_), "memset incoming");
+  // every non-root box with targets is first written by its parent's
+  // interpolation (DMMA path, write mode), so only the root needs zeros
+  // unless whole arrays are returned or the FFMA fallback accumulates
+  if (zero_all_ || !tensor_mma_supported(p, d))
+    cuda_check(cudaMemsetAsync(in, 0, sizeof(double) * nb * d * nodes, st_), "memset incoming");
+  else
+    cuda_check(cudaMemsetAsync(in, 0, sizeof(double) * d * nodes, st_), "memset incoming");
   const int N = pr.periodic ? P.N_per : P.N1;
   const double h = pr.periodic ? 2.0 * PI : PI / 3.0;
   const int M = (N - 1) / 2;
@@ -1112,6 +1121,11 @@ void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, in
   cudaEventRecord(ev_[1], st_);
   build_problem(P, dim, (int)ns, (int)nt, mode, true);
   cudaEventRecord(ev_[2], st_);
+  zero_all_ = false;  // only the evaluated outputs are returned
+  struct Restore {
+    bool& f;
+    ~Restore() { f = true; }
+  } restore{zero_all_};
   run_upward();
   cudaEventRecord(ev_[3], st_);
   upload_tree_lists_b(hq_);  // host work overlaps the upward pass on the GPU

@@ -156,6 +156,7 @@ class Context {
   int pw_used_ = 0;
   double planewave_ms();
   int rank_ = 0, nranks_ = 1;
+  bool zero_all_ = true;  // zero whole proxy arrays (pass-level API returns them)
   const int32_t* hq_ = nullptr;  // pinned sorted quantized coordinates of the current problem
   unsigned long long stats_[3] = {0, 0, 0};
 };
