@@ -546,10 +546,10 @@ __global__ void __launch_bounds__(kW * 32, 2) k_zi2(PWGrid g, int nc, int nbox, 
     const int bc = w / ncbk, c0 = (w % ncbk) * kCB;
     const double2* src = IN + (size_t)bc * g.nhalf;
     double2* dst = Fs + buf * NZ * FR;
-    for (int e = tid; e < NZ * kCB; e += blockDim.x) {
-      const int s = e / kCB, cc = e % kCB, col = c0 + cc;
-      const bool v = col < g.slab_ncol[s];
-      dev::cp_async16z(dst + s * FR + cc, v ? src + g.slab_off[s] + col : src, v);
+    for (int s = warp; s < NZ; s += kW) {  // a warp per mz row: one band lookup per row
+      const int nvalid = g.slab_ncol[s] - c0;
+      const double2* row = src + g.slab_off[s] + c0;
+      for (int cc = lane; cc < kCB; cc += 32) dev::cp_async16z(dst + s * FR + cc, cc < nvalid ? row + cc : src, cc < nvalid);
     }
     cp_commit();
   };
