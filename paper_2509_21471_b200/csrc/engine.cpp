@@ -455,13 +455,11 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
     pr.tpts = pr.spts;
     pr.tpts_caller = src;
   }
-  // quantized coordinates -> host for the box topology
-  int32_t* hq = (int32_t*)pinned_.get("hq", sizeof(int32_t) * ((size_t)ns + (pr.alias ? 0 : nt)) * d + 64);
+  // The box topology is built on the host from the GPU-sorted points, which
+  // stay on the device: the refine asks the GPU for child boundaries one level
+  // at a time; the quantized coordinates come to the host only if the 2:1
+  // repair must subdivide a leaf.
   int* hflags = (int*)pinned_.get("hflags", 64);
-  cuda_check(cudaMemcpyAsync(hq, sq, sizeof(int32_t) * (size_t)ns * d, cudaMemcpyDeviceToHost, st_), "D2H q");
-  if (!pr.alias)
-    cuda_check(cudaMemcpyAsync(hq + (size_t)ns * d, tq, sizeof(int32_t) * (size_t)nt * d, cudaMemcpyDeviceToHost, st_),
-               "D2H q");
   cuda_check(cudaMemcpyAsync(hflags, flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H flags");
   const auto w0 = std::chrono::steady_clock::now();
   sync();
@@ -469,13 +467,46 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
   if (hflags[2]) throw InvalidArgument("ParticleSystem: non-finite strength");
   if (hflags[0]) throw InvalidArgument("ParticleSystem: non-finite coordinate");
   if (hflags[1]) throw InvalidArgument("ParticleSystem: coordinate outside the unit box");
-  pr.tree = build_topology(d, pr.periodic, P.n_s, P.p, ns, hq, pr.alias ? 0 : nt,
-                           pr.alias ? nullptr : hq + (size_t)ns * d);
+  pr.sq = sq;
+  pr.tq = tq;
+  hq_ = nullptr;
+  PointAccess pa;
+  pa.split = [&](int n, const int* lvl, const int* srng, const int* trng, int* sbnd, int* tbnd) {
+    const size_t in_bytes = sizeof(int) * (size_t)n * 5, out_bytes = sizeof(int) * (size_t)n * 18;
+    int* h = (int*)pinned_.get("split", in_bytes + out_bytes + 256);
+    std::memcpy(h, lvl, sizeof(int) * n);
+    std::memcpy(h + n, srng, sizeof(int) * 2 * n);
+    std::memcpy(h + 3 * n, trng, sizeof(int) * 2 * n);
+    int* dvb = (int*)arena_.get("split", in_bytes + out_bytes + 256);
+    cuda_check(cudaMemcpyAsync(dvb, h, in_bytes, cudaMemcpyHostToDevice, st_), "split upload");
+    int* dout = dvb + 5 * n;
+    launch_split_ranges(n, dvb, dvb + n, sq, ns, d, dout, st_);
+    if (!pr.alias) launch_split_ranges(n, dvb, dvb + 3 * n, tq, nt, d, dout + 9 * n, st_);
+    launches_ += pr.alias ? 1 : 2;
+    int* hout = h + 5 * n;
+    cuda_check(cudaMemcpyAsync(hout, dout, sizeof(int) * (size_t)n * (pr.alias ? 9 : 18), cudaMemcpyDeviceToHost, st_),
+               "split download");
+    sync();
+    std::memcpy(sbnd, hout, sizeof(int) * (size_t)n * 9);
+    if (!pr.alias) std::memcpy(tbnd, hout + 9 * n, sizeof(int) * (size_t)n * 9);
+  };
+  pa.host_q = [&](const int32_t** qs_out, const int32_t** qt_out) {
+    int32_t* hq = (int32_t*)pinned_.get("hq", sizeof(int32_t) * ((size_t)ns + (pr.alias ? 0 : nt)) * d + 64);
+    cuda_check(cudaMemcpyAsync(hq, sq, sizeof(int32_t) * (size_t)ns * d, cudaMemcpyDeviceToHost, st_), "D2H q");
+    if (!pr.alias)
+      cuda_check(
+          cudaMemcpyAsync(hq + (size_t)ns * d, tq, sizeof(int32_t) * (size_t)nt * d, cudaMemcpyDeviceToHost, st_),
+          "D2H q");
+    sync();
+    hq_ = hq;
+    *qs_out = hq;
+    *qt_out = pr.alias ? nullptr : hq + (size_t)ns * d;
+  };
+  pr.tree = build_topology(d, pr.periodic, P.n_s, P.p, ns, pr.alias ? 0 : nt, pa);
   const auto w2 = std::chrono::steady_clock::now();
-  hq_ = hq;
   pr.lists_b = false;
   upload_tree_lists_a();
-  if (!defer_lists) upload_tree_lists_b(hq);
+  if (!defer_lists) upload_tree_lists_b();
   const auto w3 = std::chrono::steady_clock::now();
   if (timing_on()) {
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
@@ -646,7 +677,7 @@ void Context::upload_tree_lists_a() {
   }
 }
 
-void Context::upload_tree_lists_b(const int32_t* qs) {
+void Context::upload_tree_lists_b() {
   Problem& pr = prob_;
   const HostTree& t = pr.tree;
   const int nb = t.num_boxes(), d = pr.dim, nchild = 1 << d;
@@ -788,9 +819,6 @@ void Context::upload_tree_lists_b(const int32_t* qs) {
     }
   }
   Packer pk;
-  std::vector<int> subr;
-  leaf_subranges(t, pr.ns, qs, subr);  // source sub-cells for the residual cull
-  size_t o_sub = pk.add(subr);
   size_t o_chunks = pk.add(chunks);
   size_t o_itp = pk.add(itp), o_rs = pk.add(rs), o_rbox = pk.add(rbox), o_rinfo = pk.add(rinfo),
          o_rid = pk.add(root_ids), o_res = pk.add(root_es), o_rsl = pk.add(root_slot), o_rta = pk.add(root_tau);
@@ -815,7 +843,10 @@ void Context::upload_tree_lists_b(const int32_t* qs) {
   pr.rng_start = (int*)(dv + o_rs);
   pr.rng_box = (int*)(dv + o_rbox);
   pr.rng_info = (int*)(dv + o_rinfo);
-  pr.subrange = (int*)(dv + o_sub);
+  // source sub-cells for the residual cull, from the device-resident points
+  pr.subrange = arena_.as<int>("subrange", (size_t)nb * 9);
+  launch_leaf_subranges(pr.boxes, nb, pr.sq, pr.ns, d, pr.subrange, st_);
+  ++launches_;
   pr.res_chunks = (int*)(dv + o_chunks);
   pr.n_chunks = (int)(chunks.size() / 2);
   for (int lev = 0; lev < L; ++lev) {
@@ -1128,7 +1159,7 @@ void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, in
   } restore{zero_all_};
   run_upward();
   cudaEventRecord(ev_[3], st_);
-  upload_tree_lists_b(hq_);  // host work overlaps the upward pass on the GPU
+  upload_tree_lists_b();  // host work overlaps the upward pass on the GPU
   run_root();
   cudaEventRecord(ev_[4], st_);
   double* ufar = arena_.as<double>("ufar", (size_t)ntt * dim);

@@ -71,6 +71,7 @@ struct Problem {
   // device views (arena-owned)
   double *spts = nullptr, *sstr = nullptr, *tpts = nullptr, *tpts_caller = nullptr;
   int *sperm = nullptr, *tperm = nullptr;
+  const int32_t *sq = nullptr, *tq = nullptr;  // sorted quantized coordinates (device, SoA)
   // tree lists on device
   dev::DBox* boxes = nullptr;
   int *ant_leaves = nullptr, *int_leaves = nullptr;
@@ -126,7 +127,7 @@ class Context {
   // inputs already in the arena ("src_in", "tgt_in", "str_in"): validate, wrap, sort, topology, upload
   void build_problem(const Plan& plan, int dim, int ns, int nt, int mode, bool defer_lists = false);
   void upload_tree_lists_a();
-  void upload_tree_lists_b(const int32_t* qs);
+  void upload_tree_lists_b();
   void run_upward();
   void run_root();
   void run_downward();

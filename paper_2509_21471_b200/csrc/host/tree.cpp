@@ -31,6 +31,15 @@ struct Builder {
   HostTree t;
   Points S, T;
   int nchild = 8;
+  const PointAccess* pa = nullptr;  // device-resident points (null: S / T are host arrays)
+
+  void need_host_points() {  // the repair subdivides on the host
+    if (S.q || !pa) return;
+    const int32_t *qs = nullptr, *qt = nullptr;
+    pa->host_q(&qs, &qt);
+    S.q = qs;
+    T.q = qt;
+  }
 
   // child boundaries of [lo, hi) by binary search on the (monotone) child index
   void split_range(const Points& P, int lo, int hi, int level, int* bnd) const {
@@ -68,6 +77,7 @@ struct Builder {
   }
 
   void subdivide(int b) {
+    need_host_points();
     int sb[9], tb[9];
     split_range(S, t.boxes[b].sb, t.boxes[b].se, t.boxes[b].level, sb);
     if (t.alias)
@@ -103,20 +113,49 @@ struct Builder {
     while (!cur.empty()) {
       const int nc = (int)cur.size();
       std::vector<char> split(nc, 0);
-#pragma omp parallel for schedule(dynamic, 16) reduction(|| : capped)
-      for (int i = 0; i < nc; ++i) {
-        Node& nd = nodes[cur[i]];
-        if (nd.box.se - nd.box.sb <= t.n_s) continue;
-        if (nd.box.level >= kMaxLevel) {
-          capped = true;
-          continue;
+      if (pa) {  // one batched call per level for the boxes that split
+        std::vector<int> which, lvl, sr, tr;
+        for (int i = 0; i < nc; ++i) {
+          const Node& nd = nodes[cur[i]];
+          if (nd.box.se - nd.box.sb <= t.n_s) continue;
+          if (nd.box.level >= kMaxLevel) {
+            capped = true;
+            continue;
+          }
+          split[i] = 1;
+          which.push_back(i);
+          lvl.push_back(nd.box.level);
+          sr.push_back(nd.box.sb);
+          sr.push_back(nd.box.se);
+          tr.push_back(nd.box.tb);
+          tr.push_back(nd.box.te);
         }
-        split[i] = 1;
-        split_range(S, nd.box.sb, nd.box.se, nd.box.level, nd.sb);
-        if (t.alias)
-          for (int k = 0; k <= nchild; ++k) nd.tb[k] = nd.sb[k];
-        else
-          split_range(T, nd.box.tb, nd.box.te, nd.box.level, nd.tb);
+        const int nw = (int)which.size();
+        std::vector<int> sbv((size_t)nw * 9), tbv((size_t)nw * 9);
+        if (nw) pa->split(nw, lvl.data(), sr.data(), tr.data(), sbv.data(), tbv.data());
+        for (int k = 0; k < nw; ++k) {
+          Node& nd = nodes[cur[which[k]]];
+          for (int c = 0; c <= nchild; ++c) {
+            nd.sb[c] = sbv[(size_t)k * 9 + c];
+            nd.tb[c] = t.alias ? nd.sb[c] : tbv[(size_t)k * 9 + c];
+          }
+        }
+      } else {
+#pragma omp parallel for schedule(dynamic, 16) reduction(|| : capped)
+        for (int i = 0; i < nc; ++i) {
+          Node& nd = nodes[cur[i]];
+          if (nd.box.se - nd.box.sb <= t.n_s) continue;
+          if (nd.box.level >= kMaxLevel) {
+            capped = true;
+            continue;
+          }
+          split[i] = 1;
+          split_range(S, nd.box.sb, nd.box.se, nd.box.level, nd.sb);
+          if (t.alias)
+            for (int k = 0; k <= nchild; ++k) nd.tb[k] = nd.sb[k];
+          else
+            split_range(T, nd.box.tb, nd.box.te, nd.box.level, nd.tb);
+        }
       }
       std::vector<int> next;
       for (int i = 0; i < nc; ++i) {
@@ -415,9 +454,10 @@ std::array<double, 3> HostTree::center(int b) const {  // tree.cpp:221-228
   return c;
 }
 
-HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, const int32_t* qs, int nt,
-                        const int32_t* qt) {
+static HostTree build_topology_impl(int dim, bool periodic, int n_s, int p, int ns, const int32_t* qs, int nt,
+                                    const int32_t* qt, const PointAccess* pa) {
   Builder B;
+  B.pa = pa;
   B.t.dim = dim;
   B.t.periodic = periodic;
   B.t.n_s = n_s;
@@ -448,6 +488,15 @@ HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, const in
     std::fprintf(stderr, "build_tree: depth cap %d reached with leaves above capacity (duplicate points?)\n",
                  kMaxLevel);
   return std::move(B.t);
+}
+
+HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, const int32_t* qs, int nt,
+                        const int32_t* qt) {
+  return build_topology_impl(dim, periodic, n_s, p, ns, qs, nt, qt, nullptr);
+}
+
+HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, int nt, const PointAccess& pa) {
+  return build_topology_impl(dim, periodic, n_s, p, ns, nullptr, nt, nullptr, &pa);
 }
 
 void leaf_subranges(const HostTree& t, int ns, const int32_t* qs, std::vector<int>& out) {

@@ -19,6 +19,7 @@
 
 #include <array>
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -70,6 +71,18 @@ struct HostTree {
 // means the targets alias the sources.
 HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, const int32_t* qs, int nt,
                         const int32_t* qt);
+
+// The same with the point data kept elsewhere (the GPU): `split` gives, for
+// n boxes (level lvl[i], source range src[2i..2i+1], target range
+// tgt[2i..2i+1]), the 2^d + 1 child boundaries of each range (sb[9i..],
+// tb[9i..]); the refine calls it once per level.  `host_q` returns host
+// copies of the sorted quantized coordinates; it is called only if the 2:1
+// repair has to subdivide a leaf (never for uniform inputs).
+struct PointAccess {
+  std::function<void(int n, const int* lvl, const int* src, const int* tgt, int* sb, int* tb)> split;
+  std::function<void(const int32_t** qs, const int32_t** qt)> host_q;
+};
+HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, int nt, const PointAccess& pa);
 
 // The reference's canonical text dump (tree.cpp:325-354).
 std::string dump_topology(const HostTree& t);

@@ -43,6 +43,14 @@ void launch_gather_points(const double* pts, const int* perm, int n, int dim, do
 // AoS caller-order strengths -> SoA sorted strengths (sc components).
 void launch_gather_strengths(const double* str, const int* perm, int n, int sc, double* soa,
                              cudaStream_t st);
+// Child boundaries of nbox Morton-sorted ranges (rng[2i], rng[2i+1]) at
+// levels lvl[i]: bnd[9i + c], c = 0..2^d (tree.cpp:38-43, 109-123).
+void launch_split_ranges(int nbox, const int* lvl, const int* rng, const int32_t* q, int n, int dim, int* bnd,
+                         cudaStream_t st);
+// The residual's source sub-cells: 9 boundaries per box (children of leaves
+// with sources, else [sb, se) once), as host/tree.hpp leaf_subranges.
+void launch_leaf_subranges(const dev::DBox* boxes, int nb, const int32_t* q, int n, int dim, int* out,
+                           cudaStream_t st);
 
 // ---- anterp.cu (K3 leaf anterpolation, K11 target interpolation) -----------
 struct ChebDev {

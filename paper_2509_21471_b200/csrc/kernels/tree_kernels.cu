@@ -4,6 +4,8 @@
 #include "common.cuh"
 #include "launch.hpp"
 
+#include <algorithm>
+
 namespace sdmkb {
 
 namespace {
@@ -134,6 +136,65 @@ void launch_gather_points(const double* pts, const int* perm, int n, int dim, do
 
 void launch_gather_strengths(const double* str, const int* perm, int n, int sc, double* soa, cudaStream_t st) {
   k_gather_strengths<<<(n + 255) / 256, 256, 0, st>>>(str, perm, n, sc, soa);
+}
+
+// ---- box splitting on the device (the refine of tree.cpp:109-123 and the
+// residual's child sub-ranges) ----------------------------------------------
+namespace {
+__device__ __forceinline__ int child_index(const int32_t* __restrict__ q, int n, int m, int level, int dim) {
+  int ci = 0;
+  for (int a = 0; a < dim; ++a) ci |= ((q[(size_t)a * n + m] >> (29 - level)) & 1) << a;
+  return ci;
+}
+
+// first m in [lo, hi) whose child index at `level` is >= c (indices are
+// non-decreasing inside a box's Morton-sorted range)
+__device__ __forceinline__ int lower_child(const int32_t* __restrict__ q, int n, int lo, int hi, int level, int dim,
+                                           int c) {
+  int a = lo, b = hi;
+  while (a < b) {
+    const int m = a + (b - a) / 2;
+    if (child_index(q, n, m, level, dim) < c) a = m + 1;
+    else b = m;
+  }
+  return a;
+}
+
+__global__ void k_split_ranges(int nbox, const int* __restrict__ lvl, const int* __restrict__ rng,
+                               const int32_t* __restrict__ q, int n, int dim, int* __restrict__ bnd) {
+  const int nchild = 1 << dim;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nbox * (nchild + 1); e += gridDim.x * blockDim.x) {
+    const int b = e / (nchild + 1), c = e % (nchild + 1);
+    const int lo = rng[2 * b], hi = rng[2 * b + 1];
+    bnd[b * 9 + c] = c == 0 ? lo : (c == nchild ? hi : lower_child(q, n, lo, hi, lvl[b], dim, c));
+  }
+}
+
+__global__ void k_leaf_subranges(const dev::DBox* __restrict__ boxes, int nb, const int32_t* __restrict__ q, int n,
+                                 int dim, int* __restrict__ out) {
+  const int nchild = 1 << dim;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nb * 9; e += gridDim.x * blockDim.x) {
+    const int b = e / 9, c = e % 9;
+    const dev::DBox x = boxes[b];
+    int v;
+    if (!x.leaf || x.se == x.sb || x.level >= 30) v = c == 0 ? x.sb : x.se;
+    else v = c == 0 ? x.sb : (c >= nchild ? x.se : lower_child(q, n, x.sb, x.se, x.level, dim, c));
+    out[e] = v;
+  }
+}
+}  // namespace
+
+void launch_split_ranges(int nbox, const int* lvl, const int* rng, const int32_t* q, int n, int dim, int* bnd,
+                         cudaStream_t st) {
+  if (nbox <= 0) return;
+  const int tot = nbox * ((1 << dim) + 1);
+  k_split_ranges<<<std::min((tot + 255) / 256, 148 * 16), 256, 0, st>>>(nbox, lvl, rng, q, n, dim, bnd);
+}
+
+void launch_leaf_subranges(const dev::DBox* boxes, int nb, const int32_t* q, int n, int dim, int* out,
+                           cudaStream_t st) {
+  if (nb <= 0) return;
+  k_leaf_subranges<<<std::min((nb * 9 + 255) / 256, 148 * 16), 256, 0, st>>>(boxes, nb, q, n, dim, out);
 }
 
 }  // namespace sdmkb
