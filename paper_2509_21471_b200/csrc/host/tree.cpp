@@ -376,13 +376,21 @@ struct Builder {
           if (t.boxes[pc.box].leaf) continue;
           int o[3] = {0, 0, 0};
           rel(par, pc.box, pc.shift, ps, o);
-          for (int ci = 0; ci < nchild; ++ci) {
-            bool ok = true;
-            for (int a = 0; a < t.dim; ++a) {
-              const int dlt = 2 * o[a] + ((ci >> a) & 1) - cb[a];
-              ok = ok && dlt >= -1 && dlt <= 1;
+          // allowed child bits per axis: |2 o + cc - cb| <= 1; the set of child
+          // indices is their product, visited in ascending order
+          unsigned mask = (1u << nchild) - 1u;
+          for (int a = 0; a < t.dim; ++a) {
+            unsigned ax = 0;
+            for (int cc = 0; cc < 2; ++cc) {
+              const int dlt = 2 * o[a] + cc - cb[a];
+              if (dlt >= -1 && dlt <= 1) ax |= 1u << cc;
             }
-            if (!ok) continue;
+            static constexpr unsigned kBit0[3] = {0x55u, 0x33u, 0x0Fu};  // child indices with bit a clear
+            const unsigned full = (1u << nchild) - 1u, b0 = kBit0[a] & full, b1 = ~kBit0[a] & full;
+            mask &= ((ax & 1u) ? b0 : 0u) | ((ax & 2u) ? b1 : 0u);
+          }
+          for (; mask; mask &= mask - 1) {
+            const int ci = __builtin_ctz(mask);
             if (out) out[n] = {t.boxes[pc.box].first_child + ci, {pc.shift[0], pc.shift[1], pc.shift[2]}};
             ++n;
           }
