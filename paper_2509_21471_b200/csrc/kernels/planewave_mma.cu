@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kW * 32, 1) k_fwd_xy_mma(PWGrid g, const int* 
 // products.  X stage columns: n = 2 (m0 - 1) + part for m0 = 1..M, n = 2M for
 // m0 = 0 (E = 1).
 template <int PT, int PC, int NC>
-__global__ void __launch_bounds__(kW * 32, 1) k_fwd_xy2(PWGrid g, const int* __restrict__ boxes, int nch,
+__global__ void __launch_bounds__(kW * 32, 1) k_fwd_xy2(PWGrid g, const int* __restrict__ boxes, int nbox, int nch,
                                                        const double* __restrict__ outgoing,
                                                        double2* __restrict__ B) {
   constexpr int P8 = PT * 8;
@@ -219,11 +219,13 @@ __global__ void __launch_bounds__(kW * 32, 1) k_fwd_xy2(PWGrid g, const int* __r
   for (int e = tid; e < 4 * P8 * SAa; e += blockDim.x) a[e] = 0.0;
   __syncthreads();
   for (int c = tid; c < ncol; c += blockDim.x) colidx[(g.col_my[c] + M) * M1 + g.col_m0[c]] = c;
-  const int slot = blockIdx.x, ch = blockIdx.y;
-  const double* w = outgoing + ((size_t)boxes[slot] * nch + ch) * (size_t)(p * pp);
-  double2* Bo = B + ((size_t)slot * nch + ch) * (size_t)g.pz * ncol;
-  const int ngroups = (p + 3) / 4;
-  auto issue = [&](int grp, int buf) {
+  // persistent: items (box, channel) with stride gridDim.x, the flattened
+  // (item, slab group) sequence keeps the next group's input in flight
+  const int ngroups = (p + 3) / 4, nitems = nbox * nch;
+  const int nsteps = ((nitems - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * ngroups;
+  auto issue = [&](int step, int buf) {
+    const int wi = blockIdx.x + (step / ngroups) * gridDim.x, grp = step % ngroups;
+    const double* w = outgoing + ((size_t)boxes[wi / nch] * nch + wi % nch) * (size_t)(p * pp);
     double* dst = win + buf * 4 * P8 * SE;
     const int jz0 = grp * 4;
     for (int row = warp; row < 4 * p; row += kW) {
@@ -234,19 +236,21 @@ __global__ void __launch_bounds__(kW * 32, 1) k_fwd_xy2(PWGrid g, const int* __r
     }
     cp_commit();
   };
+  double2* Bo = B;
   auto put = [&](int iz, int my, int m0, double re, double im) {
     const int c = colidx[(my + M) * M1 + m0];
     if (c >= 0) Bo[(size_t)iz * ncol + c] = make_double2(re, im);
   };
-  issue(0, 0);
+  if (nsteps > 0) issue(0, 0);
   const int nnt = NX8 / 8;
   const int xtiles = 4 * PT * nnt;
   const int yunits = 4 * MT * MT;
-  for (int grp = 0; grp < ngroups; ++grp) {
-    const int buf = grp & 1;
+  for (int step = 0; step < nsteps; ++step) {
+    const int buf = step & 1, grp = step % ngroups;
+    Bo = B + (size_t)(blockIdx.x + (step / ngroups) * gridDim.x) * g.pz * ncol;  // (slot, ch) = item
     __syncthreads();
-    if (grp + 1 < ngroups) {
-      issue(grp + 1, buf ^ 1);
+    if (step + 1 < nsteps) {
+      issue(step + 1, buf ^ 1);
       cp_wait1();
     } else {
       cp_wait0();
@@ -971,7 +975,8 @@ void launch_forward_mma(const PWGrid& g, const int* boxes, int nbox, int nch, co
 #define FX2(PT_, PC_, NC_)                                                            \
   do {                                                                                \
     attr((const void*)k_fwd_xy2<PT_, PC_, NC_>, sm2);                                 \
-    k_fwd_xy2<PT_, PC_, NC_><<<grid, kW * 32, sm2, st>>>(g, boxes, nch, outgoing, B); \
+    k_fwd_xy2<PT_, PC_, NC_><<<std::min(nbox * nch, 2 * num_sms()), kW * 32, sm2, st>>>(g, boxes, nbox, nch,  \
+                                                                                      outgoing, B);              \
   } while (0)
       if (g.p == 23 && g.N == 33) FX2(3, 23, 33);
       else if (g.p == 22 && g.N == 33) FX2(3, 22, 33);
