@@ -24,6 +24,8 @@
  *   sdmk_target_far_fields   stokesdmk::target_far_fields     dmk.hpp:116-117, dmk.cpp:861-915
  *   sdmk_residual_pass       stokesdmk::residual_pass         dmk.hpp:128-131, dmk.cpp:919-1032
  *   sdmk_load_tables / sdmk_save_tables   import/export_split_kernel (split.hpp:153-154, SDMKSPLT v1)
+ *   sdmk_direct_sum          stokesdmk::direct_sum            oracle.hpp:60-65, oracle.cpp:143-179
+ *   sdmk_direct_residual_sum stokesdmk::direct_residual_sum   oracle.hpp:67-75, oracle.cpp:181-241
  *
  * Enumerations use the reference's enumerator order:
  *   kernel: 0 stokeslet, 1 stresslet, 2 rotlet  (KernelType, split.hpp:28)
@@ -142,6 +144,20 @@ int sdmk_incoming(sdmk_context* ctx, int stage, double* incoming);
 int sdmk_target_far_fields(sdmk_context* ctx, double* u);
 int sdmk_residual_pass(sdmk_context* ctx, double* u);
 
+/* ---- O(N*M) reference sums on the GPU ----
+   Same per-target source order, Kahan accumulation and unfused expression
+   trees as the reference (3D results are bitwise equal to it; the 2D
+   Stokeslet's log may differ by 1 ulp per pair).  Host buffers in caller
+   point order; n_tgt == 0 aliases (self pairs excluded).  direct_sum:
+   exact free-space kernels, coincident points -> SDMK_EDOMAIN.
+   direct_residual_sum: the plan's residual kernel at scale `cutoff`
+   (0 < cutoff, <= 1 when periodic), image shifts {-1,0,1}^dim when
+   periodic (inputs wrapped first). */
+int sdmk_direct_sum(sdmk_context* ctx, int kernel, int dim, int64_t n_src, const double* src, int64_t n_tgt,
+                    const double* tgt, const double* str, double* u);
+int sdmk_direct_residual_sum(sdmk_context* ctx, const sdmk_plan* plan, int dim, int64_t n_src, const double* src,
+                             int64_t n_tgt, const double* tgt, const double* str, double cutoff, int periodic,
+                             double* u);
 /* ---- multi-GPU (one process per GPU) ----
    Shard the following evaluations by target leaves:
    rank owns a contiguous Morton run of target leaves (balanced by target

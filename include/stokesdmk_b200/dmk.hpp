@@ -207,4 +207,37 @@ inline std::vector<double> evaluate(KernelType kernel, const ParticleSystem& sys
   return evaluate_with_plan(select_parameters(kernel, eps, window, sys.dim), sys, mode, report);
 }
 
+// Reference sums (oracle.hpp:60-75) on the GPU; see sdmk_direct_sum.
+inline std::vector<double> direct_sum(KernelType kernel, const ParticleSystem& sys) {
+  const int d = sys.dim;
+  if (d != 2 && d != 3) throw std::invalid_argument("ParticleSystem: dim must be 2 or 3");
+  const int64_t ns = static_cast<int64_t>(sys.sources.size()) / d;
+  const int64_t nt = static_cast<int64_t>(sys.targets.size()) / d;
+  std::vector<double> u(static_cast<size_t>(nt > 0 ? nt : ns) * d);
+  detail::check(sdmk_direct_sum(detail::context(), static_cast<int>(kernel), d, ns, sys.sources.data(), nt,
+                                nt > 0 ? sys.targets.data() : nullptr, sys.strengths.data(), u.data()));
+  return u;
+}
+
+inline std::vector<double> direct_residual_sum(const SplitKernel& sk, const ParticleSystem& sys, double cutoff,
+                                               bool periodic) {
+  const int d = sys.dim;
+  if (d != 2 && d != 3) throw std::invalid_argument("ParticleSystem: dim must be 2 or 3");
+  DmkPlan p;
+  p.kernel = sk.kernel;
+  p.dim = sk.dim;
+  p.window = sk.mollifier.window.kind;
+  p.c = sk.mollifier.window.c;
+  p.sigma = sk.mollifier.window.sigma;
+  p.table_tol = sk.table_tol;
+  sdmk_plan c = detail::to_c(p);
+  const int64_t ns = static_cast<int64_t>(sys.sources.size()) / d;
+  const int64_t nt = static_cast<int64_t>(sys.targets.size()) / d;
+  std::vector<double> u(static_cast<size_t>(nt > 0 ? nt : ns) * d);
+  detail::check(sdmk_direct_residual_sum(detail::context(), &c, d, ns, sys.sources.data(), nt,
+                                         nt > 0 ? sys.targets.data() : nullptr, sys.strengths.data(), cutoff,
+                                         periodic ? 1 : 0, u.data()));
+  return u;
+}
+
 }  // namespace stokesdmk

@@ -108,6 +108,9 @@ def lib():
             "sdmk_host_topology_dump": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, ip, C.c_int64, ip,
                                          C.c_char_p, C.c_int64], C.c_int64),
             "sdmk_set_shard": ([C.c_void_p, C.c_int, C.c_int], C.c_int),
+            "sdmk_direct_sum": ([C.c_void_p, C.c_int, C.c_int, C.c_int64, dp, C.c_int64, dp, dp, dp], C.c_int),
+            "sdmk_direct_residual_sum": ([C.c_void_p, P(sdmk_plan), C.c_int, C.c_int64, dp, C.c_int64, dp, dp,
+                                          C.c_double, C.c_int, dp], C.c_int),
             "sdmk_host_shard_plan": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, ip, C.c_int64, ip, C.c_int,
                                       C.c_int, P(C.c_int64)], C.c_int),
         }
@@ -327,6 +330,30 @@ class Context:
         _raise(lib().sdmk_residual_pass(self._h, _dptr(out)))
         return out
 
+    # ---- O(N*M) reference sums on the GPU (oracle.hpp:60-75) ---------------
+    def direct_sum(self, kernel, sys: ParticleSystem) -> np.ndarray:
+        """stokesdmk::direct_sum (oracle.cpp:143-179): exact kernels, Kahan per target."""
+        src, tgt, stw = _arr(sys.sources), _arr(sys.targets), _arr(sys.strengths)
+        d = int(sys.dim)
+        ns, nt = src.size // d, tgt.size // d
+        u = np.empty((nt if nt else ns) * d)
+        _raise(lib().sdmk_direct_sum(self._h, _enum(kernel, KERNELS), d, ns, _dptr(src), nt,
+                                     _dptr(tgt if nt else None), _dptr(stw), _dptr(u)))
+        return u
+
+    def direct_residual_sum(self, plan: DmkPlan, sys: ParticleSystem, cutoff: float,
+                            periodic: bool = False) -> np.ndarray:
+        """stokesdmk::direct_residual_sum (oracle.cpp:181-241) with the plan's split tables."""
+        src, tgt, stw = _arr(sys.sources), _arr(sys.targets), _arr(sys.strengths)
+        d = int(sys.dim)
+        ns, nt = src.size // d, tgt.size // d
+        u = np.empty((nt if nt else ns) * d)
+        cp = plan.to_c()
+        _raise(lib().sdmk_direct_residual_sum(self._h, C.byref(cp), d, ns, _dptr(src), nt,
+                                              _dptr(tgt if nt else None), _dptr(stw), float(cutoff),
+                                              1 if periodic else 0, _dptr(u)))
+        return u
+
     def set_shard(self, rank: int, nranks: int):
         """Own a contiguous Morton run of target leaves (see include/sdmk.h)."""
         _raise(lib().sdmk_set_shard(self._h, int(rank), int(nranks)))
@@ -366,6 +393,14 @@ def evaluate_with_plan(plan: DmkPlan, sys: ParticleSystem, mode=FREE_SPACE, repo
 
 def evaluate(kernel, sys: ParticleSystem, eps: float, window=PROLATE, mode=FREE_SPACE, report=None) -> np.ndarray:
     return default_context().evaluate(kernel, sys, eps, window, mode, report)
+
+
+def direct_sum(kernel, sys: ParticleSystem) -> np.ndarray:
+    return default_context().direct_sum(kernel, sys)
+
+
+def direct_residual_sum(plan: DmkPlan, sys: ParticleSystem, cutoff: float, periodic: bool = False) -> np.ndarray:
+    return default_context().direct_residual_sum(plan, sys, cutoff, periodic)
 
 
 # ---- host-only helpers (CPU tests of the setup / topology code) ----------

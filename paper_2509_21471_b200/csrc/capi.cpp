@@ -251,6 +251,25 @@ int sdmk_residual_pass(sdmk_context* c, double* out) {
   return guarded([&] { need_ctx(c)->residual(out); });
 }
 
+int sdmk_direct_sum(sdmk_context* c, int kernel, int dim, int64_t n_src, const double* src, int64_t n_tgt,
+                    const double* tgt, const double* str, double* u) {
+  return guarded([&] {
+    if (!src || !str || !u || (n_tgt > 0 && !tgt)) throw InvalidArgument("direct_sum: null array");
+    need_ctx(c)->direct(kernel, dim, n_src, src, n_tgt, tgt, str, nullptr, 1.0, false, u, false);
+  });
+}
+
+int sdmk_direct_residual_sum(sdmk_context* c, const sdmk_plan* plan, int dim, int64_t n_src, const double* src,
+                             int64_t n_tgt, const double* tgt, const double* str, double cutoff, int periodic,
+                             double* u) {
+  return guarded([&] {
+    if (!plan || !src || !str || !u || (n_tgt > 0 && !tgt)) throw InvalidArgument("direct_residual_sum: null array");
+    Context* x = need_ctx(c);
+    const Tables& t = x->tables_for(to_plan(plan));
+    x->direct(t.kernel, dim, n_src, src, n_tgt, tgt, str, &t, cutoff, periodic != 0, u, false);
+  });
+}
+
 int sdmk_set_shard(sdmk_context* c, int rank, int nranks) {
   return guarded([&] { need_ctx(c)->set_shard(rank, nranks); });
 }

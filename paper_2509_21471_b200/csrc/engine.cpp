@@ -1303,4 +1303,83 @@ void Context::residual(double* out) {
   if (hflags[3]) throw DomainError("residual_pass: coincident points");
 }
 
+void Context::direct(int kernel, int dim, int64_t ns, const double* src, int64_t nt, const double* tgt,
+                     const double* str, const Tables* tab, double cutoff, bool periodic, double* u, bool device_ptrs) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  const char* who = tab ? "direct_residual_sum" : "direct_sum";
+  if (tab) {  // oracle.cpp:184-191
+    if (!(cutoff > 0.0)) throw InvalidArgument("direct_residual_sum: cutoff must be positive");
+    if (periodic && cutoff > 1.0) throw InvalidArgument("direct_residual_sum: periodic image sums require cutoff <= 1");
+    if (dim != tab->dim) throw InvalidArgument("direct_residual_sum: dimension mismatch");
+    kernel = tab->kernel;
+  }
+  // validate_system (oracle.cpp:103-131)
+  if (kernel != kStokeslet && kernel != kStresslet && kernel != kRotlet)
+    throw InvalidArgument("particle sums support the Stokeslet, stresslet, and rotlet kernels");
+  if (dim != 2 && dim != 3) throw InvalidArgument("ParticleSystem: dim must be 2 or 3");
+  if (ns < 1) throw InvalidArgument("ParticleSystem: bad source array length");
+  if (nt < 0) throw InvalidArgument("ParticleSystem: bad target array length");
+  if (ns > (int64_t(1) << 31) - 1 || nt > (int64_t(1) << 31) - 1)
+    throw InvalidArgument(std::string(who) + ": more than 2^31-1 points");
+  const int sc = strength_width(kernel, dim);
+  const bool alias = nt == 0;
+  const int ntt = alias ? (int)ns : (int)nt;
+  double* dsrc = arena_.as<double>("dir_src", (size_t)ns * dim);
+  double* dtgt = alias ? dsrc : arena_.as<double>("dir_tgt", (size_t)nt * dim);
+  double* dstr = arena_.as<double>("dir_str", (size_t)ns * sc);
+  double* du = device_ptrs ? u : arena_.as<double>("dir_u", (size_t)ntt * dim);
+  copy_in(dsrc, src, sizeof(double) * ns * dim, device_ptrs);
+  if (!alias) copy_in(dtgt, tgt, sizeof(double) * nt * dim, device_ptrs);
+  copy_in(dstr, str, sizeof(double) * ns * sc, device_ptrs);
+  int* flags = arena_.as<int>("flags", 8);
+  cuda_check(cudaMemsetAsync(flags, 0, 8 * sizeof(int), st_), "memset");
+  const bool per = tab && periodic;
+  launch_validate(dstr, (int64_t)ns * sc, 1, flags, 2, st_);
+  launch_validate(dsrc, (int64_t)ns * dim, per, flags, 0, st_);
+  if (!alias) launch_validate(dtgt, (int64_t)nt * dim, per, flags, 0, st_);
+  int* hflags = (int*)pinned_.get("hflags", 64);
+  cuda_check(cudaMemcpyAsync(hflags, flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H flags");
+  sync();
+  if (hflags[2]) throw InvalidArgument("ParticleSystem: non-finite strength");
+  if (hflags[0]) throw InvalidArgument("ParticleSystem: non-finite coordinate");
+  if (hflags[1]) throw InvalidArgument("ParticleSystem: coordinate outside the unit box");
+  if (per) {  // wrap_into_box (oracle.cpp:133-141)
+    launch_wrap(dsrc, (int64_t)ns * dim, st_);
+    if (!alias) launch_wrap(dtgt, (int64_t)nt * dim, st_);
+  }
+  DirectTables T;
+  if (tab) {
+    const Cheb* cd = nullptr;
+    const Cheb* co = nullptr;
+    if (kernel == kStokeslet) cd = &tab->s_diag, co = &tab->s_offd;
+    else if (kernel == kStresslet) cd = &tab->t_diag, co = &tab->t_offd;
+    else co = &tab->w_offd;
+    if ((cd && cd->a.size() > (size_t)kDirectMaxCheb) || co->a.size() > (size_t)kDirectMaxCheb)
+      throw InvalidArgument("direct_residual_sum: table longer than the GPU limit");
+    double* hc = (double*)pinned_.get("dir_cheb", sizeof(double) * 2 * kDirectMaxCheb);
+    double* dc = arena_.as<double>("dir_cheb", 2 * kDirectMaxCheb);
+    if (cd) std::copy(cd->a.begin(), cd->a.end(), hc);
+    std::copy(co->a.begin(), co->a.end(), hc + kDirectMaxCheb);
+    cuda_check(cudaMemcpyAsync(dc, hc, sizeof(double) * 2 * kDirectMaxCheb, cudaMemcpyHostToDevice, st_), "H2D cheb");
+    T.cutoff = cutoff;
+    T.support = tab->support;
+    T.periodic = periodic ? 1 : 0;
+    T.cd = dc;
+    T.co = dc + kDirectMaxCheb;
+    T.nd = cd ? (int)cd->a.size() : 0;
+    T.no = (int)co->a.size();
+    if (cd) T.dlo = cd->lo, T.dhi = cd->hi;
+    T.olo = co->lo;
+    T.ohi = co->hi;
+  }
+  cuda_check(cudaMemsetAsync(flags, 0, 8 * sizeof(int), st_), "memset");
+  launch_direct(kernel, dim, dsrc, (int)ns, dtgt, ntt, dstr, alias ? 1 : 0, T, tab != nullptr, du, flags, st_);
+  cuda_check(cudaPeekAtLastError(), "direct kernel launch");
+  if (!device_ptrs) copy_out(u, du, sizeof(double) * ntt * dim);
+  cuda_check(cudaMemcpyAsync(hflags, flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H flags");
+  sync();
+  cuda_check(cudaGetLastError(), "kernel launch");
+  if (hflags[0]) throw DomainError(std::string(who) + ": coincident points");
+}
+
 }  // namespace sdmkb

@@ -122,6 +122,13 @@ class Context {
   void target_far(double* host_out);
   void residual(double* host_out);
 
+  // O(N*M) reference sums on the GPU: direct_sum (tab == nullptr; exact
+  // kernels) and direct_residual_sum (residual kernel of `tab` at scale
+  // cutoff, periodic images), oracle.cpp:143-241.  Inputs are the caller's
+  // point-major arrays; u is host or device memory as device_ptrs says.
+  void direct(int kernel, int dim, int64_t ns, const double* src, int64_t nt, const double* tgt, const double* str,
+              const Tables* tab, double cutoff, bool periodic, double* u, bool device_ptrs);
+
  private:
   void check_inputs(const Plan& plan, int dim, int64_t ns, int64_t nt, int mode);
   // inputs already in the arena ("src_in", "tgt_in", "str_in"): validate, wrap, sort, topology, upload

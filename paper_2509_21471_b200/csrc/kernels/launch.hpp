@@ -183,6 +183,23 @@ void launch_combine(int nt, int dim, const double* ufar, const double* ures, con
 // own[tperm[s]] = (t0 <= s < t1): the caller-order mask of a shard's targets
 void launch_own_mask(int nt, const int* tperm, int64_t t0, int64_t t1, unsigned char* own, cudaStream_t st);
 
+// ---- direct.cu: O(N*M) reference sums (oracle.cpp:143-241) ---------------------
+constexpr int kDirectMaxCheb = 1024;
+struct DirectTables {
+  double cutoff = 1.0, support = 1.0;  // residual scale nu and the table support
+  int periodic = 0;                    // 3^d image shifts (residual sum only)
+  const double* cd = nullptr;          // diag / offd Chebyshev coefficients (device)
+  const double* co = nullptr;
+  int nd = 0, no = 0;
+  double dlo = 0.0, dhi = 1.0, olo = 0.0, ohi = 1.0;
+};
+// u[b*dim + j] for targets b (tgt == src when alias); residual = false: the
+// exact kernels (direct_sum), true: residual_apply at scale T.cutoff
+// (direct_residual_sum).  flags[0] <- coincident points.  Inputs are the
+// caller's point-major arrays (already wrapped when periodic).
+void launch_direct(int kernel, int dim, const double* src, int ns, const double* tgt, int nt, const double* str,
+                   int alias, const DirectTables& T, bool residual, double* u, int* flags, cudaStream_t st);
+
 // ---- peak.cu ----------------------------------------------------------------
 double measure_fp64_peak_tflops(cudaStream_t st);
 

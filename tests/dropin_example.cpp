@@ -34,5 +34,8 @@ int main() {
   DmkReport rep;
   std::vector<double> u = timed_evaluate(plan, sys, EwaldMode::free_space, sk, 2, rep);
   std::vector<double> v = evaluate(KernelType::stokeslet, sys, 1e-6, WindowKind::prolate, EwaldMode::free_space);
-  return int(u.size() + v.size()) == 12 ? 0 : 1;
+  // acceptance.cpp-style accuracy check against the exact sum (acceptance.cpp:451-474)
+  std::vector<double> ex = direct_sum(KernelType::stokeslet, sys);
+  std::vector<double> res = direct_residual_sum(sk, sys, 1.0, false);
+  return int(u.size() + v.size() + ex.size() + res.size()) == 24 ? 0 : 1;
 }
