@@ -25,7 +25,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsdmk_b200.so")
+LIB_PATH = os.environ.get("SDMK_LIB") or os.path.join(_HERE, "libsdmk_b200.so")  # SDMK_LIB: A/B builds
 
 STOKESLET, STRESSLET, ROTLET = 0, 1, 2
 PROLATE, GAUSSIAN = 0, 1

@@ -1127,7 +1127,7 @@ void Context::run_residual(double* ures, bool stats) {  // dmk.cpp:919-1032
   launch_residual(rt, pr.boxes, pr.int_leaves, pr.n_int, pr.res_chunks, pr.n_chunks, pr.rng_start, pr.rng_box, pr.rng_info, pr.subrange, pr.spts, pr.ns,
                   pr.sstr, arena_.as<double>("srec", (size_t)pr.ns * ((pr.dim + pr.sc + 1) / 2 * 2)),
                   pr.periodic ? 1 : 0, pr.tpts, pr.nt, pr.tperm, pr.alias ? 1 : 0, 0.0, T.self_const, ures, flags + 3,
-                  stats ? st : nullptr, st_);
+                  stats ? st : nullptr, arena_.get("res_scratch", residual_scratch_bytes()), st_);
   ++launches_;  // source record packing
   cudaEventRecord(ev_[12], st_);
   ++launches_;

@@ -167,7 +167,9 @@ void launch_residual(const ResidTables& rt, const dev::DBox* boxes, const int* l
                      const double* spts, int ns, const double* sstr, double* srec, int periodic,
                      const double* tpts, int nt,
                      const int* tperm, int alias, double self_coef_scale, double self_const,
-                     double* ures, int* flags, unsigned long long* stats, cudaStream_t st);
+                     double* ures, int* flags, unsigned long long* stats, void* scratch, cudaStream_t st);
+// scratch for launch_residual (chunk counter + per-warp source interval lists)
+size_t residual_scratch_bytes();
 
 // ---- finalize.cu --------------------------------------------------------------
 // sums[j] = sum_a col_j(a) for j < ncomp (deterministic block tree)

@@ -21,6 +21,8 @@
 #include "common.cuh"
 #include "launch.hpp"
 
+#include <algorithm>
+
 namespace sdmkb {
 
 namespace {
@@ -31,8 +33,14 @@ constexpr int kRBlock = 256;
 constexpr int kWarps = kRBlock / 32;
 constexpr int kList = 48;        // per-lane list capacity (entries): longer lists, less lockstep padding
 constexpr int kMaxRanges = 160;
+constexpr int kMaxIvl = kMaxRanges * 8;  // source intervals per chunk: ranges x Morton sub-cells
+constexpr int kResBlocksPerSM = 2;       // persistent grid (registers and shared memory allow 2 per SM)
 constexpr int kMaxPW = 384;      // ni * (deg + 1) <= 384 (d, o) coefficient pairs
 constexpr int kCopies = 8;       // table copies, one per 16-byte bank group
+#ifndef SDMK_RES_ILP
+#define SDMK_RES_ILP 2
+#endif
+constexpr int kILP = SDMK_RES_ILP;  // list entries evaluated per step (independent chains)
 
 // Packed source record (coordinates, then strengths), padded to an even
 // number of doubles: the pair evaluation gathers one record with 16-byte loads
@@ -171,7 +179,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
                                                       const double* __restrict__ tpts, int nt,
                                                       const int* __restrict__ tperm, int alias, double self_const,
                                                       double* __restrict__ ures, int* flags,
-                                                      unsigned long long* stats) {
+                                                      unsigned long long* stats, int4* __restrict__ ivl_all,
+                                                      int* __restrict__ next_chunk) {
   extern __shared__ __align__(16) double2 dyn2[];  // [npw][kCopies] table, then the lists
   double2* s_pw = dyn2;
   const int npw = rt.ni * (rt.deg + 1);
@@ -184,28 +193,32 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     s_pw[e] = make_double2(KERNEL != 2 ? rt.pw_d[k] : 0.0, rt.pw_o[k]);
   }
   __syncthreads();
-  // one 32-target chunk of one leaf per warp (chunks never straddle leaves)
-  const int cid = blockIdx.x * kWarps + warp;
-  if (cid >= nchunks) return;
-  const int2 chunk = chunks[cid];
-  const int li = chunk.x;
-  const int leaf = leaves[li];
-  const DBox box = boxes[leaf];
-  const double r_l = box.side, r_f = 0.5 * r_l;
-  const double inv_rl = 1.0 / r_l, inv_rf = 1.0 / r_f;
+  int4* __restrict__ ivl = ivl_all + (size_t)(blockIdx.x * kWarps + warp) * kMaxIvl;  // this warp's interval list
   const double yscale = rt.ni / (rt.hi - rt.lo);
-  const int r0 = rng_start[li], nr = rng_start[li + 1] - r0;
   const double* __restrict__ spx = spts;
   const double* __restrict__ spy = spts + ns;
   const double* __restrict__ spz = spts + (size_t)(DIM == 3 ? 2 : 1) * ns;
-  double selfc = 0.0;
-  if (alias && KERNEL == 0) selfc = DIM == 3 ? self_const / r_l : self_const + log(r_l) / (4.0 * dev::kPI);
   unsigned long long n_ref = 0, n_test = 0, n_in = 0;
   int singular = 0;
-  {
+  // persistent warps: 32-target chunks of one leaf each, handed out in order
+  for (;;) {
+    int cid = 0;
+    if (lane == 0) cid = atomicAdd(next_chunk, 1);
+    cid = __shfl_sync(0xffffffffu, cid, 0);
+    if (cid >= nchunks) break;
+    const int2 chunk = chunks[cid];
+    const int li = chunk.x;
+    const int leaf = leaves[li];
+    const DBox box = boxes[leaf];
+    const double r_l = box.side, r_f = 0.5 * r_l;
+    const double inv_rl = 1.0 / r_l, inv_rf = 1.0 / r_f;
+    const int r0 = rng_start[li], nr = rng_start[li + 1] - r0;
+    double selfc = 0.0;
+    if (alias && KERNEL == 0) selfc = DIM == 3 ? self_const / r_l : self_const + log(r_l) / (4.0 * dev::kPI);
     const int t0 = chunk.y;
     const int t = t0 + lane;
     const bool valid = t < box.te;
+    const int nvalid = __popc(__ballot_sync(0xffffffffu, valid));
     const int tt = valid ? t : t0;
     double xt[3] = {0.0, 0.0, 0.0};
 #pragma unroll
@@ -222,13 +235,87 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       bl[ax] = lo;
       bh[ax] = hi;
     }
+    // 1. The source intervals this chunk must scan, lane-parallel over the
+    // leaf's near ranges (dmk.cpp:966-990): each range's box is culled
+    // against the warp's target box, then its Morton child sub-cells; the
+    // survivors are written in (range, sub-cell) order, so the scan below
+    // visits sources in the same order as a per-range loop.
+    // record: {a0, a1, meta, 0}, meta = image shift code (x+1 | y+1 << 2 |
+    // z+1 << 4) | fine-scale << 6 | zero shift << 7 | self range << 8
+    int nivl = 0;
+    for (int rb = 0; rb < nr; rb += 32) {
+      const int k = rb + lane;
+      unsigned mask = 0;
+      int sub[9];
+      int meta = 0;
+      if (k < nr) {
+        const int sbx = rng_box[r0 + k], info = rng_info[r0 + k];
+        const DBox sbox = boxes[sbx];
+        const int code = info & 31;
+        const int sh[3] = {code % 3 - 1, (code / 3) % 3 - 1, code / 9 - 1};
+        const bool fine = (info >> 5) & 1;
+        const int self = (info >> 6) & 1;
+        meta = (sh[0] + 1) | ((sh[1] + 1) << 2) | ((DIM == 3 ? sh[2] + 1 : 1) << 4) | (fine ? 64 : 0) |
+               (code == 13 ? 128 : 0) | (self ? 256 : 0);
+        const double nu = fine ? r_f : r_l;
+        const double cull = nu * rt.support * (1.0 + 1e-12) + 1e-15;
+        const double cull2 = cull * cull;
+        double lo[3];
+        double d2 = 0.0;  // distance from the warp's target box to the source box
+#pragma unroll
+        for (int ax = 0; ax < DIM; ++ax) {
+          lo[ax] = sbox.c[ax] - sbox.half + (double)sh[ax];
+          const double hi = sbox.c[ax] + sbox.half + (double)sh[ax];
+          const double dd = fmax(0.0, fmax(lo[ax] - bh[ax], bl[ax] - hi));
+          d2 += dd * dd;
+        }
+        n_ref += (unsigned long long)nvalid * (sbox.se - sbox.sb - ((alias && self) ? 1 : 0));
+        if (d2 <= cull2) {
+          const int* sp = subrange + (size_t)sbx * 9;
+#pragma unroll
+          for (int c = 0; c < 9; ++c) sub[c] = sp[c];
+          constexpr int NC = 1 << DIM;
+#pragma unroll
+          for (int ci = 0; ci < NC; ++ci) {
+            if (sub[ci] == sub[ci + 1]) continue;
+            double e2 = 0.0;
+#pragma unroll
+            for (int ax = 0; ax < DIM; ++ax) {
+              const double l = lo[ax] + ((ci >> ax) & 1) * sbox.half, h = l + sbox.half;
+              const double dd = fmax(0.0, fmax(l - bh[ax], bl[ax] - h));
+              e2 += dd * dd;
+            }
+            if (e2 <= cull2) mask |= 1u << ci;
+          }
+        }
+      }
+      const int c = __popc(mask);
+      int pre = c;  // inclusive warp scan of the survivor counts
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += v;
+      }
+      int pos = nivl + pre - c;
+      for (unsigned m = mask; m; m &= m - 1) {
+        const int ci = __ffs(m) - 1;
+        ivl[pos++] = make_int4(sub[ci], sub[ci + 1], meta, 0);
+        n_test += (unsigned long long)nvalid * (sub[ci + 1] - sub[ci]);
+      }
+      nivl += __shfl_sync(0xffffffffu, pre, 31);
+    }
+    __syncwarp();
     double u[3] = {0.0, 0.0, 0.0};
     int cnt = 0;
     auto flush = [&]() {
       int mx = cnt;
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      // two list entries per step: independent dependency chains interleave,
+#ifdef SDMK_RES_NOEVAL  // profiling: the scan alone
+      if (mx > 0) u[0] += (double)lsrc[warp][mx - 1][lane];
+      mx = 0;
+#endif
+      // kILP list entries per step: independent dependency chains interleave,
       // and their contributions are added in list order
       auto eval = [&](int i, double* c) {
         const int a = lsrc[warp][i][lane];
@@ -261,77 +348,66 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         radial_tables<KERNEL, DEG>(rt, s_pw + (lane & (kCopies - 1)), yscale, s, fd, fo);
         assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, nu, rv + DIM, c);
       };
-      for (int i = 0; i < mx; i += 2) {  // both evaluations unconditional (clamped), straight-line
-        const int i0 = min(i, cnt - 1), i1 = min(i + 1, cnt - 1);
-        double c0[3] = {0.0, 0.0, 0.0}, c1[3] = {0.0, 0.0, 0.0};
-        if (cnt > 0) {
-          eval(i0, c0);
-          eval(i1, c1);
-        }
-        const bool h0 = i < cnt, h1 = i + 1 < cnt;
+      for (int i = 0; i < mx; i += kILP) {  // all evaluations unconditional (clamped), straight-line
+        double c[kILP][3];
 #pragma unroll
-        for (int j = 0; j < DIM; ++j) {
-          if (h0) u[j] += c0[j];
-          if (h1) u[j] += c1[j];
+        for (int q = 0; q < kILP; ++q) c[q][0] = c[q][1] = c[q][2] = 0.0;
+        if (cnt > 0) {
+#pragma unroll
+          for (int q = 0; q < kILP; ++q) eval(min(i + q, cnt - 1), c[q]);
         }
+#pragma unroll
+        for (int j = 0; j < DIM; ++j)
+#pragma unroll
+          for (int q = 0; q < kILP; ++q)
+            if (i + q < cnt) u[j] += c[q][j];
       }
       cnt = 0;
     };
-    for (int k = 0; k < nr; ++k) {
-      // the range's source leaf, image shift and scale (dmk.cpp:966-990), warp-uniform
-      const int sbx = rng_box[r0 + k], info = rng_info[r0 + k];
-      const DBox sbox = boxes[sbx];
-      RangeS R;
-      {
-        const int code = info & 31;
-        const int sh[3] = {code % 3 - 1, (code / 3) % 3 - 1, code / 9 - 1};
-        R.nu = (info >> 5) & 1 ? r_f : r_l;
-        R.code = (sh[0] + 1) | ((sh[1] + 1) << 2) | ((DIM == 3 ? sh[2] + 1 : 1) << 4) | ((info & 32) << 1);
-        R.self = (info >> 6) & 1;
-        const double sup = R.nu * rt.support;
-        R.sup2 = sup * sup;
-        R.cull = sup * (1.0 + 1e-12) + 1e-15;
-        R.zero_shift = code == 13;
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-          R.sh[ax] = ax < DIM ? (double)sh[ax] : 0.0;
-          R.lo[ax] = sbox.c[ax] - sbox.half + R.sh[ax];
-          R.hi[ax] = sbox.c[ax] + sbox.half + R.sh[ax];
+    // 2. Scan: sources arrive in rounds of up to 32, one coalesced load per
+    // coordinate (lane j holds source a + j), and are broadcast to every
+    // lane's target with shuffles; the next round's load is issued before
+    // the current round is tested.  Every lane tests its own target with the
+    // reference's arithmetic (x = xt - (xs + shift)) and appends in-support
+    // pairs to its list.
+    const double sup2l = (r_l * rt.support) * (r_l * rt.support);
+    const double sup2f = (r_f * rt.support) * (r_f * rt.support);
+    for (int ib = 0; ib < nivl; ib += 32) {
+      const int nb = min(32, nivl - ib);
+      const int4 iv = lane < nb ? ivl[ib + lane] : make_int4(0, 0, 0, 0);
+      int i = 0, s = __shfl_sync(0xffffffffu, iv.x, 0);
+      int e = __shfl_sync(0xffffffffu, iv.y, 0);
+      double px = 0.0, py = 0.0, pz = 0.0;
+      auto load = [&](int s_, int e_) {
+        if (s_ + lane < e_) {
+          px = spx[s_ + lane];
+          py = spy[s_ + lane];
+          if (DIM == 3) pz = spz[s_ + lane];
         }
-        R.sb = sbox.sb;
-        R.se = sbox.se;
-        R.half = sbox.half;
-      }
-      const int* sub = subrange + (size_t)sbx * 9;
-      const int len = R.se - R.sb;
-      n_ref += valid ? len - ((alias && R.self) ? 1 : 0) : 0;
-      double d2 = 0.0;  // distance from the warp's target box to the source box
-#pragma unroll
-      for (int ax = 0; ax < DIM; ++ax) {
-        const double dd = fmax(0.0, fmax(R.lo[ax] - bh[ax], bl[ax] - R.hi[ax]));
-        d2 += dd * dd;
-      }
-      if (d2 > R.cull * R.cull) continue;
-      const double sup2 = R.sup2, cull2 = R.cull * R.cull;
-      const bool zs = R.zero_shift;
-      const bool skip_self = alias && R.self;
-      constexpr int NC = 1 << DIM;
-      for (int ci = 0; ci < NC; ++ci) {  // Morton child sub-cells of the source leaf
-        const int a0 = sub[ci], a1 = sub[ci + 1];
-        if (a0 == a1) continue;
-        double e2 = 0.0;
-#pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) {
-          const double lo = R.lo[ax] + ((ci >> ax) & 1) * R.half, hi = lo + R.half;
-          const double dd = fmax(0.0, fmax(lo - bh[ax], bl[ax] - hi));
-          e2 += dd * dd;
+      };
+      load(s, e);
+      while (i < nb) {
+        const int ci = i, cs = s, ce = e;
+        const double cx = px, cy = py, cz = pz;
+        // advance to the next round and start its load
+        s += 32;
+        if (s >= e) {
+          ++i;
+          if (i < nb) {
+            s = __shfl_sync(0xffffffffu, iv.x, i);
+            e = __shfl_sync(0xffffffffu, iv.y, i);
+          }
         }
-        if (e2 > cull2) continue;
-        n_test += valid ? a1 - a0 : 0;
-        // the zero-shift test (xs + 0 == xs) and the shifted one are separate
-        // loops, so the warp-uniform choice is made once per sub-cell
+        if (i < nb) load(s, e);
+        const int meta = __shfl_sync(0xffffffffu, iv.z, ci);
+        const int code = meta & 127;
+        const double sup2 = (meta & 64) ? sup2f : sup2l;
+        const bool skip_self = alias && (meta & 256);
+        const int nv = min(32, ce - cs);
         auto scan = [&](auto zsc) {
           constexpr bool ZS = decltype(zsc)::value;
+          const double shx = (double)((code & 3) - 1), shy = (double)(((code >> 2) & 3) - 1),
+                       shz = (double)(((code >> 4) & 3) - 1);
           auto test = [&](int a, double sx, double sy, double sz) {
             double x0, x1, x2 = 0.0;
             if (ZS) {
@@ -339,9 +415,9 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
               x1 = xt[1] - sy;
               if (DIM == 3) x2 = xt[2] - sz;
             } else {
-              x0 = xt[0] - (sx + R.sh[0]);
-              x1 = xt[1] - (sy + R.sh[1]);
-              if (DIM == 3) x2 = xt[2] - (sz + R.sh[2]);
+              x0 = xt[0] - (sx + shx);
+              x1 = xt[1] - (sy + shy);
+              if (DIM == 3) x2 = xt[2] - (sz + shz);
             }
             double r2 = x0 * x0 + x1 * x1;
             if (DIM == 3) r2 += x2 * x2;
@@ -352,30 +428,24 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
             }
             if (in) {
               lsrc[warp][cnt][lane] = a;
-              lrng[warp][cnt][lane] = (unsigned char)R.code;
+              lrng[warp][cnt][lane] = (unsigned char)code;
               ++cnt;
               ++n_in;
             }
           };
-          int a = a0;
-          for (; a + 4 <= a1; a += 4) {  // 4 broadcast loads in flight before the tests
+          for (int j = 0; j < nv; j += 4) {
             if (__any_sync(0xffffffffu, cnt > kList - 4)) flush();
-            double sx[4], sy[4], sz[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              sx[q] = spx[a + q];
-              sy[q] = spy[a + q];
-              if (DIM == 3) sz[q] = spz[a + q];
+              const int jj = j + q;
+              const double sx = __shfl_sync(0xffffffffu, cx, jj & 31);
+              const double sy = __shfl_sync(0xffffffffu, cy, jj & 31);
+              const double sz = DIM == 3 ? __shfl_sync(0xffffffffu, cz, jj & 31) : 0.0;
+              if (jj < nv) test(cs + jj, sx, sy, sz);
             }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) test(a + q, sx[q], sy[q], sz[q]);
-          }
-          for (; a < a1; ++a) {
-            if (__any_sync(0xffffffffu, cnt == kList)) flush();
-            test(a, spx[a], spy[a], DIM == 3 ? spz[a] : 0.0);
           }
         };
-        if (zs) scan(BoolC<true>{});
+        if (meta & 128) scan(BoolC<true>{});
         else scan(BoolC<false>{});
       }
     }
@@ -389,9 +459,12 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         ut[j] = v;
       }
     }
+    __syncwarp();  // the interval list is rewritten by the next chunk
   }
   if (singular) atomicOr(flags, 1);
   if (stats) {
+    // n_ref / n_test were counted once per range / interval by one lane
+    // (times the warp's valid targets); n_in per lane
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
       n_test += __shfl_xor_sync(0xffffffffu, n_test, o);
@@ -408,19 +481,32 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
 
 }  // namespace
 
+size_t residual_scratch_bytes() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return (size_t)kResBlocksPerSM * sms * kWarps * kMaxIvl * sizeof(int4) + 256;
+}
+
 void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves, int nleaf, const int* chunks,
                      int nchunks, const int* rng_start,
                      const int* rng_box, const int* rng_info, const int* subrange, const double* spts, int ns, const double* sstr,
                      double* srec, int periodic,
                      const double* tpts, int nt, const int* tperm, int alias, double /*unused*/, double self_const,
-                     double* ures, int* flags, unsigned long long* stats, cudaStream_t st) {
+                     double* ures, int* flags, unsigned long long* stats, void* scratch, cudaStream_t st) {
   if (nleaf <= 0 || nchunks <= 0) return;
   {
     const int sc = rt.kernel == 0 ? rt.dim : (rt.kernel == 1 ? 2 * rt.dim : (rt.dim == 3 ? 3 : 1));
     const int rw = (rt.dim + sc + 1) / 2 * 2;
     k_pack_sources<<<148 * 8, 256, 0, st>>>(spts, sstr, ns, rt.dim, sc, rw, srec);
   }
-  const int nblk = (nchunks + kWarps - 1) / kWarps;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int nblk = std::min(kResBlocksPerSM * sms, (nchunks + kWarps - 1) / kWarps);
+  int* next_chunk = reinterpret_cast<int*>(scratch);
+  int4* ivl = reinterpret_cast<int4*>(reinterpret_cast<char*>(scratch) + 256);
+  cudaMemsetAsync(next_chunk, 0, sizeof(int), st);
   const int2* ch2 = reinterpret_cast<const int2*>(chunks);
   const size_t dsm = (size_t)kWarps * kList * 32 * (sizeof(int) + 1) +
                      sizeof(double) * 2 * kCopies * (size_t)rt.ni * (rt.deg + 1);
@@ -438,7 +524,7 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
                                                     rng_info, subrange,                                          \
                                                      spts, ns, sstr, reinterpret_cast<const double2*>(srec),     \
                                                      periodic, tpts, nt, tperm, alias, self_const, ures,         \
-                                                     flags, stats);                                              \
+                                                     flags, stats, ivl, next_chunk);                             \
   } while (0)
   if (rt.dim == 3) {
     if (rt.kernel == 0) RES(0, 3);
