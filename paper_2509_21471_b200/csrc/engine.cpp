@@ -151,7 +151,9 @@ void* Pinned::get(const std::string& name, size_t bytes) {
 Context::Context(int device) : device_(device) {
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "cudaStreamCreate");
+  cuda_check(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking), "cudaStreamCreate");
   for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+  cuda_check(cudaEventCreateWithFlags(&str_ev_, cudaEventDisableTiming), "cudaEventCreate");
 }
 
 Context::~Context() {
@@ -160,6 +162,9 @@ Context::~Context() {
   for (auto& e : ev_) cudaEventDestroy(e);
   for (auto& e : pw_ev_) cudaEventDestroy(e);
   for (auto& e : stage_ev_) cudaEventDestroy(e);
+  if (st2_) cudaStreamSynchronize(st2_);
+  if (str_ev_) cudaEventDestroy(str_ev_);
+  if (st2_) cudaStreamDestroy(st2_);
   if (st_) cudaStreamDestroy(st_);
 }
 
@@ -418,7 +423,7 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
   // validate_system (oracle.cpp:103-131) then wrap_into_box (oracle.cpp:133-141)
   launch_validate(src, (int64_t)ns * d, pr.periodic, flags, 0, st_);
   if (tgt) launch_validate(tgt, (int64_t)nt * d, pr.periodic, flags, 0, st_);
-  launch_validate(str, (int64_t)ns * pr.sc, 1, flags, 2, st_);
+  if (!str_pending_) launch_validate(str, (int64_t)ns * pr.sc, 1, flags, 2, st_);
   if (pr.periodic) {
     launch_wrap(src, (int64_t)ns * d, st_);
     if (tgt) launch_wrap(tgt, (int64_t)nt * d, st_);
@@ -445,8 +450,19 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
   int32_t *sq = nullptr, *tq = nullptr;
   sort_set(src, ns, "s", pr.sperm, pr.spts, sq);
   pr.sstr = arena_.as<double>("sstr", (size_t)ns * pr.sc);
-  launch_gather_strengths(str, pr.sperm, ns, pr.sc, pr.sstr, st_);
-  ++launches_;
+  // strengths still in flight on the side stream: validated and gathered
+  // once the topology is built (finish_strengths)
+  auto finish_strengths = [&]() {
+    if (str_pending_) {
+      cuda_check(cudaStreamWaitEvent(st_, str_ev_, 0), "stream wait");
+      cuda_check(cudaMemsetAsync(flags + 2, 0, sizeof(int), st_), "memset");
+      launch_validate(str, (int64_t)ns * pr.sc, 1, flags, 2, st_);
+      ++launches_;
+    }
+    launch_gather_strengths(str, pr.sperm, ns, pr.sc, pr.sstr, st_);
+    ++launches_;
+  };
+  if (!str_pending_) finish_strengths();
   if (!pr.alias) {
     sort_set(tgt, nt, "t", pr.tperm, pr.tpts, tq);
     pr.tpts_caller = tgt;
@@ -464,6 +480,16 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
   const auto w0 = std::chrono::steady_clock::now();
   sync();
   const auto w1 = std::chrono::steady_clock::now();
+  auto check_strengths = [&]() {  // after finish_strengths: one more flags round trip
+    cuda_check(cudaMemcpyAsync(hflags, flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H flags");
+    sync();
+    str_pending_ = false;
+    if (hflags[2]) throw InvalidArgument("ParticleSystem: non-finite strength");
+  };
+  if (str_pending_ && (hflags[0] || hflags[1])) {  // the reference checks strengths first (oracle.cpp:116-118)
+    finish_strengths();
+    check_strengths();
+  }
   if (hflags[2]) throw InvalidArgument("ParticleSystem: non-finite strength");
   if (hflags[0]) throw InvalidArgument("ParticleSystem: non-finite coordinate");
   if (hflags[1]) throw InvalidArgument("ParticleSystem: coordinate outside the unit box");
@@ -503,6 +529,10 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
     *qt_out = pr.alias ? nullptr : hq + (size_t)ns * d;
   };
   pr.tree = build_topology(d, pr.periodic, P.n_s, P.p, ns, pr.alias ? 0 : nt, pa);
+  if (str_pending_) {
+    finish_strengths();
+    check_strengths();
+  }
   const auto w2 = std::chrono::steady_clock::now();
   pr.lists_b = false;
   upload_tree_lists_a();
@@ -1148,7 +1178,18 @@ void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, in
   cudaEventRecord(ev_[0], st_);
   copy_in(arena_.as<double>("src_in", (size_t)ns * dim), src, sizeof(double) * ns * dim, device_ptrs);
   if (!alias) copy_in(arena_.as<double>("tgt_in", (size_t)nt * dim), tgt, sizeof(double) * nt * dim, device_ptrs);
-  copy_in(arena_.as<double>("str_in", (size_t)ns * sc), str, sizeof(double) * ns * sc, device_ptrs);
+  // pinned strengths travel on a second stream while the tree is built (they
+  // are first needed by the upward pass); pageable / device ones as before
+  str_pending_ = !device_ptrs && !is_pageable(str) && ns * sc * sizeof(double) > kStageBytes;
+  if (str_pending_) {
+    cuda_check(cudaStreamWaitEvent(st2_, ev_[0], 0), "stream wait");
+    cuda_check(cudaMemcpyAsync(arena_.as<double>("str_in", (size_t)ns * sc), str, sizeof(double) * ns * sc,
+                               cudaMemcpyHostToDevice, st2_),
+               "copy in");
+    cuda_check(cudaEventRecord(str_ev_, st2_), "event record");
+  } else {
+    copy_in(arena_.as<double>("str_in", (size_t)ns * sc), str, sizeof(double) * ns * sc, device_ptrs);
+  }
   cudaEventRecord(ev_[1], st_);
   build_problem(P, dim, (int)ns, (int)nt, mode, true);
   cudaEventRecord(ev_[2], st_);
@@ -1249,6 +1290,7 @@ void Context::setup(const Plan& P, int dim, int64_t ns, const double* src, int64
   cuda_check(cudaMemcpyAsync(arena_.as<double>("str_in", (size_t)ns * sc), str, sizeof(double) * ns * sc,
                              cudaMemcpyHostToDevice, st_),
              "copy strengths");
+  str_pending_ = false;
   build_problem(P, dim, (int)ns, (int)nt, mode);
 }
 

@@ -150,6 +150,9 @@ class Context {
 
   int device_;
   cudaStream_t st_ = nullptr;
+  cudaStream_t st2_ = nullptr;     // side stream: strengths H2D overlapping the tree build
+  cudaEvent_t str_ev_ = nullptr;
+  bool str_pending_ = false;       // strengths copy in flight on st2_
   cudaEvent_t ev_[16];
   Arena arena_;
   Pinned pinned_;
