@@ -609,6 +609,159 @@ void tensor3_seg_t(int p, const double* mats, const int* in_list, const int* out
   k_tensor3<PC><<<grid, kT3W * 32, smem, st>>>(p, mats, in_list, out_box, ci, 1, nch, src, dst, 0, seg);
 }
 
+
+// Downward interpolation of one parent into its 2^3 children with the
+// shared prefix of the separable applies (dmk.cpp:835-855):
+//   out_c = (Mz_cz (x) My_cy (x) Mx_cx) in,   c = cx | cy << 1 | cz << 2.
+// z is contracted first, per group of 8 output slabs iz0..iz0+7:
+//   Z  : Z_cz[s][jy][jx]  = sum_jz Mz_cz[iz0+s][jz] in[jz][jy][jx]   (2 variants)
+//   Y  : Y_cz,cy[s][iy][jx] = sum_jy My_cy[iy][jy] Z_cz[s][jy][jx]   (4, two at a time)
+//   X  : out_c[iz0+s][iy][ix] = sum_jx Y_cz,cy[s][iy][jx] Mx_cx[ix][jx] (8)
+// -- 14 p^4 DMMA work per parent and channel instead of 24 p^4 for eight
+// independent children, and every output is final when written (write-only:
+// a child's incoming is zero before its parent's interpolation).  One CTA per
+// (parent, channel), 12 warps; Z and Y live in shared memory (fragment
+// strides == 4 mod 8 doubles); the input is read from L2 once per group.
+constexpr int kTDW = 12;
+template <int PC>
+__global__ void __launch_bounds__(kTDW * 32, 1)
+    k_tensor_down(const double* __restrict__ mats, const int* __restrict__ in_list, const int* __restrict__ out_box,
+                  const int* __restrict__ ci_list, const int* __restrict__ seg, int nch, const double* __restrict__ src,
+                  double* __restrict__ dst) {
+  constexpr int p = PC, pp = p * p, nodes = p * pp;
+  constexpr int P8 = 24, SA = 28, SZ = 28, PL = P8 * SZ;  // plane: 24 rows x SZ
+  constexpr int NN = (pp + 7) / 8;                        // Z-stage column tiles
+  constexpr int ZNT = (NN + kTDW - 1) / kTDW;             // per warp
+  static_assert(p >= 17 && p <= 24, "PT = 3 shapes");
+  extern __shared__ double sm[];
+  double* Mm = sm;            // [2][P8][SA]
+  double* Zs = Mm + 2 * P8 * SA;  // [2 cz][8 s] planes [jy][jx]
+  double* Ys = Zs + 16 * PL;      // [2 cz][8 s] planes [iy][jx] for one cy
+  __shared__ int s_out[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  for (int r = warp; r < 2 * P8; r += kTDW) {
+    const int bsel = r / P8, rr = r % P8;
+    for (int c = lane; c < SA; c += 32) Mm[r * SA + c] = (rr < p && c < p) ? mats[(size_t)bsel * pp + rr * p + c] : 0.0;
+  }
+  for (int e = tid; e < 32 * PL; e += blockDim.x) Zs[e] = 0.0;  // padding rows / columns stay zero (Zs and Ys)
+  const int par = blockIdx.x, ch = blockIdx.y;
+  if (tid < 8) s_out[tid] = -1;
+  __syncthreads();
+  int parent = 0;
+  for (int q = seg[par]; q < seg[par + 1]; ++q) {
+    parent = in_list[q];
+    if (tid == 0) s_out[ci_list[q] & 7] = out_box[q];
+  }
+  __syncthreads();
+  unsigned have = 0;  // children present
+#pragma unroll
+  for (int c = 0; c < 8; ++c) have |= (s_out[c] >= 0 ? 1u : 0u) << c;
+  const double* in = src + ((size_t)parent * nch + ch) * nodes;
+  for (int iz0 = 0; iz0 < p; iz0 += 8) {
+    // ---- Z stage: rows (cz, s), columns n = jy * p + jx, K = jz
+    {
+      double c[2][ZNT][2];
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int i = 0; i < ZNT; ++i) c[m][i][0] = c[m][i][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 6; ++ks) {
+        const int jz = ks * 4 + t;
+        double b[ZNT];
+#pragma unroll
+        for (int i = 0; i < ZNT; ++i) {
+          const int n = (warp + kTDW * i) * 8 + g;
+          b[i] = (jz < p && n < pp && warp + kTDW * i < NN) ? __ldg(in + (size_t)jz * pp + n) : 0.0;
+        }
+        const double a0 = Mm[(0 * P8 + iz0 + g) * SA + jz], a1 = Mm[(1 * P8 + iz0 + g) * SA + jz];
+#pragma unroll
+        for (int i = 0; i < ZNT; ++i) {
+          dev::dmma(c[0][i][0], c[0][i][1], a0, b[i]);
+          dev::dmma(c[1][i][0], c[1][i][1], a1, b[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < ZNT; ++i) {
+        const int nt = warp + kTDW * i;
+        if (nt >= NN) continue;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = nt * 8 + 2 * t + e;
+          if (n >= pp) continue;
+          const int jy = n / p, jx = n - jy * p;
+#pragma unroll
+          for (int m = 0; m < 2; ++m) Zs[(m * 8 + g) * PL + jy * SZ + jx] = c[m][i][e];
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int cy = 0; cy < 2; ++cy) {
+      const unsigned need = have & (cy ? 0xCCu : 0x33u);  // children with this cy
+      if (!need) continue;
+      // ---- Y stage: plane P = (cz, s): Y[iy][jx] = sum_jy My[iy][jy] Z[jy][jx];
+      // unit (P, iy tile) x the 3 jx tiles
+      const double* My = Mm + cy * P8 * SA;
+      for (int u = warp; u < 48; u += kTDW) {
+        const int P = u / 3, it = u % 3;
+        if (!(need & (0x0Fu << (4 * (P >> 3))))) continue;  // no child with this cz
+        const double* Zp = Zs + P * PL;
+        double c[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int ks = 0; ks < 6; ++ks) {
+          const double a = My[(it * 8 + g) * SA + ks * 4 + t];
+#pragma unroll
+          for (int nt = 0; nt < 3; ++nt) dev::dmma(c[nt][0], c[nt][1], a, Zp[(ks * 4 + t) * SZ + nt * 8 + g]);
+        }
+        double* Yp = Ys + P * PL + (it * 8 + g) * SZ;
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt) {
+          Yp[nt * 8 + 2 * t] = c[nt][0];
+          Yp[nt * 8 + 2 * t + 1] = c[nt][1];
+        }
+      }
+      __syncthreads();
+      // ---- X stage: unit (P, cx, iy tile) x the 3 ix tiles, straight to the child
+      for (int u = warp; u < 96; u += kTDW) {
+        const int P = u / 6, cx = (u / 3) & 1, it = u % 3;
+        const int cz = P >> 3, s = P & 7, child = cx | (cy << 1) | (cz << 2);
+        const int iz = iz0 + s;
+        if (s_out[child] < 0 || iz >= p) continue;
+        const double* Yp = Ys + P * PL;
+        const double* Mx = Mm + cx * P8 * SA;
+        double c[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int ks = 0; ks < 6; ++ks) {
+          const double a = Yp[(it * 8 + g) * SZ + ks * 4 + t];
+#pragma unroll
+          for (int nt = 0; nt < 3; ++nt) dev::dmma(c[nt][0], c[nt][1], a, Mx[(nt * 8 + g) * SA + ks * 4 + t]);
+        }
+        const int iy = it * 8 + g;
+        if (iy < p) {
+          double* o = dst + ((size_t)s_out[child] * nch + ch) * nodes + (size_t)iz * pp + iy * p;
+#pragma unroll
+          for (int nt = 0; nt < 3; ++nt) {
+            const int ix = nt * 8 + 2 * t;
+            if (ix < p) o[ix] = c[nt][0];
+            if (ix + 1 < p) o[ix + 1] = c[nt][1];
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <int PC>
+void tensor_down_t(const double* mats, const int* in_list, const int* out_box, const int* ci, const int* seg,
+                   int nseg, int nch, const double* src, double* dst, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (2 * 24 * 28 + 32 * 24 * 28);
+  cudaFuncSetAttribute(k_tensor_down<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid(nseg, nch);
+  k_tensor_down<PC><<<grid, kTDW * 32, smem, st>>>(mats, in_list, out_box, ci, seg, nch, src, dst);
+}
+
 }  // namespace
 
 bool tensor_seg_supported(int p, int dim) { return dim == 3 && p >= 17 && p <= 24 && !std::getenv("SDMK_TENSOR_OLD"); }
@@ -616,7 +769,10 @@ bool tensor_seg_supported(int p, int dim) { return dim == 3 && p >= 17 && p <= 2
 void launch_tensor_mma_seg(int p, const double* mats, const int* in_list, const int* out_box, const int* ci,
                            const int* seg, int nseg, int nch, const double* src, double* dst, cudaStream_t st) {
   if (nseg <= 0) return;
-  if (p == 23) tensor3_seg_t<23>(p, mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
+  static const bool prefix = std::getenv("SDMK_TENSOR_NOPREFIX") == nullptr;
+  if (prefix && p == 23) tensor_down_t<23>(mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
+  else if (prefix && p == 22) tensor_down_t<22>(mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
+  else if (p == 23) tensor3_seg_t<23>(p, mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
   else if (p == 22) tensor3_seg_t<22>(p, mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
   else tensor3_seg_t<0>(p, mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
 }
