@@ -18,14 +18,16 @@ unit vector) reported beside it.  Seeded synthetic data (no dataset exists).
 --impl reference times the reference's own CPU implementation (oracle/_ref)
 on a bounded sample per step (rank 0 only).
 
-Multi-GPU (torchrun): the SAME N-point system is sharded by target leaves
-(include/sdmk.h sdmk_set_shard, paper_2509_21471_b200/distributed.py): every
-rank builds the tree and the upward pass, forms the downward pass, far fields
-and residual for its own Morton run of target leaves, and one NCCL
-all_reduce assembles u (strong scaling; the sum is bitwise the 1-GPU
-result).  The timed region (CUDA events on the torch stream, the library
-call blocking in between) includes the all-reduce; barriers on both sides and
-the max over ranks.
+Multi-GPU (torchrun): the SAME N-point system is sharded (include/sdmk.h
+sdmk_comm_init, paper_2509_21471_b200/distributed.py): every rank builds the
+tree; the upward pass is split into cut subtrees owned by ranks, with one
+NCCL group exchanging the outgoing expansions each rank reads (its halo) and
+the cut boxes; each rank forms the downward pass, far fields and residual
+for its own Morton run of target leaves, and an NCCL all-reduce assembles u
+on every rank (strong scaling; the result is bitwise the 1-GPU result).  All
+of it runs on the library's stream; the timed region (CUDA events on that
+stream, the call blocking in between) has barriers on both sides and the
+max over ranks.
 """
 from __future__ import annotations
 
@@ -140,6 +142,10 @@ def run_ours(args, rank, world, local_rank):
         return float(t.item())
 
     ctx = g.Context(local_rank)
+    if world > 1:  # the library's own NCCL communicator: halo exchange + u all-reduce on its stream
+        obj = [g.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.comm_init(rank, world, obj[0])
     stream = torch.cuda.ExternalStream(ctx.stream_handle())
     n = args.n
     results = {}
@@ -149,19 +155,15 @@ def run_ours(args, rank, world, local_rank):
             continue
         plan = g.select_parameters(kernel, args.eps, g.PROLATE, 3)
         x, s = make_system(kernel, n, args.seed + kernel)  # the same system on every rank
-        if world > 1:
-            ctx.set_shard(rank, world)
         d_x = torch.from_numpy(x).cuda()
         d_s = torch.from_numpy(s).cuda()
         d_u = torch.empty(n * 3, dtype=torch.float64, device="cuda")
         rep = {}
 
-        def step_dev():
+        def step_dev():  # at N > 1 every rank returns the assembled u (NCCL inside the call)
             ctx.evaluate_device(plan, 3, n, d_x.data_ptr(), 0, 0, d_s.data_ptr(), g.FREE_SPACE, d_u.data_ptr(), rep)
-            if dist is not None:  # assemble the shards (evaluate_device returns after its stream drained)
-                dist.all_reduce(d_u, op=dist.ReduceOp.SUM)
 
-        tstream = stream if dist is None else torch.cuda.current_stream()
+        tstream = stream
 
         for _ in range(args.warmup):
             step_dev()
@@ -192,13 +194,6 @@ def run_ours(args, rank, world, local_rank):
         lib = g.lib()
 
         def step_host():
-            if dist is not None:  # host in, H2D, sharded evaluate, all-reduce, D2H
-                d_x.copy_(h_x, non_blocking=True)
-                d_s.copy_(h_s, non_blocking=True)
-                torch.cuda.current_stream().synchronize()
-                step_dev()
-                h_u.copy_(d_u)
-                return None
             r = g.sdmk_report()
             code = lib.sdmk_evaluate_with_plan(ctx._h, C.byref(cplan), 3, n, g._dptr(sys_.sources), 0, g._dptr(None),
                                                g._dptr(sys_.strengths), 0, g._dptr(h_u.numpy()), C.byref(r))
@@ -224,8 +219,6 @@ def run_ours(args, rank, world, local_rank):
         log(f"[bench] {kname}: {ms:.2f} ms/step device, {e2e_ms:.2f} ms/step e2e; report {r0}")
         del d_x, d_s, d_u
         torch.cuda.empty_cache()
-        if world > 1:
-            ctx.set_shard(0, 1)
 
     # roofline of the dominant kernel (FP64): measured DFMA peak on this GPU
     peak = ctx.fp64_peak_tflops()
@@ -283,7 +276,7 @@ def main():
     config = {"workload": f"metric: 3D free-space DMK, N={args.n:.0e} iid uniform in [-1/2,1/2]^3, eps={args.eps:g}, "
                           "prolate window, targets = sources",
               "kernels": args.kernels, "n_points": args.n, "eps": args.eps, "seed": args.seed,
-              "parallelism": (f"target-leaf shards x{world} (replicated tree + upward pass, NCCL all-reduce of u)"
+              "parallelism": (f"target-leaf shards x{world} (replicated tree; owner-local upward pass with NCCL halo exchange of outgoing expansions; NCCL all-reduce of u)"
                               if world > 1 else "single GPU"),
               "l2": "inputs (>=480 MB) and proxy grids (>10 GB) exceed the 126 MB L2; no flush needed"}
 

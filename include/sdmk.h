@@ -87,6 +87,9 @@ typedef struct sdmk_report {
   int32_t kernel_launches;
   double t_residual_kernel; /* residual kernel alone */
   double t_planewave;       /* forward/accumulate/inverse kernels of the downward pass */
+  double t_exchange;        /* multi-GPU: halo pack + exchange + unpack of outgoing expansions */
+  int64_t halo_bytes_sent;  /* multi-GPU: outgoing-expansion bytes this rank sent / received */
+  int64_t halo_bytes_recv;
 } sdmk_report;
 
 typedef struct sdmk_context sdmk_context;
@@ -168,6 +171,33 @@ int sdmk_direct_residual_sum(sdmk_context* ctx, const sdmk_plan* plan, int dim, 
    No reference counterpart (the reference is a single-process library). */
 int sdmk_set_shard(sdmk_context* ctx, int rank, int nranks);
 
+/* Distributed upward pass ("source halos exchanged").
+   sdmk_comm_unique_id on rank 0 (128 bytes, shared with the other ranks by
+   any means, e.g. torch.distributed), then sdmk_comm_init on every rank:
+   the context gets an NCCL communicator (libnccl.so.2 opened at run time)
+   and fixes (rank, nranks) as sdmk_set_shard would.  Evaluations then
+   (1) anterpolate and merge only this rank's cut subtrees (the tree is cut
+   into subtrees of <= N/(8 nranks) sources, dealt to ranks in Morton runs),
+   (2) exchange, in one NCCL group on the context stream, the outgoing
+   expansions every other rank reads (colleagues of its plane-wave targets)
+   plus all cut boxes, (3) merge the boxes above the cut on every rank, run
+   the sharded downward / far-field / residual passes, and (4) all-reduce u,
+   so every rank returns the full result, bitwise equal to nranks = 1. */
+int sdmk_comm_unique_id(unsigned char id[128]);
+int sdmk_comm_init(sdmk_context* ctx, int rank, int nranks, const unsigned char id[128]);
+/* The same evaluation without NCCL, in two halves, for tests and per-rank
+   timing on one GPU: with manual exchange on (and nranks > 1 from
+   sdmk_set_shard), sdmk_evaluate_begin runs everything up to the packed
+   halo; sdmk_halo_transfer(from, to) copies `from`'s slab for `to` into
+   `to`'s receive slab (device to device); sdmk_evaluate_end finishes and
+   writes u for this rank's targets only (zeros elsewhere; no all-reduce).
+   report->t_total then excludes the time between begin and end. */
+int sdmk_set_manual_exchange(sdmk_context* ctx, int on);
+int sdmk_evaluate_begin(sdmk_context* ctx, const sdmk_plan* plan, int dim, int64_t n_src, const double* src,
+                        int64_t n_tgt, const double* tgt, const double* str, int mode, int device_ptrs);
+int sdmk_halo_transfer(sdmk_context* from, sdmk_context* to);
+int sdmk_evaluate_end(sdmk_context* ctx, double* u, sdmk_report* report);
+
 /* ---- instrumentation ----
    the context's CUDA stream (cudaStream_t) so callers can time on it */
 int sdmk_get_stream(sdmk_context* ctx, void** stream);
@@ -192,6 +222,13 @@ int64_t sdmk_host_topology_dump(int dim, int periodic, int n_s, int p, int64_t n
    boxes whose incoming expansions the rank forms, target leaves in total */
 int sdmk_host_shard_plan(int dim, int periodic, int n_s, int p, int64_t n_src, const int32_t* q_src,
                          int64_t n_tgt, const int32_t* q_tgt, int rank, int nranks, int64_t* out);
+
+/* the exchange plan sdmk_comm_init evaluations use, from the same host
+   topology: out[f * nranks + r] = boxes rank r receives from rank f;
+   out[nranks^2 + r] = leaves with sources owned by rank r;
+   out[nranks^2 + nranks] = boxes above the cut; [.. + 1] = cut boxes */
+int sdmk_host_halo_plan(int dim, int periodic, int n_s, int p, int64_t n_src, const int32_t* q_src,
+                        int64_t n_tgt, const int32_t* q_tgt, int nranks, int64_t* out);
 
 #ifdef __cplusplus
 }

@@ -56,7 +56,8 @@ class sdmk_report(C.Structure):
                 ("t_root", C.c_double), ("t_downward", C.c_double), ("t_residual", C.c_double),
                 ("t_h2d", C.c_double), ("t_d2h", C.c_double), ("t_total", C.c_double),
                 ("p2p_candidates", C.c_int64), ("p2p_in_support", C.c_int64), ("kernel_launches", C.c_int32),
-                ("t_residual_kernel", C.c_double), ("t_planewave", C.c_double)]
+                ("t_residual_kernel", C.c_double), ("t_planewave", C.c_double), ("t_exchange", C.c_double),
+                ("halo_bytes_sent", C.c_int64), ("halo_bytes_recv", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -108,9 +109,18 @@ def lib():
             "sdmk_host_topology_dump": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, ip, C.c_int64, ip,
                                          C.c_char_p, C.c_int64], C.c_int64),
             "sdmk_set_shard": ([C.c_void_p, C.c_int, C.c_int], C.c_int),
+            "sdmk_comm_unique_id": ([C.c_char_p], C.c_int),
+            "sdmk_comm_init": ([C.c_void_p, C.c_int, C.c_int, C.c_char_p], C.c_int),
+            "sdmk_set_manual_exchange": ([C.c_void_p, C.c_int], C.c_int),
+            "sdmk_evaluate_begin": ([C.c_void_p, P(sdmk_plan), C.c_int, C.c_int64, C.c_void_p, C.c_int64,
+                                     C.c_void_p, C.c_void_p, C.c_int, C.c_int], C.c_int),
+            "sdmk_halo_transfer": ([C.c_void_p, C.c_void_p], C.c_int),
+            "sdmk_evaluate_end": ([C.c_void_p, C.c_void_p, P(sdmk_report)], C.c_int),
             "sdmk_direct_sum": ([C.c_void_p, C.c_int, C.c_int, C.c_int64, dp, C.c_int64, dp, dp, dp], C.c_int),
             "sdmk_direct_residual_sum": ([C.c_void_p, P(sdmk_plan), C.c_int, C.c_int64, dp, C.c_int64, dp, dp,
                                           C.c_double, C.c_int, dp], C.c_int),
+            "sdmk_host_halo_plan": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, ip, C.c_int64, ip, C.c_int,
+                                     P(C.c_int64)], C.c_int),
             "sdmk_host_shard_plan": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, ip, C.c_int64, ip, C.c_int,
                                       C.c_int, P(C.c_int64)], C.c_int),
         }
@@ -358,6 +368,57 @@ class Context:
         """Own a contiguous Morton run of target leaves (see include/sdmk.h)."""
         _raise(lib().sdmk_set_shard(self._h, int(rank), int(nranks)))
 
+    def comm_init(self, rank: int, nranks: int, uid: bytes):
+        """Attach an NCCL communicator (uid from comm_unique_id() on rank 0):
+        evaluations exchange outgoing-expansion halos and return the full u
+        on every rank (include/sdmk.h)."""
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        _raise(lib().sdmk_comm_init(self._h, int(rank), int(nranks), bytes(uid)))
+
+    def set_manual_exchange(self, on: bool = True):
+        """Two-phase evaluation without NCCL (tests, per-rank timing on one GPU)."""
+        _raise(lib().sdmk_set_manual_exchange(self._h, 1 if on else 0))
+
+    def evaluate_begin(self, plan: DmkPlan, sys: ParticleSystem, mode=FREE_SPACE):
+        """First half of a manual-exchange evaluation (host arrays; they are
+        copied before this returns)."""
+        src, tgt, stw = _arr(sys.sources), _arr(sys.targets), _arr(sys.strengths)
+        d = int(sys.dim)
+        ns, nt = src.size // d, tgt.size // d
+        self._pending = (d, ns, nt)
+        cp = plan.to_c()
+        _raise(lib().sdmk_evaluate_begin(self._h, C.byref(cp), d, ns, src.ctypes.data, nt,
+                                         tgt.ctypes.data if nt else None, stw.ctypes.data, _enum(mode, MODES), 0))
+
+    def evaluate_begin_device(self, plan: DmkPlan, dim: int, ns: int, d_src: int, nt: int, d_tgt: int,
+                              d_str: int, mode=FREE_SPACE):
+        """evaluate_begin with device addresses; finish with evaluate_end(d_u=...)."""
+        self._pending = (int(dim), int(ns), int(nt))
+        cp = plan.to_c()
+        _raise(lib().sdmk_evaluate_begin(self._h, C.byref(cp), int(dim), int(ns), C.c_void_p(d_src), int(nt),
+                                         C.c_void_p(d_tgt if nt else None), C.c_void_p(d_str), _enum(mode, MODES),
+                                         1))
+
+    def evaluate_end(self, report: Optional[dict] = None, d_u: Optional[int] = None):
+        """Second half: returns u (host) or writes it to the device address d_u
+        when the evaluation began with device pointers."""
+        d, ns, nt = self._pending
+        rep = sdmk_report()
+        if d_u is not None:
+            _raise(lib().sdmk_evaluate_end(self._h, C.c_void_p(d_u), C.byref(rep)))
+            u = None
+        else:
+            u = np.empty((nt if nt else ns) * d)
+            _raise(lib().sdmk_evaluate_end(self._h, u.ctypes.data, C.byref(rep)))
+        if report is not None:
+            report.update(rep.as_dict())
+        return u
+
+    def halo_transfer_to(self, other: "Context"):
+        """Copy this rank's halo slab for `other` into other's receive slab."""
+        _raise(lib().sdmk_halo_transfer(self._h, other._h))
+
     def stream_handle(self) -> int:
         """cudaStream_t of this context (for CUDA-event timing by the caller)."""
         s = C.c_void_p()
@@ -378,6 +439,13 @@ class Context:
 
 
 _default_ctx: Optional[Context] = None
+
+
+def comm_unique_id() -> bytes:
+    """NCCL unique id for Context.comm_init (call on rank 0, share the bytes)."""
+    buf = C.create_string_buffer(128)
+    _raise(lib().sdmk_comm_unique_id(buf))
+    return buf.raw
 
 
 def default_context() -> Context:
@@ -445,3 +513,22 @@ def host_shard_plan(dim, periodic, n_s, p, q_src_sorted, rank, nranks, q_tgt_sor
     _raise(lib().sdmk_host_shard_plan(dim, int(periodic), n_s, p, ns, _iptr(qs), nt, _iptr(qt), int(rank),
                                       int(nranks), out))
     return {"t0": out[0], "t1": out[1], "owned_leaves": out[2], "needed_boxes": out[3], "target_leaves": out[4]}
+
+
+def host_halo_plan(dim, periodic, n_s, p, q_src_sorted, nranks, q_tgt_sorted=None) -> dict:
+    """The exchange plan of comm_init evaluations (host topology, no GPU):
+    recv[f, r] = boxes rank r receives from rank f, owned leaves per rank,
+    boxes above the cut, cut boxes."""
+    qs = np.ascontiguousarray(np.asarray(q_src_sorted, np.int32).T.ravel())
+    ns = np.asarray(q_src_sorted).shape[0]
+    if q_tgt_sorted is not None and np.asarray(q_tgt_sorted).size:
+        qt = np.ascontiguousarray(np.asarray(q_tgt_sorted, np.int32).T.ravel())
+        nt = np.asarray(q_tgt_sorted).shape[0]
+    else:
+        qt, nt = None, 0
+    R = int(nranks)
+    out = (C.c_int64 * (R * R + R + 2))()
+    _raise(lib().sdmk_host_halo_plan(dim, int(periodic), n_s, p, ns, _iptr(qs), nt, _iptr(qt), R, out))
+    a = np.array(out[:], dtype=np.int64)
+    return {"recv": a[:R * R].reshape(R, R), "owned_leaves": a[R * R:R * R + R], "above_cut": int(a[R * R + R]),
+            "cut_boxes": int(a[R * R + R + 1])}

@@ -274,6 +274,57 @@ int sdmk_set_shard(sdmk_context* c, int rank, int nranks) {
   return guarded([&] { need_ctx(c)->set_shard(rank, nranks); });
 }
 
+int sdmk_comm_unique_id(unsigned char id[128]) {
+  return guarded([&] {
+    if (!id) throw InvalidArgument("sdmk_comm_unique_id: null output");
+    Comm::unique_id(id);
+  });
+}
+
+int sdmk_comm_init(sdmk_context* c, int rank, int nranks, const unsigned char id[128]) {
+  return guarded([&] {
+    if (!id) throw InvalidArgument("sdmk_comm_init: null id");
+    need_ctx(c)->comm_init(rank, nranks, id);
+  });
+}
+
+int sdmk_set_manual_exchange(sdmk_context* c, int on) {
+  return guarded([&] { need_ctx(c)->set_manual_exchange(on != 0); });
+}
+
+int sdmk_evaluate_begin(sdmk_context* c, const sdmk_plan* plan, int dim, int64_t ns, const double* src, int64_t nt,
+                        const double* tgt, const double* str, int mode, int device_ptrs) {
+  return guarded([&] {
+    if (!plan || !src || !str || (nt > 0 && !tgt)) throw InvalidArgument("sdmk_evaluate_begin: null pointer");
+    need_ctx(c)->evaluate_begin(to_plan(plan), dim, ns, src, nt, tgt, str, mode, device_ptrs != 0);
+  });
+}
+
+int sdmk_halo_transfer(sdmk_context* from, sdmk_context* to) {
+  return guarded([&] {
+    Context* a = need_ctx(from);
+    Context* b = need_ctx(to);
+    const int ra = a->shard_rank(), rb = b->shard_rank();
+    double *src = nullptr, *dst = nullptr;
+    int64_t ns = 0, nr = 0;
+    a->halo_slab(rb, false, &src, &ns);
+    b->halo_slab(ra, true, &dst, &nr);
+    if (ns != nr) throw InvalidArgument("sdmk_halo_transfer: slab sizes differ (different problems or shards?)");
+    if (ns > 0) {
+      cuda_check(cudaStreamSynchronize(a->stream()), "stream synchronize");
+      cuda_check(cudaMemcpyAsync(dst, src, sizeof(double) * ns, cudaMemcpyDefault, b->stream()), "halo copy");
+      cuda_check(cudaStreamSynchronize(b->stream()), "stream synchronize");
+    }
+  });
+}
+
+int sdmk_evaluate_end(sdmk_context* c, double* u, sdmk_report* rep) {
+  return guarded([&] {
+    if (!u) throw InvalidArgument("sdmk_evaluate_end: null output");
+    need_ctx(c)->evaluate_end(u, rep);
+  });
+}
+
 int sdmk_get_stream(sdmk_context* c, void** stream) {
   return guarded([&] { *stream = (void*)need_ctx(c)->stream(); });
 }
@@ -324,6 +375,28 @@ int sdmk_host_shard_plan(int dim, int periodic, int n_s, int p, int64_t ns, cons
     out[2] = (int64_t)sp.leaves.size();
     out[3] = need;
     out[4] = tl;
+  });
+}
+
+int sdmk_host_halo_plan(int dim, int periodic, int n_s, int p, int64_t ns, const int32_t* qs, int64_t nt,
+                        const int32_t* qt, int nranks, int64_t* out) {
+  return guarded([&] {
+    if (nranks < 1) throw InvalidArgument("halo plan: need nranks >= 1");
+    HostTree t = build_topology(dim, periodic != 0, n_s, p, (int)ns, qs, (int)nt, qt);
+    HaloPlan h = halo_owners(t, nranks);
+    halo_reads(t, h);
+    for (int f = 0; f < nranks; ++f)
+      for (int r = 0; r < nranks; ++r) out[f * nranks + r] = (int64_t)halo_boxes(h, f, r).size();
+    int64_t* o = out + nranks * nranks;
+    for (int r = 0; r < nranks; ++r) o[r] = 0;
+    int64_t above = 0, ncut = 0;
+    for (int b = 0; b < t.num_boxes(); ++b) {
+      if (h.owner[b] >= 0 && t.boxes[b].leaf) ++o[h.owner[b]];
+      above += h.owner[b] == -1;
+      ncut += h.cut[b];
+    }
+    o[nranks] = above;
+    o[nranks + 1] = ncut;
   });
 }
 

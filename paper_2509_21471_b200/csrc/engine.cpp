@@ -252,9 +252,35 @@ void Context::copy_out(void* dst, const void* src, size_t bytes) {
 
 void Context::set_shard(int rank, int nranks) {
   if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("set_shard: need 0 <= rank < nranks");
+  if (comm_ && (rank != comm_->rank() || nranks != comm_->nranks()))
+    throw InvalidArgument("set_shard: the context's communicator fixes rank and nranks");
   rank_ = rank;
   nranks_ = nranks;
   prob_.ready = false;  // lists depend on the shard
+}
+
+void Context::comm_init(int rank, int nranks, const unsigned char* id) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  comm_.reset();
+  comm_ = std::make_unique<Comm>(rank, nranks, id, device_);
+  rank_ = rank;
+  nranks_ = nranks;
+  prob_.ready = false;
+}
+
+void Context::set_manual_exchange(bool on) {
+  manual_x_ = on;
+  prob_.ready = false;
+}
+
+void Context::halo_slab(int peer, bool recv, double** ptr, int64_t* count) {
+  const Problem& pr = prob_;
+  if (!begun_ || !pr.halo) throw InvalidArgument("halo_slab: no evaluation between evaluate_begin and evaluate_end");
+  if (peer < 0 || peer >= nranks_) throw InvalidArgument("halo_slab: bad peer");
+  const std::vector<int64_t>& off = recv ? pr.recv_off : pr.send_off;
+  double* base = arena_.as<double>(recv ? "halo_recv" : "halo_send", 1);
+  *ptr = base + off[peer];
+  *count = off[peer + 1] - off[peer];
 }
 
 double Context::ev_ms(int a, int b) {
@@ -652,20 +678,27 @@ void Context::upload_tree_lists_a() {
     o.side = t.side(b);
     o.half = 0.5 * o.side;
   }
+  // halo mode: this rank anterpolates and merges its own cut subtrees; the
+  // boxes above the cut are merged after the exchange (top lists)
+  pr.halo = halo_run_;
+  if (pr.halo) pr.hp = halo_owners(t, nranks_);
+  else pr.hp = HaloPlan{};
+  auto mine = [&](int b) { return !pr.halo || pr.hp.owner[b] == rank_; };
   std::vector<int> ant;
   for (int b = 0; b < nb; ++b)
-    if (t.boxes[b].leaf && t.nsrc(b) > 0) ant.push_back(b);
+    if (t.boxes[b].leaf && t.nsrc(b) > 0 && mine(b)) ant.push_back(b);
   const int L = t.max_level + 1;
-  std::vector<std::vector<int>> m_out(L), m_in(L), m_ci(L);
+  std::vector<std::vector<int>> m_out(L), m_in(L), m_ci(L), u_out(L), u_in(L), u_ci(L);
   for (int lev = 0; lev < L; ++lev)
     for (int b : t.level_boxes[lev]) {
       const Box& x = t.boxes[b];
-      if (!x.leaf && t.nsrc(b) > 0) {  // upward merge (dmk.cpp:638-651)
-        m_out[lev].push_back(b);
+      if (!x.leaf && t.nsrc(b) > 0 && (mine(b) || pr.hp.owner[b] == -1)) {  // upward merge (dmk.cpp:638-651)
+        const bool top = !mine(b);
+        (top ? u_out : m_out)[lev].push_back(b);
         for (int ci = 0; ci < nchild; ++ci) {
           int c = x.first_child + ci;
-          m_in[lev].push_back(t.nsrc(c) > 0 ? c : -1);
-          m_ci[lev].push_back(ci);
+          (top ? u_in : m_in)[lev].push_back(t.nsrc(c) > 0 ? c : -1);
+          (top ? u_ci : m_ci)[lev].push_back(ci);
         }
       }
     }
@@ -682,8 +715,10 @@ void Context::upload_tree_lists_a() {
   blob.insert(blob.end(), m1.begin(), m1.end());
   Packer pk;
   const size_t o_blob = pk.add(blob), o_boxes = pk.add(boxes), o_ant = pk.add(ant);
-  std::vector<std::array<size_t, 3>> off(L);
-  for (int lev = 0; lev < L; ++lev) off[lev] = {pk.add(m_out[lev]), pk.add(m_in[lev]), pk.add(m_ci[lev])};
+  std::vector<std::array<size_t, 6>> off(L);
+  for (int lev = 0; lev < L; ++lev)
+    off[lev] = {pk.add(m_out[lev]), pk.add(m_in[lev]), pk.add(m_ci[lev]),
+                pk.add(u_out[lev]), pk.add(u_in[lev]), pk.add(u_ci[lev])};
   char* h = (char*)pinned_.get("treeA", pk.total + 64);
   for (auto& it : pk.items)
     if (it.bytes) std::memcpy(h + it.off, it.src, it.bytes);
@@ -704,6 +739,10 @@ void Context::upload_tree_lists_a() {
     X.merge_out = (int*)(dv + off[lev][0]);
     X.merge_in = (int*)(dv + off[lev][1]);
     X.merge_ci = (int*)(dv + off[lev][2]);
+    X.n_top = (int)u_out[lev].size();
+    X.top_out = (int*)(dv + off[lev][3]);
+    X.top_in = (int*)(dv + off[lev][4]);
+    X.top_ci = (int*)(dv + off[lev][5]);
   }
 }
 
@@ -717,6 +756,22 @@ void Context::upload_tree_lists_b() {
   ShardPlan sp = shard_plan(t, rank_, nranks_);
   const std::vector<int>& itp = sp.leaves;
   const std::vector<char>& need = sp.need;
+  // halo mode: what this rank reads, and the exchange lists
+  std::vector<int> send_ids, recv_ids;
+  if (pr.halo) {
+    halo_reads(t, pr.hp);
+    const int64_t elems = (int64_t)pr.nch * (d == 3 ? pr.plan.p : 1) * pr.plan.p * pr.plan.p;
+    pr.send_off.assign(nranks_ + 1, 0);
+    pr.recv_off.assign(nranks_ + 1, 0);
+    for (int q = 0; q < nranks_; ++q) {
+      std::vector<int> sv = halo_boxes(pr.hp, rank_, q), rv = halo_boxes(pr.hp, q, rank_);
+      send_ids.insert(send_ids.end(), sv.begin(), sv.end());
+      recv_ids.insert(recv_ids.end(), rv.begin(), rv.end());
+      pr.send_off[q + 1] = (int64_t)send_ids.size() * elems;
+      pr.recv_off[q + 1] = (int64_t)recv_ids.size() * elems;
+    }
+  }
+  auto reads = [&](int b) { return !pr.halo || pr.hp.reads[rank_][b]; };
   pr.t_own0 = sp.t0;
   pr.t_own1 = sp.t1;
   // near ranges per target leaf (dmk.cpp:966-990); two-pass CSR, parallel over leaves
@@ -779,7 +834,7 @@ void Context::upload_tree_lists_b() {
         }
         if ((int)V.i_in.size() > first) V.i_seg.push_back(first);  // this parent's pairs
       }
-      if (t.nsrc(b) > 0) {
+      if (t.nsrc(b) > 0 && reads(b)) {  // forward transforms of the boxes this rank reads
         gslot[b] = (int)V.sbx.size();
         V.sbx.push_back(b);
       }
@@ -849,7 +904,7 @@ void Context::upload_tree_lists_b() {
     }
   }
   Packer pk;
-  size_t o_chunks = pk.add(chunks);
+  size_t o_chunks = pk.add(chunks), o_send = pk.add(send_ids), o_recv = pk.add(recv_ids);
   size_t o_itp = pk.add(itp), o_rs = pk.add(rs), o_rbox = pk.add(rbox), o_rinfo = pk.add(rinfo),
          o_rid = pk.add(root_ids), o_res = pk.add(root_es), o_rsl = pk.add(root_slot), o_rta = pk.add(root_tau);
   struct Off {
@@ -868,6 +923,10 @@ void Context::upload_tree_lists_b() {
     if (it.bytes) std::memcpy(h + it.off, it.src, it.bytes);
   char* dv = (char*)arena_.get("treeB", pk.total + 64);
   cuda_check(cudaMemcpyAsync(dv, h, pk.total, cudaMemcpyHostToDevice, st_), "tree upload");
+  pr.send_ids = (int*)(dv + o_send);
+  pr.recv_ids = (int*)(dv + o_recv);
+  pr.n_send = (int)send_ids.size();
+  pr.n_recv = (int)recv_ids.size();
   pr.int_leaves = (int*)(dv + o_itp);
   pr.n_int = (int)itp.size();
   pr.rng_start = (int*)(dv + o_rs);
@@ -935,6 +994,24 @@ void Context::run_upward() {  // dmk.cpp:555-655
       launch_tensor_mma(p, mats_up_, X.merge_in, X.merge_out, X.merge_ci, X.n_merge, pr.nch, og, og, 2, d, st_);
     else
       launch_tensor_apply(p, pz, d, mats_up_, X.merge_in, X.merge_out, X.merge_ci, X.n_merge, pr.nch, og, og, 2, st_);
+    ++launches_;
+  }
+  cuda_check(cudaPeekAtLastError(), "kernel launch");
+}
+
+// Halo mode: the boxes above the cut, from the gathered cut boxes (the same
+// per-parent merge as run_upward, so every rank forms them bit for bit alike).
+void Context::run_upward_top() {
+  Problem& pr = prob_;
+  const int d = pr.dim, p = pr.plan.p, pz = d == 3 ? p : 1;
+  double* og = arena_.as<double>("outgoing", 1);
+  for (int lev = pr.tree.max_level - 1; lev >= 0; --lev) {
+    const Problem::LevelLists& X = pr.levels[lev];
+    if (X.n_top == 0) continue;
+    if (tensor_mma_supported(p, d))
+      launch_tensor_mma(p, mats_up_, X.top_in, X.top_out, X.top_ci, X.n_top, pr.nch, og, og, 2, d, st_);
+    else
+      launch_tensor_apply(p, pz, d, mats_up_, X.top_in, X.top_out, X.top_ci, X.n_top, pr.nch, og, og, 2, st_);
     ++launches_;
   }
   cuda_check(cudaPeekAtLastError(), "kernel launch");
@@ -1090,7 +1167,7 @@ void Context::run_target_far(double* ufar) {  // dmk.cpp:861-915
   if (mma_anterp_supported(p)) {
     // alias targets reuse the source bases computed by the upward pass
     const double* tb = nullptr;
-    if (pr.alias) {
+    if (pr.alias && !pr.halo) {  // (halo mode: this rank's source leaves are not its target leaves)
       tb = arena_.as<double>("basis_s", (size_t)3 * pr.ns * p);
     } else {
       double* b = arena_.as<double>("basis_t", (size_t)3 * pr.nt * p);
@@ -1166,7 +1243,19 @@ void Context::run_residual(double* ures, bool stats) {  // dmk.cpp:919-1032
 // ------------------------------------------------------------- entries --
 void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, int64_t nt, const double* tgt,
                        const double* str, int mode, double* u, sdmk_report* rep, bool device_ptrs) {
+  if (manual_x_ && nranks_ > 1) throw InvalidArgument("evaluate: manual exchange mode needs evaluate_begin/end");
+  evaluate_begin(P, dim, ns, src, nt, tgt, str, mode, device_ptrs);
+  if (prob_.halo) {  // NCCL point-to-point exchange of the packed halo slabs, on the stream
+    comm_->exchange(arena_.as<double>("halo_send", 1), prob_.send_off, arena_.as<double>("halo_recv", 1),
+                    prob_.recv_off, st_);
+  }
+  evaluate_end(u, rep);
+}
+
+void Context::evaluate_begin(const Plan& P, int dim, int64_t ns, const double* src, int64_t nt, const double* tgt,
+                             const double* str, int mode, bool device_ptrs) {
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  begun_ = false;
   check_inputs(P, dim, ns, nt, mode);
   tab_ = &tables_for(P);
   if (tab_->kernel != P.kernel || tab_->dim != P.dim || tab_->win.kind != P.window)
@@ -1175,6 +1264,8 @@ void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, in
   const int sc = strength_width(P.kernel, dim);
   const bool alias = nt == 0;
   const int ntt = alias ? (int)ns : (int)nt;
+  call_ = Call{dim, sc, ntt, ns, nt, alias, device_ptrs};
+  halo_run_ = nranks_ > 1 && (comm_ || manual_x_);
   cudaEventRecord(ev_[0], st_);
   copy_in(arena_.as<double>("src_in", (size_t)ns * dim), src, sizeof(double) * ns * dim, device_ptrs);
   if (!alias) copy_in(arena_.as<double>("tgt_in", (size_t)nt * dim), tgt, sizeof(double) * nt * dim, device_ptrs);
@@ -1191,16 +1282,51 @@ void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, in
     copy_in(arena_.as<double>("str_in", (size_t)ns * sc), str, sizeof(double) * ns * sc, device_ptrs);
   }
   cudaEventRecord(ev_[1], st_);
-  build_problem(P, dim, (int)ns, (int)nt, mode, true);
-  cudaEventRecord(ev_[2], st_);
   zero_all_ = false;  // only the evaluated outputs are returned
+  try {
+    build_problem(P, dim, (int)ns, (int)nt, mode, true);
+    cudaEventRecord(ev_[2], st_);
+    run_upward();
+    cudaEventRecord(ev_[3], st_);
+    upload_tree_lists_b();  // host work overlaps the upward pass on the GPU
+    cudaEventRecord(ev_[8], st_);
+    if (prob_.halo) {
+      const Problem& pr = prob_;
+      const int64_t elems = (int64_t)pr.nch * (dim == 3 ? P.p : 1) * P.p * P.p;
+      double* snd = arena_.as<double>("halo_send", (size_t)pr.send_off[nranks_]);
+      arena_.as<double>("halo_recv", (size_t)pr.recv_off[nranks_]);
+      launch_copy_boxes(pr.n_send, pr.send_ids, arena_.as<double>("outgoing", 1), nullptr, snd, elems, st_);
+      ++launches_;
+    }
+    cudaEventRecord(ev_[10], st_);
+  } catch (...) {
+    zero_all_ = true;
+    throw;
+  }
+  begun_ = true;
+}
+
+void Context::evaluate_end(double* u, sdmk_report* rep) {
+  if (!begun_) throw InvalidArgument("evaluate_end: no evaluate_begin in flight");
+  begun_ = false;
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   struct Restore {
     bool& f;
     ~Restore() { f = true; }
   } restore{zero_all_};
-  run_upward();
-  cudaEventRecord(ev_[3], st_);
-  upload_tree_lists_b();  // host work overlaps the upward pass on the GPU
+  const Plan& P = prob_.plan;
+  const int dim = call_.dim, ntt = call_.ntt;
+  const bool device_ptrs = call_.device_ptrs;
+  cudaEventRecord(ev_[11], st_);
+  if (prob_.halo) {
+    const Problem& pr = prob_;
+    const int64_t elems = (int64_t)pr.nch * (dim == 3 ? P.p : 1) * P.p * P.p;
+    launch_copy_boxes(pr.n_recv, nullptr, arena_.as<double>("halo_recv", 1), pr.recv_ids,
+                      arena_.as<double>("outgoing", 1), elems, st_);
+    ++launches_;
+  }
+  cudaEventRecord(ev_[9], st_);
+  if (prob_.halo) run_upward_top();
   run_root();
   cudaEventRecord(ev_[4], st_);
   double* ufar = arena_.as<double>("ufar", (size_t)ntt * dim);
@@ -1238,6 +1364,9 @@ void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, in
   double* du = device_ptrs ? u : arena_.as<double>("u", (size_t)ntt * dim);
   launch_combine(ntt, dim, ufar, ures, corr, corr_scale, zm, pr.tpts_caller, own, du, st_);
   ++launches_;
+  // with a communicator every rank returns the assembled u (each element has
+  // one owner; the others add exact zeros)
+  if (comm_ && nranks_ > 1) comm_->allreduce_sum(du, (size_t)ntt * dim, st_);
   cudaEventRecord(ev_[6], st_);
   if (!device_ptrs) copy_out(u, du, sizeof(double) * ntt * dim);
   cudaEventRecord(ev_[7], st_);
@@ -1253,23 +1382,30 @@ void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, in
   cuda_check(cudaGetLastError(), "kernel launch");
   if (hflags[3]) throw DomainError("residual_pass: coincident points");
   if (rep) {
+    // between evaluate_begin and evaluate_end: the exchange (NCCL) or the
+    // caller's transfers (manual mode, excluded from t_total)
+    const double gap = ev_ms(10, 11), xfer = ev_ms(8, 10) + ev_ms(11, 9);
+    const bool manual = !comm_;
     rep->num_boxes = pr.tree.num_boxes();
     rep->max_level = pr.tree.max_level;
-    rep->num_sources = (int)ns;
+    rep->num_sources = (int)call_.ns;
     rep->num_targets = ntt;
     rep->t_h2d = ev_ms(0, 1) * 1e-3;
     rep->t_tree = ev_ms(1, 2) * 1e-3;
     rep->t_upward = ev_ms(2, 3) * 1e-3;
-    rep->t_root = ev_ms(3, 4) * 1e-3;
+    rep->t_root = (ev_ms(3, 4) - ev_ms(8, 9)) * 1e-3;
     rep->t_downward = ev_ms(4, 5) * 1e-3;
     rep->t_residual = ev_ms(5, 6) * 1e-3;
     rep->t_d2h = ev_ms(6, 7) * 1e-3;
-    rep->t_total = ev_ms(0, 7) * 1e-3;
+    rep->t_total = (ev_ms(0, 7) - (manual ? gap : 0.0)) * 1e-3;
     rep->t_residual_kernel = ev_ms(13, 12) * 1e-3;
     rep->t_planewave = planewave_ms() * 1e-3;
     rep->p2p_candidates = (int64_t)hst[0];
     rep->p2p_in_support = (int64_t)hst[1];
     rep->kernel_launches = launches_;
+    rep->t_exchange = pr.halo ? (manual ? xfer : ev_ms(8, 9)) * 1e-3 : 0.0;
+    rep->halo_bytes_sent = pr.halo ? pr.send_off[nranks_] * (int64_t)sizeof(double) : 0;
+    rep->halo_bytes_recv = pr.halo ? pr.recv_off[nranks_] * (int64_t)sizeof(double) : 0;
   }
 }
 
@@ -1277,6 +1413,8 @@ void Context::setup(const Plan& P, int dim, int64_t ns, const double* src, int64
                     const double* str, int mode) {
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   prob_.ready = false;
+  begun_ = false;
+  halo_run_ = false;  // the pass-level API keeps the replicated upward pass
   check_inputs(P, dim, ns, nt, mode);
   tab_ = &tables_for(P);
   const int sc = strength_width(P.kernel, dim);

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/sdmk.h"
+#include "host/comm.hpp"
 #include "host/setup.hpp"
 #include "host/tree.hpp"
 #include "kernels/launch.hpp"
@@ -78,12 +79,22 @@ struct Problem {
   int n_ant = 0, n_int = 0;
   int *rng_start = nullptr, *rng_box = nullptr, *rng_info = nullptr, *subrange = nullptr;
   int64_t t_own0 = 0, t_own1 = 0;  // owned range of Morton-sorted targets (set_shard)
+  // distributed upward pass (multi-GPU with an exchange): each rank forms the
+  // outgoing expansions of its own cut subtrees, receives the halo it reads
+  // and every cut box, and merges the boxes above the cut itself
+  bool halo = false;
+  HaloPlan hp;
+  std::vector<int64_t> send_off, recv_off;  // per peer, in doubles
+  int *send_ids = nullptr, *recv_ids = nullptr;
+  int n_send = 0, n_recv = 0;
   bool lists_b = false;            // downward / residual lists uploaded
   int* res_chunks = nullptr;       // (leaf index, first target) per 32-target residual chunk
   int n_chunks = 0;
   struct LevelLists {
     int n_merge = 0, n_interp = 0, n_src = 0, n_tgt = 0;
     int *merge_out = nullptr, *merge_in = nullptr, *merge_ci = nullptr;
+    int n_top = 0;  // merges above the cut (halo mode), after the exchange
+    int *top_out = nullptr, *top_in = nullptr, *top_ci = nullptr;
     int *interp_in = nullptr, *interp_out = nullptr, *interp_ci = nullptr, *interp_seg = nullptr;
     int n_interp_seg = 0;
     int *src_boxes = nullptr, *tgt_boxes = nullptr;
@@ -107,6 +118,20 @@ class Context {
   // contiguous Morton run of target leaves; outputs of other ranks' targets
   // are written as zeros, so a sum over ranks assembles the full result.
   void set_shard(int rank, int nranks);
+  // NCCL communicator of this rank (one process per GPU): evaluations then
+  // exchange outgoing expansions instead of replicating the upward pass, and
+  // return the assembled u on every rank (all-reduce on the context stream).
+  void comm_init(int rank, int nranks, const unsigned char* id);
+  // Test / projection mode without NCCL: evaluate_begin stops after packing
+  // the halo, the caller moves the slabs (halo_transfer), evaluate_end
+  // finishes; u holds this rank's targets only (zeros elsewhere).
+  void set_manual_exchange(bool on);
+  void evaluate_begin(const Plan& plan, int dim, int64_t ns, const double* src, int64_t nt, const double* tgt,
+                      const double* str, int mode, bool device_ptrs);
+  void evaluate_end(double* u, sdmk_report* rep);
+  // device slab this rank sends to / receives from `peer` (count in doubles)
+  void halo_slab(int peer, bool recv, double** ptr, int64_t* count);
+  int shard_rank() const { return rank_; }
 
   // Host-pointer evaluation; u may be host memory.  report may be null.
   void evaluate(const Plan& plan, int dim, int64_t ns, const double* src, int64_t nt, const double* tgt,
@@ -136,6 +161,7 @@ class Context {
   void upload_tree_lists_a();
   void upload_tree_lists_b();
   void run_upward();
+  void run_upward_top();
   void run_root();
   void run_downward();
   void run_target_far(double* ufar);
@@ -167,6 +193,15 @@ class Context {
   int pw_used_ = 0;
   double planewave_ms();
   int rank_ = 0, nranks_ = 1;
+  std::unique_ptr<Comm> comm_;
+  bool manual_x_ = false;
+  bool halo_run_ = false;  // the current evaluation exchanges outgoing expansions
+  bool begun_ = false;     // between evaluate_begin and evaluate_end
+  struct Call {
+    int dim = 3, sc = 3, ntt = 0;
+    int64_t ns = 0, nt = 0;
+    bool alias = true, device_ptrs = false;
+  } call_;
   bool zero_all_ = true;  // zero whole proxy arrays (pass-level API returns them)
   const int32_t* hq_ = nullptr;  // pinned sorted quantized coordinates of the current problem
   unsigned long long stats_[3] = {0, 0, 0};

@@ -592,4 +592,73 @@ ShardPlan shard_plan(const HostTree& t, int rank, int nranks) {
   return sp;
 }
 
+HaloPlan halo_owners(const HostTree& t, int nranks) {
+  HaloPlan h;
+  h.nranks = nranks < 1 ? 1 : nranks;
+  const int nb = t.num_boxes();
+  h.owner.assign(nb, -2);
+  h.cut.assign(nb, 0);
+  const int64_t total = t.nsrc(0);
+  const int64_t thr = std::max<int64_t>(1, total / (8 * (int64_t)h.nranks));
+  // cut boxes in DFS order of the subdivision = increasing source ranges
+  std::vector<int> cutv, stack = {0};
+  while (!stack.empty()) {
+    const int b = stack.back();
+    stack.pop_back();
+    if (t.nsrc(b) == 0) continue;
+    const Box& x = t.boxes[b];
+    if (!x.leaf && t.nsrc(b) > thr && h.nranks > 1) {
+      h.owner[b] = -1;
+      for (int ci = (1 << t.dim) - 1; ci >= 0; --ci) stack.push_back(x.first_child + ci);
+    } else {
+      cutv.push_back(b);
+    }
+  }
+  std::sort(cutv.begin(), cutv.end(), [&](int a, int b) { return t.boxes[a].sb < t.boxes[b].sb; });
+  int64_t start = 0;
+  for (int b : cutv) {
+    const int64_t n = t.nsrc(b);
+    const int r = h.nranks == 1 ? 0 : (int)std::min<int64_t>(h.nranks - 1, ((2 * start + n) * h.nranks) / (2 * total));
+    start += n;
+    h.cut[b] = 1;
+    // the whole subtree (boxes with sources)
+    std::vector<int> st = {b};
+    while (!st.empty()) {
+      const int x = st.back();
+      st.pop_back();
+      if (t.nsrc(x) == 0) continue;
+      h.owner[x] = r;
+      if (!t.boxes[x].leaf)
+        for (int ci = 0; ci < (1 << t.dim); ++ci) st.push_back(t.boxes[x].first_child + ci);
+    }
+  }
+  return h;
+}
+
+void halo_reads(const HostTree& t, HaloPlan& h) {
+  const int nb = t.num_boxes();
+  h.reads.assign(h.nranks, std::vector<char>(nb, 0));
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int r = 0; r < h.nranks; ++r) {
+    const ShardPlan sp = shard_plan(t, r, h.nranks);
+    std::vector<char>& rd = h.reads[r];
+    // plane-wave targets of rank r (the entries of upload_tree_lists_b, dmk.cpp:760-797)
+    for (int b = 0; b < nb; ++b) {
+      const int par = t.boxes[b].parent;
+      if (t.ntgt(b) == 0 || !sp.need[par >= 0 ? par : b]) continue;
+      for (const Nbr& e : t.col[b])
+        if (t.nsrc(e.box) > 0) rd[e.box] = 1;
+    }
+  }
+}
+
+std::vector<int> halo_boxes(const HaloPlan& h, int from, int to) {
+  std::vector<int> v;
+  if (from == to) return v;
+  const int nb = (int)h.owner.size();
+  for (int b = 0; b < nb; ++b)
+    if (h.owner[b] == from && (h.cut[b] || (!h.reads.empty() && h.reads[to][b]))) v.push_back(b);
+  return v;
+}
+
 }  // namespace sdmkb

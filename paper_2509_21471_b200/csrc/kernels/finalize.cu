@@ -80,7 +80,25 @@ __global__ void k_own_mask(int nt, const int* __restrict__ tperm, int64_t t0, in
     own[tperm[s]] = (s >= t0 && s < t1) ? 1 : 0;
 }
 
+// Halo pack / unpack of whole boxes: dst box i = src box i, where a null
+// id list means the boxes are contiguous from 0.  One CTA per box, a
+// grid-stride over its elements (coalesced; the halo is a few % of the proxies).
+__global__ void k_copy_boxes(int n, const int* __restrict__ src_ids, const double* __restrict__ src,
+                             const int* __restrict__ dst_ids, double* __restrict__ dst, int64_t elems) {
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const double* s = src + (src_ids ? (int64_t)src_ids[i] : (int64_t)i) * elems;
+    double* d = dst + (dst_ids ? (int64_t)dst_ids[i] : (int64_t)i) * elems;
+    for (int64_t k = threadIdx.x; k < elems; k += blockDim.x) d[k] = s[k];
+  }
+}
+
 }  // namespace
+
+void launch_copy_boxes(int n, const int* src_ids, const double* src, const int* dst_ids, double* dst, int64_t elems,
+                       cudaStream_t st) {
+  if (n <= 0) return;
+  k_copy_boxes<<<n < 148 * 8 ? n : 148 * 8, 512, 0, st>>>(n, src_ids, src, dst_ids, dst, elems);
+}
 
 void launch_column_sums(const double* soa, int n, int ncomp, double* sums, double* scratch, cudaStream_t st) {
   k_partial<<<kSumBlocks, kSumThreads, 0, st>>>(0, soa, nullptr, n, ncomp, 0, scratch);

@@ -184,6 +184,9 @@ void launch_combine(int nt, int dim, const double* ufar, const double* ures, con
                     cudaStream_t st);
 // own[tperm[s]] = (t0 <= s < t1): the caller-order mask of a shard's targets
 void launch_own_mask(int nt, const int* tperm, int64_t t0, int64_t t1, unsigned char* own, cudaStream_t st);
+// dst box (dst_ids ? dst_ids[i] : i) = src box (src_ids ? src_ids[i] : i), boxes of `elems` doubles
+void launch_copy_boxes(int n, const int* src_ids, const double* src, const int* dst_ids, double* dst, int64_t elems,
+                       cudaStream_t st);
 
 // ---- direct.cu: O(N*M) reference sums (oracle.cpp:143-241) ---------------------
 constexpr int kDirectMaxCheb = 1024;

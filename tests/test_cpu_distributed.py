@@ -66,8 +66,20 @@ def _worker(rank, world, port, qs, out_q):
     part = torch.zeros_like(full)
     part[plan["t0"]:plan["t1"]] = full[plan["t0"]:plan["t1"]]
     dist.all_reduce(part, op=dist.ReduceOp.SUM)
+    # the halo exchange plan of the distributed upward pass: the same on both
+    # processes, and its send / receive sizes pair up in an all-to-all (the
+    # shape of the library's NCCL group of sends and receives)
+    h = g.host_halo_plan(3, False, 300, 10, qs, world)
+    hs = [None] * world
+    dist.all_gather_object(hs, h["recv"].tolist())
+    send = [int(h["recv"][rank, q]) for q in range(world)]
+    recv = [int(h["recv"][f, rank]) for f in range(world)]
+    payload = torch.full((sum(send),), float(rank + 1), dtype=torch.float64)
+    got = torch.empty(sum(recv), dtype=torch.float64)
+    dist.all_to_all_single(got, payload, output_split_sizes=recv, input_split_sizes=send)
+    ok_x = hs[0] == hs[1] and bool((got == float(2 - rank)).all()) and sum(recv) > 0
     if rank == 0:
-        out_q.put((plans, bool(torch.equal(part, full))))
+        out_q.put((plans, bool(torch.equal(part, full)) and ok_x))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -86,3 +98,124 @@ def test_gloo_world2_assembles_full_result():
         assert p.exitcode == 0
     assert equal
     assert plans[0]["t0"] == 0 and plans[0]["t1"] == plans[1]["t0"] and plans[1]["t1"] == qs.shape[0]
+
+
+# ---- distributed upward pass: the exchange plan, restated from the tree dump ----
+
+def _parse_dump(text):
+    boxes = []
+    for line in text.splitlines()[1:]:
+        f = line.split()
+        lev = int(f[1][1:])
+        anc = tuple(int(v) for v in f[2][2:].split(","))
+        sb, se = (int(v) for v in f[4][5:-1].split(","))
+        tb, te = (int(v) for v in f[5][5:-1].split(","))
+        col = line[line.index("col={") + 5:line.index("}", line.index("col={"))]
+        cols = [int(e.split("@")[0]) for e in col.split()] if col else []
+        boxes.append(dict(level=lev, a=anc, leaf=f[3] == "leaf", ns=se - sb, nt=te - tb, sb=sb, tb=tb, col=cols))
+    key = {(b["level"], b["a"]): i for i, b in enumerate(boxes)}
+    for i, b in enumerate(boxes):
+        b["children"] = []
+        if b["level"] == 0:
+            b["parent"] = -1
+            continue
+        side = 1 << (30 - b["level"] + 1)
+        b["parent"] = key[(b["level"] - 1, tuple(v - v % side for v in b["a"]))]
+    for i, b in enumerate(boxes):
+        if b["parent"] >= 0:
+            boxes[b["parent"]]["children"].append(i)
+    return boxes
+
+
+def _halo_plan_restated(boxes, R_):
+    """include/sdmk.h sdmk_comm_init: cut subtrees of <= N/(8R) sources dealt
+    to ranks by source midpoint; rank r reads the colleagues of its plane-wave
+    targets (targets whose parent it needs, the shard plan); it receives from
+    f every box f owns that it reads, and every cut box."""
+    total = boxes[0]["ns"]
+    thr = max(1, total // (8 * R_))
+    owner = [-2] * len(boxes)
+    cut, stack = [], [0]
+    while stack:
+        b = stack.pop()
+        if boxes[b]["ns"] == 0:
+            continue
+        if not boxes[b]["leaf"] and boxes[b]["ns"] > thr and R_ > 1:
+            owner[b] = -1
+            stack += boxes[b]["children"]
+        else:
+            cut.append(b)
+    cut.sort(key=lambda b: boxes[b]["sb"])
+    start = 0
+    for c in cut:
+        n = boxes[c]["ns"]
+        r = 0 if R_ == 1 else min(R_ - 1, ((2 * start + n) * R_) // (2 * total))
+        start += n
+        st = [c]
+        while st:
+            x = st.pop()
+            if boxes[x]["ns"]:
+                owner[x] = r
+                st += boxes[x]["children"]
+    # target shards (host shard plan): leaves by target start, midpoint rule
+    tl = sorted((i for i, b in enumerate(boxes) if b["leaf"] and b["nt"] > 0), key=lambda i: boxes[i]["tb"])
+    tt = sum(boxes[i]["nt"] for i in tl)
+    need = [[False] * len(boxes) for _ in range(R_)]
+    s0 = 0
+    for i in tl:
+        n = boxes[i]["nt"]
+        r = 0 if R_ == 1 else min(R_ - 1, ((2 * s0 + n) * R_) // (2 * tt))
+        s0 += n
+        x = i
+        while x >= 0 and not need[r][x]:
+            need[r][x] = True
+            x = boxes[x]["parent"]
+    reads = [[False] * len(boxes) for _ in range(R_)]
+    for r in range(R_):
+        for i, b in enumerate(boxes):
+            par = b["parent"]
+            if b["nt"] and need[r][par if par >= 0 else i]:
+                for c in b["col"]:
+                    if boxes[c]["ns"]:
+                        reads[r][c] = True
+    cutset = set(cut)
+    recv = np.zeros((R_, R_), np.int64)
+    for f in range(R_):
+        for r in range(R_):
+            if f != r:
+                recv[f, r] = sum(1 for i in range(len(boxes)) if owner[i] == f and (i in cutset or reads[r][i]))
+    owned = np.array([sum(1 for i, b in enumerate(boxes) if b["leaf"] and owner[i] == r) for r in range(R_)])
+    # closure: every box a rank reads is its own, above the cut, or received;
+    # every box above the cut has all its children with sources available
+    for r in range(R_):
+        for i in range(len(boxes)):
+            if reads[r][i]:
+                assert owner[i] >= -1
+    return recv, owned, sum(1 for o in owner if o == -1), len(cut), owner
+
+
+@pytest.mark.parametrize("nranks,periodic,n_s", [(2, False, 300), (3, False, 300), (8, False, 120), (4, True, 200)])
+def test_halo_plan_matches_restatement(nranks, periodic, n_s):
+    qs = _points(20000, seed=nranks)
+    h = g.host_halo_plan(3, periodic, n_s, 10, qs, nranks)
+    boxes = _parse_dump(g.host_topology_dump(3, periodic, n_s, 10, qs))
+    recv, owned, above, ncut, owner = _halo_plan_restated(boxes, nranks)
+    np.testing.assert_array_equal(h["recv"], recv)
+    np.testing.assert_array_equal(h["owned_leaves"], owned)
+    assert h["above_cut"] == above and h["cut_boxes"] == ncut
+    # every leaf with sources has exactly one owner; above-cut boxes are never leaves
+    assert owned.sum() == sum(1 for b in boxes if b["leaf"] and b["ns"] > 0)
+    assert all(not boxes[i]["leaf"] for i, o in enumerate(owner) if o == -1)
+    # source balance of the cut: within one cut box of N / nranks
+    if nranks > 1:
+        per = np.zeros(nranks)
+        for i, o in enumerate(owner):
+            if o >= 0 and boxes[i]["leaf"]:
+                per[o] += boxes[i]["ns"]
+        assert np.abs(per - per.mean()).max() <= 20000 / (8 * nranks) + 1
+
+
+def test_halo_plan_single_rank_is_empty():
+    qs = _points(5000)
+    h = g.host_halo_plan(3, False, 200, 8, qs, 1)
+    assert h["recv"].sum() == 0 and h["above_cut"] == 0 and h["cut_boxes"] == 1

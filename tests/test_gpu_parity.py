@@ -275,3 +275,45 @@ def test_shards_sum_to_single(case):
         acc += u
     assert np.array_equal(acc, full)
     assert owned.max() <= 1  # no target written by two ranks
+
+
+HALO_CASES = SHARD_CASES + [
+    (0, 3, 120000, 1e-6, False, "uniform", 0, 8),
+    (2, 3, 50000, 1e-6, True, "mixture", 0, 3),
+]
+
+
+@pytest.mark.parametrize("case", HALO_CASES)
+def test_halo_exchange_sums_to_single(case):
+    """Distributed upward pass (include/sdmk.h sdmk_comm_init), with the NCCL
+    exchange replaced by device copies between one context per rank on this
+    GPU, run one rank at a time (manual exchange): every rank forms only its
+    own cut subtrees, packs the halo, receives the others' slabs, merges the
+    boxes above the cut and finishes its shard.  The sum over ranks equals the
+    single-GPU result bitwise, and no rank formed the whole upward pass."""
+    kernel, dim, n, eps, per, dist, ntgt, nranks = case
+    x, s, t = _make(kernel, dim, n, 37, dist, ntgt)
+    plan = g.select_parameters(kernel, eps, 0, dim)
+    sysm = g.ParticleSystem(dim, x, t if ntgt else np.zeros(0), s)
+    full = g.Context(0).evaluate_with_plan(plan, sysm, int(per))
+    ctxs = [g.Context(0) for _ in range(nranks)]
+    for r, c in enumerate(ctxs):
+        c.set_shard(r, nranks)
+        c.set_manual_exchange(True)
+        c.evaluate_begin(plan, sysm, int(per))
+    for a in ctxs:
+        for b in ctxs:
+            if a is not b:
+                a.halo_transfer_to(b)
+    acc = np.zeros_like(full)
+    sent = 0
+    for c in ctxs:
+        rep = {}
+        acc += c.evaluate_end(rep)
+        sent += rep["halo_bytes_sent"]
+        assert rep["halo_bytes_recv"] > 0
+    assert np.array_equal(acc, full)
+    assert sent > 0
+    # the manual-exchange mode refuses the one-call entry point
+    with pytest.raises(ValueError):
+        ctxs[0].evaluate_with_plan(plan, sysm, int(per))
