@@ -554,7 +554,7 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
     *qs_out = hq;
     *qt_out = pr.alias ? nullptr : hq + (size_t)ns * d;
   };
-  pr.tree = build_topology(d, pr.periodic, P.n_s, P.p, ns, pr.alias ? 0 : nt, pa);
+  pr.tree = build_topology(d, pr.periodic, P.n_s, P.p, ns, pr.alias ? 0 : nt, pa, /*with_neighbours=*/false);
   if (str_pending_) {
     finish_strengths();
     check_strengths();
@@ -748,11 +748,14 @@ void Context::upload_tree_lists_a() {
 
 void Context::upload_tree_lists_b() {
   Problem& pr = prob_;
+  const auto hb0 = std::chrono::steady_clock::now();
+  finish_topology(pr.tree);  // neighbour lists (tree.cpp:167-212), while the GPU runs the upward pass
+  const auto hb1 = std::chrono::steady_clock::now();
   const HostTree& t = pr.tree;
   const int nb = t.num_boxes(), d = pr.dim, nchild = 1 << d;
   // target ownership (one rank owns everything unless set_shard was called):
-  // the upward pass stays replicated, the downward, far-field and residual
-  // work is restricted to the owned target leaves and their ancestors
+  // the downward, far-field and residual work is restricted to the owned
+  // target leaves and their ancestors
   ShardPlan sp = shard_plan(t, rank_, nranks_);
   const std::vector<int>& itp = sp.leaves;
   const std::vector<char>& need = sp.need;
@@ -772,6 +775,7 @@ void Context::upload_tree_lists_b() {
     }
   }
   auto reads = [&](int b) { return !pr.halo || pr.hp.reads[rank_][b]; };
+  const auto hb2 = std::chrono::steady_clock::now();
   pr.t_own0 = sp.t0;
   pr.t_own1 = sp.t1;
   // near ranges per target leaf (dmk.cpp:966-990); two-pass CSR, parallel over leaves
@@ -964,6 +968,11 @@ void Context::upload_tree_lists_b() {
   root_dev_slot_ = (int*)(dv + o_rsl);
   root_dev_tau_ = (int*)(dv + o_rta);
   pr.lists_b = true;
+  if (timing_on()) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[sdmk timing] lists B (host, overlaps the upward pass): neighbours %.2f ms, shard+halo plan %.2f ms, lists+upload %.2f ms\n",
+                 ms(hb0, hb1), ms(hb1, hb2), ms(hb2, std::chrono::steady_clock::now()));
+  }
 }
 
 // ---------------------------------------------------------------- passes --

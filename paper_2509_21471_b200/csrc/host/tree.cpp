@@ -76,7 +76,21 @@ struct Builder {
     }
   }
 
+  // repair subdivisions on device-resident points: the 2:1 sweeps depend only
+  // on the box structure (leaf flags, levels, anchors), never on point ranges,
+  // so the children's ranges are found afterwards, one batched GPU call per level
+  std::vector<int> deferred;
+
   void subdivide(int b) {
+    if (pa && !S.q) {
+      int z[9];
+      for (int i = 0; i <= nchild; ++i) z[i] = t.boxes[b].sb;  // placeholder ranges
+      int zt[9];
+      for (int i = 0; i <= nchild; ++i) zt[i] = t.boxes[b].tb;
+      make_children(b, z, zt);
+      deferred.push_back(b);
+      return;
+    }
     need_host_points();
     int sb[9], tb[9];
     split_range(S, t.boxes[b].sb, t.boxes[b].se, t.boxes[b].level, sb);
@@ -302,6 +316,42 @@ struct Builder {
     }
   }
 
+  void resolve_deferred() {
+    if (deferred.empty()) return;
+    // a box's own range is final once its parent's split is resolved: coarse levels first
+    std::stable_sort(deferred.begin(), deferred.end(),
+                     [&](int a, int b) { return t.boxes[a].level < t.boxes[b].level; });
+    for (size_t i0 = 0; i0 < deferred.size();) {
+      size_t i1 = i0;
+      const int lev = t.boxes[deferred[i0]].level;
+      while (i1 < deferred.size() && t.boxes[deferred[i1]].level == lev) ++i1;
+      const int n = (int)(i1 - i0);
+      std::vector<int> lvl(n, lev), sr(2 * n), tr(2 * n), sbn(9 * (size_t)n), tbn(9 * (size_t)n);
+      for (int k = 0; k < n; ++k) {
+        const Box& x = t.boxes[deferred[i0 + k]];
+        sr[2 * k] = x.sb;
+        sr[2 * k + 1] = x.se;
+        tr[2 * k] = x.tb;
+        tr[2 * k + 1] = x.te;
+      }
+      pa->split(n, lvl.data(), sr.data(), tr.data(), sbn.data(), tbn.data());
+      for (int k = 0; k < n; ++k) {
+        const int b = deferred[i0 + k], fc = t.boxes[b].first_child;
+        const int* sb = sbn.data() + 9 * (size_t)k;
+        const int* tb = t.alias ? sb : tbn.data() + 9 * (size_t)k;
+        for (int ci = 0; ci < nchild; ++ci) {
+          Box& c = t.boxes[fc + ci];
+          c.sb = sb[ci];
+          c.se = sb[ci + 1];
+          c.tb = tb[ci];
+          c.te = tb[ci + 1];
+        }
+      }
+      i0 = i1;
+    }
+    deferred.clear();
+  }
+
   bool touch(int b, int c, const int8_t* sh) const {  // tree.cpp:46-56
     int64_t sbz = kCells >> t.boxes[b].level, scz = kCells >> t.boxes[c].level;
     for (int a = 0; a < t.dim; ++a) {
@@ -463,7 +513,7 @@ std::array<double, 3> HostTree::center(int b) const {  // tree.cpp:221-228
 }
 
 static HostTree build_topology_impl(int dim, bool periodic, int n_s, int p, int ns, const int32_t* qs, int nt,
-                                    const int32_t* qt, const PointAccess* pa) {
+                                    const int32_t* qt, const PointAccess* pa, bool with_neighbours) {
   Builder B;
   B.pa = pa;
   B.t.dim = dim;
@@ -484,8 +534,15 @@ static HostTree build_topology_impl(int dim, bool periodic, int n_s, int p, int 
   B.refine();
   const auto c1 = std::chrono::steady_clock::now();
   B.repair();
+  B.resolve_deferred();
   const auto c2 = std::chrono::steady_clock::now();
-  B.neighbours();
+  if (with_neighbours) {
+    B.neighbours();
+    B.t.has_neighbours = true;
+  } else {
+    B.t.level_boxes.assign(B.t.max_level + 1, {});
+    for (int b = 0; b < B.t.num_boxes(); ++b) B.t.level_boxes[B.t.boxes[b].level].push_back(b);
+  }
   const auto c3 = std::chrono::steady_clock::now();
   if (std::getenv("SDMK_TIMING")) {
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
@@ -500,11 +557,22 @@ static HostTree build_topology_impl(int dim, bool periodic, int n_s, int p, int 
 
 HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, const int32_t* qs, int nt,
                         const int32_t* qt) {
-  return build_topology_impl(dim, periodic, n_s, p, ns, qs, nt, qt, nullptr);
+  return build_topology_impl(dim, periodic, n_s, p, ns, qs, nt, qt, nullptr, true);
 }
 
-HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, int nt, const PointAccess& pa) {
-  return build_topology_impl(dim, periodic, n_s, p, ns, nullptr, nt, nullptr, &pa);
+HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, int nt, const PointAccess& pa,
+                        bool with_neighbours) {
+  return build_topology_impl(dim, periodic, n_s, p, ns, nullptr, nt, nullptr, &pa, with_neighbours);
+}
+
+void finish_topology(HostTree& t) {
+  if (t.has_neighbours) return;
+  Builder B;
+  B.t = std::move(t);
+  B.nchild = 1 << B.t.dim;
+  B.neighbours();
+  B.t.has_neighbours = true;
+  t = std::move(B.t);
 }
 
 void leaf_subranges(const HostTree& t, int ns, const int32_t* qs, std::vector<int>& out) {

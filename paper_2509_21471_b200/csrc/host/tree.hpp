@@ -57,6 +57,7 @@ struct Csr {
 struct HostTree {
   int dim = 3, n_s = 0, p = 0, max_level = 0;
   bool periodic = false, alias = true, depth_capped = false;
+  bool has_neighbours = false;  // col / crs / fin built (finish_topology)
   std::vector<Box> boxes;
   std::vector<std::vector<int>> level_boxes;
   Csr col, crs, fin;  // colleagues / coarse / fine
@@ -82,7 +83,11 @@ struct PointAccess {
   std::function<void(int n, const int* lvl, const int* src, const int* tgt, int* sb, int* tb)> split;
   std::function<void(const int32_t** qs, const int32_t** qt)> host_q;
 };
-HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, int nt, const PointAccess& pa);
+// with_neighbours = false leaves col / crs / fin for finish_topology (the
+// upward pass needs only the boxes; the engine builds the lists while it runs)
+HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, int nt, const PointAccess& pa,
+                        bool with_neighbours = true);
+void finish_topology(HostTree& t);
 
 // The reference's canonical text dump (tree.cpp:325-354).
 std::string dump_topology(const HostTree& t);

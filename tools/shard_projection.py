@@ -68,7 +68,7 @@ def main():
             u_bytes = n * 3 * 8
             xfer = (rr["halo_bytes_recv"] + 2 * u_bytes * (R - 1) / R) / (a.link_gbs * 1e9)
             rows.append({"rank": r, "dev_ms": rr["t_total"] * 1e3, "tree_ms": rr["t_tree"] * 1e3,
-                         "upward_ms": rr["t_upward"] * 1e3, "pack_unpack_ms": rr["t_exchange"] * 1e3,
+                         "upward_ms": rr["t_upward"] * 1e3, "root_ms": rr["t_root"] * 1e3, "pack_unpack_ms": rr["t_exchange"] * 1e3,
                          "downward_ms": rr["t_downward"] * 1e3, "residual_ms": rr["t_residual"] * 1e3,
                          "halo_recv_MB": rr["halo_bytes_recv"] / 1e6, "xfer_est_ms": xfer * 1e3})
         # (no transfer between the sequential ranks: the received slabs hold stale
