@@ -1206,25 +1206,24 @@ void Context::run_residual(double* ures, bool stats) {  // dmk.cpp:919-1032
     co = &T.w_offd;
   }
   if (cd && (cd->lo != co->lo || cd->hi != co->hi)) throw RuntimeError("residual tables on different intervals");
-  // piecewise re-expansion of the radial tables (same values to ~1e-15; see setup.hpp)
-  // 32 intervals (degree ~8); fewer when a table needs a higher degree, so
-  // the 8 bank-group copies of the table fit the kernel's shared budget
+  // piecewise re-expansion of the radial tables (setup.hpp): the kernel reads
+  // deg + 1 coefficient pairs per pair evaluation, so it takes the finest
+  // interval grid whose degree fits its shared table, values within 1.5e-13 of
+  // max|table| (the reference's own fits are to 1e-14; the parity bar is 1e-10)
+  constexpr double kPwTol = 1.5e-13;
+  auto compiled = [](int dg) { return dg <= 5 ? 5 : (dg <= 6 ? 6 : (dg <= 8 ? 8 : (dg <= 10 ? 10 : 12))); };
   PiecewisePoly po, pd;
-  for (int ni = 32; ni >= 8; ni /= 2) {
-    po = piecewise_from_cheb(*co, ni, 4);
+  for (int ni = 128; ni >= 8; ni /= 2) {
+    po = piecewise_from_cheb(*co, ni, 4, kPwTol);
+    int deg = po.deg;
     if (cd) {
-      pd = piecewise_from_cheb(*cd, ni, 4);
-      if (pd.deg != po.deg) {
-        const int deg = std::max(pd.deg, po.deg);
-        pd = piecewise_from_cheb(*cd, ni, deg);
-        po = piecewise_from_cheb(*co, ni, deg);
-      }
+      pd = piecewise_from_cheb(*cd, ni, 4, kPwTol);
+      deg = std::max(deg, pd.deg);
     }
-    // the kernel is compiled for degrees 6, 8, 10, 12
-    const int want = std::max(6, std::max(po.deg, cd ? pd.deg : 0) + (std::max(po.deg, cd ? pd.deg : 0) & 1));
-    if (po.deg != want) po = piecewise_from_cheb(*co, ni, want);
-    if (cd && pd.deg != want) pd = piecewise_from_cheb(*cd, ni, want);
-    if (po.ni * (po.deg + 1) <= residual_max_pw() && po.deg <= 12) break;
+    deg = compiled(deg);
+    if (po.deg != deg) po = piecewise_from_cheb(*co, ni, deg, kPwTol);
+    if (cd && pd.deg != deg) pd = piecewise_from_cheb(*cd, ni, deg, kPwTol);
+    if (po.ni * (po.deg + 1) <= residual_max_pw() && po.deg <= 12 && (!cd || pd.deg == po.deg)) break;
   }
   if (po.deg > 12) throw RuntimeError("residual table re-expansion needs degree > 12");
   const int npw = po.ni * (po.deg + 1);

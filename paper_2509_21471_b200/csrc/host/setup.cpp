@@ -691,7 +691,7 @@ double Cheb::eval(double x) const {  // Clenshaw (chebyshev.cpp:9-19)
   return t * b1 - b2 + a[0];
 }
 
-PiecewisePoly piecewise_from_cheb(const Cheb& t, int ni, int min_deg) {
+PiecewisePoly piecewise_from_cheb(const Cheb& t, int ni, int min_deg, double rel_tol) {
   PiecewisePoly P;
   P.ni = ni;
   P.lo = t.lo;
@@ -703,7 +703,7 @@ PiecewisePoly piecewise_from_cheb(const Cheb& t, int ni, int min_deg) {
   }
   double fmax = 0.0;
   for (int j = 0; j <= 4096; ++j) fmax = std::max(fmax, std::fabs(t.eval(t.lo + (t.hi - t.lo) * j / 4096.0)));
-  const double tol = 4e-15 * std::max(1.0, fmax);
+  const double tol = rel_tol * std::max(1.0, fmax);
   for (int deg : {4, 5, 6, 7, 8, 10, 12, 14, 16, 20, 24}) {
     if (deg < min_deg) continue;
     const int n = deg + 1;

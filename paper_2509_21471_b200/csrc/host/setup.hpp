@@ -97,7 +97,9 @@ struct PiecewisePoly {
   double lo = 0.0, hi = 1.0, max_err = 0.0;
   std::vector<double> c;
 };
-PiecewisePoly piecewise_from_cheb(const Cheb& t, int ni = 32, int min_deg = 8);
+// lowest degree >= min_deg whose Horner values stay within rel_tol * max(1, max|t|)
+// of the Chebyshev table on every interval (checked at 65 points per interval)
+PiecewisePoly piecewise_from_cheb(const Cheb& t, int ni = 32, int min_deg = 8, double rel_tol = 4e-15);
 
 Tables build_tables(int kernel, int dim, const WindowFn& win, double tol);
 // tables exactly as evaluate_with_plan builds them when none are supplied

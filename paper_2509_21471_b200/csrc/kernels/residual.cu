@@ -12,11 +12,12 @@
 //     bounding box; conservative 1e-12 margin, so no pair with
 //     r^2 < (nu*support)^2 is ever dropped).
 //  3. Sources stream as warp-uniform broadcast loads; every lane tests its own
-//     target (same arithmetic as the reference: x = xt - (xs + shift)) and
-//     appends in-support pairs to a lane-private list in shared memory.
+//     target with a conservative single-precision pre-test and appends the
+//     candidates to a lane-private list in shared memory.
 //  4. When any list fills, all lanes evaluate their lists in lockstep: the
-//     radial tables come from a piecewise re-expansion held in shared memory
-//     (host/setup.hpp PiecewisePoly), and 1/r from rsqrt.
+//     reference's exact double-precision support test (x = xt - (xs + shift),
+//     unfused r2), the radial tables from a piecewise re-expansion held in
+//     shared memory (host/setup.hpp PiecewisePoly), and 1/r from rsqrt.
 // No atomics and a fixed per-target order: bitwise reproducible.
 #include "common.cuh"
 #include "launch.hpp"
@@ -29,13 +30,16 @@ namespace {
 
 using dev::DBox;
 
-constexpr int kRBlock = 256;
+// One 16-warp CTA per SM (persistent): the SM's single copy of the radial
+// table can then hold 128 intervals at degree 5 -- 6 coefficient loads per
+// pair instead of 9 at 32 intervals x degree 8.
+constexpr int kRBlock = 512;
 constexpr int kWarps = kRBlock / 32;
-constexpr int kList = 48;        // per-lane list capacity (entries): longer lists, less lockstep padding
+constexpr int kList = 40;        // per-lane list capacity (entries): longer lists, less lockstep padding
 constexpr int kMaxRanges = 160;
 constexpr int kMaxIvl = kMaxRanges * 8;  // source intervals per chunk: ranges x Morton sub-cells
-constexpr int kResBlocksPerSM = 2;       // persistent grid (registers and shared memory allow 2 per SM)
-constexpr int kMaxPW = 384;      // ni * (deg + 1) <= 384 (d, o) coefficient pairs
+constexpr int kResBlocksPerSM = 1;       // persistent grid (registers and shared memory: 1 per SM)
+constexpr int kMaxPW = 768;      // ni * (deg + 1) <= 768 (d, o) coefficient pairs (8 copies: 96 KB)
 constexpr int kCopies = 8;       // table copies, one per 16-byte bank group
 #ifndef SDMK_RES_ILP
 #define SDMK_RES_ILP 2
@@ -60,11 +64,6 @@ __global__ void k_pack_sources(const double* __restrict__ spts, const double* __
     for (int k = dim + sc; k < rw; ++k) r[k] = 0.0;
   }
 }
-
-template <bool B>
-struct BoolC {
-  static constexpr bool value = B;
-};
 
 // 1/sqrt(x) from the single-precision estimate and two Newton steps (~1 ulp;
 // the CUDA double rsqrt spends ~20 instructions on range handling).  x here
@@ -166,7 +165,7 @@ __device__ __forceinline__ void assemble(double fd, double fo, const double* x, 
   }
 }
 
-template <int KERNEL, int DIM, int DEG>
+template <int KERNEL, int DIM, int DEG, int PER>
 __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox* __restrict__ boxes,
                                                       const int* __restrict__ leaves, const int2* __restrict__ chunks, int nchunks,
                                                       const int* __restrict__ rng_start,
@@ -175,7 +174,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
                                                       const int* __restrict__ subrange,
                                                       const double* __restrict__ spts, int ns,
                                                       const double* __restrict__ sstr,
-                                                      const double2* __restrict__ srec, int periodic,
+                                                      const double2* __restrict__ srec,
                                                       const double* __restrict__ tpts, int nt,
                                                       const int* __restrict__ tperm, int alias, double self_const,
                                                       double* __restrict__ ures, int* flags,
@@ -223,6 +222,11 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     double xt[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int ax = 0; ax < DIM; ++ax) xt[ax] = tpts[(size_t)ax * nt + tt];
+    // single-precision copies relative to the leaf centre for the scan's
+    // conservative pre-test (see 2. below)
+    float xtf[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int ax = 0; ax < DIM; ++ax) xtf[ax] = (float)(xt[ax] - box.c[ax]);
     double bl[3], bh[3];  // the warp's target bounding box
 #pragma unroll
     for (int ax = 0; ax < DIM; ++ax) {
@@ -307,6 +311,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     __syncwarp();
     double u[3] = {0.0, 0.0, 0.0};
     int cnt = 0;
+    const double sup2l = (r_l * rt.support) * (r_l * rt.support);
+    const double sup2f = (r_f * rt.support) * (r_f * rt.support);
     auto flush = [&]() {
       int mx = cnt;
 #pragma unroll
@@ -320,7 +326,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       auto eval = [&](int i, double* c) {
         const int a = lsrc[warp][i][lane];
         const int code = lrng[warp][i][lane];  // image shift (x+1 | y+1 << 2 | z+1 << 4) | fine << 6
-        const double nu = (code & 64) ? r_f : r_l, inu = (code & 64) ? inv_rf : inv_rl;
+        const bool fine = code & 64;
+        const double nu = fine ? r_f : r_l, inu = fine ? inv_rf : inv_rl;
         constexpr int RW = Rec<KERNEL, DIM>::kW;
         double rv[RW];
         const double2* rp = srec + (size_t)a * (RW / 2);
@@ -330,8 +337,11 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           rv[2 * k] = v.x;
           rv[2 * k + 1] = v.y;
         }
-        double x[3] = {0.0, 0.0, 0.0}, r2 = 0.0;
-        if (periodic) {  // image shifts (zero shifts add exactly 0)
+        // the reference's arithmetic (dmk.cpp:1003-1008): x = xt - (xs + shift),
+        // r2 = ((x0 x0 + x1 x1) + x2 x2), every operation rounded (no FMA), so
+        // the exact support test and the coincidence test decide as it does
+        double x[3] = {0.0, 0.0, 0.0};
+        if (PER) {
           x[0] = xt[0] - (rv[0] + (double)((code & 3) - 1));
           x[1] = xt[1] - (rv[1] + (double)(((code >> 2) & 3) - 1));
           if (DIM == 3) x[2] = xt[2] - (rv[2] + (double)(((code >> 4) & 3) - 1));
@@ -340,13 +350,19 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           x[1] = xt[1] - rv[1];
           if (DIM == 3) x[2] = xt[2] - rv[2];
         }
-#pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) r2 += x[ax] * x[ax];
+        double r2 = __dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[1], x[1]));
+        if (DIM == 3) r2 = __dadd_rn(r2, __dmul_rn(x[2], x[2]));
+        const bool in = r2 < (fine ? sup2f : sup2l);
+        if (in && r2 == 0.0) singular = 1;
         const double rinv = rsqrt_nr(r2);
         const double s = (r2 * rinv) * inu;  // nu is a power of two: r * (1/nu) == r / nu
         double fd, fo;
         radial_tables<KERNEL, DEG>(rt, s_pw + (lane & (kCopies - 1)), yscale, s, fd, fo);
         assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, nu, rv + DIM, c);
+        const bool keep = in && r2 != 0.0;
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) c[j] = keep ? c[j] : 0.0;
+        return keep;
       };
       for (int i = 0; i < mx; i += kILP) {  // all evaluations unconditional (clamped), straight-line
         double c[kILP][3];
@@ -354,7 +370,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         for (int q = 0; q < kILP; ++q) c[q][0] = c[q][1] = c[q][2] = 0.0;
         if (cnt > 0) {
 #pragma unroll
-          for (int q = 0; q < kILP; ++q) eval(min(i + q, cnt - 1), c[q]);
+          for (int q = 0; q < kILP; ++q)
+            if (eval(min(i + q, cnt - 1), c[q]) && i + q < cnt) ++n_in;
         }
 #pragma unroll
         for (int j = 0; j < DIM; ++j)
@@ -367,11 +384,13 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     // 2. Scan: sources arrive in rounds of up to 32, one coalesced load per
     // coordinate (lane j holds source a + j), and are broadcast to every
     // lane's target with shuffles; the next round's load is issued before
-    // the current round is tested.  Every lane tests its own target with the
-    // reference's arithmetic (x = xt - (xs + shift)) and appends in-support
-    // pairs to its list.
-    const double sup2l = (r_l * rt.support) * (r_l * rt.support);
-    const double sup2f = (r_f * rt.support) * (r_f * rt.support);
+    // the current round is tested.  The test is a conservative pre-test in
+    // single precision on coordinates relative to the leaf centre: r2 <
+    // sup2 (1 + 1e-4), while the float error of r2 is below ~2e-6 relative
+    // near the support sphere, so every pair the reference keeps is listed;
+    // the evaluation repeats the reference's exact double-precision test
+    // (the very few extra candidates contribute exact zeros).
+    const float sup2l_hi = (float)(sup2l * (1.0 + 1e-4)), sup2f_hi = (float)(sup2f * (1.0 + 1e-4));
     for (int ib = 0; ib < nivl; ib += 32) {
       const int nb = min(32, nivl - ib);
       const int4 iv = lane < nb ? ivl[ib + lane] : make_int4(0, 0, 0, 0);
@@ -401,52 +420,42 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         if (i < nb) load(s, e);
         const int meta = __shfl_sync(0xffffffffu, iv.z, ci);
         const int code = meta & 127;
-        const double sup2 = (meta & 64) ? sup2f : sup2l;
+        const float sup2 = (meta & 64) ? sup2f_hi : sup2l_hi;
         const bool skip_self = alias && (meta & 256);
         const int nv = min(32, ce - cs);
-        auto scan = [&](auto zsc) {
-          constexpr bool ZS = decltype(zsc)::value;
-          const double shx = (double)((code & 3) - 1), shy = (double)(((code >> 2) & 3) - 1),
-                       shz = (double)(((code >> 4) & 3) - 1);
-          auto test = [&](int a, double sx, double sy, double sz) {
-            double x0, x1, x2 = 0.0;
-            if (ZS) {
-              x0 = xt[0] - sx;
-              x1 = xt[1] - sy;
-              if (DIM == 3) x2 = xt[2] - sz;
-            } else {
-              x0 = xt[0] - (sx + shx);
-              x1 = xt[1] - (sy + shy);
-              if (DIM == 3) x2 = xt[2] - (sz + shz);
+        // this lane's source of the round, shifted and relative to the leaf centre
+        float cxf, cyf, czf = 0.0f;
+        if (PER) {
+          cxf = (float)((cx + (double)((code & 3) - 1)) - box.c[0]);
+          cyf = (float)((cy + (double)(((code >> 2) & 3) - 1)) - box.c[1]);
+          if (DIM == 3) czf = (float)((cz + (double)(((code >> 4) & 3) - 1)) - box.c[2]);
+        } else {
+          cxf = (float)(cx - box.c[0]);
+          cyf = (float)(cy - box.c[1]);
+          if (DIM == 3) czf = (float)(cz - box.c[2]);
+        }
+        for (int j = 0; j < nv; j += 4) {
+          if (__any_sync(0xffffffffu, cnt > kList - 4)) flush();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int jj = j + q;
+            const float sx = __shfl_sync(0xffffffffu, cxf, jj & 31);
+            const float sy = __shfl_sync(0xffffffffu, cyf, jj & 31);
+            const float sz = DIM == 3 ? __shfl_sync(0xffffffffu, czf, jj & 31) : 0.0f;
+            const float x0 = xtf[0] - sx, x1 = xtf[1] - sy;
+            float r2 = x0 * x0 + x1 * x1;
+            if (DIM == 3) {
+              const float x2 = xtf[2] - sz;
+              r2 += x2 * x2;
             }
-            double r2 = x0 * x0 + x1 * x1;
-            if (DIM == 3) r2 += x2 * x2;
-            bool in = valid && r2 < sup2 && !(skip_self && a == t);
-            if (in && r2 == 0.0) {
-              singular = 1;
-              in = false;
-            }
-            if (in) {
+            const int a = cs + jj;
+            if (jj < nv && valid && r2 < sup2 && !(skip_self && a == t)) {
               lsrc[warp][cnt][lane] = a;
               lrng[warp][cnt][lane] = (unsigned char)code;
               ++cnt;
-              ++n_in;
-            }
-          };
-          for (int j = 0; j < nv; j += 4) {
-            if (__any_sync(0xffffffffu, cnt > kList - 4)) flush();
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int jj = j + q;
-              const double sx = __shfl_sync(0xffffffffu, cx, jj & 31);
-              const double sy = __shfl_sync(0xffffffffu, cy, jj & 31);
-              const double sz = DIM == 3 ? __shfl_sync(0xffffffffu, cz, jj & 31) : 0.0;
-              if (jj < nv) test(cs + jj, sx, sy, sz);
             }
           }
-        };
-        if (meta & 128) scan(BoolC<true>{});
-        else scan(BoolC<false>{});
+        }
       }
     }
     flush();
@@ -512,19 +521,24 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
                      sizeof(double) * 2 * kCopies * (size_t)rt.ni * (rt.deg + 1);
 #define RES(K, D)                                                                                                \
   do {                                                                                                           \
-    if (rt.deg == 6) RES1(K, D, 6);                                                                              \
+    if (rt.deg == 5) RES1(K, D, 5);                                                                              \
+    else if (rt.deg == 6) RES1(K, D, 6);                                                                         \
     else if (rt.deg == 8) RES1(K, D, 8);                                                                         \
     else if (rt.deg == 10) RES1(K, D, 10);                                                                       \
     else RES1(K, D, 12);                                                                                         \
   } while (0)
 #define RES1(K, D, G)                                                                                            \
   do {                                                                                                           \
-    cudaFuncSetAttribute(k_residual<K, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);            \
-    k_residual<K, D, G><<<nblk, kRBlock, dsm, st>>>(rt, boxes, leaves, ch2, nchunks, rng_start, rng_box,         \
-                                                    rng_info, subrange,                                          \
-                                                     spts, ns, sstr, reinterpret_cast<const double2*>(srec),     \
-                                                     periodic, tpts, nt, tperm, alias, self_const, ures,         \
-                                                     flags, stats, ivl, next_chunk);                             \
+    if (periodic) RES2(K, D, G, 1);                                                                              \
+    else RES2(K, D, G, 0);                                                                                       \
+  } while (0)
+#define RES2(K, D, G, P)                                                                                         \
+  do {                                                                                                           \
+    cudaFuncSetAttribute(k_residual<K, D, G, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);         \
+    k_residual<K, D, G, P><<<nblk, kRBlock, dsm, st>>>(rt, boxes, leaves, ch2, nchunks, rng_start, rng_box,      \
+                                                       rng_info, subrange, spts, ns, sstr,                       \
+                                                       reinterpret_cast<const double2*>(srec), tpts, nt, tperm,  \
+                                                       alias, self_const, ures, flags, stats, ivl, next_chunk);  \
   } while (0)
   if (rt.dim == 3) {
     if (rt.kernel == 0) RES(0, 3);
@@ -537,6 +551,7 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
   }
 #undef RES
 #undef RES1
+#undef RES2
 }
 
 int residual_max_ranges() { return kMaxRanges; }
