@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <malloc.h>
 
 
 namespace sdmkb {
@@ -148,7 +149,23 @@ void* Pinned::get(const std::string& name, size_t bytes) {
   return p;
 }
 
+// The host passes rebuild tree, neighbour and work lists (tens of MB of
+// std::vectors) on every evaluation.  With glibc's default thresholds those
+// blocks are mmapped and returned on free, so every call page-faults them in
+// again (~1 ms per 4 MB); keeping them in the heap makes the host critical
+// path between the sort and the upward pass ~20 % shorter.  Process-wide;
+// SDMK_NO_MALLOPT=1 leaves the allocator alone.
+static void tune_host_allocator() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  if (std::getenv("SDMK_NO_MALLOPT")) return;
+  mallopt(M_MMAP_THRESHOLD, 512 << 20);
+  mallopt(M_TRIM_THRESHOLD, 1 << 30);
+}
+
 Context::Context(int device) : device_(device) {
+  tune_host_allocator();
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "cudaStreamCreate");
   cuda_check(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -1086,7 +1103,10 @@ void Context::run_downward() {  // dmk.cpp:705-857
   cuda_check(cudaMemcpyAsync(dA, hA, Aall.size() * sizeof(double), cudaMemcpyHostToDevice, st_), "symbol upload");
   const size_t bytes_B = sizeof(double2) * pr.nch * g.pz * g.ncol;
   const size_t bytes_FC = sizeof(double2) * d * ((size_t)g.nhalf + (size_t)g.pz * g.ncol);
-  const size_t budget = size_t(2) << 30;
+  static const size_t budget = [] {  // scratch per B / F+C chunk (SDMK_PW_BUDGET_MB overrides)
+    const char* e = std::getenv("SDMK_PW_BUDGET_MB");
+    return (e ? (size_t)std::atol(e) : size_t(2048)) << 20;
+  }();
   const int chunk_src = (int)std::max<size_t>(1, budget / bytes_B);
   const int chunk_tgt = (int)std::max<size_t>(1, budget / bytes_FC);
   // plane-wave timing: one event pair per level, read after the evaluation's

@@ -80,6 +80,7 @@ struct Builder {
   // on the box structure (leaf flags, levels, anchors), never on point ranges,
   // so the children's ranges are found afterwards, one batched GPU call per level
   std::vector<int> deferred;
+  double split_ms = 0.0, dfs_ms = 0.0;  // time in the GPU split calls / DFS renumbering (SDMK_TIMING)
 
   void subdivide(int b) {
     if (pa && !S.q) {
@@ -121,6 +122,7 @@ struct Builder {
       int sb[9], tb[9];
     };
     std::vector<Node> nodes(1);
+    nodes.reserve(std::min<size_t>(size_t(1) << 24, 4 * (size_t)(S.n + T.n) / std::max(1, t.n_s) * (size_t)nchild + 64));
     nodes[0].box = t.boxes[0];
     std::vector<int> cur(1, 0);
     bool capped = false;
@@ -146,7 +148,9 @@ struct Builder {
         }
         const int nw = (int)which.size();
         std::vector<int> sbv((size_t)nw * 9), tbv((size_t)nw * 9);
+        const auto ts0 = std::chrono::steady_clock::now();
         if (nw) pa->split(nw, lvl.data(), sr.data(), tr.data(), sbv.data(), tbv.data());
+        split_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts0).count();
         for (int k = 0; k < nw; ++k) {
           Node& nd = nodes[cur[which[k]]];
           for (int c = 0; c <= nchild; ++c) {
@@ -172,6 +176,7 @@ struct Builder {
         }
       }
       std::vector<int> next;
+      next.reserve((size_t)nc * nchild);
       for (int i = 0; i < nc; ++i) {
         if (!split[i]) continue;
         const int id = cur[i];
@@ -194,8 +199,10 @@ struct Builder {
       cur.swap(next);
     }
     t.depth_capped = capped;
+    const auto td0 = std::chrono::steady_clock::now();
     // DFS pre-order id allocation (stack pop order as in tree.cpp:110-122)
     std::vector<int> final_id(nodes.size(), -1);
+    t.boxes.reserve(nodes.size() + nodes.size() / 4 + 64);  // room for the 2:1 repair's boxes
     t.boxes.assign(1, nodes[0].box);
     final_id[0] = 0;
     std::vector<int> stack(1, 0);
@@ -216,6 +223,7 @@ struct Builder {
       }
       for (int ci = nchild - 1; ci >= 0; --ci) stack.push_back(nodes[n].kids + ci);
     }
+    dfs_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - td0).count();
   }
 
   // does any of the 3^d - 1 probes of leaf b land in a leaf >= 2 levels coarser?
@@ -546,8 +554,8 @@ static HostTree build_topology_impl(int dim, bool periodic, int n_s, int p, int 
   const auto c3 = std::chrono::steady_clock::now();
   if (std::getenv("SDMK_TIMING")) {
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-    std::fprintf(stderr, "[sdmk timing] topology: refine %.2f ms, repair %.2f ms, neighbours %.2f ms\n", ms(c0, c1),
-                 ms(c1, c2), ms(c2, c3));
+    std::fprintf(stderr, "[sdmk timing] topology: refine %.2f ms (GPU split calls %.2f ms, DFS ids %.2f ms), repair %.2f ms, neighbours %.2f ms\n",
+                 ms(c0, c1), B.split_ms, B.dfs_ms, ms(c1, c2), ms(c2, c3));
   }
   if (B.t.depth_capped)
     std::fprintf(stderr, "build_tree: depth cap %d reached with leaves above capacity (duplicate points?)\n",

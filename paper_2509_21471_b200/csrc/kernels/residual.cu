@@ -35,7 +35,10 @@ using dev::DBox;
 // pair instead of 9 at 32 intervals x degree 8.
 constexpr int kRBlock = 512;
 constexpr int kWarps = kRBlock / 32;
-constexpr int kList = 40;        // per-lane list capacity (entries): longer lists, less lockstep padding
+#ifndef SDMK_RES_LIST
+#define SDMK_RES_LIST 48
+#endif
+constexpr int kList = SDMK_RES_LIST;  // per-lane list capacity (entries): longer lists, less lockstep padding
 constexpr int kMaxRanges = 160;
 constexpr int kMaxIvl = kMaxRanges * 8;  // source intervals per chunk: ranges x Morton sub-cells
 constexpr int kResBlocksPerSM = 1;       // persistent grid (registers and shared memory: 1 per SM)
@@ -391,7 +394,75 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     // the evaluation repeats the reference's exact double-precision test
     // (the very few extra candidates contribute exact zeros).
     const float sup2l_hi = (float)(sup2l * (1.0 + 1e-4)), sup2f_hi = (float)(sup2f * (1.0 + 1e-4));
-    for (int ib = 0; ib < nivl; ib += 32) {
+    // 2a. The leaf's own sources (the first near range, nu = r_l, zero shift)
+    // are in the support of most of the warp's targets, so they skip the
+    // lists: each round of 32 source records is loaded coalesced and every
+    // source is broadcast to all lanes and evaluated at once (the exact test
+    // masks the pairs outside the support).  Own-box pairs come first in the
+    // reference's order, so every target still sums its pairs in order.
+    int nself = 0;
+#ifndef SDMK_RES_NODENSE
+    {
+      const bool isself = lane < nivl && (ivl[lane].z & 256);
+      const unsigned notself = __ballot_sync(0xffffffffu, !isself);
+      nself = notself ? __ffs(notself) - 1 : 32;
+    }
+#endif
+    for (int q = 0; q < nself; ++q) {
+      const int4 iv = ivl[q];
+      constexpr int RW = Rec<KERNEL, DIM>::kW;
+      for (int base = iv.x; base < iv.y; base += 32) {
+        const int nv = min(32, iv.y - base);
+        double rv[RW];
+#pragma unroll
+        for (int k = 0; k < RW; ++k) rv[k] = 0.0;
+        if (lane < nv) {
+          const double2* rp = srec + (size_t)(base + lane) * (RW / 2);
+#pragma unroll
+          for (int k = 0; k < RW / 2; ++k) {
+            const double2 v = rp[k];
+            rv[2 * k] = v.x;
+            rv[2 * k + 1] = v.y;
+          }
+        }
+        auto dense = [&](int j, double* c) {
+          double sv[RW];
+#pragma unroll
+          for (int k = 0; k < RW; ++k) sv[k] = __shfl_sync(0xffffffffu, rv[k], j);
+          const int a = base + j;
+          double x[3] = {0.0, 0.0, 0.0};
+          x[0] = xt[0] - sv[0];
+          x[1] = xt[1] - sv[1];
+          if (DIM == 3) x[2] = xt[2] - sv[2];
+          double r2 = __dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[1], x[1]));
+          if (DIM == 3) r2 = __dadd_rn(r2, __dmul_rn(x[2], x[2]));
+          const bool in = valid && r2 < sup2l && !(alias && a == t);
+          if (in && r2 == 0.0) singular = 1;
+          const double rinv = rsqrt_nr(r2);
+          const double sc = (r2 * rinv) * inv_rl;
+          double fd, fo;
+          radial_tables<KERNEL, DEG>(rt, s_pw + (lane & (kCopies - 1)), yscale, sc, fd, fo);
+          assemble<KERNEL, DIM>(fd, fo, x, rinv, sc, rt.support, r_l, sv + DIM, c);
+          const bool keep = in && r2 != 0.0;
+#pragma unroll
+          for (int k = 0; k < DIM; ++k) c[k] = keep ? c[k] : 0.0;
+          return keep;
+        };
+        for (int j = 0; j < nv; j += 2) {
+          double c0[3] = {0.0, 0.0, 0.0}, c1[3] = {0.0, 0.0, 0.0};
+          const bool k0 = dense(j, c0);
+          const bool k1 = dense(min(j + 1, nv - 1), c1) && j + 1 < nv;
+#pragma unroll
+          for (int k = 0; k < DIM; ++k) u[k] += c0[k];
+          if (j + 1 < nv) {
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) u[k] += c1[k];
+          }
+          n_in += (k0 ? 1 : 0) + (k1 ? 1 : 0);
+        }
+      }
+    }
+    for (int ib = nself; ib < nivl; ib += 32) {
       const int nb = min(32, nivl - ib);
       const int4 iv = lane < nb ? ivl[ib + lane] : make_int4(0, 0, 0, 0);
       int i = 0, s = __shfl_sync(0xffffffffu, iv.x, 0);
