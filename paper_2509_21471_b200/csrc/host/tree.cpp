@@ -270,8 +270,16 @@ struct Builder {
     std::vector<int> cand_ids;
     {
       std::vector<int> leaves;
+      int lmin = kMaxLevel, lmax = 0;
       for (int b = 0; b < t.num_boxes(); ++b)
-        if (t.boxes[b].leaf) leaves.push_back(b);
+        if (t.boxes[b].leaf) {
+          leaves.push_back(b);
+          lmin = std::min(lmin, t.boxes[b].level);
+          lmax = std::max(lmax, t.boxes[b].level);
+        }
+      // a trigger needs two leaves whose levels differ by >= 2: none when the
+      // leaf levels span at most one level (uniform inputs), so no sweep can fire
+      if (lmax - lmin <= 1) return;
       const int nl = (int)leaves.size();
       std::vector<char> cand(nl, 0);
 #pragma omp parallel for schedule(dynamic, 64)
