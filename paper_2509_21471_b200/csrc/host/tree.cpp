@@ -423,20 +423,22 @@ struct Builder {
     t.col.v = root;
     // relative position of box c (with periodic shift sh) to box b, in units of
     // b's side, per axis: exact integer (anchors are multiples of the side)
+    // (the difference is an exact multiple of the power-of-two unit: a shift)
     auto rel = [&](int b, int c, const int8_t* sh, int64_t unit, int* o) {
+      const int lg = __builtin_ctzll((unsigned long long)unit);
       for (int a = 0; a < t.dim; ++a)
-        o[a] = int((int64_t(t.boxes[c].anchor[a]) + int64_t(sh[a]) * kCells - int64_t(t.boxes[b].anchor[a])) / unit);
+        o[a] = int((int64_t(t.boxes[c].anchor[a]) + int64_t(sh[a]) * kCells - int64_t(t.boxes[b].anchor[a])) >> lg);
     };
     for (int lev = 1; lev <= t.max_level; ++lev) {
       const std::vector<int>& ids = t.level_boxes[lev];
-      const int64_t ps = kCells >> (lev - 1), hs = ps / 2;  // parent side, child side
+      const int64_t ps = kCells >> (lev - 1);  // parent side
       // colleagues: children of the parent's non-leaf colleagues that touch b.
       // A child at offset 2 o + cc (child units) from b's parent touches b at
       // cb iff |2 o + cc - cb| <= 1 on every axis -- no child box is loaded.
       auto col_scan = [&](int b, Nbr* out) {
         const int par = t.boxes[b].parent;
         int cb[3] = {0, 0, 0};
-        for (int a = 0; a < t.dim; ++a) cb[a] = int((t.boxes[b].anchor[a] - t.boxes[par].anchor[a]) / hs);
+        for (int a = 0; a < t.dim; ++a) cb[a] = int((t.boxes[b].anchor[a] - t.boxes[par].anchor[a]) >> (kMaxLevel - lev));
         int n = 0;
         for (const Nbr& pc : t.col[par]) {
           if (t.boxes[pc.box].leaf) continue;
@@ -646,21 +648,64 @@ std::string dump_topology(const HostTree& t) {  // tree.cpp:325-354
   return os.str();
 }
 
-ShardPlan shard_plan(const HostTree& t, int rank, int nranks) {
+ShardCosts shard_costs(const HostTree& t) {
+  ShardCosts c;
+  const int nb = t.num_boxes();
+  for (int b = 0; b < nb; ++b)
+    if (t.boxes[b].leaf && t.ntgt(b) > 0) c.leaves.push_back(b);
+  std::sort(c.leaves.begin(), c.leaves.end(), [&](int a, int b) { return t.boxes[a].tb < t.boxes[b].tb; });
+  const int nl = (int)c.leaves.size();
+  c.w.assign(nl, 0);
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < nl; ++i) {
+    const int b = c.leaves[i];
+    int64_t near = 0;  // sources of the near ranges (dmk.cpp:966-990)
+    if (t.has_neighbours) {
+      near += t.nsrc(b);
+      for (const Nbr& e : t.col[b]) {
+        if (e.box == b && !e.shift[0] && !e.shift[1] && !e.shift[2]) continue;
+        if (t.boxes[e.box].leaf) near += t.nsrc(e.box);
+      }
+      for (const Nbr& e : t.crs[b]) near += t.nsrc(e.box);
+      for (const Nbr& e : t.fin[b]) near += t.nsrc(e.box);
+    }
+    // every box with targets costs kCostPerBox (its plane-wave and tensor
+    // work), shared by its target leaves in proportion to their targets
+    int64_t boxes_w = 0;
+    for (int a = b; a >= 0; a = t.boxes[a].parent) boxes_w += kCostPerBox * t.ntgt(b) / t.ntgt(a);
+    c.w[i] = (int64_t)t.ntgt(b) * (near + kCostPerTarget) + boxes_w;
+  }
+  for (int64_t w : c.w) c.total += w;
+  return c;
+}
+
+ShardPlan shard_plan(const HostTree& t, int rank, int nranks, const ShardCosts* costs) {
   ShardPlan sp;
   const int nb = t.num_boxes();
-  std::vector<int> tl;
-  for (int b = 0; b < nb; ++b)
-    if (t.boxes[b].leaf && t.ntgt(b) > 0) tl.push_back(b);
-  std::sort(tl.begin(), tl.end(), [&](int a, int b) { return t.boxes[a].tb < t.boxes[b].tb; });
-  int64_t total = 0;
-  for (int b : tl) total += t.ntgt(b);
+  if (nranks <= 1 && !costs) {  // everything, no costs needed
+    for (int b = 0; b < nb; ++b)
+      if (t.boxes[b].leaf && t.ntgt(b) > 0) sp.leaves.push_back(b);
+    sp.t0 = 0;
+    sp.t1 = t.ntgt(0);
+    sp.need.assign(nb, 0);
+    for (int b : sp.leaves)
+      for (int x = b; x >= 0 && !sp.need[x]; x = t.boxes[x].parent) sp.need[x] = 1;
+    return sp;
+  }
+  ShardCosts local;
+  if (!costs) {
+    local = shard_costs(t);
+    costs = &local;
+  }
+  const std::vector<int>& tl = costs->leaves;
+  const int64_t total = costs->total;
   sp.need.assign(nb, 0);
   if (nranks < 1) nranks = 1;
   int64_t start = 0;
   sp.t0 = -1;
-  for (int b : tl) {
-    const int64_t n = t.ntgt(b);
+  for (size_t i = 0; i < tl.size(); ++i) {
+    const int b = tl[i];
+    const int64_t n = costs->w[i];
     const int owner = nranks == 1 ? 0 : (int)std::min<int64_t>(nranks - 1, ((2 * start + n) * nranks) / (2 * total));
     if (owner == rank) {
       if (sp.t0 < 0) sp.t0 = t.boxes[b].tb;
@@ -722,9 +767,10 @@ HaloPlan halo_owners(const HostTree& t, int nranks) {
 void halo_reads(const HostTree& t, HaloPlan& h) {
   const int nb = t.num_boxes();
   h.reads.assign(h.nranks, std::vector<char>(nb, 0));
+  const ShardCosts costs = shard_costs(t);
 #pragma omp parallel for schedule(dynamic, 1)
   for (int r = 0; r < h.nranks; ++r) {
-    const ShardPlan sp = shard_plan(t, r, h.nranks);
+    const ShardPlan sp = shard_plan(t, r, h.nranks, &costs);
     std::vector<char>& rd = h.reads[r];
     // plane-wave targets of rank r (the entries of upload_tree_lists_b, dmk.cpp:760-797)
     for (int b = 0; b < nb; ++b) {

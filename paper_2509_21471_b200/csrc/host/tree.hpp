@@ -100,8 +100,13 @@ void leaf_subranges(const HostTree& t, int ns, const int32_t* qs, std::vector<in
 
 // Target-leaf ownership of rank `rank` of `nranks`: the
 // target leaves in Morton order (by the start of their target range) are cut
-// into contiguous runs of about total / nranks targets (a leaf goes to the
-// rank whose share contains its midpoint).  `need` marks the owned leaves
+// into contiguous runs of about total / nranks cost (a leaf goes to the rank
+// whose share contains its midpoint).  Cost of a target leaf, in units of one
+// residual pair test: nt * (sources in its near ranges + kCostPerTarget) +
+// sum over the leaf and its ancestors a of kCostPerBox * nt / nt(a) -- the
+// residual pairs, the interpolation per target and the plane-wave / tensor
+// work of every box shared by its target leaves (ratios from the N = 1e7
+// launch list).  `need` marks the owned leaves
 // and their ancestors -- the boxes whose incoming expansions the rank forms;
 // [t0, t1) is the owned range of Morton-sorted targets.  nranks == 1 owns
 // everything.
@@ -110,7 +115,14 @@ struct ShardPlan {
   std::vector<int> leaves;  // owned target leaves, by id
   std::vector<char> need;   // per box
 };
-ShardPlan shard_plan(const HostTree& t, int rank, int nranks);
+constexpr int64_t kCostPerTarget = 1190, kCostPerBox = 860000;
+struct ShardCosts {
+  std::vector<int> leaves;  // target leaves in Morton order
+  std::vector<int64_t> w;   // their costs
+  int64_t total = 0;
+};
+ShardCosts shard_costs(const HostTree& t);  // needs the neighbour lists
+ShardPlan shard_plan(const HostTree& t, int rank, int nranks, const ShardCosts* costs = nullptr);
 
 // Source ownership for the distributed upward pass.
 // The cut: starting from the root, every non-leaf box holding more than

@@ -33,9 +33,13 @@ def test_shard_plan_tiles_targets(nranks):
     for a, b in zip(plans, plans[1:]):
         assert a["t1"] == b["t0"]
     assert sum(p["owned_leaves"] for p in plans) == plans[0]["target_leaves"]
-    # balanced to within one leaf (leaves hold <= n_s sources)
+    # cost-balanced (host/tree.hpp shard_costs) to within one leaf's cost
+    boxes = _parse_dump(g.host_topology_dump(3, False, 300, 10, qs))
+    tl, w = _shard_costs(boxes)
+    tb = [boxes[i]["tb"] for i in tl]
     for p in plans:
-        assert abs((p["t1"] - p["t0"]) - total / nranks) <= 300
+        c = sum(wi for t0, wi in zip(tb, w) if p["t0"] <= t0 < p["t1"])
+        assert abs(c - sum(w) / nranks) <= max(w)
         assert p["needed_boxes"] >= p["owned_leaves"]
     if nranks == 1:
         assert plans[0]["owned_leaves"] == plans[0]["target_leaves"]
@@ -110,9 +114,16 @@ def _parse_dump(text):
         anc = tuple(int(v) for v in f[2][2:].split(","))
         sb, se = (int(v) for v in f[4][5:-1].split(","))
         tb, te = (int(v) for v in f[5][5:-1].split(","))
-        col = line[line.index("col={") + 5:line.index("}", line.index("col={"))]
-        cols = [int(e.split("@")[0]) for e in col.split()] if col else []
-        boxes.append(dict(level=lev, a=anc, leaf=f[3] == "leaf", ns=se - sb, nt=te - tb, sb=sb, tb=tb, col=cols))
+        def lst(tag):
+            body = line[line.index(tag + "={") + len(tag) + 2:line.index("}", line.index(tag + "={"))]
+            out = []
+            for e in body.split():
+                bx, _, sh = e.partition("@")
+                out.append((int(bx), tuple(int(v) for v in sh.split(",")) if sh else (0, 0, 0)))
+            return out
+        col, crs, fin = lst("col"), lst("crs"), lst("fin")
+        boxes.append(dict(level=lev, a=anc, leaf=f[3] == "leaf", ns=se - sb, nt=te - tb, sb=sb, tb=tb,
+                          col=[c for c, _ in col], colsh=col, crs=crs, fin=fin))
     key = {(b["level"], b["a"]): i for i, b in enumerate(boxes)}
     for i, b in enumerate(boxes):
         b["children"] = []
@@ -125,6 +136,25 @@ def _parse_dump(text):
         if b["parent"] >= 0:
             boxes[b["parent"]]["children"].append(i)
     return boxes
+
+
+def _shard_costs(boxes):
+    """host/tree.hpp shard_costs: nt * (near sources + 1190) + sum over the
+    leaf and its ancestors a of 860000 * nt // nt(a) per target leaf, near sources = own box + colleague leaves (not the
+    zero-shift self entry) + coarse + fine neighbours (dmk.cpp:966-990)."""
+    tl = sorted((i for i, b in enumerate(boxes) if b["leaf"] and b["nt"] > 0), key=lambda i: boxes[i]["tb"])
+    w = []
+    for i in tl:
+        b = boxes[i]
+        near = b["ns"]
+        near += sum(boxes[c]["ns"] for c, sh in b["colsh"] if not (c == i and sh == (0, 0, 0)) and boxes[c]["leaf"])
+        near += sum(boxes[c]["ns"] for c, _ in b["crs"]) + sum(boxes[c]["ns"] for c, _ in b["fin"])
+        bw, a = 0, i
+        while a >= 0:
+            bw += 860000 * b["nt"] // boxes[a]["nt"]
+            a = boxes[a]["parent"]
+        w.append(b["nt"] * (near + 1190) + bw)
+    return tl, w
 
 
 def _halo_plan_restated(boxes, R_):
@@ -157,13 +187,12 @@ def _halo_plan_restated(boxes, R_):
             if boxes[x]["ns"]:
                 owner[x] = r
                 st += boxes[x]["children"]
-    # target shards (host shard plan): leaves by target start, midpoint rule
-    tl = sorted((i for i, b in enumerate(boxes) if b["leaf"] and b["nt"] > 0), key=lambda i: boxes[i]["tb"])
-    tt = sum(boxes[i]["nt"] for i in tl)
+    # target shards (host shard plan): leaves by target start, cost midpoint rule
+    tl, w = _shard_costs(boxes)
+    tt = sum(w)
     need = [[False] * len(boxes) for _ in range(R_)]
     s0 = 0
-    for i in tl:
-        n = boxes[i]["nt"]
+    for i, n in zip(tl, w):
         r = 0 if R_ == 1 else min(R_ - 1, ((2 * s0 + n) * R_) // (2 * tt))
         s0 += n
         x = i
