@@ -773,13 +773,15 @@ void Context::upload_tree_lists_b() {
   // target ownership (one rank owns everything unless set_shard was called):
   // the downward, far-field and residual work is restricted to the owned
   // target leaves and their ancestors
-  ShardPlan sp = shard_plan(t, rank_, nranks_);
+  ShardCosts costs;
+  if (nranks_ > 1) costs = shard_costs(t);
+  ShardPlan sp = shard_plan(t, rank_, nranks_, nranks_ > 1 ? &costs : nullptr);
   const std::vector<int>& itp = sp.leaves;
   const std::vector<char>& need = sp.need;
   // halo mode: what this rank reads, and the exchange lists
   std::vector<int> send_ids, recv_ids;
   if (pr.halo) {
-    halo_reads(t, pr.hp);
+    halo_reads(t, pr.hp, &costs);
     const int64_t elems = (int64_t)pr.nch * (d == 3 ? pr.plan.p : 1) * pr.plan.p * pr.plan.p;
     pr.send_off.assign(nranks_ + 1, 0);
     pr.recv_off.assign(nranks_ + 1, 0);
@@ -791,7 +793,7 @@ void Context::upload_tree_lists_b() {
       pr.recv_off[q + 1] = (int64_t)recv_ids.size() * elems;
     }
   }
-  auto reads = [&](int b) { return !pr.halo || pr.hp.reads[rank_][b]; };
+  auto reads = [&](int b) { return !pr.halo || ((pr.hp.readmask[b] >> rank_) & 1); };
   const auto hb2 = std::chrono::steady_clock::now();
   pr.t_own0 = sp.t0;
   pr.t_own1 = sp.t1;

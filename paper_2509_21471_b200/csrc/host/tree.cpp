@@ -1,4 +1,5 @@
 #include "tree.hpp"
+#include "setup.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -764,21 +765,40 @@ HaloPlan halo_owners(const HostTree& t, int nranks) {
   return h;
 }
 
-void halo_reads(const HostTree& t, HaloPlan& h) {
-  const int nb = t.num_boxes();
-  h.reads.assign(h.nranks, std::vector<char>(nb, 0));
-  const ShardCosts costs = shard_costs(t);
-#pragma omp parallel for schedule(dynamic, 1)
-  for (int r = 0; r < h.nranks; ++r) {
-    const ShardPlan sp = shard_plan(t, r, h.nranks, &costs);
-    std::vector<char>& rd = h.reads[r];
-    // plane-wave targets of rank r (the entries of upload_tree_lists_b, dmk.cpp:760-797)
-    for (int b = 0; b < nb; ++b) {
-      const int par = t.boxes[b].parent;
-      if (t.ntgt(b) == 0 || !sp.need[par >= 0 ? par : b]) continue;
-      for (const Nbr& e : t.col[b])
-        if (t.nsrc(e.box) > 0) rd[e.box] = 1;
-    }
+void halo_reads(const HostTree& t, HaloPlan& h, const ShardCosts* costs) {
+  const int nb = t.num_boxes(), R = h.nranks;
+  if (R > 64) throw InvalidArgument("halo plan: at most 64 ranks");
+  ShardCosts local;
+  if (!costs) {
+    local = shard_costs(t);
+    costs = &local;
+  }
+  // need masks: bit q on every box rank q forms incoming expansions for (its
+  // target leaves by the shard rule and their ancestors)
+  std::vector<uint64_t> need(nb, 0);
+  int64_t start = 0;
+  for (size_t i = 0; i < costs->leaves.size(); ++i) {
+    const int64_t n = costs->w[i];
+    const int q = R == 1 ? 0 : (int)std::min<int64_t>(R - 1, ((2 * start + n) * R) / (2 * costs->total));
+    start += n;
+    const uint64_t bit = uint64_t(1) << q;
+    for (int x = costs->leaves[i]; x >= 0 && !(need[x] & bit); x = t.boxes[x].parent) need[x] |= bit;
+  }
+  // plane-wave targets of rank q: boxes with targets whose parent q needs;
+  // q reads every colleague of its targets, and colleagues are mutual, so
+  // the ranks reading box x are the union over x's colleagues c of tmask(c)
+  auto tmask = [&](int c) -> uint64_t {
+    if (t.ntgt(c) == 0) return 0;
+    const int par = t.boxes[c].parent;
+    return need[par >= 0 ? par : c];
+  };
+  h.readmask.assign(nb, 0);
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int x = 0; x < nb; ++x) {
+    if (t.nsrc(x) == 0) continue;
+    uint64_t m = 0;
+    for (const Nbr& e : t.col[x]) m |= tmask(e.box);
+    h.readmask[x] = m;
   }
 }
 
@@ -787,7 +807,7 @@ std::vector<int> halo_boxes(const HaloPlan& h, int from, int to) {
   if (from == to) return v;
   const int nb = (int)h.owner.size();
   for (int b = 0; b < nb; ++b)
-    if (h.owner[b] == from && (h.cut[b] || (!h.reads.empty() && h.reads[to][b]))) v.push_back(b);
+    if (h.owner[b] == from && (h.cut[b] || (!h.readmask.empty() && ((h.readmask[b] >> to) & 1)))) v.push_back(b);
   return v;
 }
 

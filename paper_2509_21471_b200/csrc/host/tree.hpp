@@ -131,19 +131,19 @@ ShardPlan shard_plan(const HostTree& t, int rank, int nranks, const ShardCosts* 
 // contiguous runs by source count (a box goes to the rank whose share holds
 // its midpoint).  A cut box's whole subtree belongs to its owner; the boxes
 // above the cut (all non-leaf) are merged by every rank from the gathered
-// cut boxes.  reads[r][b]: rank r's plane-wave pass reads box b's outgoing
+// cut boxes.  readmask[b] bit r: rank r's plane-wave pass reads box b's outgoing
 // expansion (b is a colleague of one of r's plane-wave targets -- a target
 // whose parent r needs, shard_plan).
 struct HaloPlan {
   int nranks = 1;
   std::vector<int> owner;                // per box: rank; -1 above the cut; -2 no sources
   std::vector<char> cut;                 // per box
-  std::vector<std::vector<char>> reads;  // per rank, per box
+  std::vector<uint64_t> readmask;        // per box: bit r = rank r reads it
 };
 // owner/cut only (what the upward pass of one rank needs)
 HaloPlan halo_owners(const HostTree& t, int nranks);
 // adds reads[] for every rank
-void halo_reads(const HostTree& t, HaloPlan& h);
+void halo_reads(const HostTree& t, HaloPlan& h, const ShardCosts* costs = nullptr);  // nranks <= 64
 // boxes (sorted ids) rank `to` receives from rank `from`: owned by `from`,
 // and either a cut box (every rank merges the boxes above the cut) or read by `to`
 std::vector<int> halo_boxes(const HaloPlan& h, int from, int to);
