@@ -81,7 +81,10 @@ struct Builder {
   // on the box structure (leaf flags, levels, anchors), never on point ranges,
   // so the children's ranges are found afterwards, one batched GPU call per level
   std::vector<int> deferred;
+  size_t deferred_total = 0;
   double split_ms = 0.0, dfs_ms = 0.0;  // time in the GPU split calls / DFS renumbering (SDMK_TIMING)
+  double rep_scan_ms = 0.0;             // repair: parallel pre-scan
+  int rep_leaves = 0, rep_sweeps = 0, rep_cands = 0;
 
   void subdivide(int b) {
     if (pa && !S.q) {
@@ -91,6 +94,7 @@ struct Builder {
       for (int i = 0; i <= nchild; ++i) zt[i] = t.boxes[b].tb;
       make_children(b, z, zt);
       deferred.push_back(b);
+      ++deferred_total;
       return;
     }
     need_host_points();
@@ -283,12 +287,17 @@ struct Builder {
       if (lmax - lmin <= 1) return;
       const int nl = (int)leaves.size();
       std::vector<char> cand(nl, 0);
+      const auto r0 = std::chrono::steady_clock::now();
 #pragma omp parallel for schedule(dynamic, 64)
       for (int i = 0; i < nl; ++i) cand[i] = probe_triggers(leaves[i], nullptr);
       for (int i = 0; i < nl; ++i)
         if (cand[i]) cand_ids.push_back(leaves[i]);
+      rep_scan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();
+      rep_leaves = nl;
     }
     while (!cand_ids.empty()) {
+      ++rep_sweeps;
+      rep_cands += (int)cand_ids.size();
       std::vector<int> next;
       for (const int b : cand_ids) {
         if (!t.boxes[b].leaf) continue;
@@ -567,6 +576,8 @@ static HostTree build_topology_impl(int dim, bool periodic, int n_s, int p, int 
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
     std::fprintf(stderr, "[sdmk timing] topology: refine %.2f ms (GPU split calls %.2f ms, DFS ids %.2f ms), repair %.2f ms, neighbours %.2f ms\n",
                  ms(c0, c1), B.split_ms, B.dfs_ms, ms(c1, c2), ms(c2, c3));
+    std::fprintf(stderr, "[sdmk timing] repair: pre-scan %.2f ms over %d leaves, %d sweeps, %d candidates, %zu subdivisions\n",
+                 B.rep_scan_ms, B.rep_leaves, B.rep_sweeps, B.rep_cands, B.deferred_total);
   }
   if (B.t.depth_capped)
     std::fprintf(stderr, "build_tree: depth cap %d reached with leaves above capacity (duplicate points?)\n",
