@@ -413,22 +413,24 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       constexpr int RW = Rec<KERNEL, DIM>::kW;
       for (int base = iv.x; base < iv.y; base += 32) {
         const int nv = min(32, iv.y - base);
-        double rv[RW];
-#pragma unroll
-        for (int k = 0; k < RW; ++k) rv[k] = 0.0;
+        // the round's records go to the warp's (still empty) list storage and
+        // are read back as 16-byte broadcasts
+        static_assert(RW * 32 * sizeof(double) <= kList * 32 * sizeof(int), "round buffer exceeds the list storage");
+        double2* rb = reinterpret_cast<double2*>(&lsrc[warp][0][0]);
         if (lane < nv) {
           const double2* rp = srec + (size_t)(base + lane) * (RW / 2);
 #pragma unroll
-          for (int k = 0; k < RW / 2; ++k) {
-            const double2 v = rp[k];
-            rv[2 * k] = v.x;
-            rv[2 * k + 1] = v.y;
-          }
+          for (int k = 0; k < RW / 2; ++k) rb[lane * (RW / 2) + k] = rp[k];
         }
+        __syncwarp();
         auto dense = [&](int j, double* c) {
           double sv[RW];
 #pragma unroll
-          for (int k = 0; k < RW; ++k) sv[k] = __shfl_sync(0xffffffffu, rv[k], j);
+          for (int k = 0; k < RW / 2; ++k) {
+            const double2 v = rb[j * (RW / 2) + k];
+            sv[2 * k] = v.x;
+            sv[2 * k + 1] = v.y;
+          }
           const int a = base + j;
           double x[3] = {0.0, 0.0, 0.0};
           x[0] = xt[0] - sv[0];
@@ -460,6 +462,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           }
           n_in += (k0 ? 1 : 0) + (k1 ? 1 : 0);
         }
+        __syncwarp();  // the next round overwrites the buffer
       }
     }
     for (int ib = nself; ib < nivl; ib += 32) {
