@@ -279,6 +279,10 @@ __global__ void __launch_bounds__(kAWarps * 32, 2) k_anterp_mma(int kernel_rt, C
 // instead of one per n-tile.  A warp owns NTW column tiles of the (iy, ix)
 // plane; a CTA covers 8 NTW of them, so a leaf takes ceil(p^2 / 64 NTW) CTAs.
 constexpr int kA2W = 12;  // warps per CTA
+#ifndef SDMK_A2_KC
+#define SDMK_A2_KC 32
+#endif
+constexpr int kKC2 = SDMK_A2_KC;  // points per shared chunk (k_anterp2)
 template <int MT, int NTW, int PC, int KC, int DC>
 __global__ void __launch_bounds__(kA2W * 32, 1) k_anterp2(ChebDev cb, const DBox* __restrict__ boxes,
                                                             const int* __restrict__ leaves,
@@ -292,15 +296,15 @@ __global__ void __launch_bounds__(kA2W * 32, 1) k_anterp2(ChebDev cb, const DBox
   constexpr int MR = nch * pz, NN = p * p;
   constexpr int RS = (MT * 8) % 8 == 4 ? MT * 8 : MT * 8 + 4;  // point rows: == 4 mod 8 (fragment loads)
   constexpr int XS = (p + 3) / 4 * 4 % 8 == 4 ? (p + 3) / 4 * 4 : (p + 3) / 4 * 4 + 4;  // == 4 mod 8
-  constexpr int RAW = kKC * (3 * XS + 8);
-  double* sbz = sm;                 // [kKC][RS]
-  double* raw = sbz + kKC * RS;     // 2 x { bx[kKC][XS], by[kKC][XS], bz[kKC][XS], str[kKC][8] }
+  constexpr int RAW = kKC2 * (3 * XS + 8);
+  double* sbz = sm;                 // [kKC2][RS]
+  double* raw = sbz + kKC2 * RS;     // 2 x { bx[kKC2][XS], by[kKC2][XS], bz[kKC2][XS], str[kKC2][8] }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int b = leaves[blockIdx.x];
   const DBox box = boxes[b];
   const int nt0 = blockIdx.y * kA2W * NTW;
   __shared__ int rcode[MT * 8];  // (ch, iz) of each S row
-  __shared__ double s_chv[kKC][8];
+  __shared__ double s_chv[kKC2][8];
   for (int r = tid; r < MT * 8; r += blockDim.x) rcode[r] = r < MR ? ((r / pz) | ((r % pz) << 8)) : -1;
   int iyv[NTW], ixv[NTW];
 #pragma unroll
@@ -314,26 +318,26 @@ __global__ void __launch_bounds__(kA2W * 32, 1) k_anterp2(ChebDev cb, const DBox
   for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  for (int e = tid; e < kKC * RS; e += blockDim.x) sbz[e] = 0.0;  // row padding stays zero
+  for (int e = tid; e < kKC2 * RS; e += blockDim.x) sbz[e] = 0.0;  // row padding stays zero
   const double* bxg = basis;
   const double* byg = basis + (size_t)n * p;
   const double* bzg = basis + (size_t)2 * n * p;
-  const int nchunks = (box.se - box.sb + kKC - 1) / kKC;
+  const int nchunks = (box.se - box.sb + kKC2 - 1) / kKC2;
   auto issue = [&](int c, int buf) {
-    const int a0 = box.sb + c * kKC, kc = min(kKC, box.se - a0);
+    const int a0 = box.sb + c * kKC2, kc = min(kKC2, box.se - a0);
     double* rb = raw + buf * RAW;
-    for (int e = tid; e < kKC * p; e += blockDim.x) {
+    for (int e = tid; e < kKC2 * p; e += blockDim.x) {
       const int pt = e / p, i = e % p;
       const bool v = pt < kc;
       const size_t o = (size_t)(a0 + (v ? pt : 0)) * p + i;
       dev::cp_async8(rb + pt * XS + i, bxg + o, v);
-      dev::cp_async8(rb + kKC * XS + pt * XS + i, byg + o, v);
-      if (dim == 3) dev::cp_async8(rb + 2 * kKC * XS + pt * XS + i, bzg + o, v);
+      dev::cp_async8(rb + kKC2 * XS + pt * XS + i, byg + o, v);
+      if (dim == 3) dev::cp_async8(rb + 2 * kKC2 * XS + pt * XS + i, bzg + o, v);
     }
-    for (int e = tid; e < kKC * sc; e += blockDim.x) {
+    for (int e = tid; e < kKC2 * sc; e += blockDim.x) {
       const int pt = e / sc, j = e % sc;
       const bool v = pt < kc;
-      dev::cp_async8(rb + 3 * kKC * XS + pt * 8 + j, v ? str + (size_t)j * n + a0 + pt : str, v);
+      dev::cp_async8(rb + 3 * kKC2 * XS + pt * 8 + j, v ? str + (size_t)j * n + a0 + pt : str, v);
     }
     dev::cp_commit();
   };
@@ -349,11 +353,11 @@ __global__ void __launch_bounds__(kA2W * 32, 1) k_anterp2(ChebDev cb, const DBox
     }
     __syncthreads();
     const double* bx = raw + buf * RAW;
-    const double* by = bx + kKC * XS;
-    const double* bz = by + kKC * XS;
-    const double* ss = bz + kKC * XS;
+    const double* by = bx + kKC2 * XS;
+    const double* bz = by + kKC2 * XS;
+    const double* ss = bz + kKC2 * XS;
     // channel values once per point (build_source_channels, dmk.cpp:492-525) ...
-    for (int e = tid; e < kKC * nch; e += blockDim.x) {
+    for (int e = tid; e < kKC2 * nch; e += blockDim.x) {
       const int pt = e / nch, ch = e % nch;
       const double* s = ss + pt * 8;
       double sv;
@@ -378,13 +382,13 @@ __global__ void __launch_bounds__(kA2W * 32, 1) k_anterp2(ChebDev cb, const DBox
     }
     __syncthreads();
     // ... then S[pt][(ch, iz)] = s_ch * bz over all threads
-    for (int e = tid; e < kKC * MR; e += blockDim.x) {
+    for (int e = tid; e < kKC2 * MR; e += blockDim.x) {
       const int pt = e / MR, r = e - pt * MR, code = rcode[r];
       sbz[pt * RS + r] = s_chv[pt][code & 255] * (dim == 3 ? bz[pt * XS + (code >> 8)] : 1.0);
     }
     __syncthreads();
 #pragma unroll 2
-    for (int ks = 0; ks < kKC / 4; ++ks) {
+    for (int ks = 0; ks < kKC2 / 4; ++ks) {
       const int k = ks * 4 + t;
       double bv[NTW];
 #pragma unroll
@@ -589,7 +593,7 @@ void launch_anterp_mma(int kernel, const ChebDev& cb, const DBox* boxes, const i
   do {                                                                                                  \
     constexpr int RS_ = MT_ * 8 + 4;                                                                    \
     constexpr int XS_ = (PC_ + 3) / 4 * 4 % 8 == 4 ? (PC_ + 3) / 4 * 4 : (PC_ + 3) / 4 * 4 + 4;         \
-    const size_t sm2 = sizeof(double) * (size_t)kKC * (RS_ + 2 * (3 * XS_ + 8));                       \
+    const size_t sm2 = sizeof(double) * (size_t)kKC2 * (RS_ + 2 * (3 * XS_ + 8));                      \
     const int ntt = (PC_ * PC_ + 7) / 8, per = kA2W * NTW_;                                             \
     smem_attr((const void*)k_anterp2<MT_, NTW_, PC_, KC_, 3>, sm2);                                     \
     k_anterp2<MT_, NTW_, PC_, KC_, 3><<<dim3(nleaf, (ntt + per - 1) / per), kA2W * 32, sm2, st>>>(      \
