@@ -317,3 +317,17 @@ def test_halo_exchange_sums_to_single(case):
     # the manual-exchange mode refuses the one-call entry point
     with pytest.raises(ValueError):
         ctxs[0].evaluate_with_plan(plan, sysm, int(per))
+
+
+def test_comm_single_rank():
+    """The library's NCCL communicator (include/sdmk.h sdmk_comm_init) loads
+    and initialises in one process (nranks = 1: evaluations are unchanged)."""
+    x, s, _ = _make(0, 3, 20000, 41)
+    plan = g.select_parameters(0, 1e-6, 0, 3)
+    sysm = g.ParticleSystem(3, x, np.zeros(0), s)
+    ref_u = g.Context(0).evaluate_with_plan(plan, sysm, 0)
+    ctx = g.Context(0)
+    ctx.comm_init(0, 1, g.comm_unique_id())
+    assert np.array_equal(ctx.evaluate_with_plan(plan, sysm, 0), ref_u)
+    with pytest.raises(ValueError):
+        ctx.set_shard(1, 2)  # the communicator fixes (rank, nranks)
