@@ -473,7 +473,11 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
   }
   launches_ += 3 + (pr.periodic ? 2 : 0);
   // Morton sort (tree.cpp:258-281)
-  auto sort_set = [&](const double* pts, int n, const std::string& tag, int*& perm, double*& soa, int32_t*& q) {
+  // 3D: one 64-bit radix sort on the top 64 of the 90 key bits; exact unless
+  // two keys tie there (points within 2^-21 on every axis), which the flags
+  // round trip below detects, and then the set is re-sorted on all 90 bits
+  auto sort_set = [&](const double* pts, int n, const std::string& tag, int*& perm, double*& soa, int32_t*& q,
+                      int tie_flag, bool full) {
     uint64_t* klo = arena_.as<uint64_t>("klo", n);
     uint64_t* khi = arena_.as<uint64_t>("khi", n);
     uint64_t* klo2 = arena_.as<uint64_t>("klo2", n);
@@ -483,15 +487,21 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
     perm = arena_.as<int>(tag + "perm", n);
     size_t tb = sort_temp_bytes(n);
     void* tmp = arena_.get("sort_tmp", tb);
-    launch_morton(pts, n, d, klo, khi, idx, st_);
-    sort_morton(n, d, klo, khi, idx, klo2, khi2, idx2, perm, tmp, tb, st_);
+    uint64_t* ktop = d == 3 ? arena_.as<uint64_t>("ktop", n) : nullptr;
+    launch_morton(pts, n, d, klo, khi, ktop, idx, st_);
+    if (d == 3 && !full && !std::getenv("SDMK_FULL_SORT")) {
+      sort_morton_top(n, ktop, arena_.as<uint64_t>("ktop2", n), idx, perm, tmp, tb, flags + tie_flag, st_);
+      ++launches_;
+    } else {
+      sort_morton(n, d, klo, khi, idx, klo2, khi2, idx2, perm, tmp, tb, st_);
+    }
     soa = arena_.as<double>(tag + "pts", (size_t)n * d);
     q = arena_.as<int32_t>(tag + "q", (size_t)n * d);
     launch_gather_points(pts, perm, n, d, soa, q, st_);
     launches_ += 3;
   };
   int32_t *sq = nullptr, *tq = nullptr;
-  sort_set(src, ns, "s", pr.sperm, pr.spts, sq);
+  sort_set(src, ns, "s", pr.sperm, pr.spts, sq, 4, false);
   pr.sstr = arena_.as<double>("sstr", (size_t)ns * pr.sc);
   // strengths still in flight on the side stream: validated and gathered
   // once the topology is built (finish_strengths)
@@ -507,7 +517,7 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
   };
   if (!str_pending_) finish_strengths();
   if (!pr.alias) {
-    sort_set(tgt, nt, "t", pr.tperm, pr.tpts, tq);
+    sort_set(tgt, nt, "t", pr.tperm, pr.tpts, tq, 5, false);
     pr.tpts_caller = tgt;
   } else {
     pr.tperm = pr.sperm;
@@ -536,6 +546,17 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
   if (hflags[2]) throw InvalidArgument("ParticleSystem: non-finite strength");
   if (hflags[0]) throw InvalidArgument("ParticleSystem: non-finite coordinate");
   if (hflags[1]) throw InvalidArgument("ParticleSystem: coordinate outside the unit box");
+  if (hflags[4] || hflags[5]) {  // ties in the top 64 key bits: re-sort on all 90
+    if (hflags[4]) {
+      sort_set(src, ns, "s", pr.sperm, pr.spts, sq, 4, true);
+      if (!str_pending_) finish_strengths();  // gathered with the first permutation
+    }
+    if (!pr.alias && hflags[5]) sort_set(tgt, nt, "t", pr.tperm, pr.tpts, tq, 5, true);
+    if (pr.alias) {
+      pr.tperm = pr.sperm;
+      pr.tpts = pr.spts;
+    }
+  }
   pr.sq = sq;
   pr.tq = tq;
   hq_ = nullptr;

@@ -30,8 +30,12 @@ void launch_validate(const double* pts, int64_t nvals, int periodic, int* flags,
 void launch_wrap(double* pts, int64_t nvals, cudaStream_t st);
 // 90/60-bit Morton keys of quantized points (tree.cpp:19-35) split in two
 // 64-bit words, with the identity permutation in idx.
-void launch_morton(const double* pts, int n, int dim, uint64_t* klo, uint64_t* khi, int* idx,
+void launch_morton(const double* pts, int n, int dim, uint64_t* klo, uint64_t* khi, uint64_t* ktop, int* idx,
                    cudaStream_t st);
+// 3D fast path: one 64-bit sort on the top 64 key bits; *tie_flag = 1 when two
+// sorted keys tie there (then the full two-word sort below must be used).
+void sort_morton_top(int n, uint64_t* ktop, uint64_t* ktop2, int* idx, int* perm, void* temp, size_t temp_bytes,
+                     int* tie_flag, cudaStream_t st);
 // Stable LSD radix sort of (key, index): exactly std::sort over (key, idx)
 // pairs (tree.cpp:262-267).  perm receives the sorted original indices.
 size_t sort_temp_bytes(int n);

@@ -41,7 +41,7 @@ __device__ __forceinline__ int32_t quantize(double x) {
 
 // Morton key with axis 0 in the least-significant interleaved bit (tree.cpp:29-35)
 __global__ void k_morton(const double* __restrict__ pts, int n, int dim, uint64_t* klo, uint64_t* khi,
-                         int* idx) {
+                         uint64_t* ktop, int* idx) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int32_t q[3] = {0, 0, 0};
@@ -56,7 +56,14 @@ __global__ void k_morton(const double* __restrict__ pts, int n, int dim, uint64_
     }
   klo[i] = lo;
   khi[i] = hi;
+  if (ktop) ktop[i] = (hi << 38) | (lo >> 26);  // 3D: the top 64 of the 90 key bits
   idx[i] = i;
+}
+
+// flag |= 1 when two neighbours of the sorted top-64-bit keys are equal
+__global__ void k_adjacent_equal(const uint64_t* __restrict__ k, int n, int* flag) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i + 1 < n && k[i] == k[i + 1]) *flag = 1;
 }
 
 __global__ void k_gather_u64(const uint64_t* __restrict__ src, const int* __restrict__ idx, int n,
@@ -103,8 +110,15 @@ void launch_wrap(double* pts, int64_t nvals, cudaStream_t st) {
   k_wrap<<<grid_for(nvals, 256), 256, 0, st>>>(pts, nvals);
 }
 
-void launch_morton(const double* pts, int n, int dim, uint64_t* klo, uint64_t* khi, int* idx, cudaStream_t st) {
-  k_morton<<<(n + 255) / 256, 256, 0, st>>>(pts, n, dim, klo, khi, idx);
+void launch_morton(const double* pts, int n, int dim, uint64_t* klo, uint64_t* khi, uint64_t* ktop, int* idx,
+                   cudaStream_t st) {
+  k_morton<<<(n + 255) / 256, 256, 0, st>>>(pts, n, dim, klo, khi, dim == 3 ? ktop : nullptr, idx);
+}
+
+void sort_morton_top(int n, uint64_t* ktop, uint64_t* ktop2, int* idx, int* perm, void* temp, size_t temp_bytes,
+                     int* tie_flag, cudaStream_t st) {
+  cub::DeviceRadixSort::SortPairs(temp, temp_bytes, ktop, ktop2, idx, perm, n, 0, 64, st);
+  k_adjacent_equal<<<(n + 255) / 256, 256, 0, st>>>(ktop2, n, tie_flag);
 }
 
 size_t sort_temp_bytes(int n) {

@@ -331,3 +331,32 @@ def test_comm_single_rank():
     assert np.array_equal(ctx.evaluate_with_plan(plan, sysm, 0), ref_u)
     with pytest.raises(ValueError):
         ctx.set_shard(1, 2)  # the communicator fixes (rank, nranks)
+
+
+@pytest.mark.parametrize("separate_targets", [False, True])
+def test_sort_ties_in_top_key_bits(separate_targets):
+    """The 3D sort runs on the top 64 of the 90 Morton key bits and falls back
+    to the full key when two points tie there (within 2^-21 on every axis):
+    near-duplicate points must still give the reference's tree and
+    permutation bit for bit (tree.cpp:258-281)."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-0.5, 0.5, (3000, 3))
+    x[1000:1100] = x[:100] + rng.uniform(1e-9, 5e-9, (100, 3))  # differ only in the low key bits
+    s = rng.standard_normal((3000, 3))
+    t = rng.uniform(-0.5, 0.5, (500, 3)) if separate_targets else None
+    if separate_targets:
+        t[250:300] = t[:50] + 2e-9
+    plan = ref.select_parameters(0, 1e-6, 0, 3)
+    plan["n_s"] = 40
+    R = ref.RefProblem(plan, 3, x, s, targets=t)
+    ctx = g.Context(0)
+    ctx.setup(g.DmkPlan(**plan), g.ParticleSystem(3, x, t if separate_targets else np.zeros(0), s), 0)
+    assert ctx.tree_dump() == R.tree_dump()
+    sp, tp = ctx.tree_perm()
+    rsp, rtp = R.tree_perm()
+    assert np.array_equal(sp, rsp)
+    if separate_targets:
+        assert np.array_equal(tp, rtp)
