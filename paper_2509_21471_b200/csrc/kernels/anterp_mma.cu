@@ -416,8 +416,12 @@ __global__ void __launch_bounds__(kA2W * 32, 1) k_anterp2(ChebDev cb, const DBox
 }
 
 // ------------------------------------------------------------------- K11 --
-constexpr int kIW = 12;                // warps per CTA
-constexpr int kITW = 4;                // m-tiles per warp
+#ifndef SDMK_I_W
+#define SDMK_I_W 8
+#define SDMK_I_TW 5
+#endif
+constexpr int kIW = SDMK_I_W;          // warps per CTA
+constexpr int kITW = SDMK_I_TW;        // m-tiles per warp
 constexpr int kTB = kIW * kITW * 8;    // targets per pass (one pass per leaf up to 384)
 
 // u_j(t) = sum_{iz,iy,ix} W[j,iz,iy,ix] bz[t,iz] by[t,iy] bx[t,ix]  (dmk.cpp:861-915)
