@@ -278,13 +278,15 @@ __global__ void __launch_bounds__(kAWarps * 32, 2) k_anterp_mma(int kernel_rt, C
 // feeding all MT m-tiles of the (ch, iz) rows: 1 multiply per MT DMMAs
 // instead of one per n-tile.  A warp owns NTW column tiles of the (iy, ix)
 // plane; a CTA covers 8 NTW of them, so a leaf takes ceil(p^2 / 64 NTW) CTAs.
-constexpr int kA2W = 12;  // warps per CTA
+// warps per CTA and n-tiles per warp are template parameters (A/B measured per
+// kernel: the Stokeslet runs 12 x 3 -- two CTAs per leaf --, the stresslet's
+// 17 m-tiles need the registers of 12 x 2)
 #ifndef SDMK_A2_KC
 #define SDMK_A2_KC 32
 #endif
 constexpr int kKC2 = SDMK_A2_KC;  // points per shared chunk (k_anterp2)
-template <int MT, int NTW, int PC, int KC, int DC>
-__global__ void __launch_bounds__(kA2W * 32, 1) k_anterp2(ChebDev cb, const DBox* __restrict__ boxes,
+template <int MT, int NTW, int PC, int KC, int DC, int W>
+__global__ void __launch_bounds__(W * 32, 1) k_anterp2(ChebDev cb, const DBox* __restrict__ boxes,
                                                             const int* __restrict__ leaves,
                                                             const double* __restrict__ basis,
                                                             const double* __restrict__ str, int n,
@@ -302,14 +304,14 @@ __global__ void __launch_bounds__(kA2W * 32, 1) k_anterp2(ChebDev cb, const DBox
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int b = leaves[blockIdx.x];
   const DBox box = boxes[b];
-  const int nt0 = blockIdx.y * kA2W * NTW;
+  const int nt0 = blockIdx.y * W * NTW;
   __shared__ int rcode[MT * 8];  // (ch, iz) of each S row
   __shared__ double s_chv[kKC2][8];
   for (int r = tid; r < MT * 8; r += blockDim.x) rcode[r] = r < MR ? ((r / pz) | ((r % pz) << 8)) : -1;
   int iyv[NTW], ixv[NTW];
 #pragma unroll
   for (int j = 0; j < NTW; ++j) {
-    const int col = (nt0 + warp + kA2W * j) * 8 + g;
+    const int col = (nt0 + warp + W * j) * 8 + g;
     iyv[j] = col < NN ? col / p : 0;
     ixv[j] = col < NN ? col % p : 0;
   }
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(kA2W * 32, 1) k_anterp2(ChebDev cb, const DBox
     if (m >= MR) continue;
 #pragma unroll
     for (int j = 0; j < NTW; ++j) {
-      const int cc = (nt0 + warp + kA2W * j) * 8 + 2 * t;
+      const int cc = (nt0 + warp + W * j) * 8 + 2 * t;
       if (cc < NN) ob[(size_t)m * NN + cc] = acc[i][j][0];
       if (cc + 1 < NN) ob[(size_t)m * NN + cc + 1] = acc[i][j][1];
     }
@@ -416,13 +418,10 @@ __global__ void __launch_bounds__(kA2W * 32, 1) k_anterp2(ChebDev cb, const DBox
 }
 
 // ------------------------------------------------------------------- K11 --
-#ifndef SDMK_I_W
-#define SDMK_I_W 8
-#define SDMK_I_TW 5
-#endif
-constexpr int kIW = SDMK_I_W;          // warps per CTA
-constexpr int kITW = SDMK_I_TW;        // m-tiles per warp
-constexpr int kTB = kIW * kITW * 8;    // targets per pass (one pass per leaf up to 384)
+// warps per CTA (IW) and m-tiles per warp (ITW) are template parameters:
+// 8 x 5 for TY <= 3 (p <= 24; measured 4 % faster than 12 x 4 at p = 23),
+// 12 x 4 above (the 8 x 5 accumulators would spill); one pass per leaf covers
+// IW * ITW * 8 targets
 
 // u_j(t) = sum_{iz,iy,ix} W[j,iz,iy,ix] bz[t,iz] by[t,iy] bx[t,ix]  (dmk.cpp:861-915)
 //  * x contraction on the FP64 tensor cores: C[t, (j,iz,iy)] = bx[t,:] . W[(j,iz,iy),:]
@@ -435,7 +434,7 @@ constexpr int kTB = kIW * kITW * 8;    // targets per pass (one pass per leaf up
 // per chunk, double buffered) while every target of the leaf is resident:
 // warp w owns m-tiles w, w + kIW, ..., and each B fragment feeds its
 // kITW tiles (TY x kITW independent DMMA chains per k-step).
-template <int TY, int PC, int DC>
+template <int TY, int PC, int DC, int kIW = (TY <= 3 ? 8 : 12), int kITW = (TY <= 3 ? 5 : 4)>
 __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DBox* __restrict__ boxes,
                                                            const int* __restrict__ leaves,
                                                            const double* __restrict__ tbasis, int nt,
@@ -443,6 +442,7 @@ __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DB
                                                            const double* __restrict__ incoming,
                                                            double* __restrict__ ufar) {
   constexpr int PY = 8 * TY, KS = 2 * TY, WS = PY + 4;
+  constexpr int kTB = kIW * kITW * 8;  // targets per pass
   constexpr int RG = PY >= 128 ? 1 : 128 / PY;  // (j, iz) rows per chunk
   constexpr int NR = RG * PY;                   // W rows per chunk
   extern __shared__ double sm[];
@@ -593,20 +593,20 @@ void launch_anterp_mma(int kernel, const ChebDev& cb, const DBox* boxes, const i
                                                                            str, n, out, nch, mt_per);   \
   } while (0)
 #define AM(NTT, MW) AMS(NTT, MW, 0, -1, 0)
-#define A2(MT_, NTW_, PC_, KC_)                                                                          \
+#define A2(MT_, NTW_, PC_, KC_, W_)                                                                      \
   do {                                                                                                  \
     constexpr int RS_ = MT_ * 8 + 4;                                                                    \
     constexpr int XS_ = (PC_ + 3) / 4 * 4 % 8 == 4 ? (PC_ + 3) / 4 * 4 : (PC_ + 3) / 4 * 4 + 4;         \
     const size_t sm2 = sizeof(double) * (size_t)kKC2 * (RS_ + 2 * (3 * XS_ + 8));                      \
-    const int ntt = (PC_ * PC_ + 7) / 8, per = kA2W * NTW_;                                             \
-    smem_attr((const void*)k_anterp2<MT_, NTW_, PC_, KC_, 3>, sm2);                                     \
-    k_anterp2<MT_, NTW_, PC_, KC_, 3><<<dim3(nleaf, (ntt + per - 1) / per), kA2W * 32, sm2, st>>>(      \
+    const int ntt = (PC_ * PC_ + 7) / 8, per = W_ * NTW_;                                             \
+    smem_attr((const void*)k_anterp2<MT_, NTW_, PC_, KC_, 3, W_>, sm2);                                     \
+    k_anterp2<MT_, NTW_, PC_, KC_, 3, W_><<<dim3(nleaf, (ntt + per - 1) / per), W_ * 32, sm2, st>>>(      \
         cb, boxes, leaves, basis, str, n, out);                                                         \
   } while (0)
   static const bool old_a = std::getenv("SDMK_ANTERP_OLD") != nullptr;
-  if (!old_a && cb.dim == 3 && p == 23 && kernel == 0) A2(9, 2, 23, 0);
-  else if (!old_a && cb.dim == 3 && p == 22 && kernel == 1) A2(17, 2, 22, 1);
-  else if (!old_a && cb.dim == 3 && p == 30 && kernel == 0) A2(12, 2, 30, 0);
+  if (!old_a && cb.dim == 3 && p == 23 && kernel == 0) A2(9, 3, 23, 0, 12);
+  else if (!old_a && cb.dim == 3 && p == 22 && kernel == 1) A2(17, 2, 22, 1, 12);
+  else if (!old_a && cb.dim == 3 && p == 30 && kernel == 0) A2(12, 2, 30, 0, 12);
   else if (cb.dim == 3 && p == 23 && kernel == 0) AMS(3, 6, 23, 0, 3);
   else if (cb.dim == 3 && p == 22 && kernel == 1) AMS(3, 6, 22, 1, 3);
   else if (cb.dim == 3 && p == 30 && kernel == 0) AMS(4, 4, 30, 0, 3);
@@ -628,13 +628,14 @@ void launch_interp_mma(const ChebDev& cb, const DBox* boxes, const int* leaves, 
   const int TYv = (p + 7) / 8;
   auto smem_for = [&](int TY) {
     const int PY = 8 * TY, WS = PY + 4, RG = PY >= 128 ? 1 : 128 / PY;
-    return sizeof(double) * (2 * (size_t)RG * PY * WS + (size_t)kTB * (p | 1));
+    const int tb = TY <= 3 ? 8 * 5 * 8 : 12 * 4 * 8;  // the kernel's IW * ITW * 8
+    return sizeof(double) * (2 * (size_t)RG * PY * WS + (size_t)tb * (p | 1));
   };
 #define IMS(TY_, PC_, DC_)                                                                                \
   do {                                                                                                    \
     size_t sm = smem_for(TY_);                                                                            \
     smem_attr((const void*)k_interp_mma<TY_, PC_, DC_>, sm);                                              \
-    k_interp_mma<TY_, PC_, DC_><<<nleaf, kIW * 32, sm, st>>>(cb, boxes, leaves, tbasis, nt, tperm, incoming, ufar); \
+    k_interp_mma<TY_, PC_, DC_><<<nleaf, (TY_ <= 3 ? 8 : 12) * 32, sm, st>>>(cb, boxes, leaves, tbasis, nt, tperm, incoming, ufar); \
   } while (0)
   if (cb.dim == 3 && p == 23) IMS(3, 23, 3);
   else if (cb.dim == 3 && p == 22) IMS(3, 22, 3);
