@@ -171,6 +171,7 @@ Context::Context(int device) : device_(device) {
   cuda_check(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking), "cudaStreamCreate");
   for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
   cuda_check(cudaEventCreateWithFlags(&str_ev_, cudaEventDisableTiming), "cudaEventCreate");
+  cuda_check(cudaEventCreateWithFlags(&x_ev_, cudaEventDisableTiming), "cudaEventCreate");
 }
 
 Context::~Context() {
@@ -181,6 +182,7 @@ Context::~Context() {
   for (auto& e : stage_ev_) cudaEventDestroy(e);
   if (st2_) cudaStreamSynchronize(st2_);
   if (str_ev_) cudaEventDestroy(str_ev_);
+  if (x_ev_) cudaEventDestroy(x_ev_);
   if (st2_) cudaStreamDestroy(st2_);
   if (st_) cudaStreamDestroy(st_);
 }
@@ -1234,7 +1236,7 @@ void Context::run_target_far(double* ufar) {  // dmk.cpp:861-915
   ++launches_;
 }
 
-void Context::run_residual(double* ures, bool stats) {  // dmk.cpp:919-1032
+void Context::run_residual(double* ures, bool stats, int reserve_sms) {  // dmk.cpp:919-1032
   Problem& pr = prob_;
   const Tables& T = *tab_;
   const Cheb* cd = nullptr;
@@ -1284,7 +1286,7 @@ void Context::run_residual(double* ures, bool stats) {  // dmk.cpp:919-1032
   cudaEventRecord(ev_[13], st_);
   launch_residual(rt, pr.boxes, pr.int_leaves, pr.n_int, pr.res_chunks, pr.n_chunks, pr.rng_start, pr.rng_box, pr.rng_info, pr.subrange, pr.spts, pr.ns,
                   pr.sstr, arena_.as<double>("srec", (size_t)pr.ns * ((pr.dim + pr.sc + 1) / 2 * 2)),
-                  pr.periodic ? 1 : 0, pr.tpts, pr.nt, pr.tperm, pr.alias ? 1 : 0, 0.0, T.self_const, ures, flags + 3,
+                  pr.periodic ? 1 : 0, pr.tpts, pr.nt, pr.tperm, pr.alias ? 1 : 0, reserve_sms, T.self_const, ures, flags + 3,
                   stats ? st : nullptr, arena_.get("res_scratch", residual_scratch_bytes()), st_);
   ++launches_;  // source record packing
   cudaEventRecord(ev_[12], st_);
@@ -1296,11 +1298,22 @@ void Context::evaluate(const Plan& P, int dim, int64_t ns, const double* src, in
                        const double* str, int mode, double* u, sdmk_report* rep, bool device_ptrs) {
   if (manual_x_ && nranks_ > 1) throw InvalidArgument("evaluate: manual exchange mode needs evaluate_begin/end");
   evaluate_begin(P, dim, ns, src, nt, tgt, str, mode, device_ptrs);
-  if (prob_.halo) {  // NCCL point-to-point exchange of the packed halo slabs, on the stream
+  if (prob_.halo) {  // NCCL exchange of the packed halo slabs on the side stream; evaluate_end
+                     // runs the residual (which needs no halo) while it is in flight
+    cuda_check(cudaStreamWaitEvent(st2_, ev_[10], 0), "stream wait");
+    cudaEventRecord(ev_[14], st2_);
     comm_->exchange(arena_.as<double>("halo_send", 1), prob_.send_off, arena_.as<double>("halo_recv", 1),
-                    prob_.recv_off, st_);
+                    prob_.recv_off, st2_);
+    cudaEventRecord(ev_[15], st2_);
+    cuda_check(cudaEventRecord(x_ev_, st2_), "event record");
+    x_pending_ = true;
   }
-  evaluate_end(u, rep);
+  try {
+    evaluate_end(u, rep);
+  } catch (...) {
+    x_pending_ = false;
+    throw;
+  }
 }
 
 void Context::evaluate_begin(const Plan& P, int dim, int64_t ns, const double* src, int64_t nt, const double* tgt,
@@ -1369,6 +1382,22 @@ void Context::evaluate_end(double* u, sdmk_report* rep) {
   const int dim = call_.dim, ntt = call_.ntt;
   const bool device_ptrs = call_.device_ptrs;
   cudaEventRecord(ev_[11], st_);
+  double* ufar = arena_.as<double>("ufar", (size_t)ntt * dim);
+  double* ures = arena_.as<double>("ures", (size_t)ntt * dim);
+  unsigned char* own = nullptr;
+  if (nranks_ > 1) {  // only the owned targets are written by the passes below
+    cuda_check(cudaMemsetAsync(ufar, 0, sizeof(double) * ntt * dim, st_), "memset ufar");
+    cuda_check(cudaMemsetAsync(ures, 0, sizeof(double) * ntt * dim, st_), "memset ures");
+    own = arena_.as<unsigned char>("own", (size_t)ntt);
+    launch_own_mask(ntt, prob_.tperm, prob_.t_own0, prob_.t_own1, own, st_);
+    ++launches_;
+  }
+  const bool overlap = x_pending_;
+  if (overlap) {  // near field first, beside the exchange (a few SMs left for NCCL)
+    run_residual(ures, rep != nullptr, 8);
+    cuda_check(cudaStreamWaitEvent(st_, x_ev_, 0), "stream wait");
+    x_pending_ = false;
+  }
   if (prob_.halo) {
     const Problem& pr = prob_;
     const int64_t elems = (int64_t)pr.nch * (dim == 3 ? P.p : 1) * P.p * P.p;
@@ -1380,20 +1409,10 @@ void Context::evaluate_end(double* u, sdmk_report* rep) {
   if (prob_.halo) run_upward_top();
   run_root();
   cudaEventRecord(ev_[4], st_);
-  double* ufar = arena_.as<double>("ufar", (size_t)ntt * dim);
-  double* ures = arena_.as<double>("ures", (size_t)ntt * dim);
-  unsigned char* own = nullptr;
-  if (nranks_ > 1) {  // only the owned targets are written by the passes below
-    cuda_check(cudaMemsetAsync(ufar, 0, sizeof(double) * ntt * dim, st_), "memset ufar");
-    cuda_check(cudaMemsetAsync(ures, 0, sizeof(double) * ntt * dim, st_), "memset ures");
-    own = arena_.as<unsigned char>("own", (size_t)ntt);
-    launch_own_mask(ntt, prob_.tperm, prob_.t_own0, prob_.t_own1, own, st_);
-    ++launches_;
-  }
   run_downward();
   run_target_far(ufar);
   cudaEventRecord(ev_[5], st_);
-  run_residual(ures, rep != nullptr);
+  if (!overlap) run_residual(ures, rep != nullptr);
   // global terms (dmk.cpp:1086-1102)
   Problem& pr = prob_;
   double* sums = arena_.as<double>("sums", 16);
@@ -1446,7 +1465,7 @@ void Context::evaluate_end(double* u, sdmk_report* rep) {
     rep->t_upward = ev_ms(2, 3) * 1e-3;
     rep->t_root = (ev_ms(3, 4) - ev_ms(8, 9)) * 1e-3;
     rep->t_downward = ev_ms(4, 5) * 1e-3;
-    rep->t_residual = ev_ms(5, 6) * 1e-3;
+    rep->t_residual = (overlap ? ev_ms(13, 12) : ev_ms(5, 6)) * 1e-3;
     rep->t_d2h = ev_ms(6, 7) * 1e-3;
     rep->t_total = (ev_ms(0, 7) - (manual ? gap : 0.0)) * 1e-3;
     rep->t_residual_kernel = ev_ms(13, 12) * 1e-3;
@@ -1454,7 +1473,9 @@ void Context::evaluate_end(double* u, sdmk_report* rep) {
     rep->p2p_candidates = (int64_t)hst[0];
     rep->p2p_in_support = (int64_t)hst[1];
     rep->kernel_launches = launches_;
-    rep->t_exchange = pr.halo ? (manual ? xfer : ev_ms(8, 9)) * 1e-3 : 0.0;
+    // NCCL: pack + unpack on the stream plus the exchange on the side stream
+    // (which overlaps the residual pass)
+    rep->t_exchange = pr.halo ? (manual ? xfer : ev_ms(8, 10) + ev_ms(14, 15)) * 1e-3 : 0.0;
     rep->halo_bytes_sent = pr.halo ? pr.send_off[nranks_] * (int64_t)sizeof(double) : 0;
     rep->halo_bytes_recv = pr.halo ? pr.recv_off[nranks_] * (int64_t)sizeof(double) : 0;
   }

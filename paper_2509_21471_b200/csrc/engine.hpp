@@ -165,7 +165,7 @@ class Context {
   void run_root();
   void run_downward();
   void run_target_far(double* ufar);
-  void run_residual(double* ures, bool stats);
+  void run_residual(double* ures, bool stats, int reserve_sms = 0);
   GridDev& grid(GridDev& cache, const std::string& name, int dim, int p, int N, double theta, double band_r2);
   void sync();
   double ev_ms(int a, int b);
@@ -178,6 +178,8 @@ class Context {
   cudaStream_t st_ = nullptr;
   cudaStream_t st2_ = nullptr;     // side stream: strengths H2D overlapping the tree build
   cudaEvent_t str_ev_ = nullptr;
+  cudaEvent_t x_ev_ = nullptr;     // the NCCL halo exchange on st2_ is done
+  bool x_pending_ = false;         // an exchange is in flight (evaluate with a communicator)
   bool str_pending_ = false;       // strengths copy in flight on st2_
   cudaEvent_t ev_[16];
   Arena arena_;

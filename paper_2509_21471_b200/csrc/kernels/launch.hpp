@@ -170,7 +170,7 @@ void launch_residual(const ResidTables& rt, const dev::DBox* boxes, const int* l
                      const int* chunks, int nchunks, const int* rng_start, const int* rng_box, const int* rng_info, const int* subrange,
                      const double* spts, int ns, const double* sstr, double* srec, int periodic,
                      const double* tpts, int nt,
-                     const int* tperm, int alias, double self_coef_scale, double self_const,
+                     const int* tperm, int alias, int reserve_sms, double self_const,
                      double* ures, int* flags, unsigned long long* stats, void* scratch, cudaStream_t st);
 // scratch for launch_residual (chunk counter + per-warp source interval lists)
 size_t residual_scratch_bytes();

@@ -575,7 +575,7 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
                      int nchunks, const int* rng_start,
                      const int* rng_box, const int* rng_info, const int* subrange, const double* spts, int ns, const double* sstr,
                      double* srec, int periodic,
-                     const double* tpts, int nt, const int* tperm, int alias, double /*unused*/, double self_const,
+                     const double* tpts, int nt, const int* tperm, int alias, int reserve_sms, double self_const,
                      double* ures, int* flags, unsigned long long* stats, void* scratch, cudaStream_t st) {
   if (nleaf <= 0 || nchunks <= 0) return;
   {
@@ -586,7 +586,9 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int nblk = std::min(kResBlocksPerSM * sms, (nchunks + kWarps - 1) / kWarps);
+  // reserve_sms: SMs left free for kernels running beside this one (the NCCL
+  // halo exchange of a multi-GPU evaluation)
+  const int nblk = std::min(kResBlocksPerSM * std::max(1, sms - reserve_sms), (nchunks + kWarps - 1) / kWarps);
   int* next_chunk = reinterpret_cast<int*>(scratch);
   int4* ivl = reinterpret_cast<int4*>(reinterpret_cast<char*>(scratch) + 256);
   cudaMemsetAsync(next_chunk, 0, sizeof(int), st);

@@ -8,8 +8,10 @@ halo pack/unpack, the boxes above the cut, its shard of the downward /
 far-field / residual passes), timed with CUDA events on the library stream.
 The NCCL transfers are NOT run; their bytes are reported and costed at an
 assumed NVLink rate (--link-gbs) together with the all-reduce of u.  The
-projection is max over ranks of (device time + transfer estimate); it is a
-model, not a multi-GPU measurement.
+projection is max over ranks of (device time + transfer estimate), and
+"overlap" credits the library's schedule, where the halo exchange runs on a
+side stream beside the residual pass; it is a model, not a multi-GPU
+measurement.
 
 usage: python tools/shard_projection.py [--n 1e7] [--dist uniform|cfg5] [--ranks 2,4,8]
 """
@@ -66,17 +68,25 @@ def main():
                 ctx.evaluate_begin_device(plan, 3, n, dx.data_ptr(), 0, 0, df.data_ptr(), 0)
                 ctx.evaluate_end(rr, d_u=du.data_ptr())
             u_bytes = n * 3 * 8
-            xfer = (rr["halo_bytes_recv"] + 2 * u_bytes * (R - 1) / R) / (a.link_gbs * 1e9)
+            halo_s = rr["halo_bytes_recv"] / (a.link_gbs * 1e9)
+            u_s = 2 * u_bytes * (R - 1) / R / (a.link_gbs * 1e9)
+            xfer = halo_s + u_s
+            # with a communicator the halo exchange runs beside the residual pass
+            # (engine.cpp evaluate: side stream, residual first); u's all-reduce cannot
+            hidden = max(0.0, halo_s - rr["t_residual"]) + u_s
             rows.append({"rank": r, "dev_ms": rr["t_total"] * 1e3, "tree_ms": rr["t_tree"] * 1e3,
                          "upward_ms": rr["t_upward"] * 1e3, "root_ms": rr["t_root"] * 1e3, "pack_unpack_ms": rr["t_exchange"] * 1e3,
                          "downward_ms": rr["t_downward"] * 1e3, "residual_ms": rr["t_residual"] * 1e3,
-                         "halo_recv_MB": rr["halo_bytes_recv"] / 1e6, "xfer_est_ms": xfer * 1e3})
+                         "halo_recv_MB": rr["halo_bytes_recv"] / 1e6, "xfer_est_ms": xfer * 1e3,
+                         "xfer_exposed_ms": hidden * 1e3})
         # (no transfer between the sequential ranks: the received slabs hold stale
         # data, which changes values but not the work; correctness of the same
         # code path is tests/test_gpu_parity.py::test_halo_exchange_sums_to_single)
         worst = max(rows, key=lambda q: q["dev_ms"] + q["xfer_est_ms"])
         tR = worst["dev_ms"] + worst["xfer_est_ms"]
+        tO = max(q["dev_ms"] + q["xfer_exposed_ms"] for q in rows)
         res = {"R": R, "projected_ms": tR, "projected_eff": t1 * 1e3 / (R * tR),
+               "projected_overlap_ms": tO, "projected_overlap_eff": t1 * 1e3 / (R * tO),
                "max_dev_ms": max(q["dev_ms"] for q in rows), "min_dev_ms": min(q["dev_ms"] for q in rows),
                "per_rank": rows}
         out["ranks"][R] = res
