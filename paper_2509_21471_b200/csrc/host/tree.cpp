@@ -232,6 +232,30 @@ struct Builder {
   }
 
   // does any of the 3^d - 1 probes of leaf b land in a leaf >= 2 levels coarser?
+  // The box containing `probe` found from box `from`: climb to the first
+  // ancestor that contains it, then descend, stopping at a leaf or at level
+  // maxlev.  For the 2:1 probes of a leaf b (its 3^d - 1 neighbour centres)
+  // the common ancestor is a few levels up, so this replaces most of a
+  // root-to-leaf descent.  Returns the leaf containing the probe whenever
+  // that leaf's level is < maxlev.
+  int locate(int from, const int32_t* probe, int maxlev) const {
+    int x = from;
+    for (;;) {
+      const Box& bx = t.boxes[x];
+      const int64_t side = kCells >> bx.level;
+      bool in = true;
+      for (int a = 0; a < t.dim; ++a) in = in && probe[a] >= bx.anchor[a] && int64_t(probe[a]) < bx.anchor[a] + side;
+      if (in || bx.parent < 0) break;
+      x = bx.parent;
+    }
+    while (!t.boxes[x].leaf && t.boxes[x].level < maxlev) {
+      int lev = t.boxes[x].level, ci = 0;
+      for (int a = 0; a < t.dim; ++a) ci |= ((probe[a] >> (kMaxLevel - 1 - lev)) & 1) << a;
+      x = t.boxes[x].first_child + ci;
+    }
+    return x;
+  }
+
   bool probe_triggers(int b, int* first_off) const {
     const int lev = t.boxes[b].level;
     if (lev < 2) return false;
@@ -254,7 +278,7 @@ struct Builder {
             probe[a] = int32_t(v);
           }
           if (!inside) continue;
-          const int a = descend(probe);
+          const int a = locate(t.boxes[b].parent, probe, lev - 1);
           if (t.boxes[a].leaf && t.boxes[a].level <= lev - 2) {
             if (first_off) *first_off = k;
             return true;
@@ -321,7 +345,7 @@ struct Builder {
                 probe[a] = int32_t(v);
               }
               if (!inside) continue;
-              const int a = descend(probe);
+              const int a = locate(t.boxes[b].parent, probe, lev - 1);
               if (t.boxes[a].leaf && t.boxes[a].level <= lev - 2) {
                 subdivide(a);
                 for (int ci = 0; ci < nchild; ++ci) next.push_back(t.boxes[a].first_child + ci);
