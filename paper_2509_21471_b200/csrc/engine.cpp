@@ -1392,10 +1392,13 @@ void Context::evaluate_end(double* u, sdmk_report* rep) {
     launch_own_mask(ntt, prob_.tperm, prob_.t_own0, prob_.t_own1, own, st_);
     ++launches_;
   }
-  const bool overlap = x_pending_;
-  if (overlap) {  // near field first, beside the exchange (a few SMs left for NCCL)
-    run_residual(ures, rep != nullptr, 8);
-    cuda_check(cudaStreamWaitEvent(st_, x_ev_, 0), "stream wait");
+  // halo mode: the near field first -- it needs no halo, so with NCCL it runs
+  // beside the exchange (a few SMs left free); the manual-exchange tests take
+  // the same order
+  const bool overlap = prob_.halo;
+  if (overlap) {
+    run_residual(ures, rep != nullptr, x_pending_ ? 8 : 0);
+    if (x_pending_) cuda_check(cudaStreamWaitEvent(st_, x_ev_, 0), "stream wait");
     x_pending_ = false;
   }
   if (prob_.halo) {
