@@ -213,7 +213,12 @@ void par_memcpy(void* dst, const void* src, size_t bytes) {
     std::memcpy((char*)dst + o, (const char*)src + o, n);
   }
 }
-constexpr size_t kStageBytes = size_t(32) << 20;
+constexpr size_t kStageBytes = size_t(32) << 20;     // largest ring chunk
+constexpr size_t kStageMin = size_t(1) << 20;        // pageable copies above this are staged
+// chunk of a staged copy: about an eighth of it (so the host copies and the
+// DMA overlap even for a few tens of MB), between 4 and 32 MB
+size_t stage_chunk(size_t bytes) { return std::min(kStageBytes, std::max(size_t(4) << 20, (bytes / 8 + 4095) & ~size_t(4095))); }
+constexpr size_t kSideStreamMin = size_t(32) << 20;  // pinned strengths above this go on the side stream
 constexpr int kStages = 4;
 }  // namespace
 
@@ -228,16 +233,17 @@ void Context::stage_events() {
 
 void Context::copy_in(void* dst, const void* src, size_t bytes, bool device_ptrs) {
   if (bytes == 0) return;
-  if (device_ptrs || !is_pageable(src) || bytes <= kStageBytes) {
+  if (device_ptrs || !is_pageable(src) || bytes <= kStageMin) {
     cuda_check(cudaMemcpyAsync(dst, src, bytes, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st_),
                "copy in");
     return;
   }
   stage_events();
   char* ring = (char*)pinned_.get("stage", kStages * kStageBytes);
+  const size_t ck = stage_chunk(bytes);
   int k = 0;
-  for (size_t o = 0; o < bytes; o += kStageBytes, k = (k + 1) % kStages) {
-    const size_t n = std::min(kStageBytes, bytes - o);
+  for (size_t o = 0; o < bytes; o += ck, k = (k + 1) % kStages) {
+    const size_t n = std::min(ck, bytes - o);
     cuda_check(cudaEventSynchronize(stage_ev_[k]), "stage wait");  // the chunk's previous DMA is done
     par_memcpy(ring + k * kStageBytes, (const char*)src + o, n);
     cuda_check(cudaMemcpyAsync((char*)dst + o, ring + k * kStageBytes, n, cudaMemcpyHostToDevice, st_), "copy in");
@@ -247,15 +253,16 @@ void Context::copy_in(void* dst, const void* src, size_t bytes, bool device_ptrs
 
 void Context::copy_out(void* dst, const void* src, size_t bytes) {
   if (bytes == 0) return;
-  if (!is_pageable(dst) || bytes <= kStageBytes) {
+  if (!is_pageable(dst) || bytes <= kStageMin) {
     cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st_), "copy out");
     return;
   }
   stage_events();
   char* ring = (char*)pinned_.get("stage", kStages * kStageBytes);
-  const size_t nch = (bytes + kStageBytes - 1) / kStageBytes;
+  const size_t ck = stage_chunk(bytes);
+  const size_t nch = (bytes + ck - 1) / ck;
   auto issue = [&](size_t c) {
-    const size_t o = c * kStageBytes, n = std::min(kStageBytes, bytes - o);
+    const size_t o = c * ck, n = std::min(ck, bytes - o);
     cuda_check(cudaMemcpyAsync(ring + (c % kStages) * kStageBytes, (const char*)src + o, n, cudaMemcpyDeviceToHost, st_),
                "copy out");
     cudaEventRecord(stage_ev_[c % kStages], st_);
@@ -264,7 +271,7 @@ void Context::copy_out(void* dst, const void* src, size_t bytes) {
   for (size_t c = 0; c < nch; ++c) {
     if (c + kStages - 1 < nch) issue(c + kStages - 1);  // keep the copy engine busy
     cuda_check(cudaEventSynchronize(stage_ev_[c % kStages]), "stage wait");
-    const size_t o = c * kStageBytes, n = std::min(kStageBytes, bytes - o);
+    const size_t o = c * ck, n = std::min(ck, bytes - o);
     par_memcpy((char*)dst + o, ring + (c % kStages) * kStageBytes, n);
   }
 }
@@ -1335,7 +1342,7 @@ void Context::evaluate_begin(const Plan& P, int dim, int64_t ns, const double* s
   if (!alias) copy_in(arena_.as<double>("tgt_in", (size_t)nt * dim), tgt, sizeof(double) * nt * dim, device_ptrs);
   // pinned strengths travel on a second stream while the tree is built (they
   // are first needed by the upward pass); pageable / device ones as before
-  str_pending_ = !device_ptrs && !is_pageable(str) && ns * sc * sizeof(double) > kStageBytes;
+  str_pending_ = !device_ptrs && !is_pageable(str) && ns * sc * sizeof(double) > kSideStreamMin;
   if (str_pending_) {
     cuda_check(cudaStreamWaitEvent(st2_, ev_[0], 0), "stream wait");
     cuda_check(cudaMemcpyAsync(arena_.as<double>("str_in", (size_t)ns * sc), str, sizeof(double) * ns * sc,
