@@ -278,6 +278,10 @@ __global__ void __launch_bounds__(kAWarps * 32, 2) k_anterp_mma(int kernel_rt, C
 // feeding all MT m-tiles of the (ch, iz) rows: 1 multiply per MT DMMAs
 // instead of one per n-tile.  A warp owns NTW column tiles of the (iy, ix)
 // plane; a CTA covers 8 NTW of them, so a leaf takes ceil(p^2 / 64 NTW) CTAs.
+#ifndef SDMK_A2S_MT
+#define SDMK_A2S_MT 17
+#define SDMK_A2S_NTW 2
+#endif
 // warps per CTA and n-tiles per warp are template parameters (A/B measured per
 // kernel: the Stokeslet runs 12 x 3 -- two CTAs per leaf --, the stresslet's
 // 17 m-tiles need the registers of 12 x 2)
@@ -307,7 +311,11 @@ __global__ void __launch_bounds__(W * 32, 1) k_anterp2(ChebDev cb, const DBox* _
   const int nt0 = blockIdx.y * W * NTW;
   __shared__ int rcode[MT * 8];  // (ch, iz) of each S row
   __shared__ double s_chv[kKC2][8];
-  for (int r = tid; r < MT * 8; r += blockDim.x) rcode[r] = r < MR ? ((r / pz) | ((r % pz) << 8)) : -1;
+  // rows [rb0, rb0 + 8 MT) of the MR (ch, iz) rows: blockIdx.z splits tall
+  // problems (the stresslet's 6 channels) into row blocks of the same shape
+  const int rb0 = blockIdx.z * MT * 8, nrow = min(MT * 8, MR - rb0);
+  for (int r = tid; r < MT * 8; r += blockDim.x)
+    rcode[r] = r < nrow ? (((rb0 + r) / pz) | (((rb0 + r) % pz) << 8)) : -1;
   int iyv[NTW], ixv[NTW];
 #pragma unroll
   for (int j = 0; j < NTW; ++j) {
@@ -384,8 +392,8 @@ __global__ void __launch_bounds__(W * 32, 1) k_anterp2(ChebDev cb, const DBox* _
     }
     __syncthreads();
     // ... then S[pt][(ch, iz)] = s_ch * bz over all threads
-    for (int e = tid; e < kKC2 * MR; e += blockDim.x) {
-      const int pt = e / MR, r = e - pt * MR, code = rcode[r];
+    for (int e = tid; e < kKC2 * nrow; e += blockDim.x) {
+      const int pt = e / nrow, r = e - pt * nrow, code = rcode[r];
       sbz[pt * RS + r] = s_chv[pt][code & 255] * (dim == 3 ? bz[pt * XS + (code >> 8)] : 1.0);
     }
     __syncthreads();
@@ -406,8 +414,8 @@ __global__ void __launch_bounds__(W * 32, 1) k_anterp2(ChebDev cb, const DBox* _
   double* ob = out + (size_t)b * MR * NN;
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
-    const int m = i * 8 + g;
-    if (m >= MR) continue;
+    const int ml = i * 8 + g, m = rb0 + ml;
+    if (ml >= nrow) continue;
 #pragma unroll
     for (int j = 0; j < NTW; ++j) {
       const int cc = (nt0 + warp + W * j) * 8 + 2 * t;
@@ -600,12 +608,13 @@ void launch_anterp_mma(int kernel, const ChebDev& cb, const DBox* boxes, const i
     const size_t sm2 = sizeof(double) * (size_t)kKC2 * (RS_ + 2 * (3 * XS_ + 8));                      \
     const int ntt = (PC_ * PC_ + 7) / 8, per = W_ * NTW_;                                             \
     smem_attr((const void*)k_anterp2<MT_, NTW_, PC_, KC_, 3, W_>, sm2);                                     \
-    k_anterp2<MT_, NTW_, PC_, KC_, 3, W_><<<dim3(nleaf, (ntt + per - 1) / per), W_ * 32, sm2, st>>>(      \
+    const int nrb = ((KC_ == 1 ? 6 : 3) * PC_ + MT_ * 8 - 1) / (MT_ * 8);                               \
+    k_anterp2<MT_, NTW_, PC_, KC_, 3, W_><<<dim3(nleaf, (ntt + per - 1) / per, nrb), W_ * 32, sm2, st>>>( \
         cb, boxes, leaves, basis, str, n, out);                                                         \
   } while (0)
   static const bool old_a = std::getenv("SDMK_ANTERP_OLD") != nullptr;
   if (!old_a && cb.dim == 3 && p == 23 && kernel == 0) A2(9, 3, 23, 0, 12);
-  else if (!old_a && cb.dim == 3 && p == 22 && kernel == 1) A2(17, 2, 22, 1, 12);
+  else if (!old_a && cb.dim == 3 && p == 22 && kernel == 1) A2(SDMK_A2S_MT, SDMK_A2S_NTW, 22, 1, 12);
   else if (!old_a && cb.dim == 3 && p == 30 && kernel == 0) A2(12, 2, 30, 0, 12);
   else if (cb.dim == 3 && p == 23 && kernel == 0) AMS(3, 6, 23, 0, 3);
   else if (cb.dim == 3 && p == 22 && kernel == 1) AMS(3, 6, 22, 1, 3);
