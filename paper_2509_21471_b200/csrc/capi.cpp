@@ -226,9 +226,9 @@ int sdmk_tree_perm(sdmk_context* c, int32_t* src_perm, int32_t* tgt_perm) {
 int64_t sdmk_tree_dump(sdmk_context* c, char* buf, int64_t cap) {
   int64_t len = -1;
   guarded([&] {
-    const Problem& p = need_ctx(c)->problem();
-    if (!p.ready) throw InvalidArgument("no problem set up");
-    std::string s = dump_topology(p.tree);
+    Context* x = need_ctx(c);
+    if (!x->problem().ready) throw InvalidArgument("no problem set up");
+    std::string s = x->tree_dump();
     len = (int64_t)s.size();
     if (buf && cap > 0) std::memcpy(buf, s.data(), (size_t)std::min<int64_t>(cap, len));
   });

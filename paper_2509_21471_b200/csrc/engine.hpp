@@ -141,6 +141,11 @@ class Context {
   void setup(const Plan& plan, int dim, int64_t ns, const double* src, int64_t nt, const double* tgt,
              const double* str, int mode);
   const Problem& problem() const { return prob_; }
+  // the reference's tree dump needs coarse / fine lists of every box
+  std::string tree_dump() {
+    finish_topology(prob_.tree, true);
+    return dump_topology(prob_.tree);
+  }
   cudaStream_t stream() const { return st_; }
   void upward(double* host_out);
   void incoming(int stage, double* host_out);

@@ -412,6 +412,14 @@ struct Builder {
   }
 
   // two-pass CSR fill over `ids`: count(b) then emit(b, out)
+  std::vector<int> leaf_ids(const std::vector<int>& ids) const {
+    std::vector<int> v;
+    v.reserve(ids.size());
+    for (int b : ids)
+      if (t.boxes[b].leaf) v.push_back(b);
+    return v;
+  }
+
   template <class Count, class Emit>
   void csr_pass(Csr& L, const std::vector<int>& ids, Count count, Emit emit) {
     const int n = (int)ids.size();
@@ -433,7 +441,10 @@ struct Builder {
     }
   }
 
-  void neighbours() {  // tree.cpp:167-212
+  // leaves_only: coarse / fine lists only for leaves (all the evaluation
+  // reads); the colleague lists are always complete (children's lists are
+  // built from their parent's)
+  void neighbours(bool leaves_only = false) {  // tree.cpp:167-212
     const auto tn0 = std::chrono::steady_clock::now();
     const int nb = t.num_boxes();
     for (Csr* L : {&t.col, &t.crs, &t.fin}) {
@@ -502,7 +513,7 @@ struct Builder {
       csr_pass(t.col, ids, [&](int b) { return col_scan(b, nullptr); }, [&](int b, Nbr* out) { col_scan(b, out); });
       // coarse: the parent's leaf colleagues that touch b
       csr_pass(
-          t.crs, ids,
+          t.crs, leaves_only ? leaf_ids(ids) : ids,
           [&](int b) {
             int c = 0;
             for (const Nbr& pc : t.col[t.boxes[b].parent])
@@ -544,7 +555,8 @@ struct Builder {
       }
       return c;
     };
-    csr_pass(t.fin, all, [&](int b) { return fine_scan(b, nullptr); }, [&](int b, Nbr* out) { fine_scan(b, out); });
+    csr_pass(t.fin, leaves_only ? leaf_ids(all) : all, [&](int b) { return fine_scan(b, nullptr); },
+             [&](int b, Nbr* out) { fine_scan(b, out); });
     if (std::getenv("SDMK_TIMING")) {
       auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
       std::fprintf(stderr, "[sdmk timing] neighbours: levels %.2f ms, fine %.2f ms (%d boxes, %d levels)\n",
@@ -591,6 +603,7 @@ static HostTree build_topology_impl(int dim, bool periodic, int n_s, int p, int 
   if (with_neighbours) {
     B.neighbours();
     B.t.has_neighbours = true;
+    B.t.full_neighbours = true;
   } else {
     B.t.level_boxes.assign(B.t.max_level + 1, {});
     for (int b = 0; b < B.t.num_boxes(); ++b) B.t.level_boxes[B.t.boxes[b].level].push_back(b);
@@ -619,13 +632,14 @@ HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, int nt, 
   return build_topology_impl(dim, periodic, n_s, p, ns, nullptr, nt, nullptr, &pa, with_neighbours);
 }
 
-void finish_topology(HostTree& t) {
-  if (t.has_neighbours) return;
+void finish_topology(HostTree& t, bool full) {
+  if (t.has_neighbours && (t.full_neighbours || !full)) return;
   Builder B;
   B.t = std::move(t);
   B.nchild = 1 << B.t.dim;
-  B.neighbours();
+  B.neighbours(!full);
   B.t.has_neighbours = true;
+  B.t.full_neighbours = full;
   t = std::move(B.t);
 }
 

@@ -57,7 +57,8 @@ struct Csr {
 struct HostTree {
   int dim = 3, n_s = 0, p = 0, max_level = 0;
   bool periodic = false, alias = true, depth_capped = false;
-  bool has_neighbours = false;  // col / crs / fin built (finish_topology)
+  bool has_neighbours = false;   // col / crs / fin built (finish_topology)
+  bool full_neighbours = false;  // crs / fin for every box, not only the leaves
   std::vector<Box> boxes;
   std::vector<std::vector<int>> level_boxes;
   Csr col, crs, fin;  // colleagues / coarse / fine
@@ -87,7 +88,9 @@ struct PointAccess {
 // upward pass needs only the boxes; the engine builds the lists while it runs)
 HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, int nt, const PointAccess& pa,
                         bool with_neighbours = true);
-void finish_topology(HostTree& t);
+// full = false builds coarse / fine lists for the leaves only (what the
+// evaluation reads); dump_topology needs full lists
+void finish_topology(HostTree& t, bool full = false);
 
 // The reference's canonical text dump (tree.cpp:325-354).
 std::string dump_topology(const HostTree& t);
