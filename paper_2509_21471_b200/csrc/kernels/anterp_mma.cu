@@ -613,7 +613,11 @@ void launch_anterp_mma(int kernel, const ChebDev& cb, const DBox* boxes, const i
         cb, boxes, leaves, basis, str, n, out);                                                         \
   } while (0)
   static const bool old_a = std::getenv("SDMK_ANTERP_OLD") != nullptr;
-  if (!old_a && cb.dim == 3 && p == 23 && kernel == 0) A2(9, 3, 23, 0, 12);
+#ifndef SDMK_A2K_NTW
+#define SDMK_A2K_NTW 3
+#define SDMK_A2K_W 12
+#endif
+  if (!old_a && cb.dim == 3 && p == 23 && kernel == 0) A2(9, SDMK_A2K_NTW, 23, 0, SDMK_A2K_W);
   else if (!old_a && cb.dim == 3 && p == 22 && kernel == 1) A2(SDMK_A2S_MT, SDMK_A2S_NTW, 22, 1, 12);
   else if (!old_a && cb.dim == 3 && p == 30 && kernel == 0) A2(12, 2, 30, 0, 12);
   else if (cb.dim == 3 && p == 23 && kernel == 0) AMS(3, 6, 23, 0, 3);
