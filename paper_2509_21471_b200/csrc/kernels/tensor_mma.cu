@@ -762,6 +762,166 @@ void tensor_down_t(const double* mats, const int* in_list, const int* out_box, c
   k_tensor_down<PC><<<grid, kTDW * 32, smem, st>>>(mats, in_list, out_box, ci, seg, nch, src, dst);
 }
 
+
+// Upward merge of the 2^3 children into their parent with the shared suffix
+// of the separable applies (dmk.cpp:624-653), the mirror of k_tensor_down:
+//   parent = sum_c (Mz_cz (x) My_cy (x) Mx_cx) child_c,   c = cx | cy << 1 | cz << 2.
+// Per group of G input slabs jz0..jz0+G-1 (children streamed from L2):
+//   X : S_cz,cy[s][jy][ix] = sum_cx sum_jx child_c[jz0+s][jy][jx] Mx_cx[ix][jx]   (K = 2p)
+//   Y : T_cz[s][iy][ix]    = sum_cy sum_jy My_cy[iy][jy] S_cz,cy[s][jy][ix]       (K = 2p)
+//   Z : parent[iz][iy,ix] += sum_cz sum_s Mz_cz[iz][jz0+s] T_cz[s][iy][ix]       (K = 2G)
+// -- 14 p^4 DMMA work per parent and channel instead of 24 p^4 for eight
+// independent children; the parent accumulates in registers over the groups
+// (12 warps x up to 6 column tiles x 3 row tiles) and is written once.
+// Missing children (no sources) read as zeros.
+constexpr int kTUW = 12, kTUG = 4;
+template <int PC>
+__global__ void __launch_bounds__(kTUW * 32, 1)
+    k_tensor_up(const double* __restrict__ mats, const int* __restrict__ in_list, const int* __restrict__ out_box,
+                const int* __restrict__ ci_list, int nch, const double* __restrict__ src, double* __restrict__ dst) {
+  constexpr int p = PC, pp = p * p, nodes = p * pp, G = kTUG;
+  constexpr int P8 = 24, SA = 28, SZ = 28, PL = P8 * SZ;  // plane: 24 rows x SZ
+  constexpr int NN = (pp + 7) / 8;                        // Z-stage column tiles
+  constexpr int ZNT = (NN + kTUW - 1) / kTUW;             // per warp
+  static_assert(p >= 17 && p <= 24, "PT = 3 shapes");
+  extern __shared__ double sm[];
+  double* Mm = sm;                // [2][P8][SA]
+  double* Ss = Mm + 2 * P8 * SA;  // [4 (cz,cy)][G] planes [jy][ix]
+  double* Ts = Ss + 4 * G * PL;   // [2 cz][G] planes [iy][ix]
+  __shared__ int s_in[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  for (int r = warp; r < 2 * P8; r += kTUW) {
+    const int bsel = r / P8, rr = r % P8;
+    for (int c = lane; c < SA; c += 32) Mm[r * SA + c] = (rr < p && c < p) ? mats[(size_t)bsel * pp + rr * p + c] : 0.0;
+  }
+  const int par = blockIdx.x, ch = blockIdx.y;
+  if (tid < 8) s_in[tid] = -1;
+  __syncthreads();
+  if (tid < 8) {
+    const int ib = in_list[par * 8 + tid];
+    if (ib >= 0) s_in[ci_list[par * 8 + tid] & 7] = ib;
+  }
+  __syncthreads();
+  // X-stage B fragments (Mx_cx, all ix tiles and k-steps) stay in registers
+  double bx[2][3][6];
+#pragma unroll
+  for (int cx = 0; cx < 2; ++cx)
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt)
+#pragma unroll
+      for (int ks = 0; ks < 6; ++ks) bx[cx][nt][ks] = Mm[(cx * P8 + nt * 8 + g) * SA + ks * 4 + t];
+  double acc[ZNT][3][2];
+#pragma unroll
+  for (int i = 0; i < ZNT; ++i)
+#pragma unroll
+    for (int m = 0; m < 3; ++m) acc[i][m][0] = acc[i][m][1] = 0.0;
+  for (int jz0 = 0; jz0 < p; jz0 += G) {
+    // ---- X stage: unit (pair (cz,cy), slab s, jy tile) x the 3 ix tiles
+    for (int u = warp; u < 4 * G * 3; u += kTUW) {
+      const int pr = u / (3 * G), s = (u / 3) % G, it = u % 3;
+      const int jz = jz0 + s, jy = it * 8 + g;
+      double c[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int cx = 0; cx < 2; ++cx) {
+        const int cb = s_in[cx | (pr << 1)];
+        const bool ok = cb >= 0 && jz < p && jy < p;
+        const double* in = src + ((size_t)(cb >= 0 ? cb : 0) * nch + ch) * nodes + (size_t)(jz < p ? jz : 0) * pp +
+                           (jy < p ? jy : 0) * p;
+        double a[6];
+#pragma unroll
+        for (int ks = 0; ks < 6; ++ks) {
+          const int jx = ks * 4 + t;
+          a[ks] = (ok && jx < p) ? __ldg(in + jx) : 0.0;
+        }
+#pragma unroll
+        for (int ks = 0; ks < 6; ++ks)
+#pragma unroll
+          for (int nt = 0; nt < 3; ++nt) dev::dmma(c[nt][0], c[nt][1], a[ks], bx[cx][nt][ks]);
+      }
+      double* Sp = Ss + (pr * G + s) * PL + jy * SZ;
+#pragma unroll
+      for (int nt = 0; nt < 3; ++nt) {
+        Sp[nt * 8 + 2 * t] = c[nt][0];
+        Sp[nt * 8 + 2 * t + 1] = c[nt][1];
+      }
+    }
+    __syncthreads();
+    // ---- Y stage: unit (cz, slab s, iy tile) x the 3 ix tiles, K = (cy, jy)
+    for (int u = warp; u < 2 * G * 3; u += kTUW) {
+      const int cz = u / (3 * G), s = (u / 3) % G, it = u % 3;
+      double c[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int cy = 0; cy < 2; ++cy) {
+        const double* My = Mm + cy * P8 * SA + (it * 8 + g) * SA;
+        const double* Sp = Ss + ((cz * 2 + cy) * G + s) * PL;
+#pragma unroll
+        for (int ks = 0; ks < 6; ++ks) {
+          const double a = My[ks * 4 + t];
+#pragma unroll
+          for (int nt = 0; nt < 3; ++nt) dev::dmma(c[nt][0], c[nt][1], a, Sp[(ks * 4 + t) * SZ + nt * 8 + g]);
+        }
+      }
+      double* Tp = Ts + (cz * G + s) * PL + (it * 8 + g) * SZ;
+#pragma unroll
+      for (int nt = 0; nt < 3; ++nt) {
+        Tp[nt * 8 + 2 * t] = c[nt][0];
+        Tp[nt * 8 + 2 * t + 1] = c[nt][1];
+      }
+    }
+    __syncthreads();
+    // ---- Z stage: parent[iz][n] += sum_(cz, s) Mz_cz[iz][jz0 + s] T_cz[s][n], n = iy p + ix
+    {
+      double a[3][2];
+#pragma unroll
+      for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int k = kk * 4 + t, cz = k / G, sl = k % G;
+          a[mt][kk] = jz0 + sl < p ? Mm[(cz * P8 + mt * 8 + g) * SA + jz0 + sl] : 0.0;
+        }
+#pragma unroll
+      for (int i = 0; i < ZNT; ++i) {
+        const int nt = warp + kTUW * i;
+        if (nt >= NN) continue;
+        const int n = nt * 8 + g;
+        const int iy = n / p, ix = n - iy * p;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int k = kk * 4 + t, cz = k / G, sl = k % G;
+          const double b = n < pp ? Ts[(cz * G + sl) * PL + iy * SZ + ix] : 0.0;
+#pragma unroll
+          for (int mt = 0; mt < 3; ++mt) dev::dmma(acc[i][mt][0], acc[i][mt][1], a[mt][kk], b);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  double* out = dst + ((size_t)out_box[par] * nch + ch) * nodes;
+#pragma unroll
+  for (int i = 0; i < ZNT; ++i) {
+    const int nt = warp + kTUW * i;
+    if (nt >= NN) continue;
+#pragma unroll
+    for (int mt = 0; mt < 3; ++mt) {
+      const int iz = mt * 8 + g;
+      if (iz >= p) continue;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = nt * 8 + 2 * t + e;
+        if (n < pp) out[(size_t)iz * pp + n] = acc[i][mt][e];
+      }
+    }
+  }
+}
+
+template <int PC>
+void tensor_up_t(const double* mats, const int* in_list, const int* out_box, const int* ci, int nparents, int nch,
+                 const double* src, double* dst, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (2 * 24 * 28 + 6 * kTUG * 24 * 28);
+  cudaFuncSetAttribute(k_tensor_up<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid(nparents, nch);
+  k_tensor_up<PC><<<grid, kTUW * 32, smem, st>>>(mats, in_list, out_box, ci, nch, src, dst);
+}
 }  // namespace
 
 bool tensor_seg_supported(int p, int dim) { return dim == 3 && p >= 17 && p <= 24 && !std::getenv("SDMK_TENSOR_OLD"); }
@@ -791,6 +951,12 @@ void launch_tensor_mma(int p, const double* mats, const int* in_list, const int*
 #define TM(PC_, PT_, NW_, ZT_) \
   tensor_mma_t<PC_, PT_, NW_, ZT_>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st)
   static const bool old3 = std::getenv("SDMK_TENSOR_OLD") != nullptr;
+  static const bool up_suffix = std::getenv("SDMK_TENSOR_NOSUFFIX") == nullptr;
+  if (accumulate == 2 && dim == 3 && up_suffix && !old3 && (p == 22 || p == 23)) {  // merges: shared suffix
+    if (p == 23) tensor_up_t<23>(mats, in_list, out_box, ci, npairs, nch, src, dst, st);
+    else tensor_up_t<22>(mats, in_list, out_box, ci, npairs, nch, src, dst, st);
+    return;
+  }
   if (p == 22 && !old3) tensor3_t<22>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
   else if (p == 23 && !old3) tensor3_t<23>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
   else if (PT == 3 && !old3) tensor3_t<0>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
