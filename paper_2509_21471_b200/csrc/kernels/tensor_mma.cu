@@ -802,6 +802,10 @@ __global__ void __launch_bounds__(kTUW * 32, 1)
     if (ib >= 0) s_in[ci_list[par * 8 + tid] & 7] = ib;
   }
   __syncthreads();
+#ifndef SDMK_TU_REGB
+#define SDMK_TU_REGB 0
+#endif
+#if SDMK_TU_REGB
   // X-stage B fragments (Mx_cx, all ix tiles and k-steps) stay in registers
   double bx[2][3][6];
 #pragma unroll
@@ -810,6 +814,10 @@ __global__ void __launch_bounds__(kTUW * 32, 1)
     for (int nt = 0; nt < 3; ++nt)
 #pragma unroll
       for (int ks = 0; ks < 6; ++ks) bx[cx][nt][ks] = Mm[(cx * P8 + nt * 8 + g) * SA + ks * 4 + t];
+#define TU_BX(cx, nt, ks) bx[cx][nt][ks]
+#else
+#define TU_BX(cx, nt, ks) Mm[((cx) * P8 + (nt) * 8 + g) * SA + (ks) * 4 + t]
+#endif
   double acc[ZNT][3][2];
 #pragma unroll
   for (int i = 0; i < ZNT; ++i)
@@ -836,7 +844,7 @@ __global__ void __launch_bounds__(kTUW * 32, 1)
 #pragma unroll
         for (int ks = 0; ks < 6; ++ks)
 #pragma unroll
-          for (int nt = 0; nt < 3; ++nt) dev::dmma(c[nt][0], c[nt][1], a[ks], bx[cx][nt][ks]);
+          for (int nt = 0; nt < 3; ++nt) dev::dmma(c[nt][0], c[nt][1], a[ks], TU_BX(cx, nt, ks));
       }
       double* Sp = Ss + (pr * G + s) * PL + jy * SZ;
 #pragma unroll
