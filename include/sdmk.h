@@ -163,12 +163,14 @@ int sdmk_direct_residual_sum(sdmk_context* ctx, const sdmk_plan* plan, int dim, 
                              double* u);
 /* ---- multi-GPU (one process per GPU) ----
    Shard the following evaluations by target leaves:
-   rank owns a contiguous Morton run of target leaves (balanced by target
-   count); the upward pass stays replicated, the downward, far-field and
-   residual passes run only for the owned leaves and their ancestors, and u
-   is written as zeros for other ranks' targets, so an element-wise sum over
-   ranks (an all-reduce) is the full result, bitwise equal to nranks = 1.
-   No reference counterpart (the reference is a single-process library). */
+   rank owns a contiguous Morton run of target leaves (balanced by a cost
+   model of its near-field pairs and plane-wave boxes).  Without a
+   communicator (sdmk_comm_init below) the upward pass stays replicated, the
+   downward, far-field and residual passes run only for the owned leaves and
+   their ancestors, and u is written as zeros for other ranks' targets, so an
+   element-wise sum over ranks (an all-reduce) is the full result, bitwise
+   equal to nranks = 1.  No reference counterpart (the reference is a
+   single-process library). */
 int sdmk_set_shard(sdmk_context* ctx, int rank, int nranks);
 
 /* Distributed upward pass ("source halos exchanged").
