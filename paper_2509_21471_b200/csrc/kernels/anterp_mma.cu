@@ -426,6 +426,9 @@ __global__ void __launch_bounds__(W * 32, 1) k_anterp2(ChebDev cb, const DBox* _
 }
 
 // ------------------------------------------------------------------- K11 --
+#ifndef SDMK_I_ROWS
+#define SDMK_I_ROWS 128  // W rows staged per chunk (rounded down to whole (j, iz) row groups)
+#endif
 // warps per CTA (IW) and m-tiles per warp (ITW) are template parameters:
 // 8 x 5 for TY <= 3 (p <= 24; measured 4 % faster than 12 x 4 at p = 23),
 // 12 x 4 above (the 8 x 5 accumulators would spill); one pass per leaf covers
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DB
                                                            double* __restrict__ ufar) {
   constexpr int PY = 8 * TY, KS = 2 * TY, WS = PY + 4;
   constexpr int kTB = kIW * kITW * 8;  // targets per pass
-  constexpr int RG = PY >= 128 ? 1 : 128 / PY;  // (j, iz) rows per chunk
+  constexpr int RG = PY >= SDMK_I_ROWS ? 1 : SDMK_I_ROWS / PY;  // (j, iz) rows per chunk
   constexpr int NR = RG * PY;                   // W rows per chunk
   extern __shared__ double sm[];
   const int p = PC > 0 ? PC : cb.p, dim = DC > 0 ? DC : cb.dim, pz = dim == 3 ? p : 1;
@@ -640,7 +643,7 @@ void launch_interp_mma(const ChebDev& cb, const DBox* boxes, const int* leaves, 
   const int p = cb.p;
   const int TYv = (p + 7) / 8;
   auto smem_for = [&](int TY) {
-    const int PY = 8 * TY, WS = PY + 4, RG = PY >= 128 ? 1 : 128 / PY;
+    const int PY = 8 * TY, WS = PY + 4, RG = PY >= SDMK_I_ROWS ? 1 : SDMK_I_ROWS / PY;
     const int tb = TY <= 3 ? 8 * 5 * 8 : 12 * 4 * 8;  // the kernel's IW * ITW * 8
     return sizeof(double) * (2 * (size_t)RG * PY * WS + (size_t)tb * (p | 1));
   };
