@@ -21,6 +21,7 @@
 #include <cmath>
 #include <stdexcept>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "../sdmk.h"
@@ -113,14 +114,26 @@ inline void check(int code) {
   throw std::runtime_error(msg);
 }
 
+inline int& device_slot() {
+  static thread_local int dev = 0;
+  return dev;
+}
+
+struct ContextHolder {
+  sdmk_context* c = nullptr;
+  ~ContextHolder() {
+    if (c) sdmk_destroy(c);
+  }
+};
+
+inline ContextHolder& holder() {
+  static thread_local ContextHolder h;
+  return h;
+}
+
 inline sdmk_context* context() {
-  static thread_local struct Holder {
-    sdmk_context* c = nullptr;
-    ~Holder() {
-      if (c) sdmk_destroy(c);
-    }
-  } h;
-  if (!h.c) check(sdmk_create(0, &h.c));
+  ContextHolder& h = holder();
+  if (!h.c) check(sdmk_create(device_slot(), &h.c));
   return h.c;
 }
 
@@ -239,5 +252,28 @@ inline std::vector<double> direct_residual_sum(const SplitKernel& sk, const Part
                                          periodic ? 1 : 0, u.data()));
   return u;
 }
+
+// ---- additions beyond the reference API: several GPUs, one process each ----
+// (include/sdmk.h sdmk_comm_init).  Call use_device before the first
+// evaluation on a thread; rank 0 makes the id, every rank passes the same
+// bytes to init_comm; later evaluations on this thread return the full u on
+// every rank.
+namespace b200 {
+inline void use_device(int device) {
+  if (detail::holder().c && detail::device_slot() != device)
+    throw std::invalid_argument("use_device: this thread already evaluates on another GPU");
+  detail::device_slot() = device;
+}
+
+inline std::array<unsigned char, 128> nccl_unique_id() {
+  std::array<unsigned char, 128> id{};
+  detail::check(sdmk_comm_unique_id(id.data()));
+  return id;
+}
+
+inline void init_comm(int rank, int nranks, const std::array<unsigned char, 128>& id) {
+  detail::check(sdmk_comm_init(detail::context(), rank, nranks, id.data()));
+}
+}  // namespace b200
 
 }  // namespace stokesdmk

@@ -24,6 +24,15 @@ std::vector<double> timed_evaluate(const DmkPlan& plan, const ParticleSystem& sy
   return u;
 }
 
+// the multi-GPU additions (one process per GPU; include/sdmk.h sdmk_comm_init)
+[[maybe_unused]] static std::vector<double> sharded_evaluate(int rank, int nranks, const DmkPlan& plan,
+                                                             const ParticleSystem& sys,
+                                                             const std::array<unsigned char, 128>& id) {
+  stokesdmk::b200::use_device(rank);
+  stokesdmk::b200::init_comm(rank, nranks, id);
+  return evaluate_with_plan(plan, sys, EwaldMode::free_space);
+}
+
 int main() {
   ParticleSystem sys;
   sys.dim = 3;
