@@ -45,6 +45,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK = 6551.7
+# one metric string for both arms (the driver pairs the lines by it)
+METRIC = "points/sec (3D Stokeslet DMK, N=1e7, eps=1e-6)"
 
 
 def log(*a):
@@ -232,11 +234,34 @@ def run_ours(args, rank, world, local_rank):
         e1.synchronize()
         barrier()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+        # the same through pageable host arrays (what a C++ caller passing
+        # std::vector gives the drop-in): staged copies inside the call
+        e2e_pg_ms = None
+        if world == 1 or use_comm:
+            sys_pg = g.ParticleSystem(3, np.ascontiguousarray(x), np.zeros(0), np.ascontiguousarray(s))
+            u_pg = np.empty(n * 3)
+
+            def step_pageable():
+                r = g.sdmk_report()
+                code = lib.sdmk_evaluate_with_plan(ctx._h, C.byref(cplan), 3, n, g._dptr(sys_pg.sources), 0,
+                                                   g._dptr(None), g._dptr(sys_pg.strengths), 0, g._dptr(u_pg),
+                                                   C.byref(r))
+                g._raise(code)
+
+            step_pageable()
+            barrier()
+            e0.record(tstream)
+            for _ in range(args.steps):
+                step_pageable()
+            e1.record(tstream)
+            e1.synchronize()
+            barrier()
+            e2e_pg_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
         # accuracy guard on rank 0: the device result equals the host-path result
         u_dev = d_u.cpu().numpy()
         same = float(np.max(np.abs(u_dev - h_u.numpy())))
         r0 = reps[-1]
-        results[kname] = {"ms": ms, "e2e_ms": e2e_ms, "rep": r0, "plan": plan.__dict__, "dev_vs_host_maxabs": same,
+        results[kname] = {"ms": ms, "e2e_ms": e2e_ms, "e2e_pageable_ms": e2e_pg_ms, "rep": r0, "plan": plan.__dict__, "dev_vs_host_maxabs": same,
                           "launches": int(r0["kernel_launches"])}
         log(f"[bench] {kname}: {ms:.2f} ms/step device, {e2e_ms:.2f} ms/step e2e; report {r0}")
         del d_x, d_s, d_u
@@ -258,7 +283,19 @@ def run_ours(args, rank, world, local_rank):
             traffic = int(json.load(f)["dram_bytes"]) if args.n == 10_000_000 else None
     except (OSError, ValueError, KeyError):
         traffic = None
+    hw = None  # FP64 rate the hardware executed (ncu dadd + dmul + 2 dfma over the kernel's duration)
+    try:
+        with open(os.path.join(ROOT, "profiles", "round2", "residual_hw.json")) as f:
+            hw = json.load(f)
+    except (OSError, ValueError):
+        hw = None
     roof = {"bound": "fp64", "kernel": "k_residual (near-field P2P)", "achieved": res_flops / res_t / 1e12,
+            "achieved_kind": ("algorithm-equivalent rate: SURVEY 8(d) work (8 FLOP per tested pair + "
+                              "F_in = 3(33+33)+30 = 228 per in-support pair, the reference's Clenshaw cost) over "
+                              "the kernel's CUDA-event time; the kernel evaluates degree-5 piecewise "
+                              "re-expansions, so it executes fewer FP64 operations than this counts"),
+            "hw_fp64_tflops": hw.get("hw_fp64_tflops") if hw else None,
+            "hw_fp64_source": hw.get("source") if hw else None,
             "peak": peak, "unit": "TFLOP/s", "frac": (res_flops / res_t / 1e12) / peak, "traffic": traffic,
             "traffic_source": "profiles/round1/residual_traffic.json (ncu dram__bytes_read+write, one launch)",
             "peak_source": "measured DFMA microbenchmark (sdmk_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",
@@ -317,13 +354,19 @@ def main():
                 vals.append((v, t))
         v = float(np.mean([a for a, _ in vals]))
         ms = float(np.mean([t for _, t in vals])) * 1e3
-        line = {"metric": "points/sec (3D Stokeslet DMK, eps=1e-6)", "value": v, "unit": "points/s",
+        rcfg = dict(config)
+        rcfg.update({"workload": f"bounded sample of the metric workload: 3D free-space DMK, N={args.cpu_sample} "
+                                 f"iid uniform in [-1/2,1/2]^3, eps={args.eps:g}, prolate window, targets = sources",
+                     "n_points": args.cpu_sample, "sample_of": args.n, "kernels": "stokeslet",
+                     "parallelism": f"CPU, OpenMP {threads} threads (rank 0 only)"})
+        line = {"metric": METRIC, "value": v, "unit": "points/s",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded uniform points, N(0,1) forces)", "config": config, "impl": "reference",
+                "data": "synthetic (seeded uniform points, N(0,1) forces)", "config": rcfg, "impl": "reference",
                 "cpu_baseline": {"value": v, "unit": "points/s", "cores": threads, "kind": "reference",
                                  "sample": f"evaluate_with_plan on N={args.cpu_sample} points of the same "
-                                           "distribution per step (full N=1e7 takes ~17 min on 8 cores)"},
+                                           "distribution per step; the full N=1e7 run on this host's 16 cores is "
+                                           "in profiles/round2/parity_full_size.jsonl (ref_time)"},
                 "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -349,16 +392,22 @@ def main():
     for k, r in results.items():
         extra[k] = {"points_per_s": n / (r["ms"] * 1e-3), "ms_per_step": r["ms"],
                     "e2e_points_per_s": n / (r["e2e_ms"] * 1e-3), "e2e_ms": r["e2e_ms"],
+                    "e2e_pageable_ms": r.get("e2e_pageable_ms"),
                     "p": r["plan"]["p"], "N1": r["plan"]["N1"], "num_boxes": r["rep"]["num_boxes"],
                     "max_level": r["rep"]["max_level"],
                     "pass_s": {k2: r["rep"][k2] for k2 in ("t_tree", "t_upward", "t_root", "t_downward",
                                                            "t_residual", "t_residual_kernel", "t_planewave")}}
-    line = {"metric": "points/sec (3D Stokeslet DMK, N=1e7, eps=1e-6)", "value": value, "unit": "points/s",
+    line = {"metric": METRIC, "value": value, "unit": "points/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": R["ms"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded uniform points, N(0,1) forces; stresslet normals random unit)",
             "config": config, "roofline": roof, "cpu_baseline": cpu,
-            "e2e": {"value": e2e, "unit": "points/s", "h2d_bytes_per_step": n * 6 * 8, "d2h_bytes_per_step": n * 3 * 8},
+            "e2e": {"value": e2e, "unit": "points/s", "h2d_bytes_per_step": n * 6 * 8, "d2h_bytes_per_step": n * 3 * 8,
+                    "host_buffers": "pinned"},
+            "e2e_pageable": ({"value": n / (R["e2e_pageable_ms"] * 1e-3), "unit": "points/s",
+                              "h2d_bytes_per_step": n * 6 * 8, "d2h_bytes_per_step": n * 3 * 8,
+                              "host_buffers": "pageable (numpy / std::vector)"}
+                             if R.get("e2e_pageable_ms") else None),
             "gpu_launches": R["launches"] * args.steps, "clocks": clocks, "kernels": extra}
     print(json.dumps(line), flush=True)
 

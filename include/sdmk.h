@@ -24,6 +24,16 @@
  *   sdmk_target_far_fields   stokesdmk::target_far_fields     dmk.hpp:116-117, dmk.cpp:861-915
  *   sdmk_residual_pass       stokesdmk::residual_pass         dmk.hpp:128-131, dmk.cpp:919-1032
  *   sdmk_load_tables / sdmk_save_tables   import/export_split_kernel (split.hpp:153-154, SDMKSPLT v1)
+ *   sdmk_tree_build          stokesdmk::build_tree            tree.hpp:90-92, tree.cpp:230-298
+ *   sdmk_tree_neighbors      neighbor_query / Tree::neighbors tree.hpp:44-51, 95
+ *   sdmk_tree_sorted         Tree::src_points/tgt_points/src_q/tgt_q  tree.hpp:74-78
+ *   sdmk_pass_upward         stokesdmk::upward_pass           dmk.hpp:84-85
+ *   sdmk_pass_root_far_field stokesdmk::root_far_field        dmk.hpp:98-100, dmk.cpp:671-701
+ *   sdmk_pass_downward       stokesdmk::downward_pass         dmk.hpp:110-112, dmk.cpp:705-857
+ *   sdmk_pass_target_far_fields  stokesdmk::target_far_fields dmk.hpp:116-117
+ *   sdmk_pass_residual       stokesdmk::residual_pass         dmk.hpp:128-131
+ *   sdmk_evaluate_with_tables  evaluate_with_plan(..., const SplitKernel* tables)  dmk.hpp:151-155
+ *   sdmk_host_build_tables   stokesdmk::build_split_kernel    split.hpp:89-90, split.cpp:319-396
  *   sdmk_direct_sum          stokesdmk::direct_sum            oracle.hpp:60-65, oracle.cpp:143-179
  *   sdmk_direct_residual_sum stokesdmk::direct_residual_sum   oracle.hpp:67-75, oracle.cpp:181-241
  *
@@ -146,6 +156,62 @@ int sdmk_upward_pass(sdmk_context* ctx, double* outgoing);
 int sdmk_incoming(sdmk_context* ctx, int stage, double* incoming);
 int sdmk_target_far_fields(sdmk_context* ctx, double* u);
 int sdmk_residual_pass(sdmk_context* ctx, double* u);
+
+/* ---- the reference's tree-first pass-level API ----
+   One tree per context: sdmk_tree_build replaces build_tree (tree.hpp:90-92,
+   tree.cpp:230-298) -- no wrap, points must lie in [-1/2, 1/2]^dim, the
+   reference's messages -- and the sdmk_pass_* functions replace the passes
+   of dmk.hpp:84-131 with the plan, split tables, strengths and proxies the
+   caller holds (ProxyData layout: boxes x channels x p^dim, axis 0 fastest,
+   host memory).  The tree's fields come back through sdmk_tree_info /
+   sdmk_tree_boxes / sdmk_tree_perm / sdmk_tree_dump above and: */
+int sdmk_tree_build(sdmk_context* ctx, int dim, int periodic, int n_s, int proxy_order, int64_t n_src,
+                    const double* src, int64_t n_tgt, const double* tgt);
+/* TreeNeighbors (tree.hpp:44-51): counts[3*b + k] = length of list k
+   (0 colleagues, 1 coarse, 2 fine) of box b; entries (NULL: counts only) =
+   4 int32 per entry (box, shift[0..2]) in box order, lists in that order */
+int sdmk_tree_neighbors(sdmk_context* ctx, int64_t* counts, int32_t* entries);
+/* Tree::src_points / tgt_points (point-major) and src_q / tgt_q (3 int32 per
+   point, zero third axis in 2D); any output may be NULL */
+int sdmk_tree_sorted(sdmk_context* ctx, double* src_points, double* tgt_points, int32_t* src_q, int32_t* tgt_q);
+/* upward_pass (dmk.hpp:84-85): strengths in caller order, n_str doubles */
+int sdmk_pass_upward(sdmk_context* ctx, const sdmk_plan* plan, int64_t n_str, const double* str,
+                     double* outgoing);
+/* root_far_field (dmk.hpp:98-100): incoming (n_in doubles) += root far field.
+   tables: an SDMKSPLT v1 image (the SplitKernel), or NULL for the plan's */
+int sdmk_pass_root_far_field(sdmk_context* ctx, const sdmk_plan* plan, const unsigned char* tables, int64_t nbytes,
+                             int64_t n_out, const double* outgoing, int periodic, int64_t n_in, double* incoming);
+/* downward_pass (dmk.hpp:110-112): incoming updated in place */
+int sdmk_pass_downward(sdmk_context* ctx, const sdmk_plan* plan, const unsigned char* tables, int64_t nbytes,
+                       int64_t n_out, const double* outgoing, int periodic, int64_t n_in, double* incoming);
+/* target_far_fields (dmk.hpp:116-117): u = dim * targets doubles, caller order */
+int sdmk_pass_target_far_fields(sdmk_context* ctx, const sdmk_plan* plan, int64_t n_in, const double* incoming,
+                                double* u);
+/* residual_pass (dmk.hpp:128-131); coincident points -> SDMK_EDOMAIN */
+int sdmk_pass_residual(sdmk_context* ctx, const sdmk_plan* plan, const unsigned char* tables, int64_t nbytes,
+                       int64_t n_str, const double* str, int periodic, double* u);
+/* evaluate_with_plan(plan, sys, mode, report, &tables) (dmk.hpp:151-155) with
+   the caller's split tables as an SDMKSPLT v1 image (NULL: the plan's) */
+int sdmk_evaluate_with_tables(sdmk_context* ctx, const sdmk_plan* plan, const unsigned char* tables, int64_t nbytes,
+                              int dim, int64_t n_src, const double* src, int64_t n_tgt, const double* tgt,
+                              const double* str, int mode, double* u, sdmk_report* report);
+/* build_split_kernel(kernel, dim, build_prolate(c) | build_gaussian(sigma), tol)
+   (split.cpp:319-396) on the host: writes the SDMKSPLT v1 image (at most cap
+   bytes; buf may be NULL) and returns its length, -1 on error */
+int64_t sdmk_host_build_tables(int kernel, int dim, int window, double c, double sigma, double tol,
+                               unsigned char* buf, int64_t cap);
+/* build_prolate(c) / build_gaussian(sigma) (windows.cpp): scalars[5] =
+   lambda0, norm_r, trunc_error, psi0, chi0; coeffs (at most cap) = the
+   Legendre coefficients; returns their count, -1 on error */
+int sdmk_host_build_window(int window, double c, double sigma, double* scalars, double* coeffs, int cap);
+/* window_eval (what 0), window_deriv (1), window_fourier (2), phi_tail (3),
+   mollifier_fourier (4) of a window given by its fields, at n points */
+int sdmk_host_window_eval(int window, double c, double sigma, const double* coeffs, int ncoef,
+                          const double* scalars, int what, int64_t n, const double* x, double* out);
+/* direct_residual_sum(sk, sys, cutoff, periodic) with the caller's tables */
+int sdmk_direct_residual_sum_tables(sdmk_context* ctx, const unsigned char* tables, int64_t nbytes, int dim,
+                                    int64_t n_src, const double* src, int64_t n_tgt, const double* tgt,
+                                    const double* str, double cutoff, int periodic, double* u);
 
 /* ---- O(N*M) reference sums on the GPU ----
    Same per-target source order, Kahan accumulation and unfused expression

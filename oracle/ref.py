@@ -81,6 +81,15 @@ def lib():
         L.ref_truncated_biharmonic_fourier.restype = C.c_double
         L.ref_mollifier_taylor.argtypes = [dp]
         L.ref_residual_apply.argtypes = [dp, C.c_double, dp, dp]
+        L.ref_run_full.argtypes = [dp, dp, dp, C.POINTER(ref_report)]
+        L.ref_proxy.argtypes = [C.c_int, C.POINTER(C.c_int64)]
+        L.ref_proxy.restype = dp
+        L.ref_release.argtypes = []
+        L.ref_release.restype = None
+        L.ref_time_tree.argtypes = []
+        L.ref_time_tree.restype = C.c_double
+        L.ref_count_pairs.argtypes = [C.POINTER(C.c_int64)]
+        L.ref_set_window.argtypes = [C.c_double, C.c_double]
         _lib = L
     return _lib
 
@@ -200,3 +209,38 @@ class RefProblem:
 
     def export_tables(self, path):
         _chk(lib().ref_export_tables(path.encode()))
+
+    # ---- full-size parity (tools/parity_configs.py) ----
+    def run_full(self):
+        """The passes of evaluate_with_plan once (shim ref_run_full): returns
+        far, residual, u (caller order) and the pass times; the proxies stay
+        alive for proxy() until release()."""
+        far, res, u = (np.empty(self.nt * self.dim) for _ in range(3))
+        rep = ref_report()
+        _chk(lib().ref_run_full(_dp(far), _dp(res), _dp(u), C.byref(rep)))
+        return far, res, u, {k: getattr(rep, k) for k, _ in ref_report._fields_}
+
+    def proxy(self, which: int):
+        """Zero-copy view of the kept outgoing (0) / incoming (1) proxies."""
+        n = C.c_int64()
+        ptr = lib().ref_proxy(which, C.byref(n))
+        if n.value == 0:
+            return np.empty(0)
+        return np.ctypeslib.as_array(ptr, shape=(n.value,))
+
+    def release(self):
+        lib().ref_release()
+
+    def time_tree(self) -> float:
+        return lib().ref_time_tree()
+
+    def count_pairs(self):
+        """(tested, in_support, coincident) pairs of the reference's residual loop."""
+        out = (C.c_int64 * 3)()
+        _chk(lib().ref_count_pairs(out))
+        return tuple(int(v) for v in out)
+
+    def set_window(self, c: float = 0.0, sigma: float = 0.0):
+        """Rebuild the problem's split tables with another window (same kernel, dim, table_tol)."""
+        _chk(lib().ref_set_window(float(c), float(sigma)))
+

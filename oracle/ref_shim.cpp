@@ -20,6 +20,7 @@
  * The shim keeps one "current problem" (plan, wrapped system, tables, tree)
  * so a test can fetch every pass of the same tree.  Not thread safe.
  */
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -345,6 +346,170 @@ int ref_mollifier_taylor(double* a5) {
 }
 int ref_residual_apply(const double* x, double nu, const double* s, double* u) {
   return guard([&] { residual_apply(g_sk, x, nu, s, u); });
+}
+
+
+/* ---- full-size parity support (tools/parity_configs.py) ----
+   ref_run_full runs the passes of evaluate_with_plan (dmk.cpp:1070-1084) once
+   on the current problem, in the same order and with the same calls, keeps
+   the outgoing / incoming proxies alive for ref_proxy, and returns the
+   target far field, the residual and u assembled exactly as
+   dmk.cpp:1086-1102 does (u = far + residual; corr_const * Kahan sum of f
+   for the free-space Stokeslet; periodic_zero_mode for the periodic
+   stresslet).  rep receives the pass times (steady clock, as DmkReport). */
+ProxyData g_og, g_in;
+
+int ref_run_full(double* far, double* res, double* u, ref_report* rep) {
+  return guard([&] {
+    using clock = std::chrono::steady_clock;
+    auto secs = [](clock::time_point a, clock::time_point b) {
+      return std::chrono::duration<double>(b - a).count();
+    };
+    const DmkPlan& plan = g_plan;
+    auto t1 = clock::now();
+    g_og = upward_pass(g_tree, plan, g_sys.strengths);
+    auto t2 = clock::now();
+    g_in = make_incoming(g_tree, plan);
+    root_far_field(g_tree, plan, g_sk, g_og, g_periodic, g_in);
+    auto t3 = clock::now();
+    downward_pass(g_tree, plan, g_sk, g_og, g_periodic, g_in);
+    std::vector<double> uf = target_far_fields(g_tree, plan, g_in);
+    auto t4 = clock::now();
+    std::vector<double> ur = residual_pass(g_tree, plan, g_sk, g_sys.strengths, g_periodic);
+    auto t5 = clock::now();
+    copy_out(uf, far);
+    copy_out(ur, res);
+    const int d = plan.dim;
+    const int nt = g_sys.num_targets();
+    for (size_t i = 0; i < uf.size(); ++i) uf[i] += ur[i];
+    if (plan.kernel == KernelType::stokeslet && !g_periodic && g_sk.corr_const != 0.0) {
+      double sum[3] = {0, 0, 0}, comp[3] = {0, 0, 0};
+      const int ns = g_sys.num_sources();
+      for (int a = 0; a < ns; ++a)
+        for (int j = 0; j < d; ++j) {  /* Kahan, dmk.cpp:540-548 */
+          double y = g_sys.strengths[size_t(a) * d + j] - comp[j];
+          double t = sum[j] + y;
+          comp[j] = (t - sum[j]) - y;
+          sum[j] = t;
+        }
+      for (int t = 0; t < nt; ++t)
+        for (int j = 0; j < d; ++j) uf[size_t(t) * d + j] += g_sk.corr_const * sum[j];
+    }
+    if (plan.kernel == KernelType::stresslet && g_periodic) {
+      std::vector<double> u0 = periodic_zero_mode(plan.kernel, g_sys);
+      for (size_t i = 0; i < uf.size(); ++i) uf[i] += u0[i];
+    }
+    copy_out(uf, u);
+    if (rep) {
+      rep->num_boxes = g_tree.num_boxes();
+      rep->max_level = g_tree.max_level;
+      rep->num_sources = g_sys.num_sources();
+      rep->num_targets = nt;
+      rep->t_tree = 0.0;
+      rep->t_upward = secs(t1, t2);
+      rep->t_root = secs(t2, t3);
+      rep->t_downward = secs(t3, t4);
+      rep->t_residual = secs(t4, t5);
+    }
+  });
+}
+
+/* replaces the current problem's split tables by build_split_kernel with
+   another window (prolate c, or gaussian sigma when c <= 0), same kernel,
+   dim and table_tol: the evaluate_with_plan(..., &tables) case where the
+   tables' window differs from the plan's (dmk.cpp:1059-1069) */
+int ref_set_window(double c, double sigma) {
+  return guard([&] {
+    WindowFunction w = c > 0.0 ? build_prolate(c) : build_gaussian(sigma);
+    g_sk = build_split_kernel(g_plan.kernel, g_plan.dim, w, g_sk.table_tol);
+  });
+}
+
+/* pointer to the kept proxies of ref_run_full (0 outgoing, 1 incoming) */
+const double* ref_proxy(int which, int64_t* n) {
+  const ProxyData& P = which == 0 ? g_og : g_in;
+  *n = int64_t(P.values.size());
+  return P.values.data();
+}
+
+void ref_release() {
+  g_og = ProxyData();
+  g_in = ProxyData();
+}
+
+/* build_tree alone on the current problem's wrapped points (seconds) */
+double ref_time_tree() {
+  auto a = std::chrono::steady_clock::now();
+  Tree t = build_tree(g_sys.sources, g_sys.targets, g_plan.n_s, g_plan.dim, g_periodic, g_plan.p);
+  auto b = std::chrono::steady_clock::now();
+  return std::chrono::duration<double>(b - a).count();
+}
+
+/* The residual pass's pair loop (dmk.cpp:941-1013) over the reference's own
+   tree with residual_apply left out: out[0] = pairs tested (every source of
+   every near range except the alias diagonal), out[1] = pairs in support
+   (r2 < sup2 and r2 != 0), out[2] = coincident pairs.  Same ranges, same
+   shift arithmetic and the same unfused r2 as the reference. */
+int ref_count_pairs(int64_t* out) {
+  return guard([&] {
+    const Tree& tree = g_tree;
+    const int d = g_plan.dim;
+    const bool alias = tree.targets_alias_sources;
+    const std::vector<double>& tp = alias ? tree.src_points : tree.tgt_points;
+    std::vector<int> leaves;
+    for (int b = 0; b < tree.num_boxes(); ++b)
+      if (tree.boxes[b].leaf && tree.box_tgt_count(b) > 0) leaves.push_back(b);
+    int64_t tested = 0, in = 0, zero = 0;
+    struct R { int begin, end; double shift[3]; double nu; bool selfr; };
+#pragma omp parallel reduction(+ : tested, in, zero)
+    {
+      std::vector<R> ranges;
+#pragma omp for schedule(dynamic, 4)
+      for (int li = 0; li < int(leaves.size()); ++li) {
+        const int b = leaves[li];
+        const TreeBox& box = tree.boxes[b];
+        const double r_l = tree.box_side(b), r_f = 0.5 * r_l;
+        ranges.clear();
+        auto add = [&](int sbx, const std::array<std::int8_t, 3>& sh, double nu, bool selfr) {
+          const TreeBox& sb = tree.boxes[sbx];
+          if (sb.src_end == sb.src_begin) return;
+          R r{sb.src_begin, sb.src_end, {double(sh[0]), double(sh[1]), double(sh[2])}, nu, selfr};
+          ranges.push_back(r);
+        };
+        add(b, {0, 0, 0}, r_l, true);
+        const TreeNeighbors& nb = neighbor_query(tree, b);
+        for (const NeighborEntry& e : nb.colleagues) {
+          if (e.box == b && e.shift[0] == 0 && e.shift[1] == 0 && e.shift[2] == 0) continue;
+          if (!tree.boxes[e.box].leaf) continue;
+          add(e.box, e.shift, r_f, false);
+        }
+        for (const NeighborEntry& e : nb.coarse) add(e.box, e.shift, r_l, false);
+        for (const NeighborEntry& e : nb.fine) add(e.box, e.shift, r_f, false);
+        for (int t = box.tgt_begin; t < box.tgt_end; ++t) {
+          const double* xt = tp.data() + size_t(t) * d;
+          for (const R& r : ranges) {
+            const double sup = r.nu * g_sk.support, sup2 = sup * sup;
+            for (int a = r.begin; a < r.end; ++a) {
+              if (alias && r.selfr && a == t) continue;
+              const double* xs = tree.src_points.data() + size_t(a) * d;
+              double r2 = 0.0;
+              for (int ax = 0; ax < d; ++ax) {
+                double x = xt[ax] - (xs[ax] + r.shift[ax]);
+                r2 += x * x;
+              }
+              ++tested;
+              if (r2 >= sup2) continue;
+              if (r2 == 0.0) { ++zero; continue; }
+              ++in;
+            }
+          }
+        }
+      }
+    }
+    out[0] = tested;
+    out[1] = in;
+    out[2] = zero;
+  });
 }
 
 }  // extern "C"

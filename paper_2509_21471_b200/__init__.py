@@ -121,6 +121,11 @@ def lib():
                                           C.c_double, C.c_int, dp], C.c_int),
             "sdmk_host_halo_plan": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, ip, C.c_int64, ip, C.c_int,
                                      P(C.c_int64)], C.c_int),
+            "sdmk_host_build_tables": ([C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_char_p,
+                                        C.c_int64], C.c_int64),
+            "sdmk_host_build_window": ([C.c_int, C.c_double, C.c_double, dp, dp, C.c_int], C.c_int),
+            "sdmk_host_window_eval": ([C.c_int, C.c_double, C.c_double, dp, C.c_int, dp, C.c_int, C.c_int64, dp, dp],
+                                      C.c_int),
             "sdmk_host_shard_plan": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, ip, C.c_int64, ip, C.c_int,
                                       C.c_int, P(C.c_int64)], C.c_int),
         }
@@ -225,6 +230,20 @@ def _arr(a) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=np.float64).ravel())
 
 
+def _check_lengths(kernel: int, d: int, src: np.ndarray, tgt: np.ndarray, stw: np.ndarray):
+    """validate_system's length checks (oracle.cpp:103-118), before the C-ABI reads any array."""
+    if kernel not in (STOKESLET, STRESSLET, ROTLET):
+        raise ValueError("particle sums support the Stokeslet, stresslet, and rotlet kernels")
+    if d not in (2, 3):
+        raise ValueError("ParticleSystem: dim must be 2 or 3")
+    if src.size == 0 or src.size % d:
+        raise ValueError("ParticleSystem: bad source array length")
+    if tgt.size % d:
+        raise ValueError("ParticleSystem: bad target array length")
+    if stw.size != (src.size // d) * strength_components(kernel, d):
+        raise ValueError("ParticleSystem: bad strength array length")
+
+
 class Context:
     """One GPU context (device, stream, buffers, table cache)."""
 
@@ -249,8 +268,11 @@ class Context:
                            report: Optional[dict] = None) -> np.ndarray:
         src, tgt, stw = _arr(sys.sources), _arr(sys.targets), _arr(sys.strengths)
         d = int(sys.dim)
-        ns = src.size // d if d else 0
-        nt = tgt.size // d if d else 0
+        if plan.dim != d:
+            raise ValueError("evaluate: plan and system dimensions differ")
+        _check_lengths(plan.kernel, d, src, tgt, stw)
+        ns = src.size // d
+        nt = tgt.size // d
         u = np.empty((nt if nt else ns) * d)
         rep = sdmk_report()
         cp = plan.to_c()
@@ -281,6 +303,9 @@ class Context:
     def setup(self, plan: DmkPlan, sys: ParticleSystem, mode=FREE_SPACE):
         src, tgt, stw = _arr(sys.sources), _arr(sys.targets), _arr(sys.strengths)
         d = int(sys.dim)
+        if plan.dim != d:
+            raise ValueError("evaluate: plan and system dimensions differ")
+        _check_lengths(plan.kernel, d, src, tgt, stw)
         cp = plan.to_c()
         _raise(lib().sdmk_setup(self._h, C.byref(cp), d, src.size // d, _dptr(src), tgt.size // d,
                                 _dptr(tgt if tgt.size else None), _dptr(stw), _enum(mode, MODES)))
@@ -345,6 +370,7 @@ class Context:
         """stokesdmk::direct_sum (oracle.cpp:143-179): exact kernels, Kahan per target."""
         src, tgt, stw = _arr(sys.sources), _arr(sys.targets), _arr(sys.strengths)
         d = int(sys.dim)
+        _check_lengths(_enum(kernel, KERNELS), d, src, tgt, stw)
         ns, nt = src.size // d, tgt.size // d
         u = np.empty((nt if nt else ns) * d)
         _raise(lib().sdmk_direct_sum(self._h, _enum(kernel, KERNELS), d, ns, _dptr(src), nt,
@@ -532,3 +558,28 @@ def host_halo_plan(dim, periodic, n_s, p, q_src_sorted, nranks, q_tgt_sorted=Non
     a = np.array(out[:], dtype=np.int64)
     return {"recv": a[:R * R].reshape(R, R), "owned_leaves": a[R * R:R * R + R], "above_cut": int(a[R * R + R]),
             "cut_boxes": int(a[R * R + R + 1])}
+
+
+def host_build_tables(kernel, dim: int, window, c: float, sigma: float, tol: float) -> bytes:
+    """build_split_kernel (split.cpp:319-396) on the host: the SDMKSPLT v1 image."""
+    k, w = _enum(kernel, KERNELS), _enum(window, WINDOWS)
+    n = lib().sdmk_host_build_tables(k, int(dim), w, float(c), float(sigma), float(tol), None, 0)
+    if n < 0:
+        _raise(1)
+    buf = C.create_string_buffer(int(n))
+    lib().sdmk_host_build_tables(k, int(dim), w, float(c), float(sigma), float(tol), buf, n)
+    return buf.raw[:n]
+
+
+def host_build_window(window, c: float = 0.0, sigma: float = 0.0) -> dict:
+    """build_prolate / build_gaussian (windows.cpp): scalars and Legendre coefficients."""
+    sc = np.zeros(5)
+    w = _enum(window, WINDOWS)
+    n = lib().sdmk_host_build_window(w, float(c), float(sigma), _dptr(sc), None, 0)
+    if n < 0:
+        _raise(1)
+    co = np.zeros(max(n, 1))
+    lib().sdmk_host_build_window(w, float(c), float(sigma), _dptr(sc), _dptr(co), n)
+    return {"lambda0": sc[0], "norm_r": sc[1], "trunc_error": sc[2], "psi0": sc[3], "chi0": sc[4],
+            "legendre_coeffs": co[:n]}
+

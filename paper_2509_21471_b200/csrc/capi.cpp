@@ -215,11 +215,8 @@ int sdmk_tree_boxes(sdmk_context* c, int32_t* out) {
 
 int sdmk_tree_perm(sdmk_context* c, int32_t* src_perm, int32_t* tgt_perm) {
   return guarded([&] {
-    const Problem& p = need_ctx(c)->problem();
-    if (!p.ready) throw InvalidArgument("no problem set up");
-    cuda_check(cudaMemcpy(src_perm, p.sperm, sizeof(int) * p.ns, cudaMemcpyDeviceToHost), "D2H perm");
-    if (tgt_perm && !p.alias)
-      cuda_check(cudaMemcpy(tgt_perm, p.tperm, sizeof(int) * p.nt, cudaMemcpyDeviceToHost), "D2H perm");
+    if (!src_perm) throw InvalidArgument("sdmk_tree_perm: null output");
+    need_ctx(c)->tree_perm(src_perm, tgt_perm);
   });
 }
 
@@ -249,6 +246,167 @@ int sdmk_target_far_fields(sdmk_context* c, double* out) {
 
 int sdmk_residual_pass(sdmk_context* c, double* out) {
   return guarded([&] { need_ctx(c)->residual(out); });
+}
+
+// ---- tree-first pass-level API ----
+namespace {
+const Tables* image_or_null(Context* x, const unsigned char* tables, int64_t nbytes) {
+  if (!tables) return nullptr;
+  if (nbytes <= 0) throw InvalidArgument("split tables: empty image");
+  return &x->tables_image(tables, (size_t)nbytes);
+}
+}  // namespace
+
+int sdmk_tree_build(sdmk_context* c, int dim, int periodic, int n_s, int proxy_order, int64_t n_src,
+                    const double* src, int64_t n_tgt, const double* tgt) {
+  return guarded([&] {
+    if ((n_src > 0 && !src) || (n_tgt > 0 && !tgt)) throw InvalidArgument("build_tree: null array");
+    need_ctx(c)->tree_build(dim, periodic != 0, n_s, proxy_order, n_src, src, n_tgt, tgt);
+  });
+}
+
+int sdmk_tree_neighbors(sdmk_context* c, int64_t* counts, int32_t* entries) {
+  return guarded([&] {
+    if (!counts) throw InvalidArgument("sdmk_tree_neighbors: null counts");
+    need_ctx(c)->tree_neighbors(counts, entries);
+  });
+}
+
+int sdmk_tree_sorted(sdmk_context* c, double* src_points, double* tgt_points, int32_t* src_q, int32_t* tgt_q) {
+  return guarded([&] { need_ctx(c)->tree_sorted(src_points, tgt_points, src_q, tgt_q); });
+}
+
+int sdmk_pass_upward(sdmk_context* c, const sdmk_plan* plan, int64_t n_str, const double* str, double* outgoing) {
+  return guarded([&] {
+    if (!plan || !str || !outgoing) throw InvalidArgument("upward_pass: null array");
+    need_ctx(c)->pass_upward(to_plan(plan), n_str, str, outgoing);
+  });
+}
+
+int sdmk_pass_root_far_field(sdmk_context* c, const sdmk_plan* plan, const unsigned char* tables, int64_t nbytes,
+                             int64_t n_out, const double* outgoing, int periodic, int64_t n_in, double* incoming) {
+  return guarded([&] {
+    if (!plan || !outgoing || !incoming) throw InvalidArgument("root_far_field: null array");
+    Context* x = need_ctx(c);
+    x->pass_root(to_plan(plan), image_or_null(x, tables, nbytes), n_out, outgoing, periodic != 0, n_in, incoming);
+  });
+}
+
+int sdmk_pass_downward(sdmk_context* c, const sdmk_plan* plan, const unsigned char* tables, int64_t nbytes,
+                       int64_t n_out, const double* outgoing, int periodic, int64_t n_in, double* incoming) {
+  return guarded([&] {
+    if (!plan || !outgoing || !incoming) throw InvalidArgument("downward_pass: null array");
+    Context* x = need_ctx(c);
+    x->pass_downward(to_plan(plan), image_or_null(x, tables, nbytes), n_out, outgoing, periodic != 0, n_in, incoming);
+  });
+}
+
+int sdmk_pass_target_far_fields(sdmk_context* c, const sdmk_plan* plan, int64_t n_in, const double* incoming,
+                                double* u) {
+  return guarded([&] {
+    if (!plan || !incoming || !u) throw InvalidArgument("target_far_fields: null array");
+    need_ctx(c)->pass_target_far(to_plan(plan), n_in, incoming, u);
+  });
+}
+
+int sdmk_pass_residual(sdmk_context* c, const sdmk_plan* plan, const unsigned char* tables, int64_t nbytes,
+                       int64_t n_str, const double* str, int periodic, double* u) {
+  return guarded([&] {
+    if (!plan || !str || !u) throw InvalidArgument("residual_pass: null array");
+    Context* x = need_ctx(c);
+    x->pass_residual(to_plan(plan), image_or_null(x, tables, nbytes), n_str, str, periodic != 0, u);
+  });
+}
+
+int sdmk_evaluate_with_tables(sdmk_context* c, const sdmk_plan* plan, const unsigned char* tables, int64_t nbytes,
+                              int dim, int64_t n_src, const double* src, int64_t n_tgt, const double* tgt,
+                              const double* str, int mode, double* u, sdmk_report* report) {
+  return guarded([&] {
+    if (!plan || !src || !str || !u || (n_tgt > 0 && !tgt)) throw InvalidArgument("evaluate: null array");
+    Context* x = need_ctx(c);
+    const Tables* t = image_or_null(x, tables, nbytes);
+    struct Clear {
+      Context* x;
+      ~Clear() { x->set_tables_override(nullptr); }
+    } clear{x};
+    x->set_tables_override(t);
+    x->evaluate(to_plan(plan), dim, n_src, src, n_tgt, tgt, str, mode, u, report, false);
+  });
+}
+
+int64_t sdmk_host_build_tables(int kernel, int dim, int window, double c, double sigma, double tol,
+                               unsigned char* buf, int64_t cap) {
+  int64_t len = -1;
+  guarded([&] {
+    // build_split_kernel (split.cpp:319-396) with build_prolate / build_gaussian (windows.cpp)
+    if (dim != 2 && dim != 3) throw InvalidArgument("build_split_kernel: dim must be 2 or 3");
+    if (window == kProlate && !(c > 0.0)) throw InvalidArgument("build_prolate: c must be positive");
+    if (window == kGaussian && !(sigma > 0.0)) throw InvalidArgument("build_gaussian: sigma must be positive");
+    if (window != kProlate && window != kGaussian) throw InvalidArgument("build_split_kernel: unknown window");
+    WindowFn w = window == kProlate ? make_prolate(c) : make_gaussian(sigma);
+    std::string img = serialize_tables(build_tables(kernel, dim, w, tol));
+    len = (int64_t)img.size();
+    if (buf && cap > 0) std::memcpy(buf, img.data(), (size_t)std::min<int64_t>(cap, len));
+  });
+  return len;
+}
+
+int sdmk_host_build_window(int window, double c, double sigma, double* scalars, double* coeffs, int cap) {
+  int n = -1;
+  guarded([&] {
+    if (window != kProlate && window != kGaussian) throw InvalidArgument("window: unknown kind");
+    WindowFn w = window == kProlate ? make_prolate(c) : make_gaussian(sigma);
+    if (scalars) {
+      scalars[0] = w.lambda0;
+      scalars[1] = w.norm_r;
+      scalars[2] = w.trunc_error;
+      scalars[3] = w.psi0;
+      scalars[4] = w.chi0;
+    }
+    n = (int)w.leg.size();
+    if (coeffs)
+      for (int i = 0; i < n && i < cap; ++i) coeffs[i] = w.leg[i];
+  });
+  return n;
+}
+
+int sdmk_host_window_eval(int window, double c, double sigma, const double* coeffs, int ncoef,
+                          const double* scalars, int what, int64_t n, const double* x, double* out) {
+  return guarded([&] {
+    WindowFn w;
+    w.kind = window;
+    w.c = c;
+    w.sigma = sigma;
+    if (coeffs) w.leg.assign(coeffs, coeffs + ncoef);
+    if (scalars) {
+      w.lambda0 = scalars[0];
+      w.norm_r = scalars[1];
+      w.trunc_error = scalars[2];
+      w.psi0 = scalars[3];
+      w.chi0 = scalars[4];
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      switch (what) {
+        case 0: out[i] = win_phi(w, x[i]); break;
+        case 1: out[i] = win_dphi(w, x[i]); break;
+        case 2: out[i] = win_hat(w, x[i]); break;
+        case 3: out[i] = win_tail(w, x[i]); break;
+        case 4: out[i] = moll_hat(w, x[i]); break;
+        default: throw InvalidArgument("window: unknown function");
+      }
+    }
+  });
+}
+
+int sdmk_direct_residual_sum_tables(sdmk_context* c, const unsigned char* tables, int64_t nbytes, int dim,
+                                    int64_t n_src, const double* src, int64_t n_tgt, const double* tgt,
+                                    const double* str, double cutoff, int periodic, double* u) {
+  return guarded([&] {
+    if (!tables || !src || !str || !u || (n_tgt > 0 && !tgt)) throw InvalidArgument("direct_residual_sum: null array");
+    Context* x = need_ctx(c);
+    const Tables& t = x->tables_image(tables, (size_t)nbytes);
+    x->direct(t.kernel, dim, n_src, src, n_tgt, tgt, str, &t, cutoff, periodic != 0, u, false);
+  });
 }
 
 int sdmk_direct_sum(sdmk_context* c, int kernel, int dim, int64_t n_src, const double* src, int64_t n_tgt,

@@ -320,6 +320,10 @@ void Context::load_tables(const std::string& path) {
   char key[256];
   double wpar = t.win.kind == kProlate ? t.win.c : t.win.sigma;
   std::snprintf(key, sizeof key, "%d/%d/%d/%.17g/%.17g", t.kernel, t.dim, t.win.kind, wpar, t.table_tol);
+  auto it = tables_.find(key);
+  if (it != tables_.end())  // replaced in place: drop the residual fits made from the old tables
+    for (auto c = pw_cache_.begin(); c != pw_cache_.end();)
+      c = c->first.first == &it->second ? pw_cache_.erase(c) : std::next(c);
   tables_[key] = t;
 }
 
@@ -473,10 +477,12 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
   int* flags = arena_.as<int>("flags", 8);
   cuda_check(cudaMemsetAsync(flags, 0, 8 * sizeof(int), st_), "memset");
   // validate_system (oracle.cpp:103-131) then wrap_into_box (oracle.cpp:133-141)
-  launch_validate(src, (int64_t)ns * d, pr.periodic, flags, 0, st_);
-  if (tgt) launch_validate(tgt, (int64_t)nt * d, pr.periodic, flags, 0, st_);
+  // (build_tree itself wraps nothing and accepts only points inside the box, tree.cpp:240-244)
+  const int range_free = pr.periodic && !tree_only_;
+  launch_validate(src, (int64_t)ns * d, range_free, flags, 0, st_);
+  if (tgt) launch_validate(tgt, (int64_t)nt * d, range_free, flags, 0, st_);
   if (!str_pending_) launch_validate(str, (int64_t)ns * pr.sc, 1, flags, 2, st_);
-  if (pr.periodic) {
+  if (pr.periodic && !tree_only_) {
     launch_wrap(src, (int64_t)ns * d, st_);
     if (tgt) launch_wrap(tgt, (int64_t)nt * d, st_);
   }
@@ -552,6 +558,7 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
     finish_strengths();
     check_strengths();
   }
+  if (tree_only_ && (hflags[0] || hflags[1])) throw InvalidArgument("build_tree: point outside the unit box");
   if (hflags[2]) throw InvalidArgument("ParticleSystem: non-finite strength");
   if (hflags[0]) throw InvalidArgument("ParticleSystem: non-finite coordinate");
   if (hflags[1]) throw InvalidArgument("ParticleSystem: coordinate outside the unit box");
@@ -1208,7 +1215,10 @@ void Context::run_downward() {  // dmk.cpp:705-857
       cudaEventRecord(e1, st_);
     }
     if (X.n_interp > 0) {
-      if (tensor_mma_supported(p, d))
+      if (accumulate_down_)  // children += interp(parent) (dmk.cpp:835-855 on caller-held incoming)
+        launch_tensor_apply(p, pz, d, mats_down_, X.interp_in, X.interp_out, X.interp_ci, X.n_interp, d, in, in, 1,
+                            st_);
+      else if (tensor_mma_supported(p, d))
         if (tensor_seg_supported(p, d))
           launch_tensor_mma_seg(p, mats_down_, X.interp_in, X.interp_out, X.interp_ci, X.interp_seg, X.n_interp_seg,
                                 d, in, in, st_);
@@ -1241,7 +1251,7 @@ void Context::run_target_far(double* ufar) {  // dmk.cpp:861-915
   if (mma_anterp_supported(p)) {
     // alias targets reuse the source bases computed by the upward pass
     const double* tb = nullptr;
-    if (pr.alias && !pr.halo) {  // (halo mode: this rank's source leaves are not its target leaves)
+    if (pr.alias && !pr.halo && !force_tbasis_) {  // (halo mode: this rank's source leaves are not its target leaves)
       tb = arena_.as<double>("basis_s", (size_t)3 * pr.ns * p);
     } else {
       double* b = arena_.as<double>("basis_t", (size_t)3 * pr.nt * p);
@@ -1272,34 +1282,58 @@ void Context::run_residual(double* ures, bool stats, int reserve_sms) {  // dmk.
   }
   if (cd && (cd->lo != co->lo || cd->hi != co->hi)) throw RuntimeError("residual tables on different intervals");
   // piecewise re-expansion of the radial tables (setup.hpp): the kernel reads
-  // deg + 1 coefficient pairs per pair evaluation, so it takes the finest
-  // interval grid whose degree fits its shared table, values within 1.5e-13 of
-  // max|table| (the reference's own fits are to 1e-14; the parity bar is 1e-10)
-  constexpr double kPwTol = 1.5e-13;
-  auto compiled = [](int dg) { return dg <= 5 ? 5 : (dg <= 6 ? 6 : (dg <= 8 ? 8 : (dg <= 10 ? 10 : 12))); };
-  PiecewisePoly po, pd;
-  for (int ni = 128; ni >= 8; ni /= 2) {
-    po = piecewise_from_cheb(*co, ni, 4, kPwTol);
-    int deg = po.deg;
-    if (cd) {
-      pd = piecewise_from_cheb(*cd, ni, 4, kPwTol);
-      deg = std::max(deg, pd.deg);
+  // deg + 1 coefficient pairs per pair evaluation.  Candidates in order of
+  // cost (degree), each on the finest interval grid its shared table holds;
+  // the first whose values stay within 2e-15 of the reference's Clenshaw
+  // values is taken (else the most accurate).  The bar is absolute because
+  // the residual kernels carry 1/r^2 .. 1/r^5 factors: an absolute table
+  // error at small s is amplified by close pairs (points on surfaces), and
+  // degree 5 on 128 intervals (1e-13 for the 3D stresslet) left 6e-9
+  // scaled differences at BASELINE cfg3; degree 6 is below 1e-15.
+  constexpr double kPwTol = 2e-15;
+  auto& cached = pw_cache_[{&T, pr.plan.kernel}];  // fitted once per table set and kernel
+  PiecewisePoly& po = cached.first;
+  PiecewisePoly& pd = cached.second;
+  if (po.c.empty()) {
+    PiecewisePoly best_o, best_d;
+    double best = 1e300;
+    for (int deg : {5, 6, 8, 10, 12}) {
+      const int ni = std::min(128, residual_max_pw() / (deg + 1));
+      po = piecewise_from_cheb(*co, ni, deg, 1.0);  // rel_tol 1: exactly this degree
+      double err = po.max_err;
+      if (cd) {
+        pd = piecewise_from_cheb(*cd, ni, deg, 1.0);
+        err = std::max(err, pd.max_err);
+      }
+      if (err < best) {
+        best = err;
+        best_o = po;
+        best_d = pd;
+      }
+      if (err <= kPwTol) break;
     }
-    deg = compiled(deg);
-    if (po.deg != deg) po = piecewise_from_cheb(*co, ni, deg, kPwTol);
-    if (cd && pd.deg != deg) pd = piecewise_from_cheb(*cd, ni, deg, kPwTol);
-    if (po.ni * (po.deg + 1) <= residual_max_pw() && po.deg <= 12 && (!cd || pd.deg == po.deg)) break;
+    po = best_o;
+    pd = best_d;
   }
-  if (po.deg > 12) throw RuntimeError("residual table re-expansion needs degree > 12");
   const int npw = po.ni * (po.deg + 1);
   if (npw > residual_max_pw()) throw RuntimeError("residual table re-expansion too large");
-  double* hc = (double*)pinned_.get("rtab", 2 * npw * sizeof(double));
+  const int nd = cd ? (int)cd->a.size() : 0, no = (int)co->a.size();
+  if (nd > kResidMaxCheb || no > kResidMaxCheb) throw RuntimeError("residual table longer than the GPU limit (80)");
+  const size_t nall = 2 * (size_t)npw + 2 * kResidMaxCheb;
+  double* hc = (double*)pinned_.get("rtab", nall * sizeof(double));
   std::copy(po.c.begin(), po.c.end(), hc + npw);
   if (cd) std::copy(pd.c.begin(), pd.c.end(), hc);
   else std::fill(hc, hc + npw, 0.0);
-  double* dc = arena_.as<double>("rtab", 2 * npw);
-  cuda_check(cudaMemcpyAsync(dc, hc, 2 * npw * sizeof(double), cudaMemcpyHostToDevice, st_), "table upload");
-  ResidTables rt{po.ni, po.deg, co->lo, co->hi, T.support, pr.plan.kernel, pr.dim, dc, dc + npw};
+  double* hcheb = hc + 2 * npw;
+  std::fill(hcheb, hcheb + 2 * kResidMaxCheb, 0.0);
+  if (cd) std::copy(cd->a.begin(), cd->a.end(), hcheb);
+  std::copy(co->a.begin(), co->a.end(), hcheb + kResidMaxCheb);
+  double* dc = arena_.as<double>("rtab", nall);
+  cuda_check(cudaMemcpyAsync(dc, hc, nall * sizeof(double), cudaMemcpyHostToDevice, st_), "table upload");
+  // the first piecewise interval takes the reference's own recurrence (see ResidTables)
+  const double s_exact = co->lo + (co->hi - co->lo) / po.ni;
+  ResidTables rt{po.ni, po.deg, co->lo, co->hi, T.support, pr.plan.kernel, pr.dim, dc, dc + npw,
+                 dc + 2 * npw, dc + 2 * npw + kResidMaxCheb, nd, no, s_exact};
   int* flags = arena_.as<int>("flags", 8);
   unsigned long long* st = arena_.as<unsigned long long>("stats", 4);
   if (stats) cuda_check(cudaMemsetAsync(st, 0, 4 * sizeof(unsigned long long), st_), "memset");
@@ -1341,7 +1375,7 @@ void Context::evaluate_begin(const Plan& P, int dim, int64_t ns, const double* s
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   begun_ = false;
   check_inputs(P, dim, ns, nt, mode);
-  tab_ = &tables_for(P);
+  tab_ = tab_override_ ? tab_override_ : &tables_for(P);
   if (tab_->kernel != P.kernel || tab_->dim != P.dim || tab_->win.kind != P.window)
     throw InvalidArgument("evaluate: supplied split tables do not match the plan");
   launches_ = 0;
@@ -1534,6 +1568,7 @@ static void need(const Problem& p) {
 }
 
 void Context::upward(double* out) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   need(prob_);
   run_upward();
   const int p = prob_.plan.p, pz = prob_.dim == 3 ? p : 1;
@@ -1544,6 +1579,7 @@ void Context::upward(double* out) {
 }
 
 void Context::incoming(int stage, double* out) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   need(prob_);
   run_upward();
   run_root();
@@ -1556,6 +1592,7 @@ void Context::incoming(int stage, double* out) {
 }
 
 void Context::target_far(double* out) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   need(prob_);
   run_upward();
   run_root();
@@ -1567,6 +1604,7 @@ void Context::target_far(double* out) {
 }
 
 void Context::residual(double* out) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   need(prob_);
   int* flags = arena_.as<int>("flags", 8);
   cuda_check(cudaMemsetAsync(flags, 0, 8 * sizeof(int), st_), "memset");
@@ -1617,6 +1655,7 @@ void Context::direct(int kernel, int dim, int64_t ns, const double* src, int64_t
   int* hflags = (int*)pinned_.get("hflags", 64);
   cuda_check(cudaMemcpyAsync(hflags, flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H flags");
   sync();
+  if (tree_only_ && (hflags[0] || hflags[1])) throw InvalidArgument("build_tree: point outside the unit box");
   if (hflags[2]) throw InvalidArgument("ParticleSystem: non-finite strength");
   if (hflags[0]) throw InvalidArgument("ParticleSystem: non-finite coordinate");
   if (hflags[1]) throw InvalidArgument("ParticleSystem: coordinate outside the unit box");
@@ -1657,6 +1696,247 @@ void Context::direct(int kernel, int dim, int64_t ns, const double* src, int64_t
   sync();
   cuda_check(cudaGetLastError(), "kernel launch");
   if (hflags[0]) throw DomainError(std::string(who) + ": coincident points");
+}
+
+// ---------------------------------------------- tree-first pass-level API --
+// The reference's build_tree / upward_pass / root_far_field / downward_pass /
+// target_far_fields / residual_pass (tree.hpp:90-92, dmk.hpp:84-131) with
+// every input and output a caller-held host array, so the C++ drop-in can
+// hand ProxyData between passes exactly as the reference's callers do.
+void Context::tree_build(int dim, bool periodic, int n_s, int p, int64_t ns, const double* src, int64_t nt,
+                         const double* tgt) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  prob_.ready = false;
+  begun_ = false;
+  halo_run_ = false;
+  // tree.cpp:233-244, in the reference's order
+  if (dim != 2 && dim != 3) throw InvalidArgument("build_tree: dim must be 2 or 3");
+  if (n_s < 1) throw InvalidArgument("build_tree: n_s must be >= 1");
+  if (p < 1) throw InvalidArgument("build_tree: proxy order must be >= 1");
+  if (ns < 1 || nt < 0) throw InvalidArgument("build_tree: bad point array length");
+  if (ns > (int64_t(1) << 31) - 1 || nt > (int64_t(1) << 31) - 1)
+    throw InvalidArgument("build_tree: more than 2^31-1 points");
+  if (p > (dim == 3 ? 48 : 64)) throw InvalidArgument("build_tree: proxy order above the GPU path limit (48 in 3D, 64 in 2D)");
+  Plan P;  // the tree depends on dim, periodic, n_s and p only; passes bind their own plan
+  P.kernel = kStokeslet;
+  P.dim = dim;
+  P.n_s = n_s;
+  P.p = p;
+  P.c = 1.0;
+  P.N1 = P.N_per = 1;
+  cuda_check(cudaMemcpyAsync(arena_.as<double>("src_in", (size_t)ns * dim), src, sizeof(double) * ns * dim,
+                             cudaMemcpyHostToDevice, st_),
+             "copy sources");
+  if (nt > 0)
+    cuda_check(cudaMemcpyAsync(arena_.as<double>("tgt_in", (size_t)nt * dim), tgt, sizeof(double) * nt * dim,
+                               cudaMemcpyHostToDevice, st_),
+               "copy targets");
+  cuda_check(cudaMemsetAsync(arena_.as<double>("str_in", (size_t)ns * dim), 0, sizeof(double) * ns * dim, st_),
+             "memset strengths");
+  str_pending_ = false;
+  tree_only_ = true;
+  struct Reset {
+    bool& f;
+    ~Reset() { f = false; }
+  } reset{tree_only_};
+  build_problem(P, dim, (int)ns, (int)nt, periodic ? 1 : 0);
+}
+
+void Context::tree_neighbors(int64_t* counts, int32_t* entries) {
+  need(prob_);
+  HostTree& t = prob_.tree;
+  finish_topology(t, true);
+  size_t at = 0;
+  for (int b = 0; b < t.num_boxes(); ++b) {
+    const NbrSpan lists[3] = {t.col[b], t.crs[b], t.fin[b]};
+    for (int k = 0; k < 3; ++k) {
+      counts[3 * (size_t)b + k] = lists[k].size();
+      if (entries)
+        for (const Nbr& e : lists[k]) {
+          int32_t* o = entries + 4 * at++;
+          o[0] = e.box;
+          o[1] = e.shift[0];
+          o[2] = e.shift[1];
+          o[3] = e.shift[2];
+        }
+    }
+  }
+}
+
+void Context::tree_sorted(double* src_pts, double* tgt_pts, int32_t* src_q, int32_t* tgt_q) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  need(prob_);
+  const Problem& pr = prob_;
+  const int d = pr.dim;
+  // device copies are SoA (axis-major); the reference's are point-major
+  auto fetch = [&](const double* dp, const int32_t* dq, int n, double* hp, int32_t* hq) {
+    std::vector<double> x((size_t)n * d);
+    std::vector<int32_t> q((size_t)n * d);
+    cuda_check(cudaMemcpyAsync(x.data(), dp, sizeof(double) * n * d, cudaMemcpyDeviceToHost, st_), "D2H points");
+    cuda_check(cudaMemcpyAsync(q.data(), dq, sizeof(int32_t) * n * d, cudaMemcpyDeviceToHost, st_), "D2H q");
+    sync();
+    for (int i = 0; i < n; ++i)
+      for (int a = 0; a < 3; ++a) {
+        if (hp && a < d) hp[(size_t)i * d + a] = x[(size_t)a * n + i];
+        if (hq) hq[(size_t)i * 3 + a] = a < d ? q[(size_t)a * n + i] : 0;
+      }
+  };
+  fetch(pr.spts, pr.sq, pr.ns, src_pts, src_q);
+  if (!pr.alias) fetch(pr.tpts, pr.tq, pr.nt, tgt_pts, tgt_q);
+}
+
+void Context::tree_perm(int32_t* src_perm, int32_t* tgt_perm) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  need(prob_);
+  const Problem& p = prob_;
+  // on the context stream: ordered after the (possibly re-sorting) tree build
+  cuda_check(cudaMemcpyAsync(src_perm, p.sperm, sizeof(int) * p.ns, cudaMemcpyDeviceToHost, st_), "D2H perm");
+  if (tgt_perm && !p.alias)
+    cuda_check(cudaMemcpyAsync(tgt_perm, p.tperm, sizeof(int) * p.nt, cudaMemcpyDeviceToHost, st_), "D2H perm");
+  sync();
+}
+
+// check_plan (dmk.cpp:534-539) plus what this pass needs of the plan
+void Context::bind_plan(const Plan& P, const Tables* tab, const char* who) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  need(prob_);
+  begun_ = false;
+  halo_run_ = false;
+  Problem& pr = prob_;
+  if (P.dim != pr.dim) throw InvalidArgument("dmk: tree and plan dimensions differ");
+  if (P.p != pr.tree.p) throw InvalidArgument("dmk: tree proxy order does not match plan");
+  if (P.kernel != kStokeslet && P.kernel != kStresslet && P.kernel != kRotlet)
+    throw InvalidArgument(std::string(who) + ": the Stokeslet, stresslet, and rotlet kernels only");
+  if (P.N1 < 1 || P.N1 > 127 || P.N_per < 1 || P.N_per > 127)
+    throw InvalidArgument(std::string(who) + ": Fourier grid size outside [1, 127]");
+  if (tab && (tab->kernel != P.kernel || tab->dim != P.dim))
+    throw InvalidArgument(std::string(who) + ": split tables do not match the plan's kernel and dimension");
+  const int n_s = pr.plan.n_s;
+  pr.plan = P;
+  pr.plan.n_s = n_s;  // the tree's capacity, as built
+  pr.nch = channels_out(P.kernel, pr.dim);
+  pr.sc = strength_width(P.kernel, pr.dim);
+  tab_ = tab ? tab : &tables_for(P);
+  zero_all_ = true;
+}
+
+void Context::load_strengths(int64_t nstr, const double* str, const char* who) {
+  Problem& pr = prob_;
+  if (nstr != (int64_t)pr.ns * pr.sc) throw InvalidArgument(std::string(who) + ": strength array size mismatch");
+  double* d = arena_.as<double>("str_in", (size_t)pr.ns * pr.sc);
+  cuda_check(cudaMemcpyAsync(d, str, sizeof(double) * nstr, cudaMemcpyHostToDevice, st_), "copy strengths");
+  pr.sstr = arena_.as<double>("sstr", (size_t)pr.ns * pr.sc);
+  launch_gather_strengths(d, pr.sperm, pr.ns, pr.sc, pr.sstr, st_);
+}
+
+static size_t proxy_count(const Problem& pr, int channels) {
+  const int p = pr.tree.p, pz = pr.dim == 3 ? p : 1;
+  return (size_t)pr.tree.num_boxes() * channels * pz * p * p;
+}
+
+void Context::pass_upward(const Plan& P, int64_t nstr, const double* str, double* out) {
+  bind_plan(P, nullptr, "upward_pass");
+  load_strengths(nstr, str, "upward_pass");
+  run_upward();
+  cuda_check(cudaMemcpyAsync(out, arena_.as<double>("outgoing", 1), proxy_count(prob_, prob_.nch) * sizeof(double),
+                             cudaMemcpyDeviceToHost, st_),
+             "D2H outgoing");
+  sync();
+}
+
+void Context::pass_root(const Plan& P, const Tables* tab, int64_t nog, const double* og, bool periodic, int64_t nin,
+                        double* in) {
+  bind_plan(P, tab, "root_far_field");
+  Problem& pr = prob_;
+  const size_t no = proxy_count(pr, pr.nch), ni = proxy_count(pr, pr.dim);
+  if ((size_t)nog != no) throw InvalidArgument("root_far_field: outgoing proxies do not match the tree and plan");
+  if ((size_t)nin != ni) throw InvalidArgument("root_far_field: incoming proxies do not match the tree and plan");
+  cuda_check(cudaMemcpyAsync(arena_.as<double>("outgoing", no), og, no * sizeof(double), cudaMemcpyHostToDevice, st_),
+             "H2D outgoing");
+  arena_.as<double>("incoming", ni);
+  const bool tree_periodic = pr.periodic;
+  pr.periodic = periodic;  // the lattice sum follows the argument (dmk.cpp:678-681)
+  struct Restore {
+    bool& f;
+    bool v;
+    ~Restore() { f = v; }
+  } restore{pr.periodic, tree_periodic};
+  zero_all_ = false;  // only box 0 is written and read back
+  run_root();
+  zero_all_ = true;
+  const size_t nb0 = ni / pr.tree.num_boxes();
+  std::vector<double> box0(nb0);
+  cuda_check(cudaMemcpyAsync(box0.data(), arena_.as<double>("incoming", 1), nb0 * sizeof(double),
+                             cudaMemcpyDeviceToHost, st_),
+             "D2H incoming");
+  sync();
+  for (size_t i = 0; i < nb0; ++i) in[i] += box0[i];  // inverse_grid_add into the caller's root box
+}
+
+void Context::pass_downward(const Plan& P, const Tables* tab, int64_t nog, const double* og, bool periodic,
+                            int64_t nin, double* in) {
+  (void)periodic;  // periodic images enter through the colleague shifts (dmk.cpp:708)
+  bind_plan(P, tab, "downward_pass");
+  Problem& pr = prob_;
+  const size_t no = proxy_count(pr, pr.nch), ni = proxy_count(pr, pr.dim);
+  if ((size_t)nog != no) throw InvalidArgument("downward_pass: outgoing proxies do not match the tree and plan");
+  if ((size_t)nin != ni) throw InvalidArgument("downward_pass: incoming proxies do not match the tree and plan");
+  cuda_check(cudaMemcpyAsync(arena_.as<double>("outgoing", no), og, no * sizeof(double), cudaMemcpyHostToDevice, st_),
+             "H2D outgoing");
+  double* din = arena_.as<double>("incoming", ni);
+  cuda_check(cudaMemcpyAsync(din, in, ni * sizeof(double), cudaMemcpyHostToDevice, st_), "H2D incoming");
+  accumulate_down_ = true;
+  struct Reset {
+    bool& f;
+    ~Reset() { f = false; }
+  } reset{accumulate_down_};
+  run_downward();
+  cuda_check(cudaMemcpyAsync(in, din, ni * sizeof(double), cudaMemcpyDeviceToHost, st_), "D2H incoming");
+  sync();
+}
+
+void Context::pass_target_far(const Plan& P, int64_t nin, const double* in, double* u) {
+  bind_plan(P, nullptr, "target_far_fields");
+  Problem& pr = prob_;
+  const size_t ni = proxy_count(pr, pr.dim);
+  if ((size_t)nin != ni) throw InvalidArgument("target_far_fields: incoming proxies do not match the tree and plan");
+  cuda_check(cudaMemcpyAsync(arena_.as<double>("incoming", ni), in, ni * sizeof(double), cudaMemcpyHostToDevice, st_),
+             "H2D incoming");
+  double* uf = arena_.as<double>("ufar", (size_t)pr.nt * pr.dim);
+  force_tbasis_ = true;
+  struct Reset {
+    bool& f;
+    ~Reset() { f = false; }
+  } reset{force_tbasis_};
+  run_target_far(uf);
+  cuda_check(cudaMemcpyAsync(u, uf, sizeof(double) * pr.nt * pr.dim, cudaMemcpyDeviceToHost, st_), "D2H u");
+  sync();
+  cuda_check(cudaGetLastError(), "kernel launch");
+}
+
+void Context::pass_residual(const Plan& P, const Tables* tab, int64_t nstr, const double* str, bool periodic,
+                            double* u) {
+  (void)periodic;  // images enter through the neighbour shifts (dmk.cpp:923)
+  bind_plan(P, tab, "residual_pass");
+  load_strengths(nstr, str, "residual_pass");
+  Problem& pr = prob_;
+  int* flags = arena_.as<int>("flags", 8);
+  cuda_check(cudaMemsetAsync(flags, 0, 8 * sizeof(int), st_), "memset");
+  double* ur = arena_.as<double>("ures", (size_t)pr.nt * pr.dim);
+  run_residual(ur, false);
+  int* hflags = (int*)pinned_.get("hflags", 64);
+  cuda_check(cudaMemcpyAsync(u, ur, sizeof(double) * pr.nt * pr.dim, cudaMemcpyDeviceToHost, st_), "D2H u");
+  cuda_check(cudaMemcpyAsync(hflags, flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H flags");
+  sync();
+  cuda_check(cudaGetLastError(), "kernel launch");
+  if (hflags[3]) throw DomainError("residual_pass: coincident points");
+}
+
+const Tables& Context::tables_image(const void* bytes, size_t n) {
+  std::string key(static_cast<const char*>(bytes), n);
+  auto it = image_tables_.find(key);
+  if (it == image_tables_.end()) it = image_tables_.emplace(key, parse_tables(bytes, n)).first;
+  return it->second;
 }
 
 }  // namespace sdmkb

@@ -152,6 +152,30 @@ class Context {
   void target_far(double* host_out);
   void residual(double* host_out);
 
+  // ---- the reference's pass-level API, tree first (tree.hpp:90-104,
+  // dmk.hpp:84-131): build_tree, then each pass with its own plan, tables,
+  // strengths and proxies passed in and out as host arrays ----
+  void tree_build(int dim, bool periodic, int n_s, int p, int64_t ns, const double* src, int64_t nt,
+                  const double* tgt);
+  // counts[3 b + k] = entries of list k (colleague / coarse / fine) of box b;
+  // entries (may be null) = 4 int32 per entry (box, shift0..2), box-major
+  void tree_neighbors(int64_t* counts, int32_t* entries);
+  // permuted point copies (point-major) and quantized coordinates (3 per point)
+  void tree_sorted(double* src_pts, double* tgt_pts, int32_t* src_q, int32_t* tgt_q);
+  void tree_perm(int32_t* src_perm, int32_t* tgt_perm);
+  void pass_upward(const Plan& P, int64_t nstr, const double* str, double* outgoing);
+  void pass_root(const Plan& P, const Tables* tab, int64_t nog, const double* og, bool periodic, int64_t nin,
+                 double* in);
+  void pass_downward(const Plan& P, const Tables* tab, int64_t nog, const double* og, bool periodic, int64_t nin,
+                     double* in);
+  void pass_target_far(const Plan& P, int64_t nin, const double* in, double* u);
+  void pass_residual(const Plan& P, const Tables* tab, int64_t nstr, const double* str, bool periodic, double* u);
+  // tables from an SDMKSPLT v1 memory image (cached by content)
+  const Tables& tables_image(const void* bytes, size_t n);
+  // tables an evaluation uses instead of the plan's (the reference's
+  // evaluate_with_plan(..., tables)); null restores the plan's
+  void set_tables_override(const Tables* t) { tab_override_ = t; }
+
   // O(N*M) reference sums on the GPU: direct_sum (tab == nullptr; exact
   // kernels) and direct_residual_sum (residual kernel of `tab` at scale
   // cutoff, periodic images), oracle.cpp:143-241.  Inputs are the caller's
@@ -161,6 +185,8 @@ class Context {
 
  private:
   void check_inputs(const Plan& plan, int dim, int64_t ns, int64_t nt, int mode);
+  void bind_plan(const Plan& P, const Tables* tab, const char* who);
+  void load_strengths(int64_t nstr, const double* str, const char* who);
   // inputs already in the arena ("src_in", "tgt_in", "str_in"): validate, wrap, sort, topology, upload
   void build_problem(const Plan& plan, int dim, int ns, int nt, int mode, bool defer_lists = false);
   void upload_tree_lists_a();
@@ -210,6 +236,12 @@ class Context {
     bool alias = true, device_ptrs = false;
   } call_;
   bool zero_all_ = true;  // zero whole proxy arrays (pass-level API returns them)
+  bool tree_only_ = false;     // build_problem for build_tree: no wrap, build_tree's checks
+  bool accumulate_down_ = false;  // downward interpolation adds to the children (pass-level API)
+  bool force_tbasis_ = false;  // target bases recomputed (the upward pass may not have run)
+  const Tables* tab_override_ = nullptr;
+  std::map<std::string, Tables> image_tables_;
+  std::map<std::pair<const Tables*, int>, std::pair<PiecewisePoly, PiecewisePoly>> pw_cache_;
   const int32_t* hq_ = nullptr;  // pinned sorted quantized coordinates of the current problem
   unsigned long long stats_[3] = {0, 0, 0};
 };

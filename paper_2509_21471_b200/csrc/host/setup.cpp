@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstring>
 #include <fstream>
+#include <iterator>
 #include <functional>
 
 namespace sdmkb {
@@ -845,19 +846,27 @@ double self_scaled(const Tables& t, double nu) {  // split.cpp:116-127
 // export/import (split.cpp:402-506).
 namespace {
 template <class T>
-void wr(std::ofstream& o, T v) { o.write(reinterpret_cast<const char*>(&v), sizeof(T)); }
-template <class T>
-T rd(std::ifstream& i) {
-  T v{};
-  i.read(reinterpret_cast<char*>(&v), sizeof(T));
-  return v;
-}
+void wr(std::string& o, T v) { o.append(reinterpret_cast<const char*>(&v), sizeof(T)); }
+struct Reader {
+  const char* p;
+  size_t n, at = 0;
+  bool ok = true;
+  template <class T>
+  T rd() {
+    T v{};
+    if (at + sizeof(T) > n) {
+      ok = false;
+      return v;
+    }
+    std::memcpy(&v, p + at, sizeof(T));
+    at += sizeof(T);
+    return v;
+  }
+};
 }  // namespace
 
-void save_tables(const Tables& t, const std::string& path) {
-  std::ofstream o(path, std::ios::binary);
-  if (!o) throw RuntimeError("export_split_kernel: cannot open " + path);
-  o.write("SDMKSPLT", 8);
+std::string serialize_tables(const Tables& t) {
+  std::string o("SDMKSPLT", 8);
   wr<uint32_t>(o, 1);
   wr<int32_t>(o, t.kernel);
   wr<int32_t>(o, t.dim);
@@ -875,35 +884,52 @@ void save_tables(const Tables& t, const std::string& path) {
     wr<uint32_t>(o, (uint32_t)c->a.size());
     for (double v : c->a) wr<double>(o, v);
   }
+  return o;
+}
+
+Tables parse_tables(const void* bytes, size_t n, const std::string& what) {
+  Reader r{static_cast<const char*>(bytes), n};
+  if (n < 8 || std::memcmp(bytes, "SDMKSPLT", 8) != 0) throw RuntimeError("import_split_kernel: bad magic in " + what);
+  r.at = 8;
+  if (r.rd<uint32_t>() != 1) throw RuntimeError("import_split_kernel: unsupported version");
+  Tables t;
+  t.kernel = r.rd<int32_t>();
+  t.dim = r.rd<int32_t>();
+  t.win.kind = r.rd<int32_t>();
+  t.win.c = r.rd<double>();
+  t.win.sigma = r.rd<double>();
+  const uint32_t nl = r.rd<uint32_t>();
+  if (!r.ok || nl > n / 8) throw RuntimeError("import_split_kernel: truncated file " + what);
+  t.win.leg.resize(nl);
+  for (double& v : t.win.leg) v = r.rd<double>();
+  double* scal[] = {&t.win.lambda0, &t.win.norm_r, &t.win.trunc_error, &t.win.psi0, &t.win.chi0, &t.R,
+                    &t.support, &t.table_tol, &t.self_const, &t.corr_const};
+  for (double* s : scal) *s = r.rd<double>();
+  for (Cheb* c : {&t.s_diag, &t.s_offd, &t.t_diag, &t.t_offd, &t.w_offd, &t.b_res, &t.phi}) {
+    c->lo = r.rd<double>();
+    c->hi = r.rd<double>();
+    const uint32_t m = r.rd<uint32_t>();
+    if (!r.ok || m > n / 8) throw RuntimeError("import_split_kernel: truncated file " + what);
+    c->a.resize(m);
+    for (double& v : c->a) v = r.rd<double>();
+  }
+  if (!r.ok) throw RuntimeError("import_split_kernel: truncated file " + what);
+  return t;
+}
+
+void save_tables(const Tables& t, const std::string& path) {
+  std::ofstream o(path, std::ios::binary);
+  if (!o) throw RuntimeError("export_split_kernel: cannot open " + path);
+  const std::string b = serialize_tables(t);
+  o.write(b.data(), (std::streamsize)b.size());
   if (!o) throw RuntimeError("export_split_kernel: write failed for " + path);
 }
 
 Tables load_tables(const std::string& path) {
   std::ifstream i(path, std::ios::binary);
   if (!i) throw RuntimeError("import_split_kernel: cannot open " + path);
-  char mg[8];
-  i.read(mg, 8);
-  if (!i || std::memcmp(mg, "SDMKSPLT", 8) != 0) throw RuntimeError("import_split_kernel: bad magic in " + path);
-  if (rd<uint32_t>(i) != 1) throw RuntimeError("import_split_kernel: unsupported version");
-  Tables t;
-  t.kernel = rd<int32_t>(i);
-  t.dim = rd<int32_t>(i);
-  t.win.kind = rd<int32_t>(i);
-  t.win.c = rd<double>(i);
-  t.win.sigma = rd<double>(i);
-  t.win.leg.resize(rd<uint32_t>(i));
-  for (double& v : t.win.leg) v = rd<double>(i);
-  double* scal[] = {&t.win.lambda0, &t.win.norm_r, &t.win.trunc_error, &t.win.psi0, &t.win.chi0, &t.R,
-                    &t.support, &t.table_tol, &t.self_const, &t.corr_const};
-  for (double* s : scal) *s = rd<double>(i);
-  for (Cheb* c : {&t.s_diag, &t.s_offd, &t.t_diag, &t.t_offd, &t.w_offd, &t.b_res, &t.phi}) {
-    c->lo = rd<double>(i);
-    c->hi = rd<double>(i);
-    c->a.resize(rd<uint32_t>(i));
-    for (double& v : c->a) v = rd<double>(i);
-  }
-  if (!i) throw RuntimeError("import_split_kernel: truncated file " + path);
-  return t;
+  std::string b((std::istreambuf_iterator<char>(i)), std::istreambuf_iterator<char>());
+  return parse_tables(b.data(), b.size(), path);
 }
 
 // ------------------------------------------------------ symbol tables ----

@@ -106,6 +106,9 @@ Tables build_tables(int kernel, int dim, const WindowFn& win, double tol);
 Tables tables_for_plan(const Plan& plan);
 void save_tables(const Tables& t, const std::string& path);  // SDMKSPLT v1
 Tables load_tables(const std::string& path);
+// the same format in memory (the C++ drop-in's SplitKernel travels as it)
+std::string serialize_tables(const Tables& t);
+Tables parse_tables(const void* bytes, size_t n, const std::string& what = "memory image");
 double self_scaled(const Tables& t, double nu);
 
 enum SymbolKind { kLevelDiff = 0, kRootFree = 1, kRootPeriodic = 2 };

@@ -158,7 +158,16 @@ struct ResidTables {
   int kernel, dim;
   const double* pw_d;  // diag table (unused for the rotlet)
   const double* pw_o;  // offd table
+  // the reference's Chebyshev tables themselves (chebyshev.hpp ChebTable),
+  // evaluated by its Clenshaw recurrence, unfused, for s < s_exact: near
+  // s = 0 the residual kernels multiply table values by up to 1/r^3, so
+  // there the values must match the reference's to its own rounding (~1e-17)
+  const double* cheb_d;  // n_d coefficients (n_d = 0 for the rotlet)
+  const double* cheb_o;
+  int n_d, n_o;
+  double s_exact;
 };
+constexpr int kResidMaxCheb = 80;  // longest Chebyshev table the exact branch holds in shared memory
 int residual_max_pw();
 // u_res[perm[t]*d+j] for all targets of leaves `leaves`; flags[0] <- coincident
 // points; stats[0..1] <- candidates / in-support pairs (if stats != nullptr)

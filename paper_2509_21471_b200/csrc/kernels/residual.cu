@@ -23,6 +23,7 @@
 #include "launch.hpp"
 
 #include <algorithm>
+#include <type_traits>
 
 namespace sdmkb {
 
@@ -31,18 +32,18 @@ namespace {
 using dev::DBox;
 
 // One 16-warp CTA per SM (persistent): the SM's single copy of the radial
-// table can then hold 128 intervals at degree 5 -- 6 coefficient loads per
-// pair instead of 9 at 32 intervals x degree 8.
+// table can then hold 128 intervals at degree 6 -- 7 coefficient loads per
+// pair, values within 1e-15 of the reference's Clenshaw tables.
 constexpr int kRBlock = 512;
 constexpr int kWarps = kRBlock / 32;
 #ifndef SDMK_RES_LIST
-#define SDMK_RES_LIST 48
+#define SDMK_RES_LIST 40
 #endif
 constexpr int kList = SDMK_RES_LIST;  // per-lane list capacity (entries): longer lists, less lockstep padding
 constexpr int kMaxRanges = 160;
 constexpr int kMaxIvl = kMaxRanges * 8;  // source intervals per chunk: ranges x Morton sub-cells
 constexpr int kResBlocksPerSM = 1;       // persistent grid (registers and shared memory: 1 per SM)
-constexpr int kMaxPW = 768;      // ni * (deg + 1) <= 768 (d, o) coefficient pairs (8 copies: 96 KB)
+constexpr int kMaxPW = 896;      // ni * (deg + 1) <= 896 (d, o) coefficient pairs (8 copies: 112 KB)
 constexpr int kCopies = 8;       // table copies, one per 16-byte bank group
 #ifndef SDMK_RES_ILP
 #define SDMK_RES_ILP 2
@@ -97,9 +98,40 @@ struct RangeS {
 // interleaved, copy c in 16-byte bank group c: lane L reads copy L % 8, so
 // the 8 lanes of a 128-bit load phase always hit 8 distinct bank groups
 // whatever intervals they need (no conflicts).
-template <int KERNEL, int DEG>
+// The reference's Clenshaw (chebyshev.cpp:9-19) in its own operation order,
+// every product and sum rounded separately (the reference is built without
+// FMA contraction).
+__device__ __forceinline__ double clenshaw_ref1(const double* __restrict__ c, int n, double lo, double hi, double x) {
+  if (n == 0) return 0.0;
+  const double t = __ddiv_rn(__dsub_rn(__dsub_rn(__dmul_rn(2.0, x), lo), hi), __dsub_rn(hi, lo));
+  const double t2 = __dmul_rn(2.0, t);
+  double b1 = 0.0, b2 = 0.0;
+  for (int k = n - 1; k >= 1; --k) {
+    const double b0 = __dadd_rn(__dsub_rn(__dmul_rn(t2, b1), b2), c[k]);
+    b2 = b1;
+    b1 = b0;
+  }
+  return __dadd_rn(__dsub_rn(__dmul_rn(t, b1), b2), c[0]);
+}
+
+__device__ __forceinline__ double2 clenshaw_ref(const double* __restrict__ cheb, int nd, int no, double lo, double hi,
+                                             double r2, double inu) {
+  const double se = __dmul_rn(__dsqrt_rn(r2), inu);  // s = sqrt(r2) / nu as the reference forms it
+  return make_double2(clenshaw_ref1(cheb, nd, lo, hi, se), clenshaw_ref1(cheb + kResidMaxCheb, no, lo, hi, se));
+}
+
+// EXACT: the reference's tables and recurrence (pairs with s < s_exact, rare;
+// re-evaluated after the fast pass so the hot path keeps its registers)
+template <int KERNEL, int DEG, bool EXACT>
 __device__ __forceinline__ void radial_tables(const ResidTables& rt, const double2* __restrict__ pw, double yscale,
-                                              double s, double& fd, double& fo) {
+                                              double s, double& fd, double& fo, const double* __restrict__ cheb,
+                                              double r2, double inu) {
+  if (EXACT) {
+    const double2 v = clenshaw_ref(cheb, KERNEL != 2 ? rt.n_d : 0, rt.n_o, rt.lo, rt.hi, r2, inu);
+    fd = v.x;
+    fo = v.y;
+    return;
+  }
   const bool in = s < rt.support;
   const double y = (s - rt.lo) * yscale;
   int iv = (int)y;
@@ -186,13 +218,18 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
   extern __shared__ __align__(16) double2 dyn2[];  // [npw][kCopies] table, then the lists
   double2* s_pw = dyn2;
   const int npw = rt.ni * (rt.deg + 1);
-  int* dyn = reinterpret_cast<int*>(dyn2 + npw * kCopies);  // lane-interleaved lists: [kWarps][kList][32] ints then bytes
+  double* s_cheb = reinterpret_cast<double*>(dyn2 + npw * kCopies);  // [2][kResidMaxCheb] reference tables
+  int* dyn = reinterpret_cast<int*>(s_cheb + 2 * kResidMaxCheb);  // lane-interleaved lists: [kWarps][kList][32] ints then bytes
   int (*lsrc)[kList][32] = reinterpret_cast<int (*)[kList][32]>(dyn);
   unsigned char (*lrng)[kList][32] = reinterpret_cast<unsigned char (*)[kList][32]>(dyn + kWarps * kList * 32);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int e = tid; e < npw * kCopies; e += blockDim.x) {
     const int k = e / kCopies;
     s_pw[e] = make_double2(KERNEL != 2 ? rt.pw_d[k] : 0.0, rt.pw_o[k]);
+  }
+  for (int e = tid; e < 2 * kResidMaxCheb; e += blockDim.x) {
+    const int k = e % kResidMaxCheb;
+    s_cheb[e] = e < kResidMaxCheb ? (k < rt.n_d ? rt.cheb_d[k] : 0.0) : (k < rt.n_o ? rt.cheb_o[k] : 0.0);
   }
   __syncthreads();
   int4* __restrict__ ivl = ivl_all + (size_t)(blockIdx.x * kWarps + warp) * kMaxIvl;  // this warp's interval list
@@ -312,7 +349,16 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       nivl += __shfl_sync(0xffffffffu, pre, 31);
     }
     __syncwarp();
-    double u[3] = {0.0, 0.0, 0.0};
+    // Kahan accumulation per component, as the reference's (dmk.cpp:540-548,
+    // 994-1020): only in-support pairs are added (adding 0 would fold the
+    // compensation early), in the reference's order
+    double u[3] = {0.0, 0.0, 0.0}, uc[3] = {0.0, 0.0, 0.0};
+    auto kahan = [&](int j, double v) {
+      const double y = v - uc[j];
+      const double tt = u[j] + y;
+      uc[j] = (tt - u[j]) - y;
+      u[j] = tt;
+    };
     int cnt = 0;
     const double sup2l = (r_l * rt.support) * (r_l * rt.support);
     const double sup2f = (r_f * rt.support) * (r_f * rt.support);
@@ -320,13 +366,10 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       int mx = cnt;
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-#ifdef SDMK_RES_NOEVAL  // profiling: the scan alone
-      if (mx > 0) u[0] += (double)lsrc[warp][mx - 1][lane];
-      mx = 0;
-#endif
       // kILP list entries per step: independent dependency chains interleave,
       // and their contributions are added in list order
-      auto eval = [&](int i, double* c) {
+      auto eval = [&](int i, double* c, bool& near, auto exact) {
+        constexpr bool EXACT = decltype(exact)::value;
         const int a = lsrc[warp][i][lane];
         const int code = lrng[warp][i][lane];  // image shift (x+1 | y+1 << 2 | z+1 << 4) | fine << 6
         const bool fine = code & 64;
@@ -360,27 +403,44 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         const double rinv = rsqrt_nr(r2);
         const double s = (r2 * rinv) * inu;  // nu is a power of two: r * (1/nu) == r / nu
         double fd, fo;
-        radial_tables<KERNEL, DEG>(rt, s_pw + (lane & (kCopies - 1)), yscale, s, fd, fo);
+        radial_tables<KERNEL, DEG, EXACT>(rt, s_pw + (lane & (kCopies - 1)), yscale, s, fd, fo, s_cheb, r2, inu);
         assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, nu, rv + DIM, c);
         const bool keep = in && r2 != 0.0;
+        near = s < rt.s_exact;
 #pragma unroll
         for (int j = 0; j < DIM; ++j) c[j] = keep ? c[j] : 0.0;
         return keep;
       };
       for (int i = 0; i < mx; i += kILP) {  // all evaluations unconditional (clamped), straight-line
         double c[kILP][3];
+        bool kp[kILP];
 #pragma unroll
-        for (int q = 0; q < kILP; ++q) c[q][0] = c[q][1] = c[q][2] = 0.0;
+        for (int q = 0; q < kILP; ++q) {
+          c[q][0] = c[q][1] = c[q][2] = 0.0;
+          kp[q] = false;
+        }
+        bool nr[kILP];
         if (cnt > 0) {
 #pragma unroll
-          for (int q = 0; q < kILP; ++q)
-            if (eval(min(i + q, cnt - 1), c[q]) && i + q < cnt) ++n_in;
+          for (int q = 0; q < kILP; ++q) {
+            kp[q] = eval(min(i + q, cnt - 1), c[q], nr[q], std::false_type{}) && i + q < cnt;
+            if (kp[q]) ++n_in;
+          }
+          bool any_near = false;
+#pragma unroll
+          for (int q = 0; q < kILP; ++q) any_near |= kp[q] && nr[q];
+          if (__any_sync(0xffffffffu, any_near)) {
+#pragma unroll
+            for (int q = 0; q < kILP; ++q)
+              if (kp[q] && nr[q]) eval(i + q, c[q], nr[q], std::true_type{});
+          }
         }
 #pragma unroll
-        for (int j = 0; j < DIM; ++j)
+        for (int q = 0; q < kILP; ++q)
+          if (kp[q]) {
 #pragma unroll
-          for (int q = 0; q < kILP; ++q)
-            if (i + q < cnt) u[j] += c[q][j];
+            for (int j = 0; j < DIM; ++j) kahan(j, c[q][j]);
+          }
       }
       cnt = 0;
     };
@@ -423,7 +483,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           for (int k = 0; k < RW / 2; ++k) rb[lane * (RW / 2) + k] = rp[k];
         }
         __syncwarp();
-        auto dense = [&](int j, double* c) {
+        auto dense = [&](int j, double* c, bool& near, auto exact) {
+          constexpr bool EXACT = decltype(exact)::value;
           double sv[RW];
 #pragma unroll
           for (int k = 0; k < RW / 2; ++k) {
@@ -443,22 +504,31 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           const double rinv = rsqrt_nr(r2);
           const double sc = (r2 * rinv) * inv_rl;
           double fd, fo;
-          radial_tables<KERNEL, DEG>(rt, s_pw + (lane & (kCopies - 1)), yscale, sc, fd, fo);
+          radial_tables<KERNEL, DEG, EXACT>(rt, s_pw + (lane & (kCopies - 1)), yscale, sc, fd, fo, s_cheb, r2,
+                                            inv_rl);
           assemble<KERNEL, DIM>(fd, fo, x, rinv, sc, rt.support, r_l, sv + DIM, c);
           const bool keep = in && r2 != 0.0;
+          near = sc < rt.s_exact;
 #pragma unroll
           for (int k = 0; k < DIM; ++k) c[k] = keep ? c[k] : 0.0;
           return keep;
         };
         for (int j = 0; j < nv; j += 2) {
           double c0[3] = {0.0, 0.0, 0.0}, c1[3] = {0.0, 0.0, 0.0};
-          const bool k0 = dense(j, c0);
-          const bool k1 = dense(min(j + 1, nv - 1), c1) && j + 1 < nv;
+          bool n0, n1;
+          const bool k0 = dense(j, c0, n0, std::false_type{});
+          const bool k1 = dense(min(j + 1, nv - 1), c1, n1, std::false_type{}) && j + 1 < nv;
+          if (__any_sync(0xffffffffu, (k0 && n0) || (k1 && n1))) {
+            if (k0 && n0) dense(j, c0, n0, std::true_type{});
+            if (k1 && n1) dense(j + 1, c1, n1, std::true_type{});
+          }
+          if (k0) {
 #pragma unroll
-          for (int k = 0; k < DIM; ++k) u[k] += c0[k];
-          if (j + 1 < nv) {
+            for (int k = 0; k < DIM; ++k) kahan(k, c0[k]);
+          }
+          if (k1) {
 #pragma unroll
-            for (int k = 0; k < DIM; ++k) u[k] += c1[k];
+            for (int k = 0; k < DIM; ++k) kahan(k, c1[k]);
           }
           n_in += (k0 ? 1 : 0) + (k1 ? 1 : 0);
         }
@@ -537,9 +607,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       double* ut = ures + (size_t)tperm[t] * DIM;
 #pragma unroll
       for (int j = 0; j < DIM; ++j) {
-        double v = u[j];
-        if (selfc != 0.0) v += selfc * sstr[(size_t)j * ns + t];
-        ut[j] = v;
+        if (selfc != 0.0) kahan(j, selfc * sstr[(size_t)j * ns + t]);  // dmk.cpp:1015-1018
+        ut[j] = u[j];
       }
     }
     __syncwarp();  // the interval list is rewritten by the next chunk
@@ -594,7 +663,7 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
   cudaMemsetAsync(next_chunk, 0, sizeof(int), st);
   const int2* ch2 = reinterpret_cast<const int2*>(chunks);
   const size_t dsm = (size_t)kWarps * kList * 32 * (sizeof(int) + 1) +
-                     sizeof(double) * 2 * kCopies * (size_t)rt.ni * (rt.deg + 1);
+                     sizeof(double) * 2 * kCopies * (size_t)rt.ni * (rt.deg + 1) + sizeof(double) * 2 * kResidMaxCheb;
 #define RES(K, D)                                                                                                \
   do {                                                                                                           \
     if (rt.deg == 5) RES1(K, D, 5);                                                                              \

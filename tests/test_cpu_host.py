@@ -117,3 +117,49 @@ def test_host_topology_degenerate_inputs():
         sp = R.morton_order(q)
         T = R.build_tree(pts, None, 1, 3, False, 5)
         assert g.host_topology_dump(3, False, 1, 5, q[sp]) == R.dump_tree(T)
+
+
+def test_cxx_dropin_pass_program_links():
+    """tests/dropin_passes.cpp (the pass-level drop-in program the GPU tests run)
+    compiles against the header and links with libsdmk_b200.so."""
+    lib_dir = os.path.join(ROOT, "paper_2509_21471_b200")
+    r = subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "dropin_passes.cpp"), "-o", "/tmp/_sdmk_dropin_link",
+                        "-L" + lib_dir, "-lsdmk_b200", "-Wl,-rpath," + lib_dir], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.parametrize("kernel,dim,eps", [(0, 3, 1e-6), (1, 3, 1e-6), (2, 3, 1e-9), (0, 3, 1e-12)])
+def test_host_build_tables_image_equals_reference_export(kernel, dim, eps, tmp_path):
+    """build_split_kernel through the C-ABI (the drop-in's SplitKernel) is byte-identical
+    to the reference's export_split_kernel of its own tables (3D)."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    plan = ref.select_parameters(kernel, eps, 0, dim)
+    x = np.random.default_rng(0).uniform(-0.5, 0.5, (50, dim))
+    s = np.ones((50, g.strength_components(kernel, dim)))
+    P = ref.RefProblem(plan, dim, x, s)
+    path = str(tmp_path / "t.bin")
+    P.export_tables(path)
+    img = g.host_build_tables(kernel, dim, 0, plan["c"], 0.0, plan["table_tol"])
+    assert open(path, "rb").read() == img
+    # and a window other than the plan's (the SplitKernel override case)
+    P.set_window(plan["c"] * 1.15)
+    P.export_tables(path)
+    assert open(path, "rb").read() == g.host_build_tables(kernel, dim, 0, plan["c"] * 1.15, 0.0, plan["table_tol"])
+
+
+def test_host_build_window_matches_reference():
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    plan = ref.select_parameters(0, 1e-6, 0, 3)
+    P = ref.RefProblem(plan, 3, np.zeros((1, 3)), np.ones((1, 3)))
+    sc = np.zeros(8)
+    co = np.zeros(256)
+    n = ref.lib().ref_window(ref._dp(sc), ref._dp(co), 256)
+    w = g.host_build_window(0, plan["c"])
+    assert np.array_equal(w["legendre_coeffs"], co[:n])
+    assert [w["lambda0"], w["norm_r"], w["trunc_error"], w["psi0"], w["chi0"]] == list(sc[3:8])
+    del P

@@ -56,3 +56,22 @@ def test_pinned_strength_errors_keep_reference_precedence(system):
     # the context is still usable after the failures
     ok = ctx.evaluate_with_plan(plan, g.ParticleSystem(3, hx, np.zeros(0), hg))
     assert np.all(np.isfinite(ok))
+
+
+def test_array_length_errors_are_reported_before_any_read(gpu_ctx):
+    """mismatched array lengths raise the reference's invalid_argument
+    messages (oracle.cpp:108-115, dmk.cpp:1046-1047) instead of reading past an array."""
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-0.5, 0.5, (100, 3))
+    plan = g.select_parameters(1, 1e-6, g.PROLATE, 3)  # stresslet: 6 strength doubles per source
+    cases = [
+        (g.ParticleSystem(3, x, np.zeros(0), rng.standard_normal((100, 3))), "bad strength array length"),
+        (g.ParticleSystem(3, x.ravel()[:-1], np.zeros(0), rng.standard_normal((100, 6))), "bad source array length"),
+        (g.ParticleSystem(3, x, x.ravel()[:-2], rng.standard_normal((100, 6))), "bad target array length"),
+        (g.ParticleSystem(2, x, np.zeros(0), rng.standard_normal((100, 6))), "plan and system dimensions differ"),
+    ]
+    for sys_, msg in cases:
+        with pytest.raises(ValueError, match=msg):
+            gpu_ctx.evaluate_with_plan(plan, sys_)
+    with pytest.raises(ValueError, match="bad strength array length"):
+        gpu_ctx.direct_sum(0, g.ParticleSystem(3, x, np.zeros(0), rng.standard_normal((99, 3))))
