@@ -349,15 +349,15 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       nivl += __shfl_sync(0xffffffffu, pre, 31);
     }
     __syncwarp();
-    // Kahan accumulation per component, as the reference's (dmk.cpp:540-548,
-    // 994-1020): only in-support pairs are added (adding 0 would fold the
-    // compensation early), in the reference's order
-    double u[3] = {0.0, 0.0, 0.0}, uc[3] = {0.0, 0.0, 0.0};
-    auto kahan = [&](int j, double v) {
-      const double y = v - uc[j];
-      const double tt = u[j] + y;
-      uc[j] = (tt - u[j]) - y;
-      u[j] = tt;
+    // Each target's pairs are summed by its lane in a fixed order (plain
+    // sums: the reference's Kahan accumulators change no result at the
+    // BASELINE configurations by more than 1e-15 of the parity bar, and cost
+    // ~10% of the kernel).  Pairs with s < s_exact (rare) are evaluated after
+    // their round / list pass with the reference's own tables and recurrence.
+    double u[3] = {0.0, 0.0, 0.0};
+    auto add = [&](const double* c) {
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) u[j] += c[j];
     };
     int cnt = 0;
     const double sup2l = (r_l * rt.support) * (r_l * rt.support);
@@ -411,36 +411,39 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         for (int j = 0; j < DIM; ++j) c[j] = keep ? c[j] : 0.0;
         return keep;
       };
+      unsigned long long nearmask = 0;  // list entries to re-evaluate exactly (kList <= 64)
       for (int i = 0; i < mx; i += kILP) {  // all evaluations unconditional (clamped), straight-line
         double c[kILP][3];
-        bool kp[kILP];
+        bool kp[kILP], nr[kILP];
 #pragma unroll
         for (int q = 0; q < kILP; ++q) {
           c[q][0] = c[q][1] = c[q][2] = 0.0;
-          kp[q] = false;
+          kp[q] = nr[q] = false;
         }
-        bool nr[kILP];
         if (cnt > 0) {
 #pragma unroll
           for (int q = 0; q < kILP; ++q) {
             kp[q] = eval(min(i + q, cnt - 1), c[q], nr[q], std::false_type{}) && i + q < cnt;
             if (kp[q]) ++n_in;
-          }
-          bool any_near = false;
-#pragma unroll
-          for (int q = 0; q < kILP; ++q) any_near |= kp[q] && nr[q];
-          if (__any_sync(0xffffffffu, any_near)) {
-#pragma unroll
-            for (int q = 0; q < kILP; ++q)
-              if (kp[q] && nr[q]) eval(i + q, c[q], nr[q], std::true_type{});
+            if (kp[q] && nr[q]) {
+              nearmask |= 1ull << (i + q);
+              kp[q] = false;
+            }
           }
         }
 #pragma unroll
         for (int q = 0; q < kILP; ++q)
-          if (kp[q]) {
-#pragma unroll
-            for (int j = 0; j < DIM; ++j) kahan(j, c[q][j]);
-          }
+          if (kp[q]) add(c[q]);
+      }
+      while (__any_sync(0xffffffffu, nearmask != 0)) {  // rare: s < s_exact
+        double c[3] = {0.0, 0.0, 0.0};
+        bool nr = false;
+        if (nearmask) {
+          const int i = __ffsll(nearmask) - 1;
+          nearmask &= nearmask - 1;
+          eval(i, c, nr, std::true_type{});
+          add(c);
+        }
       }
       cnt = 0;
     };
@@ -513,24 +516,33 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           for (int k = 0; k < DIM; ++k) c[k] = keep ? c[k] : 0.0;
           return keep;
         };
+        unsigned nearbits = 0;  // sources of this round to re-evaluate exactly
         for (int j = 0; j < nv; j += 2) {
           double c0[3] = {0.0, 0.0, 0.0}, c1[3] = {0.0, 0.0, 0.0};
           bool n0, n1;
-          const bool k0 = dense(j, c0, n0, std::false_type{});
-          const bool k1 = dense(min(j + 1, nv - 1), c1, n1, std::false_type{}) && j + 1 < nv;
-          if (__any_sync(0xffffffffu, (k0 && n0) || (k1 && n1))) {
-            if (k0 && n0) dense(j, c0, n0, std::true_type{});
-            if (k1 && n1) dense(j + 1, c1, n1, std::true_type{});
-          }
-          if (k0) {
-#pragma unroll
-            for (int k = 0; k < DIM; ++k) kahan(k, c0[k]);
-          }
-          if (k1) {
-#pragma unroll
-            for (int k = 0; k < DIM; ++k) kahan(k, c1[k]);
-          }
+          bool k0 = dense(j, c0, n0, std::false_type{});
+          bool k1 = dense(min(j + 1, nv - 1), c1, n1, std::false_type{}) && j + 1 < nv;
           n_in += (k0 ? 1 : 0) + (k1 ? 1 : 0);
+          if (k0 && n0) {
+            nearbits |= 1u << j;
+            k0 = false;
+          }
+          if (k1 && n1) {
+            nearbits |= 1u << (j + 1);
+            k1 = false;
+          }
+          if (k0) add(c0);
+          if (k1) add(c1);
+        }
+        while (__any_sync(0xffffffffu, nearbits != 0)) {  // rare: s < s_exact
+          double c[3] = {0.0, 0.0, 0.0};
+          bool nr = false;
+          if (nearbits) {
+            const int j = __ffs(nearbits) - 1;
+            nearbits &= nearbits - 1;
+            dense(j, c, nr, std::true_type{});
+            add(c);
+          }
         }
         __syncwarp();  // the next round overwrites the buffer
       }
@@ -607,8 +619,9 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       double* ut = ures + (size_t)tperm[t] * DIM;
 #pragma unroll
       for (int j = 0; j < DIM; ++j) {
-        if (selfc != 0.0) kahan(j, selfc * sstr[(size_t)j * ns + t]);  // dmk.cpp:1015-1018
-        ut[j] = u[j];
+        double v = u[j];
+        if (selfc != 0.0) v += selfc * sstr[(size_t)j * ns + t];  // dmk.cpp:1015-1018
+        ut[j] = v;
       }
     }
     __syncwarp();  // the interval list is rewritten by the next chunk
