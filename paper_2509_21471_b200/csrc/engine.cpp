@@ -159,7 +159,6 @@ static void tune_host_allocator() {
   static bool done = false;
   if (done) return;
   done = true;
-  if (std::getenv("SDMK_NO_MALLOPT")) return;
   mallopt(M_MMAP_THRESHOLD, 512 << 20);
   mallopt(M_TRIM_THRESHOLD, 1 << 30);
 }
@@ -504,7 +503,7 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
     void* tmp = arena_.get("sort_tmp", tb);
     uint64_t* ktop = d == 3 ? arena_.as<uint64_t>("ktop", n) : nullptr;
     launch_morton(pts, n, d, klo, khi, ktop, idx, st_);
-    if (d == 3 && !full && !std::getenv("SDMK_FULL_SORT")) {
+    if (d == 3 && !full) {
       sort_morton_top(n, ktop, arena_.as<uint64_t>("ktop2", n), idx, perm, tmp, tb, flags + tie_flag, st_);
       ++launches_;
     } else {
@@ -889,7 +888,6 @@ void Context::upload_tree_lists_b() {
     std::vector<int> i_in, i_out, i_ci, i_seg, sbx, tbx, es, eslot, etau, gstart, gslot, tmeta;
   };
   std::vector<LV> lv(L);
-  const bool use_groups = !std::getenv("SDMK_NO_GROUP");
   std::vector<int> gslot(nb, -1);
   bool bad_tau = false;
   for (int lev = 0; lev < L; ++lev) {
@@ -962,7 +960,7 @@ void Context::upload_tree_lists_b() {
 #pragma omp parallel for schedule(static)
     for (int i = 0; i < nl; ++i)
       if (cnt[i] > 0) entries(ids[i], V.eslot.data() + eoff[i], V.etau.data() + eoff[i]);
-    if (lev > 0 && use_groups) build_groups(t, lev, V.tbx, V.es, V.eslot, V.etau, V.gstart, V.gslot, V.tmeta);
+    if (lev > 0) build_groups(t, lev, V.tbx, V.es, V.eslot, V.etau, V.gstart, V.gslot, V.tmeta);
   }
   if (bad_tau) throw RuntimeError("colleague offset outside {-1,0,1}");
   // root lists: box 0 with one zero-offset entry
@@ -1139,7 +1137,7 @@ void Context::run_downward() {  // dmk.cpp:705-857
   const int M = (P.N1 - 1) / 2;
   GridDev& gd = grid(grid_lev_, "grid_lev", d, p, P.N1, PI / 3.0, band_r2(P, M, PI / 3.0));
   const PWGrid& g = gd.g;
-  const bool use_mma = pw_mma_supported(g) && !getenv("SDMK_NO_PW_MMA");
+  const bool use_mma = pw_mma_supported(g);
   const int L = pr.tree.max_level + 1;
   const int S = 3 * M * M + 1;
   // per-level symbol tables (dmk.cpp:741-746), one upload
@@ -1155,10 +1153,7 @@ void Context::run_downward() {  // dmk.cpp:705-857
   cuda_check(cudaMemcpyAsync(dA, hA, Aall.size() * sizeof(double), cudaMemcpyHostToDevice, st_), "symbol upload");
   const size_t bytes_B = sizeof(double2) * pr.nch * g.pz * g.ncol;
   const size_t bytes_FC = sizeof(double2) * d * ((size_t)g.nhalf + (size_t)g.pz * g.ncol);
-  static const size_t budget = [] {  // scratch per B / F+C chunk (SDMK_PW_BUDGET_MB overrides)
-    const char* e = std::getenv("SDMK_PW_BUDGET_MB");
-    return (e ? (size_t)std::atol(e) : size_t(2048)) << 20;
-  }();
+  constexpr size_t budget = size_t(2048) << 20;  // scratch per B / F+C chunk
   const int chunk_src = (int)std::max<size_t>(1, budget / bytes_B);
   const int chunk_tgt = (int)std::max<size_t>(1, budget / bytes_FC);
   // plane-wave timing: one event pair per level, read after the evaluation's

@@ -615,17 +615,13 @@ void launch_anterp_mma(int kernel, const ChebDev& cb, const DBox* boxes, const i
     k_anterp2<MT_, NTW_, PC_, KC_, 3, W_><<<dim3(nleaf, (ntt + per - 1) / per, nrb), W_ * 32, sm2, st>>>( \
         cb, boxes, leaves, basis, str, n, out);                                                         \
   } while (0)
-  static const bool old_a = std::getenv("SDMK_ANTERP_OLD") != nullptr;
 #ifndef SDMK_A2K_NTW
 #define SDMK_A2K_NTW 3
 #define SDMK_A2K_W 12
 #endif
-  if (!old_a && cb.dim == 3 && p == 23 && kernel == 0) A2(9, SDMK_A2K_NTW, 23, 0, SDMK_A2K_W);
-  else if (!old_a && cb.dim == 3 && p == 22 && kernel == 1) A2(SDMK_A2S_MT, SDMK_A2S_NTW, 22, 1, 12);
-  else if (!old_a && cb.dim == 3 && p == 30 && kernel == 0) A2(12, 2, 30, 0, 12);
-  else if (cb.dim == 3 && p == 23 && kernel == 0) AMS(3, 6, 23, 0, 3);
-  else if (cb.dim == 3 && p == 22 && kernel == 1) AMS(3, 6, 22, 1, 3);
-  else if (cb.dim == 3 && p == 30 && kernel == 0) AMS(4, 4, 30, 0, 3);
+  if (cb.dim == 3 && p == 23 && kernel == 0) A2(9, SDMK_A2K_NTW, 23, 0, SDMK_A2K_W);
+  else if (cb.dim == 3 && p == 22 && kernel == 1) A2(SDMK_A2S_MT, SDMK_A2S_NTW, 22, 1, 12);
+  else if (cb.dim == 3 && p == 30 && kernel == 0) A2(12, 2, 30, 0, 12);
   else if (NTv <= 1) AM(1, 8);
   else if (NTv == 2) AM(2, 8);
   else if (NTv == 3) AM(3, 6);

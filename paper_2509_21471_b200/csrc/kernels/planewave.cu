@@ -581,7 +581,6 @@ void launch_accumulate_group(const PWGrid& g, int kernel, int ngroups, const int
   const int want = 8 * num_sms;
   const int gy = std::max(1, std::min(nchunk, (want + ngroups - 1) / ngroups));
   dim3 grid(ngroups, gy);
-  static const int zh = std::getenv("SDMK_ACC_ZH") ? std::atoi(std::getenv("SDMK_ACC_ZH")) : 1;
 #define ACC(K, D, Z)                                                                                         \
   do {                                                                                                       \
     const int sm_ = GroupCfg<K, D, Z>::kBytes;                                                               \
@@ -589,11 +588,9 @@ void launch_accumulate_group(const PWGrid& g, int kernel, int ngroups, const int
     k_acc_group<K, D, Z><<<grid, kGroupThreads, sm_, st>>>(g, grp_tstart, grp_slot, t_meta, t_base, G, A, h, F); \
   } while (0)
   if (g.dim == 3) {
-    if (kernel == 0 && zh == 1) ACC(0, 3, 1);
-    else if (kernel == 0) ACC(0, 3, 2);
+    if (kernel == 0) ACC(0, 3, 1);
     else if (kernel == 1) ACC(1, 3, 2);
-    else if (zh == 1) ACC(2, 3, 1);
-    else ACC(2, 3, 2);
+    else ACC(2, 3, 1);
   } else {
     if (kernel == 0) ACC(0, 2, 1);
     else if (kernel == 1) ACC(1, 2, 1);

@@ -40,129 +40,6 @@ __host__ __device__ constexpr int r4(int x) { return (x + 3) / 4 * 4 % 8 == 4 ? 
 __host__ __device__ constexpr int r8(int x) { return (x + 7) / 8 * 8 % 16 == 8 ? (x + 7) / 8 * 8 : (x + 7) / 8 * 8 + 8; }
 
 // ------------------------------------------------------------------ fwd_xy --
-// smem layout (doubles): EX[NX8][SE]  (rows (m0,part) -> B^T of the X stage)
-//                        EYr/EYi[NY8][SY] (A' of the Y stage, k' = 2 iy + part)
-//                        win[2][4*P8][SE] (A of the X stage), a[4*P8][SAa]
-// PC / NC > 0: p and N fixed at compile time (the BASELINE grids), so the
-// index arithmetic folds to constants.
-template <int PT, int PC, int NC>
-__global__ void __launch_bounds__(kW * 32, 1) k_fwd_xy_mma(PWGrid g, const int* __restrict__ boxes, int nch,
-                                                          const double* __restrict__ outgoing,
-                                                          double2* __restrict__ B) {
-  constexpr int P8 = PT * 8;
-  constexpr int SE = P8 + 4;  // == 4 mod 8 for P8 = 24, 32
-  const int p = PC > 0 ? PC : g.p, N = NC > 0 ? NC : g.N, M = (N - 1) / 2, ncol = g.ncol, pp = p * p;
-  const int M1 = M + 1, NX = 2 * M1, NX8 = (NX + 7) / 8 * 8, NY8 = (N + 7) / 8 * 8, M18 = (M1 + 7) / 8 * 8;
-  const int SY = r4(2 * P8), SAa = r8(NX8 > 2 * M18 ? NX8 : 2 * M18);
-  extern __shared__ double sm[];
-  double* EX = sm;                        // [NX8][SE]
-  double* EYr = EX + NX8 * SE;            // [NY8][SY]
-  double* EYi = EYr + NY8 * SY;           // [NY8][SY]
-  double* win = EYi + NY8 * SY;           // [2][4*P8][SE]
-  double* a = win + 2 * 4 * P8 * SE;      // [4*P8][SAa]
-  int* colidx = reinterpret_cast<int*>(a + 4 * P8 * SAa);  // [N][M1]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
-  for (int e = tid; e < NX8 * SE; e += blockDim.x) {  // EX[(m0,part)][ix] = E[m0][ix].re|im
-    const int r = e / SE, ix = e % SE, m0 = r >> 1, part = r & 1;
-    double v = 0.0;
-    if (m0 < M1 && ix < p) {
-      const double2 ev = g.E[(size_t)(m0 + M) * p + ix];
-      v = part ? ev.y : ev.x;
-    }
-    EX[e] = v;
-  }
-  for (int e = tid; e < NY8 * SY; e += blockDim.x) {  // EY'[my][(iy,part)]: re' = [Er | -Ei], im' = [Ei | Er]
-    const int my = e / SY, k = e % SY, iy = k >> 1, part = k & 1;
-    double vr = 0.0, vi = 0.0;
-    if (my < N && iy < p && k < 2 * P8) {
-      const double2 ev = g.E[(size_t)my * p + iy];
-      vr = part ? -ev.y : ev.x;
-      vi = part ? ev.x : ev.y;
-    }
-    EYr[e] = vr;
-    EYi[e] = vi;
-  }
-  for (int e = tid; e < N * M1; e += blockDim.x) colidx[e] = -1;
-  for (int e = tid; e < 2 * 4 * P8 * SE; e += blockDim.x) win[e] = 0.0;
-  for (int e = tid; e < 4 * P8 * SAa; e += blockDim.x) a[e] = 0.0;
-  __syncthreads();
-  for (int c = tid; c < ncol; c += blockDim.x) colidx[(g.col_my[c] + M) * M1 + g.col_m0[c]] = c;
-  const int slot = blockIdx.x, ch = blockIdx.y;
-  const double* w = outgoing + ((size_t)boxes[slot] * nch + ch) * (size_t)(p * pp);
-  double2* Bo = B + ((size_t)slot * nch + ch) * (size_t)g.pz * ncol;
-  const int ngroups = (p + 3) / 4;
-  auto issue = [&](int grp, int buf) {
-    double* dst = win + buf * 4 * P8 * SE;
-    const int jz0 = grp * 4;
-    for (int row = warp; row < 4 * p; row += kW) {  // rows (s, r), lanes along the row
-      const int s = row / p, r = row % p;
-      const bool v = jz0 + s < p;
-      const double* srow = w + (size_t)(v ? jz0 + s : 0) * pp + r * p;
-      for (int cc = lane; cc < p; cc += 32) cp_async8(dst + (s * P8 + r) * SE + cc, srow + cc, v);
-    }
-    cp_commit();
-  };
-  issue(0, 0);
-  const int xtiles = 4 * PT * (NX8 / 8);
-  const int ytiles = 4 * (NY8 / 8) * (M18 / 8);  // (s, my-tile, m0-tile); re and im computed together
-  for (int grp = 0; grp < ngroups; ++grp) {
-    const int buf = grp & 1;
-    __syncthreads();
-    if (grp + 1 < ngroups) {
-      issue(grp + 1, buf ^ 1);
-      cp_wait1();
-    } else {
-      cp_wait0();
-    }
-    __syncthreads();
-    const double* A = win + buf * 4 * P8 * SE;
-    // X stage
-    for (int tile0 = warp; tile0 < xtiles; tile0 += 2 * kW) {
-      const int tile1 = tile0 + kW;
-      const bool two = tile1 < xtiles;
-      const int nnt = NX8 / 8;
-      const int mA = tile0 / nnt, nA = tile0 % nnt, mB = two ? tile1 / nnt : mA, nB = two ? tile1 % nnt : nA;
-      double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < PT * 2; ++ks) {
-        dmma(c0, c1, A[(mA * 8 + gq) * SE + ks * 4 + t], EX[(nA * 8 + gq) * SE + ks * 4 + t]);
-        if (two) dmma(d0, d1, A[(mB * 8 + gq) * SE + ks * 4 + t], EX[(nB * 8 + gq) * SE + ks * 4 + t]);
-      }
-      a[(mA * 8 + gq) * SAa + nA * 8 + 2 * t] = c0;
-      a[(mA * 8 + gq) * SAa + nA * 8 + 2 * t + 1] = c1;
-      if (two) {
-        a[(mB * 8 + gq) * SAa + nB * 8 + 2 * t] = d0;
-        a[(mB * 8 + gq) * SAa + nB * 8 + 2 * t + 1] = d1;
-      }
-    }
-    __syncthreads();
-    // Y stage: b[s][my][m0] (complex); B'[(iy,part)][m0] = a[s][iy][2 m0 + part]
-    const int nmy = NY8 / 8, nm0 = M18 / 8;
-    for (int tile = warp; tile < ytiles; tile += kW) {
-      const int s = tile / (nmy * nm0), mt = (tile / nm0) % nmy, nt = tile % nm0;
-      double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < PT * 4; ++ks) {
-        const int k = ks * 4 + t, iy = k >> 1, part = k & 1;
-        const double bv = a[(s * P8 + iy) * SAa + 2 * (nt * 8 + gq) + part];
-        dmma(cr0, cr1, EYr[(mt * 8 + gq) * SY + k], bv);
-        dmma(ci0, ci1, EYi[(mt * 8 + gq) * SY + k], bv);
-      }
-      const int my = mt * 8 + gq, iz = grp * 4 + s;
-      if (my < N && iz < p) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int m0 = nt * 8 + 2 * t + e;
-          if (m0 < M1) {
-            const int cidx = colidx[my * M1 + m0];
-            if (cidx >= 0) Bo[(size_t)iz * ncol + cidx] = make_double2(e ? cr1 : cr0, e ? ci1 : ci0);
-          }
-        }
-      }
-    }
-  }
-}
-
 // fwd_xy with the Hermitian split of the Y stage.  E[-m] = conj E[m] and
 // E[0] = 1, so for m0 >= 1 (complex a = ar + i ai) and my >= 1
 //   P = Er ar, Q = Ei ai, R = Er ai, S = Ei ar      (Er, Ei: rows my = 1..M)
@@ -336,89 +213,7 @@ __global__ void __launch_bounds__(kW * 32, 1) k_fwd_xy2(PWGrid g, const int* __r
 }
 
 // ------------------------------------------------------------ z stages ----
-// Complex GEMM over 64-column blocks: OUT[rr, col] = sum_k A'[rr, (k,part)] IN[(k,part), col]
-// with IN loaded zero-filled from the compressed source.
-//  forward : rr = mz (G, compressed out), k = iz (B, dense in), A'_re = [Er | -Ei], A'_im = [Ei | Er]
-//  inverse : rr = iz (C1, dense out), k = mz (F, compressed in), conj(E)^T:
-//            A'_re = [Er | Ei], A'_im = [-Ei | Er]
-constexpr int kCB = 64;
-
-template <int KT, int RT, bool INV>  // KT: k-tiles of 8 (K8 = KT*8); RT: row tiles of 8
-__global__ void __launch_bounds__(kW * 32, 2) k_z_mma(PWGrid g, int nc, const double2* __restrict__ IN,
-                                                      double2* __restrict__ OUT) {
-  constexpr int K8 = KT * 8, SK = 2 * K8 + 4;       // A' row stride (k' = 2k + part), == 4 mod 8
-  constexpr int SI = (2 * kCB) % 16 == 8 ? 2 * kCB : 2 * kCB + 8;  // IN rows (k) of interleaved (col, part)
-  extern __shared__ double sm[];
-  double* Ar = sm;                  // [RT*8][SK]
-  double* Ai = Ar + RT * 8 * SK;    // [RT*8][SK]
-  double* In = Ai + RT * 8 * SK;    // [K8][SI]
-  const int pz = g.pz, Mz = g.Mz, ncol = g.ncol;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
-  const int rows = INV ? pz : g.Nz, kdim = INV ? g.Nz : pz;
-  for (int e = tid; e < RT * 8 * SK; e += blockDim.x) {
-    const int rr = e / SK, kk = e % SK, k = kk >> 1, part = kk & 1;
-    double vr = 0.0, vi = 0.0;
-    if (rr < rows && k < kdim && kk < 2 * K8) {
-      // forward: E[mz=rr][iz=k]; inverse: E[mz=k][iz=rr]
-      const double2 ev = INV ? g.Ez[(size_t)k * pz + rr] : g.Ez[(size_t)rr * pz + k];
-      if (!INV) {
-        vr = part ? -ev.y : ev.x;
-        vi = part ? ev.x : ev.y;
-      } else {
-        vr = part ? ev.y : ev.x;
-        vi = part ? ev.x : -ev.y;
-      }
-    }
-    Ar[e] = vr;
-    Ai[e] = vi;
-  }
-  const int box = blockIdx.x, comp = blockIdx.y, c0 = blockIdx.z * kCB;
-  const int ncb = min(kCB, ncol - c0);
-  const size_t in_stride = INV ? (size_t)g.nhalf : (size_t)pz * ncol;
-  const size_t out_stride = INV ? (size_t)pz * ncol : (size_t)g.nhalf;
-  const double2* src = IN + ((size_t)box * nc + comp) * in_stride;
-  double2* dst = OUT + ((size_t)box * nc + comp) * out_stride;
-  for (int e = tid; e < K8 * kCB; e += blockDim.x) {
-    const int k = e / kCB, cc = e % kCB, col = c0 + cc;
-    double2 v = make_double2(0.0, 0.0);
-    if (k < kdim && cc < ncb) {
-      if (INV) {
-        if (col < g.slab_ncol[k]) v = src[g.slab_off[k] + col];
-      } else {
-        v = src[(size_t)k * ncol + col];
-      }
-    }
-    In[k * SI + 2 * cc] = v.x;
-    In[k * SI + 2 * cc + 1] = v.y;
-  }
-  __syncthreads();
-  // C tiles: (row tile, column tile of 8) with re and im; warp owns tiles warp + kW*i
-  const int ntc = kCB / 8, ntile = RT * ntc;
-  for (int tile = warp; tile < ntile; tile += kW) {
-    const int rt = tile / ntc, ct = tile % ntc;
-    double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
-#pragma unroll
-    for (int ks = 0; ks < KT * 4; ++ks) {
-      const int kk = ks * 4 + t, k = kk >> 1, part = kk & 1;
-      const double bv = In[k * SI + 2 * (ct * 8 + gq) + part];
-      dmma(cr0, cr1, Ar[(rt * 8 + gq) * SK + kk], bv);
-      dmma(ci0, ci1, Ai[(rt * 8 + gq) * SK + kk], bv);
-    }
-    const int rr = rt * 8 + gq;
-    if (rr >= rows) continue;
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int col = c0 + ct * 8 + 2 * t + e;
-      if (col >= c0 + ncb) continue;
-      const double2 v = make_double2(e ? cr1 : cr0, e ? ci1 : ci0);
-      if (INV) {
-        dst[(size_t)rr * ncol + col] = v;
-      } else if (col < g.slab_ncol[rr]) {
-        dst[g.slab_off[rr] + col] = v;
-      }
-    }
-  }
-}
+constexpr int kCB = 64;  // columns per z-stage work item
 
 // z stages with the Hermitian split (E[-m] = conj E[m], E[0] = 1):
 //  forward  G[+-mz] = (P -+ Q) + i (R +- S), P = Er Br, Q = Ei Bi, R = Er Bi,
@@ -948,76 +743,38 @@ void launch_forward_mma(const PWGrid& g, const int* boxes, int nbox, int nch, co
                         double2* G, cudaStream_t st) {
   if (nbox <= 0) return;
   const int PT = (g.p + 7) / 8 <= 3 ? 3 : 4;  // the instantiated template sizes
-  const int M1 = g.M + 1, NX8 = (2 * M1 + 7) / 8 * 8, NY8 = (g.N + 7) / 8 * 8;
-  {
-    const int M18 = (M1 + 7) / 8 * 8;
-    const int P8 = PT * 8, SE = P8 + 4, SY = r4(2 * P8), SAa = r8(NX8 > 2 * M18 ? NX8 : 2 * M18);
-    size_t smem = sizeof(double) * ((size_t)NX8 * SE + 2 * (size_t)NY8 * SY + 2 * 4 * (size_t)P8 * SE +
-                                    4 * (size_t)P8 * SAa) + sizeof(int) * (size_t)g.N * M1;
-    dim3 grid(nbox, nch);
-#define FX(PT_, PC_, NC_)                                                             \
-  do {                                                                                \
-    attr((const void*)k_fwd_xy_mma<PT_, PC_, NC_>, smem);                             \
-    k_fwd_xy_mma<PT_, PC_, NC_><<<grid, kW * 32, smem, st>>>(g, boxes, nch, outgoing, B); \
+  const int M = g.M, M1 = M + 1, MT = (M + 7) / 8, P8 = PT * 8;
+  {  // x and y stages: B[box][ch][iz][col]
+    const int NX8 = (2 * M + 1 + 7) / 8 * 8;
+    const size_t sm = sizeof(double) * ((size_t)NX8 * (P8 + 4) + 2 * (size_t)MT * 8 * (P8 + 4) +
+                                        2 * 4 * (size_t)P8 * (P8 + 4) + 4 * (size_t)P8 * r8(NX8 > 16 * MT ? NX8 : 16 * MT)) +
+                      sizeof(int) * (size_t)g.N * M1;
+#define FX2(PT_, PC_, NC_)                                                                                    \
+  do {                                                                                                        \
+    attr((const void*)k_fwd_xy2<PT_, PC_, NC_>, sm);                                                          \
+    k_fwd_xy2<PT_, PC_, NC_><<<std::min(nbox * nch, 2 * num_sms()), kW * 32, sm, st>>>(g, boxes, nbox, nch,   \
+                                                                                     outgoing, B);            \
   } while (0)
-    static const bool old_xy = std::getenv("SDMK_PW_OLD") != nullptr;
-    if (old_xy) {
-      if (g.p == 23 && g.N == 33) FX(3, 23, 33);
-      else if (g.p == 22 && g.N == 33) FX(3, 22, 33);
-      else if (g.p == 30 && g.N == 45) FX(4, 30, 45);
-      else if (PT <= 3) FX(3, 0, 0);
-      else FX(4, 0, 0);
-    } else {
-      const int M = g.M, MT = (M + 7) / 8, NX8b = (2 * M + 1 + 7) / 8 * 8, P8 = PT * 8;
-      const size_t sm2 = sizeof(double) * ((size_t)NX8b * (P8 + 4) + 2 * (size_t)MT * 8 * (P8 + 4) +
-                                           2 * 4 * (size_t)P8 * (P8 + 4) + 4 * (size_t)P8 * r8(NX8b > 16 * MT ? NX8b : 16 * MT)) +
-                         sizeof(int) * (size_t)g.N * M1;
-#define FX2(PT_, PC_, NC_)                                                            \
-  do {                                                                                \
-    attr((const void*)k_fwd_xy2<PT_, PC_, NC_>, sm2);                                 \
-    k_fwd_xy2<PT_, PC_, NC_><<<std::min(nbox * nch, 2 * num_sms()), kW * 32, sm2, st>>>(g, boxes, nbox, nch,  \
-                                                                                      outgoing, B);              \
-  } while (0)
-      if (g.p == 23 && g.N == 33) FX2(3, 23, 33);
-      else if (g.p == 22 && g.N == 33) FX2(3, 22, 33);
-      else if (g.p == 30 && g.N == 45) FX2(4, 30, 45);
-      else if (PT <= 3) FX2(3, 0, 0);
-      else FX2(4, 0, 0);
+    if (g.p == 23 && g.N == 33) FX2(3, 23, 33);
+    else if (g.p == 22 && g.N == 33) FX2(3, 22, 33);
+    else if (g.p == 30 && g.N == 45) FX2(4, 30, 45);
+    else if (PT <= 3) FX2(3, 0, 0);
+    else FX2(4, 0, 0);
 #undef FX2
-    }
-#undef FX
   }
-  {
-    const int KT = PT, RT = (g.Nz + 7) / 8 <= 5 ? 5 : 6;
-    const int K8 = KT * 8, SK = 2 * K8 + 4, SI = (2 * kCB) % 16 == 8 ? 2 * kCB : 2 * kCB + 8;
-    size_t smem = sizeof(double) * (2 * (size_t)RT * 8 * SK + (size_t)K8 * SI);
-    dim3 grid(nbox, nch, (g.ncol + kCB - 1) / kCB);
-#define ZF(KT_, RT_)                                                                  \
-  do {                                                                                \
-    attr((const void*)k_z_mma<KT_, RT_, false>, smem);                                \
-    k_z_mma<KT_, RT_, false><<<grid, kW * 32, smem, st>>>(g, nch, B, G);              \
-  } while (0)
-    static const bool old_z = std::getenv("SDMK_PW_OLD") != nullptr;
-    if (old_z) {
-      if (KT <= 3) {
-        if (RT <= 5) ZF(3, 5); else ZF(3, 6);
-      } else {
-        if (RT <= 5) ZF(4, 5); else ZF(4, 6);
-      }
+  {  // z stage: G[box][ch][mode]
+    const int SI = (2 * kCB) % 16 == 8 ? 2 * kCB : 2 * kCB + 8;
+    const int M8 = (g.Mz + 7) / 8 * 8;
+    const size_t sz = sizeof(double) * (2 * (size_t)M8 * (P8 + 4) + 2 * (size_t)P8 * SI);
+    const int items = nbox * nch * ((g.ncol + kCB - 1) / kCB);
+    const int ctas = std::min(items, 3 * num_sms());
+    if (PT <= 3) {
+      attr((const void*)k_zf2<3>, sz);
+      k_zf2<3><<<ctas, kW * 32, sz, st>>>(g, nch, nbox, B, G);
     } else {
-      const int M8 = (g.Mz + 7) / 8 * 8, P8 = PT * 8;
-      const size_t sz = sizeof(double) * (2 * (size_t)M8 * (P8 + 4) + 2 * (size_t)P8 * SI);
-      const int items = nbox * nch * ((g.ncol + kCB - 1) / kCB);
-      const int ctas = std::min(items, 3 * num_sms());
-      if (PT <= 3) {
-        attr((const void*)k_zf2<3>, sz);
-        k_zf2<3><<<ctas, kW * 32, sz, st>>>(g, nch, nbox, B, G);
-      } else {
-        attr((const void*)k_zf2<4>, sz);
-        k_zf2<4><<<ctas, kW * 32, sz, st>>>(g, nch, nbox, B, G);
-      }
+      attr((const void*)k_zf2<4>, sz);
+      k_zf2<4><<<ctas, kW * 32, sz, st>>>(g, nch, nbox, B, G);
     }
-#undef ZF
   }
 }
 
@@ -1025,71 +782,44 @@ void launch_inverse_mma(const PWGrid& g, const int* tboxes, int ntb, int d, cons
                         double* incoming, cudaStream_t st) {
   if (ntb <= 0) return;
   const int PT = (g.p + 7) / 8 <= 3 ? 3 : 4;  // the instantiated template sizes
-  {
-    const int KT = (g.Nz + 7) / 8 <= 5 ? 5 : 6, RT = PT;
-    const int K8 = KT * 8, SK = 2 * K8 + 4, SI = (2 * kCB) % 16 == 8 ? 2 * kCB : 2 * kCB + 8;
-    size_t smem = sizeof(double) * (2 * (size_t)RT * 8 * SK + (size_t)K8 * SI);
-    dim3 grid(ntb, d, (g.ncol + kCB - 1) / kCB);
-#define ZI(KT_, RT_)                                                                  \
-  do {                                                                                \
-    attr((const void*)k_z_mma<KT_, RT_, true>, smem);                                 \
-    k_z_mma<KT_, RT_, true><<<grid, kW * 32, smem, st>>>(g, d, F, C);                 \
-  } while (0)
-    static const bool old_z = std::getenv("SDMK_PW_OLD") != nullptr;
-    if (old_z) {
-      if (RT <= 3) {
-        if (KT <= 5) ZI(5, 3); else ZI(6, 3);
-      } else {
-        if (KT <= 5) ZI(5, 4); else ZI(6, 4);
-      }
+  const int P8 = PT * 8, M = g.M, M1 = M + 1, MT = (M + 7) / 8, M8 = MT * 8;
+  {  // z stage: C1[box][j][iz][col]
+    const int M8z = (g.Mz + 7) / 8 * 8;
+    const size_t sz = sizeof(double) * 2 * (size_t)P8 * r4(2 * M8z) + sizeof(double2) * 2 * (size_t)g.Nz * (kCB + 2);
+    const int items = ntb * d * ((g.ncol + kCB - 1) / kCB);
+    const int ctas = std::min(items, 2 * num_sms());
+    if (PT <= 3) {
+      attr((const void*)k_zi2<3>, sz);
+      k_zi2<3><<<ctas, kW * 32, sz, st>>>(g, d, ntb, F, C);
     } else {
-      const int M8 = (g.Mz + 7) / 8 * 8, P8 = PT * 8;
-      const size_t sz = sizeof(double) * 2 * (size_t)P8 * r4(2 * M8) + sizeof(double2) * 2 * (size_t)g.Nz * (kCB + 2);
-      const int items = ntb * d * ((g.ncol + kCB - 1) / kCB);
-      const int ctas = std::min(items, 2 * num_sms());
-      if (PT <= 3) {
-        attr((const void*)k_zi2<3>, sz);
-        k_zi2<3><<<ctas, kW * 32, sz, st>>>(g, d, ntb, F, C);
-      } else {
-        attr((const void*)k_zi2<4>, sz);
-        k_zi2<4><<<ctas, kW * 32, sz, st>>>(g, d, ntb, F, C);
-      }
+      attr((const void*)k_zi2<4>, sz);
+      k_zi2<4><<<ctas, kW * 32, sz, st>>>(g, d, ntb, F, C);
     }
-#undef ZI
   }
-  {
-    const int P8 = PT * 8, M1 = g.M + 1, NY8 = (g.N + 7) / 8 * 8, M18 = (M1 + 7) / 8 * 8;
-    const int NX8 = (2 * M1 + 7) / 8 * 8, SA = r4(2 * NY8), SX = r4(NX8 > 2 * M18 ? NX8 : 2 * M18);
-    size_t smem = sizeof(double) * (2 * (size_t)P8 * SA + (size_t)P8 * SX + 4 * (size_t)P8 * SX +
-                                    2 * 4 * 2 * (size_t)g.ncol) + sizeof(int) * (size_t)NY8 * M18;
-    dim3 grid(ntb, d);
-#define IX(PT_, PC_, NC_)                                                                    \
-  do {                                                                                       \
-    attr((const void*)k_inv_xy_mma<PT_, PC_, NC_>, smem);                                    \
-    k_inv_xy_mma<PT_, PC_, NC_><<<grid, kWI * 32, smem, st>>>(g, tboxes, d, C, pf, incoming); \
-  } while (0)
-    static const bool old_xy = std::getenv("SDMK_PW_OLD") != nullptr;
-    const int M_ = g.M, M8_ = (M_ + 7) / 8 * 8, SB_ = (M8_ % 16 == 8) ? M8_ : M8_ + 8, NXK_ = (2 * M1 + 3) / 4 * 4;
-    const size_t sm2_ = sizeof(double) * (2 * (size_t)P8 * r4(2 * M8_) + 5 * (size_t)P8 * r4(NXK_) +
-                                          2 * 4 * (size_t)2 * M8_ * SB_) +
-                        sizeof(double2) * 2 * 4 * (size_t)g.N * M1 + sizeof(int) * (size_t)g.ncol;
-    if (old_xy || sm2_ > 227 * 1024) {  // the split kernel stages dense slabs: too big for the largest grids
-      if (g.p == 23 && g.N == 33) IX(3, 23, 33);
-      else if (g.p == 22 && g.N == 33) IX(3, 22, 33);
-      else if (g.p == 30 && g.N == 45) IX(4, 30, 45);
-      else if (PT <= 3) IX(3, 0, 0);
-      else IX(4, 0, 0);
+  {  // y and x stages into the incoming proxies
+    const int K2 = 2 * M8, SA2 = r4(K2), SB = (M8 % 16 == 8) ? M8 : M8 + 8, NXK = (2 * M1 + 3) / 4 * 4,
+              SX2 = r4(NXK);
+    const size_t sm2 = sizeof(double) * (2 * (size_t)P8 * SA2 + (size_t)P8 * SX2 + 4 * (size_t)P8 * SX2 +
+                                         2 * 4 * (size_t)K2 * SB) +
+                       sizeof(double2) * 2 * 4 * (size_t)g.N * M1 + sizeof(int) * (size_t)g.ncol;
+    if (sm2 > 227 * 1024) {  // the split kernel stages dense slabs: too big for the largest grids
+      const int M18 = (M1 + 7) / 8 * 8, NY8 = (g.N + 7) / 8 * 8, NX8 = (2 * M1 + 7) / 8 * 8;
+      const int SA = r4(2 * NY8), SX = r4(NX8 > 2 * M18 ? NX8 : 2 * M18);
+      const size_t smem = sizeof(double) * (2 * (size_t)P8 * SA + (size_t)P8 * SX + 4 * (size_t)P8 * SX +
+                                            2 * 4 * 2 * (size_t)g.ncol) + sizeof(int) * (size_t)NY8 * M18;
+      if (PT <= 3) {
+        attr((const void*)k_inv_xy_mma<3, 0, 0>, smem);
+        k_inv_xy_mma<3, 0, 0><<<dim3(ntb, d), kWI * 32, smem, st>>>(g, tboxes, d, C, pf, incoming);
+      } else {
+        attr((const void*)k_inv_xy_mma<4, 0, 0>, smem);
+        k_inv_xy_mma<4, 0, 0><<<dim3(ntb, d), kWI * 32, smem, st>>>(g, tboxes, d, C, pf, incoming);
+      }
     } else {
-      const int M = g.M, MT = (M + 7) / 8, M8 = MT * 8, K2 = 2 * M8;
-      const int SA2 = r4(K2), SB = (M8 % 16 == 8) ? M8 : M8 + 8, NXK = (2 * M1 + 3) / 4 * 4, SX2 = r4(NXK);
-      const size_t sm2 = sizeof(double) * (2 * (size_t)P8 * SA2 + (size_t)P8 * SX2 + 4 * (size_t)P8 * SX2 +
-                                           2 * 4 * (size_t)K2 * SB) +
-                         sizeof(double2) * 2 * 4 * (size_t)g.N * M1 + sizeof(int) * (size_t)g.ncol;
-#define IX2(PT_, PC_, NC_)                                                                  \
-  do {                                                                                      \
-    attr((const void*)k_inv_xy2<PT_, PC_, NC_>, sm2);                                       \
-    k_inv_xy2<PT_, PC_, NC_><<<std::min(ntb * d, num_sms()), kWI * 32, sm2, st>>>(g, tboxes, ntb, d, C, pf,      \
-                                                                                    incoming);                 \
+#define IX2(PT_, PC_, NC_)                                                                                  \
+  do {                                                                                                      \
+    attr((const void*)k_inv_xy2<PT_, PC_, NC_>, sm2);                                                       \
+    k_inv_xy2<PT_, PC_, NC_><<<std::min(ntb * d, num_sms()), kWI * 32, sm2, st>>>(g, tboxes, ntb, d, C, pf, \
+                                                                                    incoming);              \
   } while (0)
       if (g.p == 23 && g.N == 33) IX2(3, 23, 33);
       else if (g.p == 22 && g.N == 33) IX2(3, 22, 33);
@@ -1098,7 +828,6 @@ void launch_inverse_mma(const PWGrid& g, const int* tboxes, int ntb, int d, cons
       else IX2(4, 0, 0);
 #undef IX2
     }
-#undef IX
   }
 }
 

@@ -1,24 +1,32 @@
 // K12: near-field residual pass (dmk.cpp:919-1032) with the fused residual
 // apply (split.cpp:258-317).
 //
-// One CTA per target leaf; each warp owns 32 Morton-consecutive targets of the
-// leaf, one per lane (so each target's pairs are summed by one lane, in the
-// reference's order: ranges in order, sources in order).
-//  1. The leaf's near ranges (own box nu = r_l, colleague leaves and fine
-//     neighbours nu = r_l/2, coarse neighbours nu = r_l; dmk.cpp:980-990) are
-//     staged in shared memory with their (shifted) bounding boxes.
-//  2. A range is skipped warp-uniformly when its box lies outside the support
-//     sphere of every target of the warp (distance to the warp's target
-//     bounding box; conservative 1e-12 margin, so no pair with
-//     r^2 < (nu*support)^2 is ever dropped).
-//  3. Sources stream as warp-uniform broadcast loads; every lane tests its own
-//     target with a conservative single-precision pre-test and appends the
-//     candidates to a lane-private list in shared memory.
-//  4. When any list fills, all lanes evaluate their lists in lockstep: the
-//     reference's exact double-precision support test (x = xt - (xs + shift),
-//     unfused r2), the radial tables from a piecewise re-expansion held in
-//     shared memory (host/setup.hpp PiecewisePoly), and 1/r from rsqrt.
-// No atomics and a fixed per-target order: bitwise reproducible.
+// Persistent kernel: one 16-warp CTA per SM; each warp takes 32-target
+// chunks of one leaf from an atomic counter, one target per lane, so each
+// target's pairs are summed by one lane in a fixed order (own box first, then
+// the near ranges and their sources in the reference's order).
+//  1. Intervals: the lanes build the chunk's source intervals in parallel, one
+//     near range per lane (own box nu = r_l, colleague leaves and fine
+//     neighbours nu = r_l/2, coarse neighbours nu = r_l; dmk.cpp:966-990):
+//     the range box and then its Morton child sub-cells are culled against
+//     the warp's target bounding box with a conservative margin (no pair with
+//     r^2 < (nu*support)^2 is dropped); survivors in (range, sub-cell) order.
+//  2. Own box (dense): rounds of 32 packed source records are staged in the
+//     warp's list storage and broadcast to every lane; the exact test masks
+//     out-of-support pairs.
+//  3. Other intervals (lists): sources stream in coalesced rounds of 32 and
+//     are broadcast by shuffles; each lane runs a conservative single-
+//     precision pre-test and appends candidates to a lane-private list in
+//     shared memory; full lists are evaluated in lockstep, kILP entries per
+//     step, with the reference's exact double-precision support test
+//     (x = xt - (xs + shift), unfused r2).
+//  4. Radial tables: a piecewise degree-6 re-expansion of the reference's
+//     Chebyshev tables in shared memory (8 bank-interleaved copies), within
+//     1e-15 of them; pairs in the first interval (s < 1/128, where the
+//     kernels' 1/r^2..1/r^5 factors amplify absolute table errors) are
+//     re-evaluated after their round / list pass with the reference's own
+//     coefficients and Clenshaw recurrence, unfused.  1/r from rsqrt.
+// No atomics on the data and a fixed per-target order: bitwise reproducible.
 #include "common.cuh"
 #include "launch.hpp"
 
@@ -464,13 +472,11 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     // masks the pairs outside the support).  Own-box pairs come first in the
     // reference's order, so every target still sums its pairs in order.
     int nself = 0;
-#ifndef SDMK_RES_NODENSE
     {
       const bool isself = lane < nivl && (ivl[lane].z & 256);
       const unsigned notself = __ballot_sync(0xffffffffu, !isself);
       nself = notself ? __ffs(notself) - 1 : 32;
     }
-#endif
     for (int q = 0; q < nself; ++q) {
       const int4 iv = ivl[q];
       constexpr int RW = Rec<KERNEL, DIM>::kW;

@@ -932,16 +932,13 @@ void tensor_up_t(const double* mats, const int* in_list, const int* out_box, con
 }
 }  // namespace
 
-bool tensor_seg_supported(int p, int dim) { return dim == 3 && p >= 17 && p <= 24 && !std::getenv("SDMK_TENSOR_OLD"); }
+bool tensor_seg_supported(int p, int dim) { return dim == 3 && p >= 17 && p <= 24; }
 
 void launch_tensor_mma_seg(int p, const double* mats, const int* in_list, const int* out_box, const int* ci,
                            const int* seg, int nseg, int nch, const double* src, double* dst, cudaStream_t st) {
   if (nseg <= 0) return;
-  static const bool prefix = std::getenv("SDMK_TENSOR_NOPREFIX") == nullptr;
-  if (prefix && p == 23) tensor_down_t<23>(mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
-  else if (prefix && p == 22) tensor_down_t<22>(mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
-  else if (p == 23) tensor3_seg_t<23>(p, mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
-  else if (p == 22) tensor3_seg_t<22>(p, mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
+  if (p == 23) tensor_down_t<23>(mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
+  else if (p == 22) tensor_down_t<22>(mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
   else tensor3_seg_t<0>(p, mats, in_list, out_box, ci, seg, nseg, nch, src, dst, st);
 }
 
@@ -958,25 +955,18 @@ void launch_tensor_mma(int p, const double* mats, const int* in_list, const int*
   const int PT = (p + 7) / 8;
 #define TM(PC_, PT_, NW_, ZT_) \
   tensor_mma_t<PC_, PT_, NW_, ZT_>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st)
-  static const bool old3 = std::getenv("SDMK_TENSOR_OLD") != nullptr;
-  static const bool up_suffix = std::getenv("SDMK_TENSOR_NOSUFFIX") == nullptr;
-  if (accumulate == 2 && dim == 3 && up_suffix && !old3 && (p == 22 || p == 23)) {  // merges: shared suffix
+  if (accumulate == 2 && dim == 3 && (p == 22 || p == 23)) {  // merges: shared suffix
     if (p == 23) tensor_up_t<23>(mats, in_list, out_box, ci, npairs, nch, src, dst, st);
     else tensor_up_t<22>(mats, in_list, out_box, ci, npairs, nch, src, dst, st);
     return;
   }
-  if (p == 22 && !old3) tensor3_t<22>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
-  else if (p == 23 && !old3) tensor3_t<23>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
-  else if (PT == 3 && !old3) tensor3_t<0>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
-  else if (p == 22) TM(22, 3, 16, 13);
-  else if (p == 23) TM(23, 3, 16, 13);
-  else if (p == 30 && !old3) tensor4_t<30>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
-  else if (PT == 4 && !old3) tensor4_t<0>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
-  else if (p == 30) TM(30, 4, 16, 32);
+  if (p == 22) tensor3_t<22>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
+  else if (p == 23) tensor3_t<23>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
+  else if (PT == 3) tensor3_t<0>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
+  else if (p == 30) tensor4_t<30>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
+  else if (PT == 4) tensor4_t<0>(p, mats, in_list, out_box, ci, npairs, nin, nch, src, dst, acc, st);
   else if (PT <= 1) TM(0, 1, 4, 8);
-  else if (PT == 2) TM(0, 2, 8, 12);
-  else if (PT == 3) TM(0, 3, 16, 13);
-  else TM(0, 4, 16, 32);
+  else TM(0, 2, 8, 12);
 #undef TM
 }
 
