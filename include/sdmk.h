@@ -249,8 +249,10 @@ int sdmk_set_shard(sdmk_context* ctx, int rank, int nranks);
    (2) exchange, in one NCCL group on the context stream, the outgoing
    expansions every other rank reads (colleagues of its plane-wave targets)
    plus all cut boxes, (3) merge the boxes above the cut on every rank, run
-   the sharded downward / far-field / residual passes, and (4) all-reduce u,
-   so every rank returns the full result, bitwise equal to nranks = 1. */
+   the sharded downward / far-field / residual passes, and (4) all-gather
+   every rank's owned Morton range of u (sdmk_host_shard_bounds) and scatter
+   it to caller order, so every rank returns the full result, bitwise equal
+   to nranks = 1. */
 int sdmk_comm_unique_id(unsigned char id[128]);
 int sdmk_comm_init(sdmk_context* ctx, int rank, int nranks, const unsigned char id[128]);
 /* The same evaluation without NCCL, in two halves, for tests and per-rank
@@ -290,6 +292,12 @@ int64_t sdmk_host_topology_dump(int dim, int periodic, int n_s, int p, int64_t n
    boxes whose incoming expansions the rank forms, target leaves in total */
 int sdmk_host_shard_plan(int dim, int periodic, int n_s, int p, int64_t n_src, const int32_t* q_src,
                          int64_t n_tgt, const int32_t* q_tgt, int rank, int nranks, int64_t* out);
+
+/* every rank's owned range of sorted targets at once (out: nranks + 1
+   bounds; rank r owns [out[r], out[r+1])): the layout of the u all-gather
+   that sdmk_comm_init evaluations end with */
+int sdmk_host_shard_bounds(int dim, int periodic, int n_s, int p, int64_t n_src, const int32_t* q_src,
+                           int64_t n_tgt, const int32_t* q_tgt, int nranks, int64_t* out);
 
 /* the exchange plan sdmk_comm_init evaluations use, from the same host
    topology: out[f * nranks + r] = boxes rank r receives from rank f;

@@ -126,6 +126,8 @@ def lib():
             "sdmk_host_build_window": ([C.c_int, C.c_double, C.c_double, dp, dp, C.c_int], C.c_int),
             "sdmk_host_window_eval": ([C.c_int, C.c_double, C.c_double, dp, C.c_int, dp, C.c_int, C.c_int64, dp, dp],
                                       C.c_int),
+            "sdmk_host_shard_bounds": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, ip, C.c_int64, ip, C.c_int,
+                                        P(C.c_int64)], C.c_int),
             "sdmk_host_shard_plan": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, ip, C.c_int64, ip, C.c_int,
                                       C.c_int, P(C.c_int64)], C.c_int),
         }
@@ -582,4 +584,18 @@ def host_build_window(window, c: float = 0.0, sigma: float = 0.0) -> dict:
     lib().sdmk_host_build_window(w, float(c), float(sigma), _dptr(sc), _dptr(co), n)
     return {"lambda0": sc[0], "norm_r": sc[1], "trunc_error": sc[2], "psi0": sc[3], "chi0": sc[4],
             "legendre_coeffs": co[:n]}
+
+
+def host_shard_bounds(dim, periodic, n_s, p, q_src_sorted, nranks, q_tgt_sorted=None) -> np.ndarray:
+    """Every rank's owned range of sorted targets (nranks + 1 bounds; host topology, no GPU)."""
+    qs = np.ascontiguousarray(np.asarray(q_src_sorted, np.int32).T.ravel())
+    ns = np.asarray(q_src_sorted).shape[0]
+    if q_tgt_sorted is not None and np.asarray(q_tgt_sorted).size:
+        qt = np.ascontiguousarray(np.asarray(q_tgt_sorted, np.int32).T.ravel())
+        nt = np.asarray(q_tgt_sorted).shape[0]
+    else:
+        qt, nt = None, 0
+    out = (C.c_int64 * (int(nranks) + 1))()
+    _raise(lib().sdmk_host_shard_bounds(dim, int(periodic), n_s, p, ns, _iptr(qs), nt, _iptr(qt), int(nranks), out))
+    return np.array(out[:], dtype=np.int64)
 

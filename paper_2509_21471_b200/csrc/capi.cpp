@@ -536,6 +536,17 @@ int sdmk_host_shard_plan(int dim, int periodic, int n_s, int p, int64_t ns, cons
   });
 }
 
+int sdmk_host_shard_bounds(int dim, int periodic, int n_s, int p, int64_t ns, const int32_t* qs, int64_t nt,
+                           const int32_t* qt, int nranks, int64_t* out) {
+  return guarded([&] {
+    if (nranks < 1) throw InvalidArgument("shard bounds: need nranks >= 1");
+    HostTree t = build_topology(dim, periodic != 0, n_s, p, (int)ns, qs, (int)nt, qt);
+    ShardCosts costs = shard_costs(t);
+    std::vector<int64_t> b = shard_bounds(t, nranks, costs);
+    std::copy(b.begin(), b.end(), out);
+  });
+}
+
 int sdmk_host_halo_plan(int dim, int periodic, int n_s, int p, int64_t ns, const int32_t* qs, int64_t nt,
                         const int32_t* qt, int nranks, int64_t* out) {
   return guarded([&] {

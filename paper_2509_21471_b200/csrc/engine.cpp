@@ -846,6 +846,17 @@ void Context::upload_tree_lists_b() {
   const auto hb2 = std::chrono::steady_clock::now();
   pr.t_own0 = sp.t0;
   pr.t_own1 = sp.t1;
+  pr.t_bounds.clear();
+  if (nranks_ > 1 && comm_) {
+    pr.t_bounds = shard_bounds(t, nranks_, costs);
+    if (pr.t_bounds[rank_] != sp.t0 || pr.t_bounds[rank_ + 1] != sp.t1)
+      throw RuntimeError("shard bounds disagree with the shard plan");
+    int64_t* hb = (int64_t*)pinned_.get("t_bounds", sizeof(int64_t) * (nranks_ + 1));
+    std::copy(pr.t_bounds.begin(), pr.t_bounds.end(), hb);
+    pr.d_bounds = arena_.as<int64_t>("t_bounds", nranks_ + 1);
+    cuda_check(cudaMemcpyAsync(pr.d_bounds, hb, sizeof(int64_t) * (nranks_ + 1), cudaMemcpyHostToDevice, st_),
+               "bounds upload");
+  }
   // near ranges per target leaf (dmk.cpp:966-990); two-pass CSR, parallel over leaves
   auto scode = [](const int8_t* s) { return (s[0] + 1) + 3 * (s[1] + 1) + 9 * (s[2] + 1); };
   auto ranges = [&](int b, int* obox, int* oinfo) {
@@ -1486,9 +1497,21 @@ void Context::evaluate_end(double* u, sdmk_report* rep) {
   double* du = device_ptrs ? u : arena_.as<double>("u", (size_t)ntt * dim);
   launch_combine(ntt, dim, ufar, ures, corr, corr_scale, zm, pr.tpts_caller, own, du, st_);
   ++launches_;
-  // with a communicator every rank returns the assembled u (each element has
-  // one owner; the others add exact zeros)
-  if (comm_ && nranks_ > 1) comm_->allreduce_sum(du, (size_t)ntt * dim, st_);
+  // with a communicator every rank returns the assembled u: each rank's owned
+  // Morton range of targets is packed in sorted order, all-gathered (padded
+  // to the longest range), and scattered to caller order on every rank --
+  // (R-1)/R of u moved per rank instead of the ~2x of an all-reduce
+  if (comm_ && nranks_ > 1) {
+    const std::vector<int64_t>& b = pr.t_bounds;
+    int64_t maxc = 1;
+    for (int r = 0; r < nranks_; ++r) maxc = std::max<int64_t>(maxc, b[r + 1] - b[r]);
+    double* snd = arena_.as<double>("ag_send", (size_t)maxc * dim);
+    double* rcv = arena_.as<double>("ag_recv", (size_t)nranks_ * maxc * dim);
+    launch_pack_owned(pr.t_own0, pr.t_own1 - pr.t_own0, dim, pr.tperm, du, snd, st_);
+    comm_->allgather(snd, rcv, (size_t)maxc * dim, st_);
+    launch_scatter_ranges(ntt, dim, pr.d_bounds, nranks_, maxc * dim, pr.tperm, rcv, du, st_);
+    launches_ += 2;
+  }
   cudaEventRecord(ev_[6], st_);
   if (!device_ptrs) copy_out(u, du, sizeof(double) * ntt * dim);
   cudaEventRecord(ev_[7], st_);

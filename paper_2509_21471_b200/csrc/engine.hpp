@@ -79,6 +79,8 @@ struct Problem {
   int n_ant = 0, n_int = 0;
   int *rng_start = nullptr, *rng_box = nullptr, *rng_info = nullptr, *subrange = nullptr;
   int64_t t_own0 = 0, t_own1 = 0;  // owned range of Morton-sorted targets (set_shard)
+  std::vector<int64_t> t_bounds;   // every rank's owned range (nranks + 1), for the u all-gather
+  int64_t* d_bounds = nullptr;
   // distributed upward pass (multi-GPU with an exchange): each rank forms the
   // outgoing expansions of its own cut subtrees, receives the halo it reads
   // and every cut box, and merges the boxes above the cut itself

@@ -24,6 +24,7 @@ struct Nccl {
   decltype(&ncclSend) Send = nullptr;
   decltype(&ncclRecv) Recv = nullptr;
   decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
 };
 
 const Nccl& nccl() {
@@ -51,6 +52,7 @@ const Nccl& nccl() {
     n.Send = (decltype(n.Send))sym("ncclSend");
     n.Recv = (decltype(n.Recv))sym("ncclRecv");
     n.AllReduce = (decltype(n.AllReduce))sym("ncclAllReduce");
+    n.AllGather = (decltype(n.AllGather))sym("ncclAllGather");
   });
   if (!err.empty()) throw RuntimeError(err);
   return n;
@@ -99,6 +101,10 @@ void Comm::exchange(const double* send, const std::vector<int64_t>& so, double* 
 
 void Comm::allreduce_sum(double* buf, size_t count, cudaStream_t st) {
   check(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)comm_, st), "ncclAllReduce");
+}
+
+void Comm::allgather(const double* send, double* recv, size_t count, cudaStream_t st) {
+  check(nccl().AllGather(send, recv, count, ncclFloat64, (ncclComm_t)comm_, st), "ncclAllGather");
 }
 
 }  // namespace sdmkb

@@ -29,6 +29,8 @@ class Comm {
   void exchange(const double* send, const std::vector<int64_t>& send_off, double* recv,
                 const std::vector<int64_t>& recv_off, cudaStream_t st);
   void allreduce_sum(double* buf, size_t count, cudaStream_t st);
+  // recv[r * count + i] = rank r's send[i]
+  void allgather(const double* send, double* recv, size_t count, cudaStream_t st);
 
  private:
   void* comm_ = nullptr;

@@ -771,6 +771,32 @@ ShardPlan shard_plan(const HostTree& t, int rank, int nranks, const ShardCosts* 
   return sp;
 }
 
+std::vector<int64_t> shard_bounds(const HostTree& t, int nranks, const ShardCosts& costs) {
+  if (nranks < 1) nranks = 1;
+  std::vector<int64_t> lo(nranks, -1), hi(nranks, -1);
+  int64_t start = 0;
+  for (size_t i = 0; i < costs.leaves.size(); ++i) {  // the owner rule of shard_plan
+    const int b = costs.leaves[i];
+    const int64_t n = costs.w[i];
+    const int owner =
+        nranks == 1 ? 0 : (int)std::min<int64_t>(nranks - 1, ((2 * start + n) * nranks) / (2 * costs.total));
+    if (lo[owner] < 0) lo[owner] = t.boxes[b].tb;
+    hi[owner] = t.boxes[b].te;
+    start += n;
+  }
+  std::vector<int64_t> bounds(nranks + 1, 0);
+  int64_t at = 0;
+  for (int r = 0; r < nranks; ++r) {
+    if (lo[r] >= 0) {
+      if (lo[r] != at) throw RuntimeError("shard_bounds: owned target ranges do not tile the targets");
+      at = hi[r];
+    }
+    bounds[r + 1] = at;
+  }
+  if (at != t.ntgt(0)) throw RuntimeError("shard_bounds: owned target ranges do not cover the targets");
+  return bounds;
+}
+
 HaloPlan halo_owners(const HostTree& t, int nranks) {
   HaloPlan h;
   h.nranks = nranks < 1 ? 1 : nranks;

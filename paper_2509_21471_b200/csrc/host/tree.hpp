@@ -126,6 +126,10 @@ struct ShardCosts {
 };
 ShardCosts shard_costs(const HostTree& t);  // needs the neighbour lists
 ShardPlan shard_plan(const HostTree& t, int rank, int nranks, const ShardCosts* costs = nullptr);
+// the owned ranges of all ranks at once: rank r owns sorted targets
+// [bounds[r], bounds[r + 1]) (the same ranges shard_plan gives; they tile
+// [0, nt) in rank order, an empty rank has bounds[r] == bounds[r + 1])
+std::vector<int64_t> shard_bounds(const HostTree& t, int nranks, const ShardCosts& costs);
 
 // Source ownership for the distributed upward pass.
 // The cut: starting from the root, every non-leaf box holding more than

@@ -80,6 +80,32 @@ __global__ void k_own_mask(int nt, const int* __restrict__ tperm, int64_t t0, in
     own[tperm[s]] = (s >= t0 && s < t1) ? 1 : 0;
 }
 
+// All-gather of the owned target ranges (multi-GPU): pack this rank's rows
+// in sorted order, then every rank scatters all ranks' rows to caller order.
+__global__ void k_pack_owned(int64_t t0, int64_t n, int dim, const int* __restrict__ tperm,
+                             const double* __restrict__ u, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * dim; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = t0 + i / dim;
+    out[i] = u[(int64_t)tperm[s] * dim + i % dim];
+  }
+}
+
+__global__ void k_scatter_ranges(int nt, int dim, const int64_t* __restrict__ bounds, int nranks, int64_t stride,
+                                 const int* __restrict__ tperm, const double* __restrict__ in,
+                                 double* __restrict__ u) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)nt * dim;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = i / dim;
+    int lo = 0, hi = nranks - 1;  // the rank r with bounds[r] <= s < bounds[r + 1]
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (bounds[mid] <= s) lo = mid;
+      else hi = mid - 1;
+    }
+    u[(int64_t)tperm[s] * dim + i % dim] = in[lo * stride + (s - bounds[lo]) * dim + i % dim];
+  }
+}
+
 // Halo pack / unpack of whole boxes: dst box i = src box i, where a null
 // id list means the boxes are contiguous from 0.  One CTA per box, a
 // grid-stride over its elements (coalesced; the halo is a few % of the proxies).
@@ -118,6 +144,20 @@ void launch_combine(int nt, int dim, const double* ufar, const double* ures, con
   int64_t g = (n + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
   k_combine<<<(int)(g < 1 ? 1 : g), 256, 0, st>>>(nt, dim, ufar, ures, corr, cs, zm, tpts_caller, own, u);
+}
+
+void launch_pack_owned(int64_t t0, int64_t n, int dim, const int* tperm, const double* u, double* out, cudaStream_t st) {
+  if (n <= 0) return;
+  int64_t g = (n * dim + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  k_pack_owned<<<(int)g, 256, 0, st>>>(t0, n, dim, tperm, u, out);
+}
+
+void launch_scatter_ranges(int nt, int dim, const int64_t* bounds, int nranks, int64_t stride, const int* tperm,
+                           const double* in, double* u, cudaStream_t st) {
+  int64_t g = ((int64_t)nt * dim + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  k_scatter_ranges<<<(int)(g < 1 ? 1 : g), 256, 0, st>>>(nt, dim, bounds, nranks, stride, tperm, in, u);
 }
 
 void launch_own_mask(int nt, const int* tperm, int64_t t0, int64_t t1, unsigned char* own, cudaStream_t st) {

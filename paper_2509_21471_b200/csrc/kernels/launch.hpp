@@ -197,6 +197,11 @@ void launch_combine(int nt, int dim, const double* ufar, const double* ures, con
                     cudaStream_t st);
 // own[tperm[s]] = (t0 <= s < t1): the caller-order mask of a shard's targets
 void launch_own_mask(int nt, const int* tperm, int64_t t0, int64_t t1, unsigned char* own, cudaStream_t st);
+// out[i][j] = u[tperm[t0 + i]][j], i < n: this rank's owned targets in sorted order
+void launch_pack_owned(int64_t t0, int64_t n, int dim, const int* tperm, const double* u, double* out, cudaStream_t st);
+// u[tperm[s]][j] = in[r * stride + (s - bounds[r]) * dim + j] for the rank r owning sorted target s
+void launch_scatter_ranges(int nt, int dim, const int64_t* bounds, int nranks, int64_t stride, const int* tperm,
+                           const double* in, double* u, cudaStream_t st);
 // dst box (dst_ids ? dst_ids[i] : i) = src box (src_ids ? src_ids[i] : i), boxes of `elems` doubles
 void launch_copy_boxes(int n, const int* src_ids, const double* src, const int* dst_ids, double* dst, int64_t elems,
                        cudaStream_t st);

@@ -45,6 +45,20 @@ def test_shard_plan_tiles_targets(nranks):
         assert plans[0]["owned_leaves"] == plans[0]["target_leaves"]
 
 
+@pytest.mark.parametrize("nranks", [1, 2, 3, 8])
+def test_shard_bounds_equal_per_rank_plans(nranks):
+    """sdmk_host_shard_bounds (the u all-gather layout) equals each rank's shard plan."""
+    qs = _points(20000, seed=4)
+    b = g.host_shard_bounds(3, False, 300, 10, qs, nranks)
+    assert b[0] == 0 and b[-1] == qs.shape[0] and np.all(np.diff(b) >= 0)
+    for r in range(nranks):
+        p = g.host_shard_plan(3, False, 300, 10, qs, r, nranks)
+        if p["t1"] > p["t0"]:
+            assert (b[r], b[r + 1]) == (p["t0"], p["t1"])
+        else:
+            assert b[r] == b[r + 1]
+
+
 def test_shard_plan_rejects_bad_rank():
     qs = _points(1000)
     with pytest.raises(ValueError):
@@ -70,6 +84,24 @@ def _worker(rank, world, port, qs, out_q):
     part = torch.zeros_like(full)
     part[plan["t0"]:plan["t1"]] = full[plan["t0"]:plan["t1"]]
     dist.all_reduce(part, op=dist.ReduceOp.SUM)
+    # the library's assembly (engine.cpp evaluate_end): pack the owned sorted
+    # rows, all-gather them padded to the longest range, scatter to caller
+    # order through the target permutation (here a random one)
+    bounds = g.host_shard_bounds(3, False, 300, 10, qs, world)
+    perm = torch.from_numpy(np.random.default_rng(9).permutation(n))
+    caller = torch.empty_like(full)
+    caller[perm] = full  # u in caller order: caller[perm[s]] = sorted row s
+    maxc = int(max(bounds[r + 1] - bounds[r] for r in range(world)))
+    snd = torch.zeros(maxc, 3, dtype=torch.float64)
+    t0, t1 = int(bounds[rank]), int(bounds[rank + 1])
+    snd[: t1 - t0] = caller[perm[t0:t1]]
+    rcv = [torch.empty_like(snd) for _ in range(world)]
+    dist.all_gather(rcv, snd)
+    out = torch.full_like(full, float("nan"))
+    for r in range(world):
+        a, b = int(bounds[r]), int(bounds[r + 1])
+        out[perm[a:b]] = rcv[r][: b - a]
+    ok_ag = bool(torch.equal(out, caller)) and t0 == plan["t0"] and t1 == plan["t1"]
     # the halo exchange plan of the distributed upward pass: the same on both
     # processes, and its send / receive sizes pair up in an all-to-all (the
     # shape of the library's NCCL group of sends and receives)
@@ -83,7 +115,7 @@ def _worker(rank, world, port, qs, out_q):
     dist.all_to_all_single(got, payload, output_split_sizes=recv, input_split_sizes=send)
     ok_x = hs[0] == hs[1] and bool((got == float(2 - rank)).all()) and sum(recv) > 0
     if rank == 0:
-        out_q.put((plans, bool(torch.equal(part, full)) and ok_x))
+        out_q.put((plans, bool(torch.equal(part, full)) and ok_x and ok_ag))
     dist.barrier()
     dist.destroy_process_group()
 
