@@ -7,7 +7,8 @@ exact device work that rank does in an R-GPU run (tree, its cut subtrees,
 halo pack/unpack, the boxes above the cut, its shard of the downward /
 far-field / residual passes), timed with CUDA events on the library stream.
 The NCCL transfers are NOT run; their bytes are reported and costed at an
-assumed NVLink rate (--link-gbs) together with the all-reduce of u.  The
+assumed NVLink rate (--link-gbs) together with the all-gather of u (each
+rank receives the other ranks' owned ranges, (R-1)/R of u).  The
 projection is max over ranks of (device time + transfer estimate), and
 "overlap" credits the library's schedule, where the halo exchange runs on a
 side stream beside the residual pass; it is a model, not a multi-GPU
@@ -69,10 +70,10 @@ def main():
                 ctx.evaluate_end(rr, d_u=du.data_ptr())
             u_bytes = n * 3 * 8
             halo_s = rr["halo_bytes_recv"] / (a.link_gbs * 1e9)
-            u_s = 2 * u_bytes * (R - 1) / R / (a.link_gbs * 1e9)
+            u_s = u_bytes * (R - 1) / R / (a.link_gbs * 1e9)  # all-gather of the owned ranges
             xfer = halo_s + u_s
             # with a communicator the halo exchange runs beside the residual pass
-            # (engine.cpp evaluate: side stream, residual first); u's all-reduce cannot
+            # (engine.cpp evaluate: side stream, residual first); u's all-gather cannot
             hidden = max(0.0, halo_s - rr["t_residual"]) + u_s
             rows.append({"rank": r, "dev_ms": rr["t_total"] * 1e3, "tree_ms": rr["t_tree"] * 1e3,
                          "upward_ms": rr["t_upward"] * 1e3, "root_ms": rr["t_root"] * 1e3, "pack_unpack_ms": rr["t_exchange"] * 1e3,
