@@ -719,6 +719,195 @@ __global__ void __launch_bounds__(kWI * 32, 1) k_inv_xy2(PWGrid g, const int* __
   }
 }
 
+// inv_xy, warp-independent form (3D, p <= 24, N <= 33).  The unit of work is
+// one (box, component, z-slab); every warp walks units with a global stride
+// and needs no CTA barrier: its slab of C1 (the compressed (my, m0) row of
+// one iz) arrives by cp.async, double buffered, scattered into a dense
+// (my, m0) tile; the Hermitian-split Y stage reads U = C[+my] + C[-my],
+// V = C[+my] - C[-my] straight from that tile at fragment-load time
+//   d.re = C0.re + [Er | Ei] [Ur ; Vi],  d.im = C0.im + [Er | -Ei] [Ui ; Vr]
+// (all PT x MT output tiles at once: the A and B fragments of a k-step are
+// loaded once for 2 PT MT DMMAs), the m0 = 0 column on the CUDA cores, and
+// the X stage with all PT x PT tiles of the slab register-blocked
+//   out[iy, ix] += pf sum_(m0, part) d[iy][(m0, part)] EXw[ix][(m0, part)]
+// (the output slab is read at the start of the unit).  Dense-tile rows have a
+// stride == 2 mod 8 complex, so the 16-byte B-fragment loads of a quarter
+// warp hit distinct bank groups.
+constexpr int kWI3 = 7;  // warps per CTA (shared memory: ~29 KB per warp)
+
+__host__ __device__ constexpr int r2c(int x) { return (x + 5) / 8 * 8 + 2; }  // >= x, == 2 mod 8
+
+template <int PC, int NC>
+__global__ void __launch_bounds__(kWI3 * 32, 1) k_inv_xy3(PWGrid g, const int* __restrict__ tboxes, int ntb, int d,
+                                                         const double2* __restrict__ C, double pf,
+                                                         double* __restrict__ incoming) {
+  constexpr int PT = 3, MTC = 2, P8 = PT * 8;
+  const int p = PC > 0 ? PC : g.p, N = NC > 0 ? NC : g.N, M = (N - 1) / 2, ncol = g.ncol, pp = p * p;
+  const int M1 = M + 1, M8 = MTC * 8, K2 = 2 * M8;
+  const int SA2 = r4(K2);                // A' rows (iy), == 4 mod 8
+  const int NXK = (2 * M1 + 3) / 4 * 4;  // X-stage K
+  const int SX = r4(NXK);
+  const int SD = r2c(M1);                // dense tile row stride (complex)
+  extern __shared__ double sm[];
+  double* Are = sm;                      // [P8][SA2]  [Er | Ei]
+  double* Aim = Are + P8 * SA2;          // [P8][SA2]  [Er | -Ei]
+  double* EXw = Aim + P8 * SA2;          // [P8 (ix)][SX]
+  int* dix = reinterpret_cast<int*>(EXw + P8 * SX);  // [ncol], padded to 16 bytes
+  double* wbase = EXw + P8 * SX + (ncol + 3) / 4 * 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
+  const size_t per_warp = 2 * (size_t)N * SD * 2 + (size_t)P8 * SX;  // doubles
+  double2* den = reinterpret_cast<double2*>(wbase + warp * per_warp);  // [2][N][SD]
+  double* dd = wbase + warp * per_warp + 2 * (size_t)N * SD * 2;       // [P8][SX]
+  for (int e = tid; e < P8 * SA2; e += blockDim.x) {
+    const int iy = e / SA2, k = e % SA2;
+    double vr = 0.0, vi = 0.0;
+    if (iy < p && k < K2) {
+      const int myp = k < M8 ? k : k - M8;
+      if (myp < M) {
+        const double2 ev = g.E[(size_t)(myp + 1 + M) * p + iy];
+        vr = k < M8 ? ev.x : ev.y;
+        vi = k < M8 ? ev.x : -ev.y;
+      }
+    }
+    Are[e] = vr;
+    Aim[e] = vi;
+  }
+  for (int e = tid; e < P8 * SX; e += blockDim.x) {  // Re(conj(E) d) = Er d.re + Ei d.im, weight 1 | 2
+    const int ix = e / SX, k = e % SX, m0 = k >> 1, part = k & 1;
+    double v = 0.0;
+    if (ix < p && m0 < M1) {
+      const double2 ev = g.E[(size_t)(m0 + M) * p + ix];
+      v = (m0 ? 2.0 : 1.0) * (part ? ev.y : ev.x);
+    }
+    EXw[e] = v;
+  }
+  for (int c = tid; c < ncol; c += blockDim.x) dix[c] = (g.col_my[c] + M) * SD + g.col_m0[c];
+  for (size_t e = lane; e < per_warp; e += 32) wbase[warp * per_warp + e] = 0.0;  // out-of-band entries stay 0
+  __syncthreads();
+  const int total = ntb * d * p;
+  const int nw = gridDim.x * kWI3;
+  auto issue = [&](int u, int buf) {
+    const int item = u / p, iz = u % p;
+    const double2* src = C + ((size_t)item * g.pz + iz) * ncol;
+    double2* dst = den + buf * N * SD;
+    for (int c = lane; c < ncol; c += 32) dev::cp_async16(dst + dix[c], src + c);
+    cp_commit();
+  };
+  int u = blockIdx.x * kWI3 + warp;
+  if (u < total) issue(u, 0);
+  for (int k = 0; u < total; ++k, u += nw) {
+    const int buf = k & 1;
+    if (u + nw < total) {
+      issue(u + nw, buf ^ 1);
+      cp_wait1();
+    } else {
+      cp_wait0();
+    }
+    __syncwarp();
+    const int item = u / p, iz = u % p, tb = item / d, j = item % d;
+    double* out = incoming + ((size_t)tboxes[tb] * d + j) * (size_t)(p * pp) + (size_t)iz * pp;
+    // the output slab's current values (read early; added to at the end)
+    double o[PT][PT][2];
+#pragma unroll
+    for (int mt = 0; mt < PT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < PT; ++nt) {
+        const int iy = mt * 8 + gq, ix = nt * 8 + 2 * t;
+        o[mt][nt][0] = (iy < p && ix < p) ? out[iy * p + ix] : 0.0;
+        o[mt][nt][1] = (iy < p && ix + 1 < p) ? out[iy * p + ix + 1] : 0.0;
+      }
+    const double2* D = den + buf * N * SD;
+    // m0 = 0 column (CUDA cores): lane = iy
+    if (lane < p) {
+      double re = D[M * SD].x, im = D[M * SD].y;
+      for (int r = 0; r < M; ++r) {
+        const double2 cp = D[(r + 1 + M) * SD], cm = D[(M - 1 - r) * SD];
+        const double er = Are[lane * SA2 + r], ei = Are[lane * SA2 + M8 + r];
+        re = fma(er, cp.x + cm.x, fma(ei, cp.y - cm.y, re));
+        im = fma(er, cp.y + cm.y, fma(-ei, cp.x - cm.x, im));
+      }
+      dd[lane * SX] = re;
+      dd[lane * SX + 1] = im;
+    }
+    // Y stage: all PT x MT tiles, re and im
+    double yr[PT][MTC][2], yi[PT][MTC][2];
+#pragma unroll
+    for (int a = 0; a < PT; ++a)
+#pragma unroll
+      for (int b = 0; b < MTC; ++b) yr[a][b][0] = yr[a][b][1] = yi[a][b][0] = yi[a][b][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < K2 / 4; ++ks) {
+      const int kk = ks * 4 + t;
+      const bool vpart = kk >= M8;
+      const int r = vpart ? kk - M8 : kk;  // my - 1
+      double bre[MTC], bim[MTC];
+#pragma unroll
+      for (int nt = 0; nt < MTC; ++nt) {
+        const int m0 = nt * 8 + gq + 1;
+        double2 cp = make_double2(0.0, 0.0), cm = cp;
+        if (r < M && m0 <= M) {
+          cp = D[(r + 1 + M) * SD + m0];
+          cm = D[(M - 1 - r) * SD + m0];
+        }
+        bre[nt] = vpart ? cp.y - cm.y : cp.x + cm.x;  // Vi | Ur
+        bim[nt] = vpart ? cp.x - cm.x : cp.y + cm.y;  // Vr | Ui
+      }
+#pragma unroll
+      for (int it = 0; it < PT; ++it) {
+        const double are = Are[(it * 8 + gq) * SA2 + kk], aim = Aim[(it * 8 + gq) * SA2 + kk];
+#pragma unroll
+        for (int nt = 0; nt < MTC; ++nt) {
+          dmma(yr[it][nt][0], yr[it][nt][1], are, bre[nt]);
+          dmma(yi[it][nt][0], yi[it][nt][1], aim, bim[nt]);
+        }
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < PT; ++it)
+#pragma unroll
+      for (int nt = 0; nt < MTC; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int m0 = nt * 8 + 2 * t + e + 1, row = it * 8 + gq;
+          if (m0 <= M) {
+            const double2 c0 = D[M * SD + m0];
+            dd[row * SX + 2 * m0] = yr[it][nt][e] + c0.x;
+            dd[row * SX + 2 * m0 + 1] = yi[it][nt][e] + c0.y;
+          }
+        }
+    __syncwarp();
+    // X stage: all PT x PT tiles of the slab
+    double x[PT][PT][2];
+#pragma unroll
+    for (int a = 0; a < PT; ++a)
+#pragma unroll
+      for (int b = 0; b < PT; ++b) x[a][b][0] = x[a][b][1] = 0.0;
+    for (int ks = 0; ks < NXK / 4; ++ks) {
+      double av[PT], bv[PT];
+#pragma unroll
+      for (int a = 0; a < PT; ++a) {
+        av[a] = dd[(a * 8 + gq) * SX + ks * 4 + t];
+        bv[a] = EXw[(a * 8 + gq) * SX + ks * 4 + t];
+      }
+#pragma unroll
+      for (int a = 0; a < PT; ++a)
+#pragma unroll
+        for (int b = 0; b < PT; ++b) dmma(x[a][b][0], x[a][b][1], av[a], bv[b]);
+    }
+#pragma unroll
+    for (int mt = 0; mt < PT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < PT; ++nt) {
+        const int iy = mt * 8 + gq, ix = nt * 8 + 2 * t;
+        if (iy < p) {
+          if (ix < p) out[iy * p + ix] = o[mt][nt][0] + pf * x[mt][nt][0];
+          if (ix + 1 < p) out[iy * p + ix + 1] = o[mt][nt][1] + pf * x[mt][nt][1];
+        }
+      }
+    __syncwarp();  // dd and this den buffer are rewritten by the next units
+  }
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -802,7 +991,22 @@ void launch_inverse_mma(const PWGrid& g, const int* tboxes, int ntb, int d, cons
     const size_t sm2 = sizeof(double) * (2 * (size_t)P8 * SA2 + (size_t)P8 * SX2 + 4 * (size_t)P8 * SX2 +
                                          2 * 4 * (size_t)K2 * SB) +
                        sizeof(double2) * 2 * 4 * (size_t)g.N * M1 + sizeof(int) * (size_t)g.ncol;
-    if (sm2 > 227 * 1024) {  // the split kernel stages dense slabs: too big for the largest grids
+    const int SD3 = r2c(M1), NXK3 = (2 * M1 + 3) / 4 * 4, SX3 = r4(NXK3);
+    const size_t sm3 = sizeof(double) * (2 * (size_t)P8 * r4(32) + (size_t)P8 * SX3 + (size_t)(g.ncol + 3) / 4 * 2 +
+                                         (size_t)kWI3 * (2 * (size_t)g.N * SD3 * 2 + (size_t)P8 * SX3));
+    if (PT == 3 && g.N <= 33 && sm3 <= 227 * 1024) {  // warp-independent slabs
+      const int units = ntb * d * g.p;
+      const int ctas = std::max(1, std::min(num_sms(), (units + kWI3 - 1) / kWI3));
+#define IX3(PC_, NC_)                                                                                        \
+  do {                                                                                                       \
+    attr((const void*)k_inv_xy3<PC_, NC_>, sm3);                                                             \
+    k_inv_xy3<PC_, NC_><<<ctas, kWI3 * 32, sm3, st>>>(g, tboxes, ntb, d, C, pf, incoming);                   \
+  } while (0)
+      if (g.p == 23 && g.N == 33) IX3(23, 33);
+      else if (g.p == 22 && g.N == 33) IX3(22, 33);
+      else IX3(0, 0);
+#undef IX3
+    } else if (sm2 > 227 * 1024) {  // the split kernel stages dense slabs: too big for the largest grids
       const int M18 = (M1 + 7) / 8 * 8, NY8 = (g.N + 7) / 8 * 8, NX8 = (2 * M1 + 7) / 8 * 8;
       const int SA = r4(2 * NY8), SX = r4(NX8 > 2 * M18 ? NX8 : 2 * M18);
       const size_t smem = sizeof(double) * (2 * (size_t)P8 * SA + (size_t)P8 * SX + 4 * (size_t)P8 * SX +
