@@ -719,6 +719,191 @@ __global__ void __launch_bounds__(kWI * 32, 1) k_inv_xy2(PWGrid g, const int* __
   }
 }
 
+// fwd_xy, warp-independent form (3D, p <= 24, N <= 33): the unit of work is
+// one (box, channel, z-slab); every warp walks units with a global stride,
+// its w slab arriving by cp.async (double buffered), and needs no CTA
+// barrier.  X stage with all PT x NX tiles register-blocked (a k-step loads
+// PT + NX fragments for PT NX DMMAs), then the Hermitian-split Y stage
+// (P = Er ar, Q = Ei ai, R = Er ai, S = Ei ar; b[+-my] = (P -+ Q) + i (R +- S))
+// with all 2 x 2 tiles of the four products at once, the my = 0 row and the
+// m0 = 0 column on the CUDA cores, and the in-band columns stored to B.
+constexpr int kWF3 = 10;  // warps per CTA (shared memory: ~18 KB per warp)
+
+template <int PC, int NC>
+__global__ void __launch_bounds__(kWF3 * 32, 1) k_fwd_xy3(PWGrid g, const int* __restrict__ boxes, int nbox, int nch,
+                                                         const double* __restrict__ outgoing,
+                                                         double2* __restrict__ B) {
+  constexpr int PT = 3, MTC = 2, P8 = PT * 8, SE = P8 + 4, SY = P8 + 4, NXT = 5;  // NX8 = 40 columns
+  const int p = PC > 0 ? PC : g.p, N = NC > 0 ? NC : g.N, M = (N - 1) / 2, ncol = g.ncol, pp = p * p;
+  const int M1 = M + 1, M8 = MTC * 8, NX8 = NXT * 8;
+  constexpr int SA = 20;  // X outputs by (m0 - 1 | M for m0 = 0) in separate re / im arrays, == 4 mod 8
+  extern __shared__ double sm[];
+  double* EXT = sm;                   // [NX8][SE]
+  double* EYr = EXT + NX8 * SE;       // [M8][SY]  rows my - 1
+  double* EYi = EYr + M8 * SY;        // [M8][SY]
+  int* colidx = reinterpret_cast<int*>(EYi + M8 * SY);  // [N][M1]
+  double* wbase = EYi + M8 * SY + (N * M1 + 3) / 4 * 2;
+  constexpr int per_warp = 2 * P8 * SE + 2 * P8 * SA;  // doubles
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
+  double* win = wbase + warp * per_warp;  // [2][P8][SE]
+  double* ar = win + 2 * P8 * SE;         // [P8][SA]  X output, real parts
+  double* ai = ar + P8 * SA;              // [P8][SA]  imaginary parts
+  for (int e = tid; e < NX8 * SE; e += blockDim.x) {
+    const int n = e / SE, ix = e % SE;
+    double v = 0.0;
+    if (ix < p) {
+      if (n < 2 * M) {
+        const double2 ev = g.E[(size_t)(n / 2 + 1 + M) * p + ix];
+        v = (n & 1) ? ev.y : ev.x;
+      } else if (n == 2 * M) {
+        v = 1.0;
+      }
+    }
+    EXT[e] = v;
+  }
+  for (int e = tid; e < M8 * SY; e += blockDim.x) {
+    const int r = e / SY, iy = e % SY;
+    double vr = 0.0, vi = 0.0;
+    if (r < M && iy < p) {
+      const double2 ev = g.E[(size_t)(r + 1 + M) * p + iy];
+      vr = ev.x;
+      vi = ev.y;
+    }
+    EYr[e] = vr;
+    EYi[e] = vi;
+  }
+  for (int e = tid; e < N * M1; e += blockDim.x) colidx[e] = -1;
+  for (int e = lane; e < per_warp; e += 32) win[e] = 0.0;  // padding rows / columns stay 0
+  __syncthreads();
+  for (int c = tid; c < ncol; c += blockDim.x) colidx[(g.col_my[c] + M) * M1 + g.col_m0[c]] = c;
+  __syncthreads();
+  const int total = nbox * nch * p;
+  const int nw = gridDim.x * kWF3;
+  auto issue = [&](int u, int buf) {
+    const int item = u / p, iz = u % p;
+    const double* src = outgoing + ((size_t)boxes[item / nch] * nch + item % nch) * (size_t)(p * pp) + (size_t)iz * pp;
+    double* dst = win + buf * P8 * SE;
+    for (int e = lane; e < pp; e += 32) cp_async8(dst + (e / p) * SE + e % p, src + e, true);
+    cp_commit();
+  };
+  int u = blockIdx.x * kWF3 + warp;
+  if (u < total) issue(u, 0);
+  for (int k = 0; u < total; ++k, u += nw) {
+    const int buf = k & 1;
+    if (u + nw < total) {
+      issue(u + nw, buf ^ 1);
+      cp_wait1();
+    } else {
+      cp_wait0();
+    }
+    __syncwarp();
+    const int item = u / p, iz = u % p;
+    double2* Bo = B + (size_t)item * g.pz * ncol + (size_t)iz * ncol;
+    const double* A = win + buf * P8 * SE;
+    // X stage: (ar + i ai)[iy][m0'] = sum_ix w[iy][ix] EXT[2 m0' + part][ix]
+    {
+      double c[PT][NXT][2];
+#pragma unroll
+      for (int i = 0; i < PT; ++i)
+#pragma unroll
+        for (int j = 0; j < NXT; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < PT * 2; ++ks) {
+        double av[PT], bv[NXT];
+#pragma unroll
+        for (int i = 0; i < PT; ++i) av[i] = A[(i * 8 + gq) * SE + ks * 4 + t];
+#pragma unroll
+        for (int j = 0; j < NXT; ++j) bv[j] = EXT[(j * 8 + gq) * SE + ks * 4 + t];
+#pragma unroll
+        for (int i = 0; i < PT; ++i)
+#pragma unroll
+          for (int j = 0; j < NXT; ++j) dmma(c[i][j][0], c[i][j][1], av[i], bv[j]);
+      }
+#pragma unroll
+      for (int i = 0; i < PT; ++i)
+#pragma unroll
+        for (int j = 0; j < NXT; ++j) {
+          ar[(i * 8 + gq) * SA + j * 4 + t] = c[i][j][0];
+          ai[(i * 8 + gq) * SA + j * 4 + t] = c[i][j][1];
+        }
+    }
+    __syncwarp();
+    auto put = [&](int my, int m0, double re, double im) {
+      const int c = colidx[(my + M) * M1 + m0];
+      if (c >= 0) Bo[c] = make_double2(re, im);
+    };
+    // Y stage (m0 >= 1, my >= 1)
+    {
+      double P[MTC][MTC][2], Q[MTC][MTC][2], R[MTC][MTC][2], S[MTC][MTC][2];
+#pragma unroll
+      for (int i = 0; i < MTC; ++i)
+#pragma unroll
+        for (int j = 0; j < MTC; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) P[i][j][e] = Q[i][j][e] = R[i][j][e] = S[i][j][e] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < PT * 2; ++ks) {
+        const int kk = ks * 4 + t;
+        double er[MTC], ei[MTC], br[MTC], bi[MTC];
+#pragma unroll
+        for (int i = 0; i < MTC; ++i) {
+          er[i] = EYr[(i * 8 + gq) * SY + kk];
+          ei[i] = EYi[(i * 8 + gq) * SY + kk];
+          br[i] = ar[kk * SA + i * 8 + gq];
+          bi[i] = ai[kk * SA + i * 8 + gq];
+        }
+#pragma unroll
+        for (int i = 0; i < MTC; ++i)
+#pragma unroll
+          for (int j = 0; j < MTC; ++j) {
+            dmma(P[i][j][0], P[i][j][1], er[i], br[j]);
+            dmma(Q[i][j][0], Q[i][j][1], ei[i], bi[j]);
+            dmma(R[i][j][0], R[i][j][1], er[i], bi[j]);
+            dmma(S[i][j][0], S[i][j][1], ei[i], br[j]);
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < MTC; ++i)
+#pragma unroll
+        for (int j = 0; j < MTC; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int my = i * 8 + gq + 1, m0 = j * 8 + 2 * t + e + 1;
+            if (my <= M && m0 <= M) {
+              const double p_ = P[i][j][e], q_ = Q[i][j][e], r_ = R[i][j][e], s_ = S[i][j][e];
+              put(my, m0, p_ - q_, r_ + s_);
+              put(-my, m0, p_ + q_, r_ - s_);
+            }
+          }
+    }
+    // remainders on the CUDA cores: the m0 = 0 column (my >= 1; a real) and the my = 0 row
+    if (lane < M) {
+      double P0 = 0.0, S0 = 0.0;
+      for (int iy = 0; iy < p; ++iy) {
+        const double a0 = ar[iy * SA + M];
+        P0 = fma(EYr[lane * SY + iy], a0, P0);
+        S0 = fma(EYi[lane * SY + iy], a0, S0);
+      }
+      put(lane + 1, 0, P0, S0);
+      put(-(lane + 1), 0, P0, -S0);
+    }
+    if (lane <= M) {
+      const int m0 = lane;
+      double re = 0.0, im = 0.0;
+      if (m0 == 0) {
+        for (int iy = 0; iy < p; ++iy) re += ar[iy * SA + M];
+      } else {
+        for (int iy = 0; iy < p; ++iy) {
+          re += ar[iy * SA + m0 - 1];
+          im += ai[iy * SA + m0 - 1];
+        }
+      }
+      put(0, m0, re, im);
+    }
+    __syncwarp();  // ar / ai and this w buffer are rewritten by the next units
+  }
+}
+
 // inv_xy, warp-independent form (3D, p <= 24, N <= 33).  The unit of work is
 // one (box, component, z-slab); every warp walks units with a global stride
 // and needs no CTA barrier: its slab of C1 (the compressed (my, m0) row of
@@ -938,6 +1123,21 @@ void launch_forward_mma(const PWGrid& g, const int* boxes, int nbox, int nch, co
     const size_t sm = sizeof(double) * ((size_t)NX8 * (P8 + 4) + 2 * (size_t)MT * 8 * (P8 + 4) +
                                         2 * 4 * (size_t)P8 * (P8 + 4) + 4 * (size_t)P8 * r8(NX8 > 16 * MT ? NX8 : 16 * MT)) +
                       sizeof(int) * (size_t)g.N * M1;
+    const size_t sm3 = sizeof(double) * (40 * 28 + 2 * 16 * 28 + (size_t)(g.N * M1 + 3) / 4 * 2 +
+                                         (size_t)kWF3 * (2 * 24 * 28 + 2 * 24 * 20));
+    if (PT == 3 && g.N <= 33 && g.dim == 3) {  // warp-independent slabs
+      const int units = nbox * nch * g.p;
+      const int ctas = std::max(1, std::min(num_sms(), (units + kWF3 - 1) / kWF3));
+#define FX3(PC_, NC_)                                                                                        \
+  do {                                                                                                       \
+    attr((const void*)k_fwd_xy3<PC_, NC_>, sm3);                                                             \
+    k_fwd_xy3<PC_, NC_><<<ctas, kWF3 * 32, sm3, st>>>(g, boxes, nbox, nch, outgoing, B);                     \
+  } while (0)
+      if (g.p == 23 && g.N == 33) FX3(23, 33);
+      else if (g.p == 22 && g.N == 33) FX3(22, 33);
+      else FX3(0, 0);
+#undef FX3
+    } else {
 #define FX2(PT_, PC_, NC_)                                                                                    \
   do {                                                                                                        \
     attr((const void*)k_fwd_xy2<PT_, PC_, NC_>, sm);                                                          \
@@ -950,6 +1150,7 @@ void launch_forward_mma(const PWGrid& g, const int* boxes, int nbox, int nch, co
     else if (PT <= 3) FX2(3, 0, 0);
     else FX2(4, 0, 0);
 #undef FX2
+    }
   }
   {  // z stage: G[box][ch][mode]
     const int SI = (2 * kCB) % 16 == 8 ? 2 * kCB : 2 * kCB + 8;
