@@ -409,6 +409,223 @@ __global__ void __launch_bounds__(kW * 32, 2) k_zi2(PWGrid g, int nc, int nbox, 
   }
 }
 
+// z stages, warp-independent forms (PT = 3, Mz <= 16): the unit of work is
+// one (box, channel, 16-column block); every warp walks units with a global
+// stride, its input block arriving by cp.async (double buffered), and does
+// all 2 x 2 (forward) / 3 x 2 (inverse) output tiles of the block at once,
+// so each k-step's fragments feed 12-16 DMMAs.  Block rows have a stride
+// == 2 mod 8 complex (16-byte fragment loads of a quarter warp hit distinct
+// bank groups).
+constexpr int kZB = 16;           // columns per unit
+constexpr int kZR = kZB + 2;      // block row stride (complex)
+constexpr int kWZF = 12, kWZI = 10;  // warps per CTA
+
+__global__ void __launch_bounds__(kWZF * 32, 1) k_zf3(PWGrid g, int nc, int nbox, const double2* __restrict__ IN,
+                                                     double2* __restrict__ OUT) {
+  constexpr int PT = 3, P8 = PT * 8, SK = P8 + 4, MTC = 2;
+  extern __shared__ double sm[];
+  const int M = g.Mz, pz = g.pz, ncol = g.ncol;
+  double* Ar = sm;                 // [16][SK]  Er[mz = r + 1][iz]
+  double* Ai = Ar + 16 * SK;       // [16][SK]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
+  double2* Bs = reinterpret_cast<double2*>(Ai + 16 * SK) + (size_t)warp * 2 * P8 * kZR;  // [2][P8][kZR]
+  for (int e = tid; e < 16 * SK; e += blockDim.x) {
+    const int r = e / SK, k = e % SK;
+    double vr = 0.0, vi = 0.0;
+    if (r < M && k < pz) {
+      const double2 ev = g.Ez[(size_t)(r + 1 + M) * pz + k];
+      vr = ev.x;
+      vi = ev.y;
+    }
+    Ar[e] = vr;
+    Ai[e] = vi;
+  }
+  for (int e = lane; e < 2 * P8 * kZR; e += 32) Bs[e] = make_double2(0.0, 0.0);  // rows iz >= pz stay 0
+  __syncthreads();
+  const int ncbk = (ncol + kZB - 1) / kZB, total = nbox * nc * ncbk;
+  const int nw = gridDim.x * kWZF;
+  auto issue = [&](int u, int buf) {
+    const int bc = u / ncbk, c0 = (u % ncbk) * kZB, ncb = min(kZB, ncol - c0);
+    const double2* src = IN + (size_t)bc * pz * ncol + c0;
+    double2* dst = Bs + buf * P8 * kZR;
+    for (int e = lane; e < pz * kZB; e += 32) {
+      const int k = e / kZB, cc = e % kZB;
+      dev::cp_async16z(dst + k * kZR + cc, cc < ncb ? src + (size_t)k * ncol + cc : src, cc < ncb);
+    }
+    cp_commit();
+  };
+  int u = blockIdx.x * kWZF + warp;
+  if (u < total) issue(u, 0);
+  for (int it = 0; u < total; ++it, u += nw) {
+    const int buf = it & 1;
+    if (u + nw < total) {
+      issue(u + nw, buf ^ 1);
+      cp_wait1();
+    } else {
+      cp_wait0();
+    }
+    __syncwarp();
+    const double2* Bb = Bs + buf * P8 * kZR;
+    const int bc = u / ncbk, c0 = (u % ncbk) * kZB, ncb = min(kZB, ncol - c0);
+    double2* dst = OUT + (size_t)bc * g.nhalf;
+    double P[MTC][2][2], Q[MTC][2][2], R[MTC][2][2], S[MTC][2][2];
+#pragma unroll
+    for (int i = 0; i < MTC; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) P[i][j][e] = Q[i][j][e] = R[i][j][e] = S[i][j][e] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 2 * PT; ++ks) {
+      const int k = ks * 4 + t;
+      double er[MTC], ei[MTC];
+      double2 b[2];
+#pragma unroll
+      for (int i = 0; i < MTC; ++i) {
+        er[i] = Ar[(i * 8 + gq) * SK + k];
+        ei[i] = Ai[(i * 8 + gq) * SK + k];
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = Bb[k * kZR + j * 8 + gq];
+#pragma unroll
+      for (int i = 0; i < MTC; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma(P[i][j][0], P[i][j][1], er[i], b[j].x);
+          dmma(Q[i][j][0], Q[i][j][1], ei[i], b[j].y);
+          dmma(R[i][j][0], R[i][j][1], er[i], b[j].y);
+          dmma(S[i][j][0], S[i][j][1], ei[i], b[j].x);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < MTC; ++i) {
+      const int mz = i * 8 + gq + 1;
+      if (mz > M) continue;
+      const int np = g.slab_ncol[mz + M], nm = g.slab_ncol[M - mz];
+      const int op = g.slab_off[mz + M], om = g.slab_off[M - mz];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cc = j * 8 + 2 * t + e, col = c0 + cc;
+          if (cc >= ncb) continue;
+          const double p_ = P[i][j][e], q_ = Q[i][j][e], r_ = R[i][j][e], s_ = S[i][j][e];
+          if (col < np) dst[op + col] = make_double2(p_ - q_, r_ + s_);
+          if (col < nm) dst[om + col] = make_double2(p_ + q_, r_ - s_);
+        }
+    }
+    if (lane < ncb && c0 + lane < g.slab_ncol[M]) {  // mz = 0: column sums over iz
+      double re = 0.0, im = 0.0;
+      for (int k = 0; k < pz; ++k) {
+        re += Bb[k * kZR + lane].x;
+        im += Bb[k * kZR + lane].y;
+      }
+      dst[g.slab_off[M] + c0 + lane] = make_double2(re, im);
+    }
+    __syncwarp();  // this buffer is refilled by the issue two units ahead
+  }
+}
+
+__global__ void __launch_bounds__(kWZI * 32, 1) k_zi3(PWGrid g, int nc, int nbox, const double2* __restrict__ IN,
+                                                     double2* __restrict__ OUT) {
+  constexpr int PT = 3, P8 = PT * 8, M8 = 16, K2 = 2 * M8, SA = 36;  // SA = r4(K2)
+  extern __shared__ double sm[];
+  const int M = g.Mz, pz = g.pz, ncol = g.ncol, NZ = 2 * M + 1;
+  double* Are = sm;              // [P8][SA]  [Er | Ei]
+  double* Aim = Are + P8 * SA;   // [P8][SA]  [Er | -Ei]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
+  double2* Fs = reinterpret_cast<double2*>(Aim + P8 * SA) + (size_t)warp * 2 * 33 * kZR;  // [2][NZ <= 33][kZR]
+  for (int e = tid; e < P8 * SA; e += blockDim.x) {
+    const int iz = e / SA, k = e % SA;
+    double vr = 0.0, vi = 0.0;
+    if (iz < pz && k < K2) {
+      const int r = k < M8 ? k : k - M8;
+      if (r < M) {
+        const double2 ev = g.Ez[(size_t)(r + 1 + M) * pz + iz];
+        vr = k < M8 ? ev.x : ev.y;
+        vi = k < M8 ? ev.x : -ev.y;
+      }
+    }
+    Are[e] = vr;
+    Aim[e] = vi;
+  }
+  __syncthreads();
+  const int ncbk = (ncol + kZB - 1) / kZB, total = nbox * nc * ncbk;
+  const int nw = gridDim.x * kWZI;
+  auto issue = [&](int u, int buf) {
+    const int bc = u / ncbk, c0 = (u % ncbk) * kZB;
+    const double2* src = IN + (size_t)bc * g.nhalf;
+    double2* dst = Fs + buf * 33 * kZR;
+    for (int e = lane; e < NZ * kZB; e += 32) {  // F rows (mz + M): a contiguous prefix of the columns
+      const int s = e / kZB, cc = e % kZB;
+      const bool v = c0 + cc < g.slab_ncol[s];
+      dev::cp_async16z(dst + s * kZR + cc, v ? src + g.slab_off[s] + c0 + cc : src, v);
+    }
+    cp_commit();
+  };
+  int u = blockIdx.x * kWZI + warp;
+  if (u < total) issue(u, 0);
+  for (int it = 0; u < total; ++it, u += nw) {
+    const int buf = it & 1;
+    if (u + nw < total) {
+      issue(u + nw, buf ^ 1);
+      cp_wait1();
+    } else {
+      cp_wait0();
+    }
+    __syncwarp();
+    const double2* Fb = Fs + buf * 33 * kZR;
+    const int bc = u / ncbk, c0 = (u % ncbk) * kZB, ncb = min(kZB, ncol - c0);
+    double2* dst = OUT + (size_t)bc * pz * ncol;
+    double re[PT][2][2], im[PT][2][2];
+#pragma unroll
+    for (int i = 0; i < PT; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) re[i][j][0] = re[i][j][1] = im[i][j][0] = im[i][j][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < K2 / 4; ++ks) {
+      const int k = ks * 4 + t;
+      const bool vpart = k >= M8;
+      const int r = vpart ? k - M8 : k;  // mz - 1
+      double br[2], bi[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        double2 fp = make_double2(0.0, 0.0), fm = fp;
+        if (r < M) {
+          fp = Fb[(M + 1 + r) * kZR + j * 8 + gq];
+          fm = Fb[(M - 1 - r) * kZR + j * 8 + gq];
+        }
+        br[j] = vpart ? fp.y - fm.y : fp.x + fm.x;  // Vi | Ur
+        bi[j] = vpart ? fp.x - fm.x : fp.y + fm.y;  // Vr | Ui
+      }
+#pragma unroll
+      for (int i = 0; i < PT; ++i) {
+        const double ar = Are[(i * 8 + gq) * SA + k], ai = Aim[(i * 8 + gq) * SA + k];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma(re[i][j][0], re[i][j][1], ar, br[j]);
+          dmma(im[i][j][0], im[i][j][1], ai, bi[j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < PT; ++i) {
+      const int iz = i * 8 + gq;
+      if (iz >= pz) continue;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cc = j * 8 + 2 * t + e;
+          if (cc >= ncb) continue;
+          const double2 f0 = Fb[M * kZR + cc];
+          dst[(size_t)iz * ncol + c0 + cc] = make_double2(re[i][j][e] + f0.x, im[i][j][e] + f0.y);
+        }
+    }
+    __syncwarp();  // this buffer is refilled by the issue two units ahead
+  }
+}
+
 // ------------------------------------------------------------------ inv_xy --
 // 16 warps; the compressed C1 rows of the next four slabs arrive by cp.async
 // (double buffered) and feed the Y-stage B fragments directly through the
@@ -1152,7 +1369,13 @@ void launch_forward_mma(const PWGrid& g, const int* boxes, int nbox, int nch, co
 #undef FX2
     }
   }
-  {  // z stage: G[box][ch][mode]
+  if (PT == 3 && g.Mz <= 16) {  // z stage, warp-independent blocks
+    const size_t sz = sizeof(double) * 2 * 16 * 28 + sizeof(double2) * (size_t)kWZF * 2 * 24 * kZR;
+    const int units = nbox * nch * ((g.ncol + kZB - 1) / kZB);
+    const int ctas = std::max(1, std::min(num_sms(), (units + kWZF - 1) / kWZF));
+    attr((const void*)k_zf3, sz);
+    k_zf3<<<ctas, kWZF * 32, sz, st>>>(g, nch, nbox, B, G);
+  } else {  // z stage: G[box][ch][mode]
     const int SI = (2 * kCB) % 16 == 8 ? 2 * kCB : 2 * kCB + 8;
     const int M8 = (g.Mz + 7) / 8 * 8;
     const size_t sz = sizeof(double) * (2 * (size_t)M8 * (P8 + 4) + 2 * (size_t)P8 * SI);
@@ -1173,7 +1396,13 @@ void launch_inverse_mma(const PWGrid& g, const int* tboxes, int ntb, int d, cons
   if (ntb <= 0) return;
   const int PT = (g.p + 7) / 8 <= 3 ? 3 : 4;  // the instantiated template sizes
   const int P8 = PT * 8, M = g.M, M1 = M + 1, MT = (M + 7) / 8, M8 = MT * 8;
-  {  // z stage: C1[box][j][iz][col]
+  if (PT == 3 && g.Mz <= 16) {  // z stage, warp-independent blocks
+    const size_t sz = sizeof(double) * 2 * 24 * 36 + sizeof(double2) * (size_t)kWZI * 2 * 33 * kZR;
+    const int units = ntb * d * ((g.ncol + kZB - 1) / kZB);
+    const int ctas = std::max(1, std::min(num_sms(), (units + kWZI - 1) / kWZI));
+    attr((const void*)k_zi3, sz);
+    k_zi3<<<ctas, kWZI * 32, sz, st>>>(g, d, ntb, F, C);
+  } else {  // z stage: C1[box][j][iz][col]
     const int M8z = (g.Mz + 7) / 8 * 8;
     const size_t sz = sizeof(double) * 2 * (size_t)P8 * r4(2 * M8z) + sizeof(double2) * 2 * (size_t)g.Nz * (kCB + 2);
     const int items = ntb * d * ((g.ncol + kCB - 1) / kCB);
