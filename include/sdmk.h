@@ -34,6 +34,7 @@
  *   sdmk_pass_residual       stokesdmk::residual_pass         dmk.hpp:128-131
  *   sdmk_evaluate_with_tables  evaluate_with_plan(..., const SplitKernel* tables)  dmk.hpp:151-155
  *   sdmk_host_build_tables   stokesdmk::build_split_kernel    split.hpp:89-90, split.cpp:319-396
+ *   sdmk_ewald               (new: FFT Ewald for the periodic Stokeslet; ewald_reference's split, ewald.cpp:81-272)
  *   sdmk_direct_sum          stokesdmk::direct_sum            oracle.hpp:60-65, oracle.cpp:143-179
  *   sdmk_direct_residual_sum stokesdmk::direct_residual_sum   oracle.hpp:67-75, oracle.cpp:181-241
  *
@@ -212,6 +213,25 @@ int sdmk_host_window_eval(int window, double c, double sigma, const double* coef
 int sdmk_direct_residual_sum_tables(sdmk_context* ctx, const unsigned char* tables, int64_t nbytes, int dim,
                                     int64_t n_src, const double* src, int64_t n_tgt, const double* tgt,
                                     const double* str, double cutoff, int periodic, double* u);
+
+/* ---- FFT Ewald (no reference counterpart:
+   SPEC.md lists it as "noted but not built") ----
+   The periodic 3D Stokeslet sum by the single-level split of
+   ewald_reference (ewald.cpp:81-272) at scale nu = 2^-level instead of 1:
+   u = residual sum over pairs closer than nu (the residual kernel over each
+   cell's 27 periodic neighbour cells) + the mollified far field
+   sum_{kappa != 0} gamma^(|k| nu) / k^4 (k^2 f^ - k (k . f^)) e^{i k x}
+   (a prolate-window NUFFT on a uniform grid, cuFFT, opened at run time)
+   + the self term (targets aliased).  The plan supplies the window (c) and
+   tolerance; the zero mode is dropped as in periodic DMK (net force zero).
+   level < 0 chooses ~200 sources per cell.  Host (sdmk_ewald) or device
+   (sdmk_ewald_device) buffers, caller point order; n_tgt == 0 aliases.
+   info (8 doubles, may be NULL): level, grid points per axis, window width,
+   kappa_max, and times in ms (sort, local, far, total). */
+int sdmk_ewald(sdmk_context* ctx, const sdmk_plan* plan, int64_t n_src, const double* src, int64_t n_tgt,
+               const double* tgt, const double* str, double* u, int level, double* info);
+int sdmk_ewald_device(sdmk_context* ctx, const sdmk_plan* plan, int64_t n_src, const double* d_src, int64_t n_tgt,
+                      const double* d_tgt, const double* d_str, double* d_u, int level, double* info);
 
 /* ---- O(N*M) reference sums on the GPU ----
    Same per-target source order, Kahan accumulation and unfused expression

@@ -121,6 +121,9 @@ def lib():
                                           C.c_double, C.c_int, dp], C.c_int),
             "sdmk_host_halo_plan": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, ip, C.c_int64, ip, C.c_int,
                                      P(C.c_int64)], C.c_int),
+            "sdmk_ewald": ([C.c_void_p, P(sdmk_plan), C.c_int64, dp, C.c_int64, dp, dp, dp, C.c_int, dp], C.c_int),
+            "sdmk_ewald_device": ([C.c_void_p, P(sdmk_plan), C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_int, dp], C.c_int),
             "sdmk_host_build_tables": ([C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_char_p,
                                         C.c_int64], C.c_int64),
             "sdmk_host_build_window": ([C.c_int, C.c_double, C.c_double, dp, dp, C.c_int], C.c_int),
@@ -390,6 +393,23 @@ class Context:
         _raise(lib().sdmk_direct_residual_sum(self._h, C.byref(cp), d, ns, _dptr(src), nt,
                                               _dptr(tgt if nt else None), _dptr(stw), float(cutoff),
                                               1 if periodic else 0, _dptr(u)))
+        return u
+
+    def ewald(self, plan: DmkPlan, sys: ParticleSystem, level: int = -1, info: Optional[dict] = None) -> np.ndarray:
+        """FFT Ewald for the periodic 3D Stokeslet (include/sdmk.h sdmk_ewald)."""
+        src, tgt, stw = _arr(sys.sources), _arr(sys.targets), _arr(sys.strengths)
+        if plan.dim != 3 or int(sys.dim) != 3:
+            raise ValueError("ewald: the FFT Ewald path covers the 3D Stokeslet")
+        _check_lengths(plan.kernel, 3, src, tgt, stw)
+        ns, nt = src.size // 3, tgt.size // 3
+        u = np.empty((nt if nt else ns) * 3)
+        out = np.zeros(8)
+        cp = plan.to_c()
+        _raise(lib().sdmk_ewald(self._h, C.byref(cp), ns, _dptr(src), nt, _dptr(tgt if nt else None), _dptr(stw),
+                                _dptr(u), int(level), _dptr(out)))
+        if info is not None:
+            info.update(dict(zip(["level", "grid", "width", "kappa_max", "t_sort_ms", "t_local_ms", "t_far_ms",
+                                  "t_total_ms"], out.tolist())))
         return u
 
     def set_shard(self, rank: int, nranks: int):

@@ -409,6 +409,22 @@ int sdmk_direct_residual_sum_tables(sdmk_context* c, const unsigned char* tables
   });
 }
 
+int sdmk_ewald(sdmk_context* c, const sdmk_plan* plan, int64_t n_src, const double* src, int64_t n_tgt,
+               const double* tgt, const double* str, double* u, int level, double* info) {
+  return guarded([&] {
+    if (!plan || !src || !str || !u || (n_tgt > 0 && !tgt)) throw InvalidArgument("ewald: null array");
+    need_ctx(c)->ewald(to_plan(plan), n_src, src, n_tgt, tgt, str, u, level, false, info);
+  });
+}
+
+int sdmk_ewald_device(sdmk_context* c, const sdmk_plan* plan, int64_t n_src, const double* d_src, int64_t n_tgt,
+                      const double* d_tgt, const double* d_str, double* d_u, int level, double* info) {
+  return guarded([&] {
+    if (!plan || !d_src || !d_str || !d_u || (n_tgt > 0 && !d_tgt)) throw InvalidArgument("ewald: null array");
+    need_ctx(c)->ewald(to_plan(plan), n_src, d_src, n_tgt, d_tgt, d_str, d_u, level, true, info);
+  });
+}
+
 int sdmk_direct_sum(sdmk_context* c, int kernel, int dim, int64_t n_src, const double* src, int64_t n_tgt,
                     const double* tgt, const double* str, double* u) {
   return guarded([&] {

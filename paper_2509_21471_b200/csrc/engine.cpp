@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <array>
 #include <chrono>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1164,7 +1165,10 @@ void Context::run_downward() {  // dmk.cpp:705-857
   cuda_check(cudaMemcpyAsync(dA, hA, Aall.size() * sizeof(double), cudaMemcpyHostToDevice, st_), "symbol upload");
   const size_t bytes_B = sizeof(double2) * pr.nch * g.pz * g.ncol;
   const size_t bytes_FC = sizeof(double2) * d * ((size_t)g.nhalf + (size_t)g.pz * g.ncol);
-  constexpr size_t budget = size_t(2048) << 20;  // scratch per B / F+C chunk
+#ifndef SDMK_PW_BUDGET_GB
+#define SDMK_PW_BUDGET_GB 2
+#endif
+  constexpr size_t budget = size_t(SDMK_PW_BUDGET_GB) << 30;  // scratch per B / F+C chunk
   const int chunk_src = (int)std::max<size_t>(1, budget / bytes_B);
   const int chunk_tgt = (int)std::max<size_t>(1, budget / bytes_FC);
   // plane-wave timing: one event pair per level, read after the evaluation's
@@ -1275,12 +1279,30 @@ void Context::run_target_far(double* ufar) {  // dmk.cpp:861-915
 void Context::run_residual(double* ures, bool stats, int reserve_sms) {  // dmk.cpp:919-1032
   Problem& pr = prob_;
   const Tables& T = *tab_;
+  const ResidTables rt = residual_tables(pr.plan.kernel, pr.dim);
+  int* flags = arena_.as<int>("flags", 8);
+  unsigned long long* st = arena_.as<unsigned long long>("stats", 4);
+  if (stats) cuda_check(cudaMemsetAsync(st, 0, 4 * sizeof(unsigned long long), st_), "memset");
+  cudaEventRecord(ev_[13], st_);
+  launch_residual(rt, pr.boxes, pr.int_leaves, pr.n_int, pr.res_chunks, pr.n_chunks, pr.rng_start, pr.rng_box, pr.rng_info, pr.subrange, pr.spts, pr.ns,
+                  pr.sstr, arena_.as<double>("srec", (size_t)pr.ns * ((pr.dim + pr.sc + 1) / 2 * 2)),
+                  pr.periodic ? 1 : 0, pr.tpts, pr.nt, pr.tperm, pr.alias ? 1 : 0, reserve_sms, T.self_const, ures, flags + 3,
+                  stats ? st : nullptr, arena_.get("res_scratch", residual_scratch_bytes()), st_);
+  ++launches_;  // source record packing
+  cudaEventRecord(ev_[12], st_);
+  ++launches_;
+}
+
+// The residual kernel's radial tables for the current tables tab_ (uploaded
+// to the arena): piecewise re-expansions and the reference's coefficients.
+ResidTables Context::residual_tables(int kernel, int dim) {
+  const Tables& T = *tab_;
   const Cheb* cd = nullptr;
   const Cheb* co = nullptr;
-  if (pr.plan.kernel == kStokeslet) {
+  if (kernel == kStokeslet) {
     cd = &T.s_diag;
     co = &T.s_offd;
-  } else if (pr.plan.kernel == kStresslet) {
+  } else if (kernel == kStresslet) {
     cd = &T.t_diag;
     co = &T.t_offd;
   } else {
@@ -1297,7 +1319,7 @@ void Context::run_residual(double* ures, bool stats, int reserve_sms) {  // dmk.
   // degree 5 on 128 intervals (1e-13 for the 3D stresslet) left 6e-9
   // scaled differences at BASELINE cfg3; degree 6 is below 1e-15.
   constexpr double kPwTol = 2e-15;
-  auto& cached = pw_cache_[{&T, pr.plan.kernel}];  // fitted once per table set and kernel
+  auto& cached = pw_cache_[{&T, kernel}];  // fitted once per table set and kernel
   PiecewisePoly& po = cached.first;
   PiecewisePoly& pd = cached.second;
   if (po.c.empty()) {
@@ -1338,19 +1360,8 @@ void Context::run_residual(double* ures, bool stats, int reserve_sms) {  // dmk.
   cuda_check(cudaMemcpyAsync(dc, hc, nall * sizeof(double), cudaMemcpyHostToDevice, st_), "table upload");
   // the first piecewise interval takes the reference's own recurrence (see ResidTables)
   const double s_exact = co->lo + (co->hi - co->lo) / po.ni;
-  ResidTables rt{po.ni, po.deg, co->lo, co->hi, T.support, pr.plan.kernel, pr.dim, dc, dc + npw,
-                 dc + 2 * npw, dc + 2 * npw + kResidMaxCheb, nd, no, s_exact};
-  int* flags = arena_.as<int>("flags", 8);
-  unsigned long long* st = arena_.as<unsigned long long>("stats", 4);
-  if (stats) cuda_check(cudaMemsetAsync(st, 0, 4 * sizeof(unsigned long long), st_), "memset");
-  cudaEventRecord(ev_[13], st_);
-  launch_residual(rt, pr.boxes, pr.int_leaves, pr.n_int, pr.res_chunks, pr.n_chunks, pr.rng_start, pr.rng_box, pr.rng_info, pr.subrange, pr.spts, pr.ns,
-                  pr.sstr, arena_.as<double>("srec", (size_t)pr.ns * ((pr.dim + pr.sc + 1) / 2 * 2)),
-                  pr.periodic ? 1 : 0, pr.tpts, pr.nt, pr.tperm, pr.alias ? 1 : 0, reserve_sms, T.self_const, ures, flags + 3,
-                  stats ? st : nullptr, arena_.get("res_scratch", residual_scratch_bytes()), st_);
-  ++launches_;  // source record packing
-  cudaEventRecord(ev_[12], st_);
-  ++launches_;
+  return ResidTables{po.ni, po.deg, co->lo, co->hi, T.support, kernel, dim, dc, dc + npw,
+                     dc + 2 * npw, dc + 2 * npw + kResidMaxCheb, nd, no, s_exact};
 }
 
 // ------------------------------------------------------------- entries --
@@ -1955,6 +1966,274 @@ const Tables& Context::tables_image(const void* bytes, size_t n) {
   auto it = image_tables_.find(key);
   if (it == image_tables_.end()) it = image_tables_.emplace(key, parse_tables(bytes, n)).first;
   return it->second;
+}
+
+// ------------------------------------------------------------- FFT Ewald --
+namespace {
+// piecewise monomials of f on [0, 1): ni intervals, degree deg (Chebyshev
+// interpolation per interval, converted to monomials in u in [-1, 1])
+std::vector<double> fit_pieces(const std::function<double(double)>& f, int ni, int deg) {
+  const int n = deg + 1;
+  std::vector<double> out((size_t)ni * n, 0.0);
+  for (int i = 0; i < ni; ++i) {
+    const double a = double(i) / ni, b = double(i + 1) / ni;
+    std::vector<double> fv(n), ch(n, 0.0);
+    for (int j = 0; j < n; ++j) fv[j] = f(0.5 * (a + b) + 0.5 * (b - a) * std::cos(PI * (2 * j + 1) / (2.0 * n)));
+    for (int k = 0; k < n; ++k) {
+      double sum = 0.0;
+      for (int j = 0; j < n; ++j) sum += fv[j] * std::cos(k * PI * (2 * j + 1) / (2.0 * n));
+      ch[k] = sum * (k ? 2.0 : 1.0) / n;
+    }
+    std::vector<double> T0(n, 0.0), T1(n, 0.0), T2(n, 0.0);
+    double* mono = out.data() + (size_t)i * n;
+    T0[0] = 1.0;
+    for (int j = 0; j < n; ++j) mono[j] += ch[0] * T0[j];
+    if (n > 1) {
+      T1[1] = 1.0;
+      for (int j = 0; j < n; ++j) mono[j] += ch[1] * T1[j];
+    }
+    for (int k = 2; k < n; ++k) {
+      for (int j = 0; j < n; ++j) T2[j] = (j ? 2.0 * T1[j - 1] : 0.0) - T0[j];
+      for (int j = 0; j < n; ++j) mono[j] += ch[k] * T2[j];
+      T0 = T1;
+      T1 = T2;
+    }
+  }
+  return out;
+}
+
+int fft_size(int want) {  // smallest 2^a 3^b 5^c 7^d >= want, even
+  for (int m = std::max(want, 2);; ++m) {
+    if (m & 1) continue;
+    int r = m;
+    for (int f : {2, 3, 5, 7})
+      while (r % f == 0) r /= f;
+    if (r == 1) return m;
+  }
+}
+}  // namespace
+
+void Context::ewald(const Plan& P, int64_t ns, const double* src, int64_t nt, const double* tgt, const double* str,
+                    double* u, int level, bool device_ptrs, double* info) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  prob_.ready = false;
+  begun_ = false;
+  if (P.kernel != kStokeslet || P.dim != 3)
+    throw InvalidArgument("ewald: the FFT Ewald path covers the 3D Stokeslet");
+  check_inputs(P, 3, ns, nt, 1);
+  tab_ = tab_override_ ? tab_override_ : &tables_for(P);
+  if (tab_->win.kind != kProlate) throw InvalidArgument("ewald: needs a prolate split window");
+  const int d = 3, sc = 3;
+  const bool alias = nt == 0;
+  const int n = (int)ns, m = alias ? (int)ns : (int)nt;
+  cudaEventRecord(ev_[0], st_);
+  double* sin = arena_.as<double>("src_in", (size_t)ns * d);
+  double* tin = alias ? sin : arena_.as<double>("tgt_in", (size_t)nt * d);
+  double* fin = arena_.as<double>("str_in", (size_t)ns * sc);
+  copy_in(sin, src, sizeof(double) * ns * d, device_ptrs);
+  if (!alias) copy_in(tin, tgt, sizeof(double) * nt * d, device_ptrs);
+  copy_in(fin, str, sizeof(double) * ns * sc, device_ptrs);
+  int* flags = arena_.as<int>("flags", 8);
+  cuda_check(cudaMemsetAsync(flags, 0, 8 * sizeof(int), st_), "memset");
+  launch_validate(fin, (int64_t)ns * sc, 1, flags, 2, st_);
+  launch_validate(sin, (int64_t)ns * d, 1, flags, 0, st_);
+  if (!alias) launch_validate(tin, (int64_t)nt * d, 1, flags, 0, st_);
+  launch_wrap(sin, (int64_t)ns * d, st_);  // wrap_into_box (oracle.cpp:133-141)
+  if (!alias) launch_wrap(tin, (int64_t)nt * d, st_);
+  // Morton sort of sources (and targets) as in build_problem
+  auto sort_set = [&](const double* pts, int cnt, const std::string& tag, int*& perm, double*& soa, int32_t*& q) {
+    uint64_t* klo = arena_.as<uint64_t>("klo", cnt);
+    uint64_t* khi = arena_.as<uint64_t>("khi", cnt);
+    uint64_t* klo2 = arena_.as<uint64_t>("klo2", cnt);
+    uint64_t* khi2 = arena_.as<uint64_t>("khi2", cnt);
+    int* idx = arena_.as<int>("idx", cnt);
+    int* idx2 = arena_.as<int>("idx2", cnt);
+    perm = arena_.as<int>(tag + "perm", cnt);
+    size_t tb = sort_temp_bytes(cnt);
+    void* tmp = arena_.get("sort_tmp", tb);
+    launch_morton(pts, cnt, d, klo, khi, nullptr, idx, st_);
+    sort_morton(cnt, d, klo, khi, idx, klo2, khi2, idx2, perm, tmp, tb, st_);
+    soa = arena_.as<double>(tag + "pts", (size_t)cnt * d);
+    q = arena_.as<int32_t>(tag + "q", (size_t)cnt * d);
+    launch_gather_points(pts, perm, cnt, d, soa, q, st_);
+  };
+  int *sperm = nullptr, *tperm = nullptr;
+  double *spts = nullptr, *tpts = nullptr;
+  int32_t *sq = nullptr, *tq = nullptr;
+  sort_set(sin, n, "s", sperm, spts, sq);
+  double* sstr = arena_.as<double>("sstr", (size_t)ns * sc);
+  launch_gather_strengths(fin, sperm, n, sc, sstr, st_);
+  if (alias) {
+    tperm = sperm;
+    tpts = spts;
+    tq = sq;
+  } else {
+    sort_set(tin, m, "t", tperm, tpts, tq);
+  }
+  // cells at level L: about 200 sources per cell
+  int L = level;
+  if (L < 0) {
+    L = 0;
+    while (L < 7 && (double)ns / std::pow(8.0, L + 1) >= 100.0) ++L;
+  }
+  if (L > 7) throw InvalidArgument("ewald: cell level above 7");
+  const int side = 1 << L, ncell = 1 << (3 * L);
+  int* sb = arena_.as<int>("ew_sbnd", (size_t)ncell + 1);
+  int* tbd = alias ? sb : arena_.as<int>("ew_tbnd", (size_t)ncell + 1);
+  launch_cell_bounds(n, sq, L, sb, st_);
+  if (!alias) launch_cell_bounds(m, tq, L, tbd, st_);
+  int* hb = (int*)pinned_.get("ew_bnd", sizeof(int) * 2 * ((size_t)ncell + 1));
+  cuda_check(cudaMemcpyAsync(hb, sb, sizeof(int) * (ncell + 1), cudaMemcpyDeviceToHost, st_), "D2H cells");
+  if (!alias)
+    cuda_check(cudaMemcpyAsync(hb + ncell + 1, tbd, sizeof(int) * (ncell + 1), cudaMemcpyDeviceToHost, st_),
+               "D2H cells");
+  int* hflags = (int*)pinned_.get("hflags", 64);
+  cuda_check(cudaMemcpyAsync(hflags, flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H flags");
+  sync();
+  if (hflags[2]) throw InvalidArgument("ParticleSystem: non-finite strength");
+  if (hflags[0]) throw InvalidArgument("ParticleSystem: non-finite coordinate");
+  cudaEventRecord(ev_[1], st_);
+  const int* tb_h = alias ? hb : hb + ncell + 1;
+  // ---- local part: residual kernel at scale nu = 2^-L over each cell's 27 neighbours (cells are
+  // the leaves of a uniform tree; every range at the leaf scale, periodic image shifts)
+  std::vector<dev::DBox> boxes(ncell);
+  auto cell_xyz = [&](int c, int* xyz) {  // Morton cell index -> integer coordinates
+    xyz[0] = xyz[1] = xyz[2] = 0;
+    for (int b = 0; b < L; ++b)
+      for (int a = 0; a < 3; ++a) xyz[a] |= ((c >> (3 * b + a)) & 1) << b;
+  };
+  auto cell_id = [&](const int* xyz) {
+    int c = 0;
+    for (int b = 0; b < L; ++b)
+      for (int a = 0; a < 3; ++a) c |= ((xyz[a] >> b) & 1) << (3 * b + a);
+    return c;
+  };
+  const double cside = std::ldexp(1.0, -L);
+  for (int c = 0; c < ncell; ++c) {
+    int xyz[3];
+    cell_xyz(c, xyz);
+    dev::DBox& o = boxes[c];
+    o.sb = hb[c];
+    o.se = hb[c + 1];
+    o.tb = tb_h[c];
+    o.te = tb_h[c + 1];
+    o.level = L;
+    o.parent = -1;
+    o.first_child = -1;
+    o.leaf = 1;
+    for (int a = 0; a < 3; ++a)  // tree.cpp:221-228
+      o.c[a] = std::ldexp(double(int64_t(xyz[a]) << (kMaxLevel - L)), -kMaxLevel) - 0.5 + 0.5 * cside;
+    o.side = cside;
+    o.half = 0.5 * cside;
+  }
+  std::vector<int> leaves, rs(1, 0), rbox, rinfo, chunks;
+  for (int c = 0; c < ncell; ++c) {
+    if (boxes[c].te == boxes[c].tb) continue;
+    const int li = (int)leaves.size();
+    leaves.push_back(c);
+    int xyz[3];
+    cell_xyz(c, xyz);
+    auto add = [&](int sbx, const int* sh, bool self) {
+      if (boxes[sbx].se == boxes[sbx].sb) return;
+      rbox.push_back(sbx);
+      rinfo.push_back((sh[0] + 1) + 3 * (sh[1] + 1) + 9 * (sh[2] + 1) + (self ? 64 : 0));  // fine-scale bit 0: nu = r_l
+    };
+    const int zero[3] = {0, 0, 0};
+    add(c, zero, true);
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          if (!dx && !dy && !dz) continue;
+          const int dd[3] = {dx, dy, dz};
+          int nb[3], sh[3];
+          for (int a = 0; a < 3; ++a) {
+            const int v = xyz[a] + dd[a];
+            sh[a] = v < 0 ? -1 : (v >= side ? 1 : 0);
+            nb[a] = v - sh[a] * side;
+          }
+          add(cell_id(nb), sh, false);
+        }
+    rs.push_back((int)rbox.size());
+    for (int t0 = boxes[c].tb; t0 < boxes[c].te; t0 += 32) {
+      chunks.push_back(li);
+      chunks.push_back(t0);
+    }
+  }
+  Packer pk;
+  const size_t o_boxes = pk.add(boxes), o_leaves = pk.add(leaves), o_rs = pk.add(rs), o_rbox = pk.add(rbox),
+               o_rinfo = pk.add(rinfo), o_chunks = pk.add(chunks);
+  char* hp = (char*)pinned_.get("ew_lists", pk.total + 64);
+  for (auto& it : pk.items) std::memcpy(hp + it.off, it.src, it.bytes);
+  char* dv = (char*)arena_.get("ew_lists", pk.total + 64);
+  cuda_check(cudaMemcpyAsync(dv, hp, pk.total, cudaMemcpyHostToDevice, st_), "ewald lists upload");
+  const dev::DBox* dboxes = (const dev::DBox*)(dv + o_boxes);
+  int* subr = arena_.as<int>("ew_subrange", (size_t)ncell * 9);
+  launch_leaf_subranges(dboxes, ncell, sq, n, d, subr, st_);
+  const ResidTables rt = residual_tables(kStokeslet, 3);
+  double* ures = arena_.as<double>("ures", (size_t)m * d);
+  launch_residual(rt, dboxes, (const int*)(dv + o_leaves), (int)leaves.size(), (const int*)(dv + o_chunks),
+                  (int)(chunks.size() / 2), (const int*)(dv + o_rs), (const int*)(dv + o_rbox),
+                  (const int*)(dv + o_rinfo), subr, spts, n, sstr, arena_.as<double>("srec", (size_t)n * 6), 1, tpts,
+                  m, tperm, alias ? 1 : 0, 0, tab_->self_const, ures, flags + 3, nullptr,
+                  arena_.get("res_scratch", residual_scratch_bytes()), st_);
+  cudaEventRecord(ev_[2], st_);
+  // ---- far part: PSWF-window NUFFT on an Mg^3 grid
+  const double nu = cside, c = P.c;
+  const int kmax = (int)std::ceil(c / (2.0 * PI * nu) - 1e-12);  // gamma^(k nu) = 0 beyond k nu = c
+  const double eps = std::max(P.tol, 1e-14);
+  const int w = std::min(16, std::max(4, (int)std::ceil(std::log(100.0 / eps) / (0.75 * PI))));
+  const int Mg = fft_size(std::max(2 * (2 * kmax + 1), 2 * w));
+  const double cs = 0.75 * PI * w;  // spreading window bandwidth (oversampling 2)
+  const WindowFn sw = make_prolate(cs);
+  const double phi0 = win_phi(sw, 0.0);
+  const int wni = 64, wdeg = 10;
+  std::vector<double> wpoly = fit_pieces([&](double z) { return win_phi(sw, z) / phi0; }, wni, wdeg);
+  const double h = 1.0 / Mg, alpha = 0.5 * w * h;
+  std::vector<double> dfac(kmax + 1);  // h / Phi_1^(k) for the window phi / phi0 scaled by alpha
+  for (int k = 0; k <= kmax; ++k) dfac[k] = h * phi0 / (alpha * win_hat(sw, 2.0 * PI * k * alpha));
+  const long s2max = 3L * kmax * kmax;
+  std::vector<double> A((size_t)s2max + 1, 0.0);  // gamma^(k nu) / k^4, the periodic mollified Stokeslet
+  for (long s2 = 1; s2 <= s2max; ++s2) {
+    const double k = 2.0 * PI * std::sqrt((double)s2);
+    A[s2] = moll_hat(tab_->win, k * nu) / (k * k * k * k);
+  }
+  Packer pk2;
+  const size_t o_w = pk2.add(wpoly), o_d = pk2.add(dfac), o_a = pk2.add(A);
+  char* hp2 = (char*)pinned_.get("ew_tabs", pk2.total + 64);
+  for (auto& it : pk2.items) std::memcpy(hp2 + it.off, it.src, it.bytes);
+  char* dv2 = (char*)arena_.get("ew_tabs", pk2.total + 64);
+  cuda_check(cudaMemcpyAsync(dv2, hp2, pk2.total, cudaMemcpyHostToDevice, st_), "ewald tables upload");
+  EwGrid g{Mg, w, kmax, s2max, h, 1.0 / h, 1.0 / alpha, wni, wdeg, (const double*)(dv2 + o_w)};
+  const size_t M3 = (size_t)Mg * Mg * Mg, S = (size_t)Mg * Mg * (Mg / 2 + 1);
+  double* grid = arena_.as<double>("ew_grid", 3 * M3);
+  double2* spec = arena_.as<double2>("ew_spec", 3 * S);
+  cuda_check(cudaMemsetAsync(grid, 0, sizeof(double) * 3 * M3, st_), "memset grid");
+  launch_ew_spread(g, n, spts, sstr, grid, st_);
+  fft_.plan(Mg, 3, st_);
+  fft_.forward(grid, spec);
+  launch_ew_symbol(g, spec, (const double*)(dv2 + o_a), (const double*)(dv2 + o_d), st_);
+  fft_.inverse(spec, grid);
+  double* ufar = arena_.as<double>("ufar", (size_t)m * d);
+  launch_ew_gather(g, m, tpts, tperm, grid, ufar, st_);
+  cudaEventRecord(ev_[3], st_);
+  double* du = device_ptrs ? u : arena_.as<double>("u", (size_t)m * d);
+  launch_combine(m, d, ufar, ures, nullptr, 0.0, nullptr, nullptr, nullptr, du, st_);
+  if (!device_ptrs) copy_out(u, du, sizeof(double) * m * d);
+  cudaEventRecord(ev_[4], st_);
+  cuda_check(cudaMemcpyAsync(hflags, flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H flags");
+  sync();
+  cuda_check(cudaGetLastError(), "ewald kernels");
+  if (hflags[3]) throw DomainError("residual_pass: coincident points");
+  if (info) {
+    info[0] = L;
+    info[1] = Mg;
+    info[2] = w;
+    info[3] = kmax;
+    info[4] = ev_ms(0, 1);
+    info[5] = ev_ms(1, 2);
+    info[6] = ev_ms(2, 3);
+    info[7] = ev_ms(0, 4);
+  }
 }
 
 }  // namespace sdmkb

@@ -12,6 +12,7 @@
 
 #include "../../include/sdmk.h"
 #include "host/comm.hpp"
+#include "host/fft.hpp"
 #include "host/setup.hpp"
 #include "host/tree.hpp"
 #include "kernels/launch.hpp"
@@ -172,6 +173,14 @@ class Context {
                      double* in);
   void pass_target_far(const Plan& P, int64_t nin, const double* in, double* u);
   void pass_residual(const Plan& P, const Tables* tab, int64_t nstr, const double* str, bool periodic, double* u);
+  // FFT Ewald: periodic 3D Stokeslet, single-level
+  // split at nu = 2^-level (level < 0: chosen from N), local part by the
+  // residual kernel over the 27 neighbour cells, far part by a PSWF-window
+  // NUFFT on a uniform grid with cuFFT.  Host or device pointers; info[8]
+  // (may be null) receives level, grid size, window width, kappa_max and
+  // the times (ms) of sort, local, far, total.
+  void ewald(const Plan& P, int64_t ns, const double* src, int64_t nt, const double* tgt, const double* str,
+             double* u, int level, bool device_ptrs, double* info);
   // tables from an SDMKSPLT v1 memory image (cached by content)
   const Tables& tables_image(const void* bytes, size_t n);
   // tables an evaluation uses instead of the plan's (the reference's
@@ -199,6 +208,7 @@ class Context {
   void run_downward();
   void run_target_far(double* ufar);
   void run_residual(double* ures, bool stats, int reserve_sms = 0);
+  ResidTables residual_tables(int kernel, int dim);
   GridDev& grid(GridDev& cache, const std::string& name, int dim, int p, int N, double theta, double band_r2);
   void sync();
   double ev_ms(int a, int b);
@@ -242,6 +252,7 @@ class Context {
   bool accumulate_down_ = false;  // downward interpolation adds to the children (pass-level API)
   bool force_tbasis_ = false;  // target bases recomputed (the upward pass may not have run)
   const Tables* tab_override_ = nullptr;
+  Fft3 fft_;
   std::map<std::string, Tables> image_tables_;
   std::map<std::pair<const Tables*, int>, std::pair<PiecewisePoly, PiecewisePoly>> pw_cache_;
   const int32_t* hq_ = nullptr;  // pinned sorted quantized coordinates of the current problem

@@ -206,6 +206,24 @@ void launch_scatter_ranges(int nt, int dim, const int64_t* bounds, int nranks, i
 void launch_copy_boxes(int n, const int* src_ids, const double* src, const int* dst_ids, double* dst, int64_t elems,
                        cudaStream_t st);
 
+// ---- ewald.cu: FFT Ewald far field (periodic 3D Stokeslet) ---------------------
+struct EwGrid {
+  int Mg;            // grid points per axis
+  int w;             // window width in grid points (<= 16)
+  int kmax;          // |kappa_i| <= kmax in the band
+  long s2max;        // |kappa|^2 <= s2max
+  double h, inv_h;   // grid spacing 1 / Mg
+  double inv_alpha;  // 1 / (w h / 2)
+  int ni, deg;       // window phi(|z|): piecewise monomials on [0, 1)
+  const double* wpoly;
+};
+void launch_ew_spread(const EwGrid& g, int n, const double* spts, const double* sstr, double* grid, cudaStream_t st);
+void launch_ew_symbol(const EwGrid& g, double2* spec, const double* A, const double* dfac, cudaStream_t st);
+void launch_ew_gather(const EwGrid& g, int n, const double* tpts, const int* tperm, const double* grid, double* u,
+                      cudaStream_t st);
+// bnd[c] = first sorted point in Morton cell >= c at level L (3D), c = 0..8^L
+void launch_cell_bounds(int n, const int32_t* q, int L, int* bnd, cudaStream_t st);
+
 // ---- direct.cu: O(N*M) reference sums (oracle.cpp:143-241) ---------------------
 constexpr int kDirectMaxCheb = 1024;
 struct DirectTables {
