@@ -140,10 +140,10 @@ __device__ __forceinline__ void radial_tables(const ResidTables& rt, const doubl
     fo = v.y;
     return;
   }
-  const bool in = s < rt.support;
+  // (pairs outside the support are dropped by the caller's exact test)
   const double y = (s - rt.lo) * yscale;
-  int iv = (int)y;
-  iv = iv < 0 ? 0 : (iv >= rt.ni ? rt.ni - 1 : iv);
+  // y >= 0 (NaN only for coincident points, which are never kept): one unsigned clamp
+  const int iv = (int)min((unsigned)(int)y, (unsigned)(rt.ni - 1));
   const double u = 2.0 * (y - iv) - 1.0;
   const double2* c = pw + iv * (DEG + 1) * kCopies;  // pw already offset by this lane's copy
   double2 v = c[DEG * kCopies];
@@ -153,8 +153,8 @@ __device__ __forceinline__ void radial_tables(const ResidTables& rt, const doubl
     if (KERNEL != 2) v.x = fma(v.x, u, ck.x);
     v.y = fma(v.y, u, ck.y);
   }
-  fd = (KERNEL != 2 && in) ? v.x : 0.0;
-  fo = in ? v.y : 0.0;
+  fd = KERNEL != 2 ? v.x : 0.0;
+  fo = v.y;
 }
 
 // residual_apply assembly (split.cpp:258-317) given the radial table values;
@@ -413,11 +413,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         double fd, fo;
         radial_tables<KERNEL, DEG, EXACT>(rt, s_pw + (lane & (kCopies - 1)), yscale, s, fd, fo, s_cheb, r2, inu);
         assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, nu, rv + DIM, c);
-        const bool keep = in && r2 != 0.0;
         near = s < rt.s_exact;
-#pragma unroll
-        for (int j = 0; j < DIM; ++j) c[j] = keep ? c[j] : 0.0;
-        return keep;
+        return in && r2 != 0.0;  // c is added only when kept
       };
       unsigned long long nearmask = 0;  // list entries to re-evaluate exactly (kList <= 64)
       for (int i = 0; i < mx; i += kILP) {  // all evaluations unconditional (clamped), straight-line
@@ -516,11 +513,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           radial_tables<KERNEL, DEG, EXACT>(rt, s_pw + (lane & (kCopies - 1)), yscale, sc, fd, fo, s_cheb, r2,
                                             inv_rl);
           assemble<KERNEL, DIM>(fd, fo, x, rinv, sc, rt.support, r_l, sv + DIM, c);
-          const bool keep = in && r2 != 0.0;
           near = sc < rt.s_exact;
-#pragma unroll
-          for (int k = 0; k < DIM; ++k) c[k] = keep ? c[k] : 0.0;
-          return keep;
+          return in && r2 != 0.0;  // c is added only when kept
         };
         unsigned nearbits = 0;  // sources of this round to re-evaluate exactly
         for (int j = 0; j < nv; j += 2) {
