@@ -15,11 +15,19 @@ ap.add_argument("--eps", type=float, default=1e-6)
 ap.add_argument("--dim", type=int, default=3)
 ap.add_argument("--periodic", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--cfg", default=None, help="a BASELINE configuration (tools/baseline_configs.py) instead")
 a = ap.parse_args()
-rng = np.random.default_rng(0)
-x = rng.uniform(-0.5, 0.5, (a.n, a.dim))
-sc = g.strength_components(a.kernel, a.dim)
-s = rng.standard_normal((a.n, sc))
+if a.cfg:
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from baseline_configs import cfg_system
+    c = cfg_system(a.cfg)
+    x, s = c["x"], c["s"]
+    a.kernel, a.dim, a.eps, a.periodic = c["kernel"], c["dim"], c["eps"], c["periodic"]
+else:
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-0.5, 0.5, (a.n, a.dim))
+    sc = g.strength_components(a.kernel, a.dim)
+    s = rng.standard_normal((a.n, sc))
 ctx = g.Context(0)
 plan = g.select_parameters(a.kernel, a.eps, g.PROLATE, a.dim)
 sys_ = g.ParticleSystem(a.dim, x, np.zeros(0), s)
