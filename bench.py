@@ -279,8 +279,8 @@ def run_ours(args, rank, world, local_rank):
     pw_t = rep["t_planewave"]
     traffic = None  # DRAM bytes per launch of the same kernel/workload from the committed ncu capture
     try:
-        with open(os.path.join(ROOT, "profiles", "round1", "residual_traffic.json")) as f:
-            traffic = int(json.load(f)["dram_bytes"]) if args.n == 10_000_000 else None
+        with open(os.path.join(ROOT, "profiles", "round2", "residual_hw.json")) as f:
+            traffic = int(json.load(f)["dram_bytes_per_launch"]) if args.n == 10_000_000 else None
     except (OSError, ValueError, KeyError):
         traffic = None
     hw = None  # FP64 rate the hardware executed (ncu dadd + dmul + 2 dfma over the kernel's duration)
@@ -297,7 +297,7 @@ def run_ours(args, rank, world, local_rank):
             "hw_fp64_tflops": hw.get("hw_fp64_tflops") if hw else None,
             "hw_fp64_source": hw.get("source") if hw else None,
             "peak": peak, "unit": "TFLOP/s", "frac": (res_flops / res_t / 1e12) / peak, "traffic": traffic,
-            "traffic_source": "profiles/round1/residual_traffic.json (ncu dram__bytes_read+write, one launch)",
+            "traffic_source": "profiles/round2/residual_hw.json (ncu dram__bytes_read+write, one launch)",
             "peak_source": "measured DFMA microbenchmark (sdmk_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",
             "share_of_step": res_t / (R["ms"] * 1e-3), "planewave_share_of_step": pw_t / (R["ms"] * 1e-3)}
     roof["multi_gpu_path"] = ("library NCCL communicator" if use_comm else "set_shard + torch all_reduce") if world > 1 else None
