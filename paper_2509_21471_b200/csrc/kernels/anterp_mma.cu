@@ -392,10 +392,12 @@ __global__ void __launch_bounds__(W * 32, 1) k_anterp2(ChebDev cb, const DBox* _
     }
     __syncthreads();
     // ... then S[pt][(ch, iz)] = s_ch * bz over all threads
-    for (int e = tid; e < kKC2 * nrow; e += blockDim.x) {
-      const int pt = e / nrow, r = e - pt * nrow, code = rcode[r];
-      sbz[pt * RS + r] = s_chv[pt][code & 255] * (dim == 3 ? bz[pt * XS + (code >> 8)] : 1.0);
-    }
+    // (a warp per point row, lanes along the (ch, iz) rows: no integer division)
+    for (int pt = warp; pt < kKC2; pt += W)
+      for (int r = lane; r < nrow; r += 32) {
+        const int code = rcode[r];
+        sbz[pt * RS + r] = s_chv[pt][code & 255] * (dim == 3 ? bz[pt * XS + (code >> 8)] : 1.0);
+      }
     __syncthreads();
 #pragma unroll 2
     for (int ks = 0; ks < kKC2 / 4; ++ks) {

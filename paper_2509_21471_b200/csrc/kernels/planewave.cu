@@ -320,32 +320,34 @@ __global__ void __launch_bounds__(kGroupThreads, GroupCfg<KERNEL, DIM, ZH>::kMin
   const size_t bstride = (size_t)NCH * nhalf;
   const int nchunk = (nhalf + kGM - 1) / kGM;
   const int my_chunks = (nchunk - (int)blockIdx.y + (int)gridDim.y - 1) / (int)gridDim.y;
-  if (tid >= kGM) {  // producer warp: refill each stage once the 4 consumer warps released it
-    if (tid == kGM) {
-      const int nrows = my_chunks * RC;
-      for (int i = 0; i < nrows; ++i) {
-        if (i >= NS) dev::mbar_wait(&empty[i % NS], (uint32_t)((i / NS - 1) & 1));
-        const int ck = (int)blockIdx.y + (i / RC) * (int)gridDim.y, r = i % RC;
-        const int zh = r / RP, rr = r % RP;
-        const int yi = rr & 3, zi = DIM == 3 ? zh + (rr >> 2) : 1;
-        const int m_begin = ck * kGM, nm = min(kGM, nhalf - m_begin);
-        const uint32_t seg = (uint32_t)nm * 16u;
-        const int* srow = s_slot + 4 * yi + 16 * zi;
+  if (tid >= kGM) {  // producer warp: refill each stage once the 4 consumer warps released it;
+                     // lane l < 4 NCH issues the bulk copy of (position l / NCH, channel l % NCH),
+                     // so the row's copies are issued in parallel
+    const int lane = tid - kGM;
+    const int xl = lane / NCH, kl = lane % NCH;
+    const int nrows = my_chunks * RC;
+    for (int i = 0; i < nrows; ++i) {
+      if (i >= NS) dev::mbar_wait(&empty[i % NS], (uint32_t)((i / NS - 1) & 1));
+      const int ck = (int)blockIdx.y + (i / RC) * (int)gridDim.y, r = i % RC;
+      const int zh = r / RP, rr = r % RP;
+      const int yi = rr & 3, zi = DIM == 3 ? zh + (rr >> 2) : 1;
+      const int m_begin = ck * kGM, nm = min(kGM, nhalf - m_begin);
+      const uint32_t seg = (uint32_t)nm * 16u;
+      const int* srow = s_slot + 4 * yi + 16 * zi;
+      uint64_t* bar = &full[i % NS];
+      if (lane == 0) {
         uint32_t tx = 0;
 #pragma unroll
         for (int xi = 0; xi < 4; ++xi) tx += srow[xi] >= 0 ? NCH * seg : 0u;
-        uint64_t* bar = &full[i % NS];
         dev::mbar_expect_tx(bar, tx);
-        double2* st = ring + (size_t)(i % NS) * 4 * NCH * kGM;
-#pragma unroll
-        for (int xi = 0; xi < 4; ++xi) {
-          const int sl = srow[xi];
-          if (sl < 0) continue;
-#pragma unroll
-          for (int k = 0; k < NCH; ++k)
-            dev::bulk_g2s(st + (xi * NCH + k) * kGM, G + (size_t)sl * bstride + (size_t)k * nhalf + m_begin, seg,
-                          bar);
-        }
+      }
+      __syncwarp();  // the byte count is registered before any copy can complete
+      double2* st = ring + (size_t)(i % NS) * 4 * NCH * kGM;
+      if (lane < 4 * NCH) {
+        const int sl = srow[xl];
+        if (sl >= 0)
+          dev::bulk_g2s(st + (xl * NCH + kl) * kGM, G + (size_t)sl * bstride + (size_t)kl * nhalf + m_begin, seg,
+                        bar);
       }
     }
     return;
