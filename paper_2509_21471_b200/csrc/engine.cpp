@@ -89,6 +89,19 @@ struct Packer {
     total += v.size() * sizeof(T);
     return off;
   }
+  // all items into one (pinned) staging buffer, in 1 MB pieces over the host threads
+  void copy_to(char* dst) const {
+    constexpr size_t kPiece = size_t(1) << 20;
+    std::vector<std::array<size_t, 3>> pieces;  // (dst offset, src item, src offset)
+    for (size_t i = 0; i < items.size(); ++i)
+      for (size_t o = 0; o < items[i].bytes; o += kPiece) pieces.push_back({items[i].off + o, i, o});
+#pragma omp parallel for schedule(dynamic, 1) if (pieces.size() > 4)
+    for (size_t k = 0; k < pieces.size(); ++k) {
+      const Item& it = items[pieces[k][1]];
+      const size_t o = pieces[k][2];
+      std::memcpy(dst + pieces[k][0], static_cast<const char*>(it.src) + o, std::min(kPiece, it.bytes - o));
+    }
+  }
 };
 
 }  // namespace
@@ -774,8 +787,7 @@ void Context::upload_tree_lists_a() {
     off[lev] = {pk.add(m_out[lev]), pk.add(m_in[lev]), pk.add(m_ci[lev]),
                 pk.add(u_out[lev]), pk.add(u_in[lev]), pk.add(u_ci[lev])};
   char* h = (char*)pinned_.get("treeA", pk.total + 64);
-  for (auto& it : pk.items)
-    if (it.bytes) std::memcpy(h + it.off, it.src, it.bytes);
+  pk.copy_to(h);
   char* dv = (char*)arena_.get("treeA", pk.total + 64);
   cuda_check(cudaMemcpyAsync(dv, h, pk.total, cudaMemcpyHostToDevice, st_), "tree upload");
   const double* db = (const double*)(dv + o_blob);
@@ -894,6 +906,8 @@ void Context::upload_tree_lists_b() {
   std::vector<int> rbox(rs[nitp]), rinfo(rs[nitp]);
 #pragma omp parallel for schedule(static)
   for (int i = 0; i < nitp; ++i) ranges(itp[i], rbox.data() + rs[i], rinfo.data() + rs[i]);
+  const auto hb3 = std::chrono::steady_clock::now();
+  double t_groups = 0.0, t_entries = 0.0;
   // per-level lists
   const int L = t.max_level + 1;
   struct LV {
@@ -950,6 +964,7 @@ void Context::upload_tree_lists_b() {
       }
       return cnt;
     };
+    const auto he0 = std::chrono::steady_clock::now();
     std::vector<int> cnt(nl);
     int max_e = 0;
 #pragma omp parallel for schedule(static) reduction(max : max_e)
@@ -972,18 +987,27 @@ void Context::upload_tree_lists_b() {
 #pragma omp parallel for schedule(static)
     for (int i = 0; i < nl; ++i)
       if (cnt[i] > 0) entries(ids[i], V.eslot.data() + eoff[i], V.etau.data() + eoff[i]);
+    const auto he1 = std::chrono::steady_clock::now();
     if (lev > 0) build_groups(t, lev, V.tbx, V.es, V.eslot, V.etau, V.gstart, V.gslot, V.tmeta);
+    const auto he2 = std::chrono::steady_clock::now();
+    t_entries += std::chrono::duration<double, std::milli>(he1 - he0).count();
+    t_groups += std::chrono::duration<double, std::milli>(he2 - he1).count();
   }
+  const auto hb4 = std::chrono::steady_clock::now();
   if (bad_tau) throw RuntimeError("colleague offset outside {-1,0,1}");
   // root lists: box 0 with one zero-offset entry
   std::vector<int> root_ids = {0}, root_es = {0, 1}, root_slot = {0}, root_tau = {13};
   // residual work items: 32-target chunks of each target leaf, in leaf order
-  std::vector<int> chunks;
+  std::vector<int> coff(nitp + 1, 0);
+  for (int i = 0; i < nitp; ++i) coff[i + 1] = coff[i] + (t.ntgt(itp[i]) + 31) / 32;
+  std::vector<int> chunks(2 * (size_t)coff[nitp]);
+#pragma omp parallel for schedule(static)
   for (int i = 0; i < nitp; ++i) {
     const Box& x = t.boxes[itp[i]];
-    for (int t0 = x.tb; t0 < x.te; t0 += 32) {
-      chunks.push_back(i);
-      chunks.push_back(t0);
+    int* o = chunks.data() + 2 * (size_t)coff[i];
+    for (int t0 = x.tb; t0 < x.te; t0 += 32, o += 2) {
+      o[0] = i;
+      o[1] = t0;
     }
   }
   Packer pk;
@@ -1001,9 +1025,10 @@ void Context::upload_tree_lists_b() {
                 pk.add(V.sbx),   pk.add(V.tbx),    pk.add(V.es),     pk.add(V.eslot),
                 pk.add(V.etau),  pk.add(V.gstart), pk.add(V.gslot),  pk.add(V.tmeta)};
   }
+  const auto hb5 = std::chrono::steady_clock::now();
   char* h = (char*)pinned_.get("treeB", pk.total + 64);
-  for (auto& it : pk.items)
-    if (it.bytes) std::memcpy(h + it.off, it.src, it.bytes);
+  pk.copy_to(h);
+  const auto hb6 = std::chrono::steady_clock::now();
   char* dv = (char*)arena_.get("treeB", pk.total + 64);
   cuda_check(cudaMemcpyAsync(dv, h, pk.total, cudaMemcpyHostToDevice, st_), "tree upload");
   pr.send_ids = (int*)(dv + o_send);
@@ -1051,6 +1076,9 @@ void Context::upload_tree_lists_b() {
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
     std::fprintf(stderr, "[sdmk timing] lists B (host, overlaps the upward pass): neighbours %.2f ms, shard+halo plan %.2f ms, lists+upload %.2f ms\n",
                  ms(hb0, hb1), ms(hb1, hb2), ms(hb2, std::chrono::steady_clock::now()));
+    std::fprintf(stderr, "[sdmk timing]   ranges %.2f, level lists %.2f (entries %.2f, groups %.2f), chunks+pack %.2f, copy to pinned %.2f (%.1f MB), rest %.2f ms\n",
+                 ms(hb2, hb3), ms(hb3, hb4), t_entries, t_groups, ms(hb4, hb5), ms(hb5, hb6), pk.total / 1e6,
+                 ms(hb6, std::chrono::steady_clock::now()));
   }
 }
 
@@ -1165,10 +1193,10 @@ void Context::run_downward() {  // dmk.cpp:705-857
   cuda_check(cudaMemcpyAsync(dA, hA, Aall.size() * sizeof(double), cudaMemcpyHostToDevice, st_), "symbol upload");
   const size_t bytes_B = sizeof(double2) * pr.nch * g.pz * g.ncol;
   const size_t bytes_FC = sizeof(double2) * d * ((size_t)g.nhalf + (size_t)g.pz * g.ncol);
-#ifndef SDMK_PW_BUDGET_GB
-#define SDMK_PW_BUDGET_GB 2
+#ifndef SDMK_PW_BUDGET_MB
+#define SDMK_PW_BUDGET_MB 2048
 #endif
-  constexpr size_t budget = size_t(SDMK_PW_BUDGET_GB) << 30;  // scratch per B / F+C chunk
+  constexpr size_t budget = size_t(SDMK_PW_BUDGET_MB) << 20;  // scratch per B / F+C chunk
   const int chunk_src = (int)std::max<size_t>(1, budget / bytes_B);
   const int chunk_tgt = (int)std::max<size_t>(1, budget / bytes_FC);
   // plane-wave timing: one event pair per level, read after the evaluation's
@@ -2163,7 +2191,7 @@ void Context::ewald(const Plan& P, int64_t ns, const double* src, int64_t nt, co
   const size_t o_boxes = pk.add(boxes), o_leaves = pk.add(leaves), o_rs = pk.add(rs), o_rbox = pk.add(rbox),
                o_rinfo = pk.add(rinfo), o_chunks = pk.add(chunks);
   char* hp = (char*)pinned_.get("ew_lists", pk.total + 64);
-  for (auto& it : pk.items) std::memcpy(hp + it.off, it.src, it.bytes);
+  pk.copy_to(hp);
   char* dv = (char*)arena_.get("ew_lists", pk.total + 64);
   cuda_check(cudaMemcpyAsync(dv, hp, pk.total, cudaMemcpyHostToDevice, st_), "ewald lists upload");
   const dev::DBox* dboxes = (const dev::DBox*)(dv + o_boxes);
@@ -2200,7 +2228,7 @@ void Context::ewald(const Plan& P, int64_t ns, const double* src, int64_t nt, co
   Packer pk2;
   const size_t o_w = pk2.add(wpoly), o_d = pk2.add(dfac), o_a = pk2.add(A);
   char* hp2 = (char*)pinned_.get("ew_tabs", pk2.total + 64);
-  for (auto& it : pk2.items) std::memcpy(hp2 + it.off, it.src, it.bytes);
+  pk2.copy_to(hp2);
   char* dv2 = (char*)arena_.get("ew_tabs", pk2.total + 64);
   cuda_check(cudaMemcpyAsync(dv2, hp2, pk2.total, cudaMemcpyHostToDevice, st_), "ewald tables upload");
   EwGrid g{Mg, w, kmax, s2max, h, 1.0 / h, 1.0 / alpha, wni, wdeg, (const double*)(dv2 + o_w)};
