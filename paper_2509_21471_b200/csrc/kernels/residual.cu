@@ -77,16 +77,35 @@ __global__ void k_pack_sources(const double* __restrict__ spts, const double* __
   }
 }
 
-// 1/sqrt(x) from the single-precision estimate and two Newton steps (~1 ulp;
-// the CUDA double rsqrt spends ~20 instructions on range handling).  x here
-// is a squared distance in (0, 3); tiny x falls back to rsqrt.
-__device__ __forceinline__ double rsqrt_nr(double x) {
-  if (x < 1e-30) return rsqrt(x);
-  double y = (double)rsqrtf(__double2float_rn(x));
-  double r = fma(-x * y, y, 1.0);
-  y = fma(0.5 * y, r, y);
-  r = fma(-x * y, y, 1.0);
-  return fma(0.5 * y, r, y);
+// 1/sqrt(x) from the hardware double-precision estimate (MUFU.RSQ64H, ~23
+// good bits, no f32 round trip) and two Newton steps (~1 ulp; the CUDA
+// double rsqrt spends ~20 instructions on range handling).  Branch-free:
+// x = 0 or subnormal gives NaN, and the callers send a NaN s to the exact
+// path (s < s_exact is tested as !(s >= s_exact)), which uses rsqrt.
+// Newton in the form y + y (1/2 - (x/2) y y): the same roundings as
+// y + (y/2)(1 - x y y), one multiply fewer.
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  double r = fma(-hx * y, y, 0.5);
+  y = fma(y, r, y);
+  r = fma(-hx * y, y, 0.5);
+  return fma(y, r, y);
+}
+
+// list appends through 32-bit shared addresses (a generic pointer would
+// carry 64-bit arithmetic into the scan loop)
+__device__ __forceinline__ void sts_u32(unsigned a, int v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v)); }
+__device__ __forceinline__ void sts_u8(unsigned a, int v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"((unsigned short)v));
+}
+
+// u += c where p (one predicated DADD; a select would cost two more)
+__device__ __forceinline__ void add_if(double& u, double c, bool p) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q add.rn.f64 %0, %0, %1;\n\t}"
+      : "+d"(u)
+      : "d"(c), "r"((unsigned)p));
 }
 
 struct RangeS {
@@ -142,9 +161,14 @@ __device__ __forceinline__ void radial_tables(const ResidTables& rt, const doubl
   }
   // (pairs outside the support are dropped by the caller's exact test)
   const double y = (s - rt.lo) * yscale;
-  // y >= 0 (NaN only for coincident points, which are never kept): one unsigned clamp
-  const int iv = (int)min((unsigned)(int)y, (unsigned)(rt.ni - 1));
-  const double u = 2.0 * (y - iv) - 1.0;
+  // interval = floor(y) without FP64 conversions: y + 2^52 rounded down holds
+  // floor(y) in its low word (y in [0, 2^31); NaN only for coincident
+  // points, which are never kept); one unsigned clamp to the last interval
+  const double t = __dadd_rd(y, 0x1p52);
+  const unsigned fl = (unsigned)__double2loint(t);
+  const int iv = (int)min(fl, (unsigned)(rt.ni - 1));
+  const double dv = fl == (unsigned)iv ? t - 0x1p52 : (double)(rt.ni - 1);
+  const double u = 2.0 * (y - dv) - 1.0;
   const double2* c = pw + iv * (DEG + 1) * kCopies;  // pw already offset by this lane's copy
   double2 v = c[DEG * kCopies];
 #pragma unroll
@@ -274,7 +298,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     // conservative pre-test (see 2. below)
     float xtf[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
-    for (int ax = 0; ax < DIM; ++ax) xtf[ax] = (float)(xt[ax] - box.c[ax]);
+    for (int ax = 0; ax < DIM; ++ax) xtf[ax] = valid ? (float)(xt[ax] - box.c[ax]) : -1e30f;  // invalid: far away
     double bl[3], bh[3];  // the warp's target bounding box
 #pragma unroll
     for (int ax = 0; ax < DIM; ++ax) {
@@ -378,8 +402,17 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       // and their contributions are added in list order
       auto eval = [&](int i, double* c, bool& near, auto exact) {
         constexpr bool EXACT = decltype(exact)::value;
-        const int a = lsrc[warp][i][lane];
-        const int code = lrng[warp][i][lane];  // image shift (x+1 | y+1 << 2 | z+1 << 4) | fine << 6
+        // free space: the entry is the source index, bit-inverted for the
+        // fine scale; periodic: the index, and the image shift (x+1 | y+1 << 2
+        // | z+1 << 4) | fine << 6 in the byte list
+        int a = lsrc[warp][i][lane];
+        int code = 0;
+        if (PER) {
+          code = lrng[warp][i][lane];
+        } else {
+          code = a < 0 ? 64 : 0;
+          a = a < 0 ? ~a : a;
+        }
         const bool fine = code & 64;
         const double nu = fine ? r_f : r_l, inu = fine ? inv_rf : inv_rl;
         constexpr int RW = Rec<KERNEL, DIM>::kW;
@@ -408,12 +441,12 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         if (DIM == 3) r2 = __dadd_rn(r2, __dmul_rn(x[2], x[2]));
         const bool in = r2 < (fine ? sup2f : sup2l);
         if (in && r2 == 0.0) singular = 1;
-        const double rinv = rsqrt_nr(r2);
+        const double rinv = EXACT ? rsqrt(r2) : rsqrt_fast(r2);
         const double s = (r2 * rinv) * inu;  // nu is a power of two: r * (1/nu) == r / nu
         double fd, fo;
         radial_tables<KERNEL, DEG, EXACT>(rt, s_pw + (lane & (kCopies - 1)), yscale, s, fd, fo, s_cheb, r2, inu);
         assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, nu, rv + DIM, c);
-        near = s < rt.s_exact;
+        near = !(s >= rt.s_exact);  // NaN (subnormal r2) too
         return in && r2 != 0.0;  // c is added only when kept
       };
       unsigned long long nearmask = 0;  // list entries to re-evaluate exactly (kList <= 64)
@@ -438,7 +471,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         }
 #pragma unroll
         for (int q = 0; q < kILP; ++q)
-          if (kp[q]) add(c[q]);
+#pragma unroll
+          for (int j = 0; j < DIM; ++j) add_if(u[j], c[q][j], kp[q]);
       }
       while (__any_sync(0xffffffffu, nearmask != 0)) {  // rare: s < s_exact
         double c[3] = {0.0, 0.0, 0.0};
@@ -507,13 +541,13 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           if (DIM == 3) r2 = __dadd_rn(r2, __dmul_rn(x[2], x[2]));
           const bool in = valid && r2 < sup2l && !(alias && a == t);
           if (in && r2 == 0.0) singular = 1;
-          const double rinv = rsqrt_nr(r2);
+          const double rinv = EXACT ? rsqrt(r2) : rsqrt_fast(r2);
           const double sc = (r2 * rinv) * inv_rl;
           double fd, fo;
           radial_tables<KERNEL, DEG, EXACT>(rt, s_pw + (lane & (kCopies - 1)), yscale, sc, fd, fo, s_cheb, r2,
                                             inv_rl);
           assemble<KERNEL, DIM>(fd, fo, x, rinv, sc, rt.support, r_l, sv + DIM, c);
-          near = sc < rt.s_exact;
+          near = !(sc >= rt.s_exact);  // NaN (subnormal r2) too
           return in && r2 != 0.0;  // c is added only when kept
         };
         unsigned nearbits = 0;  // sources of this round to re-evaluate exactly
@@ -531,8 +565,10 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
             nearbits |= 1u << (j + 1);
             k1 = false;
           }
-          if (k0) add(c0);
-          if (k1) add(c1);
+#pragma unroll
+          for (int q = 0; q < DIM; ++q) add_if(u[q], c0[q], k0);
+#pragma unroll
+          for (int q = 0; q < DIM; ++q) add_if(u[q], c1[q], k1);
         }
         while (__any_sync(0xffffffffu, nearbits != 0)) {  // rare: s < s_exact
           double c[3] = {0.0, 0.0, 0.0};
@@ -547,6 +583,12 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         __syncwarp();  // the next round overwrites the buffer
       }
     }
+    // this lane's list (shared addresses): entry k at ls0 + 128 k, lr0 + 32 k
+    const unsigned ls0 = (unsigned)__cvta_generic_to_shared(&lsrc[warp][0][lane]);
+    const unsigned lr0 = (unsigned)__cvta_generic_to_shared(&lrng[warp][0][lane]);
+    const unsigned ls_lim = ls0 + 128u * (kList - 4);
+    const unsigned lr_off = lr0 - (ls0 >> 2);  // byte entry k at (address of int entry k) / 4 + lr_off
+    unsigned ls = ls0;
     for (int ib = nself; ib < nivl; ib += 32) {
       const int nb = min(32, nivl - ib);
       const int4 iv = lane < nb ? ivl[ib + lane] : make_int4(0, 0, 0, 0);
@@ -558,6 +600,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           px = spx[s_ + lane];
           py = spy[s_ + lane];
           if (DIM == 3) pz = spz[s_ + lane];
+        } else {  // past the interval's end: far away, fails every pre-test
+          px = py = pz = 1e30;
         }
       };
       load(s, e);
@@ -577,7 +621,9 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         const int meta = __shfl_sync(0xffffffffu, iv.z, ci);
         const int code = meta & 127;
         const float sup2 = (meta & 64) ? sup2f_hi : sup2l_hi;
-        const bool skip_self = alias && (meta & 256);
+        const int enc0 = (meta & 64) ? ~cs : cs, enc_sign = (meta & 64) ? -1 : 1;  // free-space entry encoding
+        // (no self range here: it is the first range, its intervals are the
+        // first nself, and the dense rounds above took them)
         const int nv = min(32, ce - cs);
         // this lane's source of the round, shifted and relative to the leaf centre
         float cxf, cyf, czf = 0.0f;
@@ -590,30 +636,40 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           cyf = (float)(cy - box.c[1]);
           if (DIM == 3) czf = (float)(cz - box.c[2]);
         }
+        // (lanes past nv hold far-away sources and invalid targets a far-away
+        // target, so the pre-test alone decides; jj <= 31 as 32 % 4 == 0)
         for (int j = 0; j < nv; j += 4) {
-          if (__any_sync(0xffffffffu, cnt > kList - 4)) flush();
+          if (__any_sync(0xffffffffu, ls > ls_lim)) {
+            cnt = (int)(ls - ls0) >> 7;
+            flush();
+            ls = ls0;
+          }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int jj = j + q;
-            const float sx = __shfl_sync(0xffffffffu, cxf, jj & 31);
-            const float sy = __shfl_sync(0xffffffffu, cyf, jj & 31);
-            const float sz = DIM == 3 ? __shfl_sync(0xffffffffu, czf, jj & 31) : 0.0f;
+            const float sx = __shfl_sync(0xffffffffu, cxf, jj);
+            const float sy = __shfl_sync(0xffffffffu, cyf, jj);
+            const float sz = DIM == 3 ? __shfl_sync(0xffffffffu, czf, jj) : 0.0f;
             const float x0 = xtf[0] - sx, x1 = xtf[1] - sy;
             float r2 = x0 * x0 + x1 * x1;
             if (DIM == 3) {
               const float x2 = xtf[2] - sz;
               r2 += x2 * x2;
             }
-            const int a = cs + jj;
-            if (jj < nv && valid && r2 < sup2 && !(skip_self && a == t)) {
-              lsrc[warp][cnt][lane] = a;
-              lrng[warp][cnt][lane] = (unsigned char)code;
-              ++cnt;
+            if (r2 < sup2) {
+              if (PER) {
+                sts_u32(ls, cs + jj);
+                sts_u8((ls >> 2) + lr_off, code);
+              } else {
+                sts_u32(ls, enc0 + enc_sign * jj);
+              }
+              ls += 32 * sizeof(int);
             }
           }
         }
       }
     }
+    cnt = (int)(ls - ls0) >> 7;
     flush();
     if (valid) {
       double* ut = ures + (size_t)tperm[t] * DIM;
