@@ -181,11 +181,14 @@ __device__ __forceinline__ void radial_tables(const ResidTables& rt, const doubl
   fo = v.y;
 }
 
-// residual_apply assembly (split.cpp:258-317) given the radial table values;
-// rinv = 1/r from rsqrt, so 1/r, 1/r^2, 1/r^3, 1/r^5 are products.
+// residual_apply assembly (split.cpp:258-317) given the radial table values,
+// added into u when keep; rinv = 1/r from rsqrt, so 1/r, 1/r^2, 1/r^3, 1/r^5
+// are products.  Stokeslet / stresslet: the pair's two scalar amplitudes are
+// zeroed when the pair is not kept and the terms are fused into u (every
+// other factor is finite, so a dropped pair adds exact zeros).
 template <int KERNEL, int DIM>
 __device__ __forceinline__ void assemble(double fd, double fo, const double* x, double rinv, double s,
-                                         double support, double nu, const double* sv, double* u) {  // u: this pair's contribution (assigned)
+                                         double support, double nu, const double* sv, double* u, bool keep) {
   constexpr double k8pi = 1.0 / (8.0 * dev::kPI), k4pi = 1.0 / (4.0 * dev::kPI);
   const double rinv2 = rinv * rinv;
   if (KERNEL == 0) {  // Stokeslet
@@ -198,9 +201,9 @@ __device__ __forceinline__ void assemble(double fd, double fo, const double* x, 
       f[i] = sv[i];
       xf += x[i] * f[i];
     }
-    const double cd = amp * fd * c0, cf = amp * fo * c0 * xf * rinv2;
+    const double cd = keep ? amp * fd * c0 : 0.0, cf = keep ? amp * fo * c0 * xf * rinv2 : 0.0;
 #pragma unroll
-    for (int j = 0; j < DIM; ++j) u[j] = cd * f[j] + cf * x[j];
+    for (int j = 0; j < DIM; ++j) u[j] = fma(cd, f[j], fma(cf, x[j], u[j]));
   } else if (KERNEL == 1) {  // stresslet
     const double amp = DIM == 2 ? nu : 1.0;
     double f[DIM], nn[DIM], xf = 0.0, xn = 0.0, fn = 0.0;
@@ -213,22 +216,25 @@ __device__ __forceinline__ void assemble(double fd, double fo, const double* x, 
       fn += f[i] * nn[i];
     }
     const double rinv3 = rinv2 * rinv;
-    const double cd = amp * fd * k8pi * rinv3;
-    const double co = -3.0 * k4pi * amp * fo * xf * xn * rinv3 * rinv2;
+    const double cd = keep ? amp * fd * k8pi * rinv3 : 0.0;
+    const double co = keep ? -3.0 * k4pi * amp * fo * xf * xn * rinv3 * rinv2 : 0.0;
 #pragma unroll
-    for (int j = 0; j < DIM; ++j) u[j] = cd * (f[j] * xn + x[j] * fn + nn[j] * xf) + co * x[j];
+    for (int j = 0; j < DIM; ++j) u[j] = fma(cd, f[j] * xn + x[j] * fn + nn[j] * xf, fma(co, x[j], u[j]));
   } else {  // rotlet
+    double c[3];
     if (DIM == 2) {
       const double c0 = fo * sv[0] * k4pi * rinv2;
-      u[0] = c0 * x[1];
-      u[1] = -(c0 * x[0]);
+      c[0] = c0 * x[1];
+      c[1] = -(c0 * x[0]);
     } else {
       const double c0 = fo * k8pi * rinv2 * rinv;
       const double g0 = sv[0], g1 = sv[1], g2 = sv[2];
-      u[0] = c0 * (g1 * x[2] - g2 * x[1]);
-      u[1] = c0 * (g2 * x[0] - g0 * x[2]);
-      u[DIM - 1] = c0 * (g0 * x[1] - g1 * x[0]);
+      c[0] = c0 * (g1 * x[2] - g2 * x[1]);
+      c[1] = c0 * (g2 * x[0] - g0 * x[2]);
+      c[DIM - 1] = c0 * (g0 * x[1] - g1 * x[0]);
     }
+#pragma unroll
+    for (int j = 0; j < DIM; ++j) add_if(u[j], c[j], keep);
   }
 }
 
@@ -387,10 +393,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     // ~10% of the kernel).  Pairs with s < s_exact (rare) are evaluated after
     // their round / list pass with the reference's own tables and recurrence.
     double u[3] = {0.0, 0.0, 0.0};
-    auto add = [&](const double* c) {
-#pragma unroll
-      for (int j = 0; j < DIM; ++j) u[j] += c[j];
-    };
+    unsigned n_in32 = 0;  // this chunk's in-support pairs (this lane)
     int cnt = 0;
     const double sup2l = (r_l * rt.support) * (r_l * rt.support);
     const double sup2f = (r_f * rt.support) * (r_f * rt.support);
@@ -400,7 +403,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       // kILP list entries per step: independent dependency chains interleave,
       // and their contributions are added in list order
-      auto eval = [&](int i, double* c, bool& near, auto exact) {
+      // returns bit 0: in the support (counted), bit 1: deferred to the exact pass
+      auto eval = [&](int i, bool use, auto exact) -> int {
         constexpr bool EXACT = decltype(exact)::value;
         // free space: the entry is the source index, bit-inverted for the
         // fine scale; periodic: the index, and the image shift (x+1 | y+1 << 2
@@ -439,49 +443,33 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         }
         double r2 = __dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[1], x[1]));
         if (DIM == 3) r2 = __dadd_rn(r2, __dmul_rn(x[2], x[2]));
-        const bool in = r2 < (fine ? sup2f : sup2l);
+        const bool in = use && r2 < (fine ? sup2f : sup2l);
         if (in && r2 == 0.0) singular = 1;
         const double rinv = EXACT ? rsqrt(r2) : rsqrt_fast(r2);
         const double s = (r2 * rinv) * inu;  // nu is a power of two: r * (1/nu) == r / nu
+        const bool kept = in && r2 != 0.0;
+        const bool near = !EXACT && !(s >= rt.s_exact);  // NaN (subnormal r2) too
         double fd, fo;
         radial_tables<KERNEL, DEG, EXACT>(rt, s_pw + (lane & (kCopies - 1)), yscale, s, fd, fo, s_cheb, r2, inu);
-        assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, nu, rv + DIM, c);
-        near = !(s >= rt.s_exact);  // NaN (subnormal r2) too
-        return in && r2 != 0.0;  // c is added only when kept
+        assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, nu, rv + DIM, u, kept && !near);
+        return (kept ? 1 : 0) | (kept && near ? 2 : 0);
       };
       unsigned long long nearmask = 0;  // list entries to re-evaluate exactly (kList <= 64)
-      for (int i = 0; i < mx; i += kILP) {  // all evaluations unconditional (clamped), straight-line
-        double c[kILP][3];
-        bool kp[kILP], nr[kILP];
+      if (cnt > 0) {
+        for (int i = 0; i < mx; i += kILP) {  // all evaluations unconditional (clamped), straight-line
 #pragma unroll
-        for (int q = 0; q < kILP; ++q) {
-          c[q][0] = c[q][1] = c[q][2] = 0.0;
-          kp[q] = nr[q] = false;
-        }
-        if (cnt > 0) {
-#pragma unroll
-          for (int q = 0; q < kILP; ++q) {
-            kp[q] = eval(min(i + q, cnt - 1), c[q], nr[q], std::false_type{}) && i + q < cnt;
-            if (kp[q]) ++n_in;
-            if (kp[q] && nr[q]) {
-              nearmask |= 1ull << (i + q);
-              kp[q] = false;
-            }
+          for (int q = 0; q < kILP; ++q) {  // in list order
+            const int st = eval(min(i + q, cnt - 1), i + q < cnt, std::false_type{});
+            n_in32 += st & 1;
+            nearmask |= (unsigned long long)(st >> 1) << (i + q);
           }
         }
-#pragma unroll
-        for (int q = 0; q < kILP; ++q)
-#pragma unroll
-          for (int j = 0; j < DIM; ++j) add_if(u[j], c[q][j], kp[q]);
       }
       while (__any_sync(0xffffffffu, nearmask != 0)) {  // rare: s < s_exact
-        double c[3] = {0.0, 0.0, 0.0};
-        bool nr = false;
         if (nearmask) {
           const int i = __ffsll(nearmask) - 1;
           nearmask &= nearmask - 1;
-          eval(i, c, nr, std::true_type{});
-          add(c);
+          eval(i, true, std::true_type{});
         }
       }
       cnt = 0;
@@ -523,7 +511,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           for (int k = 0; k < RW / 2; ++k) rb[lane * (RW / 2) + k] = rp[k];
         }
         __syncwarp();
-        auto dense = [&](int j, double* c, bool& near, auto exact) {
+        // returns bit 0: in the support (counted), bit 1: deferred to the exact pass
+        auto dense = [&](int j, bool use, auto exact) -> int {
           constexpr bool EXACT = decltype(exact)::value;
           double sv[RW];
 #pragma unroll
@@ -539,45 +528,30 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           if (DIM == 3) x[2] = xt[2] - sv[2];
           double r2 = __dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[1], x[1]));
           if (DIM == 3) r2 = __dadd_rn(r2, __dmul_rn(x[2], x[2]));
-          const bool in = valid && r2 < sup2l && !(alias && a == t);
+          const bool in = use && valid && r2 < sup2l && !(alias && a == t);
           if (in && r2 == 0.0) singular = 1;
           const double rinv = EXACT ? rsqrt(r2) : rsqrt_fast(r2);
           const double sc = (r2 * rinv) * inv_rl;
+          const bool kept = in && r2 != 0.0;
+          const bool near = !EXACT && !(sc >= rt.s_exact);  // NaN (subnormal r2) too
           double fd, fo;
           radial_tables<KERNEL, DEG, EXACT>(rt, s_pw + (lane & (kCopies - 1)), yscale, sc, fd, fo, s_cheb, r2,
                                             inv_rl);
-          assemble<KERNEL, DIM>(fd, fo, x, rinv, sc, rt.support, r_l, sv + DIM, c);
-          near = !(sc >= rt.s_exact);  // NaN (subnormal r2) too
-          return in && r2 != 0.0;  // c is added only when kept
+          assemble<KERNEL, DIM>(fd, fo, x, rinv, sc, rt.support, r_l, sv + DIM, u, kept && !near);
+          return (kept ? 1 : 0) | (kept && near ? 2 : 0);
         };
         unsigned nearbits = 0;  // sources of this round to re-evaluate exactly
         for (int j = 0; j < nv; j += 2) {
-          double c0[3] = {0.0, 0.0, 0.0}, c1[3] = {0.0, 0.0, 0.0};
-          bool n0, n1;
-          bool k0 = dense(j, c0, n0, std::false_type{});
-          bool k1 = dense(min(j + 1, nv - 1), c1, n1, std::false_type{}) && j + 1 < nv;
-          n_in += (k0 ? 1 : 0) + (k1 ? 1 : 0);
-          if (k0 && n0) {
-            nearbits |= 1u << j;
-            k0 = false;
-          }
-          if (k1 && n1) {
-            nearbits |= 1u << (j + 1);
-            k1 = false;
-          }
-#pragma unroll
-          for (int q = 0; q < DIM; ++q) add_if(u[q], c0[q], k0);
-#pragma unroll
-          for (int q = 0; q < DIM; ++q) add_if(u[q], c1[q], k1);
+          const int s0 = dense(j, true, std::false_type{});
+          const int s1 = dense(min(j + 1, nv - 1), j + 1 < nv, std::false_type{});
+          n_in32 += (s0 & 1) + (s1 & 1);
+          nearbits |= ((unsigned)(s0 >> 1) << j) | ((unsigned)(s1 >> 1) << (j + 1));
         }
         while (__any_sync(0xffffffffu, nearbits != 0)) {  // rare: s < s_exact
-          double c[3] = {0.0, 0.0, 0.0};
-          bool nr = false;
           if (nearbits) {
             const int j = __ffs(nearbits) - 1;
             nearbits &= nearbits - 1;
-            dense(j, c, nr, std::true_type{});
-            add(c);
+            dense(j, true, std::true_type{});
           }
         }
         __syncwarp();  // the next round overwrites the buffer
@@ -680,6 +654,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         ut[j] = v;
       }
     }
+    n_in += n_in32;
     __syncwarp();  // the interval list is rewritten by the next chunk
   }
   if (singular) atomicOr(flags, 1);
