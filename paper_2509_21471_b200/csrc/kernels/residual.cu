@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <type_traits>
+#include <cstdio>
 
 namespace sdmkb {
 
@@ -51,12 +52,15 @@ constexpr int kList = SDMK_RES_LIST;  // per-lane list capacity (entries): longe
 constexpr int kMaxRanges = 160;
 constexpr int kMaxIvl = kMaxRanges * 8;  // source intervals per chunk: ranges x Morton sub-cells
 constexpr int kResBlocksPerSM = 1;       // persistent grid (registers and shared memory: 1 per SM)
+constexpr int kGCap = 256;               // per-lane global candidate list (entries; even)
 constexpr int kMaxPW = 896;      // ni * (deg + 1) <= 896 (d, o) coefficient pairs (8 copies: 112 KB)
 constexpr int kCopies = 8;       // table copies, one per 16-byte bank group
-#ifndef SDMK_RES_ILP
-#define SDMK_RES_ILP 2
+#ifdef SDMK_RES_DEBUG
+__device__ unsigned long long g_rdbg[8];  // dense slots, dense kept, list slots, list entries, flushes, chunks
+#define RDBG(i, v) atomicAdd(&g_rdbg[i], (unsigned long long)(v))
+#else
+#define RDBG(i, v)
 #endif
-constexpr int kILP = SDMK_RES_ILP;  // list entries evaluated per step (independent chains)
 
 // Packed source record (coordinates, then strengths), padded to an even
 // number of doubles: the pair evaluation gathers one record with 16-byte loads
@@ -252,6 +256,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
                                                       const int* __restrict__ tperm, int alias, double self_const,
                                                       double* __restrict__ ures, int* flags,
                                                       unsigned long long* stats, int4* __restrict__ ivl_all,
+                                                      int* __restrict__ glist, unsigned char* __restrict__ glcode,
                                                       int* __restrict__ next_chunk) {
   extern __shared__ __align__(16) double2 dyn2[];  // [npw][kCopies] table, then the lists
   double2* s_pw = dyn2;
@@ -394,85 +399,121 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     // their round / list pass with the reference's own tables and recurrence.
     double u[3] = {0.0, 0.0, 0.0};
     unsigned n_in32 = 0;  // this chunk's in-support pairs (this lane)
-    int cnt = 0;
     const double sup2l = (r_l * rt.support) * (r_l * rt.support);
     const double sup2f = (r_f * rt.support) * (r_f * rt.support);
-    auto flush = [&]() {
-      int mx = cnt;
+    // Candidate lists: each lane appends its candidates to a short list in
+    // shared memory (kList entries, lane-interleaved); when any lane's list is
+    // nearly full the warp spills every lane's list to the lane's own list in
+    // global scratch (kGCap entries, L2-resident) and carries on.  The
+    // candidates are evaluated once per chunk, in lockstep, from the global
+    // lists: during the scan the lanes fill unevenly (a source sub-cell is
+    // near some of the warp's targets and not others), but per chunk every
+    // target's total is similar, so lockstep padding stays small.
+    int* __restrict__ gl = glist + ((size_t)(blockIdx.x * kWarps + warp) * 32 + lane) * kGCap;
+    unsigned char* __restrict__ glc = glcode + (PER ? ((size_t)(blockIdx.x * kWarps + warp) * 32 + lane) * kGCap : 0);
+    int gcnt = 0;
+    // free space: the entry is the source index, bit-inverted for the fine
+    // scale; periodic: the index, and the image shift (x+1 | y+1 << 2 | z+1
+    // << 4) | fine << 6 in the code list
+    // returns bit 0: in the support (counted), bit 1: deferred to the exact pass
+    auto eval = [&](int a, int code, bool use, auto exact) -> int {
+      constexpr bool EXACT = decltype(exact)::value;
+      if (!PER) {
+        code = a < 0 ? 64 : 0;
+        a = a < 0 ? ~a : a;
+      }
+      const bool fine = code & 64;
+      const double nu = fine ? r_f : r_l, inu = fine ? inv_rf : inv_rl;
+      constexpr int RW = Rec<KERNEL, DIM>::kW;
+      double rv[RW];
+      const double2* rp = srec + (size_t)a * (RW / 2);
+#pragma unroll
+      for (int k = 0; k < RW / 2; ++k) {
+        const double2 v = rp[k];
+        rv[2 * k] = v.x;
+        rv[2 * k + 1] = v.y;
+      }
+      // the reference's arithmetic (dmk.cpp:1003-1008): x = xt - (xs + shift),
+      // r2 = ((x0 x0 + x1 x1) + x2 x2), every operation rounded (no FMA), so
+      // the exact support test and the coincidence test decide as it does
+      double x[3] = {0.0, 0.0, 0.0};
+      if (PER) {
+        x[0] = xt[0] - (rv[0] + (double)((code & 3) - 1));
+        x[1] = xt[1] - (rv[1] + (double)(((code >> 2) & 3) - 1));
+        if (DIM == 3) x[2] = xt[2] - (rv[2] + (double)(((code >> 4) & 3) - 1));
+      } else {
+        x[0] = xt[0] - rv[0];
+        x[1] = xt[1] - rv[1];
+        if (DIM == 3) x[2] = xt[2] - rv[2];
+      }
+      double r2 = __dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[1], x[1]));
+      if (DIM == 3) r2 = __dadd_rn(r2, __dmul_rn(x[2], x[2]));
+      const bool in = use && r2 < (fine ? sup2f : sup2l);
+      if (in && r2 == 0.0) singular = 1;
+      const double rinv = EXACT ? rsqrt(r2) : rsqrt_fast(r2);
+      const double s = (r2 * rinv) * inu;  // nu is a power of two: r * (1/nu) == r / nu
+      const bool kept = in && r2 != 0.0;
+      const bool near = !EXACT && !(s >= rt.s_exact);  // NaN (subnormal r2) too
+      double fd, fo;
+      radial_tables<KERNEL, DEG, EXACT>(rt, s_pw + (lane & (kCopies - 1)), yscale, s, fd, fo, s_cheb, r2, inu);
+      assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, nu, rv + DIM, u, kept && !near);
+      return (kept ? 1 : 0) | (kept && near ? 2 : 0);
+    };
+    // evaluate the global lists in order (lockstep to the longest), blocks of
+    // 64 entries; each block's near pairs (s < s_exact) are re-evaluated
+    // exactly after it
+    auto eval_global = [&]() {
+      int mx = gcnt;
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      // kILP list entries per step: independent dependency chains interleave,
-      // and their contributions are added in list order
-      // returns bit 0: in the support (counted), bit 1: deferred to the exact pass
-      auto eval = [&](int i, bool use, auto exact) -> int {
-        constexpr bool EXACT = decltype(exact)::value;
-        // free space: the entry is the source index, bit-inverted for the
-        // fine scale; periodic: the index, and the image shift (x+1 | y+1 << 2
-        // | z+1 << 4) | fine << 6 in the byte list
-        int a = lsrc[warp][i][lane];
-        int code = 0;
-        if (PER) {
-          code = lrng[warp][i][lane];
-        } else {
-          code = a < 0 ? 64 : 0;
-          a = a < 0 ? ~a : a;
+      RDBG(2, (unsigned long long)((mx + 1) / 2 * 2));
+      RDBG(3, (unsigned long long)gcnt);
+      if (lane == 0) RDBG(4, 1);
+      for (int b = 0; b < mx; b += 64) {
+        const int bend = min(mx, b + 64);
+        unsigned long long nearmask = 0;
+        int2 cur = *reinterpret_cast<const int2*>(gl + b);
+        uchar2 ccur = PER ? *reinterpret_cast<const uchar2*>(glc + b) : make_uchar2(0, 0);
+        for (int i = b; i < bend; i += 2) {
+          int2 nxt = cur;
+          uchar2 cnxt = ccur;
+          if (i + 2 < bend) {  // the next two entries in flight while these are evaluated
+            nxt = *reinterpret_cast<const int2*>(gl + i + 2);
+            if (PER) cnxt = *reinterpret_cast<const uchar2*>(glc + i + 2);
+          }
+          // in list order; entries past the lane's count are replaced by
+          // source 0 and contribute nothing
+          const bool u0 = i < gcnt, u1 = i + 1 < gcnt;
+          const int s0 = eval(u0 ? cur.x : 0, u0 ? (int)ccur.x : 0, u0, std::false_type{});
+          const int s1 = eval(u1 ? cur.y : 0, u1 ? (int)ccur.y : 0, u1, std::false_type{});
+          n_in32 += (s0 & 1) + (s1 & 1);
+          nearmask |= (unsigned long long)((s0 >> 1) | (s1 & 2)) << (i - b);
+          cur = nxt;
+          ccur = cnxt;
         }
-        const bool fine = code & 64;
-        const double nu = fine ? r_f : r_l, inu = fine ? inv_rf : inv_rl;
-        constexpr int RW = Rec<KERNEL, DIM>::kW;
-        double rv[RW];
-        const double2* rp = srec + (size_t)a * (RW / 2);
-#pragma unroll
-        for (int k = 0; k < RW / 2; ++k) {
-          const double2 v = rp[k];
-          rv[2 * k] = v.x;
-          rv[2 * k + 1] = v.y;
-        }
-        // the reference's arithmetic (dmk.cpp:1003-1008): x = xt - (xs + shift),
-        // r2 = ((x0 x0 + x1 x1) + x2 x2), every operation rounded (no FMA), so
-        // the exact support test and the coincidence test decide as it does
-        double x[3] = {0.0, 0.0, 0.0};
-        if (PER) {
-          x[0] = xt[0] - (rv[0] + (double)((code & 3) - 1));
-          x[1] = xt[1] - (rv[1] + (double)(((code >> 2) & 3) - 1));
-          if (DIM == 3) x[2] = xt[2] - (rv[2] + (double)(((code >> 4) & 3) - 1));
-        } else {
-          x[0] = xt[0] - rv[0];
-          x[1] = xt[1] - rv[1];
-          if (DIM == 3) x[2] = xt[2] - rv[2];
-        }
-        double r2 = __dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[1], x[1]));
-        if (DIM == 3) r2 = __dadd_rn(r2, __dmul_rn(x[2], x[2]));
-        const bool in = use && r2 < (fine ? sup2f : sup2l);
-        if (in && r2 == 0.0) singular = 1;
-        const double rinv = EXACT ? rsqrt(r2) : rsqrt_fast(r2);
-        const double s = (r2 * rinv) * inu;  // nu is a power of two: r * (1/nu) == r / nu
-        const bool kept = in && r2 != 0.0;
-        const bool near = !EXACT && !(s >= rt.s_exact);  // NaN (subnormal r2) too
-        double fd, fo;
-        radial_tables<KERNEL, DEG, EXACT>(rt, s_pw + (lane & (kCopies - 1)), yscale, s, fd, fo, s_cheb, r2, inu);
-        assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, nu, rv + DIM, u, kept && !near);
-        return (kept ? 1 : 0) | (kept && near ? 2 : 0);
-      };
-      unsigned long long nearmask = 0;  // list entries to re-evaluate exactly (kList <= 64)
-      if (cnt > 0) {
-        for (int i = 0; i < mx; i += kILP) {  // all evaluations unconditional (clamped), straight-line
-#pragma unroll
-          for (int q = 0; q < kILP; ++q) {  // in list order
-            const int st = eval(min(i + q, cnt - 1), i + q < cnt, std::false_type{});
-            n_in32 += st & 1;
-            nearmask |= (unsigned long long)(st >> 1) << (i + q);
+        while (__any_sync(0xffffffffu, nearmask != 0)) {  // rare: s < s_exact
+          if (nearmask) {
+            const int i = b + __ffsll(nearmask) - 1;
+            nearmask &= nearmask - 1;
+            eval(gl[i], PER ? (int)glc[i] : 0, true, std::true_type{});
           }
         }
       }
-      while (__any_sync(0xffffffffu, nearmask != 0)) {  // rare: s < s_exact
-        if (nearmask) {
-          const int i = __ffsll(nearmask) - 1;
-          nearmask &= nearmask - 1;
-          eval(i, true, std::true_type{});
+      gcnt = 0;
+    };
+    // move this lane's cnt shared-memory entries to the end of its global list
+    auto spill = [&](int cnt) {
+      if (__any_sync(0xffffffffu, gcnt + cnt > kGCap)) eval_global();  // global list full (dense clusters)
+      int mx = cnt;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      for (int k = 0; k < mx; ++k) {
+        if (k < cnt) {
+          gl[gcnt + k] = lsrc[warp][k][lane];
+          if (PER) glc[gcnt + k] = lrng[warp][k][lane];
         }
       }
-      cnt = 0;
+      gcnt += cnt;
     };
     // 2. Scan: sources arrive in rounds of up to 32, one coalesced load per
     // coordinate (lane j holds source a + j), and are broadcast to every
@@ -545,6 +586,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           const int s0 = dense(j, true, std::false_type{});
           const int s1 = dense(min(j + 1, nv - 1), j + 1 < nv, std::false_type{});
           n_in32 += (s0 & 1) + (s1 & 1);
+          RDBG(0, 2);
+          RDBG(1, (s0 & 1) + (s1 & 1));
           nearbits |= ((unsigned)(s0 >> 1) << j) | ((unsigned)(s1 >> 1) << (j + 1));
         }
         while (__any_sync(0xffffffffu, nearbits != 0)) {  // rare: s < s_exact
@@ -614,8 +657,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         // target, so the pre-test alone decides; jj <= 31 as 32 % 4 == 0)
         for (int j = 0; j < nv; j += 4) {
           if (__any_sync(0xffffffffu, ls > ls_lim)) {
-            cnt = (int)(ls - ls0) >> 7;
-            flush();
+            spill((int)(ls - ls0) >> 7);
             ls = ls0;
           }
 #pragma unroll
@@ -643,8 +685,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         }
       }
     }
-    cnt = (int)(ls - ls0) >> 7;
-    flush();
+    spill((int)(ls - ls0) >> 7);
+    eval_global();
     if (valid) {
       double* ut = ures + (size_t)tperm[t] * DIM;
 #pragma unroll
@@ -655,6 +697,8 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       }
     }
     n_in += n_in32;
+    if (lane == 0) RDBG(5, 1);
+    RDBG(6, valid ? 1 : 0);
     __syncwarp();  // the interval list is rewritten by the next chunk
   }
   if (singular) atomicOr(flags, 1);
@@ -681,7 +725,8 @@ size_t residual_scratch_bytes() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return (size_t)kResBlocksPerSM * sms * kWarps * kMaxIvl * sizeof(int4) + 256;
+  const size_t nw = (size_t)kResBlocksPerSM * sms * kWarps;
+  return nw * kMaxIvl * sizeof(int4) + nw * 32 * kGCap * (sizeof(int) + 1) + 256;
 }
 
 void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves, int nleaf, const int* chunks,
@@ -704,6 +749,9 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
   const int nblk = std::min(kResBlocksPerSM * std::max(1, sms - reserve_sms), (nchunks + kWarps - 1) / kWarps);
   int* next_chunk = reinterpret_cast<int*>(scratch);
   int4* ivl = reinterpret_cast<int4*>(reinterpret_cast<char*>(scratch) + 256);
+  const size_t nw = (size_t)kResBlocksPerSM * sms * kWarps;
+  int* glist = reinterpret_cast<int*>(ivl + nw * kMaxIvl);
+  unsigned char* glcode = reinterpret_cast<unsigned char*>(glist + nw * 32 * kGCap);
   cudaMemsetAsync(next_chunk, 0, sizeof(int), st);
   const int2* ch2 = reinterpret_cast<const int2*>(chunks);
   const size_t dsm = (size_t)kWarps * kList * 32 * (sizeof(int) + 1) +
@@ -727,7 +775,7 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
     k_residual<K, D, G, P><<<nblk, kRBlock, dsm, st>>>(rt, boxes, leaves, ch2, nchunks, rng_start, rng_box,      \
                                                        rng_info, subrange, spts, ns, sstr,                       \
                                                        reinterpret_cast<const double2*>(srec), tpts, nt, tperm,  \
-                                                       alias, self_const, ures, flags, stats, ivl, next_chunk);  \
+                                                       alias, self_const, ures, flags, stats, ivl, glist, glcode, next_chunk);  \
   } while (0)
   if (rt.dim == 3) {
     if (rt.kernel == 0) RES(0, 3);
@@ -741,6 +789,17 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
 #undef RES
 #undef RES1
 #undef RES2
+#ifdef SDMK_RES_DEBUG
+  {
+    unsigned long long h[8];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_rdbg, sizeof(h));
+    fprintf(stderr, "[rdbg] dense_slots %llu dense_kept %llu list_slots %llu list_entries %llu flushes %llu chunks %llu valid_lanes %llu\n",
+            h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_rdbg, z, sizeof(z));
+  }
+#endif
 }
 
 int residual_max_ranges() { return kMaxRanges; }
