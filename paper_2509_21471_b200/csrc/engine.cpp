@@ -1377,8 +1377,20 @@ ResidTables Context::residual_tables(int kernel, int dim) {
   if (nd > kResidMaxCheb || no > kResidMaxCheb) throw RuntimeError("residual table longer than the GPU limit (80)");
   const size_t nall = 2 * (size_t)npw + 2 * kResidMaxCheb;
   double* hc = (double*)pinned_.get("rtab", nall * sizeof(double));
-  std::copy(po.c.begin(), po.c.end(), hc + npw);
-  if (cd) std::copy(pd.c.begin(), pd.c.end(), hc);
+  // the kernel's constant factors folded into the tables (residual_apply,
+  // split.cpp:258-317): 1/(8 pi) for the 3D Stokeslet, 1/(8 pi) and -3/(4 pi)
+  // for the stresslet, 1/(8 pi) (3D) or 1/(4 pi) (2D) for the rotlet; the 2D
+  // Stokeslet's diagonal enters as -2 s log s - table, so it stays unscaled
+  const double k8 = 1.0 / (8.0 * PI), k4 = 1.0 / (4.0 * PI);
+  double sd = 1.0, so = 1.0;
+  if (kernel == kStokeslet) sd = so = dim == 3 ? k8 : 1.0;
+  else if (kernel == kStresslet) sd = k8, so = -3.0 * k4;
+  else so = dim == 3 ? k8 : k4;
+  // the kernel drops pairs past the last interval (s >= hi), where the
+  // reference's residual is zero (s >= support, split.cpp:147-179)
+  if (co->lo != 0.0 || co->hi != T.support) throw RuntimeError("residual table domain is not [0, support]");
+  for (int i = 0; i < npw; ++i) hc[npw + i] = so * po.c[i];
+  if (cd) for (int i = 0; i < npw; ++i) hc[i] = sd * pd.c[i];
   else std::fill(hc, hc + npw, 0.0);
   double* hcheb = hc + 2 * npw;
   std::fill(hcheb, hcheb + 2 * kResidMaxCheb, 0.0);
@@ -1389,7 +1401,7 @@ ResidTables Context::residual_tables(int kernel, int dim) {
   // the first piecewise interval takes the reference's own recurrence (see ResidTables)
   const double s_exact = co->lo + (co->hi - co->lo) / po.ni;
   return ResidTables{po.ni, po.deg, co->lo, co->hi, T.support, kernel, dim, dc, dc + npw,
-                     dc + 2 * npw, dc + 2 * npw + kResidMaxCheb, nd, no, s_exact};
+                     dc + 2 * npw, dc + 2 * npw + kResidMaxCheb, nd, no, s_exact, sd, so};
 }
 
 // ------------------------------------------------------------- entries --

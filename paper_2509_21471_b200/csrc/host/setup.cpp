@@ -720,25 +720,28 @@ PiecewisePoly piecewise_from_cheb(const Cheb& t, int ni, int min_deg, double rel
         for (int j = 0; j < n; ++j) s += fv[j] * std::cos(k * M_PI * (2 * j + 1) / (2.0 * n));
         ch[k] = s * (k == 0 ? 1.0 : 2.0) / n;
       }
-      // Chebyshev -> monomial: T_{k+1} = 2u T_k - T_{k-1}
+      // Chebyshev -> monomials in w = (x - a) / (b - a) in [0, 1] (the kernel's
+      // local coordinate, y - floor(y)): shifted Chebyshev polynomials
+      // T*_0 = 1, T*_1 = 2w - 1, T*_{k+1} = (4w - 2) T*_k - T*_{k-1}
       std::vector<double> Tk0(n, 0.0), Tk1(n, 0.0), Tk2(n, 0.0);
       double* mono = c.data() + (size_t)i * n;
       Tk0[0] = 1.0;
       for (int j = 0; j < n; ++j) mono[j] += ch[0] * Tk0[j];
       if (n > 1) {
-        Tk1[1] = 1.0;
+        Tk1[0] = -1.0;
+        Tk1[1] = 2.0;
         for (int j = 0; j < n; ++j) mono[j] += ch[1] * Tk1[j];
       }
       for (int k = 2; k < n; ++k) {
-        for (int j = 0; j < n; ++j) Tk2[j] = (j ? 2.0 * Tk1[j - 1] : 0.0) - Tk0[j];
+        for (int j = 0; j < n; ++j) Tk2[j] = (j ? 4.0 * Tk1[j - 1] : 0.0) - 2.0 * Tk1[j] - Tk0[j];
         for (int j = 0; j < n; ++j) mono[j] += ch[k] * Tk2[j];
         Tk0 = Tk1;
         Tk1 = Tk2;
       }
       for (int j = 0; j <= 64; ++j) {  // check with the same Horner the kernel uses
-        const double u = -1.0 + 2.0 * j / 64.0, x = 0.5 * (a + b) + 0.5 * (b - a) * u;
+        const double w = j / 64.0, x = a + (b - a) * w;
         double v = mono[deg];
-        for (int k = deg - 1; k >= 0; --k) v = std::fma(v, u, mono[k]);
+        for (int k = deg - 1; k >= 0; --k) v = std::fma(v, w, mono[k]);
         worst = std::max(worst, std::fabs(v - t.eval(x)));
       }
     }

@@ -97,6 +97,8 @@ struct PiecewisePoly {
   double lo = 0.0, hi = 1.0, max_err = 0.0;
   std::vector<double> c;
 };
+// Piecewise monomial re-expansion of a Chebyshev table: ni equal intervals,
+// coefficients in the local coordinate w in [0, 1] of each interval; the
 // lowest degree >= min_deg whose Horner values stay within rel_tol * max(1, max|t|)
 // of the Chebyshev table on every interval (checked at 65 points per interval)
 PiecewisePoly piecewise_from_cheb(const Cheb& t, int ni = 32, int min_deg = 8, double rel_tol = 4e-15);

@@ -643,33 +643,6 @@ void finish_topology(HostTree& t, bool full) {
   t = std::move(B.t);
 }
 
-void leaf_subranges(const HostTree& t, int ns, const int32_t* qs, std::vector<int>& out) {
-  const int nb = t.num_boxes(), nchild = 1 << t.dim;
-  out.assign((size_t)nb * 9, 0);
-  Points S;
-  S.n = ns;
-  S.q = qs;
-#pragma omp parallel for schedule(dynamic, 64)
-  for (int b = 0; b < nb; ++b) {
-    const Box& x = t.boxes[b];
-    int* o = out.data() + (size_t)b * 9;
-    if (!x.leaf || x.se == x.sb || x.level >= kMaxLevel) {
-      for (int c = 0; c <= nchild; ++c) o[c] = c == 0 ? x.sb : x.se;
-      continue;
-    }
-    o[0] = x.sb;
-    for (int ci = 1; ci < nchild; ++ci) {
-      int a = o[ci - 1], e = x.se;
-      while (a < e) {
-        const int m = a + (e - a) / 2;
-        if (S.child(m, x.level, t.dim) < ci) a = m + 1; else e = m;
-      }
-      o[ci] = a;
-    }
-    o[nchild] = x.se;
-  }
-}
-
 std::string dump_topology(const HostTree& t) {  // tree.cpp:325-354
   std::ostringstream os;
   auto lst = [&](const char* tag, NbrSpan v) {

@@ -95,12 +95,6 @@ void finish_topology(HostTree& t, bool full = false);
 // The reference's canonical text dump (tree.cpp:325-354).
 std::string dump_topology(const HostTree& t);
 
-// For every leaf with sources: the 2^d + 1 boundaries of its children's
-// (virtual, level + 1) source sub-ranges, by binary search on the sorted
-// quantized coordinates; out[b * 9 + ci] (leaves at the depth cap get one
-// range).  Used by the residual kernel for sub-cell culling.
-void leaf_subranges(const HostTree& t, int ns, const int32_t* qs, std::vector<int>& out);
-
 // Target-leaf ownership of rank `rank` of `nranks`: the
 // target leaves in Morton order (by the start of their target range) are cut
 // into contiguous runs of about total / nranks cost (a leaf goes to the rank

@@ -166,6 +166,9 @@ struct ResidTables {
   const double* cheb_o;
   int n_d, n_o;
   double s_exact;
+  // the piecewise tables are stored multiplied by these (the kernel's constant
+  // factors, 1 for the 2D Stokeslet); the exact branch scales the same way
+  double scale_d, scale_o;
 };
 constexpr int kResidMaxCheb = 80;  // longest Chebyshev table the exact branch holds in shared memory
 int residual_max_pw();

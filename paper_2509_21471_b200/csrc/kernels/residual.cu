@@ -16,23 +16,29 @@
 //     out-of-support pairs.
 //  3. Other intervals (lists): sources stream in coalesced rounds of 32 and
 //     are broadcast by shuffles; each lane runs a conservative single-
-//     precision pre-test and appends candidates to a lane-private list in
-//     shared memory; full lists are evaluated in lockstep, kILP entries per
-//     step, with the reference's exact double-precision support test
-//     (x = xt - (xs + shift), unfused r2).
+//     precision pre-test and appends candidates to a short lane-private list
+//     in shared memory, spilled to the lane's list in global scratch
+//     (L2-resident) whenever one lane's fills up; the chunk's lists are
+//     evaluated once at its end, in lockstep, two entries per step, with
+//     the reference's exact double-precision support test (x = xt - (xs +
+//     shift), unfused r2).  (Evaluating each shared list when it filled cost
+//     2.6 lockstep slots per candidate: the lanes fill unevenly during the
+//     scan, but per chunk their totals are similar.)
 //  4. Radial tables: a piecewise degree-6 re-expansion of the reference's
-//     Chebyshev tables in shared memory (8 bank-interleaved copies), within
-//     1e-15 of them; pairs in the first interval (s < 1/128, where the
-//     kernels' 1/r^2..1/r^5 factors amplify absolute table errors) are
-//     re-evaluated after their round / list pass with the reference's own
-//     coefficients and Clenshaw recurrence, unfused.  1/r from rsqrt.
+//     Chebyshev tables in the local coordinate w = y - floor(y), scaled by
+//     the kernel's constant factors, in shared memory (8 bank-interleaved
+//     copies), within 2e-15 of them; pairs in the first interval (s < 1/128,
+//     where the kernels' 1/r^2..1/r^5 factors amplify absolute table errors)
+//     are re-evaluated after their round / list block with the reference's
+//     own coefficients and Clenshaw recurrence, unfused.  1/r from rsqrt;
+//     contributions enter by predicated FMAs; support and zero tests on the
+//     bit patterns of r2 (integer pipe).
 // No atomics on the data and a fixed per-target order: bitwise reproducible.
 #include "common.cuh"
 #include "launch.hpp"
 
 #include <algorithm>
 #include <type_traits>
-#include <cstdio>
 
 namespace sdmkb {
 
@@ -55,12 +61,6 @@ constexpr int kResBlocksPerSM = 1;       // persistent grid (registers and share
 constexpr int kGCap = 256;               // per-lane global candidate list (entries; even)
 constexpr int kMaxPW = 896;      // ni * (deg + 1) <= 896 (d, o) coefficient pairs (8 copies: 112 KB)
 constexpr int kCopies = 8;       // table copies, one per 16-byte bank group
-#ifdef SDMK_RES_DEBUG
-__device__ unsigned long long g_rdbg[8];  // dense slots, dense kept, list slots, list entries, flushes, chunks
-#define RDBG(i, v) atomicAdd(&g_rdbg[i], (unsigned long long)(v))
-#else
-#define RDBG(i, v)
-#endif
 
 // Packed source record (coordinates, then strengths), padded to an even
 // number of doubles: the pair evaluation gathers one record with 16-byte loads
@@ -112,6 +112,20 @@ __device__ __forceinline__ void add_if(double& u, double c, bool p) {
       : "d"(c), "r"((unsigned)p));
 }
 
+// r2 < b for r2 >= 0, b > 0: the bit patterns of non-negative doubles order
+// as unsigned integers (integer pipe instead of a DSETP on the FP64 pipe)
+__device__ __forceinline__ bool lt_nonneg(double r2, double b) {
+  return (unsigned long long)__double_as_longlong(r2) < (unsigned long long)__double_as_longlong(b);
+}
+__device__ __forceinline__ bool is_zero_nonneg(double r2) { return __double_as_longlong(r2) == 0; }
+
+// u += a b where p (one predicated DFMA instead of zeroing a factor by selects)
+__device__ __forceinline__ void fma_if(double& u, double a, double b, bool p) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q fma.rn.f64 %0, %1, %2, %0;\n\t}"
+      : "+d"(u)
+      : "d"(a), "d"(b), "r"((unsigned)p));
+}
+
 struct RangeS {
   double sh[3];
   double lo[3], hi[3];
@@ -120,15 +134,19 @@ struct RangeS {
   int code;  // packed image shift (x+1 | y+1 << 2 | z+1 << 4) | fine-scale flag << 6
 };
 
-// Radial table values at s (unit scale) from the piecewise monomial form held
-// in shared memory as (diag, offdiag) pairs, one 16-byte load per degree:
-// interval i = floor((s - lo) ni / (hi - lo)), local u = 2 (frac) - 1,
-// Horner at a compile-time degree (the host pads the table with leading
-// zero coefficients, which leave Horner's value unchanged).  Zero at/after
-// the support (split.cpp:147-179).  The table is stored kCopies times
-// interleaved, copy c in 16-byte bank group c: lane L reads copy L % 8, so
-// the 8 lanes of a 128-bit load phase always hit 8 distinct bank groups
-// whatever intervals they need (no conflicts).
+// Radial table values at table coordinate y = (s - lo) ni / (hi - lo) from
+// the piecewise monomial form held in shared memory as (diag, offdiag) pairs,
+// one 16-byte load per degree: interval i = floor(y), local w = y - i in [0, 1),
+// Horner at a compile-time degree (the host pads the table with leading zero
+// coefficients, which leave Horner's value unchanged).  The host scales both
+// tables by the kernel's constant factor (ResidTables::scale_d / scale_o), so
+// the assembly multiplies by powers of 1/r only.  Returns false at/after the
+// support (y >= ni: the reference's value there is 0, split.cpp:147-179).
+// Returns floor(y) (0xffffffff for NaN y, the canonical NaN's low word):
+// fl >= ni is past the support, fl + 1 <= 1 the first interval or NaN.
+// The table is stored kCopies times interleaved, copy c in 16-byte bank group
+// c: lane L reads copy L % 8, so the 8 lanes of a 128-bit load phase always
+// hit 8 distinct bank groups whatever intervals they need (no conflicts).
 // The reference's Clenshaw (chebyshev.cpp:9-19) in its own operation order,
 // every product and sum rounded separately (the reference is built without
 // FMA contraction).
@@ -145,34 +163,27 @@ __device__ __forceinline__ double clenshaw_ref1(const double* __restrict__ c, in
   return __dadd_rn(__dsub_rn(__dmul_rn(t, b1), b2), c[0]);
 }
 
-__device__ __forceinline__ double2 clenshaw_ref(const double* __restrict__ cheb, int nd, int no, double lo, double hi,
-                                             double r2, double inu) {
-  const double se = __dmul_rn(__dsqrt_rn(r2), inu);  // s = sqrt(r2) / nu as the reference forms it
-  return make_double2(clenshaw_ref1(cheb, nd, lo, hi, se), clenshaw_ref1(cheb + kResidMaxCheb, no, lo, hi, se));
-}
-
 // EXACT: the reference's tables and recurrence (pairs with s < s_exact, rare;
-// re-evaluated after the fast pass so the hot path keeps its registers)
+// re-evaluated after the fast pass so the hot path keeps its registers),
+// scaled as the piecewise tables are
 template <int KERNEL, int DEG, bool EXACT>
-__device__ __forceinline__ void radial_tables(const ResidTables& rt, const double2* __restrict__ pw, double yscale,
-                                              double s, double& fd, double& fo, const double* __restrict__ cheb,
-                                              double r2, double inu) {
+__device__ __forceinline__ unsigned radial_tables(const ResidTables& rt, const double2* __restrict__ pw, double y,
+                                              double& fd, double& fo, const double* __restrict__ cheb, double r2,
+                                              double inu) {
   if (EXACT) {
-    const double2 v = clenshaw_ref(cheb, KERNEL != 2 ? rt.n_d : 0, rt.n_o, rt.lo, rt.hi, r2, inu);
-    fd = v.x;
-    fo = v.y;
-    return;
+    const double se = __dmul_rn(__dsqrt_rn(r2), inu);  // s = sqrt(r2) / nu as the reference forms it
+    fd = KERNEL != 2 ? rt.scale_d * clenshaw_ref1(cheb, rt.n_d, rt.lo, rt.hi, se) : 0.0;
+    fo = rt.scale_o * clenshaw_ref1(cheb + kResidMaxCheb, rt.n_o, rt.lo, rt.hi, se);
+    return 1u;  // inside the table, not in the first interval
   }
-  // (pairs outside the support are dropped by the caller's exact test)
-  const double y = (s - rt.lo) * yscale;
   // interval = floor(y) without FP64 conversions: y + 2^52 rounded down holds
   // floor(y) in its low word (y in [0, 2^31); NaN only for coincident
-  // points, which are never kept); one unsigned clamp to the last interval
+  // points, which are never kept); past the last interval the pair is dropped
+  // (the clamped evaluation below is finite and discarded)
   const double t = __dadd_rd(y, 0x1p52);
   const unsigned fl = (unsigned)__double2loint(t);
   const int iv = (int)min(fl, (unsigned)(rt.ni - 1));
-  const double dv = fl == (unsigned)iv ? t - 0x1p52 : (double)(rt.ni - 1);
-  const double u = 2.0 * (y - dv) - 1.0;
+  const double u = y - (t - 0x1p52);  // exact
   const double2* c = pw + iv * (DEG + 1) * kCopies;  // pw already offset by this lane's copy
   double2 v = c[DEG * kCopies];
 #pragma unroll
@@ -183,31 +194,40 @@ __device__ __forceinline__ void radial_tables(const ResidTables& rt, const doubl
   }
   fd = KERNEL != 2 ? v.x : 0.0;
   fo = v.y;
+  return fl;
 }
 
-// residual_apply assembly (split.cpp:258-317) given the radial table values,
-// added into u when keep; rinv = 1/r from rsqrt, so 1/r, 1/r^2, 1/r^3, 1/r^5
-// are products.  Stokeslet / stresslet: the pair's two scalar amplitudes are
-// zeroed when the pair is not kept and the terms are fused into u (every
-// other factor is finite, so a dropped pair adds exact zeros).
+// residual_apply assembly (split.cpp:258-317) given the radial table values
+// (already scaled by the kernel constants, except the 2D Stokeslet's), added
+// into u when keep by predicated FMAs; rinv = 1/r from rsqrt, so 1/r, 1/r^2,
+// 1/r^3, 1/r^5 are products.
 template <int KERNEL, int DIM>
 __device__ __forceinline__ void assemble(double fd, double fo, const double* x, double rinv, double s,
                                          double support, double nu, const double* sv, double* u, bool keep) {
-  constexpr double k8pi = 1.0 / (8.0 * dev::kPI), k4pi = 1.0 / (4.0 * dev::kPI);
+  constexpr double k8pi = 1.0 / (8.0 * dev::kPI);
   const double rinv2 = rinv * rinv;
   if (KERNEL == 0) {  // Stokeslet
-    if (DIM == 2) fd = s < support ? (s > 0.0 ? -2.0 * s * log(s) : 0.0) - fd : 0.0;  // split.cpp:147-155
-    const double amp = DIM == 2 ? nu : 1.0;
-    const double c0 = k8pi * rinv;
     double f[DIM], xf = 0.0;
 #pragma unroll
     for (int i = 0; i < DIM; ++i) {
       f[i] = sv[i];
       xf += x[i] * f[i];
     }
-    const double cd = keep ? amp * fd * c0 : 0.0, cf = keep ? amp * fo * c0 * xf * rinv2 : 0.0;
+    double cd, cf;
+    if (DIM == 2) {  // fd = -2 s log s - table (split.cpp:147-155); amp = nu; unscaled tables
+      fd = s < support ? (s > 0.0 ? -2.0 * s * log(s) : 0.0) - fd : 0.0;
+      const double c0 = k8pi * rinv;
+      cd = nu * fd * c0;
+      cf = nu * fo * c0 * xf * rinv2;
+    } else {
+      cd = fd * rinv;
+      cf = (fo * rinv) * (xf * rinv2);
+    }
 #pragma unroll
-    for (int j = 0; j < DIM; ++j) u[j] = fma(cd, f[j], fma(cf, x[j], u[j]));
+    for (int j = 0; j < DIM; ++j) {
+      fma_if(u[j], cf, x[j], keep);
+      fma_if(u[j], cd, f[j], keep);
+    }
   } else if (KERNEL == 1) {  // stresslet
     const double amp = DIM == 2 ? nu : 1.0;
     double f[DIM], nn[DIM], xf = 0.0, xn = 0.0, fn = 0.0;
@@ -220,18 +240,21 @@ __device__ __forceinline__ void assemble(double fd, double fo, const double* x, 
       fn += f[i] * nn[i];
     }
     const double rinv3 = rinv2 * rinv;
-    const double cd = keep ? amp * fd * k8pi * rinv3 : 0.0;
-    const double co = keep ? -3.0 * k4pi * amp * fo * xf * xn * rinv3 * rinv2 : 0.0;
+    const double cd = amp * fd * rinv3;
+    const double co = amp * fo * xf * xn * rinv3 * rinv2;
 #pragma unroll
-    for (int j = 0; j < DIM; ++j) u[j] = fma(cd, f[j] * xn + x[j] * fn + nn[j] * xf, fma(co, x[j], u[j]));
+    for (int j = 0; j < DIM; ++j) {
+      fma_if(u[j], co, x[j], keep);
+      fma_if(u[j], cd, f[j] * xn + x[j] * fn + nn[j] * xf, keep);
+    }
   } else {  // rotlet
     double c[3];
     if (DIM == 2) {
-      const double c0 = fo * sv[0] * k4pi * rinv2;
+      const double c0 = fo * sv[0] * rinv2;
       c[0] = c0 * x[1];
       c[1] = -(c0 * x[0]);
     } else {
-      const double c0 = fo * k8pi * rinv2 * rinv;
+      const double c0 = fo * rinv2 * rinv;
       const double g0 = sv[0], g1 = sv[1], g2 = sv[2];
       c[0] = c0 * (g1 * x[2] - g2 * x[1]);
       c[1] = c0 * (g2 * x[0] - g0 * x[2]);
@@ -276,7 +299,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
   }
   __syncthreads();
   int4* __restrict__ ivl = ivl_all + (size_t)(blockIdx.x * kWarps + warp) * kMaxIvl;  // this warp's interval list
-  const double yscale = rt.ni / (rt.hi - rt.lo);
+  const double yscale = rt.ni / (rt.hi - rt.lo), ylo = -rt.lo * yscale;
   const double* __restrict__ spx = spts;
   const double* __restrict__ spy = spts + ns;
   const double* __restrict__ spz = spts + (size_t)(DIM == 3 ? 2 : 1) * ns;
@@ -294,6 +317,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     const DBox box = boxes[leaf];
     const double r_l = box.side, r_f = 0.5 * r_l;
     const double inv_rl = 1.0 / r_l, inv_rf = 1.0 / r_f;
+    const double ysc_l = inv_rl * yscale, ysc_f = inv_rf * yscale;  // exact: 1/nu is a power of two
     const int r0 = rng_start[li], nr = rng_start[li + 1] - r0;
     double selfc = 0.0;
     if (alias && KERNEL == 0) selfc = DIM == 3 ? self_const / r_l : self_const + log(r_l) / (4.0 * dev::kPI);
@@ -412,7 +436,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     int* __restrict__ gl = glist + ((size_t)(blockIdx.x * kWarps + warp) * 32 + lane) * kGCap;
     unsigned char* __restrict__ glc = glcode + (PER ? ((size_t)(blockIdx.x * kWarps + warp) * 32 + lane) * kGCap : 0);
     int gcnt = 0;
-    // free space: the entry is the source index, bit-inverted for the fine
+    // free space: the entry is the source index, bit 31 set for the fine
     // scale; periodic: the index, and the image shift (x+1 | y+1 << 2 | z+1
     // << 4) | fine << 6 in the code list
     // returns bit 0: in the support (counted), bit 1: deferred to the exact pass
@@ -420,7 +444,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       constexpr bool EXACT = decltype(exact)::value;
       if (!PER) {
         code = a < 0 ? 64 : 0;
-        a = a < 0 ? ~a : a;
+        a &= 0x7fffffff;
       }
       const bool fine = code & 64;
       const double nu = fine ? r_f : r_l, inu = fine ? inv_rf : inv_rl;
@@ -448,15 +472,21 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       }
       double r2 = __dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[1], x[1]));
       if (DIM == 3) r2 = __dadd_rn(r2, __dmul_rn(x[2], x[2]));
-      const bool in = use && r2 < (fine ? sup2f : sup2l);
-      if (in && r2 == 0.0) singular = 1;
+      const bool in = use && lt_nonneg(r2, fine ? sup2f : sup2l);
+      const bool zero = is_zero_nonneg(r2);
+      if (in && zero) singular = 1;
       const double rinv = EXACT ? rsqrt(r2) : rsqrt_fast(r2);
-      const double s = (r2 * rinv) * inu;  // nu is a power of two: r * (1/nu) == r / nu
-      const bool kept = in && r2 != 0.0;
-      const bool near = !EXACT && !(s >= rt.s_exact);  // NaN (subnormal r2) too
+      // table coordinate y = (s - lo) ni / (hi - lo), s = r / nu (nu is a power
+      // of two: r * (1/nu) == r / nu); the first interval (y < 1) goes exact
+      const double r = r2 * rinv;
+      const double y = fma(r, fine ? ysc_f : ysc_l, ylo);
+      const double s = DIM == 2 && KERNEL == 0 ? r * inu : 0.0;
+      const bool kept = in && !zero;
       double fd, fo;
-      radial_tables<KERNEL, DEG, EXACT>(rt, s_pw + (lane & (kCopies - 1)), yscale, s, fd, fo, s_cheb, r2, inu);
-      assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, nu, rv + DIM, u, kept && !near);
+      const unsigned fl = radial_tables<KERNEL, DEG, EXACT>(rt, s_pw + (lane & (kCopies - 1)), y, fd, fo, s_cheb, r2, inu);
+      const bool tab = fl < (unsigned)rt.ni;
+      const bool near = !EXACT && fl + 1u <= 1u;  // y < 1, or NaN (subnormal r2)
+      assemble<KERNEL, DIM>(fd, fo, x, rinv, s, rt.support, nu, rv + DIM, u, kept && tab && !near);
       return (kept ? 1 : 0) | (kept && near ? 2 : 0);
     };
     // evaluate the global lists in order (lockstep to the longest), blocks of
@@ -466,9 +496,6 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       int mx = gcnt;
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      RDBG(2, (unsigned long long)((mx + 1) / 2 * 2));
-      RDBG(3, (unsigned long long)gcnt);
-      if (lane == 0) RDBG(4, 1);
       for (int b = 0; b < mx; b += 64) {
         const int bend = min(mx, b + 64);
         unsigned long long nearmask = 0;
@@ -569,16 +596,20 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           if (DIM == 3) x[2] = xt[2] - sv[2];
           double r2 = __dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[1], x[1]));
           if (DIM == 3) r2 = __dadd_rn(r2, __dmul_rn(x[2], x[2]));
-          const bool in = use && valid && r2 < sup2l && !(alias && a == t);
-          if (in && r2 == 0.0) singular = 1;
+          const bool in = use && valid && lt_nonneg(r2, sup2l) && !(alias && a == t);
+          const bool zero = is_zero_nonneg(r2);
+          if (in && zero) singular = 1;
           const double rinv = EXACT ? rsqrt(r2) : rsqrt_fast(r2);
-          const double sc = (r2 * rinv) * inv_rl;
-          const bool kept = in && r2 != 0.0;
-          const bool near = !EXACT && !(sc >= rt.s_exact);  // NaN (subnormal r2) too
+          const double r = r2 * rinv;
+          const double y = fma(r, ysc_l, ylo);
+          const double sc = DIM == 2 && KERNEL == 0 ? r * inv_rl : 0.0;
+          const bool kept = in && !zero;
           double fd, fo;
-          radial_tables<KERNEL, DEG, EXACT>(rt, s_pw + (lane & (kCopies - 1)), yscale, sc, fd, fo, s_cheb, r2,
-                                            inv_rl);
-          assemble<KERNEL, DIM>(fd, fo, x, rinv, sc, rt.support, r_l, sv + DIM, u, kept && !near);
+          const unsigned fl =
+              radial_tables<KERNEL, DEG, EXACT>(rt, s_pw + (lane & (kCopies - 1)), y, fd, fo, s_cheb, r2, inv_rl);
+          const bool tab = fl < (unsigned)rt.ni;
+          const bool near = !EXACT && fl + 1u <= 1u;  // y < 1, or NaN (subnormal r2)
+          assemble<KERNEL, DIM>(fd, fo, x, rinv, sc, rt.support, r_l, sv + DIM, u, kept && tab && !near);
           return (kept ? 1 : 0) | (kept && near ? 2 : 0);
         };
         unsigned nearbits = 0;  // sources of this round to re-evaluate exactly
@@ -586,8 +617,6 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           const int s0 = dense(j, true, std::false_type{});
           const int s1 = dense(min(j + 1, nv - 1), j + 1 < nv, std::false_type{});
           n_in32 += (s0 & 1) + (s1 & 1);
-          RDBG(0, 2);
-          RDBG(1, (s0 & 1) + (s1 & 1));
           nearbits |= ((unsigned)(s0 >> 1) << j) | ((unsigned)(s1 >> 1) << (j + 1));
         }
         while (__any_sync(0xffffffffu, nearbits != 0)) {  // rare: s < s_exact
@@ -603,7 +632,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
     // this lane's list (shared addresses): entry k at ls0 + 128 k, lr0 + 32 k
     const unsigned ls0 = (unsigned)__cvta_generic_to_shared(&lsrc[warp][0][lane]);
     const unsigned lr0 = (unsigned)__cvta_generic_to_shared(&lrng[warp][0][lane]);
-    const unsigned ls_lim = ls0 + 128u * (kList - 4);
+    const unsigned ls_lim = ls0 + 128u * (kList - 8);
     const unsigned lr_off = lr0 - (ls0 >> 2);  // byte entry k at (address of int entry k) / 4 + lr_off
     unsigned ls = ls0;
     for (int ib = nself; ib < nivl; ib += 32) {
@@ -638,7 +667,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
         const int meta = __shfl_sync(0xffffffffu, iv.z, ci);
         const int code = meta & 127;
         const float sup2 = (meta & 64) ? sup2f_hi : sup2l_hi;
-        const int enc0 = (meta & 64) ? ~cs : cs, enc_sign = (meta & 64) ? -1 : 1;  // free-space entry encoding
+        const int encb = (meta & 64) ? (int)((unsigned)cs | 0x80000000u) : cs;  // free-space entry: + jj
         // (no self range here: it is the first range, its intervals are the
         // first nself, and the dense rounds above took them)
         const int nv = min(32, ce - cs);
@@ -654,14 +683,14 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
           if (DIM == 3) czf = (float)(cz - box.c[2]);
         }
         // (lanes past nv hold far-away sources and invalid targets a far-away
-        // target, so the pre-test alone decides; jj <= 31 as 32 % 4 == 0)
-        for (int j = 0; j < nv; j += 4) {
+        // target, so the pre-test alone decides; jj <= 31 as 32 % 8 == 0)
+        for (int j = 0; j < nv; j += 8) {
           if (__any_sync(0xffffffffu, ls > ls_lim)) {
             spill((int)(ls - ls0) >> 7);
             ls = ls0;
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < 8; ++q) {
             const int jj = j + q;
             const float sx = __shfl_sync(0xffffffffu, cxf, jj);
             const float sy = __shfl_sync(0xffffffffu, cyf, jj);
@@ -677,7 +706,7 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
                 sts_u32(ls, cs + jj);
                 sts_u8((ls >> 2) + lr_off, code);
               } else {
-                sts_u32(ls, enc0 + enc_sign * jj);
+                sts_u32(ls, encb + jj);
               }
               ls += 32 * sizeof(int);
             }
@@ -697,8 +726,6 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       }
     }
     n_in += n_in32;
-    if (lane == 0) RDBG(5, 1);
-    RDBG(6, valid ? 1 : 0);
     __syncwarp();  // the interval list is rewritten by the next chunk
   }
   if (singular) atomicOr(flags, 1);
@@ -789,17 +816,6 @@ void launch_residual(const ResidTables& rt, const DBox* boxes, const int* leaves
 #undef RES
 #undef RES1
 #undef RES2
-#ifdef SDMK_RES_DEBUG
-  {
-    unsigned long long h[8];
-    cudaStreamSynchronize(st);
-    cudaMemcpyFromSymbol(h, g_rdbg, sizeof(h));
-    fprintf(stderr, "[rdbg] dense_slots %llu dense_kept %llu list_slots %llu list_entries %llu flushes %llu chunks %llu valid_lanes %llu\n",
-            h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
-    unsigned long long z[8] = {0};
-    cudaMemcpyToSymbol(g_rdbg, z, sizeof(z));
-  }
-#endif
 }
 
 int residual_max_ranges() { return kMaxRanges; }
