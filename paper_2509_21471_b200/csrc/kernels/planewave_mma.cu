@@ -441,6 +441,11 @@ __global__ void __launch_bounds__(kWZF * 32, 1) k_zf3(PWGrid g, int nc, int nbox
     Ai[e] = vi;
   }
   for (int e = lane; e < 2 * P8 * kZR; e += 32) Bs[e] = make_double2(0.0, 0.0);  // rows iz >= pz stay 0
+  __shared__ int s_ncol[33], s_off[33];  // slab table (mz + M), read per output element
+  if (tid < 2 * M + 1) {
+    s_ncol[tid] = g.slab_ncol[tid];
+    s_off[tid] = g.slab_off[tid];
+  }
   __syncthreads();
   const int ncbk = (ncol + kZB - 1) / kZB, total = nbox * nc * ncbk;
   const int nw = gridDim.x * kWZF;
@@ -501,8 +506,8 @@ __global__ void __launch_bounds__(kWZF * 32, 1) k_zf3(PWGrid g, int nc, int nbox
     for (int i = 0; i < MTC; ++i) {
       const int mz = i * 8 + gq + 1;
       if (mz > M) continue;
-      const int np = g.slab_ncol[mz + M], nm = g.slab_ncol[M - mz];
-      const int op = g.slab_off[mz + M], om = g.slab_off[M - mz];
+      const int np = s_ncol[mz + M], nm = s_ncol[M - mz];
+      const int op = s_off[mz + M], om = s_off[M - mz];
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -514,13 +519,13 @@ __global__ void __launch_bounds__(kWZF * 32, 1) k_zf3(PWGrid g, int nc, int nbox
           if (col < nm) dst[om + col] = make_double2(p_ + q_, r_ - s_);
         }
     }
-    if (lane < ncb && c0 + lane < g.slab_ncol[M]) {  // mz = 0: column sums over iz
+    if (lane < ncb && c0 + lane < s_ncol[M]) {  // mz = 0: column sums over iz
       double re = 0.0, im = 0.0;
       for (int k = 0; k < pz; ++k) {
         re += Bb[k * kZR + lane].x;
         im += Bb[k * kZR + lane].y;
       }
-      dst[g.slab_off[M] + c0 + lane] = make_double2(re, im);
+      dst[s_off[M] + c0 + lane] = make_double2(re, im);
     }
     __syncwarp();  // this buffer is refilled by the issue two units ahead
   }
@@ -549,6 +554,11 @@ __global__ void __launch_bounds__(kWZI * 32, 1) k_zi3(PWGrid g, int nc, int nbox
     Are[e] = vr;
     Aim[e] = vi;
   }
+  __shared__ int s_ncol[33], s_off[33];  // slab table (mz + M), read per input element
+  if (tid < NZ) {
+    s_ncol[tid] = g.slab_ncol[tid];
+    s_off[tid] = g.slab_off[tid];
+  }
   __syncthreads();
   const int ncbk = (ncol + kZB - 1) / kZB, total = nbox * nc * ncbk;
   const int nw = gridDim.x * kWZI;
@@ -558,8 +568,8 @@ __global__ void __launch_bounds__(kWZI * 32, 1) k_zi3(PWGrid g, int nc, int nbox
     double2* dst = Fs + buf * 33 * kZR;
     for (int e = lane; e < NZ * kZB; e += 32) {  // F rows (mz + M): a contiguous prefix of the columns
       const int s = e / kZB, cc = e % kZB;
-      const bool v = c0 + cc < g.slab_ncol[s];
-      dev::cp_async16z(dst + s * kZR + cc, v ? src + g.slab_off[s] + c0 + cc : src, v);
+      const bool v = c0 + cc < s_ncol[s];
+      dev::cp_async16z(dst + s * kZR + cc, v ? src + s_off[s] + c0 + cc : src, v);
     }
     cp_commit();
   };
