@@ -399,8 +399,11 @@ __global__ void __launch_bounds__(W * 32, 1) k_anterp2(ChebDev cb, const DBox* _
         sbz[pt * RS + r] = s_chv[pt][code & 255] * (dim == 3 ? bz[pt * XS + (code >> 8)] : 1.0);
       }
     __syncthreads();
+    // k-steps of 4 points up to the chunk's last point (the rest of a partial
+    // last chunk is zero padding)
+    const int nks = (min(kKC2, box.se - box.sb - c * kKC2) + 3) / 4;
 #pragma unroll 2
-    for (int ks = 0; ks < kKC2 / 4; ++ks) {
+    for (int ks = 0; ks < nks; ++ks) {
       const int k = ks * 4 + t;
       double bv[NTW];
 #pragma unroll
