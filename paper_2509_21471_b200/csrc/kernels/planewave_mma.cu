@@ -954,10 +954,12 @@ __global__ void __launch_bounds__(kWI * 32, 1) k_inv_xy2(PWGrid g, const int* __
 // (P = Er ar, Q = Ei ai, R = Er ai, S = Ei ar; b[+-my] = (P -+ Q) + i (R +- S))
 // with all 2 x 2 tiles of the four products at once, the my = 0 row and the
 // m0 = 0 column on the CUDA cores, and the in-band columns stored to B.
-constexpr int kWF3 = 10;  // warps per CTA (shared memory: ~18 KB per warp)
+// warps per CTA: 8 when the shared memory holds them (~27 KB per warp with
+// the staged B row), else 7
+constexpr int kWF3 = 8;
 
-template <int PC, int NC>
-__global__ void __launch_bounds__(kWF3 * 32, 1) k_fwd_xy3(PWGrid g, const int* __restrict__ boxes, int nbox, int nch,
+template <int PC, int NC, int WF>
+__global__ void __launch_bounds__(WF * 32, 1) k_fwd_xy3(PWGrid g, const int* __restrict__ boxes, int nbox, int nch,
                                                          const double* __restrict__ outgoing,
                                                          double2* __restrict__ B) {
   constexpr int PT = 3, MTC = 2, P8 = PT * 8, SE = P8 + 4, SY = P8 + 4, NXT = 5;  // NX8 = 40 columns
@@ -968,13 +970,14 @@ __global__ void __launch_bounds__(kWF3 * 32, 1) k_fwd_xy3(PWGrid g, const int* _
   double* EXT = sm;                   // [NX8][SE]
   double* EYr = EXT + NX8 * SE;       // [M8][SY]  rows my - 1
   double* EYi = EYr + M8 * SY;        // [M8][SY]
-  int* colidx = reinterpret_cast<int*>(EYi + M8 * SY);  // [N][M1]
-  double* wbase = EYi + M8 * SY + (N * M1 + 3) / 4 * 2;
-  constexpr int per_warp = 2 * P8 * SE + 2 * P8 * SA;  // doubles
+  short* colidx = reinterpret_cast<short*>(EYi + M8 * SY);  // [N][M1]
+  double* wbase = EYi + M8 * SY + (N * M1 + 7) / 8 * 2;
+  const int per_warp = 2 * P8 * SE + 2 * P8 * SA + 2 * ((ncol + 1) / 2 * 2);  // doubles (the staged row even)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gq = lane >> 2, t = lane & 3;
   double* win = wbase + warp * per_warp;  // [2][P8][SE]
   double* ar = win + 2 * P8 * SE;         // [P8][SA]  X output, real parts
   double* ai = ar + P8 * SA;              // [P8][SA]  imaginary parts
+  double2* stg = reinterpret_cast<double2*>(ai + P8 * SA);  // [ncol] this unit's B row
   for (int e = tid; e < NX8 * SE; e += blockDim.x) {
     const int n = e / SE, ix = e % SE;
     double v = 0.0;
@@ -1002,10 +1005,10 @@ __global__ void __launch_bounds__(kWF3 * 32, 1) k_fwd_xy3(PWGrid g, const int* _
   for (int e = tid; e < N * M1; e += blockDim.x) colidx[e] = -1;
   for (int e = lane; e < per_warp; e += 32) win[e] = 0.0;  // padding rows / columns stay 0
   __syncthreads();
-  for (int c = tid; c < ncol; c += blockDim.x) colidx[(g.col_my[c] + M) * M1 + g.col_m0[c]] = c;
+  for (int c = tid; c < ncol; c += blockDim.x) colidx[(g.col_my[c] + M) * M1 + g.col_m0[c]] = (short)c;
   __syncthreads();
   const int total = nbox * nch * p;
-  const int nw = gridDim.x * kWF3;
+  const int nw = gridDim.x * WF;
   auto issue = [&](int u, int buf) {
     const int item = u / p, iz = u % p;
     const double* src = outgoing + ((size_t)boxes[item / nch] * nch + item % nch) * (size_t)(p * pp) + (size_t)iz * pp;
@@ -1013,7 +1016,7 @@ __global__ void __launch_bounds__(kWF3 * 32, 1) k_fwd_xy3(PWGrid g, const int* _
     for (int e = lane; e < pp; e += 32) cp_async8(dst + (e / p) * SE + e % p, src + e, true);
     cp_commit();
   };
-  int u = blockIdx.x * kWF3 + warp;
+  int u = blockIdx.x * WF + warp;
   if (u < total) issue(u, 0);
   for (int k = 0; u < total; ++k, u += nw) {
     const int buf = k & 1;
@@ -1055,10 +1058,15 @@ __global__ void __launch_bounds__(kWF3 * 32, 1) k_fwd_xy3(PWGrid g, const int* _
         }
     }
     __syncwarp();
+    // the row is assembled in shared memory (column order is the z-extent
+    // order, scattered relative to the fragments) and leaves by one TMA bulk
+    // store, instead of one scattered 16-byte global store per element
     auto put = [&](int my, int m0, double re, double im) {
       const int c = colidx[(my + M) * M1 + m0];
-      if (c >= 0) Bo[c] = make_double2(re, im);
+      if (c >= 0) stg[c] = make_double2(re, im);
     };
+    if (lane == 0) dev::bulk_wait_read0();  // the previous unit's row has left the staging buffer
+    __syncwarp();
     // Y stage (m0 >= 1, my >= 1)
     {
       double P[MTC][MTC][2], Q[MTC][MTC][2], R[MTC][MTC][2], S[MTC][MTC][2];
@@ -1127,8 +1135,15 @@ __global__ void __launch_bounds__(kWF3 * 32, 1) k_fwd_xy3(PWGrid g, const int* _
       }
       put(0, m0, re, im);
     }
+    dev::fence_proxy_async_smem();  // the row's generic-proxy writes, visible to the TMA store
+    __syncwarp();
+    if (lane == 0) {
+      dev::bulk_s2g(Bo, stg, (uint32_t)ncol * 16u);
+      dev::bulk_commit();
+    }
     __syncwarp();  // ar / ai and this w buffer are rewritten by the next units
   }
+  if (lane == 0) dev::bulk_wait0();  // (the CTA's shared memory must outlive its stores)
 }
 
 // inv_xy, warp-independent form (3D, p <= 24, N <= 33).  The unit of work is
@@ -1350,15 +1365,24 @@ void launch_forward_mma(const PWGrid& g, const int* boxes, int nbox, int nch, co
     const size_t sm = sizeof(double) * ((size_t)NX8 * (P8 + 4) + 2 * (size_t)MT * 8 * (P8 + 4) +
                                         2 * 4 * (size_t)P8 * (P8 + 4) + 4 * (size_t)P8 * r8(NX8 > 16 * MT ? NX8 : 16 * MT)) +
                       sizeof(int) * (size_t)g.N * M1;
-    const size_t sm3 = sizeof(double) * (40 * 28 + 2 * 16 * 28 + (size_t)(g.N * M1 + 3) / 4 * 2 +
-                                         (size_t)kWF3 * (2 * 24 * 28 + 2 * 24 * 20));
+    auto sm3 = [&](int wf) {
+      return sizeof(double) * (40 * 28 + 2 * 16 * 28 + (size_t)(g.N * M1 + 7) / 8 * 2 +
+                               (size_t)wf * (2 * 24 * 28 + 2 * 24 * 20 + 2 * ((g.ncol + 1) / 2 * 2)));
+    };
     if (PT == 3 && g.N <= 33 && g.dim == 3) {  // warp-independent slabs
+      const int wf = sm3(kWF3) <= 227 * 1024 ? kWF3 : kWF3 - 1;
       const int units = nbox * nch * g.p;
-      const int ctas = std::max(1, std::min(num_sms(), (units + kWF3 - 1) / kWF3));
+      const int ctas = std::max(1, std::min(num_sms(), (units + wf - 1) / wf));
 #define FX3(PC_, NC_)                                                                                        \
   do {                                                                                                       \
-    attr((const void*)k_fwd_xy3<PC_, NC_>, sm3);                                                             \
-    k_fwd_xy3<PC_, NC_><<<ctas, kWF3 * 32, sm3, st>>>(g, boxes, nbox, nch, outgoing, B);                     \
+    if (wf == kWF3) {                                                                                        \
+      attr((const void*)k_fwd_xy3<PC_, NC_, kWF3>, sm3(kWF3));                                               \
+      k_fwd_xy3<PC_, NC_, kWF3><<<ctas, kWF3 * 32, sm3(kWF3), st>>>(g, boxes, nbox, nch, outgoing, B);      \
+    } else {                                                                                                 \
+      attr((const void*)k_fwd_xy3<PC_, NC_, kWF3 - 1>, sm3(kWF3 - 1));                                       \
+      k_fwd_xy3<PC_, NC_, kWF3 - 1><<<ctas, (kWF3 - 1) * 32, sm3(kWF3 - 1), st>>>(g, boxes, nbox, nch,       \
+                                                                               outgoing, B);                 \
+    }                                                                                                        \
   } while (0)
       if (g.p == 23 && g.N == 33) FX3(23, 33);
       else if (g.p == 22 && g.N == 33) FX3(22, 33);
