@@ -292,7 +292,7 @@ def run_ours(args, rank, world, local_rank):
     roof = {"bound": "fp64", "kernel": "k_residual (near-field P2P)", "achieved": res_flops / res_t / 1e12,
             "achieved_kind": ("algorithm-equivalent rate: SURVEY 8(d) work (8 FLOP per tested pair + "
                               "F_in = 3(33+33)+30 = 228 per in-support pair, the reference's Clenshaw cost) over "
-                              "the kernel's CUDA-event time; the kernel evaluates degree-5 piecewise "
+                              "the kernel's CUDA-event time; the kernel evaluates degree-6 piecewise "
                               "re-expansions, so it executes fewer FP64 operations than this counts"),
             "hw_fp64_tflops": hw.get("hw_fp64_tflops") if hw else None,
             "hw_fp64_source": hw.get("source") if hw else None,

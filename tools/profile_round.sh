@@ -28,6 +28,12 @@ for k in k_residual k_inv_xy k_tensor k_fwd_xy k_interp_mma k_anterp_mma k_basis
   ncu --set full --clock-control none --import-source on -k regex:"$k\\b" -c 1 -o "$out/cfg4_$k" $one4 > /dev/null 2>&1
 done
 
+# the residual kernel's executed FP64 work (bench.py's roofline reads it)
+ncu -i "$out/metric_k_residual.ncu-rep" --page source --csv --print-source sass > "$out/metric_k_residual.sass.csv" 2>/dev/null
+ncu -i "$out/metric_k_residual.ncu-rep" --page raw --csv > "$out/metric_k_residual.raw.csv" 2>/dev/null
+python tools/residual_hw.py "$out/metric_k_residual.sass.csv" "$out/metric_k_residual.raw.csv" > "$out/residual_hw.json"
+python tools/ncu_lines.py "$out/metric_k_residual.ncu-rep" 60 > "$out/metric_k_residual.lines.txt" 2>&1
+rm -f "$out/metric_k_residual.sass.csv"
 # text summaries on the box (the reports themselves exceed what gpurun copies back)
 for r in "$out"/*.ncu-rep; do
   ncu -i "$r" --page raw --csv > "${r%.ncu-rep}.raw.csv" 2>/dev/null
