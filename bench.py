@@ -267,39 +267,60 @@ def run_ours(args, rank, world, local_rank):
         del d_x, d_s, d_u
         torch.cuda.empty_cache()
 
-    # roofline of the dominant kernel (FP64): measured DFMA peak on this GPU
+    # rooflines (FP64): the three largest kernels, each over the peak of the
+    # pipe it runs on, measured live on this GPU (DFMA for the residual's
+    # CUDA-core arithmetic, DMMA for the tensor-core contractions); the bench
+    # line's roofline object is the dominant kernel (largest CUDA-event time)
     peak = ctx.fp64_peak_tflops()
+    peak_mma = ctx.fp64_mma_peak_tflops()
     R = results.get("stokeslet") or next(iter(results.values()))
     rep = R["rep"]
     plan = g.DmkPlan(**R["plan"])
+    hw_all = {}  # per-kernel ncu numbers of the same workload (profiles/round2/kernel_hw.json)
+    try:
+        with open(os.path.join(ROOT, "profiles", "round2", "kernel_hw.json")) as f:
+            hw_all = json.load(f) if args.n == 10_000_000 else {}
+    except (OSError, ValueError):
+        hw_all = {}
     # residual kernel algorithmic FLOPs (SURVEY 8(d) convention, our tested-candidate count)
     F_in = 3 * (33 + 33) + 30
     res_flops = 8 * rep["p2p_candidates"] + F_in * rep["p2p_in_support"]
-    res_t = rep["t_residual_kernel"]
-    pw_t = rep["t_planewave"]
-    traffic = None  # DRAM bytes per launch of the same kernel/workload from the committed ncu capture
-    try:
-        with open(os.path.join(ROOT, "profiles", "round2", "residual_hw.json")) as f:
-            traffic = int(json.load(f)["dram_bytes_per_launch"]) if args.n == 10_000_000 else None
-    except (OSError, ValueError, KeyError):
-        traffic = None
-    hw = None  # FP64 rate the hardware executed (ncu dadd + dmul + 2 dfma over the kernel's duration)
-    try:
-        with open(os.path.join(ROOT, "profiles", "round2", "residual_hw.json")) as f:
-            hw = json.load(f)
-    except (OSError, ValueError):
-        hw = None
-    roof = {"bound": "fp64", "kernel": "k_residual (near-field P2P)", "achieved": res_flops / res_t / 1e12,
-            "achieved_kind": ("algorithm-equivalent rate: SURVEY 8(d) work (8 FLOP per tested pair + "
-                              "F_in = 3(33+33)+30 = 228 per in-support pair, the reference's Clenshaw cost) over "
-                              "the kernel's CUDA-event time; the kernel evaluates degree-6 piecewise "
-                              "re-expansions, so it executes fewer FP64 operations than this counts"),
-            "hw_fp64_tflops": hw.get("hw_fp64_tflops") if hw else None,
-            "hw_fp64_source": hw.get("source") if hw else None,
-            "peak": peak, "unit": "TFLOP/s", "frac": (res_flops / res_t / 1e12) / peak, "traffic": traffic,
-            "traffic_source": "profiles/round2/residual_hw.json (ncu dram__bytes_read+write, one launch)",
-            "peak_source": "measured DFMA microbenchmark (sdmk_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",
-            "share_of_step": res_t / (R["ms"] * 1e-3), "planewave_share_of_step": pw_t / (R["ms"] * 1e-3)}
+    pd = plan.p ** 3
+    nch = 3  # Stokeslet channels / components in 3D
+    cands = {
+        "k_residual": {"t": rep["t_residual_kernel"], "flop": res_flops, "peak": peak, "pipe": "FP64 CUDA cores (DFMA)",
+                       "work": "8 FLOP per tested pair + F_in = 3(33+33)+30 = 228 per in-support pair (the reference's "
+                               "Clenshaw cost; an algorithm-equivalent rate: the kernel evaluates degree-6 piecewise "
+                               "re-expansions, so it executes fewer FP64 operations than this counts)"},
+        "k_interp_mma": {"t": rep.get("t_interp_kernel", 0.0), "flop": 2.0 * nch * pd * rep["num_targets"],
+                         "peak": peak_mma, "pipe": "FP64 tensor cores (DMMA m8n8k4)",
+                         "work": "2 d p^3 FLOP per target (u_j = sum W[j,iz,iy,ix] bz by bx)"},
+        "k_anterp2": {"t": rep.get("t_anterp_kernel", 0.0), "flop": 2.0 * nch * pd * rep["num_sources"],
+                      "peak": peak_mma, "pipe": "FP64 tensor cores (DMMA m8n8k4)",
+                      "work": "2 nch p^3 FLOP per source (outgoing[ch,iz,iy,ix] += s_ch bz by bx)"},
+    }
+    kern = {}
+    for name, c in cands.items():
+        if c["t"] <= 0:
+            continue
+        ach = c["flop"] / c["t"] / 1e12
+        hw = hw_all.get(name, {})
+        kern[name] = {"ms": c["t"] * 1e3, "share_of_step": c["t"] / (R["ms"] * 1e-3), "achieved": ach,
+                      "peak": c["peak"], "frac": ach / c["peak"], "pipe": c["pipe"], "work": c["work"],
+                      "traffic": hw.get("dram_bytes_per_launch"), "tensor_pipe_pct": hw.get("tensor_pct"),
+                      "fp64_pipe_pct": hw.get("fp64_pct"), "hw_fp64_tflops": hw.get("hw_fp64_tflops")}
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    d = kern[dom]
+    roof = {"bound": "fp64", "kernel": dom, "achieved": d["achieved"], "achieved_kind": d["work"],
+            "peak": d["peak"], "unit": "TFLOP/s", "frac": d["frac"], "traffic": d["traffic"],
+            "traffic_source": "profiles/round2/kernel_hw.json (ncu dram__bytes_read+write, one launch, same workload)",
+            "peak_source": ("measured live: " + ("DMMA" if "mma" in d["pipe"].lower() or "DMMA" in d["pipe"]
+                                                 else "DFMA") + " microbenchmark (sdmk_fp64_mma_peak / sdmk_fp64_peak); "
+                            "MEASURED_PEAKS.json has no FP64 figure"),
+            "pipe": d["pipe"], "share_of_step": d["share_of_step"],
+            "planewave_share_of_step": rep["t_planewave"] / (R["ms"] * 1e-3),
+            "peaks_measured": {"dfma_tflops": peak, "dmma_tflops": peak_mma},
+            "kernels": kern}
     roof["multi_gpu_path"] = ("library NCCL communicator" if use_comm else "set_shard + torch all_reduce") if world > 1 else None
     return results, roof, clocks
 

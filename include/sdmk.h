@@ -101,6 +101,8 @@ typedef struct sdmk_report {
   double t_exchange;        /* multi-GPU: halo pack + exchange + unpack of outgoing expansions */
   int64_t halo_bytes_sent;  /* multi-GPU: outgoing-expansion bytes this rank sent / received */
   int64_t halo_bytes_recv;
+  double t_interp_kernel;   /* target interpolation kernel alone (DMMA path; 0 otherwise) */
+  double t_anterp_kernel;   /* leaf anterpolation kernel alone (DMMA path; 0 otherwise) */
 } sdmk_report;
 
 typedef struct sdmk_context sdmk_context;
@@ -293,6 +295,8 @@ int sdmk_evaluate_end(sdmk_context* ctx, double* u, sdmk_report* report);
 int sdmk_get_stream(sdmk_context* ctx, void** stream);
 /* measured FP64 FMA throughput of the device (TFLOP/s, best of 5) */
 int sdmk_fp64_peak(sdmk_context* ctx, double* tflops);
+/* the same for the FP64 tensor cores (mma.sync.m8n8k4.f64, the DMMA kernels' roofline) */
+int sdmk_fp64_mma_peak(sdmk_context* ctx, double* tflops);
 
 /* ---- host-only helpers (no GPU needed; used by the CPU test suite) ----
    Plan-level setup exactly as the GPU path uses it. */

@@ -57,7 +57,8 @@ class sdmk_report(C.Structure):
                 ("t_h2d", C.c_double), ("t_d2h", C.c_double), ("t_total", C.c_double),
                 ("p2p_candidates", C.c_int64), ("p2p_in_support", C.c_int64), ("kernel_launches", C.c_int32),
                 ("t_residual_kernel", C.c_double), ("t_planewave", C.c_double), ("t_exchange", C.c_double),
-                ("halo_bytes_sent", C.c_int64), ("halo_bytes_recv", C.c_int64)]
+                ("halo_bytes_sent", C.c_int64), ("halo_bytes_recv", C.c_int64),
+                ("t_interp_kernel", C.c_double), ("t_anterp_kernel", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -103,6 +104,7 @@ def lib():
             "sdmk_residual_pass": ([C.c_void_p, dp], C.c_int),
             "sdmk_get_stream": ([C.c_void_p, P(C.c_void_p)], C.c_int),
             "sdmk_fp64_peak": ([C.c_void_p, P(C.c_double)], C.c_int),
+            "sdmk_fp64_mma_peak": ([C.c_void_p, P(C.c_double)], C.c_int),
             "sdmk_host_save_tables": ([P(sdmk_plan), C.c_char_p], C.c_int),
             "sdmk_host_symbol_table": ([P(sdmk_plan), C.c_double, C.c_int, C.c_int, C.c_double, C.c_double, dp],
                                        C.c_int),
@@ -476,6 +478,11 @@ class Context:
     def fp64_peak_tflops(self) -> float:
         v = C.c_double()
         _raise(lib().sdmk_fp64_peak(self._h, C.byref(v)))
+        return float(v.value)
+
+    def fp64_mma_peak_tflops(self) -> float:
+        v = C.c_double()
+        _raise(lib().sdmk_fp64_mma_peak(self._h, C.byref(v)))
         return float(v.value)
 
     def save_tables(self, plan: DmkPlan, path: str):

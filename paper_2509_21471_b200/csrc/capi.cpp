@@ -511,6 +511,14 @@ int sdmk_fp64_peak(sdmk_context* c, double* tflops) {
   });
 }
 
+int sdmk_fp64_mma_peak(sdmk_context* c, double* tflops) {
+  return guarded([&] {
+    Context* x = need_ctx(c);
+    *tflops = measure_dmma_peak_tflops(x->stream());
+    cuda_check(cudaGetLastError(), "fp64 mma peak kernel");
+  });
+}
+
 int sdmk_host_save_tables(const sdmk_plan* plan, const char* path) {
   return guarded([&] { save_tables(tables_for_plan(to_plan(plan)), path ? path : ""); });
 }

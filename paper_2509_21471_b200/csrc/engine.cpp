@@ -1097,7 +1097,10 @@ void Context::run_upward() {  // dmk.cpp:555-655
   if (mma_anterp_supported(p)) {
     double* basis = arena_.as<double>("basis_s", (size_t)3 * pr.ns * p);
     launch_basis(cb, pr.boxes, pr.ant_leaves, pr.n_ant, pr.spts, pr.ns, 0, basis, st_);
+    cudaEventRecord(ev_[18], st_);
     launch_anterp_mma(pr.plan.kernel, cb, pr.boxes, pr.ant_leaves, pr.n_ant, basis, pr.sstr, pr.ns, og, pr.nch, st_);
+    cudaEventRecord(ev_[19], st_);
+    anterp_timed_ = true;
     launches_ += 2;
   } else {
     launch_anterp(pr.plan.kernel, cb, pr.boxes, pr.ant_leaves, pr.n_ant, pr.spts, pr.ns, pr.sstr, og, pr.nch, st_);
@@ -1297,7 +1300,10 @@ void Context::run_target_far(double* ufar) {  // dmk.cpp:861-915
       ++launches_;
       tb = b;
     }
+    cudaEventRecord(ev_[16], st_);
     launch_interp_mma(cb, pr.boxes, pr.int_leaves, pr.n_int, tb, pr.nt, pr.tperm, incoming, ufar, st_);
+    cudaEventRecord(ev_[17], st_);
+    interp_timed_ = true;
   } else {
     launch_interp_targets(cb, pr.boxes, pr.int_leaves, pr.n_int, pr.tpts, pr.nt, pr.tperm, incoming, ufar, st_);
   }
@@ -1441,6 +1447,7 @@ void Context::evaluate_begin(const Plan& P, int dim, int64_t ns, const double* s
   const int ntt = alias ? (int)ns : (int)nt;
   call_ = Call{dim, sc, ntt, ns, nt, alias, device_ptrs};
   halo_run_ = nranks_ > 1 && (comm_ || manual_x_);
+  interp_timed_ = anterp_timed_ = false;
   cudaEventRecord(ev_[0], st_);
   copy_in(arena_.as<double>("src_in", (size_t)ns * dim), src, sizeof(double) * ns * dim, device_ptrs);
   if (!alias) copy_in(arena_.as<double>("tgt_in", (size_t)nt * dim), tgt, sizeof(double) * nt * dim, device_ptrs);
@@ -1597,6 +1604,8 @@ void Context::evaluate_end(double* u, sdmk_report* rep) {
     rep->t_d2h = ev_ms(6, 7) * 1e-3;
     rep->t_total = (ev_ms(0, 7) - (manual ? gap : 0.0)) * 1e-3;
     rep->t_residual_kernel = ev_ms(13, 12) * 1e-3;
+    rep->t_interp_kernel = interp_timed_ ? ev_ms(16, 17) * 1e-3 : 0.0;
+    rep->t_anterp_kernel = anterp_timed_ ? ev_ms(18, 19) * 1e-3 : 0.0;
     rep->t_planewave = planewave_ms() * 1e-3;
     rep->p2p_candidates = (int64_t)hst[0];
     rep->p2p_in_support = (int64_t)hst[1];

@@ -224,7 +224,8 @@ class Context {
   cudaEvent_t x_ev_ = nullptr;     // the NCCL halo exchange on st2_ is done
   bool x_pending_ = false;         // an exchange is in flight (evaluate with a communicator)
   bool str_pending_ = false;       // strengths copy in flight on st2_
-  cudaEvent_t ev_[16];
+  cudaEvent_t ev_[20];
+  bool interp_timed_ = false, anterp_timed_ = false;  // the DMMA kernels ran this call (events 16-19)
   Arena arena_;
   Pinned pinned_;
   std::map<std::string, Tables> tables_;

@@ -246,5 +246,6 @@ void launch_direct(int kernel, int dim, const double* src, int ns, const double*
 
 // ---- peak.cu ----------------------------------------------------------------
 double measure_fp64_peak_tflops(cudaStream_t st);
+double measure_dmma_peak_tflops(cudaStream_t st);
 
 }  // namespace sdmkb
