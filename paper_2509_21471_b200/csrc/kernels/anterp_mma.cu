@@ -511,6 +511,7 @@ __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DB
       v[i][0] = v[i][1] = v[i][2] = 0.0;
     }
     const int nmine = warp < ntm ? (ntm - warp + kIW - 1) / kIW : 0;  // m-tiles this warp owns
+    const bool full = nmine == kITW;
     for (int c = 0; c < nchunk; ++c) {
       const int buf = c & 1;
       if (c + 1 < nchunk) {
@@ -531,18 +532,31 @@ __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DB
 #pragma unroll
             for (int q = 0; q < TY; ++q) cc[i][q][0] = cc[i][q][1] = 0.0;
           const double* Wg = Wc + (gl * PY + g) * WS + t;
+          if (full) {
+            // every m-tile: no per-DMMA predicate (each predicated DMMA costs a
+            // WARPSYNC + NOP)
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks)
+            for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-            for (int q = 0; q < TY; ++q) {
-              const double bv = Wg[q * 8 * WS + ks * 4];
+              for (int q = 0; q < TY; ++q) {
+                const double bv = Wg[q * 8 * WS + ks * 4];
 #pragma unroll
-              for (int i = 0; i < kITW; ++i)
-                if (i < nmine) dev::dmma(cc[i][q][0], cc[i][q][1], af[i][ks], bv);
-            }
+                for (int i = 0; i < kITW; ++i) dev::dmma(cc[i][q][0], cc[i][q][1], af[i][ks], bv);
+              }
+          } else {
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+              for (int q = 0; q < TY; ++q) {
+                const double bv = Wg[q * 8 * WS + ks * 4];
+#pragma unroll
+                for (int i = 0; i < kITW; ++i)
+                  if (i < nmine) dev::dmma(cc[i][q][0], cc[i][q][1], af[i][ks], bv);
+              }
+          }
 #pragma unroll
           for (int i = 0; i < kITW; ++i) {
-            if (i >= nmine) continue;
+            if (!full && i >= nmine) continue;
             double s = 0.0;
 #pragma unroll
             for (int q = 0; q < TY; ++q) s = fma(byv[i][q][0], cc[i][q][0], fma(byv[i][q][1], cc[i][q][1], s));
