@@ -58,7 +58,7 @@ constexpr int kList = SDMK_RES_LIST;  // per-lane list capacity (entries): longe
 constexpr int kMaxRanges = 160;
 constexpr int kMaxIvl = kMaxRanges * 8;  // source intervals per chunk: ranges x Morton sub-cells
 constexpr int kResBlocksPerSM = 1;       // persistent grid (registers and shared memory: 1 per SM)
-constexpr int kGCap = 256;               // per-lane global candidate list (entries; even)
+constexpr int kGCap = 1024;              // per-lane global candidate list (entries; even)
 constexpr int kMaxPW = 896;      // ni * (deg + 1) <= 896 (d, o) coefficient pairs (8 copies: 112 KB)
 constexpr int kCopies = 8;       // table copies, one per 16-byte bank group
 
@@ -528,12 +528,44 @@ __global__ void __launch_bounds__(kRBlock) k_residual(ResidTables rt, const DBox
       }
       gcnt = 0;
     };
-    // move this lane's cnt shared-memory entries to the end of its global list
+    // the shared-memory lists (cnt entries in this lane), evaluated in place
+    // in lockstep to the longest (mx), near pairs exactly afterwards
+    auto eval_shared = [&](int cnt, int mx) {
+      unsigned long long nearmask = 0;  // kList <= 64
+      for (int i = 0; i < mx; i += 2) {
+        const bool u0 = i < cnt, u1 = i + 1 < cnt;
+        const int s0 = eval(u0 ? lsrc[warp][i][lane] : 0, PER && u0 ? (int)lrng[warp][i][lane] : 0, u0,
+                            std::false_type{});
+        const int s1 = eval(u1 ? lsrc[warp][i + 1][lane] : 0, PER && u1 ? (int)lrng[warp][i + 1][lane] : 0, u1,
+                            std::false_type{});
+        n_in32 += (s0 & 1) + (s1 & 1);
+        nearmask |= (unsigned long long)((s0 >> 1) | (s1 & 2)) << i;
+      }
+      while (__any_sync(0xffffffffu, nearmask != 0)) {  // rare: s < s_exact
+        if (nearmask) {
+          const int i = __ffsll(nearmask) - 1;
+          nearmask &= nearmask - 1;
+          eval(lsrc[warp][i][lane], PER ? (int)lrng[warp][i][lane] : 0, true, std::true_type{});
+        }
+      }
+    };
+    // a full shared list: when the lanes are evenly filled (dense
+    // neighbourhoods, e.g. the Ewald's local part: every target has many
+    // candidates) the lists are evaluated in place; otherwise every lane's
+    // entries move to the end of its global list, evaluated once at the
+    // chunk's end
     auto spill = [&](int cnt) {
-      if (__any_sync(0xffffffffu, gcnt + cnt > kGCap)) eval_global();  // global list full (dense clusters)
-      int mx = cnt;
+      int mx = cnt, sum = cnt;
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      for (int o = 16; o >= 1; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      }
+      if (5 * sum >= 3 * 32 * mx) {  // mean >= 60 % of the longest: little lockstep padding
+        eval_shared(cnt, mx);
+        return;
+      }
+      if (__any_sync(0xffffffffu, gcnt + cnt > kGCap)) eval_global();  // global list full (dense clusters)
       for (int k = 0; k < mx; ++k) {
         if (k < cnt) {
           gl[gcnt + k] = lsrc[warp][k][lane];
