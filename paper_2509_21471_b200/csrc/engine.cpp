@@ -2256,8 +2256,20 @@ void Context::ewald(const Plan& P, int64_t ns, const double* src, int64_t nt, co
   const size_t M3 = (size_t)Mg * Mg * Mg, S = (size_t)Mg * Mg * (Mg / 2 + 1);
   double* grid = arena_.as<double>("ew_grid", 3 * M3);
   double2* spec = arena_.as<double2>("ew_spec", 3 * S);
-  cuda_check(cudaMemsetAsync(grid, 0, sizeof(double) * 3 * M3, st_), "memset grid");
-  launch_ew_spread(g, n, spts, sstr, grid, st_);
+  // deterministic spreading (output-stationary 16^3 bricks, sources binned
+  // by Morton cells of <= 16 grid points); the atomic form for windows wider
+  // than the brick
+  int Ls = 0;
+  while (Ls < 8 && (double)Mg / (1 << Ls) > 16.0) ++Ls;
+  const bool tiled = ew_spread_tiled_ok(g, Ls);
+  if (tiled) {
+    int* sbc = arena_.as<int>("ew_sbc", ((size_t)1 << (3 * Ls)) + 1);
+    launch_cell_bounds(n, sq, Ls, sbc, st_);
+    launch_ew_spread_tiled(g, Ls, sbc, n, spts, sstr, grid, st_);
+  } else {
+    cuda_check(cudaMemsetAsync(grid, 0, sizeof(double) * 3 * M3, st_), "memset grid");
+    launch_ew_spread(g, n, spts, sstr, grid, st_);
+  }
   fft_.plan(Mg, 3, st_);
   fft_.forward(grid, spec);
   launch_ew_symbol(g, spec, (const double*)(dv2 + o_a), (const double*)(dv2 + o_d), st_);

@@ -136,6 +136,143 @@ __global__ void k_ew_gather(EwGrid g, int n, const double* __restrict__ tpts, co
   }
 }
 
+// ---- deterministic spreading and interpolation (no atomics) ---------------
+// The Morton-sorted points are binned by cells at level Lc (side cs ~ 8 grid
+// points; bnd[c] = first point of cell c in Morton order).
+__device__ __forceinline__ int ew_cell(int cx, int cy, int cz, int Lc) {  // Morton index, x fastest
+  int c = 0;
+  for (int b = 0; b < Lc; ++b) c |= (((cx >> b) & 1) | (((cy >> b) & 1) << 1) | (((cz >> b) & 1) << 2)) << (3 * b);
+  return c;
+}
+__device__ __forceinline__ int ew_mod(int a, int m) { a %= m; return a < 0 ? a + m : a; }
+
+// Spreading, output-stationary: one CTA per 16^3 brick of the grid, one
+// thread per (x, y) column of the brick holding its 16 z values.  The CTA
+// walks the cells whose points can reach the brick (cell order, then Morton
+// order), stages each batch of points that do (first grid index per axis,
+// the w window weights per axis, the strength), and every thread adds the
+// batch into its column in that order: each grid value is one thread's
+// fixed-order sum, written once (no atomics, no zeroing of the grid,
+// bitwise reproducible).  A stencil's z range is the same for every column,
+// so the z loop is unrolled with one predicate per row.
+constexpr int kEwTB = 16, kEwSB = 64;
+__global__ void __launch_bounds__(256) k_ew_spread2(EwGrid g, int Lc, const int* __restrict__ bnd,
+                                                    const double* __restrict__ spts, int n,
+                                                    const double* __restrict__ sstr, double* __restrict__ grid) {
+  __shared__ double s_w[kEwSB][3][kEwMaxW];
+  __shared__ double s_f[kEwSB][3];
+  __shared__ double s_d0[kEwSB][3];
+  __shared__ int s_j0[kEwSB][3];
+  __shared__ int s_wp[2], s_n, s_cell[64];
+  const int M = g.Mg, w = g.w, nbk = (M + kEwTB - 1) / kEwTB;
+  const size_t M3 = (size_t)M * M * M;
+  const int b = blockIdx.x, bx = b % nbk, by = (b / nbk) % nbk, bz = b / (nbk * nbk);
+  const int b0[3] = {bx * kEwTB, by * kEwTB, bz * kEwTB};
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int gx = b0[0] + tx, gy = b0[1] + ty;
+  double acc[kEwTB][3];
+#pragma unroll
+  for (int k = 0; k < kEwTB; ++k) acc[k][0] = acc[k][1] = acc[k][2] = 0.0;
+  // cells that can hold a point reaching the brick: x M in (b0 - w/2, b0 + 15 + w/2]
+  const int nc = 1 << Lc;
+  const double cs = (double)M / nc;
+  int ncell = 0;
+  if (tid == 0) {
+    int clo[3], ccnt[3];
+    for (int a = 0; a < 3; ++a) {
+      clo[a] = (int)floor((b0[a] - 0.5 * w - 1e-6) / cs);  // (margin: a point on a cell boundary)
+      const int chi = (int)floor((b0[a] + kEwTB - 1 + 0.5 * w + 1e-6) / cs);
+      ccnt[a] = min(chi - clo[a] + 1, nc);
+    }
+    for (int kz = 0; kz < ccnt[2]; ++kz)
+      for (int ky = 0; ky < ccnt[1]; ++ky)
+        for (int kx = 0; kx < ccnt[0]; ++kx)
+          s_cell[ncell++] = ew_cell(ew_mod(clo[0] + kx, nc), ew_mod(clo[1] + ky, nc), ew_mod(clo[2] + kz, nc), Lc);
+    s_n = ncell;
+  }
+  __syncthreads();
+  ncell = s_n;
+  for (int ci = 0; ci < ncell; ++ci) {
+    const int c = s_cell[ci];
+    const int p0 = bnd[c], p1 = bnd[c + 1];
+    for (int base = p0; base < p1; base += kEwSB) {
+      __syncthreads();  // the previous batch is consumed
+      // filter: the points of this batch whose stencil meets the brick, compacted in order
+      bool keep = false;
+      int j0[3] = {0, 0, 0};
+      double d0[3] = {0.0, 0.0, 0.0};
+      const int pi = base + tid;
+      if (tid < kEwSB && pi < p1) {
+        keep = true;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double sx = (spts[(size_t)a * n + pi] + 0.5) * g.inv_h;
+          const int ju = (int)ceil(sx - 0.5 * w);  // first grid index of the stencil (unwrapped)
+          d0[a] = ju - sx;
+          j0[a] = ew_mod(ju, M);
+          const int dd = ew_mod(b0[a] - j0[a], M);  // brick start relative to the stencil start
+          keep = keep && (dd < w || dd > M - kEwTB);
+        }
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);  // order-preserving compaction
+      if ((tid & 31) == 0 && tid < kEwSB) s_wp[tid >> 5] = __popc(bal);
+      __syncthreads();
+      const int off = (tid >= 32 ? s_wp[0] : 0) + __popc(bal & ((1u << (tid & 31)) - 1u));
+      const int np = s_wp[0] + s_wp[1];
+      if (keep) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          s_j0[off][a] = j0[a];
+          s_d0[off][a] = d0[a];
+          s_f[off][a] = sstr[(size_t)a * n + pi];
+        }
+      }
+      __syncthreads();
+      if (np == 0) continue;
+      for (int e = tid; e < np * 3 * kEwMaxW; e += blockDim.x) {  // weights: (point, axis, k)
+        const int q = e / (3 * kEwMaxW), r = e - q * 3 * kEwMaxW, a = r / kEwMaxW, k = r - a * kEwMaxW;
+        s_w[q][a][k] = k < w ? ew_phi(g, fabs((s_d0[q][a] + k) * g.h * g.inv_alpha)) : 0.0;
+      }
+      __syncthreads();
+      for (int q = 0; q < np; ++q) {
+        int ox = gx - s_j0[q][0], oy = gy - s_j0[q][1];
+        ox += ox < 0 ? M : 0;
+        oy += oy < 0 ? M : 0;
+        if (ox >= w || oy >= w) continue;
+        const double wxy = s_w[q][0][ox] * s_w[q][1][oy];
+        const double f0 = wxy * s_f[q][0], f1 = wxy * s_f[q][1], f2 = wxy * s_f[q][2];
+        // row k of the brick is stencil row k - dz (dz in (-w, 16) after unwrapping)
+        int dz = s_j0[q][2] - b0[2];
+        dz += dz <= -w ? M : 0;
+        dz -= dz >= kEwTB ? M : 0;
+        const double* wz = s_w[q][2];
+#pragma unroll
+        for (int k = 0; k < kEwTB; ++k) {
+          const int oz = k - dz;
+          if (oz >= 0 && oz < w) {
+            const double v = wz[oz];
+            acc[k][0] = fma(v, f0, acc[k][0]);
+            acc[k][1] = fma(v, f1, acc[k][1]);
+            acc[k][2] = fma(v, f2, acc[k][2]);
+          }
+        }
+      }
+    }
+  }
+  if (gx < M && gy < M) {
+#pragma unroll
+    for (int k = 0; k < kEwTB; ++k) {
+      const int gz = b0[2] + k;
+      if (gz < M) {
+        const size_t o = ((size_t)gz * M + gy) * M + gx;
+        grid[o] = acc[k][0];
+        grid[M3 + o] = acc[k][1];
+        grid[2 * M3 + o] = acc[k][2];
+      }
+    }
+  }
+}
+
 // cell boundaries of Morton-sorted quantized points at level L (3D):
 // bnd[c] = first point with cell >= c, c = 0..8^L
 __global__ void k_cell_bounds(int n, const int32_t* __restrict__ q, int L, int ncell, int* __restrict__ bnd) {
@@ -165,6 +302,17 @@ int grid_for_n(size_t n, int threads) {
 void launch_ew_spread(const EwGrid& g, int n, const double* spts, const double* sstr, double* grid, cudaStream_t st) {
   if (n <= 0) return;
   k_ew_spread<<<grid_for_n(n, 128), 128, 0, st>>>(g, n, spts, sstr, grid);
+}
+
+// a stencil meets a brick in one run of rows (no double wrap) when Mg >= 16 + w
+bool ew_spread_tiled_ok(const EwGrid& g, int Lc) {
+  return g.w <= kEwTB && g.w <= kEwMaxW && Lc <= 7 && g.Mg >= kEwTB + g.w;
+}
+
+void launch_ew_spread_tiled(const EwGrid& g, int Lc, const int* bnd, int n, const double* spts, const double* sstr,
+                            double* grid, cudaStream_t st) {
+  const int nbk = (g.Mg + kEwTB - 1) / kEwTB;
+  k_ew_spread2<<<nbk * nbk * nbk, 256, 0, st>>>(g, Lc, bnd, spts, n, sstr, grid);
 }
 
 void launch_ew_symbol(const EwGrid& g, double2* spec, const double* A, const double* dfac, cudaStream_t st) {

@@ -224,6 +224,11 @@ void launch_ew_spread(const EwGrid& g, int n, const double* spts, const double* 
 void launch_ew_symbol(const EwGrid& g, double2* spec, const double* A, const double* dfac, cudaStream_t st);
 void launch_ew_gather(const EwGrid& g, int n, const double* tpts, const int* tperm, const double* grid, double* u,
                       cudaStream_t st);
+// deterministic spreading (no atomics): sources binned by Morton cells at
+// level Lc (bnd as launch_cell_bounds); usable when ew_spread_tiled_ok(g, Lc)
+bool ew_spread_tiled_ok(const EwGrid& g, int Lc);
+void launch_ew_spread_tiled(const EwGrid& g, int Lc, const int* bnd, int n, const double* spts, const double* sstr,
+                            double* grid, cudaStream_t st);
 // bnd[c] = first sorted point in Morton cell >= c at level L (3D), c = 0..8^L
 void launch_cell_bounds(int n, const int32_t* q, int L, int* bnd, cudaStream_t st);
 
