@@ -17,7 +17,7 @@ python tools/launch_summary.py "$out/launches_metric.csv" > "$out/launches_metri
 python tools/launch_summary.py "$out/launches_cfg4.csv" > "$out/launches_cfg4.txt"
 one="python tools/prof_step.py --n 10000000 --reps 1"
 # kernel regex : launches to skip (the big level-5 launch where a kernel runs per level)
-for spec in k_residual:0 k_interp_mma:0 k_anterp2:0 k_basis:0 k_tensor_up:4 k_tensor_down:3 k_inv_xy3:8 k_acc_group:8 \
+for spec in k_residual:0 k_interp_mma:0 k_anterp2:0 k_basis:0 k_tensor_up:0 k_tensor_down:4 k_inv_xy3:8 k_acc_group:8 \
             k_fwd_xy3:5 k_zi3:8 k_zf3:5 k_morton:0 k_gather_points:0 k_pack_sources:0 k_combine:0; do
   k=${spec%%:*}; skip=${spec##*:}
   ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip $skip -c 1 \
