@@ -463,9 +463,15 @@ struct Builder {
     } else {
       root.push_back({0, {0, 0, 0}});
     }
+    // colleague and coarse lists: at most 3^d entries per box, so each box
+    // gets a fixed slot of that size (one pass per level, no counting pass,
+    // no growth); the fine lists stay compact (two-pass CSR)
+    const int K = t.dim == 3 ? 27 : 9;
+    t.col.v.resize((size_t)nb * K);
+    t.crs.v.resize((size_t)nb * K);
     t.col.off[0] = 0;
     t.col.len[0] = (int)root.size();
-    t.col.v = root;
+    std::copy(root.begin(), root.end(), t.col.v.begin());
     // relative position of box c (with periodic shift sh) to box b, in units of
     // b's side, per axis: exact integer (anchors are multiples of the side)
     // (the difference is an exact multiple of the power-of-two unit: a shift)
@@ -510,20 +516,21 @@ struct Builder {
         }
         return n;
       };
-      csr_pass(t.col, ids, [&](int b) { return col_scan(b, nullptr); }, [&](int b, Nbr* out) { col_scan(b, out); });
-      // coarse: the parent's leaf colleagues that touch b
-      csr_pass(
-          t.crs, leaves_only ? leaf_ids(ids) : ids,
-          [&](int b) {
-            int c = 0;
-            for (const Nbr& pc : t.col[t.boxes[b].parent])
-              if (t.boxes[pc.box].leaf) c += touch(b, pc.box, pc.shift);
-            return c;
-          },
-          [&](int b, Nbr* out) {
-            for (const Nbr& pc : t.col[t.boxes[b].parent])
-              if (t.boxes[pc.box].leaf && touch(b, pc.box, pc.shift)) *out++ = pc;
-          });
+      const int nl = (int)ids.size();
+#pragma omp parallel for schedule(dynamic, 128)
+      for (int i = 0; i < nl; ++i) {
+        const int b = ids[i];
+        t.col.off[b] = (int64_t)b * K;
+        t.col.len[b] = col_scan(b, t.col.v.data() + (size_t)b * K);
+        // coarse: the parent's leaf colleagues that touch b
+        if (leaves_only && !t.boxes[b].leaf) continue;
+        Nbr* out = t.crs.v.data() + (size_t)b * K;
+        int c = 0;
+        for (const Nbr& pc : t.col[t.boxes[b].parent])
+          if (t.boxes[pc.box].leaf && touch(b, pc.box, pc.shift)) out[c++] = pc;
+        t.crs.off[b] = (int64_t)b * K;
+        t.crs.len[b] = c;
+      }
     }
     // fine: leaf children of non-leaf colleagues (other than self) that touch b.
     // A colleague at offset o (b's units) has children at 2 o + cc (half
@@ -674,9 +681,15 @@ std::string dump_topology(const HostTree& t) {  // tree.cpp:325-354
 ShardCosts shard_costs(const HostTree& t) {
   ShardCosts c;
   const int nb = t.num_boxes();
+  // target leaves in Morton order = by the start of their target range
+  // (sorted as packed (tb, id) keys: no indirection in the comparisons)
+  std::vector<uint64_t> key;
+  key.reserve(nb);
   for (int b = 0; b < nb; ++b)
-    if (t.boxes[b].leaf && t.ntgt(b) > 0) c.leaves.push_back(b);
-  std::sort(c.leaves.begin(), c.leaves.end(), [&](int a, int b) { return t.boxes[a].tb < t.boxes[b].tb; });
+    if (t.boxes[b].leaf && t.ntgt(b) > 0) key.push_back((uint64_t(uint32_t(t.boxes[b].tb)) << 32) | uint32_t(b));
+  std::sort(key.begin(), key.end());
+  c.leaves.resize(key.size());
+  for (size_t i = 0; i < key.size(); ++i) c.leaves[i] = int(key[i] & 0xffffffffu);
   const int nl = (int)c.leaves.size();
   c.w.assign(nl, 0);
 #pragma omp parallel for schedule(static)
