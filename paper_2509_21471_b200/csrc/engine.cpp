@@ -2275,7 +2275,7 @@ void Context::ewald(const Plan& P, int64_t ns, const double* src, int64_t nt, co
   launch_ew_symbol(g, spec, (const double*)(dv2 + o_a), (const double*)(dv2 + o_d), st_);
   fft_.inverse(spec, grid);
   double* ufar = arena_.as<double>("ufar", (size_t)m * d);
-  launch_ew_gather(g, m, tpts, tperm, grid, ufar, st_);
+  launch_ew_gather(g, m, tpts, tperm, grid, arena_.get("ew_gi", M3 * 4 * sizeof(double)), ufar, st_);
   cudaEventRecord(ev_[3], st_);
   double* du = device_ptrs ? u : arena_.as<double>("u", (size_t)m * d);
   launch_combine(m, d, ufar, ures, nullptr, 0.0, nullptr, nullptr, nullptr, du, st_);

@@ -101,11 +101,19 @@ __global__ void k_ew_symbol(EwGrid g, double2* __restrict__ spec, const double* 
   }
 }
 
-// one thread per target (Morton order), written to caller order
+// the three component grids interleaved per point, (g0, g1) | (g2, pad), so
+// the gather reads one 16-byte and one 8-byte value per grid point instead
+// of three 8-byte values from three arrays
+__global__ void k_ew_interleave(size_t M3, const double* __restrict__ grid, double4* __restrict__ gi) {
+  for (size_t o = blockIdx.x * (size_t)blockDim.x + threadIdx.x; o < M3; o += (size_t)gridDim.x * blockDim.x)
+    gi[o] = make_double4(grid[o], grid[M3 + o], grid[2 * M3 + o], 0.0);
+}
+
+// one thread per target (Morton order: neighbouring threads share stencil
+// lines in L1), written to caller order
 __global__ void k_ew_gather(EwGrid g, int n, const double* __restrict__ tpts, const int* __restrict__ tperm,
-                            const double* __restrict__ grid, double* __restrict__ u) {
+                            const double4* __restrict__ gi, double* __restrict__ u) {
   const int M = g.Mg;
-  const size_t M3 = (size_t)M * M * M;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double wx[kEwMaxW], wy[kEwMaxW], wz[kEwMaxW];
     const int jx = ew_weights(g, tpts[i] + 0.5, wx);
@@ -116,13 +124,15 @@ __global__ void k_ew_gather(EwGrid g, int n, const double* __restrict__ tpts, co
       const size_t oz = (size_t)ew_wrap(jz + kz, M) * M;
       for (int ky = 0; ky < g.w; ++ky) {
         const double wzy = wz[kz] * wy[ky];
-        const size_t oy = (oz + ew_wrap(jy + ky, M)) * M;
+        const double4* row = gi + (oz + ew_wrap(jy + ky, M)) * M;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0;
         for (int kx = 0; kx < g.w; ++kx) {
-          const size_t o = oy + ew_wrap(jx + kx, M);
-          s0 = fma(wx[kx], grid[o], s0);
-          s1 = fma(wx[kx], grid[M3 + o], s1);
-          s2 = fma(wx[kx], grid[2 * M3 + o], s2);
+          const double2* pv = reinterpret_cast<const double2*>(row + ew_wrap(jx + kx, M));
+          const double2 a = __ldg(pv);
+          const double c = __ldg(reinterpret_cast<const double*>(pv + 1));
+          s0 = fma(wx[kx], a.x, s0);
+          s1 = fma(wx[kx], a.y, s1);
+          s2 = fma(wx[kx], c, s2);
         }
         u0 = fma(wzy, s0, u0);
         u1 = fma(wzy, s1, u1);
@@ -320,10 +330,13 @@ void launch_ew_symbol(const EwGrid& g, double2* spec, const double* A, const dou
   k_ew_symbol<<<grid_for_n(S, 256), 256, 0, st>>>(g, spec, A, dfac);
 }
 
-void launch_ew_gather(const EwGrid& g, int n, const double* tpts, const int* tperm, const double* grid, double* u,
-                      cudaStream_t st) {
+void launch_ew_gather(const EwGrid& g, int n, const double* tpts, const int* tperm, const double* grid, void* gi,
+                      double* u, cudaStream_t st) {
   if (n <= 0) return;
-  k_ew_gather<<<grid_for_n(n, 128), 128, 0, st>>>(g, n, tpts, tperm, grid, u);
+  const size_t M3 = (size_t)g.Mg * g.Mg * g.Mg;
+  double4* g4 = reinterpret_cast<double4*>(gi);
+  k_ew_interleave<<<grid_for_n(M3, 256), 256, 0, st>>>(M3, grid, g4);
+  k_ew_gather<<<grid_for_n(n, 128), 128, 0, st>>>(g, n, tpts, tperm, g4, u);
 }
 
 void launch_cell_bounds(int n, const int32_t* q, int L, int* bnd, cudaStream_t st) {

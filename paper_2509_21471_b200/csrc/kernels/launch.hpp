@@ -222,8 +222,9 @@ struct EwGrid {
 };
 void launch_ew_spread(const EwGrid& g, int n, const double* spts, const double* sstr, double* grid, cudaStream_t st);
 void launch_ew_symbol(const EwGrid& g, double2* spec, const double* A, const double* dfac, cudaStream_t st);
-void launch_ew_gather(const EwGrid& g, int n, const double* tpts, const int* tperm, const double* grid, double* u,
-                      cudaStream_t st);
+// gi: scratch of Mg^3 x 32 bytes (the grid interleaved per point)
+void launch_ew_gather(const EwGrid& g, int n, const double* tpts, const int* tperm, const double* grid, void* gi,
+                      double* u, cudaStream_t st);
 // deterministic spreading (no atomics): sources binned by Morton cells at
 // level Lc (bnd as launch_cell_bounds); usable when ew_spread_tiled_ok(g, Lc)
 bool ew_spread_tiled_ok(const EwGrid& g, int Lc);
