@@ -297,6 +297,20 @@ int sdmk_get_stream(sdmk_context* ctx, void** stream);
 int sdmk_fp64_peak(sdmk_context* ctx, double* tflops);
 /* the same for the FP64 tensor cores (mma.sync.m8n8k4.f64, the DMMA kernels' roofline) */
 int sdmk_fp64_mma_peak(sdmk_context* ctx, double* tflops);
+/* guard mode, a memcheck / initcheck stand-in (test infrastructure): on a
+   context that has not allocated yet, every device buffer is allocated at
+   exactly its requested size between two 64 KB canary regions and is
+   poisoned with all-ones bytes (NaN doubles, -1 integers), so a kernel
+   writing out of bounds trips a canary and a read of an element nothing wrote
+   reaches the result.  sdmk_guard_check returns how many buffers had a canary
+   overwritten (their names, newline-separated, into names[cap]), or -1 on
+   error. */
+int sdmk_set_guard(sdmk_context* ctx, int on);
+int64_t sdmk_guard_check(sdmk_context* ctx, char* names, int64_t cap);
+/* the detector's self-test on a guarded context: stores one byte past the end
+   and one before the start of a scratch buffer; 1 when sdmk_guard_check named
+   it both times, 0 when not (or the context is not guarded), -1 on error */
+int sdmk_guard_selftest(sdmk_context* ctx);
 
 /* ---- host-only helpers (no GPU needed; used by the CPU test suite) ----
    Plan-level setup exactly as the GPU path uses it. */

@@ -105,6 +105,9 @@ def lib():
             "sdmk_get_stream": ([C.c_void_p, P(C.c_void_p)], C.c_int),
             "sdmk_fp64_peak": ([C.c_void_p, P(C.c_double)], C.c_int),
             "sdmk_fp64_mma_peak": ([C.c_void_p, P(C.c_double)], C.c_int),
+            "sdmk_set_guard": ([C.c_void_p, C.c_int], C.c_int),
+            "sdmk_guard_check": ([C.c_void_p, C.c_char_p, C.c_int64], C.c_int64),
+            "sdmk_guard_selftest": ([C.c_void_p], C.c_int),
             "sdmk_host_save_tables": ([P(sdmk_plan), C.c_char_p], C.c_int),
             "sdmk_host_symbol_table": ([P(sdmk_plan), C.c_double, C.c_int, C.c_int, C.c_double, C.c_double, dp],
                                        C.c_int),
@@ -479,6 +482,27 @@ class Context:
         v = C.c_double()
         _raise(lib().sdmk_fp64_peak(self._h, C.byref(v)))
         return float(v.value)
+
+    def set_guard(self, on: bool = True):
+        """Guard mode (canaries around every device buffer, poisoned contents);
+        call before the context's first setup or evaluation."""
+        _raise(lib().sdmk_set_guard(self._h, 1 if on else 0))
+
+    def guard_check(self) -> list:
+        """Names of device buffers whose canaries were overwritten."""
+        buf = C.create_string_buffer(1 << 16)
+        n = lib().sdmk_guard_check(self._h, buf, len(buf))
+        if n < 0:
+            _raise(-1 if n == -1 else int(n))
+        return [s for s in buf.value.decode().split("\n") if s]
+
+    def guard_selftest(self) -> bool:
+        """Store one byte past each end of a scratch buffer; True when the
+        canary check caught both."""
+        r = lib().sdmk_guard_selftest(self._h)
+        if r < 0:
+            _raise(r)
+        return r == 1
 
     def fp64_mma_peak_tflops(self) -> float:
         v = C.c_double()

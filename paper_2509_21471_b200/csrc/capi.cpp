@@ -1,6 +1,8 @@
 // extern "C" boundary of libsdmk_b200.so (declared in include/sdmk.h).
 // Never throws: exceptions become sdmk_status codes plus sdmk_last_error().
+#include <algorithm>
 #include <cstring>
+#include <vector>
 #include <string>
 
 #include "../../include/sdmk.h"
@@ -509,6 +511,32 @@ int sdmk_fp64_peak(sdmk_context* c, double* tflops) {
     *tflops = measure_fp64_peak_tflops(x->stream());
     cuda_check(cudaGetLastError(), "fp64 peak kernel");
   });
+}
+
+int sdmk_set_guard(sdmk_context* c, int on) {
+  return guarded([&] { need_ctx(c)->set_guard(on != 0); });
+}
+
+int64_t sdmk_guard_check(sdmk_context* c, char* names, int64_t cap) {
+  int64_t n = -1;
+  const int rc = guarded([&] {
+    const std::vector<std::string> bad = need_ctx(c)->guard_check();
+    std::string s;
+    for (auto& b : bad) s += b + "\n";
+    if (names && cap > 0) {
+      const size_t k = std::min<size_t>(s.size(), (size_t)cap - 1);
+      std::memcpy(names, s.data(), k);
+      names[k] = 0;
+    }
+    n = (int64_t)bad.size();
+  });
+  return rc == 0 ? n : -1;
+}
+
+int sdmk_guard_selftest(sdmk_context* c) {
+  int caught = 0;
+  const int rc = guarded([&] { caught = need_ctx(c)->guard_selftest() ? 1 : 0; });
+  return rc == 0 ? caught : -1;
 }
 
 int sdmk_fp64_mma_peak(sdmk_context* c, double* tflops) {

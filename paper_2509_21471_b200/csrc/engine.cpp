@@ -116,31 +116,78 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 
 Arena::~Arena() {
-  for (auto& kv : bufs_) cudaFree(kv.second.first);
+  for (auto& kv : bufs_) cudaFree(kv.second.base);
 }
 
 void* Arena::get(const std::string& name, size_t bytes) {
   if (bytes == 0) bytes = 16;
   auto it = bufs_.find(name);
-  if (it != bufs_.end() && it->second.second >= bytes) return it->second.first;
+  if (it != bufs_.end() && it->second.req >= bytes) return static_cast<char*>(it->second.base) + (guard_ ? kGuard : 0);
   if (it != bufs_.end()) {
-    cudaFree(it->second.first);
+    cudaFree(it->second.base);
     bufs_.erase(it);
   }
-  size_t alloc = bytes + bytes / 16 + 256;
+  const size_t alloc = guard_ ? bytes + 2 * kGuard : bytes + bytes / 16 + 256;
   void* p = nullptr;
   cudaError_t e = cudaMalloc(&p, alloc);
   if (e != cudaSuccess) {
     cudaGetLastError();
     throw OomError("device allocation of " + std::to_string(alloc) + " bytes for '" + name + "' failed");
   }
-  bufs_[name] = {p, alloc};
-  return p;
+  if (guard_) {
+    char* c = static_cast<char*>(p);
+    cuda_check(cudaMemset(c, 0xA5, kGuard), "guard memset");
+    cuda_check(cudaMemset(c + kGuard, 0xFF, bytes), "poison memset");
+    cuda_check(cudaMemset(c + kGuard + bytes, 0xA5, kGuard), "guard memset");
+    cuda_check(cudaDeviceSynchronize(), "guard memset");
+  }
+  bufs_[name] = {p, alloc, guard_ ? bytes : alloc};
+  return static_cast<char*>(p) + (guard_ ? kGuard : 0);
+}
+
+void Arena::set_guard(bool on) {
+  if (on == guard_) return;
+  cudaDeviceSynchronize();
+  for (auto& kv : bufs_) cudaFree(kv.second.base);
+  bufs_.clear();
+  guard_ = on;
+}
+
+std::vector<std::string> Arena::check() const {
+  std::vector<std::string> bad;
+  if (!guard_) return bad;
+  cuda_check(cudaDeviceSynchronize(), "guard check");
+  std::vector<unsigned char> h(kGuard);
+  for (auto& kv : bufs_) {
+    const char* c = static_cast<const char*>(kv.second.base);
+    bool ok = true;
+    for (const char* g : {c, c + kGuard + kv.second.req}) {
+      cuda_check(cudaMemcpy(h.data(), g, kGuard, cudaMemcpyDeviceToHost), "guard check");
+      for (unsigned char v : h) ok = ok && v == 0xA5;
+    }
+    if (!ok) bad.push_back(kv.first);
+  }
+  return bad;
+}
+
+bool Arena::selftest() {
+  if (!guard_) return false;
+  bool caught = true;
+  for (int side = 0; side < 2; ++side) {
+    const std::string name = "guard_selftest";
+    char* p = static_cast<char*>(get(name, 1000));
+    cuda_check(cudaMemset(side ? p - 1 : p + 1000, 0, 1), "guard selftest");
+    const std::vector<std::string> bad = check();
+    caught = caught && bad.size() == 1 && bad[0] == name;
+    cudaFree(bufs_[name].base);
+    bufs_.erase(name);
+  }
+  return caught && check().empty();
 }
 
 size_t Arena::bytes() const {
   size_t s = 0;
-  for (auto& kv : bufs_) s += kv.second.second;
+  for (auto& kv : bufs_) s += kv.second.alloc;
   return s;
 }
 

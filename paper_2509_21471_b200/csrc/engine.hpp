@@ -40,9 +40,28 @@ class Arena {
   template <class T>
   T* as(const std::string& name, size_t count) { return static_cast<T*>(get(name, count * sizeof(T))); }
   size_t bytes() const;
+  // Guard mode (a memcheck / initcheck stand-in for pools where
+  // compute-sanitizer is closed): every buffer is allocated at exactly its
+  // requested size between two 64 KB canary regions, and its contents are
+  // poisoned with all-ones bytes (a NaN in every double, -1 in every integer)
+  // so a read of an element no kernel wrote reaches the result.  check()
+  // returns the names of buffers whose canaries were overwritten.
+  void set_guard(bool on);
+  bool guard() const { return guard_; }
+  std::vector<std::string> check() const;
+  // writes one byte past the end of a scratch buffer and one before its
+  // start, and reports whether check() names it (the detector's self-test)
+  bool selftest();
 
  private:
-  std::map<std::string, std::pair<void*, size_t>> bufs_;
+  static constexpr size_t kGuard = 64 * 1024;
+  struct Buf {
+    void* base;    // cudaMalloc'd pointer
+    size_t alloc;  // bytes allocated
+    size_t req;    // bytes the caller may touch (guard mode)
+  };
+  bool guard_ = false;
+  std::map<std::string, Buf> bufs_;
 };
 
 class Pinned {
@@ -150,6 +169,14 @@ class Context {
     return dump_topology(prob_.tree);
   }
   cudaStream_t stream() const { return st_; }
+  // guard mode (Arena::set_guard): only on a context that has not allocated yet
+  void set_guard(bool on) {
+    if (arena_.bytes() > 0 && on != arena_.guard())
+      throw InvalidArgument("sdmk_set_guard: call before the context's first setup or evaluation");
+    arena_.set_guard(on);
+  }
+  std::vector<std::string> guard_check() const { return arena_.check(); }
+  bool guard_selftest() { return arena_.selftest(); }
   void upward(double* host_out);
   void incoming(int stage, double* host_out);
   void target_far(double* host_out);

@@ -445,7 +445,8 @@ __global__ void __launch_bounds__(W * 32, 1) k_anterp2(ChebDev cb, const DBox* _
 //    has one (j, iz) and a fixed iy block;
 //  * y contraction in the epilogue: a lane's C columns are always
 //    iy = 8q + 2t + {0,1}, so its 2 TY by values per target live in registers;
-//  * z contraction once per (j, iz) row with bz from shared memory.
+//  * z contraction as one running FMA per (j, iz) row with bz from shared
+//    memory, handed to component j when its last iz row is done.
 // The leaf's W streams once through shared memory (cp.async, RG (j, iz) rows
 // per chunk, double buffered) while every target of the leaf is resident:
 // warp w owns m-tiles w, w + kIW, ..., and each B fragment feeds its
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DB
       const int a = e / p, k = e % p;
       bzs[a * BZ + k] = a < tc ? (dim == 3 ? bzg[(size_t)(t0 + a) * p + k] : (k == 0 ? 1.0 : 0.0)) : 0.0;
     }
-    double af[kITW][KS], byv[kITW][TY][2], v[kITW][3];
+    double af[kITW][KS], byv[kITW][TY][2], v[kITW][3], vz[kITW];
 #pragma unroll
     for (int i = 0; i < kITW; ++i) {
       const int r = (warp + kIW * i) * 8 + g;
@@ -508,7 +509,7 @@ __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DB
       for (int q = 0; q < TY; ++q)
 #pragma unroll
         for (int e = 0; e < 2; ++e) byv[i][q][e] = (ok && 8 * q + 2 * t + e < p) ? byr[8 * q + 2 * t + e] : 0.0;
-      v[i][0] = v[i][1] = v[i][2] = 0.0;
+      v[i][0] = v[i][1] = v[i][2] = vz[i] = 0.0;
     }
     const int nmine = warp < ntm ? (ntm - warp + kIW - 1) / kIW : 0;  // m-tiles this warp owns
     const bool full = nmine == kITW;
@@ -560,10 +561,16 @@ __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DB
             double s = 0.0;
 #pragma unroll
             for (int q = 0; q < TY; ++q) s = fma(byv[i][q][0], cc[i][q][0], fma(byv[i][q][1], cc[i][q][1], s));
-            s *= bzs[((warp + kIW * i) * 8 + g) * BZ + iz];
+            vz[i] = fma(s, bzs[((warp + kIW * i) * 8 + g) * BZ + iz], vz[i]);
+          }
+          if (iz == pz - 1) {  // the z sum of component j is complete (warp-uniform)
 #pragma unroll
-            for (int jj = 0; jj < 3; ++jj)
-              if (jj == j) v[i][jj] += s;
+            for (int i = 0; i < kITW; ++i) {
+#pragma unroll
+              for (int jj = 0; jj < 3; ++jj)
+                if (jj == j) v[i][jj] = vz[i];
+              vz[i] = 0.0;
+            }
           }
         }
       }
