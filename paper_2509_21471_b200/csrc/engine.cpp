@@ -1355,6 +1355,7 @@ void Context::run_target_far(double* ufar) {  // dmk.cpp:861-915
     launch_interp_targets(cb, pr.boxes, pr.int_leaves, pr.n_int, pr.tpts, pr.nt, pr.tperm, incoming, ufar, st_);
   }
   ++launches_;
+  cuda_check(cudaPeekAtLastError(), "far-field kernel launch");
 }
 
 void Context::run_residual(double* ures, bool stats, int reserve_sms) {  // dmk.cpp:919-1032

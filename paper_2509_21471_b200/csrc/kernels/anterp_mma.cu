@@ -434,6 +434,15 @@ __global__ void __launch_bounds__(W * 32, 1) k_anterp2(ChebDev cb, const DBox* _
 #ifndef SDMK_I_ROWS
 #define SDMK_I_ROWS 128  // W rows staged per chunk (rounded down to whole (j, iz) row groups)
 #endif
+// doubles per flat W buffer (even: 16-byte aligned buffers): the copy (RG
+// row groups of p x p plus one leading alignment double, rounded to 16 bytes)
+// and the furthest padded fragment read (row PY - 1, column PY - 1 of the
+// last group, past the leading double)
+__host__ __device__ constexpr int interp_flat(int RG, int PY, int p) {
+  return ((RG * p * p + 2 > (RG - 1) * p * p + (PY - 1) * p + PY + 1 ? RG * p * p + 2
+                                                                     : (RG - 1) * p * p + (PY - 1) * p + PY + 1) +
+          1) & ~1;
+}
 // warps per CTA (IW) and m-tiles per warp (ITW) are template parameters:
 // 8 x 5 for TY <= 3 (p <= 24; measured 4 % faster than 12 x 4 at p = 23),
 // 12 x 4 above (the 8 x 5 accumulators would spill); one pass per leaf covers
@@ -447,10 +456,14 @@ __global__ void __launch_bounds__(W * 32, 1) k_anterp2(ChebDev cb, const DBox* _
 //    iy = 8q + 2t + {0,1}, so its 2 TY by values per target live in registers;
 //  * z contraction as one running FMA per (j, iz) row with bz from shared
 //    memory, handed to component j when its last iz row is done.
-// The leaf's W streams once through shared memory (cp.async, RG (j, iz) rows
-// per chunk, double buffered) while every target of the leaf is resident:
-// warp w owns m-tiles w, w + kIW, ..., and each B fragment feeds its
-// kITW tiles (TY x kITW independent DMMA chains per k-step).
+// The leaf's W streams once through shared memory while every target of the
+// leaf is resident: RG (j, iz) row groups per chunk are one contiguous range
+// of the incoming array, moved by one 1D TMA bulk copy (cp.async.bulk, issued
+// by one thread, completion on an mbarrier; double buffered) into a flat
+// [rows][p] copy.  Fragment reads of the padding (iy >= p or ix >= p) are
+// predicated to zero, so the flat copy needs no padded rows.  Warp w owns
+// m-tiles w, w + kIW, ..., and each B fragment feeds its kITW tiles (TY x kITW
+// independent DMMA chains per k-step).
 template <int TY, int PC, int DC, int kIW = (TY <= 3 ? 8 : 12), int kITW = (TY <= 3 ? 5 : 4)>
 __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DBox* __restrict__ boxes,
                                                            const int* __restrict__ leaves,
@@ -458,40 +471,52 @@ __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DB
                                                            const int* __restrict__ tperm,
                                                            const double* __restrict__ incoming,
                                                            double* __restrict__ ufar) {
-  constexpr int PY = 8 * TY, KS = 2 * TY, WS = PY + 4;
+  constexpr int PY = 8 * TY, KS = 2 * TY;
   constexpr int kTB = kIW * kITW * 8;  // targets per pass
   constexpr int RG = PY >= SDMK_I_ROWS ? 1 : SDMK_I_ROWS / PY;  // (j, iz) rows per chunk
-  constexpr int NR = RG * PY;                   // W rows per chunk
   extern __shared__ double sm[];
+  __shared__ uint64_t bar[2];
   const int p = PC > 0 ? PC : cb.p, dim = DC > 0 ? DC : cb.dim, pz = dim == 3 ? p : 1;
   const int NG = dim * pz;          // (j, iz) rows
+  const int P2 = p * p;
+  const int FL = interp_flat(RG, PY, p);  // doubles per buffer
   const int BZ = p | 1;             // odd row stride: the 8 target rows of a fragment hit distinct banks
-  double* Ws = sm;                  // [2][NR][WS]
-  double* bzs = Ws + 2 * NR * WS;   // [kTB][BZ]
+  double* Ws = sm;                  // [2][FL]
+  double* bzs = Ws + 2 * FL;        // [kTB][BZ]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int b = leaves[blockIdx.x];
   const DBox box = boxes[b];
-  for (int e = tid; e < 2 * NR * WS; e += blockDim.x) Ws[e] = 0.0;  // k padding stays zero
-  const double* W = incoming + (size_t)b * NG * p * p;
+  if (tid == 0) {
+    dev::mbar_init(&bar[0], 1);
+    dev::mbar_init(&bar[1], 1);
+    dev::mbar_fence_init();
+  }
+  const double* W = incoming + (size_t)b * NG * P2;
   const double* bxg = tbasis;
   const double* byg = tbasis + (size_t)nt * p;
   const double* bzg = tbasis + (size_t)2 * nt * p;
   const int nchunk = (NG + RG - 1) / RG;
-  auto issue = [&](int c, int buf) {  // a warp per W row, a lane per column
-    double* dstb = Ws + buf * NR * WS;
-    for (int r = warp; r < NR; r += kIW) {
-      const int gi = c * RG + r / PY, iy = r % PY;
-      const bool v = gi < NG && iy < p;
-      const double* src = W + ((size_t)(v ? gi : 0) * p + (v ? iy : 0)) * p;
-      for (int k = lane; k < p; k += 32) dev::cp_async8(dstb + r * WS + k, src + k, v);
-    }
-    dev::cp_commit();
+  // chunk c: rows [c RG, c RG + ng) = W[c RG P2, (c RG + ng) P2), copied from
+  // the 16-byte boundary at or below its start (sh = 1 extra leading double)
+  auto shift = [&](int c) { return (int)((reinterpret_cast<uintptr_t>(W + (size_t)c * RG * P2) >> 3) & 1); };
+  auto issue = [&](int c, int buf) {  // one thread
+    const int ng = min(RG, NG - c * RG), sh = shift(c);
+    const uint32_t bytes = (uint32_t)(((ng * P2 + sh) * 8 + 15) & ~15);
+    dev::mbar_expect_tx(&bar[buf], bytes);
+    dev::bulk_g2s(Ws + buf * FL, W + (size_t)c * RG * P2 - sh, bytes, &bar[buf]);
   };
+  // per-lane validity of the padded fragment rows (iy) and columns (ix)
+  bool vq[TY], vk[KS];
+#pragma unroll
+  for (int q = 0; q < TY; ++q) vq[q] = q * 8 + g < p;
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) vk[ks] = ks * 4 + t < p;
+  int seq = 0;  // chunks issued so far (buffer seq & 1, mbarrier phase seq >> 1)
+  __syncthreads();  // barriers initialised
   for (int t0 = box.tb; t0 < box.te; t0 += kTB) {
     const int tc = min(kTB, box.te - t0);
     const int ntm = (tc + 7) / 8;
-    __syncthreads();
-    issue(0, 0);
+    if (tid == 0) issue(0, seq & 1);
     for (int e = tid; e < kTB * p; e += blockDim.x) {
       const int a = e / p, k = e % p;
       bzs[a * BZ + k] = a < tc ? (dim == 3 ? bzg[(size_t)(t0 + a) * p + k] : (k == 0 ? 1.0 : 0.0)) : 0.0;
@@ -513,16 +538,12 @@ __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DB
     }
     const int nmine = warp < ntm ? (ntm - warp + kIW - 1) / kIW : 0;  // m-tiles this warp owns
     const bool full = nmine == kITW;
-    for (int c = 0; c < nchunk; ++c) {
-      const int buf = c & 1;
-      if (c + 1 < nchunk) {
-        issue(c + 1, buf ^ 1);
-        dev::cp_wait1();
-      } else {
-        dev::cp_wait0();
-      }
-      __syncthreads();
-      const double* Wc = Ws + buf * NR * WS;
+    __syncthreads();  // bz rows staged
+    for (int c = 0; c < nchunk; ++c, ++seq) {
+      const int buf = seq & 1;
+      if (tid == 0 && c + 1 < nchunk) issue(c + 1, buf ^ 1);  // its buffer was released at the end of c - 1
+      dev::mbar_wait(&bar[buf], (uint32_t)((seq >> 1) & 1));
+      const double* Wc = Ws + buf * FL + shift(c);
       if (nmine > 0) {
         const int ng = min(RG, NG - c * RG);
         for (int gl = 0; gl < ng; ++gl) {
@@ -532,7 +553,7 @@ __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DB
           for (int i = 0; i < kITW; ++i)
 #pragma unroll
             for (int q = 0; q < TY; ++q) cc[i][q][0] = cc[i][q][1] = 0.0;
-          const double* Wg = Wc + (gl * PY + g) * WS + t;
+          const double* Wg = Wc + gl * P2 + g * p + t;
           if (full) {
             // every m-tile: no per-DMMA predicate (each predicated DMMA costs a
             // WARPSYNC + NOP)
@@ -540,7 +561,9 @@ __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DB
             for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
               for (int q = 0; q < TY; ++q) {
-                const double bv = Wg[q * 8 * WS + ks * 4];
+                double bv = Wg[q * 8 * p + ks * 4];
+                if ((PC == 0 || (q == TY - 1 && PC % 8 != 0) || (ks == KS - 1 && PC % 4 != 0)) && !(vq[q] && vk[ks]))
+                  bv = 0.0;
 #pragma unroll
                 for (int i = 0; i < kITW; ++i) dev::dmma(cc[i][q][0], cc[i][q][1], af[i][ks], bv);
               }
@@ -549,7 +572,9 @@ __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DB
             for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
               for (int q = 0; q < TY; ++q) {
-                const double bv = Wg[q * 8 * WS + ks * 4];
+                double bv = Wg[q * 8 * p + ks * 4];
+                if ((PC == 0 || (q == TY - 1 && PC % 8 != 0) || (ks == KS - 1 && PC % 4 != 0)) && !(vq[q] && vk[ks]))
+                  bv = 0.0;
 #pragma unroll
                 for (int i = 0; i < kITW; ++i)
                   if (i < nmine) dev::dmma(cc[i][q][0], cc[i][q][1], af[i][ks], bv);
@@ -574,7 +599,7 @@ __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DB
           }
         }
       }
-      __syncthreads();  // the next issue overwrites this buffer
+      __syncthreads();  // buffer released: the next issue overwrites it
     }
 #pragma unroll
     for (int i = 0; i < kITW; ++i) {
@@ -665,9 +690,9 @@ void launch_interp_mma(const ChebDev& cb, const DBox* boxes, const int* leaves, 
   const int p = cb.p;
   const int TYv = (p + 7) / 8;
   auto smem_for = [&](int TY) {
-    const int PY = 8 * TY, WS = PY + 4, RG = PY >= SDMK_I_ROWS ? 1 : SDMK_I_ROWS / PY;
+    const int PY = 8 * TY, RG = PY >= SDMK_I_ROWS ? 1 : SDMK_I_ROWS / PY;
     const int tb = TY <= 3 ? 8 * 5 * 8 : 12 * 4 * 8;  // the kernel's IW * ITW * 8
-    return sizeof(double) * (2 * (size_t)RG * PY * WS + (size_t)tb * (p | 1));
+    return sizeof(double) * (2 * (size_t)interp_flat(RG, PY, p) + (size_t)tb * (p | 1));
   };
 #define IMS(TY_, PC_, DC_)                                                                                \
   do {                                                                                                    \
