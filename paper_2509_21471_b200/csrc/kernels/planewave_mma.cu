@@ -948,8 +948,8 @@ __global__ void __launch_bounds__(kWI * 32, 1) k_inv_xy2(PWGrid g, const int* __
 
 // fwd_xy, warp-independent form (3D, p <= 24, N <= 33): the unit of work is
 // one (box, channel, z-slab); every warp walks units with a global stride,
-// its w slab arriving by cp.async (double buffered), and needs no CTA
-// barrier.  X stage with all PT x NX tiles register-blocked (a k-step loads
+// its w slab arriving by one 1D TMA bulk copy (per-warp mbarriers, double
+// buffered), and needs no CTA barrier.  X stage with all PT x NX tiles register-blocked (a k-step loads
 // PT + NX fragments for PT NX DMMAs), then the Hermitian-split Y stage
 // (P = Er ar, Q = Ei ai, R = Er ai, S = Ei ar; b[+-my] = (P -+ Q) + i (R +- S))
 // with all 2 x 2 tiles of the four products at once, the my = 0 row and the
@@ -1003,33 +1003,47 @@ __global__ void __launch_bounds__(WF * 32, 1) k_fwd_xy3(PWGrid g, const int* __r
     EYi[e] = vi;
   }
   for (int e = tid; e < N * M1; e += blockDim.x) colidx[e] = -1;
-  for (int e = lane; e < per_warp; e += 32) win[e] = 0.0;  // padding rows / columns stay 0
+  __shared__ uint64_t wbar[2 * WF];  // per warp: one mbarrier per w buffer
+  for (int e = lane; e < per_warp; e += 32) win[e] = 0.0;
+  if (lane == 0) {
+    dev::mbar_init(&wbar[2 * warp], 1);
+    dev::mbar_init(&wbar[2 * warp + 1], 1);
+    dev::mbar_fence_init();
+  }
+  dev::fence_proxy_async_smem();  // the zero fill precedes the bulk copies into the same bytes
   __syncthreads();
   for (int c = tid; c < ncol; c += blockDim.x) colidx[(g.col_my[c] + M) * M1 + g.col_m0[c]] = (short)c;
   __syncthreads();
   const int total = nbox * nch * p;
   const int nw = gridDim.x * WF;
-  auto issue = [&](int u, int buf) {
+  // a unit's w slab (p x p contiguous doubles) arrives by one 1D TMA bulk copy
+  // from the 16-byte boundary at or below its start (sh = 1 leading double)
+  // into a flat [iy][ix] copy; fragment reads of the padding are predicated
+  auto slab = [&](int u) {
     const int item = u / p, iz = u % p;
-    const double* src = outgoing + ((size_t)boxes[item / nch] * nch + item % nch) * (size_t)(p * pp) + (size_t)iz * pp;
-    double* dst = win + buf * P8 * SE;
-    for (int e = lane; e < pp; e += 32) cp_async8(dst + (e / p) * SE + e % p, src + e, true);
-    cp_commit();
+    return outgoing + ((size_t)boxes[item / nch] * nch + item % nch) * (size_t)(p * pp) + (size_t)iz * pp;
   };
+  auto issue = [&](int u, int buf) {  // lane 0
+    const double* src = slab(u);
+    const int sh = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+    const uint32_t bytes = (uint32_t)(((pp + sh) * 8 + 15) & ~15);
+    dev::mbar_expect_tx(&wbar[2 * warp + buf], bytes);
+    dev::bulk_g2s(win + buf * P8 * SE, src - sh, bytes, &wbar[2 * warp + buf]);
+  };
+  bool va[PT], vk[PT * 2];  // this lane's fragment rows (iy) and columns (ix) inside the slab
+#pragma unroll
+  for (int i = 0; i < PT; ++i) va[i] = i * 8 + gq < p;
+#pragma unroll
+  for (int ks = 0; ks < PT * 2; ++ks) vk[ks] = ks * 4 + t < p;
   int u = blockIdx.x * WF + warp;
-  if (u < total) issue(u, 0);
+  if (u < total && lane == 0) issue(u, 0);
   for (int k = 0; u < total; ++k, u += nw) {
     const int buf = k & 1;
-    if (u + nw < total) {
-      issue(u + nw, buf ^ 1);
-      cp_wait1();
-    } else {
-      cp_wait0();
-    }
-    __syncwarp();
+    if (u + nw < total && lane == 0) issue(u + nw, buf ^ 1);  // that buffer was released by the previous unit
+    dev::mbar_wait(&wbar[2 * warp + buf], (uint32_t)((k >> 1) & 1));
     const int item = u / p, iz = u % p;
     double2* Bo = B + (size_t)item * g.pz * ncol + (size_t)iz * ncol;
-    const double* A = win + buf * P8 * SE;
+    const double* A = win + buf * P8 * SE + ((reinterpret_cast<uintptr_t>(slab(u)) >> 3) & 1);
     // X stage: (ar + i ai)[iy][m0'] = sum_ix w[iy][ix] EXT[2 m0' + part][ix]
     {
       double c[PT][NXT][2];
@@ -1041,7 +1055,11 @@ __global__ void __launch_bounds__(WF * 32, 1) k_fwd_xy3(PWGrid g, const int* __r
       for (int ks = 0; ks < PT * 2; ++ks) {
         double av[PT], bv[NXT];
 #pragma unroll
-        for (int i = 0; i < PT; ++i) av[i] = A[(i * 8 + gq) * SE + ks * 4 + t];
+        for (int i = 0; i < PT; ++i) {
+          av[i] = A[(i * 8 + gq) * p + ks * 4 + t];
+          if ((PC == 0 || (i == PT - 1 && PC % 8 != 0) || (ks == PT * 2 - 1 && PC % 4 != 0)) && !(va[i] && vk[ks]))
+            av[i] = 0.0;
+        }
 #pragma unroll
         for (int j = 0; j < NXT; ++j) bv[j] = EXT[(j * 8 + gq) * SE + ks * 4 + t];
 #pragma unroll
