@@ -442,34 +442,37 @@ __global__ void __launch_bounds__(kWZF * 32, 1) k_zf3(PWGrid g, int nc, int nbox
   }
   for (int e = lane; e < 2 * P8 * kZR; e += 32) Bs[e] = make_double2(0.0, 0.0);  // rows iz >= pz stay 0
   __shared__ int s_ncol[33], s_off[33];  // slab table (mz + M), read per output element
+  __shared__ uint64_t zbar[2 * kWZF];    // per warp: one mbarrier per block buffer
   if (tid < 2 * M + 1) {
     s_ncol[tid] = g.slab_ncol[tid];
     s_off[tid] = g.slab_off[tid];
   }
+  if (lane == 0) {
+    dev::mbar_init(&zbar[2 * warp], 1);
+    dev::mbar_init(&zbar[2 * warp + 1], 1);
+    dev::mbar_fence_init();
+  }
+  dev::fence_proxy_async_smem();  // the zero fill precedes the bulk copies into the same bytes
   __syncthreads();
   const int ncbk = (ncol + kZB - 1) / kZB, total = nbox * nc * ncbk;
   const int nw = gridDim.x * kWZF;
+  // a unit's block: pz rows of ncb contiguous complex (16-byte aligned), one
+  // 1D TMA bulk copy per row, issued by lanes 0 .. pz - 1 (columns past ncb
+  // keep finite stale values; their outputs are not stored)
   auto issue = [&](int u, int buf) {
     const int bc = u / ncbk, c0 = (u % ncbk) * kZB, ncb = min(kZB, ncol - c0);
-    const double2* src = IN + (size_t)bc * pz * ncol + c0;
-    double2* dst = Bs + buf * P8 * kZR;
-    for (int e = lane; e < pz * kZB; e += 32) {
-      const int k = e / kZB, cc = e % kZB;
-      dev::cp_async16z(dst + k * kZR + cc, cc < ncb ? src + (size_t)k * ncol + cc : src, cc < ncb);
-    }
-    cp_commit();
+    if (lane == 0) dev::mbar_expect_tx(&zbar[2 * warp + buf], (uint32_t)(pz * ncb * 16));
+    __syncwarp();
+    if (lane < pz)
+      dev::bulk_g2s(Bs + buf * P8 * kZR + lane * kZR, IN + ((size_t)bc * pz + lane) * ncol + c0, (uint32_t)ncb * 16u,
+                    &zbar[2 * warp + buf]);
   };
   int u = blockIdx.x * kWZF + warp;
   if (u < total) issue(u, 0);
   for (int it = 0; u < total; ++it, u += nw) {
     const int buf = it & 1;
-    if (u + nw < total) {
-      issue(u + nw, buf ^ 1);
-      cp_wait1();
-    } else {
-      cp_wait0();
-    }
-    __syncwarp();
+    if (u + nw < total) issue(u + nw, buf ^ 1);  // that buffer was released by the previous unit
+    dev::mbar_wait(&zbar[2 * warp + buf], (uint32_t)((it >> 1) & 1));
     const double2* Bb = Bs + buf * P8 * kZR;
     const int bc = u / ncbk, c0 = (u % ncbk) * kZB, ncb = min(kZB, ncol - c0);
     double2* dst = OUT + (size_t)bc * g.nhalf;
@@ -555,35 +558,43 @@ __global__ void __launch_bounds__(kWZI * 32, 1) k_zi3(PWGrid g, int nc, int nbox
     Aim[e] = vi;
   }
   __shared__ int s_ncol[33], s_off[33];  // slab table (mz + M), read per input element
+  __shared__ uint64_t zbar[2 * kWZI];    // per warp: one mbarrier per block buffer
   if (tid < NZ) {
     s_ncol[tid] = g.slab_ncol[tid];
     s_off[tid] = g.slab_off[tid];
   }
+  for (int e = lane; e < 2 * 33 * kZR; e += 32) Fs[e] = make_double2(0.0, 0.0);
+  if (lane == 0) {
+    dev::mbar_init(&zbar[2 * warp], 1);
+    dev::mbar_init(&zbar[2 * warp + 1], 1);
+    dev::mbar_fence_init();
+  }
+  dev::fence_proxy_async_smem();  // the zero fill precedes the bulk copies into the same bytes
   __syncthreads();
   const int ncbk = (ncol + kZB - 1) / kZB, total = nbox * nc * ncbk;
   const int nw = gridDim.x * kWZI;
+  // a unit's block: F row (mz + M) holds a contiguous prefix of the columns,
+  // so each row is one 1D TMA bulk copy of its in-band part (a lane per row);
+  // reads of out-of-band entries are predicated to zero instead of zero-filled
   auto issue = [&](int u, int buf) {
     const int bc = u / ncbk, c0 = (u % ncbk) * kZB;
     const double2* src = IN + (size_t)bc * g.nhalf;
-    double2* dst = Fs + buf * 33 * kZR;
-    for (int e = lane; e < NZ * kZB; e += 32) {  // F rows (mz + M): a contiguous prefix of the columns
-      const int s = e / kZB, cc = e % kZB;
-      const bool v = c0 + cc < s_ncol[s];
-      dev::cp_async16z(dst + s * kZR + cc, v ? src + s_off[s] + c0 + cc : src, v);
+    for (int s = lane; s < NZ; s += 32) {
+      const int nv = min(kZB, s_ncol[s] - c0);
+      if (nv > 0) {
+        dev::mbar_expect_tx_only(&zbar[2 * warp + buf], (uint32_t)nv * 16u);
+        dev::bulk_g2s(Fs + buf * 33 * kZR + s * kZR, src + s_off[s] + c0, (uint32_t)nv * 16u, &zbar[2 * warp + buf]);
+      }
     }
-    cp_commit();
+    __syncwarp();
+    if (lane == 0) dev::mbar_arrive(&zbar[2 * warp + buf]);
   };
   int u = blockIdx.x * kWZI + warp;
   if (u < total) issue(u, 0);
   for (int it = 0; u < total; ++it, u += nw) {
     const int buf = it & 1;
-    if (u + nw < total) {
-      issue(u + nw, buf ^ 1);
-      cp_wait1();
-    } else {
-      cp_wait0();
-    }
-    __syncwarp();
+    if (u + nw < total) issue(u + nw, buf ^ 1);  // that buffer was released by the previous unit
+    dev::mbar_wait(&zbar[2 * warp + buf], (uint32_t)((it >> 1) & 1));
     const double2* Fb = Fs + buf * 33 * kZR;
     const int bc = u / ncbk, c0 = (u % ncbk) * kZB, ncb = min(kZB, ncol - c0);
     double2* dst = OUT + (size_t)bc * pz * ncol;
@@ -602,8 +613,9 @@ __global__ void __launch_bounds__(kWZI * 32, 1) k_zi3(PWGrid g, int nc, int nbox
       for (int j = 0; j < 2; ++j) {
         double2 fp = make_double2(0.0, 0.0), fm = fp;
         if (r < M) {
-          fp = Fb[(M + 1 + r) * kZR + j * 8 + gq];
-          fm = Fb[(M - 1 - r) * kZR + j * 8 + gq];
+          const int col = c0 + j * 8 + gq;
+          if (col < s_ncol[M + 1 + r]) fp = Fb[(M + 1 + r) * kZR + j * 8 + gq];
+          if (col < s_ncol[M - 1 - r]) fm = Fb[(M - 1 - r) * kZR + j * 8 + gq];
         }
         br[j] = vpart ? fp.y - fm.y : fp.x + fm.x;  // Vi | Ur
         bi[j] = vpart ? fp.x - fm.x : fp.y + fm.y;  // Vr | Ui
