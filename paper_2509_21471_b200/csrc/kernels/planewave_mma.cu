@@ -900,19 +900,19 @@ __global__ void __launch_bounds__(kWI * 32, 1) k_inv_xy2(PWGrid g, const int* __
       bi[myp * SB + m0p] = cp.y + cm.y;         // Ui
       bi[(M8 + myp) * SB + m0p] = cp.x - cm.x;  // Vr
     }
-    // m0 = 0 column on the CUDA cores
+    // m0 = 0 column on the CUDA cores (real part only: the X stage weighs the
+    // imaginary part by Im E(0, ix) = 0)
     for (int e = tid; e < 4 * p; e += blockDim.x) {
       const int s = e / p, iy = e % p;
       const double2* Ds = D + s * ND;
-      double re = Ds[M * M1].x, im = Ds[M * M1].y;
+      double re = Ds[M * M1].x;
       for (int myp = 0; myp < M; ++myp) {
         const double2 cp = Ds[(myp + 1 + M) * M1], cm = Ds[(M - myp - 1) * M1];
         const double er = Are[iy * SA2 + myp], ei = Are[iy * SA2 + M8 + myp];
         re = fma(er, cp.x + cm.x, fma(ei, cp.y - cm.y, re));
-        im = fma(er, cp.y + cm.y, fma(-ei, cp.x - cm.x, im));
       }
       dd[(s * P8 + iy) * SX] = re;
-      dd[(s * P8 + iy) * SX + 1] = im;
+      dd[(s * P8 + iy) * SX + 1] = 0.0;
     }
     __syncthreads();
     // Y stage: d[(s,iy), m0] for m0 = 1..M, plus the my = 0 term
@@ -1274,17 +1274,17 @@ __global__ void __launch_bounds__(kWI3 * 32, 1) k_inv_xy3(PWGrid g, const int* _
         o[mt][nt][1] = (iy < p && ix + 1 < p) ? out[iy * p + ix + 1] : 0.0;
       }
     const double2* D = den + buf * N * SD;
-    // m0 = 0 column (CUDA cores): lane = iy
+    // m0 = 0 column (CUDA cores): lane = iy.  Only its real part is formed:
+    // the X stage weighs the imaginary part by Im E(0, ix) = 0
     if (lane < p) {
-      double re = D[M * SD].x, im = D[M * SD].y;
+      double re = D[M * SD].x;
       for (int r = 0; r < M; ++r) {
         const double2 cp = D[(r + 1 + M) * SD], cm = D[(M - 1 - r) * SD];
         const double er = Are[lane * SA2 + r], ei = Are[lane * SA2 + M8 + r];
         re = fma(er, cp.x + cm.x, fma(ei, cp.y - cm.y, re));
-        im = fma(er, cp.y + cm.y, fma(-ei, cp.x - cm.x, im));
       }
       dd[lane * SX] = re;
-      dd[lane * SX + 1] = im;
+      dd[lane * SX + 1] = 0.0;
     }
     // Y stage: all PT x MT tiles, re and im
     double yr[PT][MTC][2], yi[PT][MTC][2];
