@@ -288,8 +288,10 @@ __global__ void __launch_bounds__(kAWarps * 32, 2) k_anterp_mma(int kernel_rt, C
 #ifndef SDMK_A2_KC
 #define SDMK_A2_KC 32
 #endif
-constexpr int kKC2 = SDMK_A2_KC;  // points per shared chunk (k_anterp2)
-template <int MT, int NTW, int PC, int KC, int DC, int W>
+// points per shared chunk (k_anterp2's last template parameter): 64 for the
+// Stokeslet (fewer chunk barriers), 32 for the stresslet (A/B measured)
+constexpr int kA2Chunk = SDMK_A2_KC;
+template <int MT, int NTW, int PC, int KC, int DC, int W, int kKC2>
 __global__ void __launch_bounds__(W * 32, 1) k_anterp2(ChebDev cb, const DBox* __restrict__ boxes,
                                                             const int* __restrict__ leaves,
                                                             const double* __restrict__ basis,
@@ -655,24 +657,24 @@ void launch_anterp_mma(int kernel, const ChebDev& cb, const DBox* boxes, const i
                                                                            str, n, out, nch, mt_per);   \
   } while (0)
 #define AM(NTT, MW) AMS(NTT, MW, 0, -1, 0)
-#define A2(MT_, NTW_, PC_, KC_, W_)                                                                      \
+#define A2(MT_, NTW_, PC_, KC_, W_, CH_)                                                                      \
   do {                                                                                                  \
     constexpr int RS_ = MT_ * 8 + 4;                                                                    \
     constexpr int XS_ = (PC_ + 3) / 4 * 4 % 8 == 4 ? (PC_ + 3) / 4 * 4 : (PC_ + 3) / 4 * 4 + 4;         \
-    const size_t sm2 = sizeof(double) * (size_t)kKC2 * (RS_ + 2 * (3 * XS_ + 8));                      \
+    const size_t sm2 = sizeof(double) * (size_t)CH_ * (RS_ + 2 * (3 * XS_ + 8));                      \
     const int ntt = (PC_ * PC_ + 7) / 8, per = W_ * NTW_;                                             \
-    smem_attr((const void*)k_anterp2<MT_, NTW_, PC_, KC_, 3, W_>, sm2);                                     \
+    smem_attr((const void*)k_anterp2<MT_, NTW_, PC_, KC_, 3, W_, CH_>, sm2);                                     \
     const int nrb = ((KC_ == 1 ? 6 : 3) * PC_ + MT_ * 8 - 1) / (MT_ * 8);                               \
-    k_anterp2<MT_, NTW_, PC_, KC_, 3, W_><<<dim3(nleaf, (ntt + per - 1) / per, nrb), W_ * 32, sm2, st>>>( \
+    k_anterp2<MT_, NTW_, PC_, KC_, 3, W_, CH_><<<dim3(nleaf, (ntt + per - 1) / per, nrb), W_ * 32, sm2, st>>>( \
         cb, boxes, leaves, basis, str, n, out);                                                         \
   } while (0)
 #ifndef SDMK_A2K_NTW
 #define SDMK_A2K_NTW 3
 #define SDMK_A2K_W 12
 #endif
-  if (cb.dim == 3 && p == 23 && kernel == 0) A2(9, SDMK_A2K_NTW, 23, 0, SDMK_A2K_W);
-  else if (cb.dim == 3 && p == 22 && kernel == 1) A2(SDMK_A2S_MT, SDMK_A2S_NTW, 22, 1, 12);
-  else if (cb.dim == 3 && p == 30 && kernel == 0) A2(12, 2, 30, 0, 12);
+  if (cb.dim == 3 && p == 23 && kernel == 0) A2(9, SDMK_A2K_NTW, 23, 0, SDMK_A2K_W, 64);
+  else if (cb.dim == 3 && p == 22 && kernel == 1) A2(SDMK_A2S_MT, SDMK_A2S_NTW, 22, 1, 12, kA2Chunk);
+  else if (cb.dim == 3 && p == 30 && kernel == 0) A2(12, 2, 30, 0, 12, kA2Chunk);
   else if (NTv <= 1) AM(1, 8);
   else if (NTv == 2) AM(2, 8);
   else if (NTv == 3) AM(3, 6);

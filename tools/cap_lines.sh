@@ -1,8 +1,12 @@
+#!/bin/bash
+# ncu --set full captures with source-line stall attribution of chosen kernels
+# at the metric (N = 1e7 Stokeslet).  usage: tools/cap_lines.sh <outdir> <kernel:skip> ...
 set -u
-out=gpurun_out/cap1; mkdir -p $out
+out=$1; shift
+mkdir -p $out
 one="python tools/prof_step.py --n 10000000 --reps 1"
 $one > $out/plain.log 2>&1 || { echo plain failed; exit 1; }
-for spec in k_anterp2:0 k_interp_mma:0 k_zf3:5 k_zi3:8 k_inv_xy3:8 k_fwd_xy3:5; do
+for spec in "$@"; do
   k=${spec%%:*}; skip=${spec##*:}
   ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip $skip -c 1 -o $out/$k $one > /dev/null 2>&1
   python tools/ncu_lines.py $out/$k.ncu-rep 45 > $out/$k.lines.txt 2>&1
