@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_anterp2(ChebDev cb, const DBox* _
 
 // ------------------------------------------------------------------- K11 --
 #ifndef SDMK_I_ROWS
-#define SDMK_I_ROWS 128  // W rows staged per chunk (rounded down to whole (j, iz) row groups)
+#define SDMK_I_ROWS 256  // W rows staged per chunk (rounded down to whole (j, iz) row groups)
 #endif
 // doubles per flat W buffer (even: 16-byte aligned buffers): the copy (RG
 // row groups of p x p plus one leading alignment double, rounded to 16 bytes)
