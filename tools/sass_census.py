@@ -16,11 +16,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OBJ = os.path.join(ROOT, "paper_2509_21471_b200", "csrc", "build", "kernels")
 KERNELS = [  # (object, kernel-name regex)
     ("residual.o", r"k_residual<0, 3, 6, 0>"),
-    ("anterp_mma.o", r"k_anterp2<9, 3, 23, 0, 3, 12>"),
+    ("anterp_mma.o", r"k_anterp2<9, 3, 23, 0, 3, 12, 64>"),
     ("anterp_mma.o", r"k_interp_mma<3, 23, 3"),
     ("anterp_mma.o", r"k_basis"),
     ("planewave.o", r"k_acc_group<0, 3, 1>"),
-    ("planewave_mma.o", r"k_fwd_xy3<23, 33>"),
+    ("planewave_mma.o", r"k_fwd_xy3<23, 33, 8>"),
     ("planewave_mma.o", r"k_zf3"),
     ("planewave_mma.o", r"k_zi3"),
     ("planewave_mma.o", r"k_inv_xy3<23, 33>"),
