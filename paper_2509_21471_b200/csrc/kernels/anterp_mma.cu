@@ -445,6 +445,15 @@ __host__ __device__ constexpr int interp_flat(int RG, int PY, int p) {
                                                                      : (RG - 1) * p * p + (PY - 1) * p + PY + 1) +
           1) & ~1;
 }
+// (j, iz) row groups per chunk: SDMK_I_ROWS / PY rows, cut down until the two
+// flat buffers and the bz rows of one pass fit the 227 KB of shared memory at
+// the widest p of the instantiation (PC, or 8 TY; 64 bytes kept for the barriers)
+__host__ __device__ constexpr int interp_rg(int TY, int PC) {
+  const int PY = 8 * TY, tb = TY <= 3 ? 8 * 5 * 8 : 12 * 4 * 8, pw = PC > 0 ? PC : PY;
+  int rg = PY >= SDMK_I_ROWS ? 1 : SDMK_I_ROWS / PY;
+  while (rg > 1 && 16 * (long)interp_flat(rg, PY, pw) + 8 * (long)tb * (pw | 1) + 64 > 232448) --rg;
+  return rg;
+}
 // warps per CTA (IW) and m-tiles per warp (ITW) are template parameters:
 // 8 x 5 for TY <= 3 (p <= 24; measured 4 % faster than 12 x 4 at p = 23),
 // 12 x 4 above (the 8 x 5 accumulators would spill); one pass per leaf covers
@@ -475,7 +484,7 @@ __global__ void __launch_bounds__(kIW * 32, 1) k_interp_mma(ChebDev cb, const DB
                                                            double* __restrict__ ufar) {
   constexpr int PY = 8 * TY, KS = 2 * TY;
   constexpr int kTB = kIW * kITW * 8;  // targets per pass
-  constexpr int RG = PY >= SDMK_I_ROWS ? 1 : SDMK_I_ROWS / PY;  // (j, iz) rows per chunk
+  constexpr int RG = interp_rg(TY, PC);  // (j, iz) rows per chunk
   extern __shared__ double sm[];
   __shared__ uint64_t bar[2];
   const int p = PC > 0 ? PC : cb.p, dim = DC > 0 ? DC : cb.dim, pz = dim == 3 ? p : 1;
@@ -691,14 +700,14 @@ void launch_interp_mma(const ChebDev& cb, const DBox* boxes, const int* leaves, 
   if (nleaf <= 0) return;
   const int p = cb.p;
   const int TYv = (p + 7) / 8;
-  auto smem_for = [&](int TY) {
-    const int PY = 8 * TY, RG = PY >= SDMK_I_ROWS ? 1 : SDMK_I_ROWS / PY;
+  auto smem_for = [&](int TY, int PC) {
+    const int PY = 8 * TY, RG = interp_rg(TY, PC);
     const int tb = TY <= 3 ? 8 * 5 * 8 : 12 * 4 * 8;  // the kernel's IW * ITW * 8
     return sizeof(double) * (2 * (size_t)interp_flat(RG, PY, p) + (size_t)tb * (p | 1));
   };
 #define IMS(TY_, PC_, DC_)                                                                                \
   do {                                                                                                    \
-    size_t sm = smem_for(TY_);                                                                            \
+    size_t sm = smem_for(TY_, PC_);                                                                            \
     smem_attr((const void*)k_interp_mma<TY_, PC_, DC_>, sm);                                              \
     k_interp_mma<TY_, PC_, DC_><<<nleaf, (TY_ <= 3 ? 8 : 12) * 32, sm, st>>>(cb, boxes, leaves, tbasis, nt, tperm, incoming, ufar); \
   } while (0)
