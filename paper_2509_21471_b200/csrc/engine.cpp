@@ -411,7 +411,7 @@ void Context::check_inputs(const Plan& P, int dim, int64_t ns, int64_t nt, int m
     throw InvalidArgument("evaluate: the periodic 2D stresslet sum is not absolutely convergent");
   if (P.n_s < 1) throw InvalidArgument("build_tree: n_s must be >= 1");
   if (P.p < 1) throw InvalidArgument("build_tree: proxy order must be >= 1");
-  if (P.p > (dim == 3 ? 48 : 64)) throw InvalidArgument("evaluate: proxy order above the GPU path limit (48 in 3D, 64 in 2D)");
+  if (P.p > 64) throw InvalidArgument("evaluate: proxy order above the GPU path limit (64)");
   if (P.N1 < 1 || P.N1 > 127 || P.N_per < 1 || P.N_per > 127)
     throw InvalidArgument("evaluate: Fourier grid size outside [1, 127]");
   if (P.window == kProlate && !(P.c > 0.0)) throw InvalidArgument("build_prolate: c must be positive");
@@ -1842,7 +1842,7 @@ void Context::tree_build(int dim, bool periodic, int n_s, int p, int64_t ns, con
   if (ns < 1 || nt < 0) throw InvalidArgument("build_tree: bad point array length");
   if (ns > (int64_t(1) << 31) - 1 || nt > (int64_t(1) << 31) - 1)
     throw InvalidArgument("build_tree: more than 2^31-1 points");
-  if (p > (dim == 3 ? 48 : 64)) throw InvalidArgument("build_tree: proxy order above the GPU path limit (48 in 3D, 64 in 2D)");
+  if (p > 64) throw InvalidArgument("build_tree: proxy order above the GPU path limit (64)");
   Plan P;  // the tree depends on dim, periodic, n_s and p only; passes bind their own plan
   P.kernel = kStokeslet;
   P.dim = dim;

@@ -123,8 +123,10 @@ __global__ void __launch_bounds__(kAntBlock) k_anterp(int kernel, ChebDev cb, co
   }
 }
 
-template <int PM>
-__global__ void __launch_bounds__(kIntBlock) k_interp(ChebDev cb, const DBox* __restrict__ boxes,
+// BLK targets per CTA (one per thread): BLK, or 64 for p > 48 (the three
+// basis columns per target would not fit shared memory)
+template <int PM, int BLK>
+__global__ void __launch_bounds__(BLK) k_interp(ChebDev cb, const DBox* __restrict__ boxes,
                                                       const int* __restrict__ leaves,
                                                       const double* __restrict__ tpts, int nt,
                                                       const int* __restrict__ tperm,
@@ -134,10 +136,10 @@ __global__ void __launch_bounds__(kIntBlock) k_interp(ChebDev cb, const DBox* __
   const int p = cb.p, pz = cb.pz, dim = cb.dim;
   double* nodes = sm;
   double* wts = nodes + p;
-  double* bxs = wts + p;               // p * kIntBlock (column per thread)
-  double* bys = bxs + p * kIntBlock;   // p * kIntBlock
-  double* bzs = bys + p * kIntBlock;   // p * kIntBlock
-  double* slab = bzs + p * kIntBlock;  // dim * p * p
+  double* bxs = wts + p;               // p * BLK (column per thread)
+  double* bys = bxs + p * BLK;   // p * BLK
+  double* bzs = bys + p * BLK;   // p * BLK
+  double* slab = bzs + p * BLK;  // dim * p * p
   const int tid = threadIdx.x;
   for (int i = tid; i < p; i += blockDim.x) {
     nodes[i] = cb.nodes[i];
@@ -149,20 +151,20 @@ __global__ void __launch_bounds__(kIntBlock) k_interp(ChebDev cb, const DBox* __
   const double* win = incoming + (size_t)b * dim * nodes_per;
   const double hinv = 1.0 / box.half;
   __syncthreads();
-  for (int t0 = box.tb; t0 < box.te; t0 += kIntBlock) {
+  for (int t0 = box.tb; t0 < box.te; t0 += BLK) {
     const int t = t0 + tid;
     const bool act = t < box.te;
     if (act) {
       for (int ax = 0; ax < dim; ++ax) {
         double x = __dmul_rn(__dsub_rn(tpts[(size_t)ax * nt + t], box.c[ax]), hinv);
         double* dst = (ax == 0 ? bxs : (ax == 1 ? bys : bzs)) + tid;
-        dev::cheb_basis(p, nodes, wts, x, dst, kIntBlock);
+        dev::cheb_basis(p, nodes, wts, x, dst, BLK);
       }
       if (dim == 2) bzs[tid] = 1.0;
     }
     double bx[PM];
 #pragma unroll
-    for (int i = 0; i < PM; ++i) bx[i] = (i < p && act) ? bxs[i * kIntBlock + tid] : 0.0;
+    for (int i = 0; i < PM; ++i) bx[i] = (i < p && act) ? bxs[i * BLK + tid] : 0.0;
     double u0 = 0.0, u1 = 0.0, u2 = 0.0;
     for (int iz = 0; iz < pz; ++iz) {
       __syncthreads();
@@ -171,9 +173,9 @@ __global__ void __launch_bounds__(kIntBlock) k_interp(ChebDev cb, const DBox* __
         slab[e] = win[(size_t)j * nodes_per + (size_t)iz * pp + r];
       }
       __syncthreads();
-      const double wz = act ? bzs[iz * kIntBlock + tid] : 0.0;
+      const double wz = act ? bzs[iz * BLK + tid] : 0.0;
       for (int iy = 0; iy < p; ++iy) {
-        const double wzy = wz * (act ? bys[iy * kIntBlock + tid] : 0.0);
+        const double wzy = wz * (act ? bys[iy * BLK + tid] : 0.0);
         const double* r0 = slab + iy * p;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0;
 #pragma unroll
@@ -215,13 +217,14 @@ void anterp_t(int kernel, const ChebDev& cb, const DBox* boxes, const int* leave
 template <int PM>
 void interp_t(const ChebDev& cb, const DBox* boxes, const int* leaves, int nleaf, const double* tpts, int nt,
               const int* tperm, const double* incoming, double* ufar, cudaStream_t st) {
-  size_t smem = sizeof(double) * (2 * cb.p + 3 * cb.p * kIntBlock + cb.dim * cb.p * cb.p);
+  constexpr int BLK = PM > 48 ? 64 : kIntBlock;
+  size_t smem = sizeof(double) * (2 * cb.p + 3 * cb.p * BLK + cb.dim * cb.p * cb.p);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_interp<PM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_interp<PM, BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_interp<PM><<<nleaf, kIntBlock, smem, st>>>(cb, boxes, leaves, tpts, nt, tperm, incoming, ufar);
+  k_interp<PM, BLK><<<nleaf, BLK, smem, st>>>(cb, boxes, leaves, tpts, nt, tperm, incoming, ufar);
 }
 
 }  // namespace

@@ -482,14 +482,17 @@ __global__ void __launch_bounds__(kPWBlock) k_inv_z(PWGrid g, int d, const doubl
   }
 }
 
+// stage = 0: the row of C is read in place (global memory) instead of from a
+// shared copy -- the same sums in the same order; used when E, the row and
+// the y-stage result together pass the 227 KB of shared memory (p = 60, N1 = 107)
 __global__ void __launch_bounds__(kPWBlock) k_inv_xy(PWGrid g, const int* __restrict__ tboxes, int d,
                                                      const double2* __restrict__ C, double pf,
-                                                     double* __restrict__ incoming) {
+                                                     double* __restrict__ incoming, int stage) {
   extern __shared__ double2 smc[];
   const int p = g.p, N = g.N, M = g.M, M1 = g.M + 1, pp = p * p, ncol = g.ncol;
   double2* EsT = smc;         // [p][N]
-  double2* cs = EsT + p * N;  // [ncol]
-  double2* ds = cs + ncol;    // [p][M+1]
+  double2* csm = EsT + p * N;                // [ncol] (stage)
+  double2* ds = csm + (stage ? ncol : 0);    // [p][M+1]
   const int tid = threadIdx.x;
   for (int e = tid; e < N * p; e += blockDim.x) {
     int m = e / p, i = e % p;
@@ -501,8 +504,12 @@ __global__ void __launch_bounds__(kPWBlock) k_inv_xy(PWGrid g, const int* __rest
   double* out = incoming + ((size_t)b * d + j) * (size_t)(g.pz * pp);
   for (int iz = 0; iz < g.pz; ++iz) {
     __syncthreads();
-    for (int c = tid; c < ncol; c += blockDim.x) cs[c] = Ci[(size_t)iz * ncol + c];
-    __syncthreads();
+    const double2* cs = Ci + (size_t)iz * ncol;
+    if (stage) {
+      for (int c = tid; c < ncol; c += blockDim.x) csm[c] = cs[c];
+      cs = csm;
+      __syncthreads();
+    }
     for (int e = tid; e < p * M1; e += blockDim.x) {  // y: d[iy][m0] = sum_my conj(E[my][iy]) c[(my,m0)]
       int iy = e / M1, m0 = e % M1;
       double2 acc = make_double2(0.0, 0.0);
@@ -543,6 +550,7 @@ void launch_forward(const PWGrid& g, const int* boxes, int nbox, int nch, const 
   set_smem((const void*)k_fwd_xy, smem);
   k_fwd_xy<<<grid, kPWBlock, smem, st>>>(g, boxes, nch, outgoing, B);
   size_t zs = sizeof(double2) * g.Nz * g.pz;
+  set_smem((const void*)k_fwd_z<64>, zs);  // only pz > 32 can pass 48 KB
   if (g.pz <= 1) k_fwd_z<1><<<grid, kPWBlock, zs, st>>>(g, nch, B, G);
   else if (g.pz <= 16) k_fwd_z<16><<<grid, kPWBlock, zs, st>>>(g, nch, B, G);
   else if (g.pz <= 24) k_fwd_z<24><<<grid, kPWBlock, zs, st>>>(g, nch, B, G);
@@ -606,14 +614,17 @@ void launch_inverse(const PWGrid& g, const int* tboxes, int ntb, int d, const do
   if (ntb <= 0) return;
   dim3 grid(ntb, d);
   size_t zs = sizeof(double2) * g.Nz * g.pz;
+  set_smem((const void*)k_inv_z<64>, zs);  // only pz > 32 can pass 48 KB
   if (g.pz <= 1) k_inv_z<1><<<grid, kPWBlock, zs, st>>>(g, d, F, C);
   else if (g.pz <= 16) k_inv_z<16><<<grid, kPWBlock, zs, st>>>(g, d, F, C);
   else if (g.pz <= 24) k_inv_z<24><<<grid, kPWBlock, zs, st>>>(g, d, F, C);
   else if (g.pz <= 32) k_inv_z<32><<<grid, kPWBlock, zs, st>>>(g, d, F, C);
   else k_inv_z<64><<<grid, kPWBlock, zs, st>>>(g, d, F, C);
   size_t smem = sizeof(double2) * (g.p * g.N + g.ncol + g.p * (g.M + 1));
+  const int stage = smem <= 227 * 1024;
+  if (!stage) smem -= sizeof(double2) * g.ncol;
   set_smem((const void*)k_inv_xy, smem);
-  k_inv_xy<<<grid, kPWBlock, smem, st>>>(g, tboxes, d, C, pf, incoming);
+  k_inv_xy<<<grid, kPWBlock, smem, st>>>(g, tboxes, d, C, pf, incoming, stage);
 }
 
 }  // namespace sdmkb

@@ -143,8 +143,10 @@ void launch_tensor_apply(int p, int pz, int dim, const double* mats, const int* 
     TA(576, 1, 24);
   } else if (pp <= 1024) {
     TA(512, 2, 16);
-  } else {
+  } else if (pp <= 2048) {
     TA(512, 4, 8);
+  } else {  // p = 46..64: 8 columns per thread, shorter z chunks
+    TA(512, 8, 4);
   }
 #undef TA
 }

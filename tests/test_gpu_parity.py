@@ -360,3 +360,49 @@ def test_sort_ties_in_top_key_bits(separate_targets):
     assert np.array_equal(sp, rsp)
     if separate_targets:
         assert np.array_equal(tp, rtp)
+
+
+# Proxy orders above the DMMA kernels' range: every row of the plan table up to
+# p = 64 runs (params.cpp:21-38: the Gaussian-window eps = 1e-12 rows have
+# p = 58 / 60 / 53 and N1 = 99 / 107 / 93; prolate eps = 1e-13 has p = 48).
+LARGE_P = [
+    # kernel, dim, window, eps, n, n_s, expected p
+    (0, 3, 0, 1e-13, 1200, 100, 48),
+    (0, 3, 1, 1e-12, 700, 60, 58),
+    (1, 3, 1, 1e-12, 500, 40, 60),
+    (0, 2, 1, 1e-13, 3000, 60, 63),
+]
+
+
+@pytest.mark.parametrize("case", LARGE_P)
+def test_large_proxy_orders_against_live_reference(gpu_ctx, case):
+    ref = _ref()
+    kernel, dim, window, eps, n, n_s, p = case
+    rng = np.random.default_rng(5 + n + kernel)
+    x = rng.uniform(-0.5, 0.5, (n, dim))
+    s = rng.standard_normal((n, g.strength_components(kernel, dim)))
+    plan = ref.select_parameters(kernel, eps, window, dim)
+    assert plan["p"] == p
+    plan["n_s"] = n_s
+    P = ref.RefProblem(plan, dim, x, s, None, False)
+    sys_ = g.ParticleSystem(dim, x, np.zeros(0), s)
+    gpu_ctx.setup(g.DmkPlan(**plan), sys_, 0)
+    assert gpu_ctx.tree_dump() == P.tree_dump()
+    ok, err = parity_ok(gpu_ctx.upward_pass(), P.upward(), 1e-12)
+    assert ok, ("upward", err)
+    ok, err = parity_ok(gpu_ctx.incoming(1), P.incoming(1), 1e-11)
+    assert ok, ("incoming", err)
+    ur, _ = P.evaluate()
+    rep = {}
+    u = gpu_ctx.evaluate_with_plan(g.DmkPlan(**plan), sys_, 0, rep)
+    assert rep["max_level"] >= 2
+    ok, err = parity_ok(u, ur, RTOL)
+    assert ok, ("evaluate", err)
+
+
+def test_proxy_order_above_64_is_rejected(gpu_ctx):
+    plan = g.select_parameters(1, 1e-13, g.GAUSSIAN, 3)  # extrapolated row: p = 66
+    assert plan.p > 64
+    x = np.random.default_rng(0).uniform(-0.5, 0.5, (100, 3))
+    with pytest.raises(ValueError, match="proxy order above the GPU path limit"):
+        gpu_ctx.evaluate_with_plan(plan, g.ParticleSystem(3, x, np.zeros(0), np.ones((100, 6))), 0)
