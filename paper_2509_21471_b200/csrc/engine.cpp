@@ -668,6 +668,41 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
     *qs_out = hq;
     *qt_out = pr.alias ? nullptr : hq + (size_t)ns * d;
   };
+  // refine_to_capacity in one cooperative launch; the boxes come back in the
+  // reference's id order (the host keeps the 2:1 repair and the lists)
+  static_assert(sizeof(RefBox) == sizeof(Box) && offsetof(RefBox, leaf) == offsetof(Box, leaf) &&
+                    offsetof(RefBox, anchor) == offsetof(Box, anchor) && offsetof(RefBox, sb) == offsetof(Box, sb) &&
+                    offsetof(RefBox, te) == offsetof(Box, te),
+                "RefBox mirrors host/tree.hpp Box");
+  static const bool host_refine = std::getenv("SDMK_HOST_REFINE") != nullptr;  // A/B and fallback tests
+  if (!host_refine)
+    pa.refine = [&](std::vector<Box>& boxes, int& max_level, bool& capped) {
+      const int nchild = 1 << d;
+      const int64_t want = 8 * (int64_t)nchild * ((int64_t)ns / std::max(1, P.n_s) + 1) + 4096;
+      static const char* cap_env = std::getenv("SDMK_REFINE_CAP");  // test hook: force the fallback
+      const int cap = cap_env ? std::max(16, std::atoi(cap_env)) : (int)std::min<int64_t>(want, int64_t(1) << 26);
+      void* nodes = arena_.get("refine_nodes", (size_t)cap * refine_node_bytes());
+      RefBox* out = (RefBox*)arena_.get("refine_out", (size_t)cap * sizeof(RefBox));
+      int* hdr = arena_.as<int>("refine_hdr", 64);
+      launch_refine(sq, ns, pr.alias ? nullptr : tq, pr.alias ? 0 : nt, pr.alias ? 1 : 0, d, P.n_s, cap, nodes, hdr,
+                    out, st_);
+      ++launches_;
+      cuda_check(cudaPeekAtLastError(), "refine launch");
+      int* hh = (int*)pinned_.get("refine_hdr", 64 * sizeof(int));
+      cuda_check(cudaMemcpyAsync(hh, hdr, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H refine header");
+      sync();
+      if (hh[3]) return false;  // more boxes than slots: the host refines
+      const int nb = hh[0];
+      Box* hb = (Box*)pinned_.get("refine_out", (size_t)nb * sizeof(Box));
+      cuda_check(cudaMemcpyAsync(hb, out, (size_t)nb * sizeof(Box), cudaMemcpyDeviceToHost, st_), "D2H boxes");
+      sync();
+      boxes.reserve((size_t)nb + nb / 4 + 64);  // room for the 2:1 repair's boxes
+      boxes.resize(nb);
+      std::memcpy((void*)boxes.data(), hb, (size_t)nb * sizeof(Box));
+      max_level = hh[1] - 1;
+      capped = hh[2] != 0;
+      return true;
+    };
   pr.tree = build_topology(d, pr.periodic, P.n_s, P.p, ns, pr.alias ? 0 : nt, pa, /*with_neighbours=*/false);
   if (str_pending_) {
     finish_strengths();

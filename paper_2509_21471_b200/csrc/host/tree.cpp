@@ -121,6 +121,15 @@ struct Builder {
   // depends only on counts; build it breadth first with parallel searches,
   // then allocate ids in the reference's DFS pre-order.
   void refine() {
+    if (pa && pa->refine) {
+      int maxlev = 0;
+      bool capped = false;
+      if (pa->refine(t.boxes, maxlev, capped)) {
+        t.max_level = maxlev;
+        t.depth_capped = capped;
+        return;
+      }
+    }
     struct Node {
       Box box;
       int kids = -1;  // index of first child in `nodes` (BFS order)

@@ -83,6 +83,10 @@ HostTree build_topology(int dim, bool periodic, int n_s, int p, int ns, const in
 struct PointAccess {
   std::function<void(int n, const int* lvl, const int* src, const int* tgt, int* sb, int* tb)> split;
   std::function<void(const int32_t** qs, const int32_t** qt)> host_q;
+  // optional: the whole capacity refinement on the device -- fills `boxes` in
+  // the reference's id order and returns true, or returns false (the refine
+  // then runs on the host, level by level through `split`)
+  std::function<bool(std::vector<Box>& boxes, int& max_level, bool& depth_capped)> refine;
 };
 // with_neighbours = false leaves col / crs / fin for finish_topology (the
 // upward pass needs only the boxes; the engine builds the lists while it runs)

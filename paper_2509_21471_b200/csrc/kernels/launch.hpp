@@ -51,6 +51,18 @@ void launch_gather_strengths(const double* str, const int* perm, int n, int sc, 
 // levels lvl[i]: bnd[9i + c], c = 0..2^d (tree.cpp:38-43, 109-123).
 void launch_split_ranges(int nbox, const int* lvl, const int* rng, const int32_t* q, int n, int dim, int* bnd,
                          cudaStream_t st);
+// refine_to_capacity on the device (tree.cpp:109-123): the boxes in the
+// reference's id order, in the layout of host/tree.hpp's Box.  hdr (>= 48 ints):
+// [0] boxes, [1] levels, [2] depth cap reached, [3] more than `cap` boxes
+// (nothing usable was written); nodes: cap * refine_node_bytes() of scratch.
+struct RefBox {
+  int level, parent, first_child, leaf;
+  int32_t anchor[3];
+  int sb, se, tb, te;
+};
+size_t refine_node_bytes();
+void launch_refine(const int32_t* qs, int ns, const int32_t* qt, int nt, int alias, int dim, int n_s, int cap,
+                   void* nodes, int* hdr, RefBox* out, cudaStream_t st);
 // The residual's source sub-cells: 9 boundaries per box (children of leaves
 // with sources, else [sb, se) once), as host/tree.hpp leaf_subranges.
 void launch_leaf_subranges(const dev::DBox* boxes, int nb, const int32_t* q, int n, int dim, int* out,

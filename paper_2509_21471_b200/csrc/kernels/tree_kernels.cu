@@ -1,4 +1,5 @@
 // Point validation, periodic wrap, Morton keys and the radix sort (K1).
+#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
@@ -197,6 +198,147 @@ __global__ void k_leaf_subranges(const dev::DBox* __restrict__ boxes, int nb, co
   }
 }
 }  // namespace
+
+// ---- refine_to_capacity on the device (tree.cpp:109-123) --------------------
+// One cooperative launch builds the whole capacity refinement: the boxes of a
+// level decide to split (more than n_s sources, depth below the cap), claim 2^d
+// child slots with one atomic, and the children find their ranges by binary
+// search on the Morton-sorted quantized coordinates; grid-wide barriers
+// separate the levels.  The working order (breadth first, slot claims in any
+// order) does not matter: the reference allocates ids when its DFS stack pops
+// a box that subdivides, so a subdividing box whose pre-order rank among the
+// subdividing boxes is r has children 1 + 2^d r ... -- found from the subtree
+// counts (bottom up) and the ranks (top down), and the boxes are written at
+// their final ids in the host's Box layout.
+namespace {
+namespace cg = cooperative_groups;
+
+struct RNode {
+  int level, parent, kids, cnt, rank, fid;
+  int32_t anchor[3];
+  int sb, se, tb, te;
+};
+
+__global__ void __launch_bounds__(256) k_refine(const int32_t* qs, int ns, const int32_t* qt, int nt, int alias,
+                                                 int dim, int n_s, int cap, RNode* nodes, int* hdr, RefBox* out) {
+  // hdr: [0] node count, [1] levels, [2] depth capped, [3] overflow, [8 + l] first node of level l
+  cg::grid_group grid = cg::this_grid();
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gsz = gridDim.x * blockDim.x;
+  const int nchild = 1 << dim;
+  volatile int* vh = hdr;
+  if (gtid == 0) {
+    RNode r;
+    r.level = 0; r.parent = -1; r.kids = -1; r.cnt = 0; r.rank = 0; r.fid = 0;
+    r.anchor[0] = r.anchor[1] = r.anchor[2] = 0;
+    r.sb = 0; r.se = ns; r.tb = 0; r.te = alias ? ns : nt;
+    nodes[0] = r;
+    hdr[0] = 1; hdr[1] = 1; hdr[2] = 0; hdr[3] = 0; hdr[8] = 0; hdr[9] = 1;
+  }
+  grid.sync();
+  int lev = 0, lb = 0, le = 1;
+  for (;;) {
+    for (int i = lb + gtid; i < le; i += gsz) {  // split decisions of level lev
+      RNode& nd = nodes[i];
+      if (nd.se - nd.sb <= n_s) continue;
+      if (nd.level >= kQBits) {
+        hdr[2] = 1;
+        continue;
+      }
+      const int k = atomicAdd(hdr, nchild);
+      if (k + nchild > cap) {
+        hdr[3] = 1;
+        continue;
+      }
+      nd.kids = k;
+      for (int c = 0; c < nchild; ++c) nodes[k + c].parent = i;
+    }
+    grid.sync();
+    if (vh[3]) return;  // out of node slots: the host refines instead
+    const int nle = vh[0];
+    if (nle == le) break;
+    for (int i = le + gtid; i < nle; i += gsz) {  // the new children
+      RNode& c = nodes[i];
+      const RNode& par = nodes[c.parent];
+      const int ci = i - par.kids, pl = par.level;
+      c.level = pl + 1;
+      c.kids = -1;
+      for (int a = 0; a < 3; ++a) c.anchor[a] = a < dim ? par.anchor[a] + (((ci >> a) & 1) << (kQBits - 1 - pl)) : 0;
+      c.sb = ci == 0 ? par.sb : lower_child(qs, ns, par.sb, par.se, pl, dim, ci);
+      c.se = ci == nchild - 1 ? par.se : lower_child(qs, ns, par.sb, par.se, pl, dim, ci + 1);
+      if (alias) {
+        c.tb = c.sb;
+        c.te = c.se;
+      } else {
+        c.tb = ci == 0 ? par.tb : lower_child(qt, nt, par.tb, par.te, pl, dim, ci);
+        c.te = ci == nchild - 1 ? par.te : lower_child(qt, nt, par.tb, par.te, pl, dim, ci + 1);
+      }
+    }
+    lb = le;
+    le = nle;
+    ++lev;
+    if (gtid == 0) {
+      hdr[1] = lev + 1;
+      hdr[8 + lev + 1] = nle;
+    }
+    grid.sync();
+  }
+  const int L = lev + 1;  // levels 0 .. lev
+  for (int l = L - 1; l >= 0; --l) {  // subdividing boxes per subtree
+    for (int i = vh[8 + l] + gtid; i < vh[8 + l + 1]; i += gsz) {
+      RNode& nd = nodes[i];
+      int cnt = 0;
+      if (nd.kids >= 0) {
+        cnt = 1;
+        for (int c = 0; c < nchild; ++c) cnt += nodes[nd.kids + c].cnt;
+      }
+      nd.cnt = cnt;
+    }
+    grid.sync();
+  }
+  for (int l = 0; l < L; ++l) {  // pre-order ranks and final ids
+    for (int i = vh[8 + l] + gtid; i < vh[8 + l + 1]; i += gsz) {
+      const RNode& nd = nodes[i];
+      if (nd.kids < 0) continue;
+      int run = nd.rank + 1;
+      for (int c = 0; c < nchild; ++c) {
+        RNode& ch = nodes[nd.kids + c];
+        ch.fid = 1 + nchild * nd.rank + c;
+        ch.rank = run;
+        run += ch.cnt;
+      }
+    }
+    grid.sync();
+  }
+  for (int i = gtid; i < le; i += gsz) {
+    const RNode& nd = nodes[i];
+    RefBox b;
+    b.level = nd.level;
+    b.parent = nd.parent < 0 ? -1 : nodes[nd.parent].fid;
+    b.first_child = nd.kids < 0 ? -1 : 1 + nchild * nd.rank;
+    b.leaf = nd.kids < 0 ? 1 : 0;
+    for (int a = 0; a < 3; ++a) b.anchor[a] = nd.anchor[a];
+    b.sb = nd.sb; b.se = nd.se; b.tb = nd.tb; b.te = nd.te;
+    out[nd.fid] = b;
+  }
+}
+}  // namespace
+
+size_t refine_node_bytes() { return sizeof(RNode); }
+
+void launch_refine(const int32_t* qs, int ns, const int32_t* qt, int nt, int alias, int dim, int n_s, int cap,
+                   void* nodes, int* hdr, RefBox* out, cudaStream_t st) {
+  static int grid = 0;
+  if (!grid) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_refine, 256, 0);
+    grid = sms * (per < 1 ? 1 : (per > 2 ? 2 : per));
+  }
+  RNode* nd = (RNode*)nodes;
+  void* args[] = {&qs, &ns, &qt, &nt, &alias, &dim, &n_s, &cap, &nd, &hdr, &out};
+  cudaLaunchCooperativeKernel((const void*)k_refine, dim3(grid), dim3(256), args, 0, st);
+}
 
 void launch_split_ranges(int nbox, const int* lvl, const int* rng, const int32_t* q, int n, int dim, int* bnd,
                          cudaStream_t st) {

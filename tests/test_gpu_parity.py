@@ -406,3 +406,42 @@ def test_proxy_order_above_64_is_rejected(gpu_ctx):
     x = np.random.default_rng(0).uniform(-0.5, 0.5, (100, 3))
     with pytest.raises(ValueError, match="proxy order above the GPU path limit"):
         gpu_ctx.evaluate_with_plan(plan, g.ParticleSystem(3, x, np.zeros(0), np.ones((100, 6))), 0)
+
+
+_REFINE_SCRIPT = r"""
+import sys, hashlib
+import numpy as np
+sys.path.insert(0, {root!r})
+import paper_2509_21471_b200 as g
+rng = np.random.default_rng(3)
+out = []
+for dim, n, n_s, per, nt in ((3, 20000, 30, 0, 0), (2, 20000, 7, 0, 5000), (3, 6000, 1, 1, 0), (3, 4000, 2, 0, 0)):
+    c = rng.uniform(-0.4, 0.4, (8, dim))
+    x = np.clip(c[rng.integers(0, 8, n)] + 10.0 ** rng.uniform(-6, -1, (n, 1)) * rng.standard_normal((n, dim)), -0.5, 0.5)
+    if n == 4000:
+        x[:3] = x[3]  # coincident points: the depth cap (tree.cpp:113-116)
+    t = rng.uniform(-0.5, 0.5, (nt, dim)) if nt else np.zeros(0)
+    plan = g.select_parameters(0, 1e-3, g.PROLATE, dim)
+    plan.n_s = n_s
+    ctx = g.Context(0)
+    ctx.setup(plan, g.ParticleSystem(dim, x, t, np.ones((n, dim))), per)
+    out.append(hashlib.sha256(ctx.tree_dump().encode()).hexdigest())
+print(" ".join(out))
+"""
+
+
+def test_device_refine_equals_host_refine():
+    """The cooperative-launch refine (k_refine) gives the tree of the host's
+    level-by-level refine -- clustered points, separate targets, periodic 2:1
+    repair, the depth cap -- and falls back to it when it runs out of slots."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for name, env in (("device", {}), ("host", {"SDMK_HOST_REFINE": "1"}), ("fallback", {"SDMK_REFINE_CAP": "64"})):
+        r = subprocess.run([sys.executable, "-c", _REFINE_SCRIPT.format(root=root)], env={**os.environ, **env},
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[name] = r.stdout.strip().splitlines()[-1]
+    assert res["device"] == res["host"] == res["fallback"]
