@@ -40,21 +40,50 @@ __device__ __forceinline__ int32_t quantize(double x) {
   return (int32_t)q;
 }
 
-// Morton key with axis 0 in the least-significant interleaved bit (tree.cpp:29-35)
+// bit i of x to bit 3 i (x < 2^21) / bit 2 i (x < 2^32)
+__host__ __device__ __forceinline__ uint64_t spread3(uint64_t x) {
+  x &= 0x1fffffull;
+  x = (x | x << 32) & 0x1f00000000ffffull;
+  x = (x | x << 16) & 0x1f0000ff0000ffull;
+  x = (x | x << 8) & 0x100f00f00f00f00full;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+  x = (x | x << 2) & 0x1249249249249249ull;
+  return x;
+}
+__host__ __device__ __forceinline__ uint64_t spread2(uint64_t x) {
+  x &= 0xffffffffull;
+  x = (x | x << 16) & 0x0000ffff0000ffffull;
+  x = (x | x << 8) & 0x00ff00ff00ff00ffull;
+  x = (x | x << 4) & 0x0f0f0f0f0f0f0f0full;
+  x = (x | x << 2) & 0x3333333333333333ull;
+  x = (x | x << 1) & 0x5555555555555555ull;
+  return x;
+}
+
+// Morton key with axis 0 in the least-significant interleaved bit
+// (tree.cpp:29-35): bit b of axis a sits at position b dim + a.  3D: the 90
+// bits are two words, lo = positions 0..63 (bits 0..20 of every axis and bit
+// 21 of axis 0), hi = positions 64..89; 2D: 60 bits in lo.
+__host__ __device__ __forceinline__ void morton_key(const int32_t* q, int dim, uint64_t& lo, uint64_t& hi) {
+  if (dim == 3) {
+    const uint64_t w = spread3((uint64_t)q[0] >> 21) | spread3((uint64_t)q[1] >> 21) << 1 |
+                       spread3((uint64_t)q[2] >> 21) << 2;  // bits 21..29, position 3 (b - 21) + a
+    lo = spread3((uint64_t)q[0]) | spread3((uint64_t)q[1]) << 1 | spread3((uint64_t)q[2]) << 2 | (w & 1) << 63;
+    hi = w >> 1;
+  } else {
+    lo = spread2((uint64_t)q[0]) | spread2((uint64_t)q[1]) << 1;
+    hi = 0;
+  }
+}
+
 __global__ void k_morton(const double* __restrict__ pts, int n, int dim, uint64_t* klo, uint64_t* khi,
                          uint64_t* ktop, int* idx) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int32_t q[3] = {0, 0, 0};
   for (int a = 0; a < dim; ++a) q[a] = quantize(pts[(size_t)i * dim + a]);
-  uint64_t lo = 0, hi = 0;
-  for (int bit = 0; bit < kQBits; ++bit)
-    for (int a = 0; a < dim; ++a) {
-      uint64_t b = (uint64_t)((q[a] >> bit) & 1);
-      int pos = bit * dim + a;
-      if (pos < 64) lo |= b << pos;
-      else hi |= b << (pos - 64);
-    }
+  uint64_t lo, hi;
+  morton_key(q, dim, lo, hi);
   klo[i] = lo;
   khi[i] = hi;
   if (ktop) ktop[i] = (hi << 38) | (lo >> 26);  // 3D: the top 64 of the 90 key bits
