@@ -1112,7 +1112,12 @@ void Context::upload_tree_lists_b() {
   pk.copy_to(h);
   const auto hb6 = std::chrono::steady_clock::now();
   char* dv = (char*)arena_.get("treeB", pk.total + 64);
-  cuda_check(cudaMemcpyAsync(dv, h, pk.total, cudaMemcpyHostToDevice, st_), "tree upload");
+  // inside an evaluation the upward pass is running on st_: the upload and the
+  // sub-cell kernel go to the second stream (ordered after the tree build) and
+  // st_ picks them up by an event, so they do not queue behind the upward pass
+  cudaStream_t su = lists_side_ ? st2_ : st_;
+  if (lists_side_) cuda_check(cudaStreamWaitEvent(st2_, ev_[2], 0), "stream wait");
+  cuda_check(cudaMemcpyAsync(dv, h, pk.total, cudaMemcpyHostToDevice, su), "tree upload");
   pr.send_ids = (int*)(dv + o_send);
   pr.recv_ids = (int*)(dv + o_recv);
   pr.n_send = (int)send_ids.size();
@@ -1124,8 +1129,12 @@ void Context::upload_tree_lists_b() {
   pr.rng_info = (int*)(dv + o_rinfo);
   // source sub-cells for the residual cull, from the device-resident points
   pr.subrange = arena_.as<int>("subrange", (size_t)nb * 9);
-  launch_leaf_subranges(pr.boxes, nb, pr.sq, pr.ns, d, pr.subrange, st_);
+  launch_leaf_subranges(pr.boxes, nb, pr.sq, pr.ns, d, pr.subrange, su);
   ++launches_;
+  if (lists_side_) {
+    cuda_check(cudaEventRecord(x_ev_, st2_), "event record");
+    cuda_check(cudaStreamWaitEvent(st_, x_ev_, 0), "stream wait");
+  }
   pr.res_chunks = (int*)(dv + o_chunks);
   pr.n_chunks = (int)(chunks.size() / 2);
   for (int lev = 0; lev < L; ++lev) {
@@ -1520,6 +1529,7 @@ void Context::evaluate_begin(const Plan& P, int dim, int64_t ns, const double* s
                              const double* str, int mode, bool device_ptrs) {
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   begun_ = false;
+  lists_side_ = false;
   check_inputs(P, dim, ns, nt, mode);
   tab_ = tab_override_ ? tab_override_ : &tables_for(P);
   if (tab_->kernel != P.kernel || tab_->dim != P.dim || tab_->win.kind != P.window)
@@ -1553,7 +1563,9 @@ void Context::evaluate_begin(const Plan& P, int dim, int64_t ns, const double* s
     cudaEventRecord(ev_[2], st_);
     run_upward();
     cudaEventRecord(ev_[3], st_);
+    lists_side_ = true;
     upload_tree_lists_b();  // host work overlaps the upward pass on the GPU
+    lists_side_ = false;
     cudaEventRecord(ev_[8], st_);
     if (prob_.halo) {
       const Problem& pr = prob_;
@@ -1565,6 +1577,7 @@ void Context::evaluate_begin(const Plan& P, int dim, int64_t ns, const double* s
     }
     cudaEventRecord(ev_[10], st_);
   } catch (...) {
+    lists_side_ = false;
     zero_all_ = true;
     throw;
   }

@@ -247,6 +247,7 @@ class Context {
   int device_;
   cudaStream_t st_ = nullptr;
   cudaStream_t st2_ = nullptr;     // side stream: strengths H2D overlapping the tree build
+  bool lists_side_ = false;        // upload_tree_lists_b issues its device work on st2_ (evaluate_begin)
   cudaEvent_t str_ev_ = nullptr;
   cudaEvent_t x_ev_ = nullptr;     // the NCCL halo exchange on st2_ is done
   bool x_pending_ = false;         // an exchange is in flight (evaluate with a communicator)

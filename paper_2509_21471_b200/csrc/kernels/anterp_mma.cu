@@ -41,13 +41,17 @@ __host__ __device__ __forceinline__ int cstride(int x) {  // smallest y >= x wit
 // (q from prefix / suffix products; one division per point and axis).  The
 // exact-hit rule is kept.  A warp owns 32 consecutive points of one axis; the
 // rows are assembled in shared memory and stored coalesced.
+// PC > 0: p known at compile time -- the products stay in registers and each
+// row is written to shared memory once (the generic form passes through it
+// three times); the arithmetic and its order are the same.
 constexpr int kBasisW = 8;
+template <int PC>
 __global__ void __launch_bounds__(kBasisW * 32) k_basis(ChebDev cb, const DBox* __restrict__ boxes,
                                                        const int* __restrict__ leaves, const double* __restrict__ pts,
                                                        int n, int use_targets, double* __restrict__ basis) {
   __shared__ double nodes[64], wts[64];
   extern __shared__ double rowbuf[];  // [kBasisW][32][p | 1]: odd row stride, conflict-free lanes
-  const int p = cb.p, dim = cb.dim, P1 = p | 1;
+  const int p = PC > 0 ? PC : cb.p, dim = cb.dim, P1 = p | 1;
   for (int i = threadIdx.x; i < p; i += blockDim.x) {
     nodes[i] = cb.nodes[i];
     wts[i] = cb.wts[i];
@@ -63,7 +67,38 @@ __global__ void __launch_bounds__(kBasisW * 32) k_basis(ChebDev cb, const DBox* 
     const int ax = task / nchunk, i0 = b0 + (task % nchunk) * 32, i = i0 + lane;
     const int nv = min(32, b1 - i0);
     double* r = rb + lane * P1;
-    if (lane < nv) {
+    if (PC > 0) {
+      if (lane < nv) {
+        constexpr int PR = PC > 0 ? PC : 1;
+        const double x = __dmul_rn(__dsub_rn(pts[(size_t)ax * n + i], box.c[ax]), hinv);
+        double rr[PR];
+        int hit = -1;
+        double pre = 1.0;
+#pragma unroll
+        for (int k = 0; k < PR; ++k) {  // rr[k] = prod_{j < k} d_j
+          const double dk = x - nodes[k];
+          if (dk == 0.0) hit = hit < 0 ? k : hit;
+          rr[k] = pre;
+          pre *= dk;
+        }
+        if (hit >= 0) {
+#pragma unroll
+          for (int k = 0; k < PR; ++k) r[k] = k == hit ? 1.0 : 0.0;
+        } else {
+          double suf = 1.0, sum = 0.0;
+#pragma unroll
+          for (int k = PR - 1; k >= 0; --k) {  // rr[k] = w_k prod_{j != k} d_j
+            const double v = wts[k] * (rr[k] * suf);
+            rr[k] = v;
+            sum += v;
+            suf *= x - nodes[k];
+          }
+          const double inv = 1.0 / sum;
+#pragma unroll
+          for (int k = 0; k < PR; ++k) r[k] = rr[k] * inv;
+        }
+      }
+    } else if (lane < nv) {
       const double x = __dmul_rn(__dsub_rn(pts[(size_t)ax * n + i], box.c[ax]), hinv);
       int hit = -1;
       for (int k = 0; k < p; ++k)
@@ -642,8 +677,16 @@ void launch_basis(const ChebDev& cb, const DBox* boxes, const int* leaves, int n
                   int use_targets, double* basis, cudaStream_t st) {
   if (nleaf <= 0) return;
   const size_t sm = sizeof(double) * kBasisW * 32 * (cb.p | 1);
-  cudaFuncSetAttribute((const void*)k_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_basis<<<nleaf, kBasisW * 32, sm, st>>>(cb, boxes, leaves, pts, n, use_targets, basis);
+#define KB(PC_)                                                                                              \
+  do {                                                                                                       \
+    smem_attr((const void*)k_basis<PC_>, sm);                                                                \
+    k_basis<PC_><<<nleaf, kBasisW * 32, sm, st>>>(cb, boxes, leaves, pts, n, use_targets, basis);           \
+  } while (0)
+  if (cb.p == 23) KB(23);
+  else if (cb.p == 22) KB(22);
+  else if (cb.p == 30) KB(30);
+  else KB(0);
+#undef KB
 }
 
 void launch_anterp_mma(int kernel, const ChebDev& cb, const DBox* boxes, const int* leaves, int nleaf,
