@@ -703,6 +703,16 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
       capped = hh[2] != 0;
       return true;
     };
+  if (!host_refine)
+    pa.repair_scan = [&](int nb, unsigned char* cand) {
+      unsigned char* dc = arena_.as<unsigned char>("repair_cand", (size_t)nb);
+      launch_repair_scan((const RefBox*)arena_.get("refine_out", 1), nb, d, pr.periodic ? 1 : 0, dc, st_);
+      ++launches_;
+      unsigned char* hc = (unsigned char*)pinned_.get("repair_cand", (size_t)nb);
+      cuda_check(cudaMemcpyAsync(hc, dc, (size_t)nb, cudaMemcpyDeviceToHost, st_), "D2H repair candidates");
+      sync();
+      std::memcpy(cand, hc, (size_t)nb);
+    };
   pr.tree = build_topology(d, pr.periodic, P.n_s, P.p, ns, pr.alias ? 0 : nt, pa, /*with_neighbours=*/false);
   if (str_pending_) {
     finish_strengths();

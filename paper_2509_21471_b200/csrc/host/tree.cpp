@@ -82,6 +82,7 @@ struct Builder {
   // so the children's ranges are found afterwards, one batched GPU call per level
   std::vector<int> deferred;
   size_t deferred_total = 0;
+  bool dev_boxes = false;  // the device holds these boxes (pa->refine ran): the repair's first sweep runs there
   double split_ms = 0.0, dfs_ms = 0.0;  // time in the GPU split calls / DFS renumbering (SDMK_TIMING)
   double rep_scan_ms = 0.0;             // repair: parallel pre-scan
   int rep_leaves = 0, rep_sweeps = 0, rep_cands = 0;
@@ -127,6 +128,7 @@ struct Builder {
       if (pa->refine(t.boxes, maxlev, capped)) {
         t.max_level = maxlev;
         t.depth_capped = capped;
+        dev_boxes = true;
         return;
       }
     }
@@ -321,8 +323,14 @@ struct Builder {
       const int nl = (int)leaves.size();
       std::vector<char> cand(nl, 0);
       const auto r0 = std::chrono::steady_clock::now();
+      if (dev_boxes && pa && pa->repair_scan) {
+        std::vector<unsigned char> byb(t.num_boxes());
+        pa->repair_scan(t.num_boxes(), byb.data());
+        for (int i = 0; i < nl; ++i) cand[i] = (char)byb[leaves[i]];
+      } else {
 #pragma omp parallel for schedule(dynamic, 64)
-      for (int i = 0; i < nl; ++i) cand[i] = probe_triggers(leaves[i], nullptr);
+        for (int i = 0; i < nl; ++i) cand[i] = probe_triggers(leaves[i], nullptr);
+      }
       for (int i = 0; i < nl; ++i)
         if (cand[i]) cand_ids.push_back(leaves[i]);
       rep_scan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();

@@ -87,6 +87,9 @@ struct PointAccess {
   // the reference's id order and returns true, or returns false (the refine
   // then runs on the host, level by level through `split`)
   std::function<bool(std::vector<Box>& boxes, int& max_level, bool& depth_capped)> refine;
+  // optional, after a device refine: the repair's read-only first sweep over
+  // those boxes on the device (cand[b] = leaf b can trigger a subdivision)
+  std::function<void(int nboxes, unsigned char* cand)> repair_scan;
 };
 // with_neighbours = false leaves col / crs / fin for finish_topology (the
 // upward pass needs only the boxes; the engine builds the lists while it runs)

@@ -352,6 +352,65 @@ __global__ void __launch_bounds__(256) k_refine(const int32_t* qs, int ns, const
 }
 }  // namespace
 
+// First sweep of the 2:1 repair (tree.cpp:125-165), read-only: does one of the
+// 3^d - 1 neighbour-centre probes of leaf b land in a leaf two or more levels
+// coarser?  The probe's box is found from b's parent: climb to the first
+// ancestor containing it, descend to a leaf or to level(b) - 1 (the host's
+// Builder::probe_triggers / locate).  One thread per box of the refined tree.
+namespace {
+__global__ void k_repair_scan(const RefBox* __restrict__ boxes, int nb, int dim, int periodic,
+                              unsigned char* __restrict__ cand) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const RefBox bx = boxes[b];
+  unsigned char hit = 0;
+  if (bx.leaf && bx.level >= 2) {
+    const long long cells = 1ll << kQBits, side = cells >> bx.level;
+    const int zr = dim == 3 ? 1 : 0;
+    for (int o2 = -zr; o2 <= zr && !hit; ++o2)
+      for (int o1 = -1; o1 <= 1 && !hit; ++o1)
+        for (int o0 = -1; o0 <= 1 && !hit; ++o0) {
+          if (!o0 && !o1 && !o2) continue;
+          const int off[3] = {o0, o1, o2};
+          int probe[3] = {0, 0, 0};
+          bool inside = true;
+          for (int a = 0; a < dim && inside; ++a) {
+            long long v = bx.anchor[a] + off[a] * side + side / 2;
+            if (periodic) v = ((v % cells) + cells) % cells;
+            else if (v < 0 || v >= cells) inside = false;
+            probe[a] = (int)v;
+          }
+          if (!inside) continue;
+          int x = bx.parent;
+          for (;;) {
+            const int lv = boxes[x].level, par = boxes[x].parent;
+            const long long sd = cells >> lv;
+            bool in = true;
+            for (int a = 0; a < dim; ++a) {
+              const int an = boxes[x].anchor[a];
+              in = in && probe[a] >= an && (long long)probe[a] < an + sd;
+            }
+            if (in || par < 0) break;
+            x = par;
+          }
+          while (!boxes[x].leaf && boxes[x].level < bx.level - 1) {
+            const int lv = boxes[x].level;
+            int ci = 0;
+            for (int a = 0; a < dim; ++a) ci |= ((probe[a] >> (kQBits - 1 - lv)) & 1) << a;
+            x = boxes[x].first_child + ci;
+          }
+          if (boxes[x].leaf && boxes[x].level <= bx.level - 2) hit = 1;
+        }
+  }
+  cand[b] = hit;
+}
+}  // namespace
+
+void launch_repair_scan(const RefBox* boxes, int nb, int dim, int periodic, unsigned char* cand, cudaStream_t st) {
+  if (nb <= 0) return;
+  k_repair_scan<<<(nb + 127) / 128, 128, 0, st>>>(boxes, nb, dim, periodic, cand);
+}
+
 size_t refine_node_bytes() { return sizeof(RNode); }
 
 void launch_refine(const int32_t* qs, int ns, const int32_t* qt, int nt, int alias, int dim, int n_s, int cap,
