@@ -43,7 +43,7 @@ def main():
     ap.add_argument("--n", type=float, default=1e7)
     ap.add_argument("--dist", default="uniform")
     ap.add_argument("--ranks", default="2,4,8")
-    ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--reps", type=int, default=4)
     ap.add_argument("--link-gbs", type=float, default=400.0, help="assumed per-GPU NVLink rate for the estimate")
     a = ap.parse_args()
     import torch
@@ -64,10 +64,13 @@ def main():
         rows = []
         for r in range(R):
             ctx.set_shard(r, R)
-            for k in range(a.reps):
-                rr = {}
+            rr = None
+            for k in range(a.reps):  # the fastest repetition: the host part (repair, lists) is noisy on a shared box
+                r1 = {}
                 ctx.evaluate_begin_device(plan, 3, n, dx.data_ptr(), 0, 0, df.data_ptr(), 0)
-                ctx.evaluate_end(rr, d_u=du.data_ptr())
+                ctx.evaluate_end(r1, d_u=du.data_ptr())
+                if k > 0 and (rr is None or r1["t_total"] < rr["t_total"]):
+                    rr = r1
             u_bytes = n * 3 * 8
             halo_s = rr["halo_bytes_recv"] / (a.link_gbs * 1e9)
             u_s = u_bytes * (R - 1) / R / (a.link_gbs * 1e9)  # all-gather of the owned ranges
