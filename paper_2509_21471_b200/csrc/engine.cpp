@@ -704,14 +704,15 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
       return true;
     };
   if (!host_refine)
-    pa.repair_scan = [&](int nb, unsigned char* cand) {
-      unsigned char* dc = arena_.as<unsigned char>("repair_cand", (size_t)nb);
+    pa.repair_scan = [&](int nb, uint32_t* cand) {
+      uint32_t* dc = arena_.as<uint32_t>("repair_cand", (size_t)nb);
       launch_repair_scan((const RefBox*)arena_.get("refine_out", 1), nb, d, pr.periodic ? 1 : 0, dc, st_);
       ++launches_;
-      unsigned char* hc = (unsigned char*)pinned_.get("repair_cand", (size_t)nb);
-      cuda_check(cudaMemcpyAsync(hc, dc, (size_t)nb, cudaMemcpyDeviceToHost, st_), "D2H repair candidates");
+      uint32_t* hc = (uint32_t*)pinned_.get("repair_cand", (size_t)nb * sizeof(uint32_t));
+      cuda_check(cudaMemcpyAsync(hc, dc, (size_t)nb * sizeof(uint32_t), cudaMemcpyDeviceToHost, st_),
+                 "D2H repair candidates");
       sync();
-      std::memcpy(cand, hc, (size_t)nb);
+      std::memcpy(cand, hc, (size_t)nb * sizeof(uint32_t));
     };
   pr.tree = build_topology(d, pr.periodic, P.n_s, P.p, ns, pr.alias ? 0 : nt, pa, /*with_neighbours=*/false);
   if (str_pending_) {

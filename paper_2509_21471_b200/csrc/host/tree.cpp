@@ -267,11 +267,14 @@ struct Builder {
     return x;
   }
 
-  bool probe_triggers(int b, int* first_off) const {
+  // bit k set: the k-th of the 3^d offsets (o0 fastest, the centre counted) of
+  // leaf b probes a leaf two or more levels coarser
+  uint32_t probe_mask(int b) const {
     const int lev = t.boxes[b].level;
-    if (lev < 2) return false;
+    if (lev < 2) return 0;
     const int64_t side = kCells >> lev;
     const int zr = t.dim == 3 ? 1 : 0;
+    uint32_t mask = 0;
     int k = 0;
     for (int o2 = -zr; o2 <= zr; ++o2)
       for (int o1 = -1; o1 <= 1; ++o1)
@@ -290,12 +293,9 @@ struct Builder {
           }
           if (!inside) continue;
           const int a = locate(t.boxes[b].parent, probe, lev - 1);
-          if (t.boxes[a].leaf && t.boxes[a].level <= lev - 2) {
-            if (first_off) *first_off = k;
-            return true;
-          }
+          if (t.boxes[a].leaf && t.boxes[a].level <= lev - 2) mask |= uint32_t(1) << k;
         }
-    return false;
+    return mask;
   }
 
   // repair (tree.cpp:125-165): sweeps over the leaves in id order, each leaf
@@ -308,6 +308,7 @@ struct Builder {
   // leaf in parallel; every replay runs in the reference's order.
   void repair() {
     std::vector<int> cand_ids;
+    std::vector<uint32_t> cand_mask;  // per candidate: the offsets that trigger at the start of the sweep
     {
       std::vector<int> leaves;
       int lmin = kMaxLevel, lmax = 0;
@@ -321,18 +322,21 @@ struct Builder {
       // leaf levels span at most one level (uniform inputs), so no sweep can fire
       if (lmax - lmin <= 1) return;
       const int nl = (int)leaves.size();
-      std::vector<char> cand(nl, 0);
+      std::vector<uint32_t> cand(nl, 0);
       const auto r0 = std::chrono::steady_clock::now();
       if (dev_boxes && pa && pa->repair_scan) {
-        std::vector<unsigned char> byb(t.num_boxes());
+        std::vector<uint32_t> byb(t.num_boxes());
         pa->repair_scan(t.num_boxes(), byb.data());
-        for (int i = 0; i < nl; ++i) cand[i] = (char)byb[leaves[i]];
+        for (int i = 0; i < nl; ++i) cand[i] = byb[leaves[i]];
       } else {
 #pragma omp parallel for schedule(dynamic, 64)
-        for (int i = 0; i < nl; ++i) cand[i] = probe_triggers(leaves[i], nullptr);
+        for (int i = 0; i < nl; ++i) cand[i] = probe_mask(leaves[i]);
       }
       for (int i = 0; i < nl; ++i)
-        if (cand[i]) cand_ids.push_back(leaves[i]);
+        if (cand[i]) {
+          cand_ids.push_back(leaves[i]);
+          cand_mask.push_back(cand[i]);
+        }
       rep_scan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();
       rep_leaves = nl;
     }
@@ -340,16 +344,22 @@ struct Builder {
       ++rep_sweeps;
       rep_cands += (int)cand_ids.size();
       std::vector<int> next;
-      for (const int b : cand_ids) {
+      for (size_t ic = 0; ic < cand_ids.size(); ++ic) {
+        const int b = cand_ids[ic];
+        // an offset that did not trigger when the sweep started cannot trigger
+        // later in it (subdivisions only refine): only the flagged ones are
+        // probed again, in the reference's order
+        const uint32_t mask = cand_mask[ic];
         if (!t.boxes[b].leaf) continue;
         const int lev = t.boxes[b].level;
         const int64_t side = kCells >> lev;
         const int zr = t.dim == 3 ? 1 : 0;
         bool fired = false;
+        int k = 0;
         for (int o2 = -zr; o2 <= zr; ++o2)
           for (int o1 = -1; o1 <= 1; ++o1)
-            for (int o0 = -1; o0 <= 1; ++o0) {
-              if (!o0 && !o1 && !o2) continue;
+            for (int o0 = -1; o0 <= 1; ++o0, ++k) {
+              if (!((mask >> k) & 1)) continue;
               const int off[3] = {o0, o1, o2};
               int32_t probe[3] = {0, 0, 0};
               bool inside = true;
@@ -374,12 +384,16 @@ struct Builder {
       // the next sweep's candidates, in id order (the order the sweep visits leaves)
       std::sort(next.begin(), next.end());
       next.erase(std::unique(next.begin(), next.end()), next.end());
-      std::vector<char> trig(next.size(), 0);
+      std::vector<uint32_t> trig(next.size(), 0);
 #pragma omp parallel for schedule(dynamic, 64)
-      for (int i = 0; i < (int)next.size(); ++i) trig[i] = t.boxes[next[i]].leaf && probe_triggers(next[i], nullptr);
+      for (int i = 0; i < (int)next.size(); ++i) trig[i] = t.boxes[next[i]].leaf ? probe_mask(next[i]) : 0;
       cand_ids.clear();
+      cand_mask.clear();
       for (size_t i = 0; i < next.size(); ++i)
-        if (trig[i]) cand_ids.push_back(next[i]);
+        if (trig[i]) {
+          cand_ids.push_back(next[i]);
+          cand_mask.push_back(trig[i]);
+        }
     }
   }
 

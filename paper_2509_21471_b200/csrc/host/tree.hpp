@@ -88,8 +88,9 @@ struct PointAccess {
   // then runs on the host, level by level through `split`)
   std::function<bool(std::vector<Box>& boxes, int& max_level, bool& depth_capped)> refine;
   // optional, after a device refine: the repair's read-only first sweep over
-  // those boxes on the device (cand[b] = leaf b can trigger a subdivision)
-  std::function<void(int nboxes, unsigned char* cand)> repair_scan;
+  // those boxes on the device (cand[b] bit k: the k-th of leaf b's 3^d offsets,
+  // o0 fastest and the centre counted, probes a leaf two or more levels coarser)
+  std::function<void(int nboxes, uint32_t* cand)> repair_scan;
 };
 // with_neighbours = false leaves col / crs / fin for finish_topology (the
 // upward pass needs only the boxes; the engine builds the lists while it runs)

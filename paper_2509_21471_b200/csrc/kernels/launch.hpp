@@ -61,9 +61,10 @@ struct RefBox {
   int sb, se, tb, te;
 };
 size_t refine_node_bytes();
-// the 2:1 repair's first sweep over launch_refine's boxes, read-only: cand[b] = 1
-// when leaf b has a neighbour-centre probe in a leaf two or more levels coarser
-void launch_repair_scan(const RefBox* boxes, int nb, int dim, int periodic, unsigned char* cand, cudaStream_t st);
+// the 2:1 repair's first sweep over launch_refine's boxes, read-only: cand[b] bit k
+// set when the k-th of leaf b's 3^d neighbour-centre probes (o0 fastest, the centre
+// counted) lands in a leaf two or more levels coarser
+void launch_repair_scan(const RefBox* boxes, int nb, int dim, int periodic, uint32_t* cand, cudaStream_t st);
 void launch_refine(const int32_t* qs, int ns, const int32_t* qt, int nt, int alias, int dim, int n_s, int cap,
                    void* nodes, int* hdr, RefBox* out, cudaStream_t st);
 // The residual's source sub-cells: 9 boundaries per box (children of leaves

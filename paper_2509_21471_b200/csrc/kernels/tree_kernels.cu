@@ -359,17 +359,18 @@ __global__ void __launch_bounds__(256) k_refine(const int32_t* qs, int ns, const
 // Builder::probe_triggers / locate).  One thread per box of the refined tree.
 namespace {
 __global__ void k_repair_scan(const RefBox* __restrict__ boxes, int nb, int dim, int periodic,
-                              unsigned char* __restrict__ cand) {
+                              uint32_t* __restrict__ cand) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= nb) return;
   const RefBox bx = boxes[b];
-  unsigned char hit = 0;
+  uint32_t hit = 0;  // bit k: the k-th offset (o0 fastest, the centre counted) triggers
   if (bx.leaf && bx.level >= 2) {
     const long long cells = 1ll << kQBits, side = cells >> bx.level;
     const int zr = dim == 3 ? 1 : 0;
-    for (int o2 = -zr; o2 <= zr && !hit; ++o2)
-      for (int o1 = -1; o1 <= 1 && !hit; ++o1)
-        for (int o0 = -1; o0 <= 1 && !hit; ++o0) {
+    int k = 0;
+    for (int o2 = -zr; o2 <= zr; ++o2)
+      for (int o1 = -1; o1 <= 1; ++o1)
+        for (int o0 = -1; o0 <= 1; ++o0, ++k) {
           if (!o0 && !o1 && !o2) continue;
           const int off[3] = {o0, o1, o2};
           int probe[3] = {0, 0, 0};
@@ -399,14 +400,14 @@ __global__ void k_repair_scan(const RefBox* __restrict__ boxes, int nb, int dim,
             for (int a = 0; a < dim; ++a) ci |= ((probe[a] >> (kQBits - 1 - lv)) & 1) << a;
             x = boxes[x].first_child + ci;
           }
-          if (boxes[x].leaf && boxes[x].level <= bx.level - 2) hit = 1;
+          if (boxes[x].leaf && boxes[x].level <= bx.level - 2) hit |= 1u << k;
         }
   }
   cand[b] = hit;
 }
 }  // namespace
 
-void launch_repair_scan(const RefBox* boxes, int nb, int dim, int periodic, unsigned char* cand, cudaStream_t st) {
+void launch_repair_scan(const RefBox* boxes, int nb, int dim, int periodic, uint32_t* cand, cudaStream_t st) {
   if (nb <= 0) return;
   k_repair_scan<<<(nb + 127) / 128, 128, 0, st>>>(boxes, nb, dim, periodic, cand);
 }
