@@ -684,10 +684,10 @@ void Context::build_problem(const Plan& P, int dim, int ns, int nt, int mode, bo
       void* nodes = arena_.get("refine_nodes", (size_t)cap * refine_node_bytes());
       RefBox* out = (RefBox*)arena_.get("refine_out", (size_t)cap * sizeof(RefBox));
       int* hdr = arena_.as<int>("refine_hdr", 64);
-      launch_refine(sq, ns, pr.alias ? nullptr : tq, pr.alias ? 0 : nt, pr.alias ? 1 : 0, d, P.n_s, cap, nodes, hdr,
-                    out, st_);
+      if (!launch_refine(sq, ns, pr.alias ? nullptr : tq, pr.alias ? 0 : nt, pr.alias ? 1 : 0, d, P.n_s, cap, nodes,
+                         hdr, out, st_))
+        return false;
       ++launches_;
-      cuda_check(cudaPeekAtLastError(), "refine launch");
       int* hh = (int*)pinned_.get("refine_hdr", 64 * sizeof(int));
       cuda_check(cudaMemcpyAsync(hh, hdr, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H refine header");
       sync();

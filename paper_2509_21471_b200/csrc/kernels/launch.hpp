@@ -65,7 +65,8 @@ size_t refine_node_bytes();
 // set when the k-th of leaf b's 3^d neighbour-centre probes (o0 fastest, the centre
 // counted) lands in a leaf two or more levels coarser
 void launch_repair_scan(const RefBox* boxes, int nb, int dim, int periodic, uint32_t* cand, cudaStream_t st);
-void launch_refine(const int32_t* qs, int ns, const int32_t* qt, int nt, int alias, int dim, int n_s, int cap,
+// returns false when the cooperative launch is refused (the caller refines on the host)
+bool launch_refine(const int32_t* qs, int ns, const int32_t* qt, int nt, int alias, int dim, int n_s, int cap,
                    void* nodes, int* hdr, RefBox* out, cudaStream_t st);
 // The residual's source sub-cells: 9 boundaries per box (children of leaves
 // with sources, else [sb, se) once), as host/tree.hpp leaf_subranges.

@@ -414,7 +414,7 @@ void launch_repair_scan(const RefBox* boxes, int nb, int dim, int periodic, uint
 
 size_t refine_node_bytes() { return sizeof(RNode); }
 
-void launch_refine(const int32_t* qs, int ns, const int32_t* qt, int nt, int alias, int dim, int n_s, int cap,
+bool launch_refine(const int32_t* qs, int ns, const int32_t* qt, int nt, int alias, int dim, int n_s, int cap,
                    void* nodes, int* hdr, RefBox* out, cudaStream_t st) {
   static int grid = 0;
   if (!grid) {
@@ -426,7 +426,11 @@ void launch_refine(const int32_t* qs, int ns, const int32_t* qt, int nt, int ali
   }
   RNode* nd = (RNode*)nodes;
   void* args[] = {&qs, &ns, &qt, &nt, &alias, &dim, &n_s, &cap, &nd, &hdr, &out};
-  cudaLaunchCooperativeKernel((const void*)k_refine, dim3(grid), dim3(256), args, 0, st);
+  if (cudaLaunchCooperativeKernel((const void*)k_refine, dim3(grid), dim3(256), args, 0, st) != cudaSuccess) {
+    cudaGetLastError();  // no cooperative launch here (e.g. a partitioned device): the host refines
+    return false;
+  }
+  return true;
 }
 
 void launch_split_ranges(int nbox, const int* lvl, const int* rng, const int32_t* q, int n, int dim, int* bnd,
