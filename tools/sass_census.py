@@ -18,7 +18,10 @@ KERNELS = [  # (object, kernel-name regex)
     ("residual.o", r"k_residual<0, 3, 6, 0>"),
     ("anterp_mma.o", r"k_anterp2<9, 3, 23, 0, 3, 12, 64>"),
     ("anterp_mma.o", r"k_interp_mma<3, 23, 3"),
-    ("anterp_mma.o", r"k_basis"),
+    ("anterp_mma.o", r"k_basis<23>"),
+    ("tree_kernels.o", r"k_refine"),
+    ("tree_kernels.o", r"k_repair_scan"),
+    ("tree_kernels.o", r"k_morton"),
     ("planewave.o", r"k_acc_group<0, 3, 1>"),
     ("planewave_mma.o", r"k_fwd_xy3<23, 33, 8>"),
     ("planewave_mma.o", r"k_zf3"),
